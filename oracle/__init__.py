@@ -1,0 +1,173 @@
+"""CPU oracle for the DMTz hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product package
+``paper_2409_17346_b200`` never imports it.  The numerics live in
+``oracle/dmtz_oracle.c`` (plain C + OpenMP, literal definitions, see its header);
+this module only marshals numpy arrays through ctypes.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "dmtz_oracle.c")
+_LIB = os.path.join(_HERE, "libdmtz_oracle.so")
+
+OK, E_ARG, E_DIMS, E_NONFINITE, E_BOUND, E_CAPACITY, E_ITER_CAP, E_STUCK = range(8)
+E_INTERNAL = 11
+KIND_DESC, KIND_ASC, KIND_CONN = 1, 2, 4
+BOUNDARY = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+EDIT_DTYPE = np.dtype([("v", "<u8"), ("q", "<u2"), ("lossless", "u1"), ("pad", "u1"),
+                       ("value", "<f4")])
+STATS_FIELDS = ["rounds", "n_edited", "n_quantized", "n_lossless", "n_false_round0"]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("rounds", ctypes.c_int64), ("n_edited", ctypes.c_int64),
+                ("n_quantized", ctypes.c_int64), ("n_lossless", ctypes.c_int64),
+                ("n_false_round0", ctypes.c_int64),
+                ("false_by_kind_round0", ctypes.c_int64 * 8),
+                ("status", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (gcc, OpenMP, no FMA contraction, honoured rounding modes)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fopenmp", "-ffp-contract=off",
+                               "-frounding-math", "-fPIC", "-shared", "-Wall", "-o", _LIB, _SRC])
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        P = ctypes.c_void_p
+        i64 = ctypes.c_int64
+        L.dmtz_oracle_gradient.argtypes = [P, P, P, P]
+        L.dmtz_oracle_complex_info.argtypes = [P, P, P, P, P, P]
+        L.dmtz_oracle_cell_counts.argtypes = [P, P]
+        L.dmtz_oracle_correct.argtypes = [P, P, P, ctypes.c_float, ctypes.c_int32, ctypes.c_int32,
+                                          ctypes.c_int32, i64, P, P, P, i64, P,
+                                          ctypes.POINTER(_Stats)]
+        L.dmtz_oracle_trace.argtypes = [P, P, ctypes.c_uint32, i64, i64, P, P, P, P, P, P, P]
+        for fn in ("dmtz_oracle_gradient", "dmtz_oracle_complex_info", "dmtz_oracle_cell_counts",
+                   "dmtz_oracle_correct", "dmtz_oracle_trace", "dmtz_oracle_num_threads"):
+            getattr(L, fn).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _dims(shape) -> np.ndarray:
+    """numpy shape (nz, ny, nx) or (ny, nx) -> int64[3] {nx, ny, nz}."""
+    if len(shape) == 2:
+        return np.array([shape[1], shape[0], 1], dtype=np.int64)
+    return np.array([shape[2], shape[1], shape[0]], dtype=np.int64)
+
+
+def num_threads() -> int:
+    return lib().dmtz_oracle_num_threads()
+
+
+def gradient(field: np.ndarray):
+    """Literal discrete gradient of ``field`` -> (codes, crit masks) per anchor."""
+    field = np.ascontiguousarray(field, dtype=np.float32)
+    d = _dims(field.shape)
+    n = field.size
+    codes = np.zeros(n, dtype=np.uint64 if d[2] > 1 else np.uint16)
+    crit = np.zeros(n, dtype=np.uint32)
+    st = lib().dmtz_oracle_gradient(_p(d), _p(field), _p(codes), _p(crit))
+    if st:
+        raise RuntimeError(f"oracle gradient status {st}")
+    return codes.reshape(field.shape), crit.reshape(field.shape)
+
+
+def complex_info(shape):
+    d = _dims(shape)
+    T = ctypes.c_int32()
+    dim = np.zeros(26, np.int32)
+    nlink = np.zeros(26, np.int32)
+    offs = np.zeros((26, 4, 3), np.int32)
+    links = np.zeros((26, 14, 3), np.int32)
+    lib().dmtz_oracle_complex_info(_p(d), ctypes.byref(T), _p(dim), _p(nlink), _p(offs), _p(links))
+    t = T.value
+    return dict(T=t, dim=dim[:t].copy(), nlink=nlink[:t].copy(), offsets=offs[:t].copy(),
+                links=links[:t].copy())
+
+
+def cell_counts(shape):
+    d = _dims(shape)
+    c = np.zeros(4, np.int64)
+    st = lib().dmtz_oracle_cell_counts(_p(d), _p(c))
+    if st:
+        raise RuntimeError(f"oracle cell_counts status {st}")
+    return c
+
+
+def correct(f: np.ndarray, fhat: np.ndarray, xi: float, q_max: int = 6, q_cap: int | None = None,
+            tier: int = 2, max_rounds: int = 0, edits_capacity: int | None = None):
+    """Literal synchronous C-loop.  Returns dict(status, g, state, edits, stats)."""
+    f = np.ascontiguousarray(f, dtype=np.float32)
+    fhat = np.ascontiguousarray(fhat, dtype=np.float32)
+    assert f.shape == fhat.shape
+    if q_cap is None:
+        q_cap = q_max
+    d = _dims(f.shape)
+    n = f.size
+    cap = n if edits_capacity is None else edits_capacity
+    g = np.empty_like(f)
+    state = np.zeros(f.shape, dtype=np.uint32)
+    edits = np.zeros(max(cap, 1), dtype=EDIT_DTYPE)
+    ne = ctypes.c_int64()
+    stats = _Stats()
+    st = lib().dmtz_oracle_correct(_p(d), _p(f), _p(fhat), ctypes.c_float(xi), q_max, q_cap, tier,
+                                   max_rounds, _p(g), _p(state), _p(edits), cap,
+                                   ctypes.byref(ne), ctypes.byref(stats))
+    out = {k: getattr(stats, k) for k in STATS_FIELDS}
+    out["false_by_kind_round0"] = list(stats.false_by_kind_round0)
+    out["status"] = st
+    return dict(status=st, g=g, state=state, edits=edits[:min(ne.value, cap)].copy(),
+                n_edits=ne.value, stats=out)
+
+
+def trace(field: np.ndarray, kinds: int = KIND_DESC | KIND_ASC | KIND_CONN,
+          cap_branches: int | None = None, cap_cells: int | None = None):
+    """Literal V-path traces of the gradient of ``field`` (CSR)."""
+    field = np.ascontiguousarray(field, dtype=np.float32)
+    d = _dims(field.shape)
+    L = lib()
+
+    def run(cb, cc):
+        off = np.zeros(cb + 1, np.int64)
+        cells = np.zeros(max(cc, 1), np.uint64)
+        origin = np.zeros(max(cb, 1), np.uint64)
+        term = np.zeros(max(cb, 1), np.uint64)
+        kind = np.zeros(max(cb, 1), np.uint8)
+        nb, nc = ctypes.c_int64(), ctypes.c_int64()
+        st = L.dmtz_oracle_trace(_p(d), _p(field), kinds, cb, cc, _p(off), _p(cells), _p(origin),
+                                 _p(term), _p(kind), ctypes.byref(nb), ctypes.byref(nc))
+        return st, nb.value, nc.value, off, cells, origin, term, kind
+
+    cb = cap_branches if cap_branches is not None else 1024
+    cc = cap_cells if cap_cells is not None else 65536
+    st, nb, nc, off, cells, origin, term, kind = run(cb, cc)
+    if st == E_CAPACITY and cap_branches is None and cap_cells is None:
+        st, nb, nc, off, cells, origin, term, kind = run(nb, nc)
+    if st not in (OK,):
+        raise RuntimeError(f"oracle trace status {st}")
+    return dict(offsets=off[:nb + 1], cells=cells[:nc], origin=origin[:nb], terminal=term[:nb],
+                kind=kind[:nb])

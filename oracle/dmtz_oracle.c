@@ -1,0 +1,801 @@
+/*
+ * oracle/dmtz_oracle.c -- plain, slow, literal CPU oracle for the DMTz hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  The product path
+ * (paper_2409_17346_b200/) never links, imports or calls it, and this file
+ * includes no header and shares no table, helper or constant generator with the
+ * CUDA path.  It re-derives everything it needs from the definitions in
+ * PAPER.md (cited as P:<line>) and the readings listed in DESIGN.md section 3.
+ *
+ * What it computes (each function cites its passage):
+ *   - the Freudenthal/Kuhn cell complex of a regular grid
+ *   - the discrete gradient by the Shivashankar-Natarajan rule on the
+ *     extended function of Eq. 1, LITERALLY: for every
+ *     d-cell a (d ascending, cells already paired with a facet skipped) it forms
+ *     P_a = { b cofacet of a : G0(b) = a } by sorting b's vertices and dropping
+ *     the lowest, and pairs a with the lexicographically smallest key in P_a
+ *   - critical cells (unpaired cells)
+ *   - the C-loop in synchronous rounds with the
+ *     quantized edit of Eq. 2, error bound P:138
+ *   - V-path traces: descending, ascending, saddle-saddle connectors
+ *
+ * Parity status: every function here is pinned by tests/test_oracle_*.py against
+ * brute force on an explicit complex, closed-form counts, the Euler relation and
+ * the paper's worked example (Fig. 3).  Round counts / edit counts on
+ * synthetic data have no external pin ("parity unpinned").
+ *
+ * Build: gcc -O2 -std=c11 -fopenmp -ffp-contract=off -frounding-math -fPIC -shared
+ */
+#include <fenv.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* fesetround() is honoured because the file is compiled with -frounding-math. */
+
+/* Status values: the numeric codes the C-ABI documents (include/dmtz.h is NOT
+ * included; the oracle restates the documented numbers). */
+enum {
+  OR_OK = 0, OR_E_ARG = 1, OR_E_DIMS = 2, OR_E_NONFINITE = 3, OR_E_BOUND = 4,
+  OR_E_CAPACITY = 5, OR_E_ITER_CAP = 6, OR_E_STUCK = 7, OR_E_INTERNAL = 11
+};
+
+#define MAXTYPES 26
+#define MAXLINK 14
+#define BOUNDARY_ID UINT64_MAX
+
+/* ------------------------------------------------------------------------- */
+/* The cell complex ("regular grid-based triangulation").        */
+/* ------------------------------------------------------------------------- */
+
+typedef struct {
+  int dim;              /* number of vertices - 1 */
+  int nv;
+  int off[4][3];        /* vertex offsets from the anchor, ascending global index */
+  int nlink;            /* interior link size (grid assumed unbounded) */
+  int link[MAXLINK][3]; /* link vertex offsets, ascending (dz,dy,dx) = slot order */
+  int cof_anchor[MAXLINK][3]; /* cofacet cell (cell + link[s]) : its anchor delta */
+  int cof_type[MAXLINK];      /*                                   its type      */
+  int cof_pos[MAXLINK];       /* position of link[s] inside the cofacet's vertex list */
+  int fac_anchor[4][3]; /* facet omitting vertex k : anchor delta */
+  int fac_type[4];      /*                           type         */
+} ctype_t;
+
+typedef struct {
+  int D;                 /* 2 or 3 */
+  int64_t n[3];          /* nx, ny, nz (nz == 1 for 2D) */
+  int64_t N;             /* vertex count */
+  int T;                 /* cell types per anchor */
+  int top;               /* top dimension */
+  int first_of_dim[5];   /* first type index of each dimension, [dim+1] = end */
+  ctype_t t[MAXTYPES];
+} cx_t;
+
+static void mask_off(int m, int o[3]) { o[0] = m & 1; o[1] = (m >> 1) & 1; o[2] = (m >> 2) & 1; }
+
+/* A set of lattice points is a simplex of the Kuhn/Freudenthal triangulation
+ * iff all points lie in one unit cube above their componentwise minimum and
+ * their offsets from it are totally ordered componentwise (a chain from the
+ * cube's low corner towards the main diagonal) -- S:47-48, "split on the
+ * (lowest-corner -> opposite-corner) diagonal". */
+static int is_simplex(int np, int p[][3]) {
+  int b[3] = {p[0][0], p[0][1], p[0][2]};
+  for (int i = 1; i < np; i++)
+    for (int a = 0; a < 3; a++) if (p[i][a] < b[a]) b[a] = p[i][a];
+  for (int i = 0; i < np; i++) {
+    for (int a = 0; a < 3; a++) { int d = p[i][a] - b[a]; if (d < 0 || d > 1) return 0; }
+    for (int j = i + 1; j < np; j++) {
+      int le = 1, ge = 1, eq = 1;
+      for (int a = 0; a < 3; a++) {
+        if (p[i][a] > p[j][a]) le = 0;
+        if (p[i][a] < p[j][a]) ge = 0;
+        if (p[i][a] != p[j][a]) eq = 0;
+      }
+      if (eq || (!le && !ge)) return 0;
+    }
+  }
+  return 1;
+}
+
+/* (dz,dy,dx) lexicographic order of offsets == ascending global index order */
+static int off_less(const int a[3], const int b[3]) {
+  if (a[2] != b[2]) return a[2] < b[2];
+  if (a[1] != b[1]) return a[1] < b[1];
+  return a[0] < b[0];
+}
+
+/* Find the (anchor, type) of the cell whose vertex set is pts[0..np) */
+static int locate(const cx_t* cx, int np, int pts[][3], int anchor[3], int* pos_of_last) {
+  int b[3] = {pts[0][0], pts[0][1], pts[0][2]};
+  for (int i = 1; i < np; i++)
+    for (int a = 0; a < 3; a++) if (pts[i][a] < b[a]) b[a] = pts[i][a];
+  for (int ti = 0; ti < cx->T; ti++) {
+    const ctype_t* c = &cx->t[ti];
+    if (c->nv != np) continue;
+    int all = 1, lastpos = -1;
+    for (int i = 0; i < np && all; i++) {
+      int found = 0;
+      for (int k = 0; k < np; k++)
+        if (c->off[k][0] == pts[i][0] - b[0] && c->off[k][1] == pts[i][1] - b[1] &&
+            c->off[k][2] == pts[i][2] - b[2]) { found = 1; if (i == np - 1) lastpos = k; }
+      all = found;
+    }
+    if (all) { anchor[0] = b[0]; anchor[1] = b[1]; anchor[2] = b[2]; if (pos_of_last) *pos_of_last = lastpos; return ti; }
+  }
+  return -1;
+}
+
+/* Enumerate the cell types anchored at a vertex: chains 0 = m0 < m1 < ... < md of
+ * nested bit masks in {0,1}^D, dims ascending, each dim in lexicographic order of
+ * the mask tuple (the type numbering documented in include/dmtz.h, restated). */
+static void build_complex(cx_t* cx, int64_t nx, int64_t ny, int64_t nz) {
+  memset(cx, 0, sizeof *cx);
+  cx->n[0] = nx; cx->n[1] = ny; cx->n[2] = nz;
+  cx->N = nx * ny * nz;
+  cx->D = (nz == 1) ? 2 : 3;
+  cx->top = cx->D;
+  int full = (1 << cx->D) - 1;
+  int T = 0;
+  for (int d = 0; d <= cx->D; d++) {
+    cx->first_of_dim[d] = T;
+    /* enumerate d-chains by brute force over all mask tuples, lexicographically */
+    int m[4] = {0, 0, 0, 0};
+    int total = 1;
+    for (int i = 0; i < d; i++) total *= (full + 1);
+    for (int code = 0; code < total; code++) {
+      int c = code, ok = 1;
+      /* most significant digit first -> lexicographic order */
+      for (int i = d - 1; i >= 0; i--) { m[i] = c % (full + 1); c /= (full + 1); }
+      for (int i = 0; i < d && ok; i++) {
+        if (m[i] == 0) ok = 0;
+        if (i > 0 && !((m[i - 1] & ~m[i]) == 0 && m[i - 1] != m[i])) ok = 0;
+      }
+      if (!ok) continue;
+      ctype_t* ct = &cx->t[T++];
+      ct->dim = d; ct->nv = d + 1;
+      ct->off[0][0] = ct->off[0][1] = ct->off[0][2] = 0;
+      for (int i = 0; i < d; i++) mask_off(m[i], ct->off[i + 1]);
+    }
+  }
+  cx->first_of_dim[cx->D + 1] = T;
+  cx->T = T;
+  /* links, cofacets and facets, by brute force over nearby lattice points */
+  for (int ti = 0; ti < T; ti++) {
+    ctype_t* ct = &cx->t[ti];
+    int zlo = (cx->D == 3) ? -1 : 0, zhi = (cx->D == 3) ? 2 : 0;
+    for (int z = zlo; z <= zhi; z++)
+      for (int y = -1; y <= 2; y++)
+        for (int x = -1; x <= 2; x++) {
+          int w[3] = {x, y, z}, pts[5][3], dup = 0;
+          for (int k = 0; k < ct->nv; k++) {
+            memcpy(pts[k], ct->off[k], sizeof pts[k]);
+            if (!memcmp(ct->off[k], w, sizeof w)) dup = 1;
+          }
+          if (dup) continue;
+          memcpy(pts[ct->nv], w, sizeof w);
+          if (!is_simplex(ct->nv + 1, pts)) continue;
+          /* insertion into slot order */
+          int s = ct->nlink++;
+          while (s > 0 && off_less(w, ct->link[s - 1])) { memcpy(ct->link[s], ct->link[s - 1], sizeof w); s--; }
+          memcpy(ct->link[s], w, sizeof w);
+        }
+    for (int s = 0; s < ct->nlink; s++) {
+      int pts[5][3];
+      for (int k = 0; k < ct->nv; k++) memcpy(pts[k], ct->off[k], sizeof pts[k]);
+      memcpy(pts[ct->nv], ct->link[s], sizeof pts[0]);
+      ct->cof_type[s] = locate(cx, ct->nv + 1, pts, ct->cof_anchor[s], &ct->cof_pos[s]);
+    }
+    if (ct->dim > 0)
+      for (int k = 0; k < ct->nv; k++) {
+        int pts[4][3], np = 0;
+        for (int i = 0; i < ct->nv; i++) if (i != k) memcpy(pts[np++], ct->off[i], sizeof pts[0]);
+        ct->fac_type[k] = locate(cx, np, pts, ct->fac_anchor[k], NULL);
+      }
+  }
+}
+
+typedef struct { int64_t x, y, z; } co_t;
+
+static inline co_t coords(const cx_t* cx, int64_t v) {
+  co_t c; c.x = v % cx->n[0]; c.y = (v / cx->n[0]) % cx->n[1]; c.z = v / (cx->n[0] * cx->n[1]);
+  return c;
+}
+static inline int inside(const cx_t* cx, int64_t x, int64_t y, int64_t z) {
+  return x >= 0 && y >= 0 && z >= 0 && x < cx->n[0] && y < cx->n[1] && z < cx->n[2];
+}
+static inline int64_t vid(const cx_t* cx, int64_t x, int64_t y, int64_t z) {
+  return x + cx->n[0] * (y + cx->n[1] * z);
+}
+/* global vertex ids of cell (anchor A, type ti); returns 0 if the cell leaves the grid */
+static int cell_vertices(const cx_t* cx, int64_t A, int ti, int64_t* vs) {
+  co_t a = coords(cx, A);
+  const ctype_t* ct = &cx->t[ti];
+  for (int k = 0; k < ct->nv; k++) {
+    int64_t x = a.x + ct->off[k][0], y = a.y + ct->off[k][1], z = a.z + ct->off[k][2];
+    if (!inside(cx, x, y, z)) return 0;
+    vs[k] = vid(cx, x, y, z);
+  }
+  return 1;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Simulation of simplicity and the extended function of Eq. 1.              */
+/* ------------------------------------------------------------------------- */
+
+/* u < v in the SoS total order: (value, index) lexicographic (reading A2) */
+static inline int sos_less(const float* f, int64_t u, int64_t v) {
+  return f[u] < f[v] || (f[u] == f[v] && u < v);
+}
+
+/* key of a cell = its vertices sorted descending in SoS order; lexicographic
+ * comparison of keys realises Eq. 1 with symbolic epsilon (reading A3) */
+static void key_of(const float* f, int n, const int64_t* vs, int64_t* key) {
+  for (int i = 0; i < n; i++) key[i] = vs[i];
+  for (int i = 1; i < n; i++) {
+    int64_t x = key[i]; int j = i;
+    while (j > 0 && sos_less(f, key[j - 1], x)) { key[j] = key[j - 1]; j--; }
+    key[j] = x;
+  }
+}
+static int key_less(const float* f, int n, const int64_t* a, const int64_t* b) {
+  for (int i = 0; i < n; i++) {
+    if (a[i] == b[i]) continue;
+    return sos_less(f, a[i], b[i]);
+  }
+  return 0;
+}
+static int same_set(int n, const int64_t* a, const int64_t* b) {
+  for (int i = 0; i < n; i++) {
+    int found = 0;
+    for (int j = 0; j < n; j++) if (a[i] == b[j]) found = 1;
+    if (!found) return 0;
+  }
+  return 1;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Discrete gradient.                                   */
+/* up[A*T+t] = link slot of the cofacet the cell is paired with, or -1;       */
+/* dn[A*T+t] = position (in the cell's vertex list) of the vertex that is NOT  */
+/*             in the facet it is paired with, or -1.                          */
+/* ------------------------------------------------------------------------- */
+
+typedef struct { int8_t* up; int8_t* dn; } grad_t;
+
+static int grad_alloc(const cx_t* cx, grad_t* G) {
+  size_t n = (size_t)cx->N * cx->T;
+  G->up = (int8_t*)malloc(n); G->dn = (int8_t*)malloc(n);
+  return G->up && G->dn;
+}
+static void grad_free(grad_t* G) { free(G->up); free(G->dn); G->up = G->dn = NULL; }
+
+/* cofacet b = a + {w}; its (anchor id, type) */
+static int64_t cofacet_cell(const cx_t* cx, int64_t A, int ti, int s, int* bt) {
+  co_t a = coords(cx, A);
+  const ctype_t* ct = &cx->t[ti];
+  *bt = ct->cof_type[s];
+  return vid(cx, a.x + ct->cof_anchor[s][0], a.y + ct->cof_anchor[s][1], a.z + ct->cof_anchor[s][2]);
+}
+static int64_t facet_cell(const cx_t* cx, int64_t A, int ti, int k, int* ft) {
+  co_t a = coords(cx, A);
+  const ctype_t* ct = &cx->t[ti];
+  *ft = ct->fac_type[k];
+  return vid(cx, a.x + ct->fac_anchor[k][0], a.y + ct->fac_anchor[k][1], a.z + ct->fac_anchor[k][2]);
+}
+
+/* Pair one d-cell literally.  Returns the chosen slot or -1. */
+static int pair_cell(const cx_t* cx, const float* f, int64_t A, int ti) {
+  const ctype_t* ct = &cx->t[ti];
+  int64_t av[4];
+  if (!cell_vertices(cx, A, ti, av)) return -1;
+  co_t a = coords(cx, A);
+  int n = ct->nv, best = -1;
+  int64_t bestkey[5];
+  for (int s = 0; s < ct->nlink; s++) {
+    int64_t x = a.x + ct->link[s][0], y = a.y + ct->link[s][1], z = a.z + ct->link[s][2];
+    if (!inside(cx, x, y, z)) continue;           /* cofacet leaves the grid */
+    int64_t bv[5], key[5];
+    for (int k = 0; k < n; k++) bv[k] = av[k];
+    bv[n] = vid(cx, x, y, z);
+    key_of(f, n + 1, bv, key);
+    /* G0(b) = b minus its lowest vertex = the first n entries of the key */
+    if (!same_set(n, key, av)) continue;          /* a is not the highest facet of b */
+    if (best < 0 || key_less(f, n + 1, key, bestkey)) {
+      best = s;
+      memcpy(bestkey, key, sizeof(int64_t) * (n + 1));
+    }
+  }
+  return best;
+}
+
+/* compute_gradient: dimensions ascending; a cell already paired with a facet is
+ * not paired again (S:177 / reading A4); P_a empty -> a stays unpaired. */
+static void gradient(const cx_t* cx, const float* f, grad_t* G) {
+  size_t n = (size_t)cx->N * cx->T;
+  memset(G->up, -1, n);
+  memset(G->dn, -1, n);
+  for (int d = 0; d < cx->top; d++) {
+    int t0 = cx->first_of_dim[d], t1 = cx->first_of_dim[d + 1];
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t A = 0; A < cx->N; A++) {
+      for (int ti = t0; ti < t1; ti++) {
+        if (G->dn[A * cx->T + ti] >= 0) continue;
+        int s = pair_cell(cx, f, A, ti);
+        if (s < 0) continue;
+        G->up[A * cx->T + ti] = (int8_t)s;
+        int bt;
+        int64_t B = cofacet_cell(cx, A, ti, s, &bt);
+        G->dn[B * cx->T + bt] = (int8_t)cx->t[ti].cof_pos[s];
+      }
+    }
+  }
+}
+
+static inline int cell_exists(const cx_t* cx, int64_t A, int ti) {
+  int64_t vs[4];
+  return cell_vertices(cx, A, ti, vs);
+}
+static inline int is_crit(const cx_t* cx, const grad_t* G, int64_t A, int ti) {
+  size_t i = (size_t)A * cx->T + ti;
+  return G->up[i] < 0 && G->dn[i] < 0 && cell_exists(cx, A, ti);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Exported: gradient in the documented packed form.                          */
+/*  3D code (u64): bits 0-3 vertex slot (15 = none); edges e_k at 4+3k (7 =  */
+/*  none); triangles t_k at 25+2k (3 = none).  2D code (u16): bits 0-2 vertex  */
+/*  slot (7 = none); edges at 3+2k (3 = none).                                */
+/*  crit mask (u32): bit t set iff cell (anchor, type t) is critical.         */
+/* ------------------------------------------------------------------------- */
+
+static int check_dims(const int64_t* dims) {
+  if (dims[0] < 2 || dims[1] < 2 || dims[2] < 1) return OR_E_DIMS;
+  return OR_OK;
+}
+
+static void export_codes(const cx_t* cx, const grad_t* G, void* codes, uint32_t* crit) {
+  for (int64_t A = 0; A < cx->N; A++) {
+    uint64_t c = 0;
+    uint32_t m = 0;
+    for (int ti = 0; ti < cx->T; ti++) {
+      int d = cx->t[ti].dim;
+      int k = ti - cx->first_of_dim[d];
+      int s = G->up[A * cx->T + ti];
+      if (cx->D == 3) {
+        if (d == 0) c |= (uint64_t)(s < 0 ? 15 : s);
+        else if (d == 1) c |= (uint64_t)(s < 0 ? 7 : s) << (4 + 3 * k);
+        else if (d == 2) c |= (uint64_t)(s < 0 ? 3 : s) << (25 + 2 * k);
+      } else {
+        if (d == 0) c |= (uint64_t)(s < 0 ? 7 : s);
+        else if (d == 1) c |= (uint64_t)(s < 0 ? 3 : s) << (3 + 2 * k);
+      }
+      if (is_crit(cx, G, A, ti)) m |= 1u << ti;
+    }
+    if (codes) {
+      if (cx->D == 3) ((uint64_t*)codes)[A] = c;
+      else ((uint16_t*)codes)[A] = (uint16_t)c;
+    }
+    if (crit) crit[A] = m;
+  }
+}
+
+int dmtz_oracle_gradient(const int64_t* dims, const float* field, void* codes, uint32_t* crit) {
+  int st = check_dims(dims);
+  if (st) return st;
+  for (int64_t i = 0; i < dims[0] * dims[1] * dims[2]; i++) if (!isfinite(field[i])) return OR_E_NONFINITE;
+  cx_t cx; build_complex(&cx, dims[0], dims[1], dims[2]);
+  grad_t G;
+  if (!grad_alloc(&cx, &G)) return OR_E_ARG;
+  gradient(&cx, field, &G);
+  export_codes(&cx, &G, codes, crit);
+  grad_free(&G);
+  return OR_OK;
+}
+
+/* Introspection for tests: the complex as the oracle derived it. */
+int dmtz_oracle_complex_info(const int64_t* dims, int32_t* out_T, int32_t* dim_of_type,
+                             int32_t* nlink_of_type, int32_t* offsets /* T*4*3 */,
+                             int32_t* links /* T*14*3 */) {
+  cx_t cx; build_complex(&cx, dims[0], dims[1], dims[2]);
+  *out_T = cx.T;
+  for (int ti = 0; ti < cx.T; ti++) {
+    dim_of_type[ti] = cx.t[ti].dim;
+    nlink_of_type[ti] = cx.t[ti].nlink;
+    for (int k = 0; k < 4; k++) for (int a = 0; a < 3; a++)
+      offsets[(ti * 4 + k) * 3 + a] = k < cx.t[ti].nv ? cx.t[ti].off[k][a] : 0;
+    for (int s = 0; s < MAXLINK; s++) for (int a = 0; a < 3; a++)
+      links[(ti * MAXLINK + s) * 3 + a] = s < cx.t[ti].nlink ? cx.t[ti].link[s][a] : 0;
+  }
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* The C-loop with Eq. 2 edits.         */
+/* ------------------------------------------------------------------------- */
+
+typedef struct {
+  int64_t rounds, n_edited, n_quantized, n_lossless, n_false_round0;
+  int64_t false_by_kind_round0[8]; /* FPmin FNmin FP1s FN1s FP2s FN2s FPmax FNmax */
+  int32_t status, pad;
+} or_stats;
+
+typedef struct { uint64_t v; uint16_t q; uint8_t lossless; uint8_t pad; float value; } or_edit;
+
+/* lb = RU(f - xi): the smallest float >= f - xi, so g >= lb implies |g - f| <= xi
+ * exactly (reading A9). */
+static float lower_bound_ru(float f, float xi) {
+  int old = fegetround();
+  fesetround(FE_UPWARD);
+  volatile float a = f, b = xi;
+  volatile float r = a - b;
+  fesetround(old);
+  return r;
+}
+static float upper_bound_rd(float f, float xi) {
+  int old = fegetround();
+  fesetround(FE_DOWNWARD);
+  volatile float a = f, b = xi;
+  volatile float r = a + b;
+  fesetround(old);
+  return r;
+}
+
+/* kind index: 2*critical-class + (false negative ? 1 : 0); classes: min, 1-saddle,
+ * 2-saddle, max (2D: the triangle is the max) */
+static int kind_of(const cx_t* cx, int dim, int fn) {
+  int cls = (dim == cx->top) ? 3 : dim;
+  return 2 * cls + (fn ? 1 : 0);
+}
+
+/* SoS-lowest vertex of a cell under field f */
+static int64_t lowest_vertex(const float* f, int n, const int64_t* vs) {
+  int64_t m = vs[0];
+  for (int i = 1; i < n; i++) if (sos_less(f, vs[i], m)) m = vs[i];
+  return m;
+}
+
+/* Target vertex for false cell a (rules R1/R2/R3a/R3b):
+ *  FP (critical in g, paired in f):
+ *     the vertex of the larger cell of a's f-pair that is not in the smaller one.
+ *  FN (critical in f, paired in g):
+ *     paired up in g             -> m = f-lowest vertex of a             (R2)
+ *     paired down in g with c,
+ *        y = a \ c, m != y        -> m                                    (R3a)
+ *        m == y                   -> the vertex c is paired with in f     (R3b)
+ * Returns -1 on an internal inconsistency. */
+static int64_t target_of(const cx_t* cx, const float* f, const grad_t* Gf, const grad_t* Gg,
+                         int64_t A, int ti, int fn) {
+  const ctype_t* ct = &cx->t[ti];
+  int64_t av[4];
+  cell_vertices(cx, A, ti, av);
+  size_t i = (size_t)A * cx->T + ti;
+  co_t a = coords(cx, A);
+  if (!fn) {
+    if (Gf->up[i] >= 0) {
+      int s = Gf->up[i];
+      return vid(cx, a.x + ct->link[s][0], a.y + ct->link[s][1], a.z + ct->link[s][2]);
+    }
+    return av[(int)Gf->dn[i]];
+  }
+  int64_t m = lowest_vertex(f, ct->nv, av);
+  if (Gg->up[i] >= 0) return m;
+  int k = Gg->dn[i];
+  int64_t y = av[k];
+  if (m != y) return m;
+  int ft;
+  int64_t C = facet_cell(cx, A, ti, k, &ft);
+  int s = Gf->up[(size_t)C * cx->T + ft];
+  if (s < 0) return -1;
+  co_t c = coords(cx, C);
+  const ctype_t* fc = &cx->t[ft];
+  return vid(cx, c.x + fc->link[s][0], c.y + fc->link[s][1], c.z + fc->link[s][2]);
+}
+
+/* One literal round of classification: F = C_f xor C_g (tier 1: dims 0 and top,
+ * P:140-141), target set T (a set: each vertex at most once per round).
+ * Returns |F| (or -1 on internal error); kinds[8] accumulates counts. */
+static int64_t classify(const cx_t* cx, const float* f, const grad_t* Gf, const grad_t* Gg,
+                        int tier, uint8_t* T, int64_t* kinds) {
+  int64_t nF = 0, bad = 0;
+  int64_t kk[8] = {0};
+#pragma omp parallel for schedule(dynamic, 4096) reduction(+ : nF, bad) reduction(+ : kk[:8])
+  for (int64_t A = 0; A < cx->N; A++) {
+    for (int ti = 0; ti < cx->T; ti++) {
+      int d = cx->t[ti].dim;
+      if (tier == 1 && d != 0 && d != cx->top) continue;
+      if (!cell_exists(cx, A, ti)) continue;
+      int cf = is_crit(cx, Gf, A, ti), cg = is_crit(cx, Gg, A, ti);
+      if (cf == cg) continue;
+      int fn = cf;  /* critical in f, paired in g: false negative */
+      nF++;
+      kk[kind_of(cx, d, fn)]++;
+      int64_t v = target_of(cx, f, Gf, Gg, A, ti, fn);
+      if (v < 0) { bad++; continue; }
+#pragma omp atomic write
+      T[v] = 1;
+    }
+  }
+  for (int k = 0; k < 8; k++) kinds[k] += kk[k];
+  return bad ? -1 : nF;
+}
+
+int dmtz_oracle_correct(const int64_t* dims, const float* f, const float* fhat, float xi,
+                        int32_t q_max, int32_t q_cap, int32_t tier, int64_t max_rounds,
+                        float* g_out, uint32_t* state_out, or_edit* edits, int64_t edits_capacity,
+                        int64_t* n_edits, or_stats* stats) {
+  memset(stats, 0, sizeof *stats);
+  *n_edits = 0;
+  int st = check_dims(dims);
+  if (st) { stats->status = st; return st; }
+  if (!(xi > 0.0f) || !isfinite(xi) || q_max < 0 || q_max > 30 || q_cap < 1 || q_cap > 65535 ||
+      (tier != 1 && tier != 2) || max_rounds < 0) {
+    stats->status = OR_E_ARG; return OR_E_ARG;
+  }
+  cx_t cx; build_complex(&cx, dims[0], dims[1], dims[2]);
+  int64_t N = cx.N;
+  for (int64_t v = 0; v < N; v++)
+    if (!isfinite(f[v]) || !isfinite(fhat[v])) { stats->status = OR_E_NONFINITE; return OR_E_NONFINITE; }
+  /* |fhat - f| <= xi exactly  <=>  RU(f - xi) <= fhat <= RD(f + xi) */
+  for (int64_t v = 0; v < N; v++)
+    if (fhat[v] < lower_bound_ru(f[v], xi) || fhat[v] > upper_bound_rd(f[v], xi)) {
+      stats->status = OR_E_BOUND; return OR_E_BOUND;
+    }
+  if (max_rounds == 0) max_rounds = N * (int64_t)(q_cap + 1);
+  float step = ldexpf(xi, -q_max);           /* xi / 2^q_max, exact */
+  float* lb = (float*)malloc(sizeof(float) * N);
+  uint16_t* q = (uint16_t*)calloc(N, sizeof(uint16_t));
+  uint8_t* lossless = (uint8_t*)calloc(N, 1);
+  uint8_t* T = (uint8_t*)calloc(N, 1);
+  grad_t Gf, Gg;
+  if (!lb || !q || !lossless || !T || !grad_alloc(&cx, &Gf) || !grad_alloc(&cx, &Gg)) {
+    stats->status = OR_E_ARG; return OR_E_ARG;
+  }
+  for (int64_t v = 0; v < N; v++) { lb[v] = lower_bound_ru(f[v], xi); g_out[v] = fhat[v]; }
+  gradient(&cx, f, &Gf);
+  int status = OR_OK;
+  for (int64_t round = 1;; round++) {
+    gradient(&cx, g_out, &Gg);
+    memset(T, 0, N);
+    int64_t kinds[8] = {0};
+    int64_t nF = classify(&cx, f, &Gf, &Gg, tier, T, kinds);
+    if (nF < 0) { status = OR_E_INTERNAL; break; }
+    if (round == 1) {
+      stats->n_false_round0 = nF;
+      memcpy(stats->false_by_kind_round0, kinds, sizeof kinds);
+    }
+    if (nF == 0) break;
+    stats->rounds = round;
+    int changed = 0;
+    for (int64_t v = 0; v < N; v++) {
+      if (!T[v] || lossless[v]) continue;
+      changed = 1;
+      /* Eq. 2: one step of xi/2^q_max, recomputed from fhat:
+       * g' = RN(fhat - RN((q+1) * step)), accepted iff q+1 <= q_cap and g' >= lb;
+       * otherwise clamp to the lower bound and store losslessly. */
+      if (q[v] + 1 <= q_cap) {
+        float s = (float)(q[v] + 1) * step;
+        float gp = fhat[v] - s;
+        if (gp >= lb[v]) { q[v]++; g_out[v] = gp; continue; }
+      }
+      g_out[v] = lb[v];
+      lossless[v] = 1;
+    }
+    if (!changed) { status = OR_E_STUCK; break; }
+    if (round == max_rounds) { status = OR_E_ITER_CAP; break; }
+  }
+  int64_t ne = 0;
+  for (int64_t v = 0; v < N; v++) {
+    if (state_out) state_out[v] = (uint32_t)q[v] | ((uint32_t)lossless[v] << 16);
+    if (q[v] == 0 && !lossless[v]) continue;
+    stats->n_edited++;
+    if (lossless[v]) stats->n_lossless++; else stats->n_quantized++;
+    if (edits && ne < edits_capacity) {
+      edits[ne].v = (uint64_t)v; edits[ne].q = q[v]; edits[ne].lossless = lossless[v];
+      edits[ne].pad = 0; edits[ne].value = g_out[v];
+    }
+    ne++;
+  }
+  *n_edits = ne;
+  if (status == OR_OK && edits && ne > edits_capacity) status = OR_E_CAPACITY;
+  stats->status = status;
+  free(lb); free(q); free(lossless); free(T);
+  grad_free(&Gf); grad_free(&Gg);
+  return status;
+}
+
+/* ------------------------------------------------------------------------- */
+/* V-path traces (P:82 gradient paths; P:228 ascending/descending paths and   */
+/* saddle-saddle connectors).                                                 */
+/* cell id = (dim << 56) | (anchor * T_dim + index of the type within dim).   */
+/* ------------------------------------------------------------------------- */
+
+enum { KIND_DESC = 1, KIND_ASC = 2, KIND_CONN = 4 };
+
+static uint64_t cell_id(const cx_t* cx, int64_t A, int ti) {
+  int d = cx->t[ti].dim;
+  int Td = cx->first_of_dim[d + 1] - cx->first_of_dim[d];
+  return ((uint64_t)d << 56) | (uint64_t)(A * Td + (ti - cx->first_of_dim[d]));
+}
+
+typedef struct {
+  int64_t cap_b, cap_c, nb, nc;
+  int64_t* off; uint64_t* cells; uint64_t* origin; uint64_t* terminal; uint8_t* kind;
+} csr_t;
+
+static void csr_begin(csr_t* o, uint64_t origin, uint8_t kind) {
+  if (o->nb < o->cap_b) { o->off[o->nb] = o->nc; o->origin[o->nb] = origin; o->kind[o->nb] = kind; }
+}
+static void csr_push(csr_t* o, uint64_t c) {
+  if (o->nc < o->cap_c) o->cells[o->nc] = c;
+  o->nc++;
+}
+static void csr_end(csr_t* o, uint64_t terminal) {
+  if (o->nb < o->cap_b) { o->terminal[o->nb] = terminal; o->off[o->nb + 1] = o->nc; }
+  o->nb++;
+}
+
+/* top cofacets of a (top-1)-cell (at most 2), in slot order */
+static int top_cofacets(const cx_t* cx, int64_t A, int ti, int64_t* Bs, int* bts) {
+  const ctype_t* ct = &cx->t[ti];
+  co_t a = coords(cx, A);
+  int n = 0;
+  for (int s = 0; s < ct->nlink; s++) {
+    if (!inside(cx, a.x + ct->link[s][0], a.y + ct->link[s][1], a.z + ct->link[s][2])) continue;
+    Bs[n] = cofacet_cell(cx, A, ti, s, &bts[n]);
+    n++;
+  }
+  return n;
+}
+
+int dmtz_oracle_trace(const int64_t* dims, const float* field, uint32_t kinds,
+                      int64_t cap_branches, int64_t cap_cells, int64_t* branch_offsets,
+                      uint64_t* cells, uint64_t* origin, uint64_t* terminal, uint8_t* kind,
+                      int64_t* n_branches, int64_t* n_cells) {
+  int st = check_dims(dims);
+  if (st) return st;
+  cx_t cx; build_complex(&cx, dims[0], dims[1], dims[2]);
+  grad_t G;
+  if (!grad_alloc(&cx, &G)) return OR_E_ARG;
+  gradient(&cx, field, &G);
+  csr_t o = {cap_branches, cap_cells, 0, 0, branch_offsets, cells, origin, terminal, kind};
+  if (cap_branches > 0) branch_offsets[0] = 0;
+  int64_t maxsteps = cx.N * cx.T + 1;
+  int err = 0;
+  int T = cx.T;
+  /* descending: from each endpoint of each critical edge (1-saddle), follow
+   * vertex -> paired edge -> its other vertex until a critical vertex */
+  if (kinds & KIND_DESC) {
+    for (int64_t A = 0; A < cx.N && !err; A++)
+      for (int ti = cx.first_of_dim[1]; ti < cx.first_of_dim[2] && !err; ti++) {
+        if (!is_crit(&cx, &G, A, ti)) continue;
+        int64_t ev[2];
+        cell_vertices(&cx, A, ti, ev);
+        for (int b = 0; b < 2; b++) {
+          csr_begin(&o, cell_id(&cx, A, ti), KIND_DESC);
+          int64_t v = ev[b];
+          csr_push(&o, cell_id(&cx, v, 0));
+          int64_t steps = 0;
+          while (G.up[(size_t)v * T + 0] >= 0) {
+            int s = G.up[(size_t)v * T + 0], bt;
+            int64_t E = cofacet_cell(&cx, v, 0, s, &bt);
+            co_t c = coords(&cx, v);
+            int64_t w = vid(&cx, c.x + cx.t[0].link[s][0], c.y + cx.t[0].link[s][1], c.z + cx.t[0].link[s][2]);
+            csr_push(&o, cell_id(&cx, E, bt));
+            csr_push(&o, cell_id(&cx, w, 0));
+            v = w;
+            if (++steps > maxsteps) { err = 1; break; }
+          }
+          csr_end(&o, cell_id(&cx, v, 0));
+        }
+      }
+  }
+  /* ascending: from each critical (top-1)-cell, through each top cofacet t:
+   * t critical -> maximum; else t is paired down with facet c; continue
+   * through c's other top cofacet; none -> the path leaves the domain */
+  if ((kinds & KIND_ASC) && !err) {
+    int d = cx.top - 1;
+    for (int64_t A = 0; A < cx.N && !err; A++)
+      for (int ti = cx.first_of_dim[d]; ti < cx.first_of_dim[d + 1] && !err; ti++) {
+        if (!is_crit(&cx, &G, A, ti)) continue;
+        int64_t Bs[2]; int bts[2];
+        int nb = top_cofacets(&cx, A, ti, Bs, bts);
+        for (int b = 0; b < nb; b++) {
+          csr_begin(&o, cell_id(&cx, A, ti), KIND_ASC);
+          int64_t B = Bs[b]; int bt = bts[b];
+          uint64_t term = BOUNDARY_ID;
+          int64_t steps = 0;
+          for (;;) {
+            csr_push(&o, cell_id(&cx, B, bt));
+            if (is_crit(&cx, &G, B, bt)) { term = cell_id(&cx, B, bt); break; }
+            int k = G.dn[(size_t)B * T + bt];
+            if (k < 0) { err = 1; break; }
+            int ct;
+            int64_t C = facet_cell(&cx, B, bt, k, &ct);
+            csr_push(&o, cell_id(&cx, C, ct));
+            int64_t Cs[2]; int cts[2];
+            int nc = top_cofacets(&cx, C, ct, Cs, cts);
+            int moved = 0;
+            for (int j = 0; j < nc; j++)
+              if (!(Cs[j] == B && cts[j] == bt)) { B = Cs[j]; bt = cts[j]; moved = 1; break; }
+            if (!moved) break;  /* boundary facet: BOUNDARY terminal */
+            if (++steps > maxsteps) { err = 1; break; }
+          }
+          csr_end(&o, term);
+        }
+      }
+  }
+  /* saddle-saddle connectors (3D): breadth-first from each critical triangle over
+   * facet edges: critical edge -> reached 1-saddle (recorded each time met);
+   * edge paired up with a triangle t' != current -> enqueue t' if unvisited */
+  if ((kinds & KIND_CONN) && !err && cx.D == 3) {
+    int64_t qcap = 1024;
+    int64_t* qa = (int64_t*)malloc(sizeof(int64_t) * qcap);
+    int* qt = (int*)malloc(sizeof(int) * qcap);
+    uint8_t* seen = (uint8_t*)calloc((size_t)cx.N * T, 1);
+    for (int64_t A = 0; A < cx.N && !err; A++)
+      for (int ti = cx.first_of_dim[2]; ti < cx.first_of_dim[3] && !err; ti++) {
+        if (!is_crit(&cx, &G, A, ti)) continue;
+        csr_begin(&o, cell_id(&cx, A, ti), KIND_CONN);
+        int64_t head = 0, tail = 0;
+        qa[tail] = A; qt[tail] = ti; tail++;
+        seen[(size_t)A * T + ti] = 1;
+        while (head < tail) {
+          int64_t B = qa[head]; int bt = qt[head]; head++;
+          for (int k = 0; k < 3; k++) {
+            int et;
+            int64_t E = facet_cell(&cx, B, bt, k, &et);
+            if (is_crit(&cx, &G, E, et)) { csr_push(&o, cell_id(&cx, E, et)); continue; }
+            int s = G.up[(size_t)E * T + et];
+            if (s < 0) continue;  /* paired down with a vertex: the path stops */
+            int nt;
+            int64_t Nb = cofacet_cell(&cx, E, et, s, &nt);
+            if (Nb == B && nt == bt) continue;
+            if (seen[(size_t)Nb * T + nt]) continue;
+            seen[(size_t)Nb * T + nt] = 1;
+            csr_push(&o, cell_id(&cx, Nb, nt));
+            if (tail == qcap) {
+              qcap *= 2;
+              qa = (int64_t*)realloc(qa, sizeof(int64_t) * qcap);
+              qt = (int*)realloc(qt, sizeof(int) * qcap);
+            }
+            qa[tail] = Nb; qt[tail] = nt; tail++;
+          }
+        }
+        for (int64_t j = 0; j < tail; j++) seen[(size_t)qa[j] * T + qt[j]] = 0;
+        csr_end(&o, BOUNDARY_ID);
+      }
+    free(qa); free(qt); free(seen);
+  }
+  grad_free(&G);
+  *n_branches = o.nb;
+  *n_cells = o.nc;
+  if (err) return OR_E_INTERNAL;
+  if (o.nb > cap_branches || o.nc > cap_cells) return OR_E_CAPACITY;
+  return OR_OK;
+}
+
+int dmtz_oracle_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+/* Number of cells of each dimension of the grid complex (for the closed-form
+ * count pins S:60-62 and the Euler characteristic). */
+int dmtz_oracle_cell_counts(const int64_t* dims, int64_t* counts /* [4] */) {
+  int st = check_dims(dims);
+  if (st) return st;
+  cx_t cx; build_complex(&cx, dims[0], dims[1], dims[2]);
+  for (int d = 0; d < 4; d++) counts[d] = 0;
+  for (int64_t A = 0; A < cx.N; A++)
+    for (int ti = 0; ti < cx.T; ti++)
+      if (cell_exists(&cx, A, ti)) counts[cx.t[ti].dim]++;
+  return OR_OK;
+}

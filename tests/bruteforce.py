@@ -1,0 +1,240 @@
+"""Explicit-complex brute force (pure Python, tiny inputs) -- pins for the oracle.
+
+Shares no code with ``oracle/`` or the CUDA path.  The complex is built a
+different way from the oracle's: every unit cube (square) is cut into the
+D! Kuhn simplices  b, b+e_p1, b+e_p1+e_p2, ...  (one per axis permutation p),
+and the complex is the set of all faces of those simplices.  Cells are
+frozensets of integer coordinate triples; facets and cofacets are set operations.
+
+The gradient is Eq. 1 + the pairing rule read directly off the paper
+(P:84-92): keys are the cell's (value, index) pairs sorted
+descending; P_a = {b in cofacets(a) : b minus its lowest vertex == a};
+a is paired with min-key(P_a) unless already paired with a facet.
+"""
+from __future__ import annotations
+
+import itertools
+from fractions import Fraction
+
+import numpy as np
+
+
+class Complex:
+    def __init__(self, nx, ny, nz=1, pad=0):
+        """Grid complex; ``pad`` > 0 builds it on a grid enlarged by ``pad`` on every
+        side (coordinates shifted) so that interior links of boundary cells exist."""
+        self.n = (nx, ny, nz)
+        self.D = 2 if nz == 1 else 3
+        self.pad = pad
+        D = self.D
+        lo = -pad
+        hx, hy = nx + pad, ny + pad
+        hz = nz + pad if D == 3 else 1
+        zlo = lo if D == 3 else 0
+        self.verts = [(x, y, z) for z in range(zlo, hz) for y in range(lo, hy) for x in range(lo, hx)]
+        maximal = set()
+        for z in range(zlo, hz - (1 if D == 3 else 0)):
+            for y in range(lo, hy - 1):
+                for x in range(lo, hx - 1):
+                    for perm in itertools.permutations(range(D)):
+                        p = [x, y, z]
+                        simp = [tuple(p)]
+                        for ax in perm:
+                            p[ax] += 1
+                            simp.append(tuple(p))
+                        maximal.add(frozenset(simp))
+        cells = set()
+        for s in maximal:
+            for r in range(1, len(s) + 1):
+                for sub in itertools.combinations(sorted(s), r):
+                    cells.add(frozenset(sub))
+        self.cells = cells
+        self.by_dim = {d: sorted((c for c in cells if len(c) == d + 1), key=sorted) for d in range(D + 1)}
+        self.cofacets = {c: [] for c in cells}
+        for c in cells:
+            if len(c) > 1:
+                for v in c:
+                    self.cofacets[c - {v}].append(c)
+
+    def vid(self, p):
+        nx, ny, _ = self.n
+        return p[0] + nx * (p[1] + ny * p[2])
+
+    def inside(self, p):
+        return all(0 <= p[a] < self.n[a] for a in range(3))
+
+
+def sos_key(f, p, C):
+    return (float(f[C.vid(p)]), C.vid(p))
+
+
+def cell_key(f, cell, C):
+    """Eq. 1 as a lexicographic key: vertices sorted descending by (value, index)."""
+    return sorted((sos_key(f, p, C) for p in cell), reverse=True)
+
+
+def gradient(C: Complex, f):
+    """Literal pairing.  Returns dict cell -> partner cell (both directions)."""
+    fl = np.asarray(f, dtype=np.float32).ravel()
+    pair = {}
+    for d in range(C.D):
+        for a in C.by_dim[d]:
+            if a in pair:
+                continue
+            P = []
+            for b in C.cofacets[a]:
+                kb = sorted(b, key=lambda p: sos_key(fl, p, C), reverse=True)
+                if frozenset(kb[:-1]) == a:          # G0(b) == a
+                    P.append(b)
+            if P:
+                b = min(P, key=lambda c: cell_key(fl, c, C))
+                pair[a] = b
+                pair[b] = a
+    return pair
+
+
+def critical(C: Complex, pair):
+    return {c for c in C.cells if c not in pair}
+
+
+def ru32(x: Fraction) -> np.float32:
+    """Smallest float32 >= x (exact)."""
+    c = np.float32(float(x))
+    while Fraction(float(c)) < x:
+        c = np.nextafter(c, np.float32(np.inf), dtype=np.float32)
+    while True:
+        p = np.nextafter(c, np.float32(-np.inf), dtype=np.float32)
+        if Fraction(float(p)) >= x:
+            c = p
+        else:
+            return c
+
+
+def c_loop(C: Complex, f, fhat, xi, q_max=6, q_cap=None, tier=2, max_rounds=100000):
+    """Synchronous C-loop with the target rules R1/R2/R3a/R3b,
+    written independently of the oracle.  Returns (status, g, q, lossless, stats)."""
+    if q_cap is None:
+        q_cap = q_max
+    f = np.asarray(f, np.float32).ravel()
+    fhat = np.asarray(fhat, np.float32).ravel()
+    xi32 = np.float32(xi)
+    step = np.float32(float(Fraction(float(xi32)) / 2 ** q_max))
+    assert Fraction(float(step)) == Fraction(float(xi32)) / 2 ** q_max
+    lb = np.array([ru32(Fraction(float(v)) - Fraction(float(xi32))) for v in f], np.float32)
+    g = fhat.copy()
+    q = np.zeros(f.size, np.int64)
+    lossless = np.zeros(f.size, bool)
+    pf = gradient(C, f)
+    cf = critical(C, pf)
+    top = C.D
+    stats = dict(rounds=0, n_false_round0=0, kinds=[0] * 8)
+    rnd = 0
+    while True:
+        rnd += 1
+        pg = gradient(C, g)
+        cg = critical(C, pg)
+        F = cf ^ cg
+        if tier == 1:
+            F = {c for c in F if len(c) - 1 in (0, top)}
+        if rnd == 1:
+            stats["n_false_round0"] = len(F)
+            for a in F:
+                d = len(a) - 1
+                cls = 3 if d == top else d
+                stats["kinds"][2 * cls + (1 if a in cf else 0)] += 1
+        if not F:
+            return "OK", g, q, lossless, stats
+        stats["rounds"] = rnd
+        T = set()
+        for a in F:
+            lowest_f = min(a, key=lambda p: sos_key(f, p, C))
+            if a in cg:       # FP: critical in g, paired in f  -> R1
+                b = pf[a]
+                big, small = (b, a) if len(b) > len(a) else (a, b)
+                (v,) = big - small
+            elif len(pg[a]) > len(a):   # FN, paired up in g -> R2
+                v = lowest_f
+            else:                       # FN, paired down in g with gamma -> R3
+                gamma = pg[a]
+                (y,) = a - gamma
+                if lowest_f != y:
+                    v = lowest_f
+                else:
+                    (v,) = pf[gamma] - gamma
+            T.add(C.vid(v))
+        changed = False
+        for v in sorted(T):
+            if lossless[v]:
+                continue
+            changed = True
+            if q[v] + 1 <= q_cap:
+                gp = np.float32(fhat[v] - np.float32(np.float32(q[v] + 1) * step))
+                if gp >= lb[v]:
+                    q[v] += 1
+                    g[v] = gp
+                    continue
+            g[v] = lb[v]
+            lossless[v] = True
+        if not changed:
+            return "STUCK", g, q, lossless, stats
+        if rnd == max_rounds:
+            return "ITER_CAP", g, q, lossless, stats
+
+
+def trace(C: Complex, f):
+    """Descending / ascending / connector traces, returned as python lists of
+    (kind, origin, [cells...], terminal) with cells as frozensets."""
+    fl = np.asarray(f, np.float32).ravel()
+    pair = gradient(C, fl)
+    crit = critical(C, pair)
+    top = C.D
+    out = []
+
+    def order(cells):
+        # origin cells ordered by (anchor index, type) is checked by the caller; here by vid tuple
+        return sorted(cells, key=lambda c: sorted(C.vid(p) for p in c))
+
+    for e in order(c for c in crit if len(c) == 2):
+        for v in sorted(e, key=C.vid):
+            cells = [frozenset([v])]
+            cur = frozenset([v])
+            while cur in pair:
+                edge = pair[cur]
+                assert len(edge) == 2
+                (w,) = edge - cur
+                cells += [edge, frozenset([w])]
+                cur = frozenset([w])
+            out.append(("desc", e, cells, cur))
+    for c in order(c for c in crit if len(c) == top):
+        for t in sorted(C.cofacets[c], key=lambda t: C.vid(next(iter(t - c)))):
+            cells = [t]
+            term = None
+            while True:
+                if t in crit:
+                    term = t
+                    break
+                cc = pair[t]
+                cells.append(cc)
+                others = [x for x in C.cofacets[cc] if x != t]
+                if not others:
+                    term = "BOUNDARY"
+                    break
+                t = others[0]
+                cells.append(t)
+            out.append(("asc", c, cells, term))
+    if C.D == 3:
+        for s in order(c for c in crit if len(c) == 3):
+            reached, visited = [], [s]
+            seen = {s}
+            qi = 0
+            while qi < len(visited):
+                t = visited[qi]
+                qi += 1
+                for e in (t - {p} for p in sorted(t, key=C.vid)):
+                    if e in crit:
+                        reached.append(e)
+                    elif len(pair[e]) == 3 and pair[e] != t and pair[e] not in seen:
+                        seen.add(pair[e])
+                        visited.append(pair[e])
+            out.append(("conn", s, visited[1:], reached))
+    return out
