@@ -1,0 +1,197 @@
+/*
+ * include/dmtz.h -- C ABI of the B200-native DMTz hot path (libdmtz.so).
+ *
+ * DMTz (arXiv 2409.17346) preserves the discrete Morse-Smale complex of a 2D/3D
+ * scalar field under error-bounded lossy compression by editing the
+ * decompressed field.  This library implements its data-parallel hot path on
+ * sm_100a: the discrete gradient, the
+ * critical-cell correction loop "C-loop" with quantized edits, and
+ * the V-path separatrix traces the S-loop checks.
+ * P:<n> cites line n of the paper text; DESIGN.md §3 lists every reading taken
+ * where the paper is silent or garbled.
+ *
+ * Conventions
+ *   - Every pointer is a DEVICE pointer unless marked (host).  The caller owns
+ *     every buffer; the library never allocates device memory (scratch comes
+ *     from the caller's workspace, sized by dmtz_workspace_bytes).
+ *   - Fields are float32, x fastest: v = x + nx*(y + ny*z).  nz == 1 means 2D.
+ *   - Calls are asynchronous on the given stream, except dmtz_correct and
+ *     dmtz_trace_separatrices, which synchronise the stream to read counters
+ *     and write their host outputs before returning.
+ *   - No exception crosses the ABI; every call returns a dmtz_status.  Details of
+ *     the last failure on the calling thread: dmtz_last_error().
+ *
+ * Cell complex (reading A1): the Freudenthal/Kuhn triangulation of
+ * the grid.  Every cell is identified by its anchor (its lowest-index vertex)
+ * and a TYPE: the chain 0 = m0 < m1 < ... < md of nested bit masks (dx = 1,
+ * dy = 2, dz = 4) of its vertex offsets.  Types are numbered by dimension, then
+ * lexicographically by the mask tuple:
+ *   3D (26 types): vertex 0; edges 1..7 (masks 1..7); triangles 8..19
+ *     ((1,3)(1,5)(1,7)(2,3)(2,6)(2,7)(3,7)(4,5)(4,6)(4,7)(5,7)(6,7));
+ *     tetrahedra 20..25 ((1,3,7)(1,5,7)(2,3,7)(2,6,7)(4,5,7)(4,6,7)).
+ *   2D (6 types): vertex 0; edges 1..3 (masks 1,2,3); triangles 4,5 ((1,3),(2,3)).
+ * The LINK of a cell is the set of vertices w such that cell + {w} is a cell of
+ * the unbounded grid; its SLOTS are the link vertices in ascending global index
+ * ((dz,dy,dx) lexicographic) order.
+ *
+ * Gradient codes: cell a is paired with the cofacet
+ * a + {w} ("a -> w") or is not paired upward.  One code per anchor:
+ *   3D uint64: bits 0-3 vertex slot (15 = none), edge type k (1..7) at
+ *              4 + 3(k-1) (7 = none), triangle type k (8..19) at 25 + 2(k-8)
+ *              (3 = none); bits 49-63 zero.
+ *   2D uint16: bits 0-2 vertex slot (7 = none), edge type k (1..3) at
+ *              3 + 2(k-1) (3 = none); bits 9-15 zero.
+ * A cell is CRITICAL iff it exists (all its vertices lie in the grid), it is
+ * not paired upward, and no facet is paired with it.  Critical masks are
+ * uint32 per anchor, bit t = type t critical.
+ *
+ * Cell ids (trace output): (dim << 56) | (anchor * T_dim + index of the type
+ * within its dimension), T_dim = 1/7/12/6 (3D), 1/3/2 (2D).
+ */
+#ifndef DMTZ_H
+#define DMTZ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* dmtz_stream_t; /* a cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  DMTZ_OK = 0,
+  DMTZ_E_ARG = 1,       /* bad argument (NULL pointer, xi <= 0, q_max/q_cap/tier out of range) */
+  DMTZ_E_DIMS = 2,      /* nx < 2 or ny < 2 or nz < 1 */
+  DMTZ_E_NONFINITE = 3, /* NaN/Inf in f or fhat; dmtz_last_error names the first index */
+  DMTZ_E_BOUND = 4,     /* |fhat - f| > xi somewhere; first index in dmtz_last_error */
+  DMTZ_E_CAPACITY = 5,  /* output buffer too small; the needed count is still returned */
+  DMTZ_E_ITER_CAP = 6,  /* max_rounds reached with false cells left */
+  DMTZ_E_STUCK = 7,     /* false cells left but every target is already at its lower bound
+                           (reading A10: f32 lower bounds can merge distinct values) */
+  DMTZ_E_CUDA = 8,      /* a CUDA runtime error; message in dmtz_last_error */
+  DMTZ_E_NCCL = 9,      /* reserved for the multi-GPU layer */
+  DMTZ_E_OOM = 10,      /* workspace smaller than dmtz_workspace_bytes */
+  DMTZ_E_INTERNAL = 11  /* an invariant of the gradient did not hold (never expected) */
+} dmtz_status;
+
+typedef struct { int64_t nx, ny, nz; } dmtz_dims;
+
+typedef struct {
+  float xi;            /* absolute error bound xi > 0; relative -> absolute is the caller's */
+  int32_t q_max;       /* edit step xi / 2^q_max, 0..30 (default 6) */
+  int32_t q_cap;       /* max quantized steps per vertex, 1..65535; the paper's literal
+                          "q < q_max" is q_cap = q_max (reading A6) */
+  int32_t tier;        /* 1: extrema only (dims 0 and top), 2: all critical cells */
+  int64_t max_rounds;  /* 0 = N * (q_cap + 1), the bound of the progress argument */
+  int32_t full_sweeps; /* 1: every round re-evaluates every anchor; 0: only the dirty frontier
+                          (bit-identical results) */
+  int32_t profile;     /* 1: time each round's sweep with CUDA events on `stream` (stats.sweep_ms) */
+} dmtz_correct_opts;
+
+/* One edited vertex: quantized (g = RN(fhat - RN(q * xi/2^q_max))) or
+ * lossless (g = the lower bound, stored as its float bits in `value`). */
+typedef struct {
+  uint64_t v;        /* global vertex index */
+  uint16_t q;        /* quantized steps taken (for lossless entries: steps before the clamp) */
+  uint8_t lossless;  /* 1 = value is stored losslessly */
+  uint8_t pad;
+  float value;       /* final edited value g_v (bit-exact) */
+} dmtz_edit;         /* 16 bytes; edit lists are sorted by v */
+
+typedef struct {
+  int64_t rounds;          /* C-loop rounds that found false cells (and edited) */
+  int64_t n_edited, n_quantized, n_lossless;
+  int64_t n_false_round0;  /* false critical cells before any edit */
+  int64_t false_by_kind_round0[8]; /* FPmin FNmin FP1s FN1s FP2s FN2s FPmax FNmax */
+  int32_t status;
+  int32_t pad;
+  int64_t sweeps;          /* gradient evaluations of g (rounds + 1 on success) */
+  int64_t anchors_swept;   /* sum over sweeps of anchors evaluated (frontier accounting) */
+  int64_t launches;        /* kernels this call launched */
+  double sweep_ms;         /* opts.profile: summed device time of the round sweeps */
+} dmtz_stats;
+
+typedef struct dmtz_ctx dmtz_ctx;
+
+/* Create a context for a global grid.  world == 1 only in this release (the
+ * multi-GPU slab layer drives single-rank contexts over owned slabs);
+ * nccl_unique_id must be NULL.  cuda_device: the device the caller's buffers live on. */
+dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* global, int rank, int world,
+                            const void* nccl_unique_id, int cuda_device);
+void dmtz_ctx_destroy(dmtz_ctx* ctx);
+
+/* Bytes of device workspace dmtz_correct / dmtz_compute_gradient / trace need. */
+size_t dmtz_workspace_bytes(const dmtz_ctx* ctx, const dmtz_correct_opts* opts);
+
+/* Discrete gradient of `field`: one code per anchor (layout
+ * above) into `codes` (uint64[N] in 3D, uint16[N] in 2D).  `field` must be finite
+ * (not checked here; dmtz_correct validates).  workspace may be NULL. */
+dmtz_status dmtz_compute_gradient(dmtz_ctx* ctx, const float* field, void* codes,
+                                  void* workspace, dmtz_stream_t stream);
+
+/* Critical-cell masks (uint32[N], bit t = type t critical) from gradient codes. */
+dmtz_status dmtz_critical_mask(dmtz_ctx* ctx, const void* codes, uint32_t* crit,
+                               dmtz_stream_t stream);
+
+/* The C-loop with quantized edits (Eq. 2):
+ *   validate (finite, |fhat - f| <= xi); lb = RU32(f - xi); g = fhat; q = 0
+ *   repeat: F = cells critical in exactly one of gradient(f), gradient(g)
+ *           (tier 1: dims 0 and top only); F empty -> OK
+ *           T = { target(a) : a in F } (one step per vertex per round, rules
+ *           R1/R2/R3a/R3b of DESIGN.md §3); each non-lossless v in T takes one
+ *           step g' = RN(fhat - RN((q+1) xi 2^-q_max)) if q+1 <= q_cap and
+ *           g' >= lb, else g = lb (lossless); no v changed -> STUCK
+ * Outputs: g_out (float[N], device), the sorted edit list (device, capacity
+ * edits_capacity entries), *n_edits (host) and *stats (host).  On
+ * DMTZ_E_CAPACITY g_out and *n_edits are valid and the list holds the first
+ * edits_capacity entries. */
+dmtz_status dmtz_correct(dmtz_ctx* ctx, const float* f, const float* fhat,
+                         const dmtz_correct_opts* opts, void* workspace, size_t workspace_bytes,
+                         float* g_out, dmtz_edit* edits, int64_t edits_capacity,
+                         int64_t* n_edits /* host */, dmtz_stats* stats /* host */,
+                         dmtz_stream_t stream);
+
+/* Separatrix traces of a gradient (P:82 gradient paths):
+ *   DESC: from each endpoint (ascending index) of each critical edge, vertex ->
+ *         paired edge -> its other vertex, until a critical vertex (minimum).
+ *         cells = v0, e1, v1, ..., v_min; terminal = the minimum.
+ *   ASC:  from each critical (top-1)-cell, through each top cofacet in slot
+ *         order: critical top cell -> maximum (terminal); else the top cell is
+ *         paired down with a facet c, continue through c's other top cofacet;
+ *         none -> terminal = DMTZ_BOUNDARY.  cells = t0, c1, t1, ...
+ *   CONN (3D): breadth-first from each critical triangle over facet edges (in
+ *         omitted-vertex order): critical edge -> recorded (each time met);
+ *         edge paired up with an unvisited triangle -> recorded and enqueued.
+ *         cells = the event log (triangles visited, edges reached); terminal =
+ *         DMTZ_BOUNDARY.
+ * Branches are grouped DESC, ASC, CONN; within a kind ordered by origin cell id,
+ * then branch order.  Outputs go to caller buffers with capacities cap_branches
+ * (branch_offsets holds cap_branches + 1) and cap_cells; *n_branches / *n_cells
+ * (host) receive the needed sizes; DMTZ_E_CAPACITY if they exceed the caps. */
+#define DMTZ_KIND_DESC 1u
+#define DMTZ_KIND_ASC 2u
+#define DMTZ_KIND_CONN 4u
+#define DMTZ_BOUNDARY UINT64_MAX
+typedef struct {
+  int64_t* branch_offsets; /* [cap_branches + 1] */
+  uint64_t* cells;         /* [cap_cells] */
+  uint64_t* origin;        /* [cap_branches] */
+  uint64_t* terminal;      /* [cap_branches] */
+  uint8_t* kind;           /* [cap_branches] */
+} dmtz_seps;
+dmtz_status dmtz_trace_separatrices(dmtz_ctx* ctx, const void* codes, uint32_t kinds,
+                                    void* workspace, size_t workspace_bytes, dmtz_seps* out,
+                                    int64_t cap_branches, int64_t cap_cells,
+                                    int64_t* n_branches /* host */, int64_t* n_cells /* host */,
+                                    dmtz_stream_t stream);
+
+const char* dmtz_status_string(dmtz_status s);
+const char* dmtz_last_error(void);
+int dmtz_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DMTZ_H */

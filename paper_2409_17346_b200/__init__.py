@@ -1,0 +1,282 @@
+"""B200-native DMTz hot path: thin Python binding over libdmtz.so (include/dmtz.h).
+
+Argument marshalling only: every step of the C-loop and the traces runs in the
+CUDA kernels of ``csrc/``.  PyTorch provides device memory and streams.  There is
+no CPU fallback: importing this package on a machine without the built library
+raises, and every call needs CUDA tensors.
+
+Fields are torch float32 tensors shaped (nz, ny, nx) (3D) or (ny, nx) (2D), x
+contiguous.  P:<n> cites line n of the paper text (see include/dmtz.h).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdmtz.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2409_17346_b200.build` "
+                      "(or __graft_entry__.build()); there is no CPU fallback")
+
+OK, E_ARG, E_DIMS, E_NONFINITE, E_BOUND, E_CAPACITY, E_ITER_CAP, E_STUCK, E_CUDA, E_NCCL, E_OOM, \
+    E_INTERNAL = range(12)
+KIND_DESC, KIND_ASC, KIND_CONN = 1, 2, 4
+BOUNDARY = 0xFFFFFFFFFFFFFFFF
+EDIT_DTYPE = np.dtype([("v", "<u8"), ("q", "<u2"), ("lossless", "u1"), ("pad", "u1"), ("value", "<f4")])
+
+
+class DmtzError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"dmtz status {status}: {msg}")
+        self.status = status
+
+
+class _Dims(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int64), ("ny", ctypes.c_int64), ("nz", ctypes.c_int64)]
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("xi", ctypes.c_float), ("q_max", ctypes.c_int32), ("q_cap", ctypes.c_int32),
+                ("tier", ctypes.c_int32), ("max_rounds", ctypes.c_int64), ("full_sweeps", ctypes.c_int32),
+                ("profile", ctypes.c_int32)]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("rounds", ctypes.c_int64), ("n_edited", ctypes.c_int64), ("n_quantized", ctypes.c_int64),
+                ("n_lossless", ctypes.c_int64), ("n_false_round0", ctypes.c_int64),
+                ("false_by_kind_round0", ctypes.c_int64 * 8), ("status", ctypes.c_int32),
+                ("pad", ctypes.c_int32), ("sweeps", ctypes.c_int64), ("anchors_swept", ctypes.c_int64),
+                ("launches", ctypes.c_int64), ("sweep_ms", ctypes.c_double)]
+
+
+class _Seps(ctypes.Structure):
+    _fields_ = [("branch_offsets", ctypes.c_void_p), ("cells", ctypes.c_void_p), ("origin", ctypes.c_void_p),
+                ("terminal", ctypes.c_void_p), ("kind", ctypes.c_void_p)]
+
+
+def _load():
+    L = ctypes.CDLL(LIB_PATH)
+    P, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+    L.dmtz_ctx_create.argtypes = [ctypes.POINTER(P), ctypes.POINTER(_Dims), i32, i32, P, i32]
+    L.dmtz_ctx_destroy.argtypes = [P]
+    L.dmtz_ctx_destroy.restype = None
+    L.dmtz_workspace_bytes.argtypes = [P, ctypes.POINTER(_Opts)]
+    L.dmtz_workspace_bytes.restype = ctypes.c_size_t
+    L.dmtz_compute_gradient.argtypes = [P, P, P, P, P]
+    L.dmtz_critical_mask.argtypes = [P, P, P, P]
+    L.dmtz_correct.argtypes = [P, P, P, ctypes.POINTER(_Opts), P, ctypes.c_size_t, P, P, i64,
+                               ctypes.POINTER(i64), ctypes.POINTER(_Stats), P]
+    L.dmtz_trace_separatrices.argtypes = [P, P, ctypes.c_uint32, P, ctypes.c_size_t, ctypes.POINTER(_Seps),
+                                          i64, i64, ctypes.POINTER(i64), ctypes.POINTER(i64), P]
+    L.dmtz_status_string.argtypes = [i32]
+    L.dmtz_status_string.restype = ctypes.c_char_p
+    L.dmtz_last_error.restype = ctypes.c_char_p
+    for fn in ("dmtz_ctx_create", "dmtz_compute_gradient", "dmtz_critical_mask", "dmtz_correct",
+               "dmtz_trace_separatrices", "dmtz_version"):
+        getattr(L, fn).restype = ctypes.c_int
+    return L
+
+
+_lib = _load()
+EXPORTED = ("dmtz_ctx_create", "dmtz_ctx_destroy", "dmtz_workspace_bytes", "dmtz_compute_gradient",
+            "dmtz_critical_mask", "dmtz_correct", "dmtz_trace_separatrices", "dmtz_status_string",
+            "dmtz_last_error", "dmtz_version")
+
+
+def lib():
+    return _lib
+
+
+def _check(st):
+    if st != OK:
+        raise DmtzError(st, _lib.dmtz_last_error().decode())
+
+
+def _dims_of(shape):
+    if len(shape) == 2:
+        return int(shape[1]), int(shape[0]), 1
+    if len(shape) == 3:
+        return int(shape[2]), int(shape[1]), int(shape[0])
+    raise ValueError(f"field must be 2D or 3D, got shape {tuple(shape)}")
+
+
+def _stream_ptr(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if not (isinstance(t, torch.Tensor) and t.is_cuda):
+            raise TypeError("dmtz needs CUDA tensors (no CPU fallback)")
+
+
+class Context:
+    """A dmtz_ctx for one grid plus its device workspace (a torch uint8 tensor)."""
+
+    def __init__(self, shape, device=None):
+        self.shape = tuple(int(s) for s in shape)
+        self.nx, self.ny, self.nz = _dims_of(self.shape)
+        self.D = 2 if self.nz == 1 else 3
+        self.N = self.nx * self.ny * self.nz
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        h = ctypes.c_void_p()
+        d = _Dims(self.nx, self.ny, self.nz)
+        _check(_lib.dmtz_ctx_create(ctypes.byref(h), ctypes.byref(d), 0, 1, None, self.device.index or 0))
+        self._h = h
+        self.ws_bytes = int(_lib.dmtz_workspace_bytes(h, None))
+        self.workspace = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.dmtz_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def code_dtype(self):
+        return torch.int64 if self.D == 3 else torch.int16
+
+    # ---------------------------------------------------------------- gradient
+    def compute_gradient(self, field: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+        """Discrete gradient codes, layout of include/dmtz.h."""
+        _need_cuda(field)
+        assert field.dtype == torch.float32 and tuple(field.shape) == self.shape and field.is_contiguous()
+        if out is None:
+            out = torch.empty(self.shape, dtype=self.code_dtype, device=field.device)
+        _check(_lib.dmtz_compute_gradient(self._h, ctypes.c_void_p(field.data_ptr()),
+                                          ctypes.c_void_p(out.data_ptr()), None, _stream_ptr(stream)))
+        return out
+
+    def critical_mask(self, codes: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+        _need_cuda(codes)
+        if out is None:
+            out = torch.empty(self.shape, dtype=torch.int32, device=codes.device)
+        _check(_lib.dmtz_critical_mask(self._h, ctypes.c_void_p(codes.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                       _stream_ptr(stream)))
+        return out
+
+    # ---------------------------------------------------------------- C-loop
+    def correct(self, f: torch.Tensor, fhat: torch.Tensor, xi: float, q_max: int = 6, q_cap: int | None = None,
+                tier: int = 2, max_rounds: int = 0, full_sweeps: bool = False, g_out: torch.Tensor | None = None,
+                edits: torch.Tensor | None = None, edits_capacity: int | None = None, stream=None,
+                raise_on_error: bool = True, profile: bool = False):
+        """The C-loop with Eq. 2 edits.  Returns a Result."""
+        _need_cuda(f, fhat)
+        for t in (f, fhat):
+            assert t.dtype == torch.float32 and tuple(t.shape) == self.shape and t.is_contiguous()
+        if g_out is None:
+            g_out = torch.empty_like(f)
+        if edits is None:
+            cap = self.N if edits_capacity is None else int(edits_capacity)
+            edits = torch.empty((max(cap, 1), 16), dtype=torch.uint8, device=f.device)
+        else:
+            cap = edits.shape[0] if edits_capacity is None else int(edits_capacity)
+        opts = _Opts(float(xi), int(q_max), int(q_max if q_cap is None else q_cap), int(tier), int(max_rounds),
+                     1 if full_sweeps else 0, 1 if profile else 0)
+        ne = ctypes.c_int64()
+        st = _Stats()
+        status = _lib.dmtz_correct(self._h, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(fhat.data_ptr()),
+                                   ctypes.byref(opts), ctypes.c_void_p(self.workspace.data_ptr()),
+                                   self.ws_bytes, ctypes.c_void_p(g_out.data_ptr()),
+                                   ctypes.c_void_p(edits.data_ptr()), cap, ctypes.byref(ne), ctypes.byref(st),
+                                   _stream_ptr(stream))
+        stats = dict(rounds=st.rounds, n_edited=st.n_edited, n_quantized=st.n_quantized, n_lossless=st.n_lossless,
+                     n_false_round0=st.n_false_round0, false_by_kind_round0=list(st.false_by_kind_round0),
+                     status=status, sweeps=st.sweeps, anchors_swept=st.anchors_swept, launches=st.launches,
+                     sweep_ms=st.sweep_ms)
+        msg = _lib.dmtz_last_error().decode() if status != OK else ""
+        if raise_on_error and status not in (OK, E_STUCK, E_ITER_CAP, E_CAPACITY):
+            raise DmtzError(status, msg)
+        return Result(status=status, g=g_out, edits=edits[:min(ne.value, cap)], n_edits=ne.value, stats=stats,
+                      message=msg)
+
+    # ---------------------------------------------------------------- traces
+    def trace_separatrices(self, codes: torch.Tensor, kinds: int = KIND_DESC | KIND_ASC | KIND_CONN,
+                           cap_branches: int | None = None, cap_cells: int | None = None, stream=None):
+        """V-path traces -> dict of CUDA tensors (CSR)."""
+        _need_cuda(codes)
+        dev = codes.device
+
+        def run(cb, cc):
+            bufs = dict(offsets=torch.empty(cb + 1, dtype=torch.int64, device=dev),
+                        cells=torch.empty(max(cc, 1), dtype=torch.int64, device=dev),
+                        origin=torch.empty(max(cb, 1), dtype=torch.int64, device=dev),
+                        terminal=torch.empty(max(cb, 1), dtype=torch.int64, device=dev),
+                        kind=torch.empty(max(cb, 1), dtype=torch.uint8, device=dev))
+            seps = _Seps(*(ctypes.c_void_p(bufs[k].data_ptr()) for k in ("offsets", "cells", "origin", "terminal", "kind")))
+            nb, nc = ctypes.c_int64(), ctypes.c_int64()
+            st = _lib.dmtz_trace_separatrices(self._h, ctypes.c_void_p(codes.data_ptr()), kinds,
+                                              ctypes.c_void_p(self.workspace.data_ptr()), self.ws_bytes,
+                                              ctypes.byref(seps), cb, cc, ctypes.byref(nb), ctypes.byref(nc),
+                                              _stream_ptr(stream))
+            return st, nb.value, nc.value, bufs
+
+        cb = cap_branches if cap_branches is not None else 1 << 16
+        cc = cap_cells if cap_cells is not None else 1 << 20
+        st, nb, nc, bufs = run(cb, cc)
+        if st == E_CAPACITY and cap_branches is None and cap_cells is None:
+            st, nb, nc, bufs = run(max(nb, 1), max(nc, 1))
+        _check(st)
+        return dict(offsets=bufs["offsets"][:nb + 1], cells=bufs["cells"][:nc], origin=bufs["origin"][:nb],
+                    terminal=bufs["terminal"][:nb], kind=bufs["kind"][:nb])
+
+
+@dataclass
+class Result:
+    status: int
+    g: torch.Tensor
+    edits: torch.Tensor          # (n, 16) uint8 rows in dmtz_edit layout, sorted by v
+    n_edits: int
+    stats: dict = dc_field(default_factory=dict)
+    message: str = ""
+
+    def edits_numpy(self) -> np.ndarray:
+        return self.edits.cpu().numpy().view(EDIT_DTYPE).reshape(-1)
+
+
+_ctx_cache: dict = {}
+
+
+def context(shape, device=None) -> Context:
+    key = (tuple(shape), str(device))
+    c = _ctx_cache.get(key)
+    if c is None:
+        c = _ctx_cache[key] = Context(shape, device)
+    return c
+
+
+def compute_gradient(field: torch.Tensor, stream=None):
+    return context(field.shape, field.device).compute_gradient(field, stream=stream)
+
+
+def critical_mask(codes: torch.Tensor, stream=None):
+    return context(codes.shape, codes.device).critical_mask(codes, stream=stream)
+
+
+def correct(f: torch.Tensor, fhat: torch.Tensor, xi: float, **kw) -> Result:
+    return context(f.shape, f.device).correct(f, fhat, xi, **kw)
+
+
+def trace_separatrices(codes: torch.Tensor, kinds: int = KIND_DESC | KIND_ASC | KIND_CONN, **kw):
+    return context(codes.shape, codes.device).trace_separatrices(codes, kinds, **kw)
+
+
+def correct_host(f: np.ndarray, fhat: np.ndarray, xi: float, device="cuda", **kw):
+    """End-to-end call from HOST arrays: H2D of f and fhat, the C-loop, D2H of g and
+    the edit list.  Returns (g numpy, edits numpy, stats)."""
+    ft = torch.from_numpy(np.ascontiguousarray(f, np.float32)).pin_memory().to(device, non_blocking=True)
+    fht = torch.from_numpy(np.ascontiguousarray(fhat, np.float32)).pin_memory().to(device, non_blocking=True)
+    r = correct(ft, fht, xi, **kw)
+    return r.g.cpu().numpy(), r.edits_numpy(), r.stats

@@ -1,0 +1,342 @@
+// dmtz_api.cu -- the C ABI of include/dmtz.h on top of dmtz_kernels.cuh.
+//
+// Host side of the hot path: workspace carving, the fixed-point driver of the
+// C-loop (repeat gradient -> classify -> fix until no false
+// critical cell), status/error plumbing.  No device allocation happens here:
+// every buffer is the caller's.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "../../include/dmtz.h"
+#include "dmtz_kernels.cuh"
+#include "dmtz_trace.cuh"
+
+using namespace dmtz;
+
+struct dmtz_ctx {
+  dmtz_dims dims;
+  Grid g;
+  int D;
+  int device;
+  int rank, world;
+  Counters* host_cnt;  // pinned
+  cudaEvent_t ev[2];   // sweep timing (opts.profile)
+};
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+void set_err(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+}
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      set_err("%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_));       \
+      return DMTZ_E_CUDA;                                                               \
+    }                                                                                   \
+  } while (0)
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// Workspace layout (offsets from the base, each 256-B aligned)
+struct Layout {
+  size_t cand_f, cand_g, lb, state, tbits, counters, edit_bc, trace, total;
+};
+
+Layout layout_for(const dmtz_ctx* c) {
+  const size_t N = (size_t)c->g.N;
+  const size_t cs = c->D == 3 ? 8 : 2;
+  Layout L;
+  size_t o = 0;
+  L.cand_f = o; o += align_up(N * cs);
+  L.cand_g = o; o += align_up(N * cs);
+  L.lb = o; o += align_up(N * 4);
+  L.state = o; o += align_up(N * 4);
+  L.tbits = o; o += align_up((N + 31) / 32 * 4 + 64);
+  L.counters = o; o += align_up(sizeof(Counters) * 2);
+  L.edit_bc = o; o += align_up(((N + EDIT_CHUNK - 1) / EDIT_CHUNK + 2) * 8);
+  L.trace = o; o += align_up(trace_scratch_bytes(c->g, c->D));
+  L.total = o;
+  return L;
+}
+
+dim3 anchor_grid(const Grid& g, int64_t z0, int64_t z1, int threads) {
+  int64_t bx = (g.nx + threads - 1) / threads;
+  int64_t by = g.ny < 65535 ? g.ny : 65535;
+  int64_t nzr = z1 - z0;
+  int64_t bz = nzr < 65535 ? nzr : 65535;
+  if (bz < 1) bz = 1;
+  return dim3((unsigned)(bx < 2147483647 ? bx : 2147483647), (unsigned)by, (unsigned)bz);
+}
+
+template <int D>
+void launch_codes(const Grid& g, const float* fld, void* codes, int64_t z0, int64_t z1, cudaStream_t s) {
+  if (z1 <= z0) return;
+  k_codes<D><<<anchor_grid(g, z0, z1, 128), 128, 0, s>>>(fld, (typename Tr<D>::code_t*)codes, g, z0, z1);
+}
+
+template <int D>
+uint32_t tier_mask(int tier) {
+  if (tier == 2) return 0xFFFFFFFFu;
+  // dims 0 and top only
+  return D == 3 ? (1u | (0x3Fu << 20)) : (1u | (0x3u << 4));
+}
+
+template <int D>
+dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
+                         char* ws, const Layout& L, float* g_out, dmtz_edit* edits, int64_t cap,
+                         int64_t* n_edits, dmtz_stats* st, cudaStream_t s) {
+  const Grid& g = c->g;
+  using code_t = typename Tr<D>::code_t;
+  code_t* cand_f = (code_t*)(ws + L.cand_f);
+  code_t* cand_g = (code_t*)(ws + L.cand_g);
+  float* lb = (float*)(ws + L.lb);
+  uint32_t* state = (uint32_t*)(ws + L.state);
+  uint32_t* tbits = (uint32_t*)(ws + L.tbits);
+  Counters* dc = (Counters*)(ws + L.counters);
+  unsigned long long* bc = (unsigned long long*)(ws + L.edit_bc);
+  Counters* hc = c->host_cnt;
+  const int64_t nwords = (g.N + 31) / 32;
+  const int ethreads = 256;
+  const int eblocks = (int)((g.N + ethreads - 1) / ethreads < 148 * 32 ? (g.N + ethreads - 1) / ethreads : 148 * 32);
+  const int wblocks = (int)((nwords + ethreads - 1) / ethreads < 148 * 32 ? (nwords + ethreads - 1) / ethreads : 148 * 32);
+
+  // a1: setup
+  CK(cudaMemsetAsync(dc, 0, sizeof(Counters), s));
+  CK(cudaMemsetAsync(&dc->first_nonfinite, 0xFF, 16, s));
+  CK(cudaMemsetAsync(tbits, 0, nwords * 4, s));
+  k_setup<<<eblocks, ethreads, 0, s>>>(f, fhat, o->xi, g.N, lb, g_out, state, dc);
+  st->launches++;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (hc->first_nonfinite != ~0ull) {
+    set_err("non-finite value at vertex %llu", hc->first_nonfinite);
+    st->status = DMTZ_E_NONFINITE;
+    return DMTZ_E_NONFINITE;
+  }
+  if (hc->first_bound != ~0ull) {
+    set_err("|fhat - f| > xi at vertex %llu", hc->first_bound);
+    st->status = DMTZ_E_BOUND;
+    return DMTZ_E_BOUND;
+  }
+  // a2: reference gradient of f (once)
+  launch_codes<D>(g, f, cand_f, 0, g.nz, s);
+  st->launches++;
+  CK(cudaGetLastError());
+
+  const float step = ldexpf(o->xi, -o->q_max);   // xi / 2^q_max, exact
+  const int64_t max_rounds = o->max_rounds > 0 ? o->max_rounds : g.N * (int64_t)(o->q_cap + 1);
+  const uint32_t tmask = tier_mask<D>(o->tier);
+  dmtz_status status = DMTZ_OK;
+  for (int64_t round = 1;; round++) {
+    // a3: gradient of g;  a4/a5: classify + mark targets;  a6: edit
+    CK(cudaMemsetAsync(dc, 0, offsetof(Counters, first_nonfinite), s));
+    if (o->profile) CK(cudaEventRecord(c->ev[0], s));
+    launch_codes<D>(g, g_out, cand_g, 0, g.nz, s);
+    k_diff<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(f, cand_f, cand_g, tbits, dc, g, 0, g.nz, tmask);
+    if (o->profile) CK(cudaEventRecord(c->ev[1], s));
+    k_edit<<<wblocks, ethreads, 0, s>>>(tbits, nwords, fhat, lb, g_out, state, dc, step, o->q_cap);
+    st->launches += 3;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(hc, dc, offsetof(Counters, first_nonfinite), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (o->profile) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+      st->sweep_ms += ms;
+    }
+    st->sweeps++;
+    st->anchors_swept += g.N;
+    if (hc->n_internal) {
+      set_err("gradient invariant violated at %llu false cells (round %lld)", hc->n_internal, (long long)round);
+      status = DMTZ_E_INTERNAL;
+      break;
+    }
+    if (round == 1) {
+      st->n_false_round0 = (int64_t)hc->n_false;
+      for (int k = 0; k < 8; k++) st->false_by_kind_round0[k] = (int64_t)hc->kinds[k];
+    }
+    if (hc->n_false == 0) break;
+    st->rounds = round;
+    if (hc->n_changed == 0) { status = DMTZ_E_STUCK; set_err("no target could move (round %lld)", (long long)round); break; }
+    if (round == max_rounds) { status = DMTZ_E_ITER_CAP; set_err("round cap %lld reached", (long long)round); break; }
+  }
+  // a8: edit list
+  const int64_t nb = (g.N + EDIT_CHUNK - 1) / EDIT_CHUNK;
+  CK(cudaMemsetAsync(&dc->n_lossless, 0, 8, s));
+  k_edit_count<<<(unsigned)nb, EDIT_THREADS, 0, s>>>(state, g.N, bc, dc);
+  k_scan_counts<<<1, EDIT_THREADS, 0, s>>>(bc, nb, dc);
+  k_edit_write<<<(unsigned)nb, EDIT_THREADS, 0, s>>>(state, g_out, g.N, bc, (EditOut*)edits, cap);
+  st->launches += 3;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  *n_edits = (int64_t)hc->n_edits;
+  st->n_edited = *n_edits;
+  st->n_lossless = (int64_t)hc->n_lossless;
+  st->n_quantized = st->n_edited - st->n_lossless;
+  if (status == DMTZ_OK && *n_edits > cap) { status = DMTZ_E_CAPACITY; set_err("edit list needs %lld entries", (long long)*n_edits); }
+  st->status = status;
+  return status;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dmtz_version(void) { return 1; }
+
+const char* dmtz_last_error(void) { return g_err; }
+
+const char* dmtz_status_string(dmtz_status s) {
+  switch (s) {
+    case DMTZ_OK: return "ok";
+    case DMTZ_E_ARG: return "invalid argument";
+    case DMTZ_E_DIMS: return "invalid grid dimensions";
+    case DMTZ_E_NONFINITE: return "non-finite input value";
+    case DMTZ_E_BOUND: return "decompressed field violates the error bound";
+    case DMTZ_E_CAPACITY: return "output capacity exceeded";
+    case DMTZ_E_ITER_CAP: return "round cap reached";
+    case DMTZ_E_STUCK: return "stuck: every target is at its lower bound";
+    case DMTZ_E_CUDA: return "CUDA error";
+    case DMTZ_E_NCCL: return "NCCL error";
+    case DMTZ_E_OOM: return "workspace too small";
+    case DMTZ_E_INTERNAL: return "internal invariant violated";
+  }
+  return "unknown status";
+}
+
+dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int world, const void* nccl_id,
+                            int cuda_device) {
+  if (!out || !d) { set_err("NULL argument"); return DMTZ_E_ARG; }
+  *out = nullptr;
+  if (d->nx < 2 || d->ny < 2 || d->nz < 1) { set_err("dims %lld x %lld x %lld", (long long)d->nx, (long long)d->ny, (long long)d->nz); return DMTZ_E_DIMS; }
+  if (world != 1 || rank != 0 || nccl_id != nullptr) { set_err("world must be 1 (slab layer drives per-rank contexts)"); return DMTZ_E_ARG; }
+  CK(cudaSetDevice(cuda_device));
+  dmtz_ctx* c = new (std::nothrow) dmtz_ctx();
+  if (!c) return DMTZ_E_OOM;
+  c->dims = *d;
+  c->g.nx = d->nx; c->g.ny = d->ny; c->g.nz = d->nz;
+  c->g.N = d->nx * d->ny * d->nz;
+  c->g.sy = d->nx; c->g.sz = d->nx * d->ny;
+  c->D = d->nz == 1 ? 2 : 3;
+  c->device = cuda_device;
+  c->rank = rank; c->world = world;
+  cudaError_t e = cudaMallocHost((void**)&c->host_cnt, sizeof(Counters) * 2);
+  if (e != cudaSuccess) { delete c; set_err("cudaMallocHost: %s", cudaGetErrorString(e)); return DMTZ_E_CUDA; }
+  for (int i = 0; i < 2; i++) {
+    e = cudaEventCreate(&c->ev[i]);
+    if (e != cudaSuccess) { set_err("cudaEventCreate: %s", cudaGetErrorString(e)); return DMTZ_E_CUDA; }
+  }
+  *out = c;
+  return DMTZ_OK;
+}
+
+void dmtz_ctx_destroy(dmtz_ctx* c) {
+  if (!c) return;
+  cudaFreeHost(c->host_cnt);
+  cudaEventDestroy(c->ev[0]);
+  cudaEventDestroy(c->ev[1]);
+  delete c;
+}
+
+size_t dmtz_workspace_bytes(const dmtz_ctx* c, const dmtz_correct_opts*) {
+  if (!c) return 0;
+  return layout_for(c).total;
+}
+
+dmtz_status dmtz_compute_gradient(dmtz_ctx* c, const float* field, void* codes, void*, dmtz_stream_t stream) {
+  if (!c || !field || !codes) { set_err("NULL argument"); return DMTZ_E_ARG; }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (c->D == 3) launch_codes<3>(c->g, field, codes, 0, c->g.nz, s);
+  else launch_codes<2>(c->g, field, codes, 0, c->g.nz, s);
+  CK(cudaGetLastError());
+  return DMTZ_OK;
+}
+
+dmtz_status dmtz_critical_mask(dmtz_ctx* c, const void* codes, uint32_t* crit, dmtz_stream_t stream) {
+  if (!c || !codes || !crit) { set_err("NULL argument"); return DMTZ_E_ARG; }
+  cudaStream_t s = (cudaStream_t)stream;
+  dim3 grid = anchor_grid(c->g, 0, c->g.nz, 128);
+  if (c->D == 3) k_critmask<3><<<grid, 128, 0, s>>>((const Tr<3>::code_t*)codes, crit, c->g);
+  else k_critmask<2><<<grid, 128, 0, s>>>((const Tr<2>::code_t*)codes, crit, c->g);
+  CK(cudaGetLastError());
+  return DMTZ_OK;
+}
+
+dmtz_status dmtz_correct(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
+                         void* workspace, size_t workspace_bytes, float* g_out, dmtz_edit* edits,
+                         int64_t edits_capacity, int64_t* n_edits, dmtz_stats* st, dmtz_stream_t stream) {
+  if (!c || !f || !fhat || !o || !workspace || !g_out || !n_edits || !st || (edits_capacity > 0 && !edits) ||
+      edits_capacity < 0) {
+    set_err("NULL argument");
+    return DMTZ_E_ARG;
+  }
+  memset(st, 0, sizeof *st);
+  *n_edits = 0;
+  if (!(o->xi > 0.0f) || !isfinite(o->xi) || o->q_max < 0 || o->q_max > 30 || o->q_cap < 1 ||
+      o->q_cap > 65535 || (o->tier != 1 && o->tier != 2) || o->max_rounds < 0) {
+    set_err("invalid options (xi=%g q_max=%d q_cap=%d tier=%d)", (double)o->xi, o->q_max, o->q_cap, o->tier);
+    st->status = DMTZ_E_ARG;
+    return DMTZ_E_ARG;
+  }
+  Layout L = layout_for(c);
+  if (workspace_bytes < L.total) {
+    set_err("workspace %zu < %zu bytes", workspace_bytes, L.total);
+    st->status = DMTZ_E_OOM;
+    return DMTZ_E_OOM;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  dmtz_status r;
+  if (c->D == 3) r = correct_impl<3>(c, f, fhat, o, (char*)workspace, L, g_out, edits, edits_capacity, n_edits, st, s);
+  else r = correct_impl<2>(c, f, fhat, o, (char*)workspace, L, g_out, edits, edits_capacity, n_edits, st, s);
+  if (r == DMTZ_E_CUDA) st->status = r;
+  return r;
+}
+
+dmtz_status dmtz_trace_separatrices(dmtz_ctx* c, const void* codes, uint32_t kinds, void* workspace,
+                                    size_t workspace_bytes, dmtz_seps* out, int64_t cap_b, int64_t cap_c,
+                                    int64_t* n_b, int64_t* n_c, dmtz_stream_t stream) {
+  if (!c || !codes || !workspace || !out || !n_b || !n_c || cap_b < 0 || cap_c < 0) {
+    set_err("NULL argument");
+    return DMTZ_E_ARG;
+  }
+  Layout L = layout_for(c);
+  if (workspace_bytes < L.total) { set_err("workspace %zu < %zu bytes", workspace_bytes, L.total); return DMTZ_E_OOM; }
+  char* ws = (char*)workspace;
+  TraceArgs a;
+  a.g = c->g;
+  a.codes = codes;
+  a.kinds = kinds;
+  a.scratch = ws + L.trace;
+  a.cnt = (Counters*)(ws + L.counters);
+  a.host_cnt = c->host_cnt;
+  a.out_offsets = out->branch_offsets;
+  a.out_cells = out->cells;
+  a.out_origin = out->origin;
+  a.out_terminal = out->terminal;
+  a.out_kind = out->kind;
+  a.cap_b = cap_b;
+  a.cap_c = cap_c;
+  cudaError_t e = c->D == 3 ? run_trace<3>(a, (cudaStream_t)stream) : run_trace<2>(a, (cudaStream_t)stream);
+  if (e != cudaSuccess) { set_err("trace: %s", cudaGetErrorString(e)); return DMTZ_E_CUDA; }
+  *n_b = a.n_branches;
+  *n_c = a.n_cells;
+  if (a.n_internal) { set_err("trace: cycle or inconsistent gradient"); return DMTZ_E_INTERNAL; }
+  if (a.n_branches > cap_b || a.n_cells > cap_c) { set_err("trace needs %lld branches / %lld cells", (long long)a.n_branches, (long long)a.n_cells); return DMTZ_E_CAPACITY; }
+  return DMTZ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,416 @@
+// dmtz_kernels.cuh -- sm_100a kernels of the DMTz hot path (C-loop + trace).
+//
+// Citations: P:<n> = PAPER.md line n.  The kernels implement, per anchor
+// vertex, the local form of the gradient (DESIGN.md §3 "local form"):
+//   cand(c) = argmin_SoS(c U link(c)) if that minimum is a link vertex, else NONE
+// which equals the Shivashankar-Natarajan pairing of P:84-92 / P:152-155 (proved in
+// DESIGN.md §3 and checked element-by-element against the literal CPU oracle).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dmtz_tables.h"
+
+namespace dmtz {
+
+struct Grid {
+  int64_t nx, ny, nz, N, sy, sz;  // sy = nx, sz = nx*ny
+};
+
+struct Counters {                 // device-side round counters (one 256 B block)
+  unsigned long long n_false;
+  unsigned long long kinds[8];
+  unsigned long long n_changed;   // targets that took a step or were clamped
+  unsigned long long n_targets;   // distinct targets marked
+  unsigned long long n_internal;  // invariant violations (expected 0)
+  unsigned long long first_nonfinite;
+  unsigned long long first_bound;
+  unsigned long long n_edits;
+  unsigned long long n_lossless;  // lossless entries of the edit list
+  unsigned long long pad[16];
+};
+static_assert(sizeof(Counters) == 256, "counters are one 256 B block");
+
+template <int D> struct Tr;
+template <> struct Tr<3> {
+  using code_t = unsigned long long;
+  static constexpr int NT = k3d::NT, TOP = 3, NDELTA = 8;
+  static constexpr uint64_t ALL_NONE = k3d::ALL_NONE;
+};
+template <> struct Tr<2> {
+  using code_t = unsigned short;
+  static constexpr int NT = k2d::NT, TOP = 2, NDELTA = 4;
+  static constexpr uint64_t ALL_NONE = k2d::ALL_NONE;
+};
+
+// table accessors (constant-folded when t is a compile-time constant after unrolling)
+#define DMTZ_TAB(D, name) ((D) == 3 ? k3d::name : k2d::name)
+template <int D> __device__ __forceinline__ int t_dim(int t) { return D == 3 ? k3d::DIM[t] : k2d::DIM[t]; }
+template <int D> __device__ __forceinline__ int t_nv(int t) { return D == 3 ? k3d::NV[t] : k2d::NV[t]; }
+template <int D> __device__ __forceinline__ int t_shift(int t) { return D == 3 ? k3d::SHIFT[t] : k2d::SHIFT[t]; }
+template <int D> __device__ __forceinline__ int t_none(int t) { return D == 3 ? k3d::NONE[t] : k2d::NONE[t]; }
+template <int D> __device__ __forceinline__ int t_nfacet(int t) { return D == 3 ? k3d::NFACET[t] : k2d::NFACET[t]; }
+template <int D> __device__ __forceinline__ int t_facet(int t, int j, int c) {
+  return D == 3 ? k3d::FACET[t][j][c] : k2d::FACET[t][j][c];
+}
+template <int D> __device__ __forceinline__ int t_vmask(int t, int k) { return D == 3 ? k3d::VMASK[t][k] : k2d::VMASK[t][k]; }
+template <int D> __device__ __forceinline__ int t_link(int t, int s, int a) { return D == 3 ? k3d::LINK[t][s][a] : k2d::LINK[t][s][a]; }
+template <int D> __device__ __forceinline__ int t_nlink(int t) { return D == 3 ? k3d::NLINK[t] : k2d::NLINK[t]; }
+template <int D> __device__ __forceinline__ int t_cof_type(int t, int s) { return D == 3 ? k3d::COF_TYPE[t][s] : k2d::COF_TYPE[t][s]; }
+template <int D> __device__ __forceinline__ int t_cof_anchor(int t, int s, int a) {
+  return D == 3 ? k3d::COF_ANCHOR[t][s][a] : k2d::COF_ANCHOR[t][s][a];
+}
+template <int D> __device__ __forceinline__ uint32_t t_exist(int ok) { return D == 3 ? k3d::EXIST[ok] : k2d::EXIST[ok]; }
+template <int D> __device__ __forceinline__ uint64_t t_nonex_fill(int ok) {
+  return D == 3 ? k3d::NONEX_FILL[ok] : k2d::NONEX_FILL[ok];
+}
+template <int D> __device__ __forceinline__ int t_first_of_dim(int d) {
+  return D == 3 ? k3d::FIRST_OF_DIM[d] : k2d::FIRST_OF_DIM[d];
+}
+
+template <int D> __device__ __forceinline__ uint32_t field_of(uint64_t code, int t) {
+  return (uint32_t)(code >> t_shift<D>(t)) & (uint32_t)t_none<D>(t);
+}
+
+__device__ __forceinline__ int64_t mask_delta(const Grid& g, int m) {
+  return (int64_t)(m & 1) + ((m >> 1) & 1) * g.sy + ((m >> 2) & 1) * g.sz;
+}
+
+// 'axes with a +1 neighbour' bit mask of an anchor
+__device__ __forceinline__ int axes_ok(const Grid& g, int64_t x, int64_t y, int64_t z) {
+  return (x + 1 < g.nx ? 1 : 0) | (y + 1 < g.ny ? 2 : 0) | (z + 1 < g.nz ? 4 : 0);
+}
+
+// SoS order (reading A2): (value, index) lexicographic
+__device__ __forceinline__ bool sos_less(float a, int64_t ia, float b, int64_t ib) {
+  return a < b || (a == b && ia < ib);
+}
+
+// --------------------------------------------------------------------------
+// Gradient codes of a field (a2/a3): one thread per anchor, 3^D stencil.
+// --------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ uint64_t anchor_code(const float* __restrict__ fld, const Grid& g, int64_t v,
+                                                int64_t x, int64_t y, int64_t z) {
+  const float INF = __int_as_float(0x7f800000);
+  float s[27];
+#pragma unroll
+  for (int dz = -1; dz <= 1; dz++)
+#pragma unroll
+    for (int dy = -1; dy <= 1; dy++)
+#pragma unroll
+      for (int dx = -1; dx <= 1; dx++) {
+        const int p = (dx + 1) + 3 * (dy + 1) + 9 * (dz + 1);
+        if (D == 2 && dz != 0) { s[p] = INF; continue; }
+        bool in = (x + dx >= 0) && (x + dx < g.nx) && (y + dy >= 0) && (y + dy < g.ny) &&
+                  (z + dz >= 0) && (z + dz < g.nz);
+        s[p] = in ? __ldg(fld + v + dx + dy * g.sy + dz * g.sz) : INF;
+      }
+  uint64_t code = (D == 3) ? k3d::cand_code(s) : k2d::cand_code(s);
+  return code | t_nonex_fill<D>(axes_ok(g, x, y, z));
+}
+
+// iterate anchors of z-planes [z0, z1) with a 3D launch: x fastest, grid-stride in y/z
+#define DMTZ_FOR_ANCHORS(g, z0, z1)                                                        \
+  for (int64_t z = (z0) + blockIdx.z; z < (z1); z += gridDim.z)                            \
+    for (int64_t y = blockIdx.y; y < (g).ny; y += gridDim.y)                               \
+      for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < (g).nx;         \
+           x += (int64_t)gridDim.x * blockDim.x)
+
+template <int D>
+__global__ void k_codes(const float* __restrict__ fld, typename Tr<D>::code_t* __restrict__ codes,
+                        Grid g, int64_t z0, int64_t z1) {
+  DMTZ_FOR_ANCHORS(g, z0, z1) {
+    int64_t v = x + y * g.sy + z * g.sz;
+    codes[v] = (typename Tr<D>::code_t)anchor_code<D>(fld, g, v, x, y, z);
+  }
+}
+
+// --------------------------------------------------------------------------
+// Critical masks from the codes at u + {0,1}^D (a4).
+// crit(c) <=> c exists, cand(c) = NONE, and no facet points to c.
+// --------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ uint32_t decode_crit(const uint64_t (&c)[Tr<D>::NDELTA], int ok) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int t = 0; t < Tr<D>::NT; t++) {
+    bool crit = true;
+    if (t_dim<D>(t) < Tr<D>::TOP) crit = field_of<D>(c[0], t) == (uint32_t)t_none<D>(t);
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      if (j < t_nfacet<D>(t)) {
+        const int dm = t_facet<D>(t, j, 0), ft = t_facet<D>(t, j, 1), sl = t_facet<D>(t, j, 2);
+        crit = crit && (field_of<D>(c[dm], ft) != (uint32_t)sl);
+      }
+    }
+    m |= (crit ? 1u : 0u) << t;
+  }
+  return m & t_exist<D>(ok);
+}
+
+template <int D>
+__device__ __forceinline__ void load_codes8(const typename Tr<D>::code_t* __restrict__ codes, const Grid& g,
+                                            int64_t v, int ok, uint64_t (&c)[Tr<D>::NDELTA]) {
+#pragma unroll
+  for (int dm = 0; dm < Tr<D>::NDELTA; dm++)
+    c[dm] = ((dm & ~ok) == 0) ? (uint64_t)__ldg(codes + v + mask_delta(g, dm)) : Tr<D>::ALL_NONE;
+}
+
+template <int D>
+__global__ void k_critmask(const typename Tr<D>::code_t* __restrict__ codes, uint32_t* __restrict__ crit,
+                           Grid g) {
+  DMTZ_FOR_ANCHORS(g, 0, g.nz) {
+    int64_t v = x + y * g.sy + z * g.sz;
+    int ok = axes_ok(g, x, y, z);
+    uint64_t c[Tr<D>::NDELTA];
+    load_codes8<D>(codes, g, v, ok, c);
+    crit[v] = decode_crit<D>(c, ok);
+  }
+}
+
+// --------------------------------------------------------------------------
+// Target of a false cell (a5): rules R1 / R2 / R3a / R3b.
+// Rare path: tables are indexed dynamically, codes re-read through L1/L2.
+// Returns -1 on an internal inconsistency.
+// --------------------------------------------------------------------------
+template <int D>
+__device__ int64_t target_of(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__ cand_f,
+                             const typename Tr<D>::code_t* __restrict__ cand_g, const Grid& g, int64_t u,
+                             int t, bool fn) {
+  const int nv = t_nv<D>(t);
+  int64_t vid[4];
+  int64_t m = -1;
+  float fm = 0.f;
+  for (int k = 0; k < nv; k++) {
+    vid[k] = u + mask_delta(g, t_vmask<D>(t, k));
+    float fv = __ldg(f + vid[k]);
+    if (m < 0 || sos_less(fv, vid[k], fm, m)) { m = vid[k]; fm = fv; }
+  }
+  const int top = Tr<D>::TOP;
+  if (!fn) {                                    // FP: paired in f, critical in g (R1)
+    if (t_dim<D>(t) < top) {
+      uint32_t s = field_of<D>((uint64_t)__ldg(cand_f + u), t);
+      if (s != (uint32_t)t_none<D>(t))
+        return u + t_link<D>(t, s, 0) + t_link<D>(t, s, 1) * g.sy + t_link<D>(t, s, 2) * g.sz;
+    }
+    return m;                                   // paired down in f: the f-lowest vertex
+  }
+  if (t_dim<D>(t) < top) {                      // FN: critical in f, paired in g
+    uint32_t s = field_of<D>((uint64_t)__ldg(cand_g + u), t);
+    if (s != (uint32_t)t_none<D>(t)) return m;  // paired up in g (R2)
+  }
+  for (int j = 0; j < t_nfacet<D>(t); j++) {    // paired down in g with gamma
+    const int dm = t_facet<D>(t, j, 0), ft = t_facet<D>(t, j, 1), sl = t_facet<D>(t, j, 2);
+    const int k = t_facet<D>(t, j, 3);
+    const int64_t ga = u + mask_delta(g, dm);
+    if (field_of<D>((uint64_t)__ldg(cand_g + ga), ft) != (uint32_t)sl) continue;
+    const int64_t y = vid[k];
+    if (m != y) return m;                       // R3a
+    uint32_t s2 = field_of<D>((uint64_t)__ldg(cand_f + ga), ft);   // R3b
+    if (s2 == (uint32_t)t_none<D>(ft)) return -1;
+    return ga + t_link<D>(ft, s2, 0) + t_link<D>(ft, s2, 1) * g.sy + t_link<D>(ft, s2, 2) * g.sz;
+  }
+  return -1;
+}
+
+__device__ __forceinline__ void warp_add(unsigned long long* dst, unsigned long long v) {
+  // warp-aggregated atomic for a value that may be zero on most lanes
+  unsigned mask = __ballot_sync(0xffffffffu, v != 0);
+  if (!mask) return;
+  unsigned long long s = v;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == (unsigned)(__ffs(mask) - 1)) atomicAdd(dst, s);
+}
+
+// --------------------------------------------------------------------------
+// The sweep of one C-loop round (a4+a5): classify every cell of the anchors of
+// z-planes [z0, z1), mark the target set T (bitmap, atomicOr), count F by kind.
+// --------------------------------------------------------------------------
+template <int D>
+__global__ void k_diff(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__ cand_f,
+                       const typename Tr<D>::code_t* __restrict__ cand_g, uint32_t* __restrict__ tbits,
+                       Counters* __restrict__ cnt, Grid g, int64_t z0, int64_t z1, uint32_t tier_mask) {
+  unsigned long long nfalse = 0, nint = 0;
+  unsigned long long kinds[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int64_t z = z0 + blockIdx.z; z < z1; z += gridDim.z)
+    for (int64_t y = blockIdx.y; y < g.ny; y += gridDim.y)
+      for (int64_t xb = (int64_t)blockIdx.x * blockDim.x; xb < g.nx; xb += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t x = xb + threadIdx.x;
+        if (x < g.nx) {
+          const int64_t u = x + y * g.sy + z * g.sz;
+          const int ok = axes_ok(g, x, y, z);
+          uint64_t cf[Tr<D>::NDELTA], cg[Tr<D>::NDELTA];
+          load_codes8<D>(cand_f, g, u, ok, cf);
+          load_codes8<D>(cand_g, g, u, ok, cg);
+          const uint32_t critf = decode_crit<D>(cf, ok);
+          const uint32_t critg = decode_crit<D>(cg, ok);
+          uint32_t diff = (critf ^ critg) & tier_mask;
+          while (diff) {
+            const int t = __ffs(diff) - 1;
+            diff &= diff - 1;
+            const bool fn = (critf >> t) & 1;
+            const int d = t_dim<D>(t);
+            const int cls = (d == Tr<D>::TOP) ? 3 : d;
+            nfalse++;
+            kinds[2 * cls + (fn ? 1 : 0)]++;
+            const int64_t tv = target_of<D>(f, cand_f, cand_g, g, u, t, fn);
+            if (tv < 0) { nint++; continue; }
+            atomicOr(tbits + (tv >> 5), 1u << (tv & 31));
+          }
+        }
+      }
+  warp_add(&cnt->n_false, nfalse);
+  warp_add(&cnt->n_internal, nint);
+#pragma unroll
+  for (int k = 0; k < 8; k++) warp_add(&cnt->kinds[k], kinds[k]);
+}
+
+// --------------------------------------------------------------------------
+// Eq. 2 edits (a6) on the marked targets; clears the bitmap for the next round.
+// state = q | lossless << 16.
+// --------------------------------------------------------------------------
+__global__ void k_edit(uint32_t* __restrict__ tbits, int64_t nwords, const float* __restrict__ fhat,
+                       const float* __restrict__ lb, float* __restrict__ gf, uint32_t* __restrict__ state,
+                       Counters* __restrict__ cnt, float step, int q_cap) {
+  unsigned long long changed = 0, targets = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nwords;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t w = tbits[i];
+    if (!w) continue;
+    tbits[i] = 0;
+    while (w) {
+      const int b = __ffs(w) - 1;
+      w &= w - 1;
+      const int64_t v = i * 32 + b;
+      targets++;
+      uint32_t st = state[v];
+      if (st >> 16) continue;                     // lossless: no-op
+      changed++;
+      const uint32_t q = st & 0xFFFFu;
+      if ((int)q + 1 <= q_cap) {
+        // g' = RN(fhat - RN((q+1) * step)), two roundings, never fused
+        const float gp = __fsub_rn(fhat[v], __fmul_rn((float)(q + 1), step));
+        if (gp >= lb[v]) { state[v] = q + 1; gf[v] = gp; continue; }
+      }
+      gf[v] = lb[v];                              // clamp, stored losslessly
+      state[v] = q | (1u << 16);
+    }
+  }
+  warp_add(&cnt->n_changed, changed);
+  warp_add(&cnt->n_targets, targets);
+}
+
+// --------------------------------------------------------------------------
+// Setup (a1): validate, lb = RU32(f - xi), g = fhat, state = 0.
+// |fhat - f| <= xi exactly  <=>  RU(f - xi) <= fhat <= RD(f + xi).
+// --------------------------------------------------------------------------
+__global__ void k_setup(const float* __restrict__ f, const float* __restrict__ fhat, float xi, int64_t n,
+                        float* __restrict__ lb, float* __restrict__ gf, uint32_t* __restrict__ state,
+                        Counters* __restrict__ cnt) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const float a = f[v], b = fhat[v];
+    if (!isfinite(a) || !isfinite(b)) { atomicMin(&cnt->first_nonfinite, (unsigned long long)v); continue; }
+    const float lo = __fsub_ru(a, xi);
+    if (b < lo || b > __fadd_rd(a, xi)) atomicMin(&cnt->first_bound, (unsigned long long)v);
+    lb[v] = lo;
+    gf[v] = b;
+    state[v] = 0;
+  }
+}
+
+// --------------------------------------------------------------------------
+// Edit-list emission (a8): ordered stream compaction of {v : state_v != 0}.
+// Chunk = EDIT_CHUNK vertices per block; count -> exclusive scan -> write.
+// --------------------------------------------------------------------------
+constexpr int EDIT_CHUNK = 8192;
+constexpr int EDIT_THREADS = 1024;
+
+__device__ __forceinline__ unsigned long long block_sum(unsigned long long v, unsigned long long* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  unsigned long long s = 0;
+  if (w == 0) {
+    s = (l < (int)(blockDim.x >> 5)) ? sh[l] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  }
+  __syncthreads();
+  return s;  // valid in warp 0
+}
+
+__global__ void k_edit_count(const uint32_t* __restrict__ state, int64_t n, unsigned long long* __restrict__ bc,
+                             Counters* __restrict__ cnt) {
+  __shared__ unsigned long long sh[32];
+  const int64_t base = (int64_t)blockIdx.x * EDIT_CHUNK;
+  unsigned long long c = 0, nl = 0;
+  for (int i = threadIdx.x; i < EDIT_CHUNK; i += blockDim.x) {
+    const int64_t v = base + i;
+    const uint32_t st = v < n ? state[v] : 0u;
+    if (st != 0) c++;
+    if (st >> 16) nl++;
+  }
+  warp_add(&cnt->n_lossless, nl);
+  c = block_sum(c, sh);
+  if (threadIdx.x == 0) bc[blockIdx.x] = c;
+}
+
+// exclusive scan of nb block counts in one block; total -> cnt->n_edits
+__global__ void k_scan_counts(unsigned long long* __restrict__ bc, int64_t nb, Counters* __restrict__ cnt) {
+  __shared__ unsigned long long part[EDIT_THREADS];
+  const int64_t per = (nb + blockDim.x - 1) / blockDim.x;
+  const int64_t lo = threadIdx.x * per, hi = min(nb, lo + per);
+  unsigned long long s = 0;
+  for (int64_t i = lo; i < hi; i++) s += bc[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long acc = 0;
+    for (int i = 0; i < (int)blockDim.x; i++) { unsigned long long t = part[i]; part[i] = acc; acc += t; }
+    cnt->n_edits = acc;
+  }
+  __syncthreads();
+  unsigned long long acc = part[threadIdx.x];
+  for (int64_t i = lo; i < hi; i++) { unsigned long long t = bc[i]; bc[i] = acc; acc += t; }
+}
+
+struct EditOut { unsigned long long v; unsigned short q; unsigned char lossless; unsigned char pad; float value; };
+static_assert(sizeof(EditOut) == 16, "dmtz_edit is 16 bytes");
+
+__global__ void k_edit_write(const uint32_t* __restrict__ state, const float* __restrict__ gf, int64_t n,
+                             const unsigned long long* __restrict__ boff, EditOut* __restrict__ out, int64_t cap) {
+  __shared__ unsigned int wsum[32];
+  const int64_t base = (int64_t)blockIdx.x * EDIT_CHUNK;
+  unsigned long long off = boff[blockIdx.x];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int seg = 0; seg < EDIT_CHUNK; seg += blockDim.x) {
+    const int64_t v = base + seg + threadIdx.x;
+    const uint32_t st = (v < n) ? state[v] : 0u;
+    const bool e = st != 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, e);
+    if (lane == 0) wsum[w] = __popc(bal);
+    __syncthreads();
+    unsigned int before = 0, total = 0;
+    for (int k = 0; k < nw; k++) { unsigned int c = wsum[k]; if (k < w) before += c; total += c; }
+    if (e) {
+      const unsigned long long pos = off + before + __popc(bal & ((1u << lane) - 1u));
+      if ((int64_t)pos < cap) {
+        EditOut o;
+        o.v = (unsigned long long)v;
+        o.q = (unsigned short)(st & 0xFFFFu);
+        o.lossless = (unsigned char)(st >> 16);
+        o.pad = 0;
+        o.value = gf[v];
+        out[pos] = o;
+      }
+    }
+    off += total;
+    __syncthreads();
+  }
+}
+
+}  // namespace dmtz

@@ -1,0 +1,147 @@
+"""GPU parity (``-m gpu``): the CUDA path, called through the C-ABI, against the CPU
+oracle on the same seeded inputs -- bit-exact on gradient codes, critical masks,
+edited-field bits, edit lists and statistics."""
+import numpy as np
+import pytest
+import torch
+
+import dmtz_inputs as di
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dmtz():
+    import paper_2409_17346_b200 as d
+    return d
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _codes_np(t):
+    a = t.cpu().numpy()
+    return a.view(np.uint64) if a.dtype == np.int64 else a.view(np.uint16)
+
+
+GRAD_CASES = [((3, 3), 0, False), ((17, 23), 1, False), ((64, 64), 2, True), ((130, 257), 3, False),
+              ((2, 2, 2), 4, False), ((3, 4, 5), 5, True), ((9, 8, 7), 6, False), ((33, 35, 131), 7, False),
+              ((20, 40, 30), 8, True)]
+
+
+@pytest.mark.parametrize("shape,seed,ties", GRAD_CASES)
+def test_gradient_codes_and_crit_bit_exact(dmtz, shape, seed, ties):
+    f, fh, _ = di.random_case(shape, seed, ties=ties)
+    for fld in (f, fh):
+        oc, om = oracle.gradient(fld)
+        gc = dmtz.compute_gradient(_cuda(fld))
+        gm = dmtz.critical_mask(gc)
+        torch.cuda.synchronize()
+        assert np.array_equal(_codes_np(gc), oc)
+        assert np.array_equal(gm.cpu().numpy().view(np.uint32), om)
+
+
+@pytest.mark.parametrize("name,shape", [("C1", None), ("C2", (180, 360)), ("C3", (20, 50, 50)),
+                                        ("C4", (24, 24, 24)), ("C5", (20, 24, 28))])
+def test_gradient_config_crops(dmtz, name, shape):
+    f, fh, _, _ = di.config_inputs(name, shape=shape)
+    for fld in (f, fh):
+        oc, om = oracle.gradient(fld)
+        gc = dmtz.compute_gradient(_cuda(fld))
+        assert np.array_equal(_codes_np(gc), oc)
+        assert np.array_equal(dmtz.critical_mask(gc).cpu().numpy().view(np.uint32), om)
+
+
+def _compare_correct(dmtz, f, fh, xi, q_cap=6, tier=2, full_sweeps=False):
+    ref = oracle.correct(f, fh, xi, 6, q_cap, tier)
+    r = dmtz.correct(_cuda(f), _cuda(fh), xi, q_max=6, q_cap=q_cap, tier=tier, full_sweeps=full_sweeps)
+    assert r.status == ref["status"], r.message
+    assert np.array_equal(r.g.cpu().numpy().view(np.uint32), ref["g"].view(np.uint32))
+    e = r.edits_numpy()
+    assert r.n_edits == ref["n_edits"]
+    assert np.array_equal(e["v"], ref["edits"]["v"])
+    assert np.array_equal(e["q"], ref["edits"]["q"])
+    assert np.array_equal(e["lossless"], ref["edits"]["lossless"])
+    assert np.array_equal(e["value"].view(np.uint32), ref["edits"]["value"].view(np.uint32))
+    for k in ("rounds", "n_edited", "n_quantized", "n_lossless", "n_false_round0", "false_by_kind_round0"):
+        assert r.stats[k] == ref["stats"][k], k
+    return r, ref
+
+
+CLOOP_CASES = [  # (family, shape, seed, eps, perturb, q_cap, tier, ties)
+    ("noise", (4, 4), 10, 5e-2, "lorenzo", 6, 2, False),
+    ("lognormal", (5, 6), 3, 5e-2, "noise", 1, 2, False),
+    ("lognormal", (5, 6), 3, 5e-2, "noise", 65535, 2, False),
+    ("gauss2d", (40, 70), 3, 0.05, "noise", 6, 2, False),
+    ("gauss2d", (40, 70), 3, 0.05, "noise", 6, 1, False),
+    ("lognormal", (57, 61), 3, 0.02, "lorenzo", 6, 2, True),
+    ("lognormal", (4, 4, 4), 3, 5e-2, "noise", 6, 2, False),
+    ("lognormal", (13, 17, 19), 3, 0.01, "noise", 6, 2, False),
+    ("lognormal", (13, 17, 19), 3, 0.01, "noise", 65535, 2, False),
+    ("lognormal", (13, 17, 19), 3, 0.01, "noise", 6, 1, False),
+    ("multiscale", (16, 16, 40), 3, 0.05, "noise", 6, 2, True),
+    ("hurricane", (10, 33, 70), 4, 0.01, "lorenzo", 6, 2, False),
+]
+
+
+@pytest.mark.parametrize("family,shape,seed,eps,perturb,q_cap,tier,ties", CLOOP_CASES)
+def test_cloop_bit_exact(dmtz, family, shape, seed, eps, perturb, q_cap, tier, ties):
+    f, fh, xi = di.random_case(shape, seed, eps=eps, ties=ties, perturb=perturb, family=family)
+    _compare_correct(dmtz, f, fh, xi, q_cap, tier)
+
+
+@pytest.mark.parametrize("name,shape", [("C1", None), ("C2", (180, 360)), ("C3", (20, 50, 50)),
+                                        ("C4", (32, 32, 32)), ("C5", (24, 24, 24))])
+@pytest.mark.parametrize("full_sweeps", [False, True])
+def test_cloop_config_crops(dmtz, name, shape, full_sweeps):
+    f, fh, xi, _ = di.config_inputs(name, shape=shape)
+    r, ref = _compare_correct(dmtz, f, fh, xi, full_sweeps=full_sweeps)
+    assert ref["status"] == 0 and ref["stats"]["rounds"] > 0
+
+
+def test_b1_golden_on_gpu(dmtz):
+    f = np.array([[1, 2], [4, 3]], np.float32)
+    fh = np.array([[2, 1], [4, 3]], np.float32)
+    r, _ = _compare_correct(dmtz, f, fh, 1.0, q_cap=6)
+    assert r.g.cpu().numpy().ravel().tolist() == [0.0, 1.0, 4.0, 3.0] and r.stats["rounds"] == 7
+    r, _ = _compare_correct(dmtz, f, fh, 1.0, q_cap=65535)
+    assert r.stats["rounds"] == 64
+
+
+def test_errors_and_capacity(dmtz):
+    f, fh, xi = di.random_case((20, 30), 3, eps=0.05, family="gauss2d", perturb="noise")
+    bad = fh.copy()
+    bad[3, 4] = np.nan
+    r = dmtz.correct(_cuda(f), _cuda(bad), xi, raise_on_error=False)
+    assert r.status == dmtz.E_NONFINITE and "vertex" in r.message
+    bad = fh.copy()
+    bad[5, 5] = f[5, 5] + 2 * xi
+    r = dmtz.correct(_cuda(f), _cuda(bad), xi, raise_on_error=False)
+    assert r.status == dmtz.E_BOUND
+    ref = oracle.correct(f, fh, xi)
+    assert ref["n_edits"] > 2
+    r = dmtz.correct(_cuda(f), _cuda(fh), xi, edits_capacity=2)
+    assert r.status == dmtz.E_CAPACITY and r.n_edits == ref["n_edits"]
+    assert np.array_equal(r.edits_numpy()["v"], ref["edits"]["v"][:2])
+    with pytest.raises(TypeError):
+        dmtz.correct(torch.from_numpy(f), torch.from_numpy(fh), xi)
+
+
+def test_stuck_matches_oracle(dmtz):
+    rng = np.random.default_rng(3)
+    seen = set()
+    for i in range(6):
+        f = (rng.random((6, 6)) * 1e-7).astype(np.float32)
+        fh = (f + (rng.random((6, 6)) - 0.5) * 0.5).astype(np.float32)
+        r, ref = _compare_correct(dmtz, f, fh, 0.5)
+        seen.add(r.status)
+    assert dmtz.E_STUCK in seen
+
+
+def test_deterministic(dmtz):
+    f, fh, xi, _ = di.config_inputs("C4", shape=(40, 40, 40))
+    a = dmtz.correct(_cuda(f), _cuda(fh), xi)
+    b = dmtz.correct(_cuda(f), _cuda(fh), xi)
+    assert torch.equal(a.g.view(torch.int32), b.g.view(torch.int32)) and torch.equal(a.edits, b.edits)
