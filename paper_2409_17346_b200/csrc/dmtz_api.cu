@@ -8,6 +8,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -25,6 +26,7 @@ struct dmtz_ctx {
   int rank, world;
   Counters* host_cnt;  // pinned
   cudaEvent_t ev[2];   // sweep timing (opts.profile)
+  int verbose;         // DMTZ_VERBOSE=1: per-round counters on stderr
 };
 
 namespace {
@@ -159,6 +161,9 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
     }
     st->sweeps++;
     st->anchors_swept += g.N;
+    if (c->verbose)
+      fprintf(stderr, "dmtz round %lld: false %llu targets %llu changed %llu\n", (long long)round,
+              hc->n_false, hc->n_targets, hc->n_changed);
     if (hc->n_internal) {
       set_err("gradient invariant violated at %llu false cells (round %lld)", hc->n_internal, (long long)round);
       status = DMTZ_E_INTERNAL;
@@ -234,6 +239,8 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
   c->D = d->nz == 1 ? 2 : 3;
   c->device = cuda_device;
   c->rank = rank; c->world = world;
+  const char* vb = getenv("DMTZ_VERBOSE");
+  c->verbose = vb && vb[0] == '1';
   cudaError_t e = cudaMallocHost((void**)&c->host_cnt, sizeof(Counters) * 2);
   if (e != cudaSuccess) { delete c; set_err("cudaMallocHost: %s", cudaGetErrorString(e)); return DMTZ_E_CUDA; }
   for (int i = 0; i < 2; i++) {
