@@ -27,7 +27,8 @@ struct Counters {                 // device-side round counters (one 256 B block
   unsigned long long first_bound;
   unsigned long long n_edits;
   unsigned long long n_lossless;  // lossless entries of the edit list
-  unsigned long long pad[16];
+  unsigned long long n_swept;     // anchors evaluated by the round's sweep
+  unsigned long long pad[15];
 };
 static_assert(sizeof(Counters) == 256, "counters are one 256 B block");
 
