@@ -15,7 +15,7 @@
 
 #include "../../include/dmtz.h"
 #include "dmtz_kernels.cuh"
-#include "dmtz_sweep3d.cuh"
+#include "dmtz_sweep.cuh"
 #include "dmtz_trace.cuh"
 
 using namespace dmtz;
@@ -55,8 +55,8 @@ inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 // Workspace layout (offsets from the base, each 256-B aligned)
 struct Layout {
-  size_t cand_f, cand_g, lb, state, tbits, counters, edit_bc, frontier, trace, total;
-  int64_t fwords;  // frontier words (3D bricks)
+  size_t cand_f, cand_g, lb, state, tbits, counters, edit_bc, dbits, units, frontier, trace, total;
+  int64_t fwords;  // frontier bitmap words (one bit per row-block unit)
 };
 
 Layout layout_for(const dmtz_ctx* c) {
@@ -71,11 +71,11 @@ Layout layout_for(const dmtz_ctx* c) {
   L.tbits = o; o += align_up((N + 31) / 32 * 4 + 64);
   L.counters = o; o += align_up(sizeof(Counters) * 2);
   L.edit_bc = o; o += align_up(((N + EDIT_CHUNK - 1) / EDIT_CHUNK + 2) * 8);
-  {
-    BrickGeom bg = brick_geom3(c->g);
-    L.fwords = (bg.bx * bg.by * bg.bz + 31) / 32;
-  }
-  L.frontier = o; o += align_up(2 * L.fwords * 4);
+  const RowGeom rg = row_geom(c->g);
+  L.fwords = (rg.units + 31) / 32;
+  L.dbits = o; o += align_up((size_t)(c->g.nz * c->g.ny * rg.wpr) * 4 + 64);
+  L.units = o; o += align_up((size_t)rg.units * 4);
+  L.frontier = o; o += align_up(L.fwords * 4 + 64);
   L.trace = o; o += align_up(trace_scratch_bytes(c->g, c->D));
   L.total = o;
   return L;
@@ -110,7 +110,7 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
   const Grid& g = c->g;
   using code_t = typename Tr<D>::code_t;
   code_t* cand_f = (code_t*)(ws + L.cand_f);
-  code_t* cand_g = (code_t*)(ws + L.cand_g);
+  code_t* cand_g = (code_t*)(ws + L.cand_g);  // sparse: valid where the d bit is set
   float* lb = (float*)(ws + L.lb);
   uint32_t* state = (uint32_t*)(ws + L.state);
   uint32_t* tbits = (uint32_t*)(ws + L.tbits);
@@ -149,48 +149,51 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
   const float step = ldexpf(o->xi, -o->q_max);   // xi / 2^q_max, exact
   const int64_t max_rounds = o->max_rounds > 0 ? o->max_rounds : g.N * (int64_t)(o->q_cap + 1);
   const uint32_t tmask = tier_mask<D>(o->tier);
-  dmtz_status status = DMTZ_OK;
-  const BrickGeom bg = brick_geom3(g);
-  const int64_t nbricks = bg.bx * bg.by * bg.bz;
-  uint32_t* fr_cur = (uint32_t*)(ws + L.frontier);
-  uint32_t* fr_next = fr_cur + L.fwords;
+  const RowGeom rg = row_geom(g);
+  uint32_t* dbits = (uint32_t*)(ws + L.dbits);
+  uint32_t* units = (uint32_t*)(ws + L.units);
+  uint32_t* fbits = (uint32_t*)(ws + L.frontier);
+  unsigned long long* n_units = &dc->n_units;
+  const bool frontier_mode = !o->full_sweeps;
   const int fwords_smem = L.fwords * 4 <= 32768 ? (int)L.fwords : 0;
-  const bool frontier_mode = (D == 3) && !o->full_sweeps;
+  const int sweep_blocks = 148 * 8;
+  // round 1 (and every round of a full sweep) processes every unit
+  k_units_all<<<(unsigned)((rg.units + 255) / 256 < 4096 ? (rg.units + 255) / 256 : 4096), 256, 0, s>>>(
+      rg.units, units, n_units);
+  st->launches++;
+  dmtz_status status = DMTZ_OK;
   for (int64_t round = 1;; round++) {
-    // a3: gradient of g;  a4/a5: classify + mark targets;  a6: edit
+    // a3: gradient of g (screened);  a4/a5: classify + mark targets;  a6: edit;  a7: frontier
     CK(cudaMemsetAsync(dc, 0, offsetof(Counters, first_nonfinite), s));
-    if (frontier_mode) CK(cudaMemsetAsync(fr_next, 0, L.fwords * 4, s));
+    if (frontier_mode) CK(cudaMemsetAsync(fbits, 0, L.fwords * 4, s));
     if (o->profile) CK(cudaEventRecord(c->ev[0], s));
-    if constexpr (D == 3) {
-      const uint32_t* frontier = (frontier_mode && round > 1) ? fr_cur : nullptr;
-      k_sweep3<<<(unsigned)nbricks, sw3::THREADS, sizeof(SweepSmem3), s>>>(
-          f, g_out, (const unsigned long long*)cand_f, tbits, frontier, dc, g, bg, tmask);
-      if (o->profile) CK(cudaEventRecord(c->ev[1], s));
-      k_edit3<<<wblocks, ethreads, fwords_smem * 4, s>>>(tbits, nwords, fhat, lb, g_out, state, dc, step,
-                                                         o->q_cap, frontier_mode ? fr_next : nullptr, g, bg,
-                                                         frontier_mode ? fwords_smem : 0);
-      st->launches += 2;
-    } else {
-      launch_codes<D>(g, g_out, cand_g, 0, g.nz, s);
-      k_diff<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(f, cand_f, cand_g, tbits, dc, g, 0, g.nz, tmask);
-      if (o->profile) CK(cudaEventRecord(c->ev[1], s));
-      k_edit<<<wblocks, ethreads, 0, s>>>(tbits, nwords, fhat, lb, g_out, state, dc, step, o->q_cap);
-      st->launches += 3;
-    }
+    k_screen<D><<<sweep_blocks, 256, 0, s>>>(g_out, cand_f, cand_g, dbits, units, n_units, g, rg, dc);
+    k_decode<D><<<sweep_blocks, 256, 0, s>>>(f, cand_f, cand_g, dbits, tbits, units, n_units, g, rg, tmask, dc);
+    if (o->profile) CK(cudaEventRecord(c->ev[1], s));
+    k_edit_rows<D><<<wblocks, ethreads, frontier_mode ? fwords_smem * 4 : 0, s>>>(
+        tbits, nwords, fhat, lb, g_out, state, dc, step, o->q_cap, frontier_mode ? fbits : nullptr, g, rg,
+        frontier_mode ? fwords_smem : 0);
+    st->launches += 3;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(hc, dc, offsetof(Counters, first_nonfinite), cudaMemcpyDeviceToHost, s));
+    if (frontier_mode) {
+      // next round's unit list (after the counters were copied: n_units is reset here)
+      CK(cudaMemsetAsync(n_units, 0, 8, s));
+      k_units_from_bits<<<(unsigned)((rg.units + 255) / 256 < 4096 ? (rg.units + 255) / 256 : 4096), 256, 0, s>>>(
+          fbits, rg.units, units, n_units);
+      st->launches++;
+    }
     CK(cudaStreamSynchronize(s));
     if (o->profile) {
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
       st->sweep_ms += ms;
     }
-    std::swap(fr_cur, fr_next);
     st->sweeps++;
-    st->anchors_swept += D == 3 ? (int64_t)hc->n_swept : g.N;
+    st->anchors_swept += (int64_t)hc->n_swept;
     if (c->verbose)
-      fprintf(stderr, "dmtz round %lld: false %llu targets %llu changed %llu\n", (long long)round,
-              hc->n_false, hc->n_targets, hc->n_changed);
+      fprintf(stderr, "dmtz round %lld: swept %llu false %llu targets %llu changed %llu\n", (long long)round,
+              hc->n_swept, hc->n_false, hc->n_targets, hc->n_changed);
     if (hc->n_internal) {
       set_err("gradient invariant violated at %llu false cells (round %lld)", hc->n_internal, (long long)round);
       status = DMTZ_E_INTERNAL;

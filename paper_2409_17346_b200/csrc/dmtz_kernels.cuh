@@ -23,12 +23,13 @@ struct Counters {                 // device-side round counters (one 256 B block
   unsigned long long n_changed;   // targets that took a step or were clamped
   unsigned long long n_targets;   // distinct targets marked
   unsigned long long n_internal;  // invariant violations (expected 0)
+  unsigned long long n_swept;     // anchors evaluated by the round's sweep
   unsigned long long first_nonfinite;
   unsigned long long first_bound;
   unsigned long long n_edits;
   unsigned long long n_lossless;  // lossless entries of the edit list
-  unsigned long long n_swept;     // anchors evaluated by the round's sweep
-  unsigned long long pad[15];
+  unsigned long long n_units;     // active units of the current round (frontier list length)
+  unsigned long long pad[14];
 };
 static_assert(sizeof(Counters) == 256, "counters are one 256 B block");
 
@@ -170,51 +171,6 @@ __global__ void k_critmask(const typename Tr<D>::code_t* __restrict__ codes, uin
   }
 }
 
-// --------------------------------------------------------------------------
-// Target of a false cell (a5): rules R1 / R2 / R3a / R3b.
-// Rare path: tables are indexed dynamically, codes re-read through L1/L2.
-// Returns -1 on an internal inconsistency.
-// --------------------------------------------------------------------------
-template <int D>
-__device__ int64_t target_of(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__ cand_f,
-                             const typename Tr<D>::code_t* __restrict__ cand_g, const Grid& g, int64_t u,
-                             int t, bool fn) {
-  const int nv = t_nv<D>(t);
-  int64_t vid[4];
-  int64_t m = -1;
-  float fm = 0.f;
-  for (int k = 0; k < nv; k++) {
-    vid[k] = u + mask_delta(g, t_vmask<D>(t, k));
-    float fv = __ldg(f + vid[k]);
-    if (m < 0 || sos_less(fv, vid[k], fm, m)) { m = vid[k]; fm = fv; }
-  }
-  const int top = Tr<D>::TOP;
-  if (!fn) {                                    // FP: paired in f, critical in g (R1)
-    if (t_dim<D>(t) < top) {
-      uint32_t s = field_of<D>((uint64_t)__ldg(cand_f + u), t);
-      if (s != (uint32_t)t_none<D>(t))
-        return u + t_link<D>(t, s, 0) + t_link<D>(t, s, 1) * g.sy + t_link<D>(t, s, 2) * g.sz;
-    }
-    return m;                                   // paired down in f: the f-lowest vertex
-  }
-  if (t_dim<D>(t) < top) {                      // FN: critical in f, paired in g
-    uint32_t s = field_of<D>((uint64_t)__ldg(cand_g + u), t);
-    if (s != (uint32_t)t_none<D>(t)) return m;  // paired up in g (R2)
-  }
-  for (int j = 0; j < t_nfacet<D>(t); j++) {    // paired down in g with gamma
-    const int dm = t_facet<D>(t, j, 0), ft = t_facet<D>(t, j, 1), sl = t_facet<D>(t, j, 2);
-    const int k = t_facet<D>(t, j, 3);
-    const int64_t ga = u + mask_delta(g, dm);
-    if (field_of<D>((uint64_t)__ldg(cand_g + ga), ft) != (uint32_t)sl) continue;
-    const int64_t y = vid[k];
-    if (m != y) return m;                       // R3a
-    uint32_t s2 = field_of<D>((uint64_t)__ldg(cand_f + ga), ft);   // R3b
-    if (s2 == (uint32_t)t_none<D>(ft)) return -1;
-    return ga + t_link<D>(ft, s2, 0) + t_link<D>(ft, s2, 1) * g.sy + t_link<D>(ft, s2, 2) * g.sz;
-  }
-  return -1;
-}
-
 __device__ __forceinline__ void warp_add(unsigned long long* dst, unsigned long long v) {
   // warp-aggregated atomic for a value that may be zero on most lanes
   unsigned mask = __ballot_sync(0xffffffffu, v != 0);
@@ -223,84 +179,6 @@ __device__ __forceinline__ void warp_add(unsigned long long* dst, unsigned long 
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if ((threadIdx.x & 31) == (unsigned)(__ffs(mask) - 1)) atomicAdd(dst, s);
-}
-
-// --------------------------------------------------------------------------
-// The sweep of one C-loop round (a4+a5): classify every cell of the anchors of
-// z-planes [z0, z1), mark the target set T (bitmap, atomicOr), count F by kind.
-// --------------------------------------------------------------------------
-template <int D>
-__global__ void k_diff(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__ cand_f,
-                       const typename Tr<D>::code_t* __restrict__ cand_g, uint32_t* __restrict__ tbits,
-                       Counters* __restrict__ cnt, Grid g, int64_t z0, int64_t z1, uint32_t tier_mask) {
-  unsigned long long nfalse = 0, nint = 0;
-  unsigned long long kinds[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int64_t z = z0 + blockIdx.z; z < z1; z += gridDim.z)
-    for (int64_t y = blockIdx.y; y < g.ny; y += gridDim.y)
-      for (int64_t xb = (int64_t)blockIdx.x * blockDim.x; xb < g.nx; xb += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t x = xb + threadIdx.x;
-        if (x < g.nx) {
-          const int64_t u = x + y * g.sy + z * g.sz;
-          const int ok = axes_ok(g, x, y, z);
-          uint64_t cf[Tr<D>::NDELTA], cg[Tr<D>::NDELTA];
-          load_codes8<D>(cand_f, g, u, ok, cf);
-          load_codes8<D>(cand_g, g, u, ok, cg);
-          const uint32_t critf = decode_crit<D>(cf, ok);
-          const uint32_t critg = decode_crit<D>(cg, ok);
-          uint32_t diff = (critf ^ critg) & tier_mask;
-          while (diff) {
-            const int t = __ffs(diff) - 1;
-            diff &= diff - 1;
-            const bool fn = (critf >> t) & 1;
-            const int d = t_dim<D>(t);
-            const int cls = (d == Tr<D>::TOP) ? 3 : d;
-            nfalse++;
-            kinds[2 * cls + (fn ? 1 : 0)]++;
-            const int64_t tv = target_of<D>(f, cand_f, cand_g, g, u, t, fn);
-            if (tv < 0) { nint++; continue; }
-            atomicOr(tbits + (tv >> 5), 1u << (tv & 31));
-          }
-        }
-      }
-  warp_add(&cnt->n_false, nfalse);
-  warp_add(&cnt->n_internal, nint);
-#pragma unroll
-  for (int k = 0; k < 8; k++) warp_add(&cnt->kinds[k], kinds[k]);
-}
-
-// --------------------------------------------------------------------------
-// Eq. 2 edits (a6) on the marked targets; clears the bitmap for the next round.
-// state = q | lossless << 16.
-// --------------------------------------------------------------------------
-__global__ void k_edit(uint32_t* __restrict__ tbits, int64_t nwords, const float* __restrict__ fhat,
-                       const float* __restrict__ lb, float* __restrict__ gf, uint32_t* __restrict__ state,
-                       Counters* __restrict__ cnt, float step, int q_cap) {
-  unsigned long long changed = 0, targets = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nwords;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t w = tbits[i];
-    if (!w) continue;
-    tbits[i] = 0;
-    while (w) {
-      const int b = __ffs(w) - 1;
-      w &= w - 1;
-      const int64_t v = i * 32 + b;
-      targets++;
-      uint32_t st = state[v];
-      if (st >> 16) continue;                     // lossless: no-op
-      changed++;
-      const uint32_t q = st & 0xFFFFu;
-      if ((int)q + 1 <= q_cap) {
-        // g' = RN(fhat - RN((q+1) * step)), two roundings, never fused
-        const float gp = __fsub_rn(fhat[v], __fmul_rn((float)(q + 1), step));
-        if (gp >= lb[v]) { state[v] = q + 1; gf[v] = gp; continue; }
-      }
-      gf[v] = lb[v];                              // clamp, stored losslessly
-      state[v] = q | (1u << 16);
-    }
-  }
-  warp_add(&cnt->n_changed, changed);
-  warp_add(&cnt->n_targets, targets);
 }
 
 // --------------------------------------------------------------------------

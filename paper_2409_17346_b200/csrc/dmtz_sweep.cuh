@@ -1,0 +1,363 @@
+// dmtz_sweep.cuh -- the round sweep of the C-loop (a3 + a4 + a5) for sm_100a.
+//
+// Work unit: a ROW BLOCK = UY consecutive y-rows of one z-plane (all x).  The
+// rounds process an on-device list of active units (the frontier, a7), so
+// late rounds touch only units near last round's edits.
+//
+//  k_screen<D>  per anchor u of an active unit: cand_g(u) from the 3^D stencil
+//               of g (the local form of the gradient), compared
+//               with cand_f(u).  Writes the bit d(u) = [cand_g(u) != cand_f(u)]
+//               (row-padded bitmap, one word per 32 anchors of a row) and, where
+//               d(u) = 1, cand_g(u) into a sparse code buffer.  Both are
+//               memoized across rounds: an anchor outside the frontier keeps
+//               its stencil, hence its code.
+//  k_decode<D>  per anchor u of an active unit whose 2^D code neighbourhood
+//               u + {0,1}^D has a d bit set (a cell's criticality is a function
+//               of those codes): decode crit_f / crit_g, mark the false cells'
+//               targets (rules R1/R2/R3a/R3b, unrolled per cell type).
+//  k_edit_rows<D> Eq. 2 edits of the marked targets and the next frontier
+//               (units meeting v + [-2,1]^D for every target v).
+#pragma once
+#include <utility>
+
+#include "dmtz_kernels.cuh"
+
+namespace dmtz {
+
+constexpr int UY = 4;  // rows per unit
+
+struct RowGeom {
+  int64_t wpr;     // bitmap words per row = ceil(nx / 32)
+  int64_t ub;      // y-blocks per plane = ceil(ny / UY)
+  int64_t units;   // ub * nz
+};
+
+__host__ __device__ inline RowGeom row_geom(const Grid& g) {
+  RowGeom r;
+  r.wpr = (g.nx + 31) / 32;
+  r.ub = (g.ny + UY - 1) / UY;
+  r.units = r.ub * g.nz;
+  return r;
+}
+
+// bit word of anchor row (y, z), x-chunk c
+__device__ __forceinline__ int64_t dword_index(const Grid& g, const RowGeom& rg, int64_t y, int64_t z, int64_t c) {
+  return (z * g.ny + y) * rg.wpr + c;
+}
+
+// ---------------------------------------------------------------------------
+// Stencil load: the 3^D neighbourhood of u, +inf outside the grid.
+// ---------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ void load_stencil(const float* __restrict__ fld, const Grid& g, int64_t v, int64_t x,
+                                             int64_t y, int64_t z, float (&s)[27]) {
+  const float INF = __int_as_float(0x7f800000);
+  const bool interior = x > 0 && x + 1 < g.nx && y > 0 && y + 1 < g.ny && (D == 2 || (z > 0 && z + 1 < g.nz));
+  if (interior) {
+#pragma unroll
+    for (int dz = -1; dz <= 1; dz++)
+#pragma unroll
+      for (int dy = -1; dy <= 1; dy++)
+#pragma unroll
+        for (int dx = -1; dx <= 1; dx++) {
+          const int p = (dx + 1) + 3 * (dy + 1) + 9 * (dz + 1);
+          if (D == 2 && dz != 0) { s[p] = INF; continue; }
+          s[p] = __ldg(fld + v + dx + dy * g.sy + dz * g.sz);
+        }
+  } else {
+#pragma unroll
+    for (int dz = -1; dz <= 1; dz++)
+#pragma unroll
+      for (int dy = -1; dy <= 1; dy++)
+#pragma unroll
+        for (int dx = -1; dx <= 1; dx++) {
+          const int p = (dx + 1) + 3 * (dy + 1) + 9 * (dz + 1);
+          if (D == 2 && dz != 0) { s[p] = INF; continue; }
+          const bool in = (x + dx >= 0) && (x + dx < g.nx) && (y + dy >= 0) && (y + dy < g.ny) &&
+                          (z + dz >= 0) && (z + dz < g.nz);
+          s[p] = in ? __ldg(fld + v + dx + dy * g.sy + dz * g.sz) : INF;
+        }
+  }
+}
+
+template <int D>
+__device__ __forceinline__ uint64_t cand_of(const float (&s)[27]) {
+  if constexpr (D == 3) return k3d::cand_code(s);
+  else return k2d::cand_code(s);
+}
+
+// ---------------------------------------------------------------------------
+// k_screen: codes of g + screening bits.  One warp per 32-anchor row chunk.
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(256)
+k_screen(const float* __restrict__ gfld, const typename Tr<D>::code_t* __restrict__ cand_f,
+         typename Tr<D>::code_t* __restrict__ cg_buf, uint32_t* __restrict__ dbits,
+         const uint32_t* __restrict__ units, const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg,
+         Counters* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n_units = (int64_t)*n_units_p;
+  const int64_t per_unit = (int64_t)UY * rg.wpr;  // row chunks per unit
+  const int64_t total = n_units * per_unit;
+  unsigned long long swept = 0;
+  for (int64_t it = warp; it < total; it += nwarps) {
+    const int64_t ui = it / per_unit, rem = it - ui * per_unit;
+    const int64_t unit = units[ui];
+    const int64_t z = unit / rg.ub, y = (unit - z * rg.ub) * UY + rem / rg.wpr;
+    const int64_t c = rem % rg.wpr;
+    if (y >= g.ny) continue;  // warp-uniform
+    const int64_t x = c * 32 + lane;
+    bool d = false;
+    if (x < g.nx) {
+      const int64_t v = x + y * g.sy + z * g.sz;
+      float s[27];
+      load_stencil<D>(gfld, g, v, x, y, z, s);
+      const int ok = axes_ok(g, x, y, z);
+      const uint64_t cgv = cand_of<D>(s) | t_nonex_fill<D>(ok);
+      const uint64_t cfv = (uint64_t)__ldg(cand_f + v);
+      d = cgv != cfv;
+      if (d) cg_buf[v] = (typename Tr<D>::code_t)cgv;
+      swept++;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, d);
+    if (lane == 0) dbits[dword_index(g, rg, y, z, c)] = bal;
+  }
+  warp_add(&cnt->n_swept, swept);
+}
+
+// ---------------------------------------------------------------------------
+// Static target rule of cell type T (twin of target_of in dmtz_kernels.cuh).
+// ---------------------------------------------------------------------------
+template <int D, int T>
+__device__ __forceinline__ int64_t link_offset(const Grid& g, uint32_t s) {
+  int64_t off = 0;
+#pragma unroll
+  for (int j = 0; j < 14; j++) {
+    if (j < t_nlink<D>(T) && s == (uint32_t)j)
+      off = t_link<D>(T, j, 0) + t_link<D>(T, j, 1) * g.sy + t_link<D>(T, j, 2) * g.sz;
+  }
+  return off;
+}
+
+template <int D, int T>
+__device__ __forceinline__ int64_t target_static(const float* __restrict__ f, const Grid& g, int64_t u,
+                                                 const uint64_t (&cf)[Tr<D>::NDELTA],
+                                                 const uint64_t (&cg)[Tr<D>::NDELTA], bool fn) {
+  constexpr int TOP = Tr<D>::TOP;
+  const int nv = t_nv<D>(T);
+  int64_t vid[4];
+  int64_t m = -1;
+  float fm = 0.f;
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    if (k < nv) {
+      vid[k] = u + mask_delta(g, t_vmask<D>(T, k));
+      const float fv = __ldg(f + vid[k]);
+      if (k == 0 || sos_less(fv, vid[k], fm, m)) { m = vid[k]; fm = fv; }
+    }
+  }
+  if (!fn) {                                 // FP: paired in f, critical in g (R1)
+    if (t_dim<D>(T) < TOP) {
+      const uint32_t s = field_of<D>(cf[0], T);
+      if (s != (uint32_t)t_none<D>(T)) return u + link_offset<D, T>(g, s);
+    }
+    return m;                                // paired down in f: the f-lowest vertex
+  }
+  if (t_dim<D>(T) < TOP) {                   // FN paired up in g (R2)
+    if (field_of<D>(cg[0], T) != (uint32_t)t_none<D>(T)) return m;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; j++) {              // FN paired down in g with gamma (R3a / R3b)
+    if (j >= t_nfacet<D>(T)) continue;
+    const int dm = t_facet<D>(T, j, 0), ft = t_facet<D>(T, j, 1), sl = t_facet<D>(T, j, 2), k = t_facet<D>(T, j, 3);
+    if (field_of<D>(cg[dm], ft) != (uint32_t)sl) continue;
+    if (m != vid[k]) return m;
+    const uint32_t s2 = field_of<D>(cf[dm], ft);
+    if (s2 == (uint32_t)t_none<D>(ft)) return -1;
+    int64_t off = 0;
+#pragma unroll
+    for (int q = 0; q < 14; q++)
+      if (q < t_nlink<D>(ft) && s2 == (uint32_t)q)
+        off = t_link<D>(ft, q, 0) + t_link<D>(ft, q, 1) * g.sy + t_link<D>(ft, q, 2) * g.sz;
+    return u + mask_delta(g, dm) + off;
+  }
+  return -1;
+}
+
+template <int D, int T>
+__device__ __forceinline__ void handle_type(uint32_t diff, uint32_t critf, const float* __restrict__ f,
+                                            const Grid& g, int64_t u, const uint64_t (&cf)[Tr<D>::NDELTA],
+                                            const uint64_t (&cg)[Tr<D>::NDELTA], uint32_t* __restrict__ tbits,
+                                            unsigned long long (&kinds)[8], unsigned long long& nint) {
+  if (!((diff >> T) & 1u)) return;
+  const bool fn = (critf >> T) & 1u;
+  const int d = t_dim<D>(T);
+  const int cls = (d == Tr<D>::TOP) ? 3 : d;
+  if (fn) kinds[2 * cls + 1]++;
+  else kinds[2 * cls]++;
+  const int64_t tv = target_static<D, T>(f, g, u, cf, cg, fn);
+  if (tv < 0) { nint++; return; }
+  atomicOr(tbits + (tv >> 5), 1u << (tv & 31));
+}
+
+template <int D, int... Ts>
+__device__ __forceinline__ void handle_all(std::integer_sequence<int, Ts...>, uint32_t diff, uint32_t critf,
+                                           const float* __restrict__ f, const Grid& g, int64_t u,
+                                           const uint64_t (&cf)[Tr<D>::NDELTA], const uint64_t (&cg)[Tr<D>::NDELTA],
+                                           uint32_t* __restrict__ tbits, unsigned long long (&kinds)[8],
+                                           unsigned long long& nint) {
+  (handle_type<D, Ts>(diff, critf, f, g, u, cf, cg, tbits, kinds, nint), ...);
+}
+
+// ---------------------------------------------------------------------------
+// k_decode: classification of the anchors whose code neighbourhood changed.
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(256)
+k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__ cand_f,
+         const typename Tr<D>::code_t* __restrict__ cg_buf, const uint32_t* __restrict__ dbits,
+         uint32_t* __restrict__ tbits, const uint32_t* __restrict__ units,
+         const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg, uint32_t tier_mask,
+         Counters* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n_units = (int64_t)*n_units_p;
+  const int64_t per_unit = (int64_t)UY * rg.wpr;
+  const int64_t total = n_units * per_unit;
+  unsigned long long kinds[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long nfalse = 0, nint = 0;
+  for (int64_t it = warp; it < total; it += nwarps) {
+    const int64_t ui = it / per_unit, rem = it - ui * per_unit;
+    const int64_t unit = units[ui];
+    const int64_t z = unit / rg.ub, y = (unit - z * rg.ub) * UY + rem / rg.wpr;
+    const int64_t c = rem % rg.wpr;
+    if (y >= g.ny) continue;
+    // need bits: d over u + {0,1}^D, i.e. rows (y, y+1) x planes (z, z+1), bits x and x+1
+    uint32_t need = 0;
+#pragma unroll
+    for (int r = 0; r < (D == 3 ? 4 : 2); r++) {
+      const int64_t yy = y + (r & 1), zz = z + (r >> 1);
+      if (yy >= g.ny || zz >= g.nz) continue;
+      const int64_t wi = dword_index(g, rg, yy, zz, c);
+      const uint32_t w0 = __ldg(dbits + wi);
+      const uint32_t w1 = (c + 1 < rg.wpr) ? __ldg(dbits + wi + 1) : 0u;
+      need |= w0 | (w0 >> 1) | (w1 << 31);
+    }
+    if (!need) continue;  // warp-uniform
+    const int64_t x = c * 32 + lane;
+    if (!((need >> lane) & 1u) || x >= g.nx) continue;
+    const int64_t u = x + y * g.sy + z * g.sz;
+    const int ok = axes_ok(g, x, y, z);
+    uint64_t cf[Tr<D>::NDELTA], cg[Tr<D>::NDELTA];
+#pragma unroll
+    for (int dm = 0; dm < Tr<D>::NDELTA; dm++) {
+      if ((dm & ~ok) != 0) { cf[dm] = cg[dm] = Tr<D>::ALL_NONE; continue; }
+      const int64_t w = u + mask_delta(g, dm);
+      cf[dm] = (uint64_t)__ldg(cand_f + w);
+      const int64_t xx = x + (dm & 1), yy = y + ((dm >> 1) & 1), zz = z + ((dm >> 2) & 1);
+      const uint32_t wd = __ldg(dbits + dword_index(g, rg, yy, zz, xx >> 5));
+      cg[dm] = ((wd >> (xx & 31)) & 1u) ? (uint64_t)__ldg(cg_buf + w) : cf[dm];
+    }
+    const uint32_t critf = decode_crit<D>(cf, ok), critg = decode_crit<D>(cg, ok);
+    const uint32_t diff = (critf ^ critg) & tier_mask;
+    if (!diff) continue;
+    nfalse += __popc(diff);
+    handle_all<D>(std::make_integer_sequence<int, Tr<D>::NT>{}, diff, critf, f, g, u, cf, cg, tbits, kinds, nint);
+  }
+  warp_add(&cnt->n_false, nfalse);
+  warp_add(&cnt->n_internal, nint);
+#pragma unroll
+  for (int k = 0; k < 8; k++) warp_add(&cnt->kinds[k], kinds[k]);
+}
+
+// ---------------------------------------------------------------------------
+// Edits (a6) + next frontier.  One warp per 32 target-bitmap words; lanes take
+// the 32 bits of each non-empty word in parallel.  The frontier (a7) marks the
+// units meeting v + [-2,1]^D for every target v (a value change at v can alter
+// only cells anchored there, and every false cell is anchored there relative
+// to its own target), aggregated in shared memory when it fits.
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void k_edit_rows(uint32_t* __restrict__ tbits, int64_t nwords, const float* __restrict__ fhat,
+                            const float* __restrict__ lb, float* __restrict__ gf, uint32_t* __restrict__ state,
+                            Counters* __restrict__ cnt, float step, int q_cap, uint32_t* __restrict__ next_frontier,
+                            Grid g, RowGeom rg, int fwords_smem) {
+  extern __shared__ uint32_t sfr[];
+  for (int i = threadIdx.x; i < fwords_smem; i += blockDim.x) sfr[i] = 0;
+  __syncthreads();
+  uint32_t* fr = fwords_smem ? sfr : next_frontier;
+  unsigned long long changed = 0, targets = 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp0 * 32; base < nwords; base += nwarps * 32) {
+    const int64_t wi = base + lane;
+    uint32_t word = wi < nwords ? tbits[wi] : 0u;
+    if (word) tbits[wi] = 0;
+    unsigned nz = __ballot_sync(0xffffffffu, word != 0);
+    while (nz) {
+      const int src = __ffs(nz) - 1;
+      nz &= nz - 1;
+      const uint32_t wv = __shfl_sync(0xffffffffu, word, src);
+      if (!((wv >> lane) & 1u)) continue;
+      const int64_t v = (base + src) * 32 + lane;
+      targets++;
+      if (next_frontier) {
+        const int64_t vy = (v / g.nx) % g.ny, vz = v / g.sz;
+        const int64_t y0 = vy >= 2 ? vy - 2 : 0, y1 = vy + 1 < g.ny ? vy + 1 : g.ny - 1;
+        const int64_t z0 = vz >= 2 ? vz - 2 : 0, z1 = vz + 1 < g.nz ? vz + 1 : g.nz - 1;
+        for (int64_t zz = z0; zz <= z1; zz++)
+          for (int64_t b = y0 / UY; b <= y1 / UY; b++) {
+            const int64_t unit = zz * rg.ub + b;
+            atomicOr(fr + (unit >> 5), 1u << (unit & 31));
+          }
+      }
+      const uint32_t st = state[v];
+      if (st >> 16) continue;  // lossless: no-op, but its cells stay in the frontier
+      changed++;
+      const uint32_t q = st & 0xFFFFu;
+      if ((int)q + 1 <= q_cap) {
+        // g' = RN(fhat - RN((q+1) * step)): two roundings, never fused
+        const float gp = __fsub_rn(fhat[v], __fmul_rn((float)(q + 1), step));
+        if (gp >= lb[v]) { state[v] = q + 1; gf[v] = gp; continue; }
+      }
+      gf[v] = lb[v];              // clamp to the lower bound, stored losslessly
+      state[v] = q | (1u << 16);
+    }
+  }
+  warp_add(&cnt->n_changed, changed);
+  warp_add(&cnt->n_targets, targets);
+  if (fwords_smem) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < fwords_smem; i += blockDim.x)
+      if (sfr[i]) atomicOr(next_frontier + i, sfr[i]);
+  }
+}
+
+// active unit list from the frontier bitmap (ordered compaction), count -> *n_out
+__global__ void k_units_from_bits(const uint32_t* __restrict__ fbits, int64_t n_units, uint32_t* __restrict__ list,
+                                  unsigned long long* __restrict__ n_out) {
+  // single pass with one atomic per warp; order inside the list does not matter
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) - lane; base < n_units;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t u = base + lane;
+    const bool on = u < n_units && ((fbits[u >> 5] >> (u & 31)) & 1u);
+    const unsigned bal = __ballot_sync(0xffffffffu, on);
+    unsigned long long pos = 0;
+    if (lane == 0 && bal) pos = atomicAdd(n_out, (unsigned long long)__popc(bal));
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    if (on) list[pos + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)u;
+  }
+}
+
+__global__ void k_units_all(int64_t n_units, uint32_t* __restrict__ list, unsigned long long* __restrict__ n_out) {
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n_units; u += (int64_t)gridDim.x * blockDim.x)
+    list[u] = (uint32_t)u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_out = (unsigned long long)n_units;
+}
+
+}  // namespace dmtz
