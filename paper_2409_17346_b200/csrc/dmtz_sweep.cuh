@@ -128,106 +128,116 @@ k_screen(const float* __restrict__ gfld, const typename Tr<D>::code_t* __restric
 }
 
 // ---------------------------------------------------------------------------
-// Static target rule of cell type T (twin of target_of in dmtz_kernels.cuh).
+// Target rules with shared-memory tables (one copy per CTA).  The false-cell
+// path is rare per anchor in late rounds but, in the first rounds of a dense
+// workload, runs ~5 times per anchor: a compact loop over the set bits of the
+// false mask keeps the code small.
 // ---------------------------------------------------------------------------
-template <int D, int T>
-__device__ __forceinline__ int64_t link_offset(const Grid& g, uint32_t s) {
-  int64_t off = 0;
+struct TargetTables {
+  uint32_t tinfo[26];      // dim | nv << 2 | shift << 5 | none << 11 | nfacet << 15
+  uint32_t vm[26];         // vertex delta masks, 3 bits each
+  uint32_t fac[26][4];     // dm | ft << 3 | slot << 8 | k << 12
+  int64_t loff[26][14];    // link slot -> linear offset
+  int64_t doff[8];         // delta mask -> linear offset
+};
+
+template <int D>
+__device__ __forceinline__ void init_target_tables(TargetTables& T, const Grid& g) {
+  if (threadIdx.x == 0) {
 #pragma unroll
-  for (int j = 0; j < 14; j++) {
-    if (j < t_nlink<D>(T) && s == (uint32_t)j)
-      off = t_link<D>(T, j, 0) + t_link<D>(T, j, 1) * g.sy + t_link<D>(T, j, 2) * g.sz;
+    for (int t = 0; t < Tr<D>::NT; t++) {
+      T.tinfo[t] = (uint32_t)t_dim<D>(t) | ((uint32_t)t_nv<D>(t) << 2) | ((uint32_t)t_shift<D>(t) << 5) |
+                   ((uint32_t)t_none<D>(t) << 11) | ((uint32_t)t_nfacet<D>(t) << 15);
+      uint32_t vm = 0;
+#pragma unroll
+      for (int k = 0; k < 4; k++) vm |= (uint32_t)t_vmask<D>(t, k) << (3 * k);
+      T.vm[t] = vm;
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+        T.fac[t][j] = (uint32_t)t_facet<D>(t, j, 0) | ((uint32_t)t_facet<D>(t, j, 1) << 3) |
+                      ((uint32_t)t_facet<D>(t, j, 2) << 8) | ((uint32_t)t_facet<D>(t, j, 3) << 12);
+#pragma unroll
+      for (int q = 0; q < 14; q++)
+        T.loff[t][q] = t_link<D>(t, q, 0) + t_link<D>(t, q, 1) * g.sy + t_link<D>(t, q, 2) * g.sz;
+    }
+#pragma unroll
+    for (int m = 0; m < 8; m++) T.doff[m] = mask_delta(g, m);
   }
-  return off;
+  __syncthreads();
 }
 
-template <int D, int T>
-__device__ __forceinline__ int64_t target_static(const float* __restrict__ f, const Grid& g, int64_t u,
-                                                 const uint64_t (&cf)[Tr<D>::NDELTA],
-                                                 const uint64_t (&cg)[Tr<D>::NDELTA], bool fn) {
-  constexpr int TOP = Tr<D>::TOP;
-  const int nv = t_nv<D>(T);
-  int64_t vid[4];
-  int64_t m = -1;
-  float fm = 0.f;
+template <int N>
+__device__ __forceinline__ uint64_t pick(const uint64_t (&c)[N], int i) {
+  uint64_t r = c[0];
 #pragma unroll
-  for (int k = 0; k < 4; k++) {
+  for (int k = 1; k < N; k++) r = (i == k) ? c[k] : r;
+  return r;
+}
+
+// Rules R1 / R2 / R3a / R3b for the false cell (u, t).
+template <int D>
+__device__ __forceinline__ int64_t target_dyn(const TargetTables& T, const float* __restrict__ f, int64_t u, int t,
+                                              bool fn, const uint64_t (&cf)[Tr<D>::NDELTA],
+                                              const uint64_t (&cg)[Tr<D>::NDELTA]) {
+  const uint32_t ti = T.tinfo[t];
+  const int dim = ti & 3, nv = (ti >> 2) & 7, shift = (ti >> 5) & 63, nfacet = (ti >> 15) & 7;
+  const uint32_t none = (ti >> 11) & 15;
+  const uint32_t vm = T.vm[t];
+  int64_t m = u, vid[4] = {u, u, u, u};
+  float fm = __ldg(f + u);
+#pragma unroll
+  for (int k = 1; k < 4; k++) {
     if (k < nv) {
-      vid[k] = u + mask_delta(g, t_vmask<D>(T, k));
+      vid[k] = u + T.doff[(vm >> (3 * k)) & 7];
       const float fv = __ldg(f + vid[k]);
-      if (k == 0 || sos_less(fv, vid[k], fm, m)) { m = vid[k]; fm = fv; }
+      if (sos_less(fv, vid[k], fm, m)) { m = vid[k]; fm = fv; }
     }
   }
-  if (!fn) {                                 // FP: paired in f, critical in g (R1)
-    if (t_dim<D>(T) < TOP) {
-      const uint32_t s = field_of<D>(cf[0], T);
-      if (s != (uint32_t)t_none<D>(T)) return u + link_offset<D, T>(g, s);
+  if (!fn) {                                        // FP: paired in f, critical in g (R1)
+    if (dim < Tr<D>::TOP) {
+      const uint32_t s = (uint32_t)(cf[0] >> shift) & none;
+      if (s != none) return u + T.loff[t][s];
     }
-    return m;                                // paired down in f: the f-lowest vertex
+    return m;                                       // paired down in f: the f-lowest vertex
   }
-  if (t_dim<D>(T) < TOP) {                   // FN paired up in g (R2)
-    if (field_of<D>(cg[0], T) != (uint32_t)t_none<D>(T)) return m;
-  }
-#pragma unroll
-  for (int j = 0; j < 4; j++) {              // FN paired down in g with gamma (R3a / R3b)
-    if (j >= t_nfacet<D>(T)) continue;
-    const int dm = t_facet<D>(T, j, 0), ft = t_facet<D>(T, j, 1), sl = t_facet<D>(T, j, 2), k = t_facet<D>(T, j, 3);
-    if (field_of<D>(cg[dm], ft) != (uint32_t)sl) continue;
-    if (m != vid[k]) return m;
-    const uint32_t s2 = field_of<D>(cf[dm], ft);
-    if (s2 == (uint32_t)t_none<D>(ft)) return -1;
-    int64_t off = 0;
-#pragma unroll
-    for (int q = 0; q < 14; q++)
-      if (q < t_nlink<D>(ft) && s2 == (uint32_t)q)
-        off = t_link<D>(ft, q, 0) + t_link<D>(ft, q, 1) * g.sy + t_link<D>(ft, q, 2) * g.sz;
-    return u + mask_delta(g, dm) + off;
+  if (dim < Tr<D>::TOP && ((uint32_t)(cg[0] >> shift) & none) != none) return m;   // R2
+  for (int j = 0; j < nfacet; j++) {                // paired down in g with gamma: R3a / R3b
+    const uint32_t fc = T.fac[t][j];
+    const int dm = fc & 7, ft = (fc >> 3) & 31, sl = (fc >> 8) & 15, k = (fc >> 12) & 3;
+    const uint32_t fti = T.tinfo[ft];
+    const int fsh = (fti >> 5) & 63;
+    const uint32_t fno = (fti >> 11) & 15;
+    if (((uint32_t)(pick(cg, dm) >> fsh) & fno) != (uint32_t)sl) continue;
+    const int64_t y = k == 0 ? vid[0] : k == 1 ? vid[1] : k == 2 ? vid[2] : vid[3];
+    if (m != y) return m;
+    const uint32_t s2 = (uint32_t)(pick(cf, dm) >> fsh) & fno;
+    if (s2 == fno) return -1;
+    return u + T.doff[dm] + T.loff[ft][s2];
   }
   return -1;
 }
 
-template <int D, int T>
-__device__ __forceinline__ void handle_type(uint32_t diff, uint32_t critf, const float* __restrict__ f,
-                                            const Grid& g, int64_t u, const uint64_t (&cf)[Tr<D>::NDELTA],
-                                            const uint64_t (&cg)[Tr<D>::NDELTA], uint32_t* __restrict__ tbits,
-                                            unsigned long long (&kinds)[8], unsigned long long& nint) {
-  if (!((diff >> T) & 1u)) return;
-  const bool fn = (critf >> T) & 1u;
-  const int d = t_dim<D>(T);
-  const int cls = (d == Tr<D>::TOP) ? 3 : d;
-  if (fn) kinds[2 * cls + 1]++;
-  else kinds[2 * cls]++;
-  const int64_t tv = target_static<D, T>(f, g, u, cf, cg, fn);
-  if (tv < 0) { nint++; return; }
-  atomicOr(tbits + (tv >> 5), 1u << (tv & 31));
-}
-
-template <int D, int... Ts>
-__device__ __forceinline__ void handle_all(std::integer_sequence<int, Ts...>, uint32_t diff, uint32_t critf,
-                                           const float* __restrict__ f, const Grid& g, int64_t u,
-                                           const uint64_t (&cf)[Tr<D>::NDELTA], const uint64_t (&cg)[Tr<D>::NDELTA],
-                                           uint32_t* __restrict__ tbits, unsigned long long (&kinds)[8],
-                                           unsigned long long& nint) {
-  (handle_type<D, Ts>(diff, critf, f, g, u, cf, cg, tbits, kinds, nint), ...);
-}
-
 // ---------------------------------------------------------------------------
 // k_decode: classification of the anchors whose code neighbourhood changed.
+// crit_f is precomputed once per call; crit_g is decoded from the codes at
+// u + {0,1}^D (cand_f where d = 0, the sparse cand_g buffer where d = 1).
 // ---------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(256)
 k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__ cand_f,
-         const typename Tr<D>::code_t* __restrict__ cg_buf, const uint32_t* __restrict__ dbits,
-         uint32_t* __restrict__ tbits, const uint32_t* __restrict__ units,
+         const uint32_t* __restrict__ crit_f, const typename Tr<D>::code_t* __restrict__ cg_buf,
+         const uint32_t* __restrict__ dbits, uint32_t* __restrict__ tbits, const uint32_t* __restrict__ units,
          const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg, uint32_t tier_mask,
          Counters* __restrict__ cnt) {
+  __shared__ TargetTables T;
+  init_target_tables<D>(T, g);
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t n_units = (int64_t)*n_units_p;
   const int64_t per_unit = (int64_t)UY * rg.wpr;
   const int64_t total = n_units * per_unit;
-  unsigned long long kinds[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long k0 = 0, k1 = 0, k2 = 0, k3 = 0, k4 = 0, k5 = 0, k6 = 0, k7 = 0;
   unsigned long long nfalse = 0, nint = 0;
   for (int64_t it = warp; it < total; it += nwarps) {
     const int64_t ui = it / per_unit, rem = it - ui * per_unit;
@@ -236,15 +246,15 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
     const int64_t c = rem % rg.wpr;
     if (y >= g.ny) continue;
     // need bits: d over u + {0,1}^D, i.e. rows (y, y+1) x planes (z, z+1), bits x and x+1
-    uint32_t need = 0;
+    uint32_t need = 0, drow[4] = {0, 0, 0, 0}, drow1[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int r = 0; r < (D == 3 ? 4 : 2); r++) {
       const int64_t yy = y + (r & 1), zz = z + (r >> 1);
       if (yy >= g.ny || zz >= g.nz) continue;
       const int64_t wi = dword_index(g, rg, yy, zz, c);
-      const uint32_t w0 = __ldg(dbits + wi);
-      const uint32_t w1 = (c + 1 < rg.wpr) ? __ldg(dbits + wi + 1) : 0u;
-      need |= w0 | (w0 >> 1) | (w1 << 31);
+      drow[r] = __ldg(dbits + wi);
+      drow1[r] = (c + 1 < rg.wpr) ? __ldg(dbits + wi + 1) : 0u;
+      need |= drow[r] | (drow[r] >> 1) | (drow1[r] << 31);
     }
     if (!need) continue;  // warp-uniform
     const int64_t x = c * 32 + lane;
@@ -257,20 +267,34 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
       if ((dm & ~ok) != 0) { cf[dm] = cg[dm] = Tr<D>::ALL_NONE; continue; }
       const int64_t w = u + mask_delta(g, dm);
       cf[dm] = (uint64_t)__ldg(cand_f + w);
-      const int64_t xx = x + (dm & 1), yy = y + ((dm >> 1) & 1), zz = z + ((dm >> 2) & 1);
-      const uint32_t wd = __ldg(dbits + dword_index(g, rg, yy, zz, xx >> 5));
-      cg[dm] = ((wd >> (xx & 31)) & 1u) ? (uint64_t)__ldg(cg_buf + w) : cf[dm];
+      const int r = ((dm >> 1) & 1) | (((dm >> 2) & 1) << 1);
+      const bool dset = (dm & 1) ? (lane < 31 ? ((drow[r] >> (lane + 1)) & 1u) : (drow1[r] & 1u))
+                                 : ((drow[r] >> lane) & 1u);
+      cg[dm] = dset ? (uint64_t)__ldg(cg_buf + w) : cf[dm];
     }
-    const uint32_t critf = decode_crit<D>(cf, ok), critg = decode_crit<D>(cg, ok);
-    const uint32_t diff = (critf ^ critg) & tier_mask;
+    const uint32_t critf = __ldg(crit_f + u), critg = decode_crit<D>(cg, ok);
+    uint32_t diff = (critf ^ critg) & tier_mask;
     if (!diff) continue;
     nfalse += __popc(diff);
-    handle_all<D>(std::make_integer_sequence<int, Tr<D>::NT>{}, diff, critf, f, g, u, cf, cg, tbits, kinds, nint);
+    while (diff) {
+      const int t = __ffs(diff) - 1;
+      diff &= diff - 1;
+      const bool fn = (critf >> t) & 1u;
+      const int dim = T.tinfo[t] & 3;
+      const int cls = (dim == Tr<D>::TOP) ? 3 : dim;
+      const int kind = 2 * cls + (fn ? 1 : 0);
+      k0 += kind == 0; k1 += kind == 1; k2 += kind == 2; k3 += kind == 3;
+      k4 += kind == 4; k5 += kind == 5; k6 += kind == 6; k7 += kind == 7;
+      const int64_t tv = target_dyn<D>(T, f, u, t, fn, cf, cg);
+      if (tv < 0) { nint++; continue; }
+      atomicOr(tbits + (tv >> 5), 1u << (tv & 31));
+    }
   }
   warp_add(&cnt->n_false, nfalse);
   warp_add(&cnt->n_internal, nint);
-#pragma unroll
-  for (int k = 0; k < 8; k++) warp_add(&cnt->kinds[k], kinds[k]);
+  warp_add(&cnt->kinds[0], k0); warp_add(&cnt->kinds[1], k1); warp_add(&cnt->kinds[2], k2);
+  warp_add(&cnt->kinds[3], k3); warp_add(&cnt->kinds[4], k4); warp_add(&cnt->kinds[5], k5);
+  warp_add(&cnt->kinds[6], k6); warp_add(&cnt->kinds[7], k7);
 }
 
 // ---------------------------------------------------------------------------
