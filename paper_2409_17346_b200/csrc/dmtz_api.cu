@@ -55,7 +55,8 @@ inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 // Workspace layout (offsets from the base, each 256-B aligned)
 struct Layout {
-  size_t cand_f, cand_g, crit_f, lb, state, tbits, counters, edit_bc, dbits, units, frontier, trace, total;
+  size_t cand_f, cand_g, crit_f, crit_g, lb, state, tbits, counters, edit_bc, ebits, fmark, units, frontier, trace,
+      total;
   int64_t fwords;  // frontier bitmap words (one bit per row-block unit)
 };
 
@@ -67,6 +68,7 @@ Layout layout_for(const dmtz_ctx* c) {
   L.cand_f = o; o += align_up(N * cs);
   L.cand_g = o; o += align_up(N * cs);
   L.crit_f = o; o += align_up(N * 4);
+  L.crit_g = o; o += align_up(N * 4);
   L.lb = o; o += align_up(N * 4);
   L.state = o; o += align_up(N * 4);
   L.tbits = o; o += align_up((N + 31) / 32 * 4 + 64);
@@ -74,7 +76,8 @@ Layout layout_for(const dmtz_ctx* c) {
   L.edit_bc = o; o += align_up(((N + EDIT_CHUNK - 1) / EDIT_CHUNK + 2) * 8);
   const RowGeom rg = row_geom(c->g);
   L.fwords = (rg.units + 31) / 32;
-  L.dbits = o; o += align_up((size_t)(c->g.nz * c->g.ny * rg.wpr) * 4 + 64);
+  L.ebits = o; o += align_up((size_t)(c->g.nz * c->g.ny * rg.wpr) * 4 + 64);
+  L.fmark = o; o += align_up((size_t)(c->g.nz * c->g.ny * rg.wpr) * 4 + 64);
   L.units = o; o += align_up((size_t)rg.units * 4);
   L.frontier = o; o += align_up(L.fwords * 4 + 64);
   L.trace = o; o += align_up(trace_scratch_bytes(c->g, c->D));
@@ -111,7 +114,7 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
   const Grid& g = c->g;
   using code_t = typename Tr<D>::code_t;
   code_t* cand_f = (code_t*)(ws + L.cand_f);
-  code_t* cand_g = (code_t*)(ws + L.cand_g);  // sparse: valid where the d bit is set
+  code_t* cand_g = (code_t*)(ws + L.cand_g);  // codes of g, memoized across rounds
   float* lb = (float*)(ws + L.lb);
   uint32_t* state = (uint32_t*)(ws + L.state);
   uint32_t* tbits = (uint32_t*)(ws + L.tbits);
@@ -153,7 +156,11 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
   const int64_t max_rounds = o->max_rounds > 0 ? o->max_rounds : g.N * (int64_t)(o->q_cap + 1);
   const uint32_t tmask = tier_mask<D>(o->tier);
   const RowGeom rg = row_geom(g);
-  uint32_t* dbits = (uint32_t*)(ws + L.dbits);
+  uint32_t* ebits = (uint32_t*)(ws + L.ebits);
+  uint32_t* fmark = (uint32_t*)(ws + L.fmark);
+  uint32_t* crit_g = (uint32_t*)(ws + L.crit_g);
+  const size_t rowbit_bytes = (size_t)(g.nz * g.ny * rg.wpr) * 4;
+  CK(cudaMemsetAsync(fmark, 0, rowbit_bytes, s));
   uint32_t* units = (uint32_t*)(ws + L.units);
   uint32_t* fbits = (uint32_t*)(ws + L.frontier);
   unsigned long long* n_units = &dc->n_units;
@@ -169,10 +176,11 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
     // a3: gradient of g (screened);  a4/a5: classify + mark targets;  a6: edit;  a7: frontier
     CK(cudaMemsetAsync(dc, 0, offsetof(Counters, first_nonfinite), s));
     if (frontier_mode) CK(cudaMemsetAsync(fbits, 0, L.fwords * 4, s));
+    if (frontier_mode && round > 1) CK(cudaMemsetAsync(ebits, 0, rowbit_bytes, s));
     if (o->profile) CK(cudaEventRecord(c->ev[0], s));
-    k_screen<D><<<sweep_blocks, 256, 0, s>>>(g_out, cand_f, cand_g, dbits, units, n_units, g, rg, dc);
-    k_decode<D><<<sweep_blocks, 256, 0, s>>>(f, cand_f, crit_f, cand_g, dbits, tbits, units, n_units, g, rg, tmask,
-                                             dc);
+    k_screen<D><<<sweep_blocks, 256, 0, s>>>(g_out, cand_g, ebits, units, n_units, g, rg, round == 1 ? 1 : 0, dc);
+    k_decode<D><<<sweep_blocks, 256, 0, s>>>(f, cand_f, crit_f, cand_g, crit_g, ebits, fmark, tbits, units, n_units,
+                                             g, rg, tmask, dc);
     if (o->profile) CK(cudaEventRecord(c->ev[1], s));
     k_edit_rows<D><<<wblocks, ethreads, frontier_mode ? fwords_smem * 4 : 0, s>>>(
         tbits, nwords, fhat, lb, g_out, state, dc, step, o->q_cap, frontier_mode ? fbits : nullptr, g, rg,

@@ -1,22 +1,22 @@
 // dmtz_sweep.cuh -- the round sweep of the C-loop (a3 + a4 + a5) for sm_100a.
 //
-// Work unit: a ROW BLOCK = UY consecutive y-rows of one z-plane (all x).  The
-// rounds process an on-device list of active units (the frontier, a7), so
-// late rounds touch only units near last round's edits.
+// Work unit: a ROW BLOCK = UY consecutive y-rows of one z-plane (all x).  Each
+// round processes an on-device list of active units (the frontier, a7): every
+// unit in round 1 and in full-sweep mode, afterwards only units meeting
+// v + [-2,1]^D for some target v of the previous round.
 //
-//  k_screen<D>  per anchor u of an active unit: cand_g(u) from the 3^D stencil
-//               of g (the local form of the gradient), compared
-//               with cand_f(u).  Writes the bit d(u) = [cand_g(u) != cand_f(u)]
-//               (row-padded bitmap, one word per 32 anchors of a row) and, where
-//               d(u) = 1, cand_g(u) into a sparse code buffer.  Both are
-//               memoized across rounds: an anchor outside the frontier keeps
-//               its stencil, hence its code.
-//  k_decode<D>  per anchor u of an active unit whose 2^D code neighbourhood
-//               u + {0,1}^D has a d bit set (a cell's criticality is a function
-//               of those codes): decode crit_f / crit_g, mark the false cells'
-//               targets (rules R1/R2/R3a/R3b, unrolled per cell type).
-//  k_edit_rows<D> Eq. 2 edits of the marked targets and the next frontier
-//               (units meeting v + [-2,1]^D for every target v).
+//  k_screen<D>  for every anchor u of an active unit: cand_g(u) from the 3^D
+//               stencil of g (the local form of the gradient).
+//               The dense code buffer cg keeps the previous round's codes; the
+//               bit e(u) = [code changed this round] goes to a row-padded bitmap
+//               (one word per 32 anchors of a row).
+//  k_decode<D>  for every anchor u of an active unit with a changed code in
+//               u + {0,1}^D (criticality is a function of those 8 codes) or
+//               with false cells last round: crit_g(u) (decoded, or memoized
+//               when no code around u changed), F(u) = crit_f(u) xor crit_g(u),
+//               and the targets of F(u) (rules R1/R2/R3a/R3b), OR-ed into the
+//               round's target bitmap with warp-aggregated atomics.
+//  k_edit_rows<D> Eq. 2 edits of the marked targets and the next frontier.
 #pragma once
 #include <utility>
 
@@ -87,14 +87,13 @@ __device__ __forceinline__ uint64_t cand_of(const float (&s)[27]) {
 }
 
 // ---------------------------------------------------------------------------
-// k_screen: codes of g + screening bits.  One warp per 32-anchor row chunk.
+// k_screen: codes of g; e(u) = code changed.  One warp per 32-anchor row chunk.
 // ---------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(256)
-k_screen(const float* __restrict__ gfld, const typename Tr<D>::code_t* __restrict__ cand_f,
-         typename Tr<D>::code_t* __restrict__ cg_buf, uint32_t* __restrict__ dbits,
+k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg, uint32_t* __restrict__ ebits,
          const uint32_t* __restrict__ units, const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg,
-         Counters* __restrict__ cnt) {
+         int first_round, Counters* __restrict__ cnt) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -109,20 +108,19 @@ k_screen(const float* __restrict__ gfld, const typename Tr<D>::code_t* __restric
     const int64_t c = rem % rg.wpr;
     if (y >= g.ny) continue;  // warp-uniform
     const int64_t x = c * 32 + lane;
-    bool d = false;
+    bool e = false;
     if (x < g.nx) {
       const int64_t v = x + y * g.sy + z * g.sz;
       float s[27];
       load_stencil<D>(gfld, g, v, x, y, z, s);
       const int ok = axes_ok(g, x, y, z);
-      const uint64_t cgv = cand_of<D>(s) | t_nonex_fill<D>(ok);
-      const uint64_t cfv = (uint64_t)__ldg(cand_f + v);
-      d = cgv != cfv;
-      if (d) cg_buf[v] = (typename Tr<D>::code_t)cgv;
+      const uint64_t code = cand_of<D>(s) | t_nonex_fill<D>(ok);
+      e = first_round || code != (uint64_t)cg[v];
+      if (e) cg[v] = (typename Tr<D>::code_t)code;
       swept++;
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, d);
-    if (lane == 0) dbits[dword_index(g, rg, y, z, c)] = bal;
+    const unsigned bal = __ballot_sync(0xffffffffu, e);
+    if (lane == 0) ebits[dword_index(g, rg, y, z, c)] = bal;
   }
   warp_add(&cnt->n_swept, swept);
 }
@@ -218,15 +216,15 @@ __device__ __forceinline__ int64_t target_dyn(const TargetTables& T, const float
 }
 
 // ---------------------------------------------------------------------------
-// k_decode: classification of the anchors whose code neighbourhood changed.
-// crit_f is precomputed once per call; crit_g is decoded from the codes at
-// u + {0,1}^D (cand_f where d = 0, the sparse cand_g buffer where d = 1).
+// k_decode: classification.  crit_f is precomputed once per call; crit_g is
+// memoized per anchor and re-decoded only where a code of u + {0,1}^D changed.
 // ---------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(256)
 k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__ cand_f,
-         const uint32_t* __restrict__ crit_f, const typename Tr<D>::code_t* __restrict__ cg_buf,
-         const uint32_t* __restrict__ dbits, uint32_t* __restrict__ tbits, const uint32_t* __restrict__ units,
+         const uint32_t* __restrict__ crit_f, const typename Tr<D>::code_t* __restrict__ cg,
+         uint32_t* __restrict__ crit_g, const uint32_t* __restrict__ ebits, uint32_t* __restrict__ fmark,
+         uint32_t* __restrict__ tbits, const uint32_t* __restrict__ units,
          const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg, uint32_t tier_mask,
          Counters* __restrict__ cnt) {
   __shared__ TargetTables T;
@@ -245,49 +243,69 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
     const int64_t z = unit / rg.ub, y = (unit - z * rg.ub) * UY + rem / rg.wpr;
     const int64_t c = rem % rg.wpr;
     if (y >= g.ny) continue;
-    // need bits: d over u + {0,1}^D, i.e. rows (y, y+1) x planes (z, z+1), bits x and x+1
-    uint32_t need = 0, drow[4] = {0, 0, 0, 0}, drow1[4] = {0, 0, 0, 0};
+    // changed codes in u + {0,1}^D: rows (y, y+1) x planes (z, z+1), bits x and x+1
+    uint32_t chg = 0;
 #pragma unroll
     for (int r = 0; r < (D == 3 ? 4 : 2); r++) {
       const int64_t yy = y + (r & 1), zz = z + (r >> 1);
       if (yy >= g.ny || zz >= g.nz) continue;
       const int64_t wi = dword_index(g, rg, yy, zz, c);
-      drow[r] = __ldg(dbits + wi);
-      drow1[r] = (c + 1 < rg.wpr) ? __ldg(dbits + wi + 1) : 0u;
-      need |= drow[r] | (drow[r] >> 1) | (drow1[r] << 31);
+      const uint32_t w0 = __ldg(ebits + wi);
+      const uint32_t w1 = (c + 1 < rg.wpr) ? __ldg(ebits + wi + 1) : 0u;
+      chg |= w0 | (w0 >> 1) | (w1 << 31);
     }
-    if (!need) continue;  // warp-uniform
+    const int64_t fwi = dword_index(g, rg, y, z, c);
+    const uint32_t had = fmark[fwi];
+    if (!(chg | had)) continue;  // warp-uniform
     const int64_t x = c * 32 + lane;
-    if (!((need >> lane) & 1u) || x >= g.nx) continue;
     const int64_t u = x + y * g.sy + z * g.sz;
-    const int ok = axes_ok(g, x, y, z);
-    uint64_t cf[Tr<D>::NDELTA], cg[Tr<D>::NDELTA];
+    const bool active = x < g.nx && (((chg | had) >> lane) & 1u);
+    uint32_t diff = 0, critf = 0;
+    uint64_t cf[Tr<D>::NDELTA], cgv[Tr<D>::NDELTA];
+    if (active) {
+      const int ok = axes_ok(g, x, y, z);
 #pragma unroll
-    for (int dm = 0; dm < Tr<D>::NDELTA; dm++) {
-      if ((dm & ~ok) != 0) { cf[dm] = cg[dm] = Tr<D>::ALL_NONE; continue; }
-      const int64_t w = u + mask_delta(g, dm);
-      cf[dm] = (uint64_t)__ldg(cand_f + w);
-      const int r = ((dm >> 1) & 1) | (((dm >> 2) & 1) << 1);
-      const bool dset = (dm & 1) ? (lane < 31 ? ((drow[r] >> (lane + 1)) & 1u) : (drow1[r] & 1u))
-                                 : ((drow[r] >> lane) & 1u);
-      cg[dm] = dset ? (uint64_t)__ldg(cg_buf + w) : cf[dm];
+      for (int dm = 0; dm < Tr<D>::NDELTA; dm++) {
+        if ((dm & ~ok) != 0) { cf[dm] = cgv[dm] = Tr<D>::ALL_NONE; continue; }
+        const int64_t w = u + mask_delta(g, dm);
+        cf[dm] = (uint64_t)__ldg(cand_f + w);
+        cgv[dm] = (uint64_t)__ldg(cg + w);
+      }
+      uint32_t cgm;
+      if ((chg >> lane) & 1u) {
+        cgm = decode_crit<D>(cgv, ok);
+        crit_g[u] = cgm;
+      } else {
+        cgm = crit_g[u];
+      }
+      critf = __ldg(crit_f + u);
+      diff = (critf ^ cgm) & tier_mask;
     }
-    const uint32_t critf = __ldg(crit_f + u), critg = decode_crit<D>(cg, ok);
-    uint32_t diff = (critf ^ critg) & tier_mask;
-    if (!diff) continue;
+    const unsigned fb = __ballot_sync(0xffffffffu, diff != 0);
+    if (lane == 0 && fb != had) fmark[fwi] = fb;
     nfalse += __popc(diff);
-    while (diff) {
-      const int t = __ffs(diff) - 1;
-      diff &= diff - 1;
-      const bool fn = (critf >> t) & 1u;
-      const int dim = T.tinfo[t] & 3;
-      const int cls = (dim == Tr<D>::TOP) ? 3 : dim;
-      const int kind = 2 * cls + (fn ? 1 : 0);
-      k0 += kind == 0; k1 += kind == 1; k2 += kind == 2; k3 += kind == 3;
-      k4 += kind == 4; k5 += kind == 5; k6 += kind == 6; k7 += kind == 7;
-      const int64_t tv = target_dyn<D>(T, f, u, t, fn, cf, cg);
-      if (tv < 0) { nint++; continue; }
-      atomicOr(tbits + (tv >> 5), 1u << (tv & 31));
+    // lockstep over the false cells of the 32 lanes; same-word targets merged per warp
+    while (__any_sync(0xffffffffu, diff != 0)) {
+      int64_t tv = -1;
+      if (diff) {
+        const int t = __ffs(diff) - 1;
+        diff &= diff - 1;
+        const bool fn = (critf >> t) & 1u;
+        const int dim = T.tinfo[t] & 3;
+        const int cls = (dim == Tr<D>::TOP) ? 3 : dim;
+        const int kind = 2 * cls + (fn ? 1 : 0);
+        k0 += kind == 0; k1 += kind == 1; k2 += kind == 2; k3 += kind == 3;
+        k4 += kind == 4; k5 += kind == 5; k6 += kind == 6; k7 += kind == 7;
+        tv = target_dyn<D>(T, f, u, t, fn, cf, cgv);
+        if (tv < 0) nint++;
+      }
+      const unsigned have = __ballot_sync(0xffffffffu, tv >= 0);
+      if (tv >= 0) {
+        const int64_t word = tv >> 5;
+        const unsigned same = __match_any_sync(have, word);
+        const uint32_t bits = __reduce_or_sync(same, 1u << (tv & 31));
+        if (lane == __ffs(same) - 1) atomicOr(tbits + word, bits);
+      }
     }
   }
   warp_add(&cnt->n_false, nfalse);
