@@ -40,6 +40,29 @@ __host__ __device__ inline RowGeom row_geom(const Grid& g) {
   return r;
 }
 
+// Work decomposition of the active units: item = (unit, row, group of CG row
+// chunks of 32 anchors); warps stride over items, 32-bit index arithmetic.
+constexpr int CG = 4;
+#define WORK_LOOP_BEGIN                                                                          \
+  {                                                                                              \
+    const uint32_t n_units_ = (uint32_t)*n_units_p;                                              \
+    const uint32_t ncg_ = (uint32_t)((rg.wpr + CG - 1) / CG);                                    \
+    const uint32_t per_unit_ = (uint32_t)UY * ncg_;                                              \
+    const uint64_t total_ = (uint64_t)n_units_ * per_unit_;                                      \
+    for (uint64_t it_ = (uint64_t)warp; it_ < total_; it_ += (uint64_t)nwarps) {                 \
+      const uint32_t ui_ = (uint32_t)(it_ / per_unit_), rem_ = (uint32_t)(it_ - (uint64_t)ui_ * per_unit_); \
+      const uint32_t unit_ = units[ui_];                                                         \
+      const uint32_t ub_ = (uint32_t)rg.ub;                                                      \
+      const int64_t z = unit_ / ub_;                                                             \
+      const int64_t y = (int64_t)(unit_ - (uint32_t)z * ub_) * UY + rem_ / ncg_;                 \
+      const int64_t c0_ = (int64_t)(rem_ % ncg_) * CG;                                           \
+      if (y >= g.ny) continue;                                                                   \
+      for (int64_t c = c0_; c < c0_ + CG && c < rg.wpr; c++) {
+#define WORK_LOOP_END \
+      }               \
+    }                 \
+  }
+
 // bit word of anchor row (y, z), x-chunk c
 __device__ __forceinline__ int64_t dword_index(const Grid& g, const RowGeom& rg, int64_t y, int64_t z, int64_t c) {
   return (z * g.ny + y) * rg.wpr + c;
@@ -97,16 +120,8 @@ k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t n_units = (int64_t)*n_units_p;
-  const int64_t per_unit = (int64_t)UY * rg.wpr;  // row chunks per unit
-  const int64_t total = n_units * per_unit;
   unsigned long long swept = 0;
-  for (int64_t it = warp; it < total; it += nwarps) {
-    const int64_t ui = it / per_unit, rem = it - ui * per_unit;
-    const int64_t unit = units[ui];
-    const int64_t z = unit / rg.ub, y = (unit - z * rg.ub) * UY + rem / rg.wpr;
-    const int64_t c = rem % rg.wpr;
-    if (y >= g.ny) continue;  // warp-uniform
+  WORK_LOOP_BEGIN
     const int64_t x = c * 32 + lane;
     bool e = false;
     if (x < g.nx) {
@@ -121,7 +136,7 @@ k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg
     }
     const unsigned bal = __ballot_sync(0xffffffffu, e);
     if (lane == 0) ebits[dword_index(g, rg, y, z, c)] = bal;
-  }
+  WORK_LOOP_END
   warp_add(&cnt->n_swept, swept);
 }
 
@@ -232,17 +247,9 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t n_units = (int64_t)*n_units_p;
-  const int64_t per_unit = (int64_t)UY * rg.wpr;
-  const int64_t total = n_units * per_unit;
   unsigned long long k0 = 0, k1 = 0, k2 = 0, k3 = 0, k4 = 0, k5 = 0, k6 = 0, k7 = 0;
   unsigned long long nfalse = 0, nint = 0;
-  for (int64_t it = warp; it < total; it += nwarps) {
-    const int64_t ui = it / per_unit, rem = it - ui * per_unit;
-    const int64_t unit = units[ui];
-    const int64_t z = unit / rg.ub, y = (unit - z * rg.ub) * UY + rem / rg.wpr;
-    const int64_t c = rem % rg.wpr;
-    if (y >= g.ny) continue;
+  WORK_LOOP_BEGIN
     // changed codes in u + {0,1}^D: rows (y, y+1) x planes (z, z+1), bits x and x+1
     uint32_t chg = 0;
 #pragma unroll
@@ -307,7 +314,7 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
         if (lane == __ffs(same) - 1) atomicOr(tbits + word, bits);
       }
     }
-  }
+  WORK_LOOP_END
   warp_add(&cnt->n_false, nfalse);
   warp_add(&cnt->n_internal, nint);
   warp_add(&cnt->kinds[0], k0); warp_add(&cnt->kinds[1], k1); warp_add(&cnt->kinds[2], k2);
