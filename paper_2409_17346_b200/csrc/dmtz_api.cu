@@ -179,7 +179,7 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
     if (frontier_mode && round > 1) CK(cudaMemsetAsync(ebits, 0, rowbit_bytes, s));
     if (o->profile) CK(cudaEventRecord(c->ev[0], s));
     k_screen<D><<<sweep_blocks, 256, 0, s>>>(g_out, cand_g, ebits, units, n_units, g, rg, round == 1 ? 1 : 0, dc);
-    k_decode<D><<<sweep_blocks, 256, 0, s>>>(f, cand_f, crit_f, cand_g, crit_g, ebits, fmark, tbits, units, n_units,
+    k_decode<D><<<sweep_blocks * 2, DECODE_THREADS, 0, s>>>(f, cand_f, crit_f, cand_g, crit_g, ebits, fmark, tbits, units, n_units,
                                              g, rg, tmask, dc);
     if (o->profile) CK(cudaEventRecord(c->ev[1], s));
     k_edit_rows<D><<<wblocks, ethreads, frontier_mode ? fwords_smem * 4 : 0, s>>>(

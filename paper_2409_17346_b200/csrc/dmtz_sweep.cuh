@@ -48,9 +48,9 @@ constexpr int CG = 4;
     const uint32_t n_units_ = (uint32_t)*n_units_p;                                              \
     const uint32_t ncg_ = (uint32_t)((rg.wpr + CG - 1) / CG);                                    \
     const uint32_t per_unit_ = (uint32_t)UY * ncg_;                                              \
-    const uint64_t total_ = (uint64_t)n_units_ * per_unit_;                                      \
-    for (uint64_t it_ = (uint64_t)warp; it_ < total_; it_ += (uint64_t)nwarps) {                 \
-      const uint32_t ui_ = (uint32_t)(it_ / per_unit_), rem_ = (uint32_t)(it_ - (uint64_t)ui_ * per_unit_); \
+    const uint32_t total_ = n_units_ * per_unit_;                                                \
+    for (uint32_t it_ = (uint32_t)warp; it_ < total_; it_ += (uint32_t)nwarps) {                 \
+      const uint32_t ui_ = it_ / per_unit_, rem_ = it_ - ui_ * per_unit_;                        \
       const uint32_t unit_ = units[ui_];                                                         \
       const uint32_t ub_ = (uint32_t)rg.ub;                                                      \
       const int64_t z = unit_ / ub_;                                                             \
@@ -187,11 +187,13 @@ __device__ __forceinline__ uint64_t pick(const uint64_t (&c)[N], int i) {
   return r;
 }
 
-// Rules R1 / R2 / R3a / R3b for the false cell (u, t).
+// Rules R1 / R2 / R3a / R3b for the false cell (u, t).  The
+// anchor's codes at u + {0,1}^D are read from the warp's shared-memory copy
+// (cfs[dm * 32 + src], cgs[dm * 32 + src]).
 template <int D>
 __device__ __forceinline__ int64_t target_dyn(const TargetTables& T, const float* __restrict__ f, int64_t u, int t,
-                                              bool fn, const uint64_t (&cf)[Tr<D>::NDELTA],
-                                              const uint64_t (&cg)[Tr<D>::NDELTA]) {
+                                              bool fn, const unsigned long long* cfs,
+                                              const unsigned long long* cgs, int src) {
   const uint32_t ti = T.tinfo[t];
   const int dim = ti & 3, nv = (ti >> 2) & 7, shift = (ti >> 5) & 63, nfacet = (ti >> 15) & 7;
   const uint32_t none = (ti >> 11) & 15;
@@ -208,22 +210,22 @@ __device__ __forceinline__ int64_t target_dyn(const TargetTables& T, const float
   }
   if (!fn) {                                        // FP: paired in f, critical in g (R1)
     if (dim < Tr<D>::TOP) {
-      const uint32_t s = (uint32_t)(cf[0] >> shift) & none;
-      if (s != none) return u + T.loff[t][s];
+      const uint32_t sl = (uint32_t)(cfs[src] >> shift) & none;
+      if (sl != none) return u + T.loff[t][sl];
     }
     return m;                                       // paired down in f: the f-lowest vertex
   }
-  if (dim < Tr<D>::TOP && ((uint32_t)(cg[0] >> shift) & none) != none) return m;   // R2
+  if (dim < Tr<D>::TOP && ((uint32_t)(cgs[src] >> shift) & none) != none) return m;   // R2
   for (int j = 0; j < nfacet; j++) {                // paired down in g with gamma: R3a / R3b
     const uint32_t fc = T.fac[t][j];
     const int dm = fc & 7, ft = (fc >> 3) & 31, sl = (fc >> 8) & 15, k = (fc >> 12) & 3;
     const uint32_t fti = T.tinfo[ft];
     const int fsh = (fti >> 5) & 63;
     const uint32_t fno = (fti >> 11) & 15;
-    if (((uint32_t)(pick(cg, dm) >> fsh) & fno) != (uint32_t)sl) continue;
+    if (((uint32_t)(cgs[dm * 32 + src] >> fsh) & fno) != (uint32_t)sl) continue;
     const int64_t y = k == 0 ? vid[0] : k == 1 ? vid[1] : k == 2 ? vid[2] : vid[3];
     if (m != y) return m;
-    const uint32_t s2 = (uint32_t)(pick(cf, dm) >> fsh) & fno;
+    const uint32_t s2 = (uint32_t)(cfs[dm * 32 + src] >> fsh) & fno;
     if (s2 == fno) return -1;
     return u + T.doff[dm] + T.loff[ft][s2];
   }
@@ -234,8 +236,16 @@ __device__ __forceinline__ int64_t target_dyn(const TargetTables& T, const float
 // k_decode: classification.  crit_f is precomputed once per call; crit_g is
 // memoized per anchor and re-decoded only where a code of u + {0,1}^D changed.
 // ---------------------------------------------------------------------------
+constexpr int DECODE_THREADS = 128;
+struct DecodeWarpSmem {
+  unsigned long long cf[8 * 32];
+  unsigned long long cg[8 * 32];
+  uint32_t critf[32];
+  uint16_t items[32 * 26];
+};
+
 template <int D>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(DECODE_THREADS)
 k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__ cand_f,
          const uint32_t* __restrict__ crit_f, const typename Tr<D>::code_t* __restrict__ cg,
          uint32_t* __restrict__ crit_g, const uint32_t* __restrict__ ebits, uint32_t* __restrict__ fmark,
@@ -243,8 +253,10 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
          const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg, uint32_t tier_mask,
          Counters* __restrict__ cnt) {
   __shared__ TargetTables T;
+  __shared__ DecodeWarpSmem WS[DECODE_THREADS / 32];
   init_target_tables<D>(T, g);
   const int lane = threadIdx.x & 31;
+  DecodeWarpSmem& W = WS[threadIdx.x >> 5];
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long k0 = 0, k1 = 0, k2 = 0, k3 = 0, k4 = 0, k5 = 0, k6 = 0, k7 = 0;
@@ -269,6 +281,8 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
     const bool active = x < g.nx && (((chg | had) >> lane) & 1u);
     uint32_t diff = 0, critf = 0;
     uint64_t cf[Tr<D>::NDELTA], cgv[Tr<D>::NDELTA];
+#pragma unroll
+    for (int dm = 0; dm < Tr<D>::NDELTA; dm++) cf[dm] = cgv[dm] = Tr<D>::ALL_NONE;
     if (active) {
       const int ok = axes_ok(g, x, y, z);
 #pragma unroll
@@ -290,20 +304,44 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
     }
     const unsigned fb = __ballot_sync(0xffffffffu, diff != 0);
     if (lane == 0 && fb != had) fmark[fwi] = fb;
-    nfalse += __popc(diff);
-    // lockstep over the false cells of the 32 lanes; same-word targets merged per warp
-    while (__any_sync(0xffffffffu, diff != 0)) {
+    if (!fb) continue;  // warp-uniform
+    // warp work list of the false cells (source lane, type): all lanes then share them
+    const int nmine = __popc(diff);
+    nfalse += nmine;
+    int pre = nmine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= o) pre += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, pre, 31);
+    pre -= nmine;
+    if (diff) {
+#pragma unroll
+      for (int dm = 0; dm < Tr<D>::NDELTA; dm++) { W.cf[dm * 32 + lane] = cf[dm]; W.cg[dm * 32 + lane] = cgv[dm]; }
+      W.critf[lane] = critf;
+      uint32_t dd = diff;
+      for (int k = 0; dd; k++) {
+        const int t = __ffs(dd) - 1;
+        dd &= dd - 1;
+        W.items[pre + k] = (uint16_t)(lane | (t << 5));
+      }
+    }
+    __syncwarp();
+    const int64_t ubase = u - lane;
+    for (int i0 = 0; i0 < total; i0 += 32) {
+      const int i = i0 + lane;
       int64_t tv = -1;
-      if (diff) {
-        const int t = __ffs(diff) - 1;
-        diff &= diff - 1;
-        const bool fn = (critf >> t) & 1u;
+      if (i < total) {
+        const int item = W.items[i];
+        const int src = item & 31, t = item >> 5;
+        const bool fn = (W.critf[src] >> t) & 1u;
         const int dim = T.tinfo[t] & 3;
         const int cls = (dim == Tr<D>::TOP) ? 3 : dim;
         const int kind = 2 * cls + (fn ? 1 : 0);
         k0 += kind == 0; k1 += kind == 1; k2 += kind == 2; k3 += kind == 3;
         k4 += kind == 4; k5 += kind == 5; k6 += kind == 6; k7 += kind == 7;
-        tv = target_dyn<D>(T, f, u, t, fn, cf, cgv);
+        tv = target_dyn<D>(T, f, ubase + src, t, fn, W.cf, W.cg, src);
         if (tv < 0) nint++;
       }
       const unsigned have = __ballot_sync(0xffffffffu, tv >= 0);
@@ -314,6 +352,7 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
         if (lane == __ffs(same) - 1) atomicOr(tbits + word, bits);
       }
     }
+    __syncwarp();
   WORK_LOOP_END
   warp_add(&cnt->n_false, nfalse);
   warp_add(&cnt->n_internal, nint);
