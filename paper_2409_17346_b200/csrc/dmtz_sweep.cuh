@@ -261,21 +261,45 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long k0 = 0, k1 = 0, k2 = 0, k3 = 0, k4 = 0, k5 = 0, k6 = 0, k7 = 0;
   unsigned long long nfalse = 0, nint = 0;
-  WORK_LOOP_BEGIN
-    // changed codes in u + {0,1}^D: rows (y, y+1) x planes (z, z+1), bits x and x+1
-    uint32_t chg = 0;
+  // items = (unit, row, group of 32 row chunks); lane j of the warp first scans
+  // chunk c0 + j (changed-code words of u + {0,1}^D and the false-cell mark),
+  // then the warp processes the chunks that need work, lanes = the 32 anchors.
+  const uint32_t n_units_ = (uint32_t)*n_units_p;
+  const uint32_t ngr = (uint32_t)((rg.wpr + 31) / 32);
+  const uint32_t per_unit_ = (uint32_t)UY * ngr;
+  const uint32_t total_ = n_units_ * per_unit_;
+  for (uint32_t it_ = (uint32_t)warp; it_ < total_; it_ += (uint32_t)nwarps) {
+    const uint32_t ui_ = it_ / per_unit_, rem_ = it_ - ui_ * per_unit_;
+    const uint32_t unit_ = units[ui_];
+    const uint32_t ub_ = (uint32_t)rg.ub;
+    const int64_t z = unit_ / ub_;
+    const int64_t y = (int64_t)(unit_ - (uint32_t)z * ub_) * UY + rem_ / ngr;
+    if (y >= g.ny) continue;  // warp-uniform
+    const int64_t cbase = (int64_t)(rem_ % ngr) * 32;
+    uint32_t chg_l = 0, had_l = 0;
+    {
+      const int64_t cl = cbase + lane;
+      if (cl < rg.wpr) {
 #pragma unroll
-    for (int r = 0; r < (D == 3 ? 4 : 2); r++) {
-      const int64_t yy = y + (r & 1), zz = z + (r >> 1);
-      if (yy >= g.ny || zz >= g.nz) continue;
-      const int64_t wi = dword_index(g, rg, yy, zz, c);
-      const uint32_t w0 = __ldg(ebits + wi);
-      const uint32_t w1 = (c + 1 < rg.wpr) ? __ldg(ebits + wi + 1) : 0u;
-      chg |= w0 | (w0 >> 1) | (w1 << 31);
+        for (int r = 0; r < (D == 3 ? 4 : 2); r++) {
+          const int64_t yy = y + (r & 1), zz = z + (r >> 1);
+          if (yy >= g.ny || zz >= g.nz) continue;
+          const int64_t wi = dword_index(g, rg, yy, zz, cl);
+          const uint32_t w0 = __ldg(ebits + wi);
+          const uint32_t w1 = (cl + 1 < rg.wpr) ? __ldg(ebits + wi + 1) : 0u;
+          chg_l |= w0 | (w0 >> 1) | (w1 << 31);
+        }
+        had_l = fmark[dword_index(g, rg, y, z, cl)];
+      }
     }
-    const int64_t fwi = dword_index(g, rg, y, z, c);
-    const uint32_t had = fmark[fwi];
-    if (!(chg | had)) continue;  // warp-uniform
+    unsigned todo = __ballot_sync(0xffffffffu, (chg_l | had_l) != 0);
+    while (todo) {
+      const int j = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int64_t c = cbase + j;
+      const uint32_t chg = __shfl_sync(0xffffffffu, chg_l, j);
+      const uint32_t had = __shfl_sync(0xffffffffu, had_l, j);
+      const int64_t fwi = dword_index(g, rg, y, z, c);
     const int64_t x = c * 32 + lane;
     const int64_t u = x + y * g.sy + z * g.sz;
     const bool active = x < g.nx && (((chg | had) >> lane) & 1u);
@@ -304,7 +328,7 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
     }
     const unsigned fb = __ballot_sync(0xffffffffu, diff != 0);
     if (lane == 0 && fb != had) fmark[fwi] = fb;
-    if (!fb) continue;  // warp-uniform
+    if (!fb) continue;  // warp-uniform (next chunk of this row)
     // warp work list of the false cells (source lane, type): all lanes then share them
     const int nmine = __popc(diff);
     nfalse += nmine;
@@ -353,7 +377,8 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
       }
     }
     __syncwarp();
-  WORK_LOOP_END
+    }
+  }
   warp_add(&cnt->n_false, nfalse);
   warp_add(&cnt->n_internal, nint);
   warp_add(&cnt->kinds[0], k0); warp_add(&cnt->kinds[1], k1); warp_add(&cnt->kinds[2], k2);
