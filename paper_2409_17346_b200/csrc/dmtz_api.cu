@@ -55,7 +55,7 @@ inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 // Workspace layout (offsets from the base, each 256-B aligned)
 struct Layout {
-  size_t cand_f, cand_g, crit_f, crit_g, lb, state, tbits, counters, edit_bc, ebits, fmark, units, frontier, trace,
+  size_t cand_f, cand_g, crit_f, crit_g, lowpos, lb, state, tbits, counters, edit_bc, ebits, fmark, units, frontier, trace,
       total;
   int64_t fwords;  // frontier bitmap words (one bit per row-block unit)
 };
@@ -69,6 +69,7 @@ Layout layout_for(const dmtz_ctx* c) {
   L.cand_g = o; o += align_up(N * cs);
   L.crit_f = o; o += align_up(N * 4);
   L.crit_g = o; o += align_up(N * 4);
+  L.lowpos = o; o += align_up(N * 8);
   L.lb = o; o += align_up(N * 4);
   L.state = o; o += align_up(N * 4);
   L.tbits = o; o += align_up((N + 31) / 32 * 4 + 64);
@@ -149,7 +150,9 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
   launch_codes<D>(g, f, cand_f, 0, g.nz, s);
   uint32_t* crit_f = (uint32_t*)(ws + L.crit_f);
   k_critmask<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(cand_f, crit_f, g);
-  st->launches += 2;
+  unsigned long long* lowpos = (unsigned long long*)(ws + L.lowpos);
+  k_lowpos<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(f, lowpos, g);
+  st->launches += 3;
   CK(cudaGetLastError());
 
   const float step = ldexpf(o->xi, -o->q_max);   // xi / 2^q_max, exact
@@ -180,7 +183,7 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
     if (o->profile) CK(cudaEventRecord(c->ev[0], s));
     k_screen<D><<<sweep_blocks, 256, 0, s>>>(g_out, cand_g, ebits, units, n_units, g, rg, round == 1 ? 1 : 0, dc);
     k_decode<D><<<sweep_blocks * 2, DECODE_THREADS, 0, s>>>(f, cand_f, crit_f, cand_g, crit_g, ebits, fmark, tbits, units, n_units,
-                                             g, rg, tmask, dc);
+                                             g, rg, tmask, lowpos, round == 1 ? 1 : 0, dc);
     if (o->profile) CK(cudaEventRecord(c->ev[1], s));
     k_edit_rows<D><<<wblocks, ethreads, frontier_mode ? fwords_smem * 4 : 0, s>>>(
         tbits, nwords, fhat, lb, g_out, state, dc, step, o->q_cap, frontier_mode ? fbits : nullptr, g, rg,

@@ -191,23 +191,16 @@ __device__ __forceinline__ uint64_t pick(const uint64_t (&c)[N], int i) {
 // anchor's codes at u + {0,1}^D are read from the warp's shared-memory copy
 // (cfs[dm * 32 + src], cgs[dm * 32 + src]).
 template <int D>
-__device__ __forceinline__ int64_t target_dyn(const TargetTables& T, const float* __restrict__ f, int64_t u, int t,
-                                              bool fn, const unsigned long long* cfs,
-                                              const unsigned long long* cgs, int src) {
+__device__ __forceinline__ int64_t target_dyn(const TargetTables& T, int64_t u, int t, bool fn, uint64_t lowpos,
+                                              const unsigned long long* cfs, const unsigned long long* cgs,
+                                              int src) {
   const uint32_t ti = T.tinfo[t];
-  const int dim = ti & 3, nv = (ti >> 2) & 7, shift = (ti >> 5) & 63, nfacet = (ti >> 15) & 7;
+  const int dim = ti & 3, shift = (ti >> 5) & 63, nfacet = (ti >> 15) & 7;
   const uint32_t none = (ti >> 11) & 15;
   const uint32_t vm = T.vm[t];
-  int64_t m = u, vid[4] = {u, u, u, u};
-  float fm = __ldg(f + u);
-#pragma unroll
-  for (int k = 1; k < 4; k++) {
-    if (k < nv) {
-      vid[k] = u + T.doff[(vm >> (3 * k)) & 7];
-      const float fv = __ldg(f + vid[k]);
-      if (sos_less(fv, vid[k], fm, m)) { m = vid[k]; fm = fv; }
-    }
-  }
+  // m = the f-lowest vertex of the cell (SoS), precomputed per anchor and type
+  const int mp = (int)(lowpos >> (2 * t)) & 3;
+  const int64_t m = u + T.doff[(vm >> (3 * mp)) & 7];
   if (!fn) {                                        // FP: paired in f, critical in g (R1)
     if (dim < Tr<D>::TOP) {
       const uint32_t sl = (uint32_t)(cfs[src] >> shift) & none;
@@ -223,8 +216,7 @@ __device__ __forceinline__ int64_t target_dyn(const TargetTables& T, const float
     const int fsh = (fti >> 5) & 63;
     const uint32_t fno = (fti >> 11) & 15;
     if (((uint32_t)(cgs[dm * 32 + src] >> fsh) & fno) != (uint32_t)sl) continue;
-    const int64_t y = k == 0 ? vid[0] : k == 1 ? vid[1] : k == 2 ? vid[2] : vid[3];
-    if (m != y) return m;
+    if (mp != k) return m;                          // R3a: y = the vertex omitted by gamma
     const uint32_t s2 = (uint32_t)(cfs[dm * 32 + src] >> fsh) & fno;
     if (s2 == fno) return -1;
     return u + T.doff[dm] + T.loff[ft][s2];
@@ -240,18 +232,19 @@ constexpr int DECODE_THREADS = 128;
 struct DecodeWarpSmem {
   unsigned long long cf[8 * 32];
   unsigned long long cg[8 * 32];
+  unsigned long long lowpos[32];
   uint32_t critf[32];
   uint16_t items[32 * 26];
 };
 
 template <int D>
-__global__ void __launch_bounds__(DECODE_THREADS)
+__global__ void __launch_bounds__(DECODE_THREADS, 5)
 k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__ cand_f,
          const uint32_t* __restrict__ crit_f, const typename Tr<D>::code_t* __restrict__ cg,
          uint32_t* __restrict__ crit_g, const uint32_t* __restrict__ ebits, uint32_t* __restrict__ fmark,
          uint32_t* __restrict__ tbits, const uint32_t* __restrict__ units,
          const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg, uint32_t tier_mask,
-         Counters* __restrict__ cnt) {
+         const unsigned long long* __restrict__ lowpos_f, int count_kinds, Counters* __restrict__ cnt) {
   __shared__ TargetTables T;
   __shared__ DecodeWarpSmem WS[DECODE_THREADS / 32];
   init_target_tables<D>(T, g);
@@ -344,6 +337,7 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
 #pragma unroll
       for (int dm = 0; dm < Tr<D>::NDELTA; dm++) { W.cf[dm * 32 + lane] = cf[dm]; W.cg[dm * 32 + lane] = cgv[dm]; }
       W.critf[lane] = critf;
+      W.lowpos[lane] = __ldg(lowpos_f + u);
       uint32_t dd = diff;
       for (int k = 0; dd; k++) {
         const int t = __ffs(dd) - 1;
@@ -360,12 +354,14 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
         const int item = W.items[i];
         const int src = item & 31, t = item >> 5;
         const bool fn = (W.critf[src] >> t) & 1u;
-        const int dim = T.tinfo[t] & 3;
-        const int cls = (dim == Tr<D>::TOP) ? 3 : dim;
-        const int kind = 2 * cls + (fn ? 1 : 0);
-        k0 += kind == 0; k1 += kind == 1; k2 += kind == 2; k3 += kind == 3;
-        k4 += kind == 4; k5 += kind == 5; k6 += kind == 6; k7 += kind == 7;
-        tv = target_dyn<D>(T, f, ubase + src, t, fn, W.cf, W.cg, src);
+        if (count_kinds) {
+          const int dim = T.tinfo[t] & 3;
+          const int cls = (dim == Tr<D>::TOP) ? 3 : dim;
+          const int kind = 2 * cls + (fn ? 1 : 0);
+          k0 += kind == 0; k1 += kind == 1; k2 += kind == 2; k3 += kind == 3;
+          k4 += kind == 4; k5 += kind == 5; k6 += kind == 6; k7 += kind == 7;
+        }
+        tv = target_dyn<D>(T, ubase + src, t, fn, W.lowpos[src], W.cf, W.cg, src);
         if (tv < 0) nint++;
       }
       const unsigned have = __ballot_sync(0xffffffffu, tv >= 0);
@@ -447,6 +443,40 @@ __global__ void k_edit_rows(uint32_t* __restrict__ tbits, int64_t nwords, const 
     __syncthreads();
     for (int i = threadIdx.x; i < fwords_smem; i += blockDim.x)
       if (sfr[i]) atomicOr(next_frontier + i, sfr[i]);
+  }
+}
+
+// Per anchor and cell type: position (in the type's vertex list) of the cell's
+// lowest vertex under f in the SoS order -- 2 bits per type.  Computed
+// once per call; the target rules read it instead of re-sorting f.
+template <int D>
+__global__ void k_lowpos(const float* __restrict__ f, unsigned long long* __restrict__ out, Grid g) {
+  const float INF = __int_as_float(0x7f800000);
+  DMTZ_FOR_ANCHORS(g, 0, g.nz) {
+    const int64_t v = x + y * g.sy + z * g.sz;
+    const int ok = axes_ok(g, x, y, z);
+    float c[8];
+#pragma unroll
+    for (int dm = 0; dm < 8; dm++) {
+      if (D == 2 && dm >= 4) { c[dm] = INF; continue; }
+      c[dm] = ((dm & ~ok) == 0) ? __ldg(f + v + mask_delta(g, dm)) : INF;
+    }
+    uint64_t w = 0;
+#pragma unroll
+    for (int t = 0; t < Tr<D>::NT; t++) {
+      int best = 0;
+      float fb = c[t_vmask<D>(t, 0)];
+#pragma unroll
+      for (int k = 1; k < 4; k++) {
+        if (k < t_nv<D>(t)) {
+          // vertices are listed in ascending index order: ties keep the earlier one
+          const float fv = c[t_vmask<D>(t, k)];
+          if (fv < fb) { fb = fv; best = k; }
+        }
+      }
+      w |= (uint64_t)best << (2 * t);
+    }
+    out[v] = w;
   }
 }
 
