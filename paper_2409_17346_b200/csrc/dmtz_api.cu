@@ -66,7 +66,7 @@ Layout layout_for(const dmtz_ctx* c) {
   Layout L;
   size_t o = 0;
   L.cand_f = o; o += align_up(N * cs);
-  L.cand_g = o; o += align_up(N * cs);
+  L.cand_g = o; o += align_up(N * 8);  // u64 even in 2D: the trace reuses it as int64 scratch
   L.crit_f = o; o += align_up(N * 4);
   L.crit_g = o; o += align_up(N * 4);
   L.lowpos = o; o += align_up(N * 8);
@@ -372,7 +372,11 @@ dmtz_status dmtz_trace_separatrices(dmtz_ctx* c, const void* codes, uint32_t kin
   a.g = c->g;
   a.codes = codes;
   a.kinds = kinds;
-  a.scratch = ws + L.trace;
+  a.pre = (long long*)(ws + L.cand_g);
+  a.bfs = (unsigned long long*)(ws + L.lowpos);
+  a.bfs_bytes = (size_t)c->g.N * 8;
+  a.crit = (uint32_t*)(ws + L.crit_g);
+  a.bsum = (unsigned long long*)(ws + L.edit_bc);
   a.cnt = (Counters*)(ws + L.counters);
   a.host_cnt = c->host_cnt;
   a.out_offsets = out->branch_offsets;

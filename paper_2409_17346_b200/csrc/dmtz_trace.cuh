@@ -1,7 +1,22 @@
-// dmtz_trace.cuh -- V-path separatrix traces (a9-a11), see include/dmtz.h.
+// dmtz_trace.cuh -- V-path separatrix traces (a9-a11) for sm_100a; see include/dmtz.h.
+//
+// Gradient paths from the saddles, on the gradient given as codes:
+//   DESC  vertex -> paired edge -> other vertex ... -> minimum      (pointer chase)
+//   ASC   top cell -> paired facet -> other top cofacet ... -> maximum | BOUNDARY
+//   CONN  breadth-first over triangle -> facet edge -> paired triangle (3D)
+// Layout of the work:
+//   1. crit masks of the codes (k_critmask)
+//   2. per kind: per-anchor branch counts -> exclusive scan -> emit branch
+//      descriptors (origin id, kind, branch index j) in (origin id, j) order
+//   3. per branch: walk once to count cells -> scan -> walk again writing cells
+// One thread per branch for the walks; connector BFS runs per saddle with a
+// private queue + open-addressing visited set in workspace scratch (saddles
+// whose search outgrows the slot are redone alone with the whole scratch).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <vector>
 
 #include "dmtz_kernels.cuh"
 
@@ -11,7 +26,11 @@ struct TraceArgs {
   Grid g;
   const void* codes;
   uint32_t kinds;
-  char* scratch;
+  long long* pre;            // N x 8 B workspace region: per-anchor branch counts, then overflow flags
+  unsigned long long* bfs;   // N x 8 B workspace region: connector BFS slots (zeroed, self-cleaning)
+  size_t bfs_bytes;
+  uint32_t* crit;            // N x 4 B workspace region
+  unsigned long long* bsum;  // scan block sums (>= N / 8192 + 2 entries)
   Counters* cnt;
   Counters* host_cnt;
   int64_t* out_offsets;
@@ -23,11 +42,445 @@ struct TraceArgs {
   int64_t n_branches = 0, n_cells = 0, n_internal = 0;
 };
 
-inline size_t trace_scratch_bytes(const Grid&, int) { return 0; }
+constexpr uint64_t CELL_BOUNDARY = ~0ull;
+constexpr int SCAN_CHUNK = 8192;
+
+template <int D> __host__ __device__ constexpr int types_of_dim(int d) {
+  return D == 3 ? (d == 0 ? 1 : d == 1 ? 7 : d == 2 ? 12 : 6) : (d == 0 ? 1 : d == 1 ? 3 : 2);
+}
 
 template <int D>
-cudaError_t run_trace(TraceArgs&, cudaStream_t) {
-  return cudaErrorNotSupported;
+__device__ __forceinline__ uint64_t cell_id(int64_t anchor, int t) {
+  const int d = t_dim<D>(t);
+  const int k = t - t_first_of_dim<D>(d);
+  return ((uint64_t)d << 56) | (uint64_t)(anchor * types_of_dim<D>(d) + k);
+}
+
+template <int D>
+__device__ __forceinline__ uint64_t code_at(const void* codes, int64_t a) {
+  return D == 3 ? (uint64_t)((const unsigned long long*)codes)[a] : (uint64_t)((const unsigned short*)codes)[a];
+}
+
+__device__ __forceinline__ void coords_of(const Grid& g, int64_t v, int64_t& x, int64_t& y, int64_t& z) {
+  z = v / g.sz;
+  const int64_t r = v - z * g.sz;
+  y = r / g.nx;
+  x = r - y * g.nx;
+}
+
+template <int D>
+__device__ __forceinline__ bool link_in_grid(const Grid& g, int64_t a, int t, int s) {
+  int64_t x, y, z;
+  coords_of(g, a, x, y, z);
+  x += t_link<D>(t, s, 0);
+  y += t_link<D>(t, s, 1);
+  z += t_link<D>(t, s, 2);
+  return x >= 0 && y >= 0 && z >= 0 && x < g.nx && y < g.ny && z < g.nz;
+}
+
+template <int D>
+__device__ __forceinline__ int64_t cof_anchor(const Grid& g, int64_t a, int t, int s) {
+  return a + t_cof_anchor<D>(t, s, 0) + t_cof_anchor<D>(t, s, 1) * g.sy + t_cof_anchor<D>(t, s, 2) * g.sz;
+}
+
+// facet of top cell (B, bt) paired with it (its code points at B), or -1 if critical
+template <int D>
+__device__ __forceinline__ int paired_facet(const void* codes, const Grid& g, int64_t B, int bt, int64_t& fa,
+                                            int& ftype) {
+  for (int j = 0; j < t_nfacet<D>(bt); j++) {
+    const int dm = t_facet<D>(bt, j, 0), ft = t_facet<D>(bt, j, 1), sl = t_facet<D>(bt, j, 2);
+    const int64_t a = B + mask_delta(g, dm);
+    if (field_of<D>(code_at<D>(codes, a), ft) == (uint32_t)sl) { fa = a; ftype = ft; return j; }
+  }
+  return -1;
+}
+
+// ----------------------------------------------------------------------------- counting / emission
+template <int D>
+__device__ __forceinline__ int branch_count(const Grid& g, int kind, uint32_t cm, int64_t a) {
+  const int top = Tr<D>::TOP;
+  if (kind == 1) {  // DESC: two branches per critical edge
+    const uint32_t em = ((1u << t_first_of_dim<D>(2)) - 1u) & ~1u;
+    return 2 * __popc(cm & em);
+  }
+  if (kind == 2) {  // ASC: one branch per in-grid top cofacet of each critical (top-1)-cell
+    int n = 0;
+    for (int t = t_first_of_dim<D>(top - 1); t < t_first_of_dim<D>(top); t++) {
+      if (!((cm >> t) & 1u)) continue;
+      for (int s = 0; s < t_nlink<D>(t); s++) n += link_in_grid<D>(g, a, t, s) ? 1 : 0;
+    }
+    return n;
+  }
+  // CONN: one branch per critical triangle (3D)
+  if (D != 3) return 0;
+  const uint32_t tm = ((1u << t_first_of_dim<D>(3)) - 1u) & ~((1u << t_first_of_dim<D>(2)) - 1u);
+  return __popc(cm & tm);
+}
+
+template <int D>
+__global__ void k_branch_count(const uint32_t* __restrict__ crit, long long* __restrict__ cnt_out, Grid g, int kind) {
+  DMTZ_FOR_ANCHORS(g, 0, g.nz) {
+    const int64_t a = x + y * g.sy + z * g.sz;
+    cnt_out[a] = branch_count<D>(g, kind, crit[a], a);
+  }
+}
+
+// exclusive scan helpers (int64, in place); block sums -> one-block scan -> apply
+__global__ void k_scan_local(long long* __restrict__ a, int64_t n, unsigned long long* __restrict__ bsum) {
+  __shared__ long long part[1024];
+  const int64_t base = (int64_t)blockIdx.x * SCAN_CHUNK;
+  const int per = SCAN_CHUNK / 1024;
+  long long s = 0;
+  for (int k = 0; k < per; k++) {
+    const int64_t i = base + threadIdx.x * per + k;
+    if (i < n) s += a[i];
+  }
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    long long v = threadIdx.x >= (unsigned)o ? part[threadIdx.x - o] : 0;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  long long run = part[threadIdx.x] - s;  // exclusive within block
+  for (int k = 0; k < per; k++) {
+    const int64_t i = base + threadIdx.x * per + k;
+    if (i < n) { const long long v = a[i]; a[i] = run; run += v; }
+  }
+  if (threadIdx.x == 1023) bsum[blockIdx.x] = (unsigned long long)part[1023];
+}
+
+__global__ void k_scan_top(unsigned long long* __restrict__ bsum, int64_t nb, unsigned long long* __restrict__ total) {
+  if (threadIdx.x == 0) {
+    unsigned long long acc = 0;
+    for (int64_t i = 0; i < nb; i++) { const unsigned long long v = bsum[i]; bsum[i] = acc; acc += v; }
+    *total = acc;
+  }
+}
+
+__global__ void k_scan_add(long long* __restrict__ a, int64_t n, const unsigned long long* __restrict__ bsum) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] += (long long)bsum[i / SCAN_CHUNK];
+}
+
+template <int D>
+__global__ void k_branch_emit(const uint32_t* __restrict__ crit, const long long* __restrict__ pre, Grid g, int kind,
+                              int64_t base, uint64_t* __restrict__ origin, uint8_t* __restrict__ kout,
+                              uint64_t* __restrict__ jout) {
+  DMTZ_FOR_ANCHORS(g, 0, g.nz) {
+    const int64_t a = x + y * g.sy + z * g.sz;
+    const uint32_t cm = crit[a];
+    int64_t b = base + pre[a];
+    const int top = Tr<D>::TOP;
+    if (kind == 1) {
+      for (int t = 1; t < t_first_of_dim<D>(2); t++) {
+        if (!((cm >> t) & 1u)) continue;
+        for (int j = 0; j < 2; j++) { origin[b] = cell_id<D>(a, t); kout[b] = 1; jout[b] = (uint64_t)j; b++; }
+      }
+    } else if (kind == 2) {
+      for (int t = t_first_of_dim<D>(top - 1); t < t_first_of_dim<D>(top); t++) {
+        if (!((cm >> t) & 1u)) continue;
+        for (int s = 0; s < t_nlink<D>(t); s++) {
+          if (!link_in_grid<D>(g, a, t, s)) continue;
+          origin[b] = cell_id<D>(a, t); kout[b] = 2; jout[b] = (uint64_t)s; b++;
+        }
+      }
+    } else if (D == 3) {
+      for (int t = t_first_of_dim<D>(2); t < t_first_of_dim<D>(3); t++) {
+        if (!((cm >> t) & 1u)) continue;
+        origin[b] = cell_id<D>(a, t); kout[b] = 4; jout[b] = 0; b++;
+      }
+    }
+  }
+}
+
+// decode a cell id back to (anchor, type)
+template <int D>
+__device__ __forceinline__ void id_cell(uint64_t id, int64_t& a, int& t) {
+  const int d = (int)(id >> 56);
+  const int64_t r = (int64_t)(id & ((1ull << 56) - 1));
+  const int Td = types_of_dim<D>(d);
+  a = r / Td;
+  t = t_first_of_dim<D>(d) + (int)(r - a * Td);
+}
+
+// ----------------------------------------------------------------------------- walks
+// write == false: count cells only.  Returns the cell count or -1 on a cycle.
+template <int D>
+__device__ int64_t walk_desc(const void* codes, const Grid& g, int64_t a, int t, int j, bool write,
+                             uint64_t* cells, uint64_t* term, int64_t cap_steps) {
+  int64_t v = a + mask_delta(g, t_vmask<D>(t, j));
+  int64_t n = 0;
+  if (write) cells[n] = cell_id<D>(v, 0);
+  n++;
+  for (int64_t step = 0;; step++) {
+    if (step > cap_steps) return -1;
+    const uint32_t s = field_of<D>(code_at<D>(codes, v), 0);
+    if (s == (uint32_t)t_none<D>(0)) break;  // critical vertex (a vertex has no facets)
+    const int64_t w = v + t_link<D>(0, s, 0) + t_link<D>(0, s, 1) * g.sy + t_link<D>(0, s, 2) * g.sz;
+    if (write) {
+      cells[n] = cell_id<D>(cof_anchor<D>(g, v, 0, s), t_cof_type<D>(0, s));
+      cells[n + 1] = cell_id<D>(w, 0);
+    }
+    n += 2;
+    v = w;
+  }
+  if (write) *term = cell_id<D>(v, 0);
+  return n;
+}
+
+template <int D>
+__device__ int64_t walk_asc(const void* codes, const Grid& g, int64_t a, int t, int s0, bool write,
+                            uint64_t* cells, uint64_t* term, int64_t cap_steps) {
+  int64_t B = cof_anchor<D>(g, a, t, s0);
+  int bt = t_cof_type<D>(t, s0);
+  int64_t n = 0;
+  uint64_t terminal = CELL_BOUNDARY;
+  for (int64_t step = 0;; step++) {
+    if (step > cap_steps) return -1;
+    if (write) cells[n] = cell_id<D>(B, bt);
+    n++;
+    int64_t ca;
+    int ct;
+    if (paired_facet<D>(codes, g, B, bt, ca, ct) < 0) { terminal = cell_id<D>(B, bt); break; }  // maximum
+    if (write) cells[n] = cell_id<D>(ca, ct);
+    n++;
+    // the other top cofacet of (ca, ct)
+    bool moved = false;
+    for (int s = 0; s < t_nlink<D>(ct); s++) {
+      if (!link_in_grid<D>(g, ca, ct, s)) continue;
+      const int64_t nb = cof_anchor<D>(g, ca, ct, s);
+      const int nt = t_cof_type<D>(ct, s);
+      if (nb == B && nt == bt) continue;
+      B = nb; bt = nt; moved = true;
+      break;
+    }
+    if (!moved) break;  // boundary facet: the path leaves the domain
+  }
+  if (write) *term = terminal;
+  return n;
+}
+
+// Connector BFS from critical triangle (a, t), private queue + visited hash set.
+// Returns the event count, -2 if the scratch slot was too small, -1 on error.
+template <int D>
+__device__ int64_t bfs_conn(const void* codes, const uint32_t* __restrict__ crit, const Grid& g, int64_t a, int t,
+                            bool write, uint64_t* cells, unsigned long long* queue, int64_t qcap,
+                            unsigned long long* hset, int64_t hcap /* power of 2 */) {
+  // hset starts all-zero; every inserted key is also in the queue, and the
+  // clean-up below removes exactly those, so the slot is zero again on exit
+  auto key = [](int64_t an, int ty) { return (unsigned long long)(an * 32 + ty) + 1ull; };
+  auto slot_of = [&](unsigned long long k) { return (k * 0x9E3779B97F4A7C15ull) >> 20; };
+  auto insert = [&](unsigned long long k) -> int {  // 1 inserted, 0 present, -1 full
+    const unsigned long long h = slot_of(k);
+    for (int64_t p = 0; p < hcap / 2; p++) {
+      const int64_t i = (int64_t)((h + p) & (unsigned long long)(hcap - 1));
+      if (hset[i] == k) return 0;
+      if (hset[i] == 0ull) { hset[i] = k; return 1; }
+    }
+    return -1;
+  };
+  int64_t head = 0, tail = 0, n = 0, result = 0;
+  queue[tail++] = key(a, t);
+  insert(key(a, t));
+  while (head < tail && result == 0) {
+    const unsigned long long cur = queue[head++] - 1ull;
+    const int64_t B = (int64_t)(cur / 32);
+    const int bt = (int)(cur % 32);
+    for (int j = 0; j < t_nfacet<D>(bt); j++) {
+      const int dm = t_facet<D>(bt, j, 0), et = t_facet<D>(bt, j, 1);
+      const int64_t E = B + mask_delta(g, dm);
+      if ((crit[E] >> et) & 1u) {  // critical edge: a reached 1-saddle
+        if (write) cells[n] = cell_id<D>(E, et);
+        n++;
+        continue;
+      }
+      const uint32_t s = field_of<D>(code_at<D>(codes, E), et);
+      if (s == (uint32_t)t_none<D>(et)) continue;  // paired down with a vertex: the path stops
+      const int64_t Nb = cof_anchor<D>(g, E, et, (int)s);
+      const int nt = t_cof_type<D>(et, (int)s);
+      if (Nb == B && nt == bt) continue;
+      if (tail >= qcap) { result = -2; break; }
+      const int ins = insert(key(Nb, nt));
+      if (ins < 0) { result = -2; break; }
+      if (ins == 0) continue;
+      if (write) cells[n] = cell_id<D>(Nb, nt);
+      n++;
+      queue[tail++] = key(Nb, nt);
+    }
+  }
+  for (int64_t q = 0; q < tail; q++) {  // clean the visited set
+    const unsigned long long k = queue[q], h = slot_of(k);
+    for (int64_t p = 0; p < hcap; p++) {
+      const int64_t i = (int64_t)((h + p) & (unsigned long long)(hcap - 1));
+      if (hset[i] == k) { hset[i] = 0ull; break; }
+      if (hset[i] == 0ull) break;
+    }
+  }
+  return result ? result : n;
+}
+
+template <int D>
+__global__ void k_walk(const void* codes, const uint32_t* __restrict__ crit, Grid g, int64_t nb,
+                       const uint64_t* __restrict__ origin, const uint8_t* __restrict__ kind,
+                       uint64_t* __restrict__ jterm, long long* __restrict__ off, uint64_t* __restrict__ cells,
+                       bool write, unsigned long long* __restrict__ scratch, int64_t slot_q, int64_t slot_h,
+                       int64_t nslots, int* __restrict__ overflow, Counters* __restrict__ cnt) {
+  const int64_t cap_steps = g.N * 26 + 1;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a;
+    int t;
+    id_cell<D>(origin[b], a, t);
+    const int k = kind[b];
+    int64_t n;
+    uint64_t* out = write ? cells + off[b] : nullptr;
+    uint64_t term = CELL_BOUNDARY;
+    if (k == 1) n = walk_desc<D>(codes, g, a, t, (int)jterm[b], write, out, &term, cap_steps);
+    else if (k == 2) n = walk_asc<D>(codes, g, a, t, (int)jterm[b], write, out, &term, cap_steps);
+    else {
+      // connector: slots are handed out per thread; overflowing saddles go to the big pass
+      const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // < nslots by launch
+      unsigned long long* q = scratch + slot * (slot_q + slot_h);
+      n = bfs_conn<D>(codes, crit, g, a, t, write, out, q, slot_q, q + slot_q, slot_h);
+      if (n == -2) { overflow[b] = 1; continue; }
+    }
+    if (n < 0) { atomicAdd(&cnt->n_internal, 1ull); n = 0; }
+    if (!write) off[b] = n;
+    else jterm[b] = term;
+  }
+}
+
+// one saddle at a time with the whole scratch (connectors that outgrew their slot)
+template <int D>
+__global__ void k_walk_big(const void* codes, const uint32_t* __restrict__ crit, Grid g, int64_t b,
+                           const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
+                           long long* __restrict__ off, uint64_t* __restrict__ cells, bool write,
+                           unsigned long long* __restrict__ scratch, int64_t q, int64_t h, Counters* __restrict__ cnt) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  int64_t a;
+  int t;
+  id_cell<D>(origin[b], a, t);
+  int64_t n = bfs_conn<D>(codes, crit, g, a, t, write, write ? cells + off[b] : nullptr, scratch, q, scratch + q, h);
+  if (n < 0) { atomicAdd(&cnt->n_internal, 1ull); n = 0; }
+  if (!write) off[b] = n;
+  else jterm[b] = CELL_BOUNDARY;
+}
+
+inline size_t trace_scratch_bytes(const Grid&, int) { return 0; }  // reuses free workspace regions
+
+// ----------------------------------------------------------------------------- driver
+#define TCK(x)                                  \
+  do {                                          \
+    cudaError_t e_ = (x);                       \
+    if (e_ != cudaSuccess) return e_;           \
+  } while (0)
+
+inline cudaError_t scan_i64(long long* a, int64_t n, unsigned long long* bsum, unsigned long long* total,
+                            unsigned long long* host_total, cudaStream_t s) {
+  const int64_t nb = (n + SCAN_CHUNK - 1) / SCAN_CHUNK;
+  if (n > 0) {
+    k_scan_local<<<(unsigned)nb, 1024, 0, s>>>(a, n, bsum);
+    k_scan_top<<<1, 32, 0, s>>>(bsum, nb, total);
+    k_scan_add<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, n, bsum);
+  } else {
+    TCK(cudaMemsetAsync(total, 0, 8, s));
+  }
+  TCK(cudaGetLastError());
+  TCK(cudaMemcpyAsync(host_total, total, 8, cudaMemcpyDeviceToHost, s));
+  TCK(cudaStreamSynchronize(s));
+  return cudaSuccess;
+}
+
+inline dim3 trace_anchor_grid(const Grid& g) {
+  int64_t bx = (g.nx + 127) / 128, by = g.ny < 65535 ? g.ny : 65535, bz = g.nz < 65535 ? g.nz : 65535;
+  return dim3((unsigned)bx, (unsigned)by, (unsigned)bz);
+}
+
+template <int D>
+cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
+  const Grid& g = A.g;
+  Counters* dc = A.cnt;
+  Counters* hc = A.host_cnt;
+  TCK(cudaMemsetAsync(dc, 0, sizeof(Counters), s));
+  k_critmask<D><<<trace_anchor_grid(g), 128, 0, s>>>((const typename Tr<D>::code_t*)A.codes, A.crit, g);
+  TCK(cudaGetLastError());
+  long long* pre = A.pre;
+  unsigned long long* total = &dc->pad[0];
+  const int kinds_list[3] = {1, 2, 4};
+  int64_t nbk[3] = {0, 0, 0};
+  for (int ki = 0; ki < 3; ki++) {
+    const int kind = kinds_list[ki];
+    if (!(A.kinds & (uint32_t)kind) || (kind == 4 && D != 3)) continue;
+    k_branch_count<D><<<trace_anchor_grid(g), 128, 0, s>>>(A.crit, pre, g, kind);
+    TCK(cudaGetLastError());
+    TCK(scan_i64(pre, g.N, A.bsum, total, &hc->pad[0], s));
+    nbk[ki] = (int64_t)hc->pad[0];
+  }
+  const int64_t nb = nbk[0] + nbk[1] + nbk[2];
+  A.n_branches = nb;
+  if (nb > A.cap_b) return cudaSuccess;  // caller reports DMTZ_E_CAPACITY with the needed size
+  if (nb * 4 + 8 > g.N * 8) return cudaErrorMemoryAllocation;
+  int64_t base = 0;
+  for (int ki = 0; ki < 3; ki++) {
+    const int kind = kinds_list[ki];
+    if (!nbk[ki]) continue;
+    k_branch_count<D><<<trace_anchor_grid(g), 128, 0, s>>>(A.crit, pre, g, kind);
+    TCK(scan_i64(pre, g.N, A.bsum, total, &hc->pad[0], s));
+    k_branch_emit<D><<<trace_anchor_grid(g), 128, 0, s>>>(A.crit, pre, g, kind, base, A.out_origin, A.out_kind,
+                                                          A.out_terminal);
+    TCK(cudaGetLastError());
+    base += nbk[ki];
+  }
+  // walks: lengths -> offsets -> cells.  Connector slots: one per thread of the launch.
+  int* ovf = (int*)pre;
+  unsigned long long* sc = A.bfs;
+  const int64_t words = (int64_t)(A.bfs_bytes / 8);
+  const int64_t slot_q = 1024, slot_h = 2048;
+  const int threads = 128;
+  int64_t nslots = words / (slot_q + slot_h);
+  if (nslots > 65536) nslots = 65536;
+  nslots = nslots / threads * threads;
+  int64_t blocks = (nb + threads - 1) / threads;
+  if (nbk[2] && blocks * threads > nslots) blocks = nslots / threads;
+  if (blocks < 1) blocks = 1;
+  if (nbk[2] && nslots < threads) return cudaErrorMemoryAllocation;
+  long long* off = (long long*)A.out_offsets;
+  TCK(cudaMemsetAsync(sc, 0, A.bfs_bytes, s));
+  int64_t hbig = 1;
+  while (hbig * 2 * 3 <= words) hbig *= 2;
+  const int64_t qbig = words - hbig;
+  std::vector<int> hov;
+  for (int pass = 0; pass < 2; pass++) {
+    const bool write = pass == 1;
+    TCK(cudaMemsetAsync(ovf, 0, (size_t)nb * 4 + 4, s));
+    k_walk<D><<<(unsigned)blocks, threads, 0, s>>>(A.codes, A.crit, g, nb, A.out_origin, A.out_kind, A.out_terminal,
+                                                   off, A.out_cells, write, sc, slot_q, slot_h, nslots, ovf, dc);
+    TCK(cudaGetLastError());
+    if (nbk[2]) {  // connectors that outgrew their slot: one at a time with the whole scratch
+      hov.assign((size_t)nb, 0);
+      TCK(cudaMemcpyAsync(hov.data(), ovf, (size_t)nb * 4, cudaMemcpyDeviceToHost, s));
+      TCK(cudaStreamSynchronize(s));
+      for (int64_t b = 0; b < nb; b++) {
+        if (!hov[(size_t)b]) continue;
+        TCK(cudaMemsetAsync(sc, 0, A.bfs_bytes, s));
+        k_walk_big<D><<<1, 1, 0, s>>>(A.codes, A.crit, g, b, A.out_origin, A.out_terminal, off, A.out_cells, write,
+                                      sc, qbig, hbig, dc);
+        TCK(cudaGetLastError());
+      }
+      TCK(cudaMemsetAsync(sc, 0, A.bfs_bytes, s));
+    }
+    if (!write) {
+      TCK(cudaMemsetAsync(off + nb, 0, 8, s));
+      TCK(scan_i64(off, nb + 1, A.bsum, total, &hc->pad[0], s));
+      A.n_cells = (int64_t)hc->pad[0];
+      if (A.n_cells > A.cap_c) break;
+    }
+  }
+  TCK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+  TCK(cudaStreamSynchronize(s));
+  A.n_internal = (int64_t)hc->n_internal;
+  return cudaSuccess;
 }
 
 }  // namespace dmtz

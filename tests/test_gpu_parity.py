@@ -145,3 +145,50 @@ def test_deterministic(dmtz):
     a = dmtz.correct(_cuda(f), _cuda(fh), xi)
     b = dmtz.correct(_cuda(f), _cuda(fh), xi)
     assert torch.equal(a.g.view(torch.int32), b.g.view(torch.int32)) and torch.equal(a.edits, b.edits)
+
+
+TRACE_CASES = [("noise", (6, 7), 1), ("noise", (40, 33), 2), ("gauss2d", (64, 64), 3), ("noise", (4, 4, 4), 3),
+               ("noise", (5, 6, 7), 4), ("lognormal", (12, 13, 14), 5), ("hurricane", (10, 30, 40), 6)]
+
+
+def _compare_trace(dmtz, fld):
+    ref = oracle.trace(fld)
+    codes = dmtz.compute_gradient(_cuda(fld))
+    tr = dmtz.trace_separatrices(codes)
+    for k in ("offsets", "cells", "origin", "terminal"):
+        got = tr[k].cpu().numpy()
+        want = ref[k]
+        if want.dtype == np.uint64:
+            got = got.view(np.uint64)
+        assert np.array_equal(got, want), k
+    assert np.array_equal(tr["kind"].cpu().numpy(), ref["kind"])
+    return ref
+
+
+@pytest.mark.parametrize("family,shape,seed", TRACE_CASES)
+def test_trace_bit_exact(dmtz, family, shape, seed):
+    f, fh, xi = di.random_case(shape, seed, family=family)
+    ref = _compare_trace(dmtz, f)
+    assert len(ref["origin"]) > 0
+    _compare_trace(dmtz, fh)
+
+
+@pytest.mark.parametrize("name,shape", [("C1", None), ("C3", (20, 50, 50)), ("C4", (24, 24, 24))])
+def test_trace_after_correct(dmtz, name, shape):
+    """The separatrices of the converged field g (the S-loop's input)."""
+    f, fh, xi, _ = di.config_inputs(name, shape=shape)
+    r = dmtz.correct(_cuda(f), _cuda(fh), xi)
+    _compare_trace(dmtz, r.g.cpu().numpy())
+
+
+def test_trace_capacity(dmtz):
+    f, _, _ = di.random_case((5, 6, 7), 4)
+    ref = oracle.trace(f)
+    codes = dmtz.compute_gradient(_cuda(f))
+    with pytest.raises(dmtz.DmtzError) as ei:
+        dmtz.trace_separatrices(codes, cap_branches=3, cap_cells=10)
+    assert ei.value.status == dmtz.E_CAPACITY
+    tr = dmtz.trace_separatrices(codes, kinds=dmtz.KIND_DESC)
+    nd = int((ref["kind"] == 1).sum())
+    assert tr["origin"].shape[0] == nd
+    assert np.array_equal(tr["cells"].cpu().numpy().view(np.uint64), ref["cells"][:ref["offsets"][nd]])
