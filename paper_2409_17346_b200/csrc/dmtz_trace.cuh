@@ -326,7 +326,8 @@ __global__ void k_walk(const void* codes, const uint32_t* __restrict__ crit, Gri
                        const uint64_t* __restrict__ origin, const uint8_t* __restrict__ kind,
                        uint64_t* __restrict__ jterm, long long* __restrict__ off, uint64_t* __restrict__ cells,
                        bool write, unsigned long long* __restrict__ scratch, int64_t slot_q, int64_t slot_h,
-                       int64_t nslots, int* __restrict__ overflow, Counters* __restrict__ cnt) {
+                       int64_t nslots, int* __restrict__ overflow, int64_t conn_base,
+                       Counters* __restrict__ cnt) {
   const int64_t cap_steps = g.N * 26 + 1;
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
     int64_t a;
@@ -343,7 +344,11 @@ __global__ void k_walk(const void* codes, const uint32_t* __restrict__ crit, Gri
       const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // < nslots by launch
       unsigned long long* q = scratch + slot * (slot_q + slot_h);
       n = bfs_conn<D>(codes, crit, g, a, t, write, out, q, slot_q, q + slot_q, slot_h);
-      if (n == -2) { overflow[b] = 1; continue; }
+      if (n == -2) {  // overflow bit of connector branch b - conn_base
+        const int64_t cb = b - conn_base;
+        atomicOr((unsigned int*)overflow + (cb >> 5), 1u << (cb & 31));
+        continue;
+      }
     }
     if (n < 0) { atomicAdd(&cnt->n_internal, 1ull); n = 0; }
     if (!write) off[b] = n;
@@ -420,7 +425,8 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   const int64_t nb = nbk[0] + nbk[1] + nbk[2];
   A.n_branches = nb;
   if (nb > A.cap_b) return cudaSuccess;  // caller reports DMTZ_E_CAPACITY with the needed size
-  if (nb * 4 + 8 > g.N * 8) return cudaErrorMemoryAllocation;
+  const int64_t conn_base = nbk[0] + nbk[1];
+  const int64_t ovf_words = (nbk[2] + 31) / 32;
   int64_t base = 0;
   for (int ki = 0; ki < 3; ki++) {
     const int kind = kinds_list[ki];
@@ -453,16 +459,18 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   std::vector<int> hov;
   for (int pass = 0; pass < 2; pass++) {
     const bool write = pass == 1;
-    TCK(cudaMemsetAsync(ovf, 0, (size_t)nb * 4 + 4, s));
+    TCK(cudaMemsetAsync(ovf, 0, (size_t)ovf_words * 4 + 4, s));
     k_walk<D><<<(unsigned)blocks, threads, 0, s>>>(A.codes, A.crit, g, nb, A.out_origin, A.out_kind, A.out_terminal,
-                                                   off, A.out_cells, write, sc, slot_q, slot_h, nslots, ovf, dc);
+                                                   off, A.out_cells, write, sc, slot_q, slot_h, nslots, ovf,
+                                                   conn_base, dc);
     TCK(cudaGetLastError());
     if (nbk[2]) {  // connectors that outgrew their slot: one at a time with the whole scratch
-      hov.assign((size_t)nb, 0);
-      TCK(cudaMemcpyAsync(hov.data(), ovf, (size_t)nb * 4, cudaMemcpyDeviceToHost, s));
+      hov.assign((size_t)ovf_words + 1, 0);
+      TCK(cudaMemcpyAsync(hov.data(), ovf, (size_t)ovf_words * 4, cudaMemcpyDeviceToHost, s));
       TCK(cudaStreamSynchronize(s));
-      for (int64_t b = 0; b < nb; b++) {
-        if (!hov[(size_t)b]) continue;
+      for (int64_t cb = 0; cb < nbk[2]; cb++) {
+        if (!((hov[(size_t)(cb >> 5)] >> (cb & 31)) & 1)) continue;
+        const int64_t b = conn_base + cb;
         TCK(cudaMemsetAsync(sc, 0, A.bfs_bytes, s));
         k_walk_big<D><<<1, 1, 0, s>>>(A.codes, A.crit, g, b, A.out_origin, A.out_terminal, off, A.out_cells, write,
                                       sc, qbig, hbig, dc);
