@@ -69,7 +69,8 @@ Layout layout_for(const dmtz_ctx* c) {
   L.cand_g = o; o += align_up(N * 8);  // u64 even in 2D: the trace reuses it as int64 scratch
   L.crit_f = o; o += align_up(N * 4);
   L.crit_g = o; o += align_up(N * 4);
-  L.lowpos = o; o += align_up(N * 8);
+  // lowpos doubles as the trace's connector-BFS scratch: at least 128 slots of 3 x 1024 words
+  L.lowpos = o; o += align_up(N * 8 > (size_t)128 * 3072 * 8 ? N * 8 : (size_t)128 * 3072 * 8);
   L.lb = o; o += align_up(N * 4);
   L.state = o; o += align_up(N * 4);
   L.tbits = o; o += align_up((N + 31) / 32 * 4 + 64);
@@ -374,7 +375,7 @@ dmtz_status dmtz_trace_separatrices(dmtz_ctx* c, const void* codes, uint32_t kin
   a.kinds = kinds;
   a.pre = (long long*)(ws + L.cand_g);
   a.bfs = (unsigned long long*)(ws + L.lowpos);
-  a.bfs_bytes = (size_t)c->g.N * 8;
+  a.bfs_bytes = L.lb - L.lowpos;  // the lowpos region, which lb follows
   a.crit = (uint32_t*)(ws + L.crit_g);
   a.bsum = (unsigned long long*)(ws + L.edit_bc);
   a.cnt = (Counters*)(ws + L.counters);

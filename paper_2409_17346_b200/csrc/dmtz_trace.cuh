@@ -442,7 +442,10 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   int* ovf = (int*)pre;
   unsigned long long* sc = A.bfs;
   const int64_t words = (int64_t)(A.bfs_bytes / 8);
-  const int64_t slot_q = 1024, slot_h = 2048;
+  // a connector visits at most the 12 N triangles; small grids get small slots
+  const int64_t slot_q = 12 * g.N + 16 < 1024 ? 12 * g.N + 16 : 1024;
+  int64_t slot_h = 1;
+  while (slot_h < 2 * slot_q) slot_h *= 2;
   const int threads = 128;
   int64_t nslots = words / (slot_q + slot_h);
   if (nslots > 65536) nslots = 65536;
