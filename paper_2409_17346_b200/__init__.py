@@ -226,8 +226,12 @@ class Context:
         cb = cap_branches if cap_branches is not None else 1 << 16
         cc = cap_cells if cap_cells is not None else 1 << 20
         st, nb, nc, bufs = run(cb, cc)
-        if st == E_CAPACITY and cap_branches is None and cap_cells is None:
-            st, nb, nc, bufs = run(max(nb, 1), max(nc, 1))
+        tries = 0
+        while st == E_CAPACITY and cap_branches is None and cap_cells is None and tries < 2:
+            # the branch count is known first; the cell count once the branches fit
+            cb, cc = max(nb, cb), max(nc, cc)
+            st, nb, nc, bufs = run(cb, cc)
+            tries += 1
         _check(st)
         return dict(offsets=bufs["offsets"][:nb + 1], cells=bufs["cells"][:nc], origin=bufs["origin"][:nb],
                     terminal=bufs["terminal"][:nb], kind=bufs["kind"][:nb])

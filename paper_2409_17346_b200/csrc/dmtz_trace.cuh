@@ -310,7 +310,9 @@ __device__ int64_t bfs_conn(const void* codes, const uint32_t* __restrict__ crit
       queue[tail++] = key(Nb, nt);
     }
   }
-  for (int64_t q = 0; q < tail; q++) {  // clean the visited set
+  // clean the visited set in reverse insertion order: linear-probing chains of the
+  // keys still present stay intact, so every key is found and removed
+  for (int64_t q = tail - 1; q >= 0; q--) {
     const unsigned long long k = queue[q], h = slot_of(k);
     for (int64_t p = 0; p < hcap; p++) {
       const int64_t i = (int64_t)((h + p) & (unsigned long long)(hcap - 1));
