@@ -324,14 +324,15 @@ __device__ int64_t bfs_conn(const void* codes, const uint32_t* __restrict__ crit
 }
 
 template <int D>
-__global__ void k_walk(const void* codes, const uint32_t* __restrict__ crit, Grid g, int64_t nb,
+__global__ void k_walk(const void* codes, const uint32_t* __restrict__ crit, Grid g, int64_t b0, int64_t nb,
                        const uint64_t* __restrict__ origin, const uint8_t* __restrict__ kind,
                        uint64_t* __restrict__ jterm, long long* __restrict__ off, uint64_t* __restrict__ cells,
                        bool write, unsigned long long* __restrict__ scratch, int64_t slot_q, int64_t slot_h,
                        int64_t nslots, int* __restrict__ overflow, int64_t conn_base,
                        Counters* __restrict__ cnt) {
   const int64_t cap_steps = g.N * 26 + 1;
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t b = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x) {
     int64_t a;
     int t;
     id_cell<D>(origin[b], a, t);
@@ -358,20 +359,28 @@ __global__ void k_walk(const void* codes, const uint32_t* __restrict__ crit, Gri
   }
 }
 
-// one saddle at a time with the whole scratch (connectors that outgrew their slot)
+// connectors that outgrew their slot, retried with bigger slots: list[i] = connector index
 template <int D>
-__global__ void k_walk_big(const void* codes, const uint32_t* __restrict__ crit, Grid g, int64_t b,
-                           const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
-                           long long* __restrict__ off, uint64_t* __restrict__ cells, bool write,
-                           unsigned long long* __restrict__ scratch, int64_t q, int64_t h, Counters* __restrict__ cnt) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  int64_t a;
-  int t;
-  id_cell<D>(origin[b], a, t);
-  int64_t n = bfs_conn<D>(codes, crit, g, a, t, write, write ? cells + off[b] : nullptr, scratch, q, scratch + q, h);
-  if (n < 0) { atomicAdd(&cnt->n_internal, 1ull); n = 0; }
-  if (!write) off[b] = n;
-  else jterm[b] = CELL_BOUNDARY;
+__global__ void k_walk_list(const void* codes, const uint32_t* __restrict__ crit, Grid g,
+                            const long long* __restrict__ list, int64_t nlist, int64_t conn_base,
+                            const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
+                            long long* __restrict__ off, uint64_t* __restrict__ cells, bool write,
+                            unsigned long long* __restrict__ scratch, int64_t slot_q, int64_t slot_h,
+                            unsigned int* __restrict__ overflow, Counters* __restrict__ cnt) {
+  const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // < nslots by launch
+  for (int64_t i = slot; i < nlist; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cb = list[i], b = conn_base + cb;
+    int64_t a;
+    int t;
+    id_cell<D>(origin[b], a, t);
+    unsigned long long* q = scratch + slot * (slot_q + slot_h);
+    int64_t n = bfs_conn<D>(codes, crit, g, a, t, write, write ? cells + off[b] : nullptr, q, slot_q, q + slot_q,
+                            slot_h);
+    if (n == -2) { atomicOr(overflow + (cb >> 5), 1u << (cb & 31)); continue; }
+    if (n < 0) { atomicAdd(&cnt->n_internal, 1ull); n = 0; }
+    if (!write) off[b] = n;
+    else jterm[b] = CELL_BOUNDARY;
+  }
 }
 
 inline size_t trace_scratch_bytes(const Grid&, int) { return 0; }  // reuses free workspace regions
@@ -427,8 +436,6 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   const int64_t nb = nbk[0] + nbk[1] + nbk[2];
   A.n_branches = nb;
   if (nb > A.cap_b) return cudaSuccess;  // caller reports DMTZ_E_CAPACITY with the needed size
-  const int64_t conn_base = nbk[0] + nbk[1];
-  const int64_t ovf_words = (nbk[2] + 31) / 32;
   int64_t base = 0;
   for (int ki = 0; ki < 3; ki++) {
     const int kind = kinds_list[ki];
@@ -445,41 +452,66 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   unsigned long long* sc = A.bfs;
   const int64_t words = (int64_t)(A.bfs_bytes / 8);
   // a connector visits at most the 12 N triangles; small grids get small slots
-  const int64_t slot_q = 12 * g.N + 16 < 1024 ? 12 * g.N + 16 : 1024;
+  const int64_t slot_q = 12 * g.N + 16 < 256 ? 12 * g.N + 16 : 256;
   int64_t slot_h = 1;
   while (slot_h < 2 * slot_q) slot_h *= 2;
   const int threads = 128;
   int64_t nslots = words / (slot_q + slot_h);
   if (nslots > 65536) nslots = 65536;
   nslots = nslots / threads * threads;
-  int64_t blocks = (nb + threads - 1) / threads;
-  if (nbk[2] && blocks * threads > nslots) blocks = nslots / threads;
-  if (blocks < 1) blocks = 1;
+  const int64_t conn_base = nbk[0] + nbk[1];
+  const int64_t ovf_words = (nbk[2] + 31) / 32;
+  if ((ovf_words + 2) * 4 + 64 * 8 > g.N * 8) return cudaErrorMemoryAllocation;  // overflow bits + list space
+  const int64_t list_cap = (g.N * 8 - (ovf_words + 2) * 4) / 8;
   if (nbk[2] && nslots < threads) return cudaErrorMemoryAllocation;
+  const int64_t blocks_path = conn_base > 0 ? (conn_base + threads - 1) / threads : 0;
+  int64_t blocks_conn = (nbk[2] + threads - 1) / threads;
+  if (blocks_conn * threads > nslots) blocks_conn = nslots / threads;
   long long* off = (long long*)A.out_offsets;
   TCK(cudaMemsetAsync(sc, 0, A.bfs_bytes, s));
-  int64_t hbig = 1;
-  while (hbig * 2 * 3 <= words) hbig *= 2;
-  const int64_t qbig = words - hbig;
   std::vector<int> hov;
   for (int pass = 0; pass < 2; pass++) {
     const bool write = pass == 1;
     TCK(cudaMemsetAsync(ovf, 0, (size_t)ovf_words * 4 + 4, s));
-    k_walk<D><<<(unsigned)blocks, threads, 0, s>>>(A.codes, A.crit, g, nb, A.out_origin, A.out_kind, A.out_terminal,
-                                                   off, A.out_cells, write, sc, slot_q, slot_h, nslots, ovf,
-                                                   conn_base, dc);
+    if (blocks_path)  // descending / ascending paths: one thread per branch
+      k_walk<D><<<(unsigned)blocks_path, threads, 0, s>>>(A.codes, A.crit, g, 0, conn_base, A.out_origin, A.out_kind,
+                                                          A.out_terminal, off, A.out_cells, write, sc, slot_q,
+                                                          slot_h, nslots, ovf, conn_base, dc);
+    if (blocks_conn)  // connectors: one scratch slot per thread
+      k_walk<D><<<(unsigned)blocks_conn, threads, 0, s>>>(A.codes, A.crit, g, conn_base, nb, A.out_origin, A.out_kind,
+                                                          A.out_terminal, off, A.out_cells, write, sc, slot_q,
+                                                          slot_h, nslots, ovf, conn_base, dc);
     TCK(cudaGetLastError());
-    if (nbk[2]) {  // connectors that outgrew their slot: one at a time with the whole scratch
-      hov.assign((size_t)ovf_words + 1, 0);
-      TCK(cudaMemcpyAsync(hov.data(), ovf, (size_t)ovf_words * 4, cudaMemcpyDeviceToHost, s));
-      TCK(cudaStreamSynchronize(s));
-      for (int64_t cb = 0; cb < nbk[2]; cb++) {
-        if (!((hov[(size_t)(cb >> 5)] >> (cb & 31)) & 1)) continue;
-        const int64_t b = conn_base + cb;
+    if (nbk[2]) {  // connectors that outgrew their slot: retry with 16x bigger slots, fewer threads
+      int64_t q = slot_q;
+      long long* dlist = (long long*)(ovf + ovf_words + 2);
+      for (int level = 0; level < 8; level++) {
+        hov.assign((size_t)ovf_words + 1, 0);
+        TCK(cudaMemcpyAsync(hov.data(), ovf, (size_t)ovf_words * 4, cudaMemcpyDeviceToHost, s));
+        TCK(cudaStreamSynchronize(s));
+        std::vector<long long> lst;
+        for (int64_t cb = 0; cb < nbk[2]; cb++)
+          if ((hov[(size_t)(cb >> 5)] >> (cb & 31)) & 1) lst.push_back(cb);
+        if (lst.empty()) break;
+        if (q * 3 >= words) { A.n_internal += (int64_t)lst.size(); break; }  // larger than all scratch
+        q = q * 16 < words / 3 ? q * 16 : words / 3;
+        int64_t h = 1;
+        while (h < 2 * q) h *= 2;
+        if (q + h > words) h /= 2;
+        int64_t ns = words / (q + h);
+        if (ns < 1) ns = 1;
         TCK(cudaMemsetAsync(sc, 0, A.bfs_bytes, s));
-        k_walk_big<D><<<1, 1, 0, s>>>(A.codes, A.crit, g, b, A.out_origin, A.out_terminal, off, A.out_cells, write,
-                                      sc, qbig, hbig, dc);
-        TCK(cudaGetLastError());
+        TCK(cudaMemsetAsync(ovf, 0, (size_t)ovf_words * 4 + 4, s));
+        const int64_t th = ns < 128 ? ns : 128;
+        for (int64_t c0 = 0; c0 < (int64_t)lst.size(); c0 += list_cap) {
+          const int64_t cn = (int64_t)lst.size() - c0 < list_cap ? (int64_t)lst.size() - c0 : list_cap;
+          TCK(cudaMemcpyAsync(dlist, lst.data() + c0, (size_t)cn * 8, cudaMemcpyHostToDevice, s));
+          k_walk_list<D><<<(unsigned)(ns / th), (unsigned)th, 0, s>>>(
+              A.codes, A.crit, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write, sc, q,
+              h, (unsigned int*)ovf, dc);
+          TCK(cudaGetLastError());
+          TCK(cudaStreamSynchronize(s));  // lst is pageable host memory
+        }
       }
       TCK(cudaMemsetAsync(sc, 0, A.bfs_bytes, s));
     }
