@@ -66,7 +66,8 @@ Layout layout_for(const dmtz_ctx* c) {
   Layout L;
   size_t o = 0;
   L.cand_f = o; o += align_up(N * cs);
-  L.cand_g = o; o += align_up(N * 8);  // u64 even in 2D: the trace reuses it as int64 scratch
+  // u64 even in 2D: the trace reuses it as int64 scratch (>= 1 MiB for small grids)
+  L.cand_g = o; o += align_up(N * 8 > (size_t)(1 << 20) ? N * 8 : (size_t)(1 << 20));
   L.crit_f = o; o += align_up(N * 4);
   L.crit_g = o; o += align_up(N * 4);
   // lowpos doubles as the trace's connector-BFS scratch: at least 128 slots of 3 x 1024 words
@@ -374,6 +375,7 @@ dmtz_status dmtz_trace_separatrices(dmtz_ctx* c, const void* codes, uint32_t kin
   a.codes = codes;
   a.kinds = kinds;
   a.pre = (long long*)(ws + L.cand_g);
+  a.pre_bytes = L.crit_f - L.cand_g;
   a.bfs = (unsigned long long*)(ws + L.lowpos);
   a.bfs_bytes = L.lb - L.lowpos;  // the lowpos region, which lb follows
   a.crit = (uint32_t*)(ws + L.crit_g);

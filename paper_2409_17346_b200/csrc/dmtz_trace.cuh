@@ -26,7 +26,8 @@ struct TraceArgs {
   Grid g;
   const void* codes;
   uint32_t kinds;
-  long long* pre;            // N x 8 B workspace region: per-anchor branch counts, then overflow flags
+  long long* pre;            // >= N x 8 B workspace region: per-anchor branch counts, then overflow flags
+  size_t pre_bytes;
   unsigned long long* bfs;   // N x 8 B workspace region: connector BFS slots (zeroed, self-cleaning)
   size_t bfs_bytes;
   uint32_t* crit;            // N x 4 B workspace region
@@ -359,27 +360,163 @@ __global__ void k_walk(const void* codes, const uint32_t* __restrict__ crit, Gri
   }
 }
 
-// connectors that outgrew their slot, retried with bigger slots: list[i] = connector index
+// Block-parallel connector BFS for the saddles that outgrew a per-thread slot.
+// Reproduces the sequential FIFO order exactly: a batch = the next (up to 256)
+// queue entries, each producing its facet events in facet order; a discovered
+// triangle is new iff it was never seen before this batch and this is its first
+// occurrence in (entry, facet) order within the batch -- decided by an atomic
+// max of ~(batch << 32 | candidate) on the visited slot's owner word.  A block
+// scan then places events and new queue entries in that order.
+constexpr int BFS_THREADS = 256;
+
+__device__ __forceinline__ int64_t bfs_find_or_insert(unsigned long long* keys, int64_t hcap, unsigned long long k) {
+  const unsigned long long h = (k * 0x9E3779B97F4A7C15ull) >> 20;
+  for (int64_t p = 0; p < hcap / 2; p++) {
+    const int64_t i = (int64_t)((h + p) & (unsigned long long)(hcap - 1));
+    const unsigned long long v = atomicCAS(keys + i, 0ull, k);
+    if (v == 0ull || v == k) return i;
+  }
+  return -1;
+}
+__device__ __forceinline__ int64_t bfs_find(const unsigned long long* keys, int64_t hcap, unsigned long long k) {
+  const unsigned long long h = (k * 0x9E3779B97F4A7C15ull) >> 20;
+  for (int64_t p = 0; p < hcap; p++) {
+    const int64_t i = (int64_t)((h + p) & (unsigned long long)(hcap - 1));
+    if (keys[i] == k) return i;
+    if (keys[i] == 0ull) return -1;
+  }
+  return -1;
+}
+
 template <int D>
-__global__ void k_walk_list(const void* codes, const uint32_t* __restrict__ crit, Grid g,
-                            const long long* __restrict__ list, int64_t nlist, int64_t conn_base,
-                            const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
-                            long long* __restrict__ off, uint64_t* __restrict__ cells, bool write,
-                            unsigned long long* __restrict__ scratch, int64_t slot_q, int64_t slot_h,
-                            unsigned int* __restrict__ overflow, Counters* __restrict__ cnt) {
-  const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // < nslots by launch
-  for (int64_t i = slot; i < nlist; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t cb = list[i], b = conn_base + cb;
-    int64_t a;
-    int t;
-    id_cell<D>(origin[b], a, t);
-    unsigned long long* q = scratch + slot * (slot_q + slot_h);
-    int64_t n = bfs_conn<D>(codes, crit, g, a, t, write, write ? cells + off[b] : nullptr, q, slot_q, q + slot_q,
-                            slot_h);
-    if (n == -2) { atomicOr(overflow + (cb >> 5), 1u << (cb & 31)); continue; }
-    if (n < 0) { atomicAdd(&cnt->n_internal, 1ull); n = 0; }
-    if (!write) off[b] = n;
-    else jterm[b] = CELL_BOUNDARY;
+__global__ void __launch_bounds__(BFS_THREADS)
+k_walk_block(const void* codes, const uint32_t* __restrict__ crit, Grid g, const long long* __restrict__ list,
+             int64_t nlist, int64_t conn_base, const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
+             long long* __restrict__ off, uint64_t* __restrict__ cells, bool write,
+             unsigned long long* __restrict__ scratch, int64_t qcap, int64_t hcap,
+             unsigned int* __restrict__ overflow, Counters* __restrict__ cnt) {
+  __shared__ int s_warp[BFS_THREADS / 32];
+  __shared__ int s_flag;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  unsigned long long* queue = scratch + (int64_t)blockIdx.x * (qcap + 2 * hcap);
+  unsigned long long* keys = queue + qcap;
+  unsigned long long* owner = keys + hcap;
+  auto key = [](int64_t an, int ty) { return (unsigned long long)(an * 32 + ty) + 1ull; };
+  for (int64_t li = blockIdx.x; li < nlist; li += gridDim.x) {
+    const int64_t cb = list[li], b = conn_base + cb;
+    int64_t a0;
+    int t0;
+    id_cell<D>(origin[b], a0, t0);
+    uint64_t* out = write ? cells + off[b] : nullptr;
+    if (tid == 0) {
+      queue[0] = key(a0, t0);
+      const int64_t sl = bfs_find_or_insert(keys, hcap, key(a0, t0));
+      owner[sl] = ~0ull;  // seen before every batch
+      s_flag = 0;
+    }
+    __syncthreads();
+    int64_t head = 0, tail = 1, nev = 0;
+    unsigned long long batch = 1;
+    while (head < tail) {
+      const int64_t K = tail - head < BFS_THREADS ? tail - head : BFS_THREADS;
+      // candidates of entry head + tid: per facet j, kind 1 = reached edge, 2 = triangle
+      int ckind[3] = {0, 0, 0};
+      uint64_t cid[3] = {0, 0, 0};
+      unsigned long long ckey[3] = {0, 0, 0};
+      int64_t cslot[3] = {-1, -1, -1};
+      if (tid < K) {
+        const unsigned long long cur = queue[head + tid] - 1ull;
+        const int64_t B = (int64_t)(cur / 32);
+        const int bt = (int)(cur % 32);
+        for (int j = 0; j < 3; j++) {
+          const int dm = t_facet<D>(bt, j, 0), et = t_facet<D>(bt, j, 1);
+          const int64_t E = B + mask_delta(g, dm);
+          if ((crit[E] >> et) & 1u) { ckind[j] = 1; cid[j] = cell_id<D>(E, et); continue; }
+          const uint32_t sl = field_of<D>(code_at<D>(codes, E), et);
+          if (sl == (uint32_t)t_none<D>(et)) continue;
+          const int64_t Nb = cof_anchor<D>(g, E, et, (int)sl);
+          const int nt = t_cof_type<D>(et, (int)sl);
+          if (Nb == B && nt == bt) continue;
+          ckind[j] = 2;
+          cid[j] = cell_id<D>(Nb, nt);
+          ckey[j] = key(Nb, nt);
+          const int64_t slot = bfs_find_or_insert(keys, hcap, ckey[j]);
+          if (slot < 0) { s_flag = 1; continue; }
+          cslot[j] = slot;
+          atomicMax(owner + slot, ~((batch << 32) | (unsigned long long)(tid * 3 + j)));
+        }
+      }
+      __syncthreads();
+      if (s_flag) break;
+      int nmine = 0, qmine = 0;
+      bool isnew[3] = {false, false, false};
+      for (int j = 0; j < 3; j++) {
+        if (ckind[j] == 1) nmine++;
+        if (ckind[j] == 2 && owner[cslot[j]] == ~((batch << 32) | (unsigned long long)(tid * 3 + j))) {
+          isnew[j] = true;
+          nmine++;
+          qmine++;
+        }
+      }
+      // block exclusive scan of (events, enqueues) packed in one int
+      int v = nmine | (qmine << 16), incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      if (lane == 31) s_warp[wid] = incl;
+      __syncthreads();
+      int wbase = 0, tot = 0;
+      for (int w2 = 0; w2 < BFS_THREADS / 32; w2++) {
+        const int x = s_warp[w2];
+        if (w2 < wid) wbase += x;
+        tot += x;
+      }
+      const int ex = wbase + incl - v;
+      int pe = ex & 0xFFFF, pq = ex >> 16;
+      const int tot_e = tot & 0xFFFF, tot_q = tot >> 16;
+      if (tail + tot_q > qcap) {
+        if (tid == 0) s_flag = 1;
+      } else {
+        for (int j = 0; j < 3; j++) {
+          if (ckind[j] == 1 || isnew[j]) {
+            if (write) out[nev + pe] = cid[j];
+            pe++;
+          }
+          if (isnew[j]) { queue[tail + pq] = ckey[j]; pq++; }
+        }
+      }
+      __syncthreads();
+      if (s_flag) break;
+      nev += tot_e;
+      tail += tot_q;
+      head += K;
+      batch++;
+      __syncthreads();
+    }
+    const bool ovf = s_flag != 0;
+    __syncthreads();
+    // clean the visited set: find every queued key's slot first, then clear
+    for (int64_t i = tid; i < tail; i += BFS_THREADS) {
+      const int64_t sl = bfs_find(keys, hcap, queue[i]);
+      queue[i] = (unsigned long long)sl;
+    }
+    __syncthreads();
+    for (int64_t i = tid; i < tail; i += BFS_THREADS) {
+      const long long sl = (long long)queue[i];
+      if (sl >= 0) { keys[sl] = 0ull; owner[sl] = 0ull; }
+    }
+    __syncthreads();
+    if (ovf) {
+      // keys inserted beyond the queue (the failing batch) are not tracked: wipe the whole slot
+      for (int64_t i = tid; i < hcap; i += BFS_THREADS) { keys[i] = 0ull; owner[i] = 0ull; }
+      if (tid == 0) atomicOr(overflow + (cb >> 5), 1u << (cb & 31));
+    } else if (tid == 0) {
+      if (!write) off[b] = nev;
+      else jterm[b] = CELL_BOUNDARY;
+    }
+    __syncthreads();
   }
 }
 
@@ -461,8 +598,9 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   nslots = nslots / threads * threads;
   const int64_t conn_base = nbk[0] + nbk[1];
   const int64_t ovf_words = (nbk[2] + 31) / 32;
-  if ((ovf_words + 2) * 4 + 64 * 8 > g.N * 8) return cudaErrorMemoryAllocation;  // overflow bits + list space
-  const int64_t list_cap = (g.N * 8 - (ovf_words + 2) * 4) / 8;
+  const int64_t pre_words = (int64_t)(A.pre_bytes / 8);
+  if (nbk[2] && (ovf_words + 2) * 4 + 64 * 8 > pre_words * 8) return cudaErrorMemoryAllocation;
+  const int64_t list_cap = (pre_words * 8 - (ovf_words + 2) * 4) / 8;
   if (nbk[2] && nslots < threads) return cudaErrorMemoryAllocation;
   const int64_t blocks_path = conn_base > 0 ? (conn_base + threads - 1) / threads : 0;
   int64_t blocks_conn = (nbk[2] + threads - 1) / threads;
@@ -493,22 +631,23 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
         for (int64_t cb = 0; cb < nbk[2]; cb++)
           if ((hov[(size_t)(cb >> 5)] >> (cb & 31)) & 1) lst.push_back(cb);
         if (lst.empty()) break;
-        if (q * 3 >= words) { A.n_internal += (int64_t)lst.size(); break; }  // larger than all scratch
-        q = q * 16 < words / 3 ? q * 16 : words / 3;
+        if (q >= words / 5) { A.n_internal += (int64_t)lst.size(); break; }  // larger than all scratch
+        q = q * 16 < words / 5 ? q * 16 : words / 5;
         int64_t h = 1;
         while (h < 2 * q) h *= 2;
-        if (q + h > words) h /= 2;
-        int64_t ns = words / (q + h);
+        while (q + 2 * h > words) h /= 2;
+        int64_t ns = words / (q + 2 * h);
         if (ns < 1) ns = 1;
+        if (ns > 4096) ns = 4096;
         TCK(cudaMemsetAsync(sc, 0, A.bfs_bytes, s));
         TCK(cudaMemsetAsync(ovf, 0, (size_t)ovf_words * 4 + 4, s));
-        const int64_t th = ns < 128 ? ns : 128;
         for (int64_t c0 = 0; c0 < (int64_t)lst.size(); c0 += list_cap) {
           const int64_t cn = (int64_t)lst.size() - c0 < list_cap ? (int64_t)lst.size() - c0 : list_cap;
           TCK(cudaMemcpyAsync(dlist, lst.data() + c0, (size_t)cn * 8, cudaMemcpyHostToDevice, s));
-          k_walk_list<D><<<(unsigned)(ns / th), (unsigned)th, 0, s>>>(
-              A.codes, A.crit, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write, sc, q,
-              h, (unsigned int*)ovf, dc);
+          const int64_t nblk = cn < ns ? cn : ns;
+          k_walk_block<D><<<(unsigned)nblk, BFS_THREADS, 0, s>>>(A.codes, A.crit, g, dlist, cn, conn_base,
+                                                                 A.out_origin, A.out_terminal, off, A.out_cells,
+                                                                 write, sc, q, h, (unsigned int*)ovf, dc);
           TCK(cudaGetLastError());
           TCK(cudaStreamSynchronize(s));  // lst is pageable host memory
         }
