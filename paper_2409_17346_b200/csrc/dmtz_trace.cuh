@@ -622,7 +622,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
     TCK(cudaGetLastError());
     if (nbk[2]) {  // connectors that outgrew their slot: retry with 16x bigger slots, fewer threads
       int64_t q = slot_q;
-      long long* dlist = (long long*)(ovf + ovf_words + 2);
+      long long* dlist = (long long*)(ovf + ((ovf_words + 3) & ~(int64_t)1));  // 8-byte aligned
       for (int level = 0; level < 8; level++) {
         hov.assign((size_t)ovf_words + 1, 0);
         TCK(cudaMemcpyAsync(hov.data(), ovf, (size_t)ovf_words * 4, cudaMemcpyDeviceToHost, s));
