@@ -1,20 +1,23 @@
 #!/usr/bin/env python3
 """Benchmark of the DMTz hot path on B200 (contract: one JSON line on rank 0).
 
-A STEP is one pass of the whole hot path over one synthetic input: the C-loop
-to its fixed point (a1-a8 of SURVEY.md §8a: setup, reference gradient, every
-round's gradient sweep + classification + edits, edit-list emission) with
-full sweeps (every round evaluates every anchor), followed by the V-path
-traces of the converged field (a9-a11) when the library provides them.
-
-metric  "C-loop Mvoxels/s per iteration" = N * sweeps / step time (BASELINE.json)
-e2e     the same metric through the public API from HOST arrays: pinned H2D of
+STEP    one pass of the C-loop to its fixed point on one synthetic input (rows
+        a1-a8 of SURVEY.md §8a: setup + bound check, reference gradient, every
+        round's gradient screening + classification + Eq. 2 edits, edit-list
+        emission), every round sweeping every anchor (full_sweeps=1).
+value   "C-loop Mvoxels/s per iteration" = N * sweeps / step time (BASELINE.json)
+frontier_mode  the same C-loop in the default frontier mode (bit-identical
+        output): time-to-fixed-point, the second half of BASELINE's metric
+trace   rows a9-a11 (descending / ascending / connector V-paths) of the
+        converged field, timed once after the steps
+e2e     the same metric through the public API from pinned HOST arrays: H2D of
         f and fhat, the C-loop, D2H of g and the edit list, every step
-roofline the sweep of one round (gradient codes of g + classification), timed
-        with CUDA events on the launching stream inside the library, against
-        12 B/voxel algorithmic traffic (read g f32 + cand_f u64)
+roofline the dominant kernel, k_screen (gradient codes of g), on the rounds it
+        sweeps every anchor, timed with CUDA events on the launching stream
+        inside the library; algorithmic work per anchor: 105 SoS compare-selects
+        (210 ALU ops) and 12 B (g f32 + the stored u64 code), DESIGN.md §7
 Workload: BASELINE config C4 (3D 512^3 lognormal "cosmology" field, rel. eps
-1e-4, closed-loop Lorenzo quantizer), inputs 537 MB each > 126 MB L2.
+1e-4, closed-loop Lorenzo quantizer); inputs 537 MB each > 126 MB L2.
 
 --impl reference times the CPU oracle (this tier's reference arm) on a bounded
 crop of the same workload on the host cores.
@@ -36,12 +39,26 @@ sys.path.insert(0, ROOT)
 
 import dmtz_inputs as di  # noqa: E402
 
+METRIC = "C-loop Mvoxels/s per iteration"
+ALU_OPS_PER_ANCHOR = {3: 210, 2: 30}      # 2 x SoS compares per anchor (105 in 3D, 15 in 2D)
+BYTES_PER_ANCHOR = {3: 12, 2: 6}          # g f32 + stored code (u64 3D / u16 2D)
+
 
 def _peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         return {}
+
+
+def _ncu_traffic(kernel: str, workload: str):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        e = d.get(workload, {}).get(kernel)
+        return e["dram_bytes"] if e else None
+    except Exception:
+        return None
 
 
 class Clocks:
@@ -91,7 +108,7 @@ def cpu_cores():
         return os.cpu_count()
 
 
-def oracle_sample(f, fh, xi, edge, budget_s=20.0):
+def oracle_sample(f, fh, xi, edge):
     """Time the oracle (as it stands) on a bounded crop of the workload."""
     import oracle
     oracle.build()
@@ -100,31 +117,28 @@ def oracle_sample(f, fh, xi, edge, budget_s=20.0):
     t0 = time.perf_counter()
     r = oracle.correct(fc, fhc, xi)
     dt = time.perf_counter() - t0
-    n = fc.size
     sweeps = r["stats"]["rounds"] + 1
-    return dict(value=n * sweeps / dt / 1e6, seconds=dt, sweeps=sweeps, shape=list(fc.shape), rounds=r["stats"]["rounds"],
-                threads=oracle.num_threads())
+    return dict(value=fc.size * sweeps / dt / 1e6, seconds=dt, sweeps=sweeps, shape=list(fc.shape),
+                rounds=r["stats"]["rounds"], threads=oracle.num_threads())
 
 
 def run_reference(args, cfg, f, fh, xi):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    if int(os.environ.get("RANK", "0")) != 0:
         return
-    os.environ.setdefault("OMP_NUM_THREADS", str(cpu_cores()))
     vals = []
     for i in range(args.warmup + args.steps):
         s = oracle_sample(f, fh, xi, args.ref_edge)
         if i >= args.warmup:
             vals.append(s)
     v = float(np.median([s["value"] for s in vals]))
-    sample = (f"oracle C-loop to fixed point on the {vals[0]['shape']} crop of {cfg.name} "
+    sample = (f"oracle C-loop to its fixed point on the {vals[0]['shape']} crop of {cfg.name} "
               f"({vals[0]['sweeps']} sweeps, {vals[0]['seconds']:.1f} s each)")
-    line = {"impl": "reference", "metric": "C-loop Mvoxels/s per iteration", "value": v, "unit": "Mvoxels/s",
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Mvoxels/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": float(np.median([s["seconds"] for s in vals]) * 1e3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{cfg.name} {cfg.family} {'x'.join(map(str, cfg.shape))} eps {cfg.eps} (crop)",
-                       "crop": vals[0]["shape"], "parallelism": "host cores"},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{cfg.name} {cfg.family} {'x'.join(map(str, cfg.shape))} rel eps {cfg.eps}",
+                       "crop": vals[0]["shape"], "parallelism": "host cores (OpenMP)"},
             "cpu_baseline": {"value": v, "unit": "Mvoxels/s", "cores": vals[0]["threads"], "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": v, "unit": "Mvoxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -138,12 +152,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dmtz", choices=["dmtz", "reference"])
     ap.add_argument("--config", default="C4")
-    ap.add_argument("--shape", default=None, help="override config shape, e.g. 128,128,128")
-    ap.add_argument("--ref-edge", type=int, default=64, help="oracle crop edge for the CPU baseline")
+    ap.add_argument("--shape", default=None, help="override the config shape, e.g. 128,128,128")
+    ap.add_argument("--ref-edge", type=int, default=96, help="oracle crop edge for the CPU baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-trace", action="store_true")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if args.impl == "dmtz" else args.warmup
+    if args.impl == "dmtz":
+        args.warmup = max(args.warmup, 3)
 
     shape = tuple(int(x) for x in args.shape.split(",")) if args.shape else None
     t0 = time.time()
@@ -161,73 +177,62 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2409_17346_b200 as dmtz
+    if world > 1:
+        from paper_2409_17346_b200 import slab
+        return slab.bench_main(args, f, fh, xi, cfg, world, rank, local)
 
     dev = torch.device("cuda", local)
+    D = len(f.shape)
+    N = f.size
     ft = torch.from_numpy(f).to(dev)
     fht = torch.from_numpy(fh).to(dev)
     ctx = dmtz.Context(f.shape, dev)
     g = torch.empty_like(ft)
-    edits = torch.empty((f.size, 16), dtype=torch.uint8, device=dev)
+    edits = torch.empty((N, 16), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
-    has_trace = True
 
-    def step(profile=False):
-        nonlocal has_trace
-        r = ctx.correct(ft, fht, xi, full_sweeps=True, g_out=g, edits=edits, profile=profile)
-        ntr = 0
-        if has_trace:
-            try:
-                codes = ctx.compute_gradient(g)
-                tr = ctx.trace_separatrices(codes)
-                ntr = int(tr["origin"].shape[0])
-            except dmtz.DmtzError:
-                has_trace = False
-        return r, ntr
+    def step():
+        return ctx.correct(ft, fht, xi, full_sweeps=True, g_out=g, edits=edits, profile=True)
 
     for _ in range(args.warmup):
-        r, _ = step()
+        r = step()
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    times, sweeps, launches, prof = [], [], 0, []
+    times, stats = [], []
     with Clocks(local) as clk:
         for _ in range(args.steps):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            r, ntr = step(profile=True)
+            r = step()
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
-            sweeps.append(r.stats["sweeps"])
-            launches += r.stats.get("launches", 0)
-            prof.append(r.stats)
+            stats.append(r.stats)
     ms = float(np.median(times))
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    N = f.size
-    sw = int(np.median(sweeps))
-    value = N * sw / (ms * 1e-3) / 1e6
+    sweeps = int(np.median([s["sweeps"] for s in stats]))
+    value = N * sweeps / (ms * 1e-3) / 1e6
 
-    # roofline of the per-round sweep (codes of g + classification), live CUDA events
+    # roofline of the dominant kernel (k_screen on the full-sweep rounds), live CUDA events
     peaks = _peaks()
-    hbm = peaks.get("hbm_gbs")
-    sweep_ms = float(np.median([p["sweep_ms"] / max(p["sweeps"], 1) for p in prof]))
-    bytes_alg = N * (12 if len(f.shape) == 3 else 6)
-    achieved = bytes_alg / (sweep_ms * 1e-3) / 1e9
-    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm if hbm else None, "traffic": None,
-            "kernel": "round sweep (gradient of g + classification)", "kernel_ms": sweep_ms,
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else "fallback 6650 GB/s"}
-    if not hbm:
-        roof["peak"] = 6650.0
-        roof["frac"] = achieved / 6650.0
+    hbm = peaks.get("hbm_gbs") or 6650.0
+    sm_mhz = peaks.get("sm_max_mhz") or 1965.0
+    t_launch = float(np.median([s["screen_ms_full"] / max(s["n_screen_full"], 1) for s in stats])) * 1e-3
+    alu_peak = 148 * 64 * sm_mhz * 1e6 / 1e9          # Gop/s: 148 SMs x 4 SMSP x 16-lane ALU pipe
+    alu_achieved = ALU_OPS_PER_ANCHOR[D] * N / t_launch / 1e9
+    gbs = BYTES_PER_ANCHOR[D] * N / t_launch / 1e9
+    workload = f"{cfg.name} {'x'.join(map(str, f.shape))}"
+    traffic = _ncu_traffic("k_screen", workload)
+    roof = {"bound": "alu", "achieved": alu_achieved, "peak": alu_peak, "unit": "Gop/s",
+            "frac": alu_achieved / alu_peak, "traffic": traffic,
+            "kernel": "k_screen (gradient codes of g, every anchor)", "launch_ms": t_launch * 1e3,
+            "alu_ops_per_anchor": ALU_OPS_PER_ANCHOR[D], "bytes_per_anchor": BYTES_PER_ANCHOR[D],
+            "hbm_achieved_gbs": gbs, "hbm_peak_gbs": hbm, "hbm_frac": gbs / hbm,
+            "peak_source": ("ALU: 148 SMs x 64 lanes/clk x MEASURED_PEAKS sm_max_mhz; HBM: MEASURED_PEAKS hbm_gbs"),
+            "share_of_step": float(np.median([s["screen_ms"] for s in stats])) / ms}
 
-    # time-to-fixed-point in the default (frontier) mode: device-resident inputs -> g + edit list
+    # time-to-fixed-point in the default (frontier) mode
     ttfp = []
-    for i in range(3):
+    for _ in range(3):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -237,23 +242,49 @@ def main():
         ttfp.append(e0.elapsed_time(e1))
     assert rf.stats["rounds"] == r.stats["rounds"] and rf.n_edits == r.n_edits
     frontier = {"time_to_fixed_point_ms": float(np.median(ttfp)), "rounds": rf.stats["rounds"],
-                "anchors_swept": rf.stats["anchors_swept"], "sweeps": rf.stats["sweeps"],
-                "full_sweep_equivalents": rf.stats["anchors_swept"] / N}
+                "sweeps": rf.stats["sweeps"], "anchors_swept": rf.stats["anchors_swept"],
+                "full_sweep_equivalents": rf.stats["anchors_swept"] / N,
+                "value": N * rf.stats["sweeps"] / (float(np.median(ttfp)) * 1e-3) / 1e6}
+
+    # traces of the converged field (a9-a11), once
+    trace = None
+    if not args.no_trace:
+        codes = ctx.compute_gradient(g)
+        try:
+            sizes = ctx.trace_sizes(codes)
+            need = sizes["n_branches"] * 33 + sizes["n_cells"] * 8
+            free = torch.cuda.mem_get_info()[0]
+            if need < 0.8 * free:
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                tr = ctx.trace_separatrices(codes, cap_branches=sizes["n_branches"], cap_cells=sizes["n_cells"])
+                e1.record(stream)
+                torch.cuda.synchronize()
+                kinds = torch.bincount(tr["kind"].long(), minlength=5).tolist()
+                trace = {"trace_ms": e0.elapsed_time(e1), "n_branches": sizes["n_branches"],
+                         "n_cells": sizes["n_cells"], "desc": kinds[1], "asc": kinds[2], "conn": kinds[4]}
+                del tr
+            else:
+                trace = {"skipped": f"needs {need / 1e9:.1f} GB of outputs", **sizes}
+        except Exception as e:  # noqa: BLE001
+            trace = {"error": str(e)[:200]}
+        torch.cuda.empty_cache()
 
     e2e = None
     if not args.no_e2e:
         fp = torch.from_numpy(f).pin_memory()
         fhp = torch.from_numpy(fh).pin_memory()
         gh = torch.empty(f.shape, dtype=torch.float32).pin_memory()
-        eh = torch.empty((f.size, 16), dtype=torch.uint8).pin_memory()
+        eh = torch.empty((N, 16), dtype=torch.uint8).pin_memory()
         et = []
-        for i in range(2):
+        for _ in range(2):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             ft.copy_(fp, non_blocking=True)
             fht.copy_(fhp, non_blocking=True)
-            r2, _ = step()
+            r2 = step()
             gh.copy_(g, non_blocking=True)
             ne = r2.n_edits
             eh[:ne].copy_(edits[:ne], non_blocking=True)
@@ -262,36 +293,33 @@ def main():
             et.append(e0.elapsed_time(e1))
         ems = float(np.median(et))
         e2e = {"value": N * r2.stats["sweeps"] / (ems * 1e-3) / 1e6, "unit": "Mvoxels/s",
-               "h2d_bytes_per_step": 2 * 4 * N, "d2h_bytes_per_step": 4 * N + 16 * r2.n_edits,
-               "ms_per_step": ems}
+               "h2d_bytes_per_step": 2 * 4 * N, "d2h_bytes_per_step": 4 * N + 16 * r2.n_edits, "ms_per_step": ems}
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if not args.no_cpu_baseline:
         s = oracle_sample(f, fh, xi, args.ref_edge)
         cpu = {"value": s["value"], "unit": "Mvoxels/s", "cores": s["threads"], "kind": "oracle",
-               "sample": f"oracle C-loop to fixed point on the {s['shape']} crop of {cfg.name} "
+               "sample": f"oracle C-loop to its fixed point on the {s['shape']} crop of {cfg.name} "
                          f"({s['sweeps']} sweeps in {s['seconds']:.1f} s)"}
 
     st = r.stats
     line = {
-        "metric": "C-loop Mvoxels/s per iteration", "value": value, "unit": "Mvoxels/s", "n_gpus": world,
+        "metric": METRIC, "value": value, "unit": "Mvoxels/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{cfg.name} {cfg.family} {'x'.join(map(str, f.shape))} rel eps {cfg.eps}",
-                   "xi": xi, "q_max": 6, "q_cap": 6, "tier": 2, "sweeps_per_step": sw,
-                   "rounds": st["rounds"], "full_sweeps": True, "l2": "inputs > L2 (537 MB each)",
-                   "parallelism": f"slab{world}" if world > 1 else "1 GPU"},
-        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "frontier_mode": frontier,
-        "gpu_launches": launches // max(args.steps, 1),
+                   "xi": xi, "q_max": 6, "q_cap": 6, "tier": 2, "sweeps_per_step": sweeps, "rounds": st["rounds"],
+                   "mode": "full sweeps (every round evaluates every anchor)",
+                   "l2": "inputs larger than L2 (2 x 537 MB)", "parallelism": "1 GPU"},
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "frontier_mode": frontier, "trace": trace,
+        "gpu_launches": st["launches"],
         "clocks": clk.summary(),
         "stats": {k: st[k] for k in ("rounds", "sweeps", "n_edited", "n_quantized", "n_lossless", "n_false_round0",
-                                     "false_by_kind_round0")},
+                                     "false_by_kind_round0", "screen_ms", "decode_ms")},
         "gen_seconds": t_gen,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -110,7 +110,11 @@ typedef struct {
   int64_t sweeps;          /* gradient evaluations of g (rounds + 1 on success) */
   int64_t anchors_swept;   /* sum over sweeps of anchors evaluated (frontier accounting) */
   int64_t launches;        /* kernels this call launched */
-  double sweep_ms;         /* opts.profile: summed device time of the round sweeps */
+  double sweep_ms;         /* opts.profile: summed device time of the round sweeps (screen + decode) */
+  double screen_ms;        /* opts.profile: of which the gradient screening kernel */
+  double decode_ms;        /* opts.profile: of which the classification / target kernel */
+  double screen_ms_full;   /* opts.profile: screening time of the rounds that swept every anchor */
+  int64_t n_screen_full;   /* number of such rounds */
 } dmtz_stats;
 
 typedef struct dmtz_ctx dmtz_ctx;

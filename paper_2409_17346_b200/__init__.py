@@ -52,7 +52,8 @@ class _Stats(ctypes.Structure):
                 ("n_lossless", ctypes.c_int64), ("n_false_round0", ctypes.c_int64),
                 ("false_by_kind_round0", ctypes.c_int64 * 8), ("status", ctypes.c_int32),
                 ("pad", ctypes.c_int32), ("sweeps", ctypes.c_int64), ("anchors_swept", ctypes.c_int64),
-                ("launches", ctypes.c_int64), ("sweep_ms", ctypes.c_double)]
+                ("launches", ctypes.c_int64), ("sweep_ms", ctypes.c_double), ("screen_ms", ctypes.c_double),
+                ("decode_ms", ctypes.c_double), ("screen_ms_full", ctypes.c_double), ("n_screen_full", ctypes.c_int64)]
 
 
 class _Seps(ctypes.Structure):
@@ -195,7 +196,8 @@ class Context:
         stats = dict(rounds=st.rounds, n_edited=st.n_edited, n_quantized=st.n_quantized, n_lossless=st.n_lossless,
                      n_false_round0=st.n_false_round0, false_by_kind_round0=list(st.false_by_kind_round0),
                      status=status, sweeps=st.sweeps, anchors_swept=st.anchors_swept, launches=st.launches,
-                     sweep_ms=st.sweep_ms)
+                     sweep_ms=st.sweep_ms, screen_ms=st.screen_ms, decode_ms=st.decode_ms,
+                     screen_ms_full=st.screen_ms_full, n_screen_full=st.n_screen_full)
         msg = _lib.dmtz_last_error().decode() if status != OK else ""
         if raise_on_error and status not in (OK, E_STUCK, E_ITER_CAP, E_CAPACITY):
             raise DmtzError(status, msg)
@@ -203,6 +205,32 @@ class Context:
                       message=msg)
 
     # ---------------------------------------------------------------- traces
+    def trace_sizes(self, codes: torch.Tensor, kinds: int = KIND_DESC | KIND_ASC | KIND_CONN, stream=None):
+        """Branch and cell counts of the traces (two sizing calls: branches, then cells)."""
+        _need_cuda(codes)
+        nb, nc = ctypes.c_int64(), ctypes.c_int64()
+        seps = _Seps(None, None, None, None, None)
+        one = torch.empty(8, dtype=torch.int64, device=codes.device)
+        seps.branch_offsets = ctypes.c_void_p(one.data_ptr())
+        st = _lib.dmtz_trace_separatrices(self._h, ctypes.c_void_p(codes.data_ptr()), kinds,
+                                          ctypes.c_void_p(self.workspace.data_ptr()), self.ws_bytes,
+                                          ctypes.byref(seps), 0, 0, ctypes.byref(nb), ctypes.byref(nc),
+                                          _stream_ptr(stream))
+        if st not in (OK, E_CAPACITY):
+            _check(st)
+        n_b = nb.value
+        bufs = [torch.empty(max(n_b, 1) + 1, dtype=torch.int64, device=codes.device) for _ in range(3)]
+        kb = torch.empty(max(n_b, 1), dtype=torch.uint8, device=codes.device)
+        seps = _Seps(ctypes.c_void_p(bufs[0].data_ptr()), None, ctypes.c_void_p(bufs[1].data_ptr()),
+                     ctypes.c_void_p(bufs[2].data_ptr()), ctypes.c_void_p(kb.data_ptr()))
+        st = _lib.dmtz_trace_separatrices(self._h, ctypes.c_void_p(codes.data_ptr()), kinds,
+                                          ctypes.c_void_p(self.workspace.data_ptr()), self.ws_bytes,
+                                          ctypes.byref(seps), n_b, 0, ctypes.byref(nb), ctypes.byref(nc),
+                                          _stream_ptr(stream))
+        if st not in (OK, E_CAPACITY):
+            _check(st)
+        return {"n_branches": n_b, "n_cells": nc.value}
+
     def trace_separatrices(self, codes: torch.Tensor, kinds: int = KIND_DESC | KIND_ASC | KIND_CONN,
                            cap_branches: int | None = None, cap_cells: int | None = None, stream=None):
         """V-path traces -> dict of CUDA tensors (CSR)."""

@@ -27,7 +27,7 @@ struct dmtz_ctx {
   int device;
   int rank, world;
   Counters* host_cnt;  // pinned
-  cudaEvent_t ev[2];   // sweep timing (opts.profile)
+  cudaEvent_t ev[3];   // sweep timing (opts.profile): screen | decode
   int verbose;         // DMTZ_VERBOSE=1: per-round counters on stderr
 };
 
@@ -184,9 +184,10 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
     if (frontier_mode && round > 1) CK(cudaMemsetAsync(ebits, 0, rowbit_bytes, s));
     if (o->profile) CK(cudaEventRecord(c->ev[0], s));
     k_screen<D><<<sweep_blocks, 256, 0, s>>>(g_out, cand_g, ebits, units, n_units, g, rg, round == 1 ? 1 : 0, dc);
+    if (o->profile) CK(cudaEventRecord(c->ev[1], s));
     k_decode<D><<<sweep_blocks * 2, DECODE_THREADS, 0, s>>>(f, cand_f, crit_f, cand_g, crit_g, ebits, fmark, tbits, units, n_units,
                                              g, rg, tmask, lowpos, round == 1 ? 1 : 0, dc);
-    if (o->profile) CK(cudaEventRecord(c->ev[1], s));
+    if (o->profile) CK(cudaEventRecord(c->ev[2], s));
     k_edit_rows<D><<<wblocks, ethreads, frontier_mode ? fwords_smem * 4 : 0, s>>>(
         tbits, nwords, fhat, lb, g_out, state, dc, step, o->q_cap, frontier_mode ? fbits : nullptr, g, rg,
         frontier_mode ? fwords_smem : 0);
@@ -202,9 +203,13 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
     }
     CK(cudaStreamSynchronize(s));
     if (o->profile) {
-      float ms = 0.f;
-      CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
-      st->sweep_ms += ms;
+      float ms0 = 0.f, ms1 = 0.f;
+      CK(cudaEventElapsedTime(&ms0, c->ev[0], c->ev[1]));
+      CK(cudaEventElapsedTime(&ms1, c->ev[1], c->ev[2]));
+      st->sweep_ms += ms0 + ms1;
+      st->screen_ms += ms0;
+      st->decode_ms += ms1;
+      if (ms0 > 0 && (int64_t)hc->n_swept == g.N) { st->screen_ms_full += ms0; st->n_screen_full++; }
     }
     st->sweeps++;
     st->anchors_swept += (int64_t)hc->n_swept;
@@ -290,7 +295,7 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
   c->verbose = vb && vb[0] == '1';
   cudaError_t e = cudaMallocHost((void**)&c->host_cnt, sizeof(Counters) * 2);
   if (e != cudaSuccess) { delete c; set_err("cudaMallocHost: %s", cudaGetErrorString(e)); return DMTZ_E_CUDA; }
-  for (int i = 0; i < 2; i++) {
+  for (int i = 0; i < 3; i++) {
     e = cudaEventCreate(&c->ev[i]);
     if (e != cudaSuccess) { set_err("cudaEventCreate: %s", cudaGetErrorString(e)); return DMTZ_E_CUDA; }
   }
@@ -301,8 +306,7 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
 void dmtz_ctx_destroy(dmtz_ctx* c) {
   if (!c) return;
   cudaFreeHost(c->host_cnt);
-  cudaEventDestroy(c->ev[0]);
-  cudaEventDestroy(c->ev[1]);
+  for (int i = 0; i < 3; i++) cudaEventDestroy(c->ev[i]);
   delete c;
 }
 

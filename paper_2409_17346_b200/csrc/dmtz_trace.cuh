@@ -573,6 +573,11 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   const int64_t nb = nbk[0] + nbk[1] + nbk[2];
   A.n_branches = nb;
   if (nb > A.cap_b) return cudaSuccess;  // caller reports DMTZ_E_CAPACITY with the needed size
+  if (nb == 0) {
+    if (A.out_offsets) TCK(cudaMemsetAsync(A.out_offsets, 0, 8, s));
+    TCK(cudaStreamSynchronize(s));
+    return cudaSuccess;
+  }
   int64_t base = 0;
   for (int ki = 0; ki < 3; ki++) {
     const int kind = kinds_list[ki];
