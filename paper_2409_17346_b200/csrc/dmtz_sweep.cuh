@@ -150,8 +150,8 @@ struct TargetTables {
   uint32_t tinfo[26];      // dim | nv << 2 | shift << 5 | none << 11 | nfacet << 15
   uint32_t vm[26];         // vertex delta masks, 3 bits each
   uint32_t fac[26][4];     // dm | ft << 3 | slot << 8 | k << 12
-  int64_t loff[26][14];    // link slot -> linear offset
-  int64_t doff[8];         // delta mask -> linear offset
+  int32_t loff[26][14];    // link slot -> linear offset (|offset| <= nx*ny + nx + 1)
+  int32_t doff[8];         // delta mask -> linear offset
 };
 
 template <int D>
@@ -171,10 +171,10 @@ __device__ __forceinline__ void init_target_tables(TargetTables& T, const Grid& 
                       ((uint32_t)t_facet<D>(t, j, 2) << 8) | ((uint32_t)t_facet<D>(t, j, 3) << 12);
 #pragma unroll
       for (int q = 0; q < 14; q++)
-        T.loff[t][q] = t_link<D>(t, q, 0) + t_link<D>(t, q, 1) * g.sy + t_link<D>(t, q, 2) * g.sz;
+        T.loff[t][q] = (int32_t)(t_link<D>(t, q, 0) + t_link<D>(t, q, 1) * g.sy + t_link<D>(t, q, 2) * g.sz);
     }
 #pragma unroll
-    for (int m = 0; m < 8; m++) T.doff[m] = mask_delta(g, m);
+    for (int m = 0; m < 8; m++) T.doff[m] = (int32_t)mask_delta(g, m);
   }
   __syncthreads();
 }
@@ -187,41 +187,44 @@ __device__ __forceinline__ uint64_t pick(const uint64_t (&c)[N], int i) {
   return r;
 }
 
-// Rules R1 / R2 / R3a / R3b for the false cell (u, t).  The
-// anchor's codes at u + {0,1}^D are read from the warp's shared-memory copy
-// (cfs[dm * 32 + src], cgs[dm * 32 + src]).
+// field of a code held as two 32-bit halves (funnel shift: one SHF for shift < 32)
+__device__ __forceinline__ uint32_t field2(uint2 c, int shift, uint32_t none) {
+  const uint32_t w = shift < 32 ? __funnelshift_r(c.x, c.y, shift) : (c.y >> (shift - 32));
+  return w & none;
+}
+
+// Rules R1 / R2 / R3a / R3b for the false cell (anchor u, type t):
+// returns the target's offset from u.  The anchor's codes at u + {0,1}^D come
+// from the warp's shared-memory copy (cfs[dm * 32 + src], cgs[dm * 32 + src]).
+// Returns INT32_MIN on an internal inconsistency.
 template <int D>
-__device__ __forceinline__ int64_t target_dyn(const TargetTables& T, int64_t u, int t, bool fn, uint64_t lowpos,
-                                              const unsigned long long* cfs, const unsigned long long* cgs,
-                                              int src) {
+__device__ __forceinline__ int32_t target_off(const TargetTables& T, int t, bool fn, uint64_t lowpos,
+                                              const uint2* cfs, const uint2* cgs, int src) {
   const uint32_t ti = T.tinfo[t];
   const int dim = ti & 3, shift = (ti >> 5) & 63, nfacet = (ti >> 15) & 7;
   const uint32_t none = (ti >> 11) & 15;
-  const uint32_t vm = T.vm[t];
-  // m = the f-lowest vertex of the cell (SoS), precomputed per anchor and type
+  // m = the cell's f-lowest vertex (SoS), precomputed per anchor and type
   const int mp = (int)(lowpos >> (2 * t)) & 3;
-  const int64_t m = u + T.doff[(vm >> (3 * mp)) & 7];
+  const int32_t m_off = T.doff[(T.vm[t] >> (3 * mp)) & 7];
+  const bool has_cand = dim < Tr<D>::TOP;
   if (!fn) {                                        // FP: paired in f, critical in g (R1)
-    if (dim < Tr<D>::TOP) {
-      const uint32_t sl = (uint32_t)(cfs[src] >> shift) & none;
-      if (sl != none) return u + T.loff[t][sl];
-    }
-    return m;                                       // paired down in f: the f-lowest vertex
+    const uint32_t sl = has_cand ? field2(cfs[src], shift, none) : none;
+    return sl != none ? T.loff[t][sl] : m_off;      // paired up: its cofacet's vertex; down: m
   }
-  if (dim < Tr<D>::TOP && ((uint32_t)(cgs[src] >> shift) & none) != none) return m;   // R2
+  if (has_cand && field2(cgs[src], shift, none) != none) return m_off;   // R2
   for (int j = 0; j < nfacet; j++) {                // paired down in g with gamma: R3a / R3b
     const uint32_t fc = T.fac[t][j];
     const int dm = fc & 7, ft = (fc >> 3) & 31, sl = (fc >> 8) & 15, k = (fc >> 12) & 3;
     const uint32_t fti = T.tinfo[ft];
     const int fsh = (fti >> 5) & 63;
     const uint32_t fno = (fti >> 11) & 15;
-    if (((uint32_t)(cgs[dm * 32 + src] >> fsh) & fno) != (uint32_t)sl) continue;
-    if (mp != k) return m;                          // R3a: y = the vertex omitted by gamma
-    const uint32_t s2 = (uint32_t)(cfs[dm * 32 + src] >> fsh) & fno;
-    if (s2 == fno) return -1;
-    return u + T.doff[dm] + T.loff[ft][s2];
+    if (field2(cgs[dm * 32 + src], fsh, fno) != (uint32_t)sl) continue;
+    if (mp != k) return m_off;                      // R3a: y = the vertex gamma omits
+    const uint32_t s2 = field2(cfs[dm * 32 + src], fsh, fno);   // R3b
+    if (s2 == fno) return INT32_MIN;
+    return T.doff[dm] + T.loff[ft][s2];
   }
-  return -1;
+  return INT32_MIN;
 }
 
 // ---------------------------------------------------------------------------
@@ -230,8 +233,8 @@ __device__ __forceinline__ int64_t target_dyn(const TargetTables& T, int64_t u, 
 // ---------------------------------------------------------------------------
 constexpr int DECODE_THREADS = 128;
 struct DecodeWarpSmem {
-  unsigned long long cf[8 * 32];
-  unsigned long long cg[8 * 32];
+  uint2 cf[8 * 32];
+  uint2 cg[8 * 32];
   unsigned long long lowpos[32];
   uint32_t critf[32];
   uint16_t items[32 * 26];
@@ -252,7 +255,10 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
   DecodeWarpSmem& W = WS[threadIdx.x >> 5];
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long k0 = 0, k1 = 0, k2 = 0, k3 = 0, k4 = 0, k5 = 0, k6 = 0, k7 = 0;
+  __shared__ unsigned int kcs[8];
+  if (threadIdx.x < 8) kcs[threadIdx.x] = 0;
+  __syncthreads();
+  unsigned int* kc = kcs;  // kind counts of round 1 (shared-memory histogram)
   unsigned long long nfalse = 0, nint = 0;
   // items = (unit, row, group of 32 row chunks); lane j of the warp first scans
   // chunk c0 + j (changed-code words of u + {0,1}^D and the false-cell mark),
@@ -335,7 +341,10 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
     pre -= nmine;
     if (diff) {
 #pragma unroll
-      for (int dm = 0; dm < Tr<D>::NDELTA; dm++) { W.cf[dm * 32 + lane] = cf[dm]; W.cg[dm * 32 + lane] = cgv[dm]; }
+      for (int dm = 0; dm < Tr<D>::NDELTA; dm++) {
+        W.cf[dm * 32 + lane] = make_uint2((uint32_t)cf[dm], (uint32_t)(cf[dm] >> 32));
+        W.cg[dm * 32 + lane] = make_uint2((uint32_t)cgv[dm], (uint32_t)(cgv[dm] >> 32));
+      }
       W.critf[lane] = critf;
       W.lowpos[lane] = __ldg(lowpos_f + u);
       uint32_t dd = diff;
@@ -349,7 +358,8 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
     const int64_t ubase = u - lane;
     for (int i0 = 0; i0 < total; i0 += 32) {
       const int i = i0 + lane;
-      int64_t tv = -1;
+      bool have_t = false;
+      uint32_t word = 0, bit = 0;
       if (i < total) {
         const int item = W.items[i];
         const int src = item & 31, t = item >> 5;
@@ -357,18 +367,22 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
         if (count_kinds) {
           const int dim = T.tinfo[t] & 3;
           const int cls = (dim == Tr<D>::TOP) ? 3 : dim;
-          const int kind = 2 * cls + (fn ? 1 : 0);
-          k0 += kind == 0; k1 += kind == 1; k2 += kind == 2; k3 += kind == 3;
-          k4 += kind == 4; k5 += kind == 5; k6 += kind == 6; k7 += kind == 7;
+          atomicAdd(kc + 2 * cls + (fn ? 1 : 0), 1u);
         }
-        tv = target_dyn<D>(T, ubase + src, t, fn, W.lowpos[src], W.cf, W.cg, src);
-        if (tv < 0) nint++;
+        const int32_t off = target_off<D>(T, t, fn, W.lowpos[src], W.cf, W.cg, src);
+        if (off == INT32_MIN) {
+          nint++;
+        } else {
+          const int64_t tv = ubase + src + off;
+          word = (uint32_t)(tv >> 5);
+          bit = 1u << (tv & 31);
+          have_t = true;
+        }
       }
-      const unsigned have = __ballot_sync(0xffffffffu, tv >= 0);
-      if (tv >= 0) {
-        const int64_t word = tv >> 5;
+      const unsigned have = __ballot_sync(0xffffffffu, have_t);
+      if (have_t) {
         const unsigned same = __match_any_sync(have, word);
-        const uint32_t bits = __reduce_or_sync(same, 1u << (tv & 31));
+        const uint32_t bits = __reduce_or_sync(same, bit);
         if (lane == __ffs(same) - 1) atomicOr(tbits + word, bits);
       }
     }
@@ -377,9 +391,8 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
   }
   warp_add(&cnt->n_false, nfalse);
   warp_add(&cnt->n_internal, nint);
-  warp_add(&cnt->kinds[0], k0); warp_add(&cnt->kinds[1], k1); warp_add(&cnt->kinds[2], k2);
-  warp_add(&cnt->kinds[3], k3); warp_add(&cnt->kinds[4], k4); warp_add(&cnt->kinds[5], k5);
-  warp_add(&cnt->kinds[6], k6); warp_add(&cnt->kinds[7], k7);
+  __syncthreads();
+  if (count_kinds && threadIdx.x < 8 && kcs[threadIdx.x]) atomicAdd(&cnt->kinds[threadIdx.x], (unsigned long long)kcs[threadIdx.x]);
 }
 
 // ---------------------------------------------------------------------------

@@ -192,3 +192,73 @@ def test_trace_capacity(dmtz):
     nd = int((ref["kind"] == 1).sum())
     assert tr["origin"].shape[0] == nd
     assert np.array_equal(tr["cells"].cpu().numpy().view(np.uint64), ref["cells"][:ref["offsets"][nd]])
+
+
+# ----------------------------------------------------------------------------- full BASELINE sizes
+def _crop_check(full_codes, full_crit, fld, rng, shape, edge, n=4):
+    """Oracle gradient of random crops vs the GPU result on the full field, on the crop
+    anchors whose codes (margin 1) and criticality (margin 1 below, 2 above) cannot see
+    the crop boundary."""
+    D = len(shape)
+    for _ in range(n):
+        lo = [int(rng.integers(0, s - edge + 1)) for s in shape]
+        sl = tuple(slice(l, l + edge) for l in lo)
+        oc, om = oracle.gradient(np.ascontiguousarray(fld[sl]))
+        inner_c = tuple(slice(1, edge - 1) for _ in range(D))
+        inner_m = tuple(slice(1, edge - 2) for _ in range(D))
+        gc, gm = full_codes[sl], full_crit[sl]
+        assert np.array_equal(gc[inner_c], oc[inner_c])
+        assert np.array_equal(gm[inner_m], om[inner_m])
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+def test_full_size_gradient_sampled(dmtz, name):
+    f, fh, xi, cfg = di.config_inputs(name)
+    rng = np.random.default_rng(7)
+    edge = 96 if len(cfg.shape) == 2 else 20
+    for fld in (f, fh):
+        gc = dmtz.compute_gradient(_cuda(fld))
+        gm = dmtz.critical_mask(gc).cpu().numpy().view(np.uint32)
+        _crop_check(_codes_np(gc), gm, fld, rng, cfg.shape, edge)
+
+
+def test_full_size_cloop_C2_bit_exact(dmtz):
+    """BASELINE config C2 (2D 1800x3600) end to end against the full oracle run."""
+    f, fh, xi, _ = di.config_inputs("C2")
+    r, ref = _compare_correct(dmtz, f, fh, xi)
+    assert ref["stats"]["rounds"] > 10
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_full_size_cloop_properties(dmtz, name):
+    """Full-size C-loop (the launch configuration bench.py times): exact error bound,
+    monotone edits, edit list replays g, and no false critical cell at exit -- checked
+    by the oracle on sampled crops of f and g."""
+    f, fh, xi, cfg = di.config_inputs(name)
+    r = dmtz.correct(_cuda(f), _cuda(fh), xi, full_sweeps=True)
+    assert r.status == dmtz.OK and r.stats["rounds"] > 0
+    g = r.g.cpu().numpy()
+    F, FH, G = f.astype(np.float64), fh.astype(np.float64), g.astype(np.float64)
+    assert np.all(G <= FH) and np.all(np.abs(G - F) <= np.float64(np.float32(xi)))
+    e = r.edits_numpy()
+    assert np.all(np.diff(e["v"].astype(np.int64)) > 0)
+    rec = fh.ravel().copy()
+    step = np.float32(xi) * np.float32(2.0 ** -6)
+    ql = e["lossless"] == 0
+    rec[e["v"][ql]] = (fh.ravel()[e["v"][ql]] - (e["q"][ql].astype(np.float32) * step).astype(np.float32))
+    rec[e["v"][~ql]] = e["value"][~ql]
+    assert np.array_equal(rec.view(np.uint32), g.ravel().view(np.uint32))
+    changed = np.nonzero(g.ravel() != fh.ravel())[0]
+    assert np.isin(changed, e["v"]).all()
+    # crit(g) == crit(f) everywhere on the GPU, and on oracle-sampled crops
+    cf = dmtz.critical_mask(dmtz.compute_gradient(_cuda(f)))
+    cg = dmtz.critical_mask(dmtz.compute_gradient(r.g))
+    assert torch.equal(cf, cg)
+    rng = np.random.default_rng(11)
+    for _ in range(4):
+        lo = [int(rng.integers(0, s - 20 + 1)) for s in cfg.shape]
+        sl = tuple(slice(l, l + 20) for l in lo)
+        _, mf = oracle.gradient(np.ascontiguousarray(f[sl]))
+        _, mg = oracle.gradient(np.ascontiguousarray(g[sl]))
+        inner = tuple(slice(1, 18) for _ in cfg.shape)
+        assert np.array_equal(mf[inner], mg[inner])
