@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdmtz.so")
 SOURCES = ["dmtz_api.cu"]
-HEADERS = ["dmtz_kernels.cuh", "dmtz_trace.cuh", "dmtz_tables.h"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 NVCC_FLAGS = [
     "-std=c++17", "-O3", "-lineinfo",

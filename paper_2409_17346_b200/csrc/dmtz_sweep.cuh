@@ -241,7 +241,7 @@ struct DecodeWarpSmem {
 };
 
 template <int D>
-__global__ void __launch_bounds__(DECODE_THREADS, 5)
+__global__ void __launch_bounds__(DECODE_THREADS, 8)
 k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__ cand_f,
          const uint32_t* __restrict__ crit_f, const typename Tr<D>::code_t* __restrict__ cg,
          uint32_t* __restrict__ crit_g, const uint32_t* __restrict__ ebits, uint32_t* __restrict__ fmark,
