@@ -191,6 +191,39 @@ dmtz_status dmtz_trace_separatrices(dmtz_ctx* ctx, const void* codes, uint32_t k
                                     int64_t* n_branches /* host */, int64_t* n_cells /* host */,
                                     dmtz_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * Slab mode (multi-GPU z-slab decomposition).  One context per
+ * rank, created for its LOCAL grid: the owned z-planes plus up to 3 halo planes
+ * below and above (nz_local = own + halos).  The caller drives the rounds and,
+ * between them, refreshes the halo planes of g from the neighbouring ranks (the
+ * library never communicates).  Cells are classified only when anchored in local
+ * planes [anchor_z0, anchor_z1) -- own_z0 - 2 .. own_z1 + 1 clipped to the grid:
+ * every cell whose target can be an owned vertex -- and only owned vertices are
+ * edited, so the rounds are those of dmtz_correct on the global grid and the
+ * concatenated edit lists are its edit list (bit for bit).
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int64_t z_offset;              /* global z of local plane 0 */
+  int64_t own_z0, own_z1;        /* owned local planes */
+  int64_t anchor_z0, anchor_z1;  /* local planes whose anchored cells are classified */
+} dmtz_slab;
+
+/* Validate (finite, |fhat - f| <= xi), lb, g = fhat, gradient of f on the local grid. */
+dmtz_status dmtz_slab_begin(dmtz_ctx* ctx, const float* f, const float* fhat, const dmtz_correct_opts* opts,
+                            const dmtz_slab* slab, void* workspace, size_t workspace_bytes, float* g,
+                            dmtz_stream_t stream);
+/* One round (a3-a6) with g's halo planes current.  counters (host, 4): false cells
+ * anchored in the classified planes, targets that moved, targets, invariant
+ * violations; kinds (host, 8): false cells by kind (round 1 only, else zero).
+ * The caller sums counters over ranks and stops as dmtz_correct does. */
+dmtz_status dmtz_slab_round(dmtz_ctx* ctx, const float* f, const float* fhat, const dmtz_correct_opts* opts,
+                            const dmtz_slab* slab, void* workspace, size_t workspace_bytes, float* g,
+                            int64_t round, int64_t* counters, int64_t* kinds, dmtz_stream_t stream);
+/* The owned edits (global vertex indices, sorted). */
+dmtz_status dmtz_slab_end(dmtz_ctx* ctx, const dmtz_slab* slab, void* workspace, size_t workspace_bytes,
+                          const float* g, dmtz_edit* edits, int64_t edits_capacity, int64_t* n_edits /* host */,
+                          int64_t* n_lossless /* host */, dmtz_stream_t stream);
+
 const char* dmtz_status_string(dmtz_status s);
 const char* dmtz_last_error(void);
 int dmtz_version(void);

@@ -61,8 +61,10 @@ def lib():
                                           ctypes.c_int32, i64, P, P, P, i64, P,
                                           ctypes.POINTER(_Stats)]
         L.dmtz_oracle_trace.argtypes = [P, P, ctypes.c_uint32, i64, i64, P, P, P, P, P, P, P]
+        L.dmtz_oracle_slab_round.argtypes = [P, P, P, ctypes.c_float, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                             i64, i64, i64, i64, P, P, P, P]
         for fn in ("dmtz_oracle_gradient", "dmtz_oracle_complex_info", "dmtz_oracle_cell_counts",
-                   "dmtz_oracle_correct", "dmtz_oracle_trace", "dmtz_oracle_num_threads"):
+                   "dmtz_oracle_correct", "dmtz_oracle_trace", "dmtz_oracle_num_threads", "dmtz_oracle_slab_round"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -171,3 +173,21 @@ def trace(field: np.ndarray, kinds: int = KIND_DESC | KIND_ASC | KIND_CONN,
         raise RuntimeError(f"oracle trace status {st}")
     return dict(offsets=off[:nb + 1], cells=cells[:nc], origin=origin[:nb], terminal=term[:nb],
                 kind=kind[:nb])
+
+
+def slab_round(f, fhat, xi, g, state, anchor_planes, owned_planes, q_max=6, q_cap=None, tier=2):
+    """One literal C-loop round on a z-slab (local arrays incl. halos; g, state updated
+    in place).  Returns (n_false, n_changed, n_targets, kinds[8])."""
+    f = np.ascontiguousarray(f, dtype=np.float32)
+    fhat = np.ascontiguousarray(fhat, dtype=np.float32)
+    assert g.dtype == np.float32 and g.flags.c_contiguous and state.dtype == np.uint32
+    d = _dims(f.shape)
+    out = np.zeros(3, np.int64)
+    kinds = np.zeros(8, np.int64)
+    st = lib().dmtz_oracle_slab_round(_p(d), _p(f), _p(fhat), ctypes.c_float(xi), q_max,
+                                      q_max if q_cap is None else q_cap, tier, anchor_planes[0],
+                                      anchor_planes[1], owned_planes[0], owned_planes[1], _p(g), _p(state),
+                                      _p(out), _p(kinds))
+    if st:
+        raise RuntimeError(f"oracle slab_round status {st}")
+    return int(out[0]), int(out[1]), int(out[2]), kinds

@@ -799,3 +799,61 @@ int dmtz_oracle_cell_counts(const int64_t* dims, int64_t* counts /* [4] */) {
       if (cell_exists(&cx, A, ti)) counts[cx.t[ti].dim]++;
   return OR_OK;
 }
+
+/* ------------------------------------------------------------------------- */
+/* One synchronous C-loop round on a z-slab (for the multi-rank tests).        */
+/* The local grid is the slab plus halo planes; only cells anchored in local   */
+/* planes [az0, az1) are classified and only targets in planes [oz0, oz1)      */
+/* (the owned planes) are edited.  Same literal rules as dmtz_oracle_correct.  */
+/* out = {n_false (anchored in owned planes), n_changed, n_targets}; kinds[8]. */
+/* ------------------------------------------------------------------------- */
+int dmtz_oracle_slab_round(const int64_t* dims, const float* f, const float* fhat, float xi, int32_t q_max,
+                           int32_t q_cap, int32_t tier, int64_t az0, int64_t az1, int64_t oz0, int64_t oz1,
+                           float* g, uint32_t* state, int64_t* out, int64_t* kinds) {
+  int st = check_dims(dims);
+  if (st) return st;
+  cx_t cx; build_complex(&cx, dims[0], dims[1], dims[2]);
+  int64_t N = cx.N, plane = cx.n[0] * cx.n[1];
+  grad_t Gf, Gg;
+  uint8_t* T = (uint8_t*)calloc(N, 1);
+  if (!T || !grad_alloc(&cx, &Gf) || !grad_alloc(&cx, &Gg)) return OR_E_ARG;
+  gradient(&cx, f, &Gf);
+  gradient(&cx, g, &Gg);
+  int64_t nF = 0, bad = 0;
+  for (int64_t A = az0 * plane; A < az1 * plane && A < N; A++) {
+    for (int ti = 0; ti < cx.T; ti++) {
+      int d = cx.t[ti].dim;
+      if (tier == 1 && d != 0 && d != cx.top) continue;
+      if (!cell_exists(&cx, A, ti)) continue;
+      int cf = is_crit(&cx, &Gf, A, ti), cg = is_crit(&cx, &Gg, A, ti);
+      if (cf == cg) continue;
+      if (A >= oz0 * plane && A < oz1 * plane) {  /* each anchor is counted by its owner */
+        nF++;
+        kinds[kind_of(&cx, d, cf)]++;
+      }
+      int64_t v = target_of(&cx, f, &Gf, &Gg, A, ti, cf);
+      if (v < 0) { bad++; continue; }
+      if (v >= oz0 * plane && v < oz1 * plane) T[v] = 1;
+    }
+  }
+  float step = ldexpf(xi, -q_max);
+  int64_t changed = 0, targets = 0;
+  for (int64_t v = 0; v < N; v++) {
+    if (!T[v]) continue;
+    targets++;
+    uint32_t q = state[v] & 0xFFFFu, ll = state[v] >> 16;
+    if (ll) continue;
+    changed++;
+    float lb = lower_bound_ru(f[v], xi);
+    if ((int64_t)q + 1 <= q_cap) {
+      float s = (float)(q + 1) * step;
+      float gp = fhat[v] - s;
+      if (gp >= lb) { state[v] = q + 1; g[v] = gp; continue; }
+    }
+    g[v] = lb;
+    state[v] = q | (1u << 16);
+  }
+  out[0] = nF; out[1] = changed; out[2] = targets;
+  free(T); grad_free(&Gf); grad_free(&Gg);
+  return bad ? OR_E_INTERNAL : OR_OK;
+}

@@ -55,8 +55,8 @@ inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 // Workspace layout (offsets from the base, each 256-B aligned)
 struct Layout {
-  size_t cand_f, cand_g, crit_f, crit_g, lowpos, lb, state, tbits, counters, edit_bc, ebits, fmark, units, frontier, trace,
-      total;
+  size_t cand_f, cand_g, crit_f, crit_g, lowpos, lb, state, tbits, counters, edit_bc, ebits, fmark, units, units2,
+      frontier, trace, total;
   int64_t fwords;  // frontier bitmap words (one bit per row-block unit)
 };
 
@@ -82,6 +82,7 @@ Layout layout_for(const dmtz_ctx* c) {
   L.ebits = o; o += align_up((size_t)(c->g.nz * c->g.ny * rg.wpr) * 4 + 64);
   L.fmark = o; o += align_up((size_t)(c->g.nz * c->g.ny * rg.wpr) * 4 + 64);
   L.units = o; o += align_up((size_t)rg.units * 4);
+  L.units2 = o; o += align_up((size_t)rg.units * 4);
   L.frontier = o; o += align_up(L.fwords * 4 + 64);
   L.trace = o; o += align_up(trace_scratch_bytes(c->g, c->D));
   L.total = o;
@@ -110,98 +111,172 @@ uint32_t tier_mask(int tier) {
   return D == 3 ? (1u | (0x3Fu << 20)) : (1u | (0x3u << 4));
 }
 
+// Device views of the workspace
+template <int D>
+struct WS {
+  using code_t = typename Tr<D>::code_t;
+  code_t* cand_f;
+  code_t* cand_g;            // codes of g, memoized across rounds
+  uint32_t *crit_f, *crit_g, *state, *tbits, *ebits, *fmark, *units, *units2, *fbits;
+  unsigned long long* lowpos;
+  float* lb;
+  Counters* dc;
+  unsigned long long* bc;
+  size_t rowbit_bytes;
+  WS(char* ws, const Layout& L, const Grid& g) {
+    cand_f = (code_t*)(ws + L.cand_f);
+    cand_g = (code_t*)(ws + L.cand_g);
+    crit_f = (uint32_t*)(ws + L.crit_f);
+    crit_g = (uint32_t*)(ws + L.crit_g);
+    lowpos = (unsigned long long*)(ws + L.lowpos);
+    lb = (float*)(ws + L.lb);
+    state = (uint32_t*)(ws + L.state);
+    tbits = (uint32_t*)(ws + L.tbits);
+    dc = (Counters*)(ws + L.counters);
+    bc = (unsigned long long*)(ws + L.edit_bc);
+    ebits = (uint32_t*)(ws + L.ebits);
+    fmark = (uint32_t*)(ws + L.fmark);
+    units = (uint32_t*)(ws + L.units);
+    units2 = (uint32_t*)(ws + L.units2);
+    fbits = (uint32_t*)(ws + L.frontier);
+    const RowGeom rg = row_geom(g);
+    rowbit_bytes = (size_t)(g.nz * g.ny * rg.wpr) * 4;
+  }
+};
+
+inline int clamp_blocks(int64_t n, int threads, int64_t cap = 148 * 32) {
+  int64_t b = (n + threads - 1) / threads;
+  return (int)(b < 1 ? 1 : b < cap ? b : cap);
+}
+
+// a1 + a2: validate, lb, g = fhat, state = 0, codes / criticality / lowest vertex of f.
+// Error messages report vertex index + v_report_off (the global index in slab mode).
+template <int D>
+dmtz_status setup_phase(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o, WS<D>& W,
+                        float* g_out, int64_t v_report_off, int64_t* launches, cudaStream_t s) {
+  const Grid& g = c->g;
+  Counters* hc = c->host_cnt;
+  const int64_t nwords = (g.N + 31) / 32;
+  CK(cudaMemsetAsync(W.dc, 0, sizeof(Counters), s));
+  CK(cudaMemsetAsync(&W.dc->first_nonfinite, 0xFF, 16, s));
+  CK(cudaMemsetAsync(W.tbits, 0, nwords * 4, s));
+  CK(cudaMemsetAsync(W.fmark, 0, W.rowbit_bytes, s));
+  k_setup<<<clamp_blocks(g.N, 256), 256, 0, s>>>(f, fhat, o->xi, g.N, W.lb, g_out, W.state, W.dc);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(hc, W.dc, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (hc->first_nonfinite != ~0ull) {
+    set_err("non-finite value at vertex %llu", hc->first_nonfinite + (unsigned long long)v_report_off);
+    return DMTZ_E_NONFINITE;
+  }
+  if (hc->first_bound != ~0ull) {
+    set_err("|fhat - f| > xi at vertex %llu", hc->first_bound + (unsigned long long)v_report_off);
+    return DMTZ_E_BOUND;
+  }
+  launch_codes<D>(g, f, W.cand_f, 0, g.nz, s);
+  k_critmask<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(W.cand_f, W.crit_f, g);
+  k_lowpos<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(f, W.lowpos, g);
+  CK(cudaGetLastError());
+  *launches += 4;
+  return DMTZ_OK;
+}
+
+// unit list of the z-planes [z0, z1) into `list` (count -> *n)
+inline cudaError_t units_range(const RowGeom& rg, int64_t z0, int64_t z1, uint32_t* list, unsigned long long* n,
+                               cudaStream_t s) {
+  const int64_t cnt = (z1 - z0) * rg.ub;
+  k_units_all<<<clamp_blocks(cnt > 0 ? cnt : 1, 256, 4096), 256, 0, s>>>(rg.ub, z0, z1, list, n);
+  return cudaGetLastError();
+}
+
+// One C-loop round (a3-a6, + a7 frontier bits when fbits != nullptr).  The
+// screen runs over `units`/`n_units`, the decode over `dunits`/`n_dunits`;
+// targets outside [own_lo, own_hi) are dropped (slab mode).  Counters are copied
+// to host_cnt before returning (stream synchronised).
+template <int D>
+dmtz_status round_phase(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o, WS<D>& W,
+                        float* g_out, int64_t round, const uint32_t* units, unsigned long long* n_units,
+                        const uint32_t* dunits, unsigned long long* n_dunits, uint32_t* fbits, int fwords,
+                        int64_t own_lo, int64_t own_hi, int64_t count_z0, int64_t count_z1, bool profile,
+                        int64_t* launches, cudaStream_t s) {
+  const Grid& g = c->g;
+  const RowGeom rg = row_geom(g);
+  const int64_t nwords = (g.N + 31) / 32;
+  const int sweep_blocks = 148 * 8;
+  const float step = ldexpf(o->xi, -o->q_max);  // xi / 2^q_max, exact
+  const int fwords_smem = fbits && fwords * 4 <= 32768 ? fwords : 0;
+  CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));
+  if (fbits) CK(cudaMemsetAsync(fbits, 0, (size_t)fwords * 4, s));
+  if (fbits && round > 1) CK(cudaMemsetAsync(W.ebits, 0, W.rowbit_bytes, s));
+  if (profile) CK(cudaEventRecord(c->ev[0], s));
+  k_screen<D><<<sweep_blocks, 256, 0, s>>>(g_out, W.cand_g, W.ebits, units, n_units, g, rg, round == 1 ? 1 : 0,
+                                           W.dc);
+  if (profile) CK(cudaEventRecord(c->ev[1], s));
+  k_decode<D><<<sweep_blocks * 2, DECODE_THREADS, 0, s>>>(
+      f, W.cand_f, W.crit_f, W.cand_g, W.crit_g, W.ebits, W.fmark, W.tbits, dunits, n_dunits, g, rg,
+      tier_mask<D>(o->tier), W.lowpos, round == 1 ? 1 : 0, own_lo, own_hi, count_z0, count_z1, W.dc);
+  if (profile) CK(cudaEventRecord(c->ev[2], s));
+  k_edit_rows<D><<<clamp_blocks(nwords, 256), 256, fwords_smem * 4, s>>>(
+      W.tbits, nwords, fhat, W.lb, g_out, W.state, W.dc, step, o->q_cap, fbits, g, rg, fwords_smem);
+  *launches += 3;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(c->host_cnt, W.dc, offsetof(Counters, first_nonfinite), cudaMemcpyDeviceToHost, s));
+  if (fbits) {
+    // next round's unit list (after the counters were copied)
+    CK(cudaMemsetAsync(n_units, 0, 8, s));
+    k_units_from_bits<<<clamp_blocks(rg.units, 256, 4096), 256, 0, s>>>(fbits, rg.units, (uint32_t*)units, n_units);
+    *launches += 1;
+  }
+  CK(cudaStreamSynchronize(s));
+  return DMTZ_OK;
+}
+
+// a8: ordered edit list of the vertices [v0, v1), indices shifted by v_off
+template <int D>
+dmtz_status edits_phase(dmtz_ctx* c, WS<D>& W, const float* g_out, int64_t v0, int64_t v1, int64_t v_off,
+                        dmtz_edit* edits, int64_t cap, int64_t* n_edits, int64_t* n_lossless, int64_t* launches,
+                        cudaStream_t s) {
+  Counters* hc = c->host_cnt;
+  const int64_t nb = (v1 - v0 + EDIT_CHUNK - 1) / EDIT_CHUNK;
+  CK(cudaMemsetAsync(&W.dc->n_lossless, 0, 8, s));
+  if (nb > 0) {
+    k_edit_count<<<(unsigned)nb, EDIT_THREADS, 0, s>>>(W.state, v0, v1, W.bc, W.dc);
+    k_scan_counts<<<1, EDIT_THREADS, 0, s>>>(W.bc, nb, W.dc);
+    k_edit_write<<<(unsigned)nb, EDIT_THREADS, 0, s>>>(W.state, g_out, v0, v1, W.bc, (EditOut*)edits, cap, v_off);
+    *launches += 3;
+  } else {
+    CK(cudaMemsetAsync(&W.dc->n_edits, 0, 8, s));
+  }
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(hc, W.dc, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  *n_edits = (int64_t)hc->n_edits;
+  *n_lossless = (int64_t)hc->n_lossless;
+  return DMTZ_OK;
+}
+
 template <int D>
 dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
                          char* ws, const Layout& L, float* g_out, dmtz_edit* edits, int64_t cap,
                          int64_t* n_edits, dmtz_stats* st, cudaStream_t s) {
   const Grid& g = c->g;
-  using code_t = typename Tr<D>::code_t;
-  code_t* cand_f = (code_t*)(ws + L.cand_f);
-  code_t* cand_g = (code_t*)(ws + L.cand_g);  // codes of g, memoized across rounds
-  float* lb = (float*)(ws + L.lb);
-  uint32_t* state = (uint32_t*)(ws + L.state);
-  uint32_t* tbits = (uint32_t*)(ws + L.tbits);
-  Counters* dc = (Counters*)(ws + L.counters);
-  unsigned long long* bc = (unsigned long long*)(ws + L.edit_bc);
+  WS<D> W(ws, L, g);
   Counters* hc = c->host_cnt;
-  const int64_t nwords = (g.N + 31) / 32;
-  const int ethreads = 256;
-  const int eblocks = (int)((g.N + ethreads - 1) / ethreads < 148 * 32 ? (g.N + ethreads - 1) / ethreads : 148 * 32);
-  const int wblocks = (int)((nwords + ethreads - 1) / ethreads < 148 * 32 ? (nwords + ethreads - 1) / ethreads : 148 * 32);
-
-  // a1: setup
-  CK(cudaMemsetAsync(dc, 0, sizeof(Counters), s));
-  CK(cudaMemsetAsync(&dc->first_nonfinite, 0xFF, 16, s));
-  CK(cudaMemsetAsync(tbits, 0, nwords * 4, s));
-  k_setup<<<eblocks, ethreads, 0, s>>>(f, fhat, o->xi, g.N, lb, g_out, state, dc);
-  st->launches++;
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  if (hc->first_nonfinite != ~0ull) {
-    set_err("non-finite value at vertex %llu", hc->first_nonfinite);
-    st->status = DMTZ_E_NONFINITE;
-    return DMTZ_E_NONFINITE;
-  }
-  if (hc->first_bound != ~0ull) {
-    set_err("|fhat - f| > xi at vertex %llu", hc->first_bound);
-    st->status = DMTZ_E_BOUND;
-    return DMTZ_E_BOUND;
-  }
-  // a2: reference gradient of f (once)
-  launch_codes<D>(g, f, cand_f, 0, g.nz, s);
-  uint32_t* crit_f = (uint32_t*)(ws + L.crit_f);
-  k_critmask<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(cand_f, crit_f, g);
-  unsigned long long* lowpos = (unsigned long long*)(ws + L.lowpos);
-  k_lowpos<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(f, lowpos, g);
-  st->launches += 3;
-  CK(cudaGetLastError());
-
-  const float step = ldexpf(o->xi, -o->q_max);   // xi / 2^q_max, exact
+  dmtz_status status = setup_phase<D>(c, f, fhat, o, W, g_out, 0, &st->launches, s);
+  if (status != DMTZ_OK) { st->status = status; return status; }
   const int64_t max_rounds = o->max_rounds > 0 ? o->max_rounds : g.N * (int64_t)(o->q_cap + 1);
-  const uint32_t tmask = tier_mask<D>(o->tier);
   const RowGeom rg = row_geom(g);
-  uint32_t* ebits = (uint32_t*)(ws + L.ebits);
-  uint32_t* fmark = (uint32_t*)(ws + L.fmark);
-  uint32_t* crit_g = (uint32_t*)(ws + L.crit_g);
-  const size_t rowbit_bytes = (size_t)(g.nz * g.ny * rg.wpr) * 4;
-  CK(cudaMemsetAsync(fmark, 0, rowbit_bytes, s));
-  uint32_t* units = (uint32_t*)(ws + L.units);
-  uint32_t* fbits = (uint32_t*)(ws + L.frontier);
-  unsigned long long* n_units = &dc->n_units;
+  unsigned long long* n_units = &W.dc->n_units;
   const bool frontier_mode = !o->full_sweeps;
-  const int fwords_smem = L.fwords * 4 <= 32768 ? (int)L.fwords : 0;
-  const int sweep_blocks = 148 * 8;
   // round 1 (and every round of a full sweep) processes every unit
-  k_units_all<<<(unsigned)((rg.units + 255) / 256 < 4096 ? (rg.units + 255) / 256 : 4096), 256, 0, s>>>(
-      rg.units, units, n_units);
+  CK(units_range(rg, 0, g.nz, W.units, n_units, s));
   st->launches++;
-  dmtz_status status = DMTZ_OK;
   for (int64_t round = 1;; round++) {
     // a3: gradient of g (screened);  a4/a5: classify + mark targets;  a6: edit;  a7: frontier
-    CK(cudaMemsetAsync(dc, 0, offsetof(Counters, first_nonfinite), s));
-    if (frontier_mode) CK(cudaMemsetAsync(fbits, 0, L.fwords * 4, s));
-    if (frontier_mode && round > 1) CK(cudaMemsetAsync(ebits, 0, rowbit_bytes, s));
-    if (o->profile) CK(cudaEventRecord(c->ev[0], s));
-    k_screen<D><<<sweep_blocks, 256, 0, s>>>(g_out, cand_g, ebits, units, n_units, g, rg, round == 1 ? 1 : 0, dc);
-    if (o->profile) CK(cudaEventRecord(c->ev[1], s));
-    k_decode<D><<<sweep_blocks * 2, DECODE_THREADS, 0, s>>>(f, cand_f, crit_f, cand_g, crit_g, ebits, fmark, tbits, units, n_units,
-                                             g, rg, tmask, lowpos, round == 1 ? 1 : 0, dc);
-    if (o->profile) CK(cudaEventRecord(c->ev[2], s));
-    k_edit_rows<D><<<wblocks, ethreads, frontier_mode ? fwords_smem * 4 : 0, s>>>(
-        tbits, nwords, fhat, lb, g_out, state, dc, step, o->q_cap, frontier_mode ? fbits : nullptr, g, rg,
-        frontier_mode ? fwords_smem : 0);
-    st->launches += 3;
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(hc, dc, offsetof(Counters, first_nonfinite), cudaMemcpyDeviceToHost, s));
-    if (frontier_mode) {
-      // next round's unit list (after the counters were copied: n_units is reset here)
-      CK(cudaMemsetAsync(n_units, 0, 8, s));
-      k_units_from_bits<<<(unsigned)((rg.units + 255) / 256 < 4096 ? (rg.units + 255) / 256 : 4096), 256, 0, s>>>(
-          fbits, rg.units, units, n_units);
-      st->launches++;
-    }
-    CK(cudaStreamSynchronize(s));
+    status = round_phase<D>(c, f, fhat, o, W, g_out, round, W.units, n_units, W.units, n_units,
+                            frontier_mode ? W.fbits : nullptr, (int)L.fwords, 0, g.N, 0, g.nz, o->profile != 0,
+                            &st->launches, s);
+    if (status != DMTZ_OK) break;
     if (o->profile) {
       float ms0 = 0.f, ms1 = 0.f;
       CK(cudaEventElapsedTime(&ms0, c->ev[0], c->ev[1]));
@@ -230,19 +305,13 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
     if (hc->n_changed == 0) { status = DMTZ_E_STUCK; set_err("no target could move (round %lld)", (long long)round); break; }
     if (round == max_rounds) { status = DMTZ_E_ITER_CAP; set_err("round cap %lld reached", (long long)round); break; }
   }
+  if (status == DMTZ_E_CUDA) { st->status = status; return status; }
   // a8: edit list
-  const int64_t nb = (g.N + EDIT_CHUNK - 1) / EDIT_CHUNK;
-  CK(cudaMemsetAsync(&dc->n_lossless, 0, 8, s));
-  k_edit_count<<<(unsigned)nb, EDIT_THREADS, 0, s>>>(state, g.N, bc, dc);
-  k_scan_counts<<<1, EDIT_THREADS, 0, s>>>(bc, nb, dc);
-  k_edit_write<<<(unsigned)nb, EDIT_THREADS, 0, s>>>(state, g_out, g.N, bc, (EditOut*)edits, cap);
-  st->launches += 3;
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  *n_edits = (int64_t)hc->n_edits;
+  int64_t nl = 0;
+  dmtz_status es = edits_phase<D>(c, W, g_out, 0, g.N, 0, edits, cap, n_edits, &nl, &st->launches, s);
+  if (es != DMTZ_OK) { st->status = es; return es; }
   st->n_edited = *n_edits;
-  st->n_lossless = (int64_t)hc->n_lossless;
+  st->n_lossless = nl;
   st->n_quantized = st->n_edited - st->n_lossless;
   if (status == DMTZ_OK && *n_edits > cap) { status = DMTZ_E_CAPACITY; set_err("edit list needs %lld entries", (long long)*n_edits); }
   st->status = status;
@@ -362,6 +431,81 @@ dmtz_status dmtz_correct(dmtz_ctx* c, const float* f, const float* fhat, const d
   else r = correct_impl<2>(c, f, fhat, o, (char*)workspace, L, g_out, edits, edits_capacity, n_edits, st, s);
   if (r == DMTZ_E_CUDA) st->status = r;
   return r;
+}
+
+static dmtz_status slab_check(dmtz_ctx* c, const dmtz_slab* sl, void* ws, size_t wsb, Layout* L) {
+  if (!c || !sl || !ws) { set_err("NULL argument"); return DMTZ_E_ARG; }
+  if (c->D != 3) { set_err("slab mode needs a 3D grid"); return DMTZ_E_DIMS; }
+  if (sl->own_z0 < 0 || sl->own_z1 > c->g.nz || sl->own_z0 >= sl->own_z1 || sl->anchor_z0 < 0 ||
+      sl->anchor_z1 > c->g.nz || sl->anchor_z0 > sl->anchor_z1) {
+    set_err("bad slab planes");
+    return DMTZ_E_ARG;
+  }
+  *L = layout_for(c);
+  if (wsb < L->total) { set_err("workspace %zu < %zu bytes", wsb, L->total); return DMTZ_E_OOM; }
+  return DMTZ_OK;
+}
+
+dmtz_status dmtz_slab_begin(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
+                            const dmtz_slab* sl, void* workspace, size_t wsb, float* g_out, dmtz_stream_t stream) {
+  Layout L;
+  dmtz_status st = slab_check(c, sl, workspace, wsb, &L);
+  if (st) return st;
+  if (!f || !fhat || !o || !g_out || !(o->xi > 0.0f) || o->q_max < 0 || o->q_max > 30 || o->q_cap < 1 ||
+      o->q_cap > 65535 || (o->tier != 1 && o->tier != 2)) {
+    set_err("invalid argument");
+    return DMTZ_E_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  WS<3> W((char*)workspace, L, c->g);
+  int64_t launches = 0;
+  st = setup_phase<3>(c, f, fhat, o, W, g_out, sl->z_offset * c->g.sz, &launches, s);
+  if (st) return st;
+  const RowGeom rg = row_geom(c->g);
+  CK(units_range(rg, 0, c->g.nz, W.units, &W.dc->n_units, s));
+  CK(units_range(rg, sl->anchor_z0, sl->anchor_z1, W.units2, &W.dc->n_units2, s));
+  CK(cudaStreamSynchronize(s));
+  return DMTZ_OK;
+}
+
+dmtz_status dmtz_slab_round(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
+                            const dmtz_slab* sl, void* workspace, size_t wsb, float* g_out, int64_t round,
+                            int64_t* counters, int64_t* kinds, dmtz_stream_t stream) {
+  Layout L;
+  dmtz_status st = slab_check(c, sl, workspace, wsb, &L);
+  if (st) return st;
+  if (!counters || !kinds || round < 1) { set_err("invalid argument"); return DMTZ_E_ARG; }
+  cudaStream_t s = (cudaStream_t)stream;
+  WS<3> W((char*)workspace, L, c->g);
+  int64_t launches = 0;
+  const int64_t plane = c->g.sz;
+  st = round_phase<3>(c, f, fhat, o, W, g_out, round, W.units, &W.dc->n_units, W.units2, &W.dc->n_units2, nullptr,
+                      0, sl->own_z0 * plane, sl->own_z1 * plane, sl->own_z0, sl->own_z1, false, &launches, s);
+  if (st) return st;
+  Counters* hc = c->host_cnt;
+  counters[0] = (int64_t)hc->n_false;
+  counters[1] = (int64_t)hc->n_changed;
+  counters[2] = (int64_t)hc->n_targets;
+  counters[3] = (int64_t)hc->n_internal;
+  for (int k = 0; k < 8; k++) kinds[k] = round == 1 ? (int64_t)hc->kinds[k] : 0;
+  return DMTZ_OK;
+}
+
+dmtz_status dmtz_slab_end(dmtz_ctx* c, const dmtz_slab* sl, void* workspace, size_t wsb, const float* g,
+                          dmtz_edit* edits, int64_t cap, int64_t* n_edits, int64_t* n_lossless,
+                          dmtz_stream_t stream) {
+  Layout L;
+  dmtz_status st = slab_check(c, sl, workspace, wsb, &L);
+  if (st) return st;
+  if (!g || !n_edits || !n_lossless || cap < 0 || (cap > 0 && !edits)) { set_err("invalid argument"); return DMTZ_E_ARG; }
+  WS<3> W((char*)workspace, L, c->g);
+  int64_t launches = 0;
+  const int64_t plane = c->g.sz;
+  st = edits_phase<3>(c, W, g, sl->own_z0 * plane, sl->own_z1 * plane, sl->z_offset * plane, edits, cap, n_edits,
+                      n_lossless, &launches, (cudaStream_t)stream);
+  if (st) return st;
+  if (*n_edits > cap) { set_err("edit list needs %lld entries", (long long)*n_edits); return DMTZ_E_CAPACITY; }
+  return DMTZ_OK;
 }
 
 dmtz_status dmtz_trace_separatrices(dmtz_ctx* c, const void* codes, uint32_t kinds, void* workspace,

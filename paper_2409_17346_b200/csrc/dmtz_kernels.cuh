@@ -29,7 +29,8 @@ struct Counters {                 // device-side round counters (one 256 B block
   unsigned long long n_edits;
   unsigned long long n_lossless;  // lossless entries of the edit list
   unsigned long long n_units;     // active units of the current round (frontier list length)
-  unsigned long long pad[14];
+  unsigned long long n_units2;    // slab mode: units whose cells are classified
+  unsigned long long pad[13];
 };
 static_assert(sizeof(Counters) == 256, "counters are one 256 B block");
 
@@ -222,10 +223,11 @@ __device__ __forceinline__ unsigned long long block_sum(unsigned long long v, un
   return s;  // valid in warp 0
 }
 
-__global__ void k_edit_count(const uint32_t* __restrict__ state, int64_t n, unsigned long long* __restrict__ bc,
-                             Counters* __restrict__ cnt) {
+// vertices [v0, n) (slab mode: the owned planes)
+__global__ void k_edit_count(const uint32_t* __restrict__ state, int64_t v0, int64_t n,
+                             unsigned long long* __restrict__ bc, Counters* __restrict__ cnt) {
   __shared__ unsigned long long sh[32];
-  const int64_t base = (int64_t)blockIdx.x * EDIT_CHUNK;
+  const int64_t base = v0 + (int64_t)blockIdx.x * EDIT_CHUNK;
   unsigned long long c = 0, nl = 0;
   for (int i = threadIdx.x; i < EDIT_CHUNK; i += blockDim.x) {
     const int64_t v = base + i;
@@ -260,10 +262,11 @@ __global__ void k_scan_counts(unsigned long long* __restrict__ bc, int64_t nb, C
 struct EditOut { unsigned long long v; unsigned short q; unsigned char lossless; unsigned char pad; float value; };
 static_assert(sizeof(EditOut) == 16, "dmtz_edit is 16 bytes");
 
-__global__ void k_edit_write(const uint32_t* __restrict__ state, const float* __restrict__ gf, int64_t n,
-                             const unsigned long long* __restrict__ boff, EditOut* __restrict__ out, int64_t cap) {
+__global__ void k_edit_write(const uint32_t* __restrict__ state, const float* __restrict__ gf, int64_t v0, int64_t n,
+                             const unsigned long long* __restrict__ boff, EditOut* __restrict__ out, int64_t cap,
+                             int64_t v_global_off) {
   __shared__ unsigned int wsum[32];
-  const int64_t base = (int64_t)blockIdx.x * EDIT_CHUNK;
+  const int64_t base = v0 + (int64_t)blockIdx.x * EDIT_CHUNK;
   unsigned long long off = boff[blockIdx.x];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int seg = 0; seg < EDIT_CHUNK; seg += blockDim.x) {
@@ -279,7 +282,7 @@ __global__ void k_edit_write(const uint32_t* __restrict__ state, const float* __
       const unsigned long long pos = off + before + __popc(bal & ((1u << lane) - 1u));
       if ((int64_t)pos < cap) {
         EditOut o;
-        o.v = (unsigned long long)v;
+        o.v = (unsigned long long)(v + v_global_off);
         o.q = (unsigned short)(st & 0xFFFFu);
         o.lossless = (unsigned char)(st >> 16);
         o.pad = 0;

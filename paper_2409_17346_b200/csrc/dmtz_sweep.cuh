@@ -247,7 +247,8 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
          uint32_t* __restrict__ crit_g, const uint32_t* __restrict__ ebits, uint32_t* __restrict__ fmark,
          uint32_t* __restrict__ tbits, const uint32_t* __restrict__ units,
          const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg, uint32_t tier_mask,
-         const unsigned long long* __restrict__ lowpos_f, int count_kinds, Counters* __restrict__ cnt) {
+         const unsigned long long* __restrict__ lowpos_f, int count_kinds, int64_t own_lo, int64_t own_hi,
+         int64_t count_z0, int64_t count_z1, Counters* __restrict__ cnt) {
   __shared__ TargetTables T;
   __shared__ DecodeWarpSmem WS[DECODE_THREADS / 32];
   init_target_tables<D>(T, g);
@@ -330,7 +331,8 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
     if (!fb) continue;  // warp-uniform (next chunk of this row)
     // warp work list of the false cells (source lane, type): all lanes then share them
     const int nmine = __popc(diff);
-    nfalse += nmine;
+    const bool counted = z >= count_z0 && z < count_z1;  // slab mode: each anchor counted by its owner
+    if (counted) nfalse += nmine;
     int pre = nmine;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -364,7 +366,7 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
         const int item = W.items[i];
         const int src = item & 31, t = item >> 5;
         const bool fn = (W.critf[src] >> t) & 1u;
-        if (count_kinds) {
+        if (count_kinds && counted) {
           const int dim = T.tinfo[t] & 3;
           const int cls = (dim == Tr<D>::TOP) ? 3 : dim;
           atomicAdd(kc + 2 * cls + (fn ? 1 : 0), 1u);
@@ -376,7 +378,7 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
           const int64_t tv = ubase + src + off;
           word = (uint32_t)(tv >> 5);
           bit = 1u << (tv & 31);
-          have_t = true;
+          have_t = tv >= own_lo && tv < own_hi;  // slab mode: only the owned vertices
         }
       }
       const unsigned have = __ballot_sync(0xffffffffu, have_t);
@@ -510,10 +512,13 @@ __global__ void k_units_from_bits(const uint32_t* __restrict__ fbits, int64_t n_
   }
 }
 
-__global__ void k_units_all(int64_t n_units, uint32_t* __restrict__ list, unsigned long long* __restrict__ n_out) {
-  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n_units; u += (int64_t)gridDim.x * blockDim.x)
-    list[u] = (uint32_t)u;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *n_out = (unsigned long long)n_units;
+// units of the z-planes [z0, z1) (all units: z0 = 0, z1 = nz); unit = z * ub + y-block
+__global__ void k_units_all(int64_t ub, int64_t z0, int64_t z1, uint32_t* __restrict__ list,
+                            unsigned long long* __restrict__ n_out) {
+  const int64_t n = (z1 - z0) * ub;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    list[i] = (uint32_t)(z0 * ub + i);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_out = (unsigned long long)(n > 0 ? n : 0);
 }
 
 }  // namespace dmtz

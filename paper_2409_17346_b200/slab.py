@@ -1,0 +1,273 @@
+"""Multi-GPU C-loop: z-slab decomposition driven over torch.distributed.
+
+Each rank owns a contiguous range of z-planes and every edit decision there.
+Its LOCAL grid is the owned planes plus up to HALO = 3 planes below and above:
+a target lies within [-1, 2]^3 of its false cell's anchor, so the cells whose
+targets can be owned vertices are anchored in [z0 - 2, z1 + 1), and their
+criticality reads values in [z0 - 3, z1 + 3).  Per round each rank
+
+  1. refreshes its halo planes of g from the neighbours (send/recv of contiguous
+     planes: NCCL over NVLink on GPUs, gloo on CPU),
+  2. runs one round (dmtz_slab_round: screen, classify the anchored cells,
+     edit the owned targets),
+  3. all-reduces the round counters, so every rank takes the same stop decision.
+
+The rounds are exactly those of dmtz_correct on the global grid (edits are
+set-synchronous and read only round-start values), hence the concatenated
+owned edit lists equal the single-GPU edit list bit for bit.
+
+The driver is generic over an *engine* (the per-rank round kernels): the CUDA
+engine below, or a test engine.  ``run_emulated`` steps several engines in one
+process with in-memory halo copies (one GPU standing in for several, strictly
+sequentially -- no rank ever waits on another inside a kernel).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+HALO = 3
+OK, E_ITER_CAP, E_STUCK, E_INTERNAL = 0, 6, 7, 11
+
+
+@dataclass(frozen=True)
+class SlabPlan:
+    rank: int
+    world: int
+    nz: int
+    z0: int          # owned global planes [z0, z1)
+    z1: int
+    lz0: int         # global planes of the local grid [lz0, lz1)
+    lz1: int
+
+    @property
+    def own_local(self):
+        return self.z0 - self.lz0, self.z1 - self.lz0
+
+    @property
+    def anchor_local(self):
+        a0 = max(0, self.z0 - 2)
+        a1 = min(self.nz, self.z1 + 1)
+        return a0 - self.lz0, a1 - self.lz0
+
+    @property
+    def halo_below(self):   # local planes received from rank - 1
+        return 0, self.z0 - self.lz0
+
+    @property
+    def halo_above(self):   # local planes received from rank + 1
+        return self.z1 - self.lz0, self.lz1 - self.lz0
+
+
+def partition(nz: int, world: int):
+    """Balanced contiguous z-ranges; every rank owns at least HALO planes."""
+    if world * HALO > nz:
+        raise ValueError(f"{world} ranks need nz >= {world * HALO} (got {nz})")
+    base, extra = divmod(nz, world)
+    out, z = [], 0
+    for r in range(world):
+        n = base + (1 if r < extra else 0)
+        out.append((z, z + n))
+        z += n
+    return out
+
+
+def plan(nz: int, world: int, rank: int) -> SlabPlan:
+    z0, z1 = partition(nz, world)[rank]
+    return SlabPlan(rank, world, nz, z0, z1, max(0, z0 - HALO), min(nz, z1 + HALO))
+
+
+def halo_pairs(p: SlabPlan):
+    """[(peer, send local planes (a, b), recv local planes (c, d))] of this rank."""
+    out = []
+    if p.rank > 0:
+        lo = p.halo_below
+        out.append((p.rank - 1, (p.z0 - p.lz0, p.z0 - p.lz0 + (lo[1] - lo[0])), lo))
+    if p.rank < p.world - 1:
+        hi = p.halo_above
+        n = hi[1] - hi[0]
+        out.append((p.rank + 1, (p.z1 - p.lz0 - n, p.z1 - p.lz0), hi))
+    return out
+
+
+class _Slab(ctypes.Structure):
+    _fields_ = [("z_offset", ctypes.c_int64), ("own_z0", ctypes.c_int64), ("own_z1", ctypes.c_int64),
+                ("anchor_z0", ctypes.c_int64), ("anchor_z1", ctypes.c_int64)]
+
+
+class CudaSlabEngine:
+    """The rank's round kernels: libdmtz slab entry points on its local grid."""
+
+    def __init__(self, p: SlabPlan, ny: int, nx: int, device):
+        from . import Context, _Opts, _check, _lib, _stream_ptr
+        self._lib, self._check, self._Opts, self._stream_ptr = _lib, _check, _Opts, _stream_ptr
+        self.p = p
+        self.shape = (p.lz1 - p.lz0, ny, nx)
+        self.ctx = Context(self.shape, device)
+        o0, o1 = p.own_local
+        a0, a1 = p.anchor_local
+        self.slab = _Slab(p.lz0, o0, o1, a0, a1)
+        self.device = torch.device(device)
+
+    def _P(self, t):
+        return ctypes.c_void_p(t.data_ptr())
+
+    def begin(self, f, fhat, xi, q_max=6, q_cap=None, tier=2):
+        self.f, self.fhat = f.contiguous(), fhat.contiguous()
+        self.g = torch.empty_like(self.f)
+        self.opts = self._Opts(float(xi), int(q_max), int(q_max if q_cap is None else q_cap), int(tier), 0, 1, 0)
+        self._check(self._lib.dmtz_slab_begin(self.ctx._h, self._P(self.f), self._P(self.fhat),
+                                              ctypes.byref(self.opts), ctypes.byref(self.slab),
+                                              self._P(self.ctx.workspace), self.ctx.ws_bytes, self._P(self.g),
+                                              self._stream_ptr()))
+
+    def round(self, r: int):
+        c = (ctypes.c_int64 * 4)()
+        k = (ctypes.c_int64 * 8)()
+        self._check(self._lib.dmtz_slab_round(self.ctx._h, self._P(self.f), self._P(self.fhat),
+                                              ctypes.byref(self.opts), ctypes.byref(self.slab),
+                                              self._P(self.ctx.workspace), self.ctx.ws_bytes, self._P(self.g), r, c,
+                                              k, self._stream_ptr()))
+        return np.array(c[:], np.int64), np.array(k[:], np.int64)
+
+    def end(self):
+        o0, o1 = self.p.own_local
+        cap = (o1 - o0) * self.shape[1] * self.shape[2]
+        edits = torch.empty((max(cap, 1), 16), dtype=torch.uint8, device=self.device)
+        ne, nl = ctypes.c_int64(), ctypes.c_int64()
+        self._check(self._lib.dmtz_slab_end(self.ctx._h, ctypes.byref(self.slab), self._P(self.ctx.workspace),
+                                            self.ctx.ws_bytes, self._P(self.g), self._P(edits), cap,
+                                            ctypes.byref(ne), ctypes.byref(nl), self._stream_ptr()))
+        return edits[:ne.value], nl.value
+
+    def owned_g(self):
+        o0, o1 = self.p.own_local
+        return self.g[o0:o1]
+
+
+def _stop(round_, tot, max_rounds):
+    """Same stop rule as dmtz_correct on the summed counters."""
+    if tot[3]:
+        return E_INTERNAL
+    if tot[0] == 0:
+        return OK
+    if tot[1] == 0:
+        return E_STUCK
+    if round_ == max_rounds:
+        return E_ITER_CAP
+    return None
+
+
+def run_distributed(engine, f, fhat, xi, q_max=6, q_cap=None, tier=2, max_rounds=0, group=None):
+    """One rank of the slab C-loop over torch.distributed (call on every rank)."""
+    import torch.distributed as dist
+    p = engine.p
+    engine.begin(f, fhat, xi, q_max, q_cap, tier)
+    pairs = halo_pairs(p)
+    dev = engine.g.device
+    stats = dict(rounds=0, n_false_round0=0, false_by_kind_round0=[0] * 8)
+    status = None
+    r = 0
+    while status is None:
+        r += 1
+        if r > 1 and pairs:
+            ops = []
+            for peer, (sa, sb), (ra, rb) in pairs:
+                ops.append(dist.P2POp(dist.isend, engine.g[sa:sb].contiguous(), peer, group))
+                ops.append(dist.P2POp(dist.irecv, engine.g[ra:rb], peer, group))
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        c, k = engine.round(r)
+        tot = torch.tensor(np.concatenate([c, k]), dtype=torch.int64, device=dev)
+        dist.all_reduce(tot, group=group)
+        tot = tot.cpu().numpy()
+        if r == 1:
+            stats["n_false_round0"] = int(tot[0])
+            stats["false_by_kind_round0"] = [int(x) for x in tot[4:12]]
+        status = _stop(r, tot, max_rounds)
+        if status != OK:
+            stats["rounds"] = r
+    edits, nl = engine.end()
+    stats["status"] = status
+    return edits, nl, stats
+
+
+def run_emulated(engines, fs, fhats, xi, q_max=6, q_cap=None, tier=2, max_rounds=0):
+    """All ranks in one process (one device or CPU): sequential rounds, in-memory halos."""
+    for e, f, fh in zip(engines, fs, fhats):
+        e.begin(f, fh, xi, q_max, q_cap, tier)
+    stats = dict(rounds=0, n_false_round0=0, false_by_kind_round0=[0] * 8)
+    status = None
+    r = 0
+    while status is None:
+        r += 1
+        if r > 1:
+            for e in engines:
+                for peer, (sa, sb), (ra, rb) in halo_pairs(e.p):
+                    src = engines[peer]
+                    # the peer's planes that this rank keeps as halo = peer's send range towards us
+                    (_, (psa, psb), _) = [x for x in halo_pairs(src.p) if x[0] == e.p.rank][0]
+                    e.g[ra:rb] = src.g[psa:psb]
+        tot = np.zeros(12, np.int64)
+        for e in engines:
+            c, k = e.round(r)
+            tot += np.concatenate([c, k])
+        if r == 1:
+            stats["n_false_round0"] = int(tot[0])
+            stats["false_by_kind_round0"] = [int(x) for x in tot[4:12]]
+        status = _stop(r, tot, max_rounds)
+        if status != OK:
+            stats["rounds"] = r
+    outs = [e.end() for e in engines]
+    stats["status"] = status
+    return outs, stats
+
+
+def local_inputs(f: np.ndarray, fhat: np.ndarray, p: SlabPlan):
+    """The rank's local arrays (owned planes + halos) of global inputs."""
+    return (np.ascontiguousarray(f[p.lz0:p.lz1]), np.ascontiguousarray(fhat[p.lz0:p.lz1]))
+
+
+def bench_main(args, f, fh, xi, cfg, world, rank, local):
+    """bench.py --gpus N (torchrun): strong scaling of the slab C-loop on the config."""
+    import json
+
+    import torch.distributed as dist
+    dev = torch.device("cuda", local)
+    p = plan(f.shape[0], world, rank)
+    lf, lfh = local_inputs(f, fh, p)
+    eng = CudaSlabEngine(p, f.shape[1], f.shape[2], dev)
+    ft, fht = torch.from_numpy(lf).to(dev), torch.from_numpy(lfh).to(dev)
+    for _ in range(args.warmup):
+        run_distributed(eng, ft, fht, xi)
+    torch.cuda.synchronize()
+    dist.barrier()
+    times = []
+    for _ in range(args.steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        edits, nl, st = run_distributed(eng, ft, fht, xi)
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1)], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        times.append(float(t.item()))
+    ms = float(np.median(times))
+    sweeps = st["rounds"] + 1
+    value = f.size * sweeps / (ms * 1e-3) / 1e6
+    if rank == 0:
+        line = {"metric": "C-loop Mvoxels/s per iteration", "value": value, "unit": "Mvoxels/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"{cfg.name} {cfg.family} {'x'.join(map(str, f.shape))} rel eps {cfg.eps}",
+                           "parallelism": f"z-slabs x{world} (NCCL halo send/recv + counter all-reduce)",
+                           "sweeps_per_step": sweeps, "rounds": st["rounds"], "mode": "full sweeps per slab"},
+                "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": None,
+                "stats": st}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()

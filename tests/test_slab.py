@@ -1,0 +1,121 @@
+"""Multi-rank slab C-loop: partition / halo logic, and the whole driver against the
+single-domain oracle -- emulated in one process and over torch.distributed gloo with
+world size 2 on CPU (the NCCL/GPU path runs the same driver)."""
+import os
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import dmtz_inputs as di
+import oracle
+from paper_2409_17346_b200 import slab
+from tests.slab_engines import OracleSlabEngine
+
+
+@pytest.mark.parametrize("nz,world", [(12, 2), (13, 3), (9, 3), (40, 4), (24, 8)])
+def test_partition_covers_and_halos(nz, world):
+    parts = slab.partition(nz, world)
+    assert parts[0][0] == 0 and parts[-1][1] == nz
+    assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+    assert all(z1 - z0 >= slab.HALO for z0, z1 in parts)
+    for r in range(world):
+        p = slab.plan(nz, world, r)
+        a0, a1 = p.anchor_local
+        # classified anchors: every anchor whose false cell can target an owned vertex
+        assert p.lz0 + a0 == max(0, p.z0 - 2) and p.lz0 + a1 == min(nz, p.z1 + 1)
+        # criticality of those anchors reads values in [z0 - 3, z1 + 3): inside the local grid
+        assert p.lz0 <= max(0, p.z0 - 3) and p.lz1 >= min(nz, p.z1 + 3)
+        for peer, (sa, sb), (ra, rb) in slab.halo_pairs(p):
+            q = slab.plan(nz, world, peer)
+            back = [x for x in slab.halo_pairs(q) if x[0] == r][0]
+            # what I receive is exactly what the peer sends me, plane for plane (global z)
+            assert list(range(q.lz0 + back[1][0], q.lz0 + back[1][1])) == list(range(p.lz0 + ra, p.lz0 + rb))
+            assert list(range(p.lz0 + sa, p.lz0 + sb)) == list(range(q.lz0 + back[2][0], q.lz0 + back[2][1]))
+            assert p.z0 <= p.lz0 + sa and p.lz0 + sb <= p.z1   # only owned planes are sent
+    with pytest.raises(ValueError):
+        slab.partition(5, 2)
+
+
+def _case(shape, seed):
+    return di.random_case(shape, seed, eps=0.05, perturb="noise", family="lognormal")
+
+
+def _check_against_oracle(f, fh, xi, outs, stats):
+    ref = oracle.correct(f, fh, xi)
+    assert stats["status"] == ref["status"]
+    assert stats["rounds"] == ref["stats"]["rounds"]
+    assert stats["n_false_round0"] == ref["stats"]["n_false_round0"]
+    assert stats["false_by_kind_round0"] == ref["stats"]["false_by_kind_round0"]
+    e = np.concatenate([o[0] for o in outs])
+    assert np.array_equal(e["v"], ref["edits"]["v"])
+    assert np.array_equal(e["q"], ref["edits"]["q"])
+    assert np.array_equal(e["lossless"], ref["edits"]["lossless"])
+    assert np.array_equal(e["value"].view(np.uint32), ref["edits"]["value"].view(np.uint32))
+
+
+@pytest.mark.parametrize("shape,world,seed", [((12, 7, 9), 2, 1), ((13, 6, 5), 3, 2), ((24, 5, 6), 4, 3)])
+def test_slab_emulated_oracle_engine(shape, world, seed):
+    f, fh, xi = _case(shape, seed)
+    plans = [slab.plan(shape[0], world, r) for r in range(world)]
+    engines = [OracleSlabEngine(p, shape[1], shape[2]) for p in plans]
+    fs, fhs = zip(*[slab.local_inputs(f, fh, p) for p in plans])
+    outs, stats = slab.run_emulated(engines, fs, fhs, xi)
+    assert stats["rounds"] > 1
+    _check_against_oracle(f, fh, xi, outs, stats)
+
+
+def _gloo_worker(rank, world, port, shape, seed, outdir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    f, fh, xi = _case(shape, seed)
+    p = slab.plan(shape[0], world, rank)
+    lf, lfh = slab.local_inputs(f, fh, p)
+    eng = OracleSlabEngine(p, shape[1], shape[2])
+    edits, _, stats = slab.run_distributed(eng, torch.from_numpy(lf), torch.from_numpy(lfh), xi)
+    np.save(os.path.join(outdir, f"edits{rank}.npy"), edits)
+    np.save(os.path.join(outdir, f"stats{rank}.npy"), np.array([stats["status"], stats["rounds"],
+                                                                 stats["n_false_round0"]] +
+                                                                stats["false_by_kind_round0"], np.int64))
+    dist.destroy_process_group()
+
+
+def test_slab_gloo_world2():
+    shape, seed, world = (14, 7, 8), 5, 2
+    with tempfile.TemporaryDirectory() as d:
+        port = 29500 + (os.getpid() % 1000)
+        mp.spawn(_gloo_worker, args=(world, port, shape, seed, d), nprocs=world, join=True)
+        outs = [(np.load(os.path.join(d, f"edits{r}.npy")), 0) for r in range(world)]
+        st = [np.load(os.path.join(d, f"stats{r}.npy")) for r in range(world)]
+    assert all(np.array_equal(st[0], s) for s in st)   # every rank took the same decisions
+    stats = dict(status=int(st[0][0]), rounds=int(st[0][1]), n_false_round0=int(st[0][2]),
+                 false_by_kind_round0=[int(x) for x in st[0][3:11]])
+    f, fh, xi = _case(shape, seed)
+    _check_against_oracle(f, fh, xi, outs, stats)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,shape,world", [("C4", (40, 37, 33), 2), ("C4", (40, 37, 33), 4),
+                                              ("C3", (30, 60, 70), 3), ("C4", (96, 96, 96), 8)])
+def test_slab_cuda_emulated_matches_single_gpu(name, shape, world):
+    """P slab ranks of the CUDA engine stepped in one process on one GPU (in-memory
+    halos) reproduce the single-GPU dmtz_correct bit for bit."""
+    import paper_2409_17346_b200 as dmtz
+    f, fh, xi, _ = di.config_inputs(name, shape=shape)
+    dev = torch.device("cuda", 0)
+    ref = dmtz.correct(torch.from_numpy(f).to(dev), torch.from_numpy(fh).to(dev), xi)
+    plans = [slab.plan(shape[0], world, r) for r in range(world)]
+    engines = [slab.CudaSlabEngine(p, shape[1], shape[2], dev) for p in plans]
+    loc = [slab.local_inputs(f, fh, p) for p in plans]
+    outs, stats = slab.run_emulated(engines, [torch.from_numpy(a).to(dev) for a, _ in loc],
+                                    [torch.from_numpy(b).to(dev) for _, b in loc], xi)
+    assert stats["status"] == ref.status and stats["rounds"] == ref.stats["rounds"]
+    assert stats["n_false_round0"] == ref.stats["n_false_round0"]
+    assert stats["false_by_kind_round0"] == ref.stats["false_by_kind_round0"]
+    e = torch.cat([o[0] for o in outs])
+    assert torch.equal(e, ref.edits)
+    g = torch.cat([eng.owned_g() for eng in engines])
+    assert torch.equal(g.view(torch.int32), ref.g.view(torch.int32))
