@@ -75,11 +75,15 @@ def _load():
                                ctypes.POINTER(i64), ctypes.POINTER(_Stats), P]
     L.dmtz_trace_separatrices.argtypes = [P, P, ctypes.c_uint32, P, ctypes.c_size_t, ctypes.POINTER(_Seps),
                                           i64, i64, ctypes.POINTER(i64), ctypes.POINTER(i64), P]
+    SZ = ctypes.c_size_t
+    L.dmtz_slab_begin.argtypes = [P, P, P, ctypes.POINTER(_Opts), P, P, SZ, P, P]
+    L.dmtz_slab_round.argtypes = [P, P, P, ctypes.POINTER(_Opts), P, P, SZ, P, i64, P, P, P]
+    L.dmtz_slab_end.argtypes = [P, P, P, SZ, P, P, i64, ctypes.POINTER(i64), ctypes.POINTER(i64), P]
     L.dmtz_status_string.argtypes = [i32]
     L.dmtz_status_string.restype = ctypes.c_char_p
     L.dmtz_last_error.restype = ctypes.c_char_p
     for fn in ("dmtz_ctx_create", "dmtz_compute_gradient", "dmtz_critical_mask", "dmtz_correct",
-               "dmtz_trace_separatrices", "dmtz_version"):
+               "dmtz_trace_separatrices", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end"):
         getattr(L, fn).restype = ctypes.c_int
     return L
 
@@ -87,7 +91,7 @@ def _load():
 _lib = _load()
 EXPORTED = ("dmtz_ctx_create", "dmtz_ctx_destroy", "dmtz_workspace_bytes", "dmtz_compute_gradient",
             "dmtz_critical_mask", "dmtz_correct", "dmtz_trace_separatrices", "dmtz_status_string",
-            "dmtz_last_error", "dmtz_version")
+            "dmtz_last_error", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end")
 
 
 def lib():

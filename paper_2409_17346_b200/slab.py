@@ -129,8 +129,9 @@ class CudaSlabEngine:
         k = (ctypes.c_int64 * 8)()
         self._check(self._lib.dmtz_slab_round(self.ctx._h, self._P(self.f), self._P(self.fhat),
                                               ctypes.byref(self.opts), ctypes.byref(self.slab),
-                                              self._P(self.ctx.workspace), self.ctx.ws_bytes, self._P(self.g), r, c,
-                                              k, self._stream_ptr()))
+                                              self._P(self.ctx.workspace), self.ctx.ws_bytes, self._P(self.g), r,
+                                              ctypes.cast(c, ctypes.c_void_p), ctypes.cast(k, ctypes.c_void_p),
+                                              self._stream_ptr()))
         return np.array(c[:], np.int64), np.array(k[:], np.int64)
 
     def end(self):
