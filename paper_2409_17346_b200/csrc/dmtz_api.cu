@@ -20,6 +20,24 @@
 
 using namespace dmtz;
 
+// The CUDA graph of the round loop: a conditional WHILE node whose body is one
+// captured round (enqueue_round); k_loop_check sets the condition on the device.
+struct LoopGraph {
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  // key: everything the captured body depends on
+  const void *f = nullptr, *fhat = nullptr, *g = nullptr, *ws = nullptr;
+  float xi = 0.f;
+  int q_max = -1, q_cap = -1, tier = -1, frontier = -1;
+  long long max_rounds = -1;
+  void reset() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    exec = nullptr;
+    graph = nullptr;
+  }
+};
+
 struct dmtz_ctx {
   dmtz_dims dims;
   Grid g;
@@ -28,7 +46,10 @@ struct dmtz_ctx {
   int rank, world;
   Counters* host_cnt;  // pinned
   cudaEvent_t ev[3];   // sweep timing (opts.profile): screen | decode
-  int verbose;         // DMTZ_VERBOSE=1: per-round counters on stderr
+  int verbose;         // DMTZ_VERBOSE=1: per-round counters on stderr (host-driven rounds)
+  int no_graph;        // DMTZ_NO_GRAPH=1: host-driven rounds instead of the CUDA-graph loop
+  LoopState* host_ls;  // pinned
+  struct LoopGraph* graph;
 };
 
 namespace {
@@ -121,6 +142,7 @@ struct WS {
   unsigned long long* lowpos;
   float* lb;
   Counters* dc;
+  LoopState* ls;             // second 256 B block of the counters region
   unsigned long long* bc;
   size_t rowbit_bytes;
   WS(char* ws, const Layout& L, const Grid& g) {
@@ -133,6 +155,7 @@ struct WS {
     state = (uint32_t*)(ws + L.state);
     tbits = (uint32_t*)(ws + L.tbits);
     dc = (Counters*)(ws + L.counters);
+    ls = (LoopState*)(ws + L.counters + sizeof(Counters));
     bc = (unsigned long long*)(ws + L.edit_bc);
     ebits = (uint32_t*)(ws + L.ebits);
     fmark = (uint32_t*)(ws + L.fmark);
@@ -189,16 +212,17 @@ inline cudaError_t units_range(const RowGeom& rg, int64_t z0, int64_t z1, uint32
   return cudaGetLastError();
 }
 
-// One C-loop round (a3-a6, + a7 frontier bits when fbits != nullptr).  The
-// screen runs over `units`/`n_units`, the decode over `dunits`/`n_dunits`;
-// targets outside [own_lo, own_hi) are dropped (slab mode).  Counters are copied
-// to host_cnt before returning (stream synchronised).
+// Enqueue one C-loop round (a3-a6, + a7 frontier when fbits != nullptr) and the
+// loop check; no host synchronisation, so the same sequence is captured into the
+// body of the CUDA-graph WHILE node.  The screen runs over `units`/`n_units`, the
+// decode over `dunits`/`n_dunits`; targets outside [own_lo, own_hi) are dropped
+// and only anchors in planes [count_z0, count_z1) are counted (slab mode).
 template <int D>
-dmtz_status round_phase(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o, WS<D>& W,
-                        float* g_out, int64_t round, const uint32_t* units, unsigned long long* n_units,
-                        const uint32_t* dunits, unsigned long long* n_dunits, uint32_t* fbits, int fwords,
-                        int64_t own_lo, int64_t own_hi, int64_t count_z0, int64_t count_z1, bool profile,
-                        int64_t* launches, cudaStream_t s) {
+dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o, WS<D>& W,
+                          float* g_out, const uint32_t* units, unsigned long long* n_units, const uint32_t* dunits,
+                          unsigned long long* n_dunits, uint32_t* fbits, int fwords, int64_t own_lo, int64_t own_hi,
+                          int64_t count_z0, int64_t count_z1, bool profile, unsigned long long max_rounds,
+                          cudaGraphConditionalHandle h, int use_cond, int64_t* launches, cudaStream_t s) {
   const Grid& g = c->g;
   const RowGeom rg = row_geom(g);
   const int64_t nwords = (g.N + 31) / 32;
@@ -206,27 +230,44 @@ dmtz_status round_phase(dmtz_ctx* c, const float* f, const float* fhat, const dm
   const float step = ldexpf(o->xi, -o->q_max);  // xi / 2^q_max, exact
   const int fwords_smem = fbits && fwords * 4 <= 32768 ? fwords : 0;
   CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));
-  if (fbits) CK(cudaMemsetAsync(fbits, 0, (size_t)fwords * 4, s));
-  if (fbits && round > 1) CK(cudaMemsetAsync(W.ebits, 0, W.rowbit_bytes, s));
+  if (fbits) {
+    CK(cudaMemsetAsync(fbits, 0, (size_t)fwords * 4, s));
+    CK(cudaMemsetAsync(W.ebits, 0, W.rowbit_bytes, s));  // rewritten for every active unit
+  }
   if (profile) CK(cudaEventRecord(c->ev[0], s));
-  k_screen<D><<<sweep_blocks, 256, 0, s>>>(g_out, W.cand_g, W.ebits, units, n_units, g, rg, round == 1 ? 1 : 0,
-                                           W.dc);
+  k_screen<D><<<sweep_blocks, 256, 0, s>>>(g_out, W.cand_g, W.ebits, units, n_units, g, rg, W.ls, W.dc);
   if (profile) CK(cudaEventRecord(c->ev[1], s));
   k_decode<D><<<sweep_blocks * 2, DECODE_THREADS, 0, s>>>(
       f, W.cand_f, W.crit_f, W.cand_g, W.crit_g, W.ebits, W.fmark, W.tbits, dunits, n_dunits, g, rg,
-      tier_mask<D>(o->tier), W.lowpos, round == 1 ? 1 : 0, own_lo, own_hi, count_z0, count_z1, W.dc);
+      tier_mask<D>(o->tier), W.lowpos, W.ls, own_lo, own_hi, count_z0, count_z1, W.dc);
   if (profile) CK(cudaEventRecord(c->ev[2], s));
   k_edit_rows<D><<<clamp_blocks(nwords, 256), 256, fwords_smem * 4, s>>>(
       W.tbits, nwords, fhat, W.lb, g_out, W.state, W.dc, step, o->q_cap, fbits, g, rg, fwords_smem);
-  *launches += 3;
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(c->host_cnt, W.dc, offsetof(Counters, first_nonfinite), cudaMemcpyDeviceToHost, s));
+  k_loop_check<<<1, 32, 0, s>>>(W.dc, W.ls, max_rounds, h, use_cond);
+  *launches += 4;
   if (fbits) {
-    // next round's unit list (after the counters were copied)
+    // next round's unit list (after the check read this round's counters)
     CK(cudaMemsetAsync(n_units, 0, 8, s));
     k_units_from_bits<<<clamp_blocks(rg.units, 256, 4096), 256, 0, s>>>(fbits, rg.units, (uint32_t*)units, n_units);
     *launches += 1;
   }
+  CK(cudaGetLastError());
+  return DMTZ_OK;
+}
+
+// One round with a host synchronisation: counters -> c->host_cnt, loop state -> *hls
+template <int D>
+dmtz_status round_phase(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o, WS<D>& W,
+                        float* g_out, const uint32_t* units, unsigned long long* n_units, const uint32_t* dunits,
+                        unsigned long long* n_dunits, uint32_t* fbits, int fwords, int64_t own_lo, int64_t own_hi,
+                        int64_t count_z0, int64_t count_z1, bool profile, unsigned long long max_rounds,
+                        LoopState* hls, int64_t* launches, cudaStream_t s) {
+  dmtz_status st = enqueue_round<D>(c, f, fhat, o, W, g_out, units, n_units, dunits, n_dunits, fbits, fwords, own_lo,
+                                    own_hi, count_z0, count_z1, profile, max_rounds, cudaGraphConditionalHandle(), 0,
+                                    launches, s);
+  if (st) return st;
+  CK(cudaMemcpyAsync(c->host_cnt, W.dc, offsetof(Counters, first_nonfinite), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hls, W.ls, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return DMTZ_OK;
 }
@@ -256,56 +297,103 @@ dmtz_status edits_phase(dmtz_ctx* c, WS<D>& W, const float* g_out, int64_t v0, i
 }
 
 template <int D>
+dmtz_status build_loop_graph(dmtz_ctx* c, LoopGraph& G, const float* f, const float* fhat,
+                             const dmtz_correct_opts* o, WS<D>& W, float* g_out, char* ws, const Layout& L,
+                             unsigned long long max_rounds, bool frontier_mode, cudaStream_t s) {
+  G.reset();
+  CK(cudaGraphCreate(&G.graph, 0));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, G.graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, G.graph, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CK(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  int64_t launches = 0;
+  dmtz_status st = enqueue_round<D>(c, f, fhat, o, W, g_out, W.units, &W.dc->n_units, W.units, &W.dc->n_units,
+                                    frontier_mode ? W.fbits : nullptr, (int)L.fwords, 0, c->g.N, 0, c->g.nz, false,
+                                    max_rounds, h, 1, &launches, s);
+  cudaGraph_t captured;
+  cudaError_t e = cudaStreamEndCapture(s, &captured);
+  if (st) return st;
+  CK(e);
+  CK(cudaGraphInstantiate(&G.exec, G.graph, 0));
+  G.f = f; G.fhat = fhat; G.g = g_out; G.ws = ws; G.xi = o->xi; G.q_max = o->q_max; G.q_cap = o->q_cap;
+  G.tier = o->tier; G.frontier = frontier_mode; G.max_rounds = (long long)max_rounds;
+  return DMTZ_OK;
+}
+
+template <int D>
 dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
                          char* ws, const Layout& L, float* g_out, dmtz_edit* edits, int64_t cap,
                          int64_t* n_edits, dmtz_stats* st, cudaStream_t s) {
   const Grid& g = c->g;
   WS<D> W(ws, L, g);
   Counters* hc = c->host_cnt;
+  LoopState* hls = c->host_ls;
   dmtz_status status = setup_phase<D>(c, f, fhat, o, W, g_out, 0, &st->launches, s);
   if (status != DMTZ_OK) { st->status = status; return status; }
-  const int64_t max_rounds = o->max_rounds > 0 ? o->max_rounds : g.N * (int64_t)(o->q_cap + 1);
+  const unsigned long long max_rounds =
+      o->max_rounds > 0 ? (unsigned long long)o->max_rounds : (unsigned long long)g.N * (unsigned long long)(o->q_cap + 1);
   const RowGeom rg = row_geom(g);
   unsigned long long* n_units = &W.dc->n_units;
   const bool frontier_mode = !o->full_sweeps;
   // round 1 (and every round of a full sweep) processes every unit
   CK(units_range(rg, 0, g.nz, W.units, n_units, s));
-  st->launches++;
-  for (int64_t round = 1;; round++) {
-    // a3: gradient of g (screened);  a4/a5: classify + mark targets;  a6: edit;  a7: frontier
-    status = round_phase<D>(c, f, fhat, o, W, g_out, round, W.units, n_units, W.units, n_units,
-                            frontier_mode ? W.fbits : nullptr, (int)L.fwords, 0, g.N, 0, g.nz, o->profile != 0,
-                            &st->launches, s);
-    if (status != DMTZ_OK) break;
-    if (o->profile) {
-      float ms0 = 0.f, ms1 = 0.f;
-      CK(cudaEventElapsedTime(&ms0, c->ev[0], c->ev[1]));
-      CK(cudaEventElapsedTime(&ms1, c->ev[1], c->ev[2]));
-      st->sweep_ms += ms0 + ms1;
-      st->screen_ms += ms0;
-      st->decode_ms += ms1;
-      if (ms0 > 0 && (int64_t)hc->n_swept == g.N) { st->screen_ms_full += ms0; st->n_screen_full++; }
+  k_loop_reset<<<1, 32, 0, s>>>(W.ls);
+  st->launches += 2;
+  const bool use_graph = !o->profile && !c->verbose && !c->no_graph;
+  if (use_graph) {
+    // a3-a7 on the device: one graph launch runs every round
+    LoopGraph& G = *c->graph;
+    if (!G.exec || G.f != f || G.fhat != fhat || G.g != g_out || G.ws != ws || G.xi != o->xi ||
+        G.q_max != o->q_max || G.q_cap != o->q_cap || G.tier != o->tier || G.frontier != (int)frontier_mode ||
+        G.max_rounds != (long long)max_rounds) {
+      status = build_loop_graph<D>(c, G, f, fhat, o, W, g_out, ws, L, max_rounds, frontier_mode, s);
+      if (status != DMTZ_OK) { st->status = status; return status; }
     }
-    st->sweeps++;
-    st->anchors_swept += (int64_t)hc->n_swept;
-    if (c->verbose)
-      fprintf(stderr, "dmtz round %lld: swept %llu false %llu targets %llu changed %llu\n", (long long)round,
-              hc->n_swept, hc->n_false, hc->n_targets, hc->n_changed);
-    if (hc->n_internal) {
-      set_err("gradient invariant violated at %llu false cells (round %lld)", hc->n_internal, (long long)round);
-      status = DMTZ_E_INTERNAL;
-      break;
+    CK(cudaGraphLaunch(G.exec, s));
+    CK(cudaMemcpyAsync(hls, W.ls, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    st->launches += 5 * (int64_t)hls->sweeps;
+  } else {
+    for (;;) {
+      const int64_t round = (int64_t)hls->round;
+      (void)round;
+      status = round_phase<D>(c, f, fhat, o, W, g_out, W.units, n_units, W.units, n_units,
+                              frontier_mode ? W.fbits : nullptr, (int)L.fwords, 0, g.N, 0, g.nz, o->profile != 0,
+                              max_rounds, hls, &st->launches, s);
+      if (status != DMTZ_OK) break;
+      if (o->profile) {
+        float ms0 = 0.f, ms1 = 0.f;
+        CK(cudaEventElapsedTime(&ms0, c->ev[0], c->ev[1]));
+        CK(cudaEventElapsedTime(&ms1, c->ev[1], c->ev[2]));
+        st->sweep_ms += ms0 + ms1;
+        st->screen_ms += ms0;
+        st->decode_ms += ms1;
+        if (ms0 > 0 && (int64_t)hc->n_swept == g.N) { st->screen_ms_full += ms0; st->n_screen_full++; }
+      }
+      if (c->verbose)
+        fprintf(stderr, "dmtz round %llu: swept %llu false %llu targets %llu changed %llu\n", hls->sweeps,
+                hc->n_swept, hc->n_false, hc->n_targets, hc->n_changed);
+      const bool go = hls->status == 0 && hls->rounds == hls->sweeps;  // check advanced the round
+      if (!go) break;
     }
-    if (round == 1) {
-      st->n_false_round0 = (int64_t)hc->n_false;
-      for (int k = 0; k < 8; k++) st->false_by_kind_round0[k] = (int64_t)hc->kinds[k];
-    }
-    if (hc->n_false == 0) break;
-    st->rounds = round;
-    if (hc->n_changed == 0) { status = DMTZ_E_STUCK; set_err("no target could move (round %lld)", (long long)round); break; }
-    if (round == max_rounds) { status = DMTZ_E_ITER_CAP; set_err("round cap %lld reached", (long long)round); break; }
   }
   if (status == DMTZ_E_CUDA) { st->status = status; return status; }
+  st->sweeps = (int64_t)hls->sweeps;
+  st->anchors_swept = (int64_t)hls->anchors_swept;
+  st->rounds = (int64_t)hls->rounds;
+  st->n_false_round0 = (int64_t)hls->n_false0;
+  for (int k = 0; k < 8; k++) st->false_by_kind_round0[k] = (int64_t)hls->kinds0[k];
+  status = (dmtz_status)hls->status;
+  if (status == DMTZ_E_INTERNAL) set_err("gradient invariant violated (round %llu)", hls->round);
+  else if (status == DMTZ_E_STUCK) set_err("no target could move (round %llu)", hls->round);
+  else if (status == DMTZ_E_ITER_CAP) set_err("round cap %llu reached", hls->round);
   // a8: edit list
   int64_t nl = 0;
   dmtz_status es = edits_phase<D>(c, W, g_out, 0, g.N, 0, edits, cap, n_edits, &nl, &st->launches, s);
@@ -359,10 +447,14 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
   c->g.sy = d->nx; c->g.sz = d->nx * d->ny;
   c->D = d->nz == 1 ? 2 : 3;
   c->device = cuda_device;
+  c->graph = new (std::nothrow) LoopGraph();
   c->rank = rank; c->world = world;
   const char* vb = getenv("DMTZ_VERBOSE");
   c->verbose = vb && vb[0] == '1';
+  const char* ng = getenv("DMTZ_NO_GRAPH");
+  c->no_graph = ng && ng[0] == '1';
   cudaError_t e = cudaMallocHost((void**)&c->host_cnt, sizeof(Counters) * 2);
+  if (e == cudaSuccess) e = cudaMallocHost((void**)&c->host_ls, sizeof(LoopState));
   if (e != cudaSuccess) { delete c; set_err("cudaMallocHost: %s", cudaGetErrorString(e)); return DMTZ_E_CUDA; }
   for (int i = 0; i < 3; i++) {
     e = cudaEventCreate(&c->ev[i]);
@@ -374,7 +466,9 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
 
 void dmtz_ctx_destroy(dmtz_ctx* c) {
   if (!c) return;
+  if (c->graph) { c->graph->reset(); delete c->graph; }
   cudaFreeHost(c->host_cnt);
+  cudaFreeHost(c->host_ls);
   for (int i = 0; i < 3; i++) cudaEventDestroy(c->ev[i]);
   delete c;
 }
@@ -479,8 +573,10 @@ dmtz_status dmtz_slab_round(dmtz_ctx* c, const float* f, const float* fhat, cons
   WS<3> W((char*)workspace, L, c->g);
   int64_t launches = 0;
   const int64_t plane = c->g.sz;
-  st = round_phase<3>(c, f, fhat, o, W, g_out, round, W.units, &W.dc->n_units, W.units2, &W.dc->n_units2, nullptr,
-                      0, sl->own_z0 * plane, sl->own_z1 * plane, sl->own_z0, sl->own_z1, false, &launches, s);
+  k_set_round<<<1, 32, 0, s>>>(W.ls, (unsigned long long)round);
+  st = round_phase<3>(c, f, fhat, o, W, g_out, W.units, &W.dc->n_units, W.units2, &W.dc->n_units2, nullptr, 0,
+                      sl->own_z0 * plane, sl->own_z1 * plane, sl->own_z0, sl->own_z1, false, ~0ull, c->host_ls,
+                      &launches, s);
   if (st) return st;
   Counters* hc = c->host_cnt;
   counters[0] = (int64_t)hc->n_false;

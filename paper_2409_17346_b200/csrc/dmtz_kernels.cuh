@@ -34,6 +34,38 @@ struct Counters {                 // device-side round counters (one 256 B block
 };
 static_assert(sizeof(Counters) == 256, "counters are one 256 B block");
 
+// Device-side state of the round loop (a7), updated by k_loop_check after every
+// round; lets the loop run inside a CUDA-graph conditional WHILE node.
+struct LoopState {
+  unsigned long long round;          // the round about to run / running (1-based)
+  unsigned long long rounds;         // rounds that found false cells
+  unsigned long long sweeps;
+  unsigned long long anchors_swept;
+  unsigned long long n_false0;       // false cells before any edit
+  unsigned long long kinds0[8];
+  unsigned long long status;         // dmtz_status of the loop (0 while running / OK)
+  unsigned long long last_false, last_changed, last_targets, last_swept;
+  unsigned long long pad[14];
+};
+static_assert(sizeof(LoopState) == 256, "loop state is one 256 B block");
+
+__global__ void k_set_round(LoopState* ls, unsigned long long r) {
+  if (threadIdx.x == 0) ls->round = r;
+}
+
+__global__ void k_loop_reset(LoopState* ls) {
+  if (threadIdx.x == 0) {
+    LoopState z = {};
+    z.round = 1;
+    *ls = z;
+  }
+}
+
+// The stop rule of the C-loop: F empty -> OK; no target
+// could move -> STUCK; round cap -> ITER_CAP.  Sets the WHILE condition when use_cond.
+__global__ void k_loop_check(const struct Counters* cnt, LoopState* ls, unsigned long long max_rounds,
+                             cudaGraphConditionalHandle h, int use_cond);
+
 template <int D> struct Tr;
 template <> struct Tr<3> {
   using code_t = unsigned long long;
@@ -45,6 +77,34 @@ template <> struct Tr<2> {
   static constexpr int NT = k2d::NT, TOP = 2, NDELTA = 4;
   static constexpr uint64_t ALL_NONE = k2d::ALL_NONE;
 };
+
+__global__ void k_loop_check(const Counters* cnt, LoopState* ls, unsigned long long max_rounds,
+                             cudaGraphConditionalHandle h, int use_cond) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long r = ls->round;
+  ls->sweeps++;
+  ls->anchors_swept += cnt->n_swept;
+  ls->last_false = cnt->n_false;
+  ls->last_changed = cnt->n_changed;
+  ls->last_targets = cnt->n_targets;
+  ls->last_swept = cnt->n_swept;
+  bool go = false;
+  if (cnt->n_internal) {
+    ls->status = 11;  // DMTZ_E_INTERNAL
+  } else {
+    if (r == 1) {
+      ls->n_false0 = cnt->n_false;
+      for (int k = 0; k < 8; k++) ls->kinds0[k] = cnt->kinds[k];
+    }
+    if (cnt->n_false != 0) {
+      ls->rounds = r;
+      if (cnt->n_changed == 0) ls->status = 7;        // DMTZ_E_STUCK
+      else if (r == max_rounds) ls->status = 6;        // DMTZ_E_ITER_CAP
+      else { ls->round = r + 1; go = true; }
+    }
+  }
+  if (use_cond) cudaGraphSetConditional(h, go ? 1u : 0u);
+}
 
 // table accessors (constant-folded when t is a compile-time constant after unrolling)
 #define DMTZ_TAB(D, name) ((D) == 3 ? k3d::name : k2d::name)

@@ -116,7 +116,8 @@ template <int D>
 __global__ void __launch_bounds__(256)
 k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg, uint32_t* __restrict__ ebits,
          const uint32_t* __restrict__ units, const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg,
-         int first_round, Counters* __restrict__ cnt) {
+         const LoopState* __restrict__ ls, Counters* __restrict__ cnt) {
+  const bool first_round = ls->round == 1;
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -247,8 +248,9 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
          uint32_t* __restrict__ crit_g, const uint32_t* __restrict__ ebits, uint32_t* __restrict__ fmark,
          uint32_t* __restrict__ tbits, const uint32_t* __restrict__ units,
          const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg, uint32_t tier_mask,
-         const unsigned long long* __restrict__ lowpos_f, int count_kinds, int64_t own_lo, int64_t own_hi,
-         int64_t count_z0, int64_t count_z1, Counters* __restrict__ cnt) {
+         const unsigned long long* __restrict__ lowpos_f, const LoopState* __restrict__ ls, int64_t own_lo,
+         int64_t own_hi, int64_t count_z0, int64_t count_z1, Counters* __restrict__ cnt) {
+  const bool count_kinds = ls->round == 1;  // kinds are reported for round 1 only
   __shared__ TargetTables T;
   __shared__ DecodeWarpSmem WS[DECODE_THREADS / 32];
   init_target_tables<D>(T, g);
