@@ -50,6 +50,7 @@ struct dmtz_ctx {
   int no_graph;        // DMTZ_NO_GRAPH=1: host-driven rounds instead of the CUDA-graph loop
   LoopState* host_ls;  // pinned
   struct LoopGraph* graph;
+  cudaStream_t cap_stream;  // private stream the loop body is captured on (the caller's may be the legacy stream)
 };
 
 namespace {
@@ -312,13 +313,15 @@ dmtz_status build_loop_graph(dmtz_ctx* c, LoopGraph& G, const float* f, const fl
   cudaGraphNode_t node;
   CK(cudaGraphAddNode(&node, G.graph, nullptr, 0, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
-  CK(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  (void)s;
+  cudaStream_t cs = c->cap_stream;
+  CK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   int64_t launches = 0;
   dmtz_status st = enqueue_round<D>(c, f, fhat, o, W, g_out, W.units, &W.dc->n_units, W.units, &W.dc->n_units,
                                     frontier_mode ? W.fbits : nullptr, (int)L.fwords, 0, c->g.N, 0, c->g.nz, false,
-                                    max_rounds, h, 1, &launches, s);
+                                    max_rounds, h, 1, &launches, cs);
   cudaGraph_t captured;
-  cudaError_t e = cudaStreamEndCapture(s, &captured);
+  cudaError_t e = cudaStreamEndCapture(cs, &captured);
   if (st) return st;
   CK(e);
   CK(cudaGraphInstantiate(&G.exec, G.graph, 0));
@@ -346,7 +349,7 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
   CK(units_range(rg, 0, g.nz, W.units, n_units, s));
   k_loop_reset<<<1, 32, 0, s>>>(W.ls);
   st->launches += 2;
-  const bool use_graph = !o->profile && !c->verbose && !c->no_graph;
+  const bool use_graph = !o->profile && !c->verbose && !c->no_graph && c->cap_stream && c->graph;
   if (use_graph) {
     // a3-a7 on the device: one graph launch runs every round
     LoopGraph& G = *c->graph;
@@ -448,6 +451,7 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
   c->D = d->nz == 1 ? 2 : 3;
   c->device = cuda_device;
   c->graph = new (std::nothrow) LoopGraph();
+  if (cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess) c->cap_stream = nullptr;
   c->rank = rank; c->world = world;
   const char* vb = getenv("DMTZ_VERBOSE");
   c->verbose = vb && vb[0] == '1';
@@ -467,6 +471,7 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
 void dmtz_ctx_destroy(dmtz_ctx* c) {
   if (!c) return;
   if (c->graph) { c->graph->reset(); delete c->graph; }
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   cudaFreeHost(c->host_cnt);
   cudaFreeHost(c->host_ls);
   for (int i = 0; i < 3; i++) cudaEventDestroy(c->ev[i]);
