@@ -227,7 +227,9 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
   const Grid& g = c->g;
   const RowGeom rg = row_geom(g);
   const int64_t nwords = (g.N + 31) / 32;
-  const int sweep_blocks = 148 * 8;
+  // grids sized by the largest possible work list (small grids: few blocks, cheap launches)
+  const int64_t max_items = rg.units * UY * ((rg.wpr + CG - 1) / CG);
+  const int sweep_blocks = (int)(max_items / 8 + 1 < 148 * 8 ? max_items / 8 + 1 : 148 * 8);
   const float step = ldexpf(o->xi, -o->q_max);  // xi / 2^q_max, exact
   const int fwords_smem = fbits && fwords * 4 <= 32768 ? fwords : 0;
   CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));
