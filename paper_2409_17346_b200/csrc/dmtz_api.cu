@@ -232,11 +232,8 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
   const int sweep_blocks = (int)(max_items / 8 + 1 < 148 * 8 ? max_items / 8 + 1 : 148 * 8);
   const float step = ldexpf(o->xi, -o->q_max);  // xi / 2^q_max, exact
   const int fwords_smem = fbits && fwords * 4 <= 32768 ? fwords : 0;
-  CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));
-  if (fbits) {
-    CK(cudaMemsetAsync(fbits, 0, (size_t)fwords * 4, s));
-    CK(cudaMemsetAsync(W.ebits, 0, W.rowbit_bytes, s));  // rewritten for every active unit
-  }
+  if (!use_cond) CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));  // else: k_loop_check
+  if (fbits) CK(cudaMemsetAsync(W.ebits, 0, W.rowbit_bytes, s));  // rewritten for every active unit
   if (profile) CK(cudaEventRecord(c->ev[0], s));
   k_screen<D><<<sweep_blocks, 256, 0, s>>>(g_out, W.cand_g, W.ebits, units, n_units, g, rg, W.ls, W.dc);
   if (profile) CK(cudaEventRecord(c->ev[1], s));
@@ -246,11 +243,11 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
   if (profile) CK(cudaEventRecord(c->ev[2], s));
   k_edit_rows<D><<<clamp_blocks(nwords, 256), 256, fwords_smem * 4, s>>>(
       W.tbits, nwords, fhat, W.lb, g_out, W.state, W.dc, step, o->q_cap, fbits, g, rg, fwords_smem);
-  k_loop_check<<<1, 32, 0, s>>>(W.dc, W.ls, max_rounds, h, use_cond);
+  k_loop_check<<<1, 32, 0, s>>>(W.dc, W.ls, max_rounds, h, use_cond, fbits ? n_units : nullptr);
   *launches += 4;
   if (fbits) {
-    // next round's unit list (after the check read this round's counters)
-    CK(cudaMemsetAsync(n_units, 0, 8, s));
+    // next round's unit list (after the check read this round's counters); clears fbits
+    if (!use_cond) CK(cudaMemsetAsync(n_units, 0, 8, s));
     k_units_from_bits<<<clamp_blocks(rg.units, 256, 4096), 256, 0, s>>>(fbits, rg.units, (uint32_t*)units, n_units);
     *launches += 1;
   }
@@ -349,6 +346,8 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
   const bool frontier_mode = !o->full_sweeps;
   // round 1 (and every round of a full sweep) processes every unit
   CK(units_range(rg, 0, g.nz, W.units, n_units, s));
+  CK(cudaMemsetAsync(W.fbits, 0, (size_t)L.fwords * 4, s));
+  CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));
   k_loop_reset<<<1, 32, 0, s>>>(W.ls);
   st->launches += 2;
   const bool use_graph = !o->profile && !c->verbose && !c->no_graph && c->cap_stream && c->graph;

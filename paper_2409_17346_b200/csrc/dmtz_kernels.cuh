@@ -63,8 +63,8 @@ __global__ void k_loop_reset(LoopState* ls) {
 
 // The stop rule of the C-loop: F empty -> OK; no target
 // could move -> STUCK; round cap -> ITER_CAP.  Sets the WHILE condition when use_cond.
-__global__ void k_loop_check(const struct Counters* cnt, LoopState* ls, unsigned long long max_rounds,
-                             cudaGraphConditionalHandle h, int use_cond);
+__global__ void k_loop_check(struct Counters* cnt, LoopState* ls, unsigned long long max_rounds,
+                             cudaGraphConditionalHandle h, int use_cond, unsigned long long* n_units_clear);
 
 template <int D> struct Tr;
 template <> struct Tr<3> {
@@ -78,8 +78,8 @@ template <> struct Tr<2> {
   static constexpr uint64_t ALL_NONE = k2d::ALL_NONE;
 };
 
-__global__ void k_loop_check(const Counters* cnt, LoopState* ls, unsigned long long max_rounds,
-                             cudaGraphConditionalHandle h, int use_cond) {
+__global__ void k_loop_check(Counters* cnt, LoopState* ls, unsigned long long max_rounds,
+                             cudaGraphConditionalHandle h, int use_cond, unsigned long long* n_units_clear) {
   if (threadIdx.x != 0) return;
   const unsigned long long r = ls->round;
   ls->sweeps++;
@@ -103,8 +103,16 @@ __global__ void k_loop_check(const Counters* cnt, LoopState* ls, unsigned long l
       else { ls->round = r + 1; go = true; }
     }
   }
-  if (use_cond) cudaGraphSetConditional(h, go ? 1u : 0u);
+  if (use_cond) {
+    // device-driven loop: clear this round's counters (and the frontier list length)
+    // for the next round here instead of with memset nodes
+    unsigned long long* p = (unsigned long long*)cnt;
+    for (int i = 0; i < (int)(offsetof(Counters, first_nonfinite) / 8); i++) p[i] = 0ull;
+    if (n_units_clear) *n_units_clear = 0ull;
+    cudaGraphSetConditional(h, go ? 1u : 0u);
+  }
 }
+
 
 // table accessors (constant-folded when t is a compile-time constant after unrolling)
 #define DMTZ_TAB(D, name) ((D) == 3 ? k3d::name : k2d::name)

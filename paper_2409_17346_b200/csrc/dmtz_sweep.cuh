@@ -498,15 +498,17 @@ __global__ void k_lowpos(const float* __restrict__ f, unsigned long long* __rest
 }
 
 // active unit list from the frontier bitmap (ordered compaction), count -> *n_out
-__global__ void k_units_from_bits(const uint32_t* __restrict__ fbits, int64_t n_units, uint32_t* __restrict__ list,
+__global__ void k_units_from_bits(uint32_t* __restrict__ fbits, int64_t n_units, uint32_t* __restrict__ list,
                                   unsigned long long* __restrict__ n_out) {
   // single pass with one atomic per warp; order inside the list does not matter
   const int lane = threadIdx.x & 31;
   for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) - lane; base < n_units;
        base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t u = base + lane;
-    const bool on = u < n_units && ((fbits[u >> 5] >> (u & 31)) & 1u);
+    const uint32_t word = u < n_units ? fbits[u >> 5] : 0u;
+    const bool on = (word >> (u & 31)) & 1u;
     const unsigned bal = __ballot_sync(0xffffffffu, on);
+    if (lane == 0 && u < n_units) fbits[u >> 5] = 0u;  // cleared for the next round
     unsigned long long pos = 0;
     if (lane == 0 && bal) pos = atomicAdd(n_out, (unsigned long long)__popc(bal));
     pos = __shfl_sync(0xffffffffu, pos, 0);
