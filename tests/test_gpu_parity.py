@@ -262,3 +262,15 @@ def test_full_size_cloop_properties(dmtz, name):
         _, mg = oracle.gradient(np.ascontiguousarray(g[sl]))
         inner = tuple(slice(1, 18) for _ in cfg.shape)
         assert np.array_equal(mf[inner], mg[inner])
+
+
+@pytest.mark.parametrize("full_sweeps", [False, True])
+def test_iter_cap_matches_oracle(dmtz, full_sweeps):
+    """The device-side stop rule (CUDA-graph WHILE loop) on the round cap."""
+    f, fh, xi, _ = di.config_inputs("C4", shape=(20, 21, 22))
+    ref = oracle.correct(f, fh, xi, 6, 6, 2, max_rounds=3)
+    assert ref["status"] == oracle.E_ITER_CAP
+    r = dmtz.correct(_cuda(f), _cuda(fh), xi, max_rounds=3, full_sweeps=full_sweeps)
+    assert r.status == dmtz.E_ITER_CAP and r.stats["rounds"] == 3 == ref["stats"]["rounds"]
+    assert np.array_equal(r.g.cpu().numpy().view(np.uint32), ref["g"].view(np.uint32))
+    assert np.array_equal(r.edits_numpy()["v"], ref["edits"]["v"])
