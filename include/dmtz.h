@@ -113,8 +113,10 @@ typedef struct {
   double sweep_ms;         /* opts.profile: summed device time of the round sweeps (screen + decode) */
   double screen_ms;        /* opts.profile: of which the gradient screening kernel */
   double decode_ms;        /* opts.profile: of which the classification / target kernel */
-  double screen_ms_full;   /* opts.profile: screening time of the rounds that swept every anchor */
+  double screen_ms_full;   /* opts.profile: screening time of the rounds that recomputed every code */
   int64_t n_screen_full;   /* number of such rounds */
+  int64_t anchors_recomputed; /* sum over sweeps of anchors whose code was recomputed (the rest
+                                 provably kept theirs: no vertex of their 3x3x3 box changed) */
 } dmtz_stats;
 
 typedef struct dmtz_ctx dmtz_ctx;

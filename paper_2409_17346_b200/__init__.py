@@ -53,7 +53,8 @@ class _Stats(ctypes.Structure):
                 ("false_by_kind_round0", ctypes.c_int64 * 8), ("status", ctypes.c_int32),
                 ("pad", ctypes.c_int32), ("sweeps", ctypes.c_int64), ("anchors_swept", ctypes.c_int64),
                 ("launches", ctypes.c_int64), ("sweep_ms", ctypes.c_double), ("screen_ms", ctypes.c_double),
-                ("decode_ms", ctypes.c_double), ("screen_ms_full", ctypes.c_double), ("n_screen_full", ctypes.c_int64)]
+                ("decode_ms", ctypes.c_double), ("screen_ms_full", ctypes.c_double), ("n_screen_full", ctypes.c_int64),
+                ("anchors_recomputed", ctypes.c_int64)]
 
 
 class _Seps(ctypes.Structure):
@@ -201,7 +202,8 @@ class Context:
                      n_false_round0=st.n_false_round0, false_by_kind_round0=list(st.false_by_kind_round0),
                      status=status, sweeps=st.sweeps, anchors_swept=st.anchors_swept, launches=st.launches,
                      sweep_ms=st.sweep_ms, screen_ms=st.screen_ms, decode_ms=st.decode_ms,
-                     screen_ms_full=st.screen_ms_full, n_screen_full=st.n_screen_full)
+                     screen_ms_full=st.screen_ms_full, n_screen_full=st.n_screen_full,
+                     anchors_recomputed=st.anchors_recomputed)
         msg = _lib.dmtz_last_error().decode() if status != OK else ""
         if raise_on_error and status not in (OK, E_STUCK, E_ITER_CAP, E_CAPACITY):
             raise DmtzError(status, msg)

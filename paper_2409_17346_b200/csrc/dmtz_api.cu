@@ -77,8 +77,8 @@ inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 // Workspace layout (offsets from the base, each 256-B aligned)
 struct Layout {
-  size_t cand_f, cand_g, crit_f, crit_g, lowpos, lb, state, tbits, counters, edit_bc, ebits, fmark, units, units2,
-      frontier, trace, total;
+  size_t cand_f, cand_g, crit_f, crit_g, lowpos, lb, state, tbits, counters, edit_bc, ebits, fmark, vchg, units,
+      units2, frontier, trace, total;
   int64_t fwords;  // frontier bitmap words (one bit per row-block unit)
 };
 
@@ -103,6 +103,7 @@ Layout layout_for(const dmtz_ctx* c) {
   L.fwords = (rg.units + 31) / 32;
   L.ebits = o; o += align_up((size_t)(c->g.nz * c->g.ny * rg.wpr) * 4 + 64);
   L.fmark = o; o += align_up((size_t)(c->g.nz * c->g.ny * rg.wpr) * 4 + 64);
+  L.vchg = o; o += align_up(2 * (size_t)(c->g.nz * c->g.ny * rg.wpr) * 4 + 64);
   L.units = o; o += align_up((size_t)rg.units * 4);
   L.units2 = o; o += align_up((size_t)rg.units * 4);
   L.frontier = o; o += align_up(L.fwords * 4 + 64);
@@ -139,7 +140,8 @@ struct WS {
   using code_t = typename Tr<D>::code_t;
   code_t* cand_f;
   code_t* cand_g;            // codes of g, memoized across rounds
-  uint32_t *crit_f, *crit_g, *state, *tbits, *ebits, *fmark, *units, *units2, *fbits;
+  uint32_t *crit_f, *crit_g, *state, *tbits, *ebits, *fmark, *vchg, *units, *units2, *fbits;
+  int64_t vwords;
   unsigned long long* lowpos;
   float* lb;
   Counters* dc;
@@ -160,11 +162,13 @@ struct WS {
     bc = (unsigned long long*)(ws + L.edit_bc);
     ebits = (uint32_t*)(ws + L.ebits);
     fmark = (uint32_t*)(ws + L.fmark);
+    vchg = (uint32_t*)(ws + L.vchg);
     units = (uint32_t*)(ws + L.units);
     units2 = (uint32_t*)(ws + L.units2);
     fbits = (uint32_t*)(ws + L.frontier);
     const RowGeom rg = row_geom(g);
     rowbit_bytes = (size_t)(g.nz * g.ny * rg.wpr) * 4;
+    vwords = g.nz * g.ny * rg.wpr;
   }
 };
 
@@ -185,6 +189,7 @@ dmtz_status setup_phase(dmtz_ctx* c, const float* f, const float* fhat, const dm
   CK(cudaMemsetAsync(&W.dc->first_nonfinite, 0xFF, 16, s));
   CK(cudaMemsetAsync(W.tbits, 0, nwords * 4, s));
   CK(cudaMemsetAsync(W.fmark, 0, W.rowbit_bytes, s));
+  CK(cudaMemsetAsync(W.vchg, 0, 2 * W.rowbit_bytes, s));
   k_setup<<<clamp_blocks(g.N, 256), 256, 0, s>>>(f, fhat, o->xi, g.N, W.lb, g_out, W.state, W.dc);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(hc, W.dc, sizeof(Counters), cudaMemcpyDeviceToHost, s));
@@ -223,7 +228,8 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
                           float* g_out, const uint32_t* units, unsigned long long* n_units, const uint32_t* dunits,
                           unsigned long long* n_dunits, uint32_t* fbits, int fwords, int64_t own_lo, int64_t own_hi,
                           int64_t count_z0, int64_t count_z1, bool profile, unsigned long long max_rounds,
-                          cudaGraphConditionalHandle h, int use_cond, int64_t* launches, cudaStream_t s) {
+                          cudaGraphConditionalHandle h, int use_cond, int use_skip, int64_t* launches,
+                          cudaStream_t s) {
   const Grid& g = c->g;
   const RowGeom rg = row_geom(g);
   const int64_t nwords = (g.N + 31) / 32;
@@ -235,14 +241,16 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
   if (!use_cond) CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));  // else: k_loop_check
   if (fbits) CK(cudaMemsetAsync(W.ebits, 0, W.rowbit_bytes, s));  // rewritten for every active unit
   if (profile) CK(cudaEventRecord(c->ev[0], s));
-  k_screen<D><<<sweep_blocks, 256, 0, s>>>(g_out, W.cand_g, W.ebits, units, n_units, g, rg, W.ls, W.dc);
+  k_screen<D><<<sweep_blocks, 256, 0, s>>>(g_out, W.cand_g, W.ebits, W.vchg, W.vwords, use_skip, units, n_units, g,
+                                           rg, W.ls, W.dc);
   if (profile) CK(cudaEventRecord(c->ev[1], s));
   k_decode<D><<<sweep_blocks * 2, DECODE_THREADS, 0, s>>>(
       f, W.cand_f, W.crit_f, W.cand_g, W.crit_g, W.ebits, W.fmark, W.tbits, dunits, n_dunits, g, rg,
       tier_mask<D>(o->tier), W.lowpos, W.ls, own_lo, own_hi, count_z0, count_z1, W.dc);
   if (profile) CK(cudaEventRecord(c->ev[2], s));
   k_edit_rows<D><<<clamp_blocks(nwords, 256), 256, fwords_smem * 4, s>>>(
-      W.tbits, nwords, fhat, W.lb, g_out, W.state, W.dc, step, o->q_cap, fbits, g, rg, fwords_smem);
+      W.tbits, nwords, fhat, W.lb, g_out, W.state, W.dc, step, o->q_cap, fbits, g, rg, fwords_smem,
+      use_skip ? W.vchg : nullptr, W.vwords, W.ls);
   k_loop_check<<<1, 32, 0, s>>>(W.dc, W.ls, max_rounds, h, use_cond, fbits ? n_units : nullptr);
   *launches += 4;
   if (fbits) {
@@ -261,10 +269,10 @@ dmtz_status round_phase(dmtz_ctx* c, const float* f, const float* fhat, const dm
                         float* g_out, const uint32_t* units, unsigned long long* n_units, const uint32_t* dunits,
                         unsigned long long* n_dunits, uint32_t* fbits, int fwords, int64_t own_lo, int64_t own_hi,
                         int64_t count_z0, int64_t count_z1, bool profile, unsigned long long max_rounds,
-                        LoopState* hls, int64_t* launches, cudaStream_t s) {
+                        int use_skip, LoopState* hls, int64_t* launches, cudaStream_t s) {
   dmtz_status st = enqueue_round<D>(c, f, fhat, o, W, g_out, units, n_units, dunits, n_dunits, fbits, fwords, own_lo,
                                     own_hi, count_z0, count_z1, profile, max_rounds, cudaGraphConditionalHandle(), 0,
-                                    launches, s);
+                                    use_skip, launches, s);
   if (st) return st;
   CK(cudaMemcpyAsync(c->host_cnt, W.dc, offsetof(Counters, first_nonfinite), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(hls, W.ls, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
@@ -318,7 +326,7 @@ dmtz_status build_loop_graph(dmtz_ctx* c, LoopGraph& G, const float* f, const fl
   int64_t launches = 0;
   dmtz_status st = enqueue_round<D>(c, f, fhat, o, W, g_out, W.units, &W.dc->n_units, W.units, &W.dc->n_units,
                                     frontier_mode ? W.fbits : nullptr, (int)L.fwords, 0, c->g.N, 0, c->g.nz, false,
-                                    max_rounds, h, 1, &launches, cs);
+                                    max_rounds, h, 1, 1, &launches, cs);
   cudaGraph_t captured;
   cudaError_t e = cudaStreamEndCapture(cs, &captured);
   if (st) return st;
@@ -370,7 +378,7 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
       (void)round;
       status = round_phase<D>(c, f, fhat, o, W, g_out, W.units, n_units, W.units, n_units,
                               frontier_mode ? W.fbits : nullptr, (int)L.fwords, 0, g.N, 0, g.nz, o->profile != 0,
-                              max_rounds, hls, &st->launches, s);
+                              max_rounds, 1, hls, &st->launches, s);
       if (status != DMTZ_OK) break;
       if (o->profile) {
         float ms0 = 0.f, ms1 = 0.f;
@@ -379,7 +387,7 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
         st->sweep_ms += ms0 + ms1;
         st->screen_ms += ms0;
         st->decode_ms += ms1;
-        if (ms0 > 0 && (int64_t)hc->n_swept == g.N) { st->screen_ms_full += ms0; st->n_screen_full++; }
+        if (ms0 > 0 && (int64_t)hc->n_recomputed == g.N) { st->screen_ms_full += ms0; st->n_screen_full++; }
       }
       if (c->verbose)
         fprintf(stderr, "dmtz round %llu: swept %llu false %llu targets %llu changed %llu\n", hls->sweeps,
@@ -391,6 +399,7 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
   if (status == DMTZ_E_CUDA) { st->status = status; return status; }
   st->sweeps = (int64_t)hls->sweeps;
   st->anchors_swept = (int64_t)hls->anchors_swept;
+  st->anchors_recomputed = (int64_t)hls->recomputed;
   st->rounds = (int64_t)hls->rounds;
   st->n_false_round0 = (int64_t)hls->n_false0;
   for (int k = 0; k < 8; k++) st->false_by_kind_round0[k] = (int64_t)hls->kinds0[k];
@@ -581,8 +590,8 @@ dmtz_status dmtz_slab_round(dmtz_ctx* c, const float* f, const float* fhat, cons
   const int64_t plane = c->g.sz;
   k_set_round<<<1, 32, 0, s>>>(W.ls, (unsigned long long)round);
   st = round_phase<3>(c, f, fhat, o, W, g_out, W.units, &W.dc->n_units, W.units2, &W.dc->n_units2, nullptr, 0,
-                      sl->own_z0 * plane, sl->own_z1 * plane, sl->own_z0, sl->own_z1, false, ~0ull, c->host_ls,
-                      &launches, s);
+                      sl->own_z0 * plane, sl->own_z1 * plane, sl->own_z0, sl->own_z1, false, ~0ull,
+                      0 /* halos change outside this rank's edits: no change skipping */, c->host_ls, &launches, s);
   if (st) return st;
   Counters* hc = c->host_cnt;
   counters[0] = (int64_t)hc->n_false;

@@ -115,30 +115,59 @@ __device__ __forceinline__ uint64_t cand_of(const float (&s)[27]) {
 template <int D>
 __global__ void __launch_bounds__(256)
 k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg, uint32_t* __restrict__ ebits,
-         const uint32_t* __restrict__ units, const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg,
-         const LoopState* __restrict__ ls, Counters* __restrict__ cnt) {
-  const bool first_round = ls->round == 1;
+         uint32_t* __restrict__ vchg, int64_t vwords, int use_skip, const uint32_t* __restrict__ units,
+         const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg, const LoopState* __restrict__ ls,
+         Counters* __restrict__ cnt) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long swept = 0;
+  const unsigned long long round = ls->round;
+  const bool first_round = round == 1;
+  // vertices whose value changed in the previous round (its edits) / this round's (cleared here)
+  const uint32_t* vprev = vchg + (int64_t)((round - 1) & 1) * vwords;
+  uint32_t* vcur = vchg + (int64_t)(round & 1) * vwords;
+  const bool skip = use_skip && !first_round;
+  unsigned long long swept = 0, recomputed = 0;
   WORK_LOOP_BEGIN
+    // need(u): a vertex of u's 3x3x3 box changed -> the code may change; else it provably
+    // did not (a code is a function of that box) and the memoized one stays.
+    uint32_t need = 0xffffffffu;
+    if (skip) {
+      uint32_t contrib = 0;
+      if (lane < 27) {
+        const int dx = lane / 9 - 1, r9 = lane % 9;
+        const int64_t yy = y + (r9 % 3) - 1, zz = D == 3 ? z + (r9 / 3) - 1 : z;
+        const int64_t cc = c + dx;
+        const bool ok_row = yy >= 0 && yy < g.ny && zz >= 0 && zz < g.nz && cc >= 0 && cc < rg.wpr &&
+                            (D == 3 || r9 / 3 == 1);
+        if (ok_row) {
+          const uint32_t w = __ldg(vprev + dword_index(g, rg, yy, zz, cc));
+          contrib = dx < 0 ? (w >> 31) : dx > 0 ? (w << 31) : (w | (w << 1) | (w >> 1));
+        }
+      }
+      need = __reduce_or_sync(0xffffffffu, contrib);
+    }
+    if (lane == 0) vcur[dword_index(g, rg, y, z, c)] = 0u;
     const int64_t x = c * 32 + lane;
     bool e = false;
     if (x < g.nx) {
-      const int64_t v = x + y * g.sy + z * g.sz;
-      float s[27];
-      load_stencil<D>(gfld, g, v, x, y, z, s);
-      const int ok = axes_ok(g, x, y, z);
-      const uint64_t code = cand_of<D>(s) | t_nonex_fill<D>(ok);
-      e = first_round || code != (uint64_t)cg[v];
-      if (e) cg[v] = (typename Tr<D>::code_t)code;
       swept++;
+      if ((need >> lane) & 1u) {
+        const int64_t v = x + y * g.sy + z * g.sz;
+        float s[27];
+        load_stencil<D>(gfld, g, v, x, y, z, s);
+        const int ok = axes_ok(g, x, y, z);
+        const uint64_t code = cand_of<D>(s) | t_nonex_fill<D>(ok);
+        e = first_round || code != (uint64_t)cg[v];
+        if (e) cg[v] = (typename Tr<D>::code_t)code;
+        recomputed++;
+      }
     }
     const unsigned bal = __ballot_sync(0xffffffffu, e);
     if (lane == 0) ebits[dword_index(g, rg, y, z, c)] = bal;
   WORK_LOOP_END
   warp_add(&cnt->n_swept, swept);
+  warp_add(&cnt->n_recomputed, recomputed);
 }
 
 // ---------------------------------------------------------------------------
@@ -410,7 +439,9 @@ template <int D>
 __global__ void k_edit_rows(uint32_t* __restrict__ tbits, int64_t nwords, const float* __restrict__ fhat,
                             const float* __restrict__ lb, float* __restrict__ gf, uint32_t* __restrict__ state,
                             Counters* __restrict__ cnt, float step, int q_cap, uint32_t* __restrict__ next_frontier,
-                            Grid g, RowGeom rg, int fwords_smem) {
+                            Grid g, RowGeom rg, int fwords_smem, uint32_t* __restrict__ vchg, int64_t vwords,
+                            const LoopState* __restrict__ ls) {
+  uint32_t* vcur = vchg ? vchg + (int64_t)(ls->round & 1) * vwords : nullptr;
   extern __shared__ uint32_t sfr[];
   for (int i = threadIdx.x; i < fwords_smem; i += blockDim.x) sfr[i] = 0;
   __syncthreads();
@@ -431,8 +462,8 @@ __global__ void k_edit_rows(uint32_t* __restrict__ tbits, int64_t nwords, const 
       if (!((wv >> lane) & 1u)) continue;
       const int64_t v = (base + src) * 32 + lane;
       targets++;
+      const int64_t vx = v % g.nx, vy = (v / g.nx) % g.ny, vz = v / g.sz;
       if (next_frontier) {
-        const int64_t vy = (v / g.nx) % g.ny, vz = v / g.sz;
         const int64_t y0 = vy >= 2 ? vy - 2 : 0, y1 = vy + 1 < g.ny ? vy + 1 : g.ny - 1;
         const int64_t z0 = vz >= 2 ? vz - 2 : 0, z1 = vz + 1 < g.nz ? vz + 1 : g.nz - 1;
         for (int64_t zz = z0; zz <= z1; zz++)
@@ -444,6 +475,7 @@ __global__ void k_edit_rows(uint32_t* __restrict__ tbits, int64_t nwords, const 
       const uint32_t st = state[v];
       if (st >> 16) continue;  // lossless: no-op, but its cells stay in the frontier
       changed++;
+      if (vcur) atomicOr(vcur + dword_index(g, rg, vy, vz, vx >> 5), 1u << (vx & 31));
       const uint32_t q = st & 0xFFFFu;
       if ((int)q + 1 <= q_cap) {
         // g' = RN(fhat - RN((q+1) * step)): two roundings, never fused
