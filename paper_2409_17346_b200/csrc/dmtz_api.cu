@@ -96,7 +96,7 @@ Layout layout_for(const dmtz_ctx* c) {
   L.lowpos = o; o += align_up(N * 8 > (size_t)128 * 3072 * 8 ? N * 8 : (size_t)128 * 3072 * 8);
   L.lb = o; o += align_up(N * 4);
   L.state = o; o += align_up(N * 4);
-  L.tbits = o; o += align_up((N + 31) / 32 * 4 + 64);
+  L.tbits = o; o += align_up((size_t)(c->g.nz * c->g.ny * ((c->g.nx + 31) / 32)) * 4 + 64);  // row-padded
   L.counters = o; o += align_up(sizeof(Counters) * 2);
   L.edit_bc = o; o += align_up(((N + EDIT_CHUNK - 1) / EDIT_CHUNK + 2) * 8);
   const RowGeom rg = row_geom(c->g);
@@ -184,7 +184,7 @@ dmtz_status setup_phase(dmtz_ctx* c, const float* f, const float* fhat, const dm
                         float* g_out, int64_t v_report_off, int64_t* launches, cudaStream_t s) {
   const Grid& g = c->g;
   Counters* hc = c->host_cnt;
-  const int64_t nwords = (g.N + 31) / 32;
+  const int64_t nwords = (int64_t)(W.rowbit_bytes / 4);
   CK(cudaMemsetAsync(W.dc, 0, sizeof(Counters), s));
   CK(cudaMemsetAsync(&W.dc->first_nonfinite, 0xFF, 16, s));
   CK(cudaMemsetAsync(W.tbits, 0, nwords * 4, s));
@@ -226,13 +226,13 @@ inline cudaError_t units_range(const RowGeom& rg, int64_t z0, int64_t z1, uint32
 template <int D>
 dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o, WS<D>& W,
                           float* g_out, const uint32_t* units, unsigned long long* n_units, const uint32_t* dunits,
-                          unsigned long long* n_dunits, uint32_t* fbits, int fwords, int64_t own_lo, int64_t own_hi,
+                          unsigned long long* n_dunits, uint32_t* fbits, int fwords, int64_t own_z0, int64_t own_z1,
                           int64_t count_z0, int64_t count_z1, bool profile, unsigned long long max_rounds,
                           cudaGraphConditionalHandle h, int use_cond, int use_skip, int64_t* launches,
                           cudaStream_t s) {
   const Grid& g = c->g;
   const RowGeom rg = row_geom(g);
-  const int64_t nwords = (g.N + 31) / 32;
+  const int64_t nwords = (int64_t)(W.rowbit_bytes / 4);  // row-padded target bitmap
   // grids sized by the largest possible work list (small grids: few blocks, cheap launches)
   const int64_t max_items = rg.units * UY * ((rg.wpr + CG - 1) / CG);
   const int sweep_blocks = (int)(max_items / 8 + 1 < 148 * 8 ? max_items / 8 + 1 : 148 * 8);
@@ -245,8 +245,8 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
                                            rg, W.ls, W.dc);
   if (profile) CK(cudaEventRecord(c->ev[1], s));
   k_decode<D><<<sweep_blocks * 2, DECODE_THREADS, 0, s>>>(
-      f, W.cand_f, W.crit_f, W.cand_g, W.crit_g, W.ebits, W.fmark, W.tbits, dunits, n_dunits, g, rg,
-      tier_mask<D>(o->tier), W.lowpos, W.ls, own_lo, own_hi, count_z0, count_z1, W.dc);
+      f, W.cand_f, W.crit_f, W.cand_g, W.ebits, W.fmark, W.tbits, dunits, n_dunits, g, rg,
+      tier_mask<D>(o->tier), W.lowpos, W.ls, own_z0, own_z1, count_z0, count_z1, W.dc);
   if (profile) CK(cudaEventRecord(c->ev[2], s));
   k_edit_rows<D><<<clamp_blocks(nwords, 256), 256, fwords_smem * 4, s>>>(
       W.tbits, nwords, fhat, W.lb, g_out, W.state, W.dc, step, o->q_cap, fbits, g, rg, fwords_smem,
@@ -267,11 +267,11 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
 template <int D>
 dmtz_status round_phase(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o, WS<D>& W,
                         float* g_out, const uint32_t* units, unsigned long long* n_units, const uint32_t* dunits,
-                        unsigned long long* n_dunits, uint32_t* fbits, int fwords, int64_t own_lo, int64_t own_hi,
+                        unsigned long long* n_dunits, uint32_t* fbits, int fwords, int64_t own_z0, int64_t own_z1,
                         int64_t count_z0, int64_t count_z1, bool profile, unsigned long long max_rounds,
                         int use_skip, LoopState* hls, int64_t* launches, cudaStream_t s) {
-  dmtz_status st = enqueue_round<D>(c, f, fhat, o, W, g_out, units, n_units, dunits, n_dunits, fbits, fwords, own_lo,
-                                    own_hi, count_z0, count_z1, profile, max_rounds, cudaGraphConditionalHandle(), 0,
+  dmtz_status st = enqueue_round<D>(c, f, fhat, o, W, g_out, units, n_units, dunits, n_dunits, fbits, fwords, own_z0,
+                                    own_z1, count_z0, count_z1, profile, max_rounds, cudaGraphConditionalHandle(), 0,
                                     use_skip, launches, s);
   if (st) return st;
   CK(cudaMemcpyAsync(c->host_cnt, W.dc, offsetof(Counters, first_nonfinite), cudaMemcpyDeviceToHost, s));
@@ -325,7 +325,7 @@ dmtz_status build_loop_graph(dmtz_ctx* c, LoopGraph& G, const float* f, const fl
   CK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   int64_t launches = 0;
   dmtz_status st = enqueue_round<D>(c, f, fhat, o, W, g_out, W.units, &W.dc->n_units, W.units, &W.dc->n_units,
-                                    frontier_mode ? W.fbits : nullptr, (int)L.fwords, 0, c->g.N, 0, c->g.nz, false,
+                                    frontier_mode ? W.fbits : nullptr, (int)L.fwords, 0, c->g.nz, 0, c->g.nz, false,
                                     max_rounds, h, 1, 1, &launches, cs);
   cudaGraph_t captured;
   cudaError_t e = cudaStreamEndCapture(cs, &captured);
@@ -377,7 +377,7 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
       const int64_t round = (int64_t)hls->round;
       (void)round;
       status = round_phase<D>(c, f, fhat, o, W, g_out, W.units, n_units, W.units, n_units,
-                              frontier_mode ? W.fbits : nullptr, (int)L.fwords, 0, g.N, 0, g.nz, o->profile != 0,
+                              frontier_mode ? W.fbits : nullptr, (int)L.fwords, 0, g.nz, 0, g.nz, o->profile != 0,
                               max_rounds, 1, hls, &st->launches, s);
       if (status != DMTZ_OK) break;
       if (o->profile) {
@@ -590,7 +590,7 @@ dmtz_status dmtz_slab_round(dmtz_ctx* c, const float* f, const float* fhat, cons
   const int64_t plane = c->g.sz;
   k_set_round<<<1, 32, 0, s>>>(W.ls, (unsigned long long)round);
   st = round_phase<3>(c, f, fhat, o, W, g_out, W.units, &W.dc->n_units, W.units2, &W.dc->n_units2, nullptr, 0,
-                      sl->own_z0 * plane, sl->own_z1 * plane, sl->own_z0, sl->own_z1, false, ~0ull,
+                      sl->own_z0, sl->own_z1, sl->own_z0, sl->own_z1, false, ~0ull,
                       0 /* halos change outside this rank's edits: no change skipping */, c->host_ls, &launches, s);
   if (st) return st;
   Counters* hc = c->host_cnt;

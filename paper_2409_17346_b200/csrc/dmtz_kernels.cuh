@@ -223,6 +223,35 @@ __device__ __forceinline__ uint32_t decode_crit(const uint64_t (&c)[Tr<D>::NDELT
   return m & t_exist<D>(ok);
 }
 
+// crit mask, and in *dp for every type the index j (2 bits at 2t) of the facet whose
+// code points at the cell -- its down-pair partner when it has one (a gradient pairs
+// a cell with at most one facet)
+template <int D>
+__device__ __forceinline__ uint32_t decode_crit_dp(const uint64_t (&c)[Tr<D>::NDELTA], int ok, uint64_t* dp) {
+  uint32_t m = 0;
+  uint32_t dlo = 0, dhi = 0;
+#pragma unroll
+  for (int t = 0; t < Tr<D>::NT; t++) {
+    bool crit = true;
+    if (t_dim<D>(t) < Tr<D>::TOP) crit = field_of<D>(c[0], t) == (uint32_t)t_none<D>(t);
+    uint32_t jsel = 0;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      if (j < t_nfacet<D>(t)) {
+        const int dm = t_facet<D>(t, j, 0), ft = t_facet<D>(t, j, 1), sl = t_facet<D>(t, j, 2);
+        const bool hit = field_of<D>(c[dm], ft) == (uint32_t)sl;
+        crit = crit && !hit;
+        if (j > 0) jsel = hit ? (uint32_t)j : jsel;
+      }
+    }
+    m |= (crit ? 1u : 0u) << t;
+    if (t < 16) dlo |= jsel << (2 * t);
+    else dhi |= jsel << (2 * (t - 16));
+  }
+  *dp = ((uint64_t)dhi << 32) | dlo;
+  return m & t_exist<D>(ok);
+}
+
 template <int D>
 __device__ __forceinline__ void load_codes8(const typename Tr<D>::code_t* __restrict__ codes, const Grid& g,
                                             int64_t v, int ok, uint64_t (&c)[Tr<D>::NDELTA]) {

@@ -12,10 +12,11 @@
 //               (one word per 32 anchors of a row).
 //  k_decode<D>  for every anchor u of an active unit with a changed code in
 //               u + {0,1}^D (criticality is a function of those 8 codes) or
-//               with false cells last round: crit_g(u) (decoded, or memoized
-//               when no code around u changed), F(u) = crit_f(u) xor crit_g(u),
-//               and the targets of F(u) (rules R1/R2/R3a/R3b), OR-ed into the
-//               round's target bitmap with warp-aggregated atomics.
+//               with false cells last round: crit_g(u) and the down-pair facets,
+//               F(u) = crit_f(u) xor crit_g(u), and the targets of F(u) (rules
+//               R1/R2/R3a/R3b) over a per-warp shared-memory work list, OR-ed
+//               into a shared-memory window of the chunk, then into the round's
+//               (row-padded) target bitmap with one atomic per non-empty word.
 //  k_edit_rows<D> Eq. 2 edits of the marked targets and the next frontier.
 #pragma once
 #include <utility>
@@ -180,8 +181,7 @@ struct TargetTables {
   uint32_t tinfo[26];      // dim | nv << 2 | shift << 5 | none << 11 | nfacet << 15
   uint32_t vm[26];         // vertex delta masks, 3 bits each
   uint32_t fac[26][4];     // dm | ft << 3 | slot << 8 | k << 12
-  int32_t loff[26][14];    // link slot -> linear offset (|offset| <= nx*ny + nx + 1)
-  int32_t doff[8];         // delta mask -> linear offset
+  uint8_t ldel[26][14];    // link slot -> packed (dx+1) | (dy+1) << 2 | (dz+1) << 4
 };
 
 template <int D>
@@ -201,10 +201,9 @@ __device__ __forceinline__ void init_target_tables(TargetTables& T, const Grid& 
                       ((uint32_t)t_facet<D>(t, j, 2) << 8) | ((uint32_t)t_facet<D>(t, j, 3) << 12);
 #pragma unroll
       for (int q = 0; q < 14; q++)
-        T.loff[t][q] = (int32_t)(t_link<D>(t, q, 0) + t_link<D>(t, q, 1) * g.sy + t_link<D>(t, q, 2) * g.sz);
+        T.ldel[t][q] = (uint8_t)((t_link<D>(t, q, 0) + 1) | ((t_link<D>(t, q, 1) + 1) << 2) |
+                                 ((t_link<D>(t, q, 2) + 1) << 4));
     }
-#pragma unroll
-    for (int m = 0; m < 8; m++) T.doff[m] = (int32_t)mask_delta(g, m);
   }
   __syncthreads();
 }
@@ -223,49 +222,53 @@ __device__ __forceinline__ uint32_t field2(uint2 c, int shift, uint32_t none) {
   return w & none;
 }
 
+// delta mask (dx = bit 0, dy = bit 1, dz = bit 2) -> packed (dx+1) | (dy+1) << 2 | (dz+1) << 4
+__device__ __forceinline__ uint32_t mask_del(int m) { return 0x15u + (m & 1) + ((m & 2) << 1) + ((m & 4) << 2); }
+
 // Rules R1 / R2 / R3a / R3b for the false cell (anchor u, type t):
-// returns the target's offset from u.  The anchor's codes at u + {0,1}^D come
-// from the warp's shared-memory copy (cfs[dm * 32 + src], cgs[dm * 32 + src]).
-// Returns INT32_MIN on an internal inconsistency.
+// returns the target's offset from the anchor as packed (dx+1) | (dy+1) << 2 |
+// (dz+1) << 4, each component in [-1, 2].  The anchor's codes at u + {0,1}^D come
+// from the warp's shared-memory copy (cfs[dm * 32 + src]); dp = the down-pair facet
+// indices of the cells in g (decode_crit_dp).  Returns 0xFFFFFFFF on an inconsistency.
 template <int D>
-__device__ __forceinline__ int32_t target_off(const TargetTables& T, int t, bool fn, uint64_t lowpos,
-                                              const uint2* cfs, const uint2* cgs, int src) {
+__device__ __forceinline__ uint32_t target_del(const TargetTables& T, int t, bool fn, uint64_t lowpos, uint64_t dp,
+                                               const uint2* cfs, const uint2* cgs, int src) {
   const uint32_t ti = T.tinfo[t];
-  const int dim = ti & 3, shift = (ti >> 5) & 63, nfacet = (ti >> 15) & 7;
+  const int dim = ti & 3, shift = (ti >> 5) & 63;
   const uint32_t none = (ti >> 11) & 15;
   // m = the cell's f-lowest vertex (SoS), precomputed per anchor and type
   const int mp = (int)(lowpos >> (2 * t)) & 3;
-  const int32_t m_off = T.doff[(T.vm[t] >> (3 * mp)) & 7];
+  const uint32_t m_del = mask_del((T.vm[t] >> (3 * mp)) & 7);
   const bool has_cand = dim < Tr<D>::TOP;
   if (!fn) {                                        // FP: paired in f, critical in g (R1)
     const uint32_t sl = has_cand ? field2(cfs[src], shift, none) : none;
-    return sl != none ? T.loff[t][sl] : m_off;      // paired up: its cofacet's vertex; down: m
+    return sl != none ? T.ldel[t][sl] : m_del;      // paired up: its cofacet's vertex; down: m
   }
-  if (has_cand && field2(cgs[src], shift, none) != none) return m_off;   // R2
-  for (int j = 0; j < nfacet; j++) {                // paired down in g with gamma: R3a / R3b
-    const uint32_t fc = T.fac[t][j];
-    const int dm = fc & 7, ft = (fc >> 3) & 31, sl = (fc >> 8) & 15, k = (fc >> 12) & 3;
-    const uint32_t fti = T.tinfo[ft];
-    const int fsh = (fti >> 5) & 63;
-    const uint32_t fno = (fti >> 11) & 15;
-    if (field2(cgs[dm * 32 + src], fsh, fno) != (uint32_t)sl) continue;
-    if (mp != k) return m_off;                      // R3a: y = the vertex gamma omits
-    const uint32_t s2 = field2(cfs[dm * 32 + src], fsh, fno);   // R3b
-    if (s2 == fno) return INT32_MIN;
-    return T.doff[dm] + T.loff[ft][s2];
-  }
-  return INT32_MIN;
+  if (has_cand && field2(cgs[src], shift, none) != none) return m_del;   // R2
+  // paired down in g with gamma = the facet j that points at it (R3a / R3b)
+  const int j = (int)(dp >> (2 * t)) & 3;
+  const uint32_t fc = T.fac[t][j];
+  const int dm = fc & 7, ft = (fc >> 3) & 31, k = (fc >> 12) & 3;
+  if (mp != k) return m_del;                        // R3a: y = the vertex gamma omits != m
+  const uint32_t fti = T.tinfo[ft];
+  const int fsh = (fti >> 5) & 63;
+  const uint32_t fno = (fti >> 11) & 15;
+  const uint32_t s2 = field2(cfs[dm * 32 + src], fsh, fno);   // R3b: gamma's f-pair vertex
+  if (s2 == fno) return 0xFFFFFFFFu;
+  return mask_del(dm) + T.ldel[ft][s2] - 0x15u;
 }
 
 // ---------------------------------------------------------------------------
-// k_decode: classification.  crit_f is precomputed once per call; crit_g is
-// memoized per anchor and re-decoded only where a code of u + {0,1}^D changed.
+// k_decode: classification.  crit_f is precomputed once per call; anchors are
+// revisited only where a code of u + {0,1}^D changed or false cells remain.
 // ---------------------------------------------------------------------------
 constexpr int DECODE_THREADS = 128;
 struct DecodeWarpSmem {
   uint2 cf[8 * 32];
   uint2 cg[8 * 32];
   unsigned long long lowpos[32];
+  unsigned long long dp[32];
+  uint32_t tw[48];   // target window of a 32-anchor chunk: z-1..z+2 x y-1..y+2 rows x 3 words (x0-32 .. x0+63)
   uint32_t critf[32];
   uint16_t items[32 * 26];
 };
@@ -274,11 +277,11 @@ template <int D>
 __global__ void __launch_bounds__(DECODE_THREADS, 8)
 k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__ cand_f,
          const uint32_t* __restrict__ crit_f, const typename Tr<D>::code_t* __restrict__ cg,
-         uint32_t* __restrict__ crit_g, const uint32_t* __restrict__ ebits, uint32_t* __restrict__ fmark,
+         const uint32_t* __restrict__ ebits, uint32_t* __restrict__ fmark,
          uint32_t* __restrict__ tbits, const uint32_t* __restrict__ units,
          const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg, uint32_t tier_mask,
-         const unsigned long long* __restrict__ lowpos_f, const LoopState* __restrict__ ls, int64_t own_lo,
-         int64_t own_hi, int64_t count_z0, int64_t count_z1, Counters* __restrict__ cnt) {
+         const unsigned long long* __restrict__ lowpos_f, const LoopState* __restrict__ ls, int64_t own_z0,
+         int64_t own_z1, int64_t count_z0, int64_t count_z1, Counters* __restrict__ cnt) {
   const bool count_kinds = ls->round == 1;  // kinds are reported for round 1 only
   __shared__ TargetTables T;
   __shared__ DecodeWarpSmem WS[DECODE_THREADS / 32];
@@ -335,6 +338,7 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
     const int64_t u = x + y * g.sy + z * g.sz;
     const bool active = x < g.nx && (((chg | had) >> lane) & 1u);
     uint32_t diff = 0, critf = 0;
+    uint64_t dp = 0;
     uint64_t cf[Tr<D>::NDELTA], cgv[Tr<D>::NDELTA];
 #pragma unroll
     for (int dm = 0; dm < Tr<D>::NDELTA; dm++) cf[dm] = cgv[dm] = Tr<D>::ALL_NONE;
@@ -347,13 +351,7 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
         cf[dm] = (uint64_t)__ldg(cand_f + w);
         cgv[dm] = (uint64_t)__ldg(cg + w);
       }
-      uint32_t cgm;
-      if ((chg >> lane) & 1u) {
-        cgm = decode_crit<D>(cgv, ok);
-        crit_g[u] = cgm;
-      } else {
-        cgm = crit_g[u];
-      }
+      const uint32_t cgm = decode_crit_dp<D>(cgv, ok, &dp);
       critf = __ldg(crit_f + u);
       diff = (critf ^ cgm) & tier_mask;
     }
@@ -372,6 +370,8 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
     }
     const int total = __shfl_sync(0xffffffffu, pre, 31);
     pre -= nmine;
+    W.tw[lane] = 0u;
+    if (lane < 16) W.tw[32 + lane] = 0u;
     if (diff) {
 #pragma unroll
       for (int dm = 0; dm < Tr<D>::NDELTA; dm++) {
@@ -379,6 +379,7 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
         W.cg[dm * 32 + lane] = make_uint2((uint32_t)cgv[dm], (uint32_t)(cgv[dm] >> 32));
       }
       W.critf[lane] = critf;
+      W.dp[lane] = dp;
       W.lowpos[lane] = __ldg(lowpos_f + u);
       uint32_t dd = diff;
       for (int k = 0; dd; k++) {
@@ -388,36 +389,31 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
       }
     }
     __syncwarp();
-    const int64_t ubase = u - lane;
-    for (int i0 = 0; i0 < total; i0 += 32) {
-      const int i = i0 + lane;
-      bool have_t = false;
-      uint32_t word = 0, bit = 0;
-      if (i < total) {
-        const int item = W.items[i];
-        const int src = item & 31, t = item >> 5;
-        const bool fn = (W.critf[src] >> t) & 1u;
-        if (count_kinds && counted) {
-          const int dim = T.tinfo[t] & 3;
-          const int cls = (dim == Tr<D>::TOP) ? 3 : dim;
-          atomicAdd(kc + 2 * cls + (fn ? 1 : 0), 1u);
-        }
-        const int32_t off = target_off<D>(T, t, fn, W.lowpos[src], W.cf, W.cg, src);
-        if (off == INT32_MIN) {
-          nint++;
-        } else {
-          const int64_t tv = ubase + src + off;
-          word = (uint32_t)(tv >> 5);
-          bit = 1u << (tv & 31);
-          have_t = tv >= own_lo && tv < own_hi;  // slab mode: only the owned vertices
-        }
+    // targets -> the chunk's target window in shared memory (x relative to x0 - 32)
+    for (int i = lane; i < total; i += 32) {
+      const int item = W.items[i];
+      const int src = item & 31, t = item >> 5;
+      const bool fn = (W.critf[src] >> t) & 1u;
+      if (count_kinds && counted) {
+        const int dim = T.tinfo[t] & 3;
+        const int cls = (dim == Tr<D>::TOP) ? 3 : dim;
+        atomicAdd(kc + 2 * cls + (fn ? 1 : 0), 1u);
       }
-      const unsigned have = __ballot_sync(0xffffffffu, have_t);
-      if (have_t) {
-        const unsigned same = __match_any_sync(have, word);
-        const uint32_t bits = __reduce_or_sync(same, bit);
-        if (lane == __ffs(same) - 1) atomicOr(tbits + word, bits);
-      }
+      const uint32_t del = target_del<D>(T, t, fn, W.lowpos[src], W.dp[src], W.cf, W.cg, src);
+      if (del == 0xFFFFFFFFu) { nint++; continue; }
+      const int X = 32 + src + (int)(del & 3) - 1;              // 31 .. 65
+      const int row = (int)((del >> 4) & 3) * 4 + (int)((del >> 2) & 3);   // (dz+1) * 4 + (dy+1)
+      atomicOr(&W.tw[row * 3 + (X >> 5)], 1u << (X & 31));
+    }
+    __syncwarp();
+    // flush the window: one aligned atomicOr per non-empty word (row-padded target bitmap)
+    for (int i = lane; i < 48; i += 32) {
+      const uint32_t wv = W.tw[i];
+      if (!wv) continue;
+      const int row = i / 3, wd = i - (i / 3) * 3;
+      const int64_t ty = y + (row & 3) - 1, tz = z + (row >> 2) - 1, tc = c + wd - 1;
+      if (tz < own_z0 || tz >= own_z1) continue;   // slab mode: only the owned vertices
+      atomicOr(tbits + dword_index(g, rg, ty, tz, tc), wv);
     }
     __syncwarp();
     }
@@ -460,9 +456,12 @@ __global__ void k_edit_rows(uint32_t* __restrict__ tbits, int64_t nwords, const 
       nz &= nz - 1;
       const uint32_t wv = __shfl_sync(0xffffffffu, word, src);
       if (!((wv >> lane) & 1u)) continue;
-      const int64_t v = (base + src) * 32 + lane;
+      // row-padded target bitmap: word = (z * ny + y) * wpr + x / 32
+      const int64_t wrow = (base + src) / rg.wpr;
+      const int64_t vx = ((base + src) - wrow * rg.wpr) * 32 + lane;
+      const int64_t vy = wrow % g.ny, vz = wrow / g.ny;
+      const int64_t v = vx + vy * g.sy + vz * g.sz;
       targets++;
-      const int64_t vx = v % g.nx, vy = (v / g.nx) % g.ny, vz = v / g.sz;
       if (next_frontier) {
         const int64_t y0 = vy >= 2 ? vy - 2 : 0, y1 = vy + 1 < g.ny ? vy + 1 : g.ny - 1;
         const int64_t z0 = vz >= 2 ? vz - 2 : 0, z1 = vz + 1 < g.nz ? vz + 1 : g.nz - 1;
