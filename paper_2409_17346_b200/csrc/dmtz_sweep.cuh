@@ -274,7 +274,7 @@ struct DecodeWarpSmem {
 };
 
 template <int D>
-__global__ void __launch_bounds__(DECODE_THREADS, 8)
+__global__ void __launch_bounds__(DECODE_THREADS, 6)
 k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__ cand_f,
          const uint32_t* __restrict__ crit_f, const typename Tr<D>::code_t* __restrict__ cg,
          const uint32_t* __restrict__ ebits, uint32_t* __restrict__ fmark,
