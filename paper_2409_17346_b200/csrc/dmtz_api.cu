@@ -587,7 +587,6 @@ dmtz_status dmtz_slab_round(dmtz_ctx* c, const float* f, const float* fhat, cons
   cudaStream_t s = (cudaStream_t)stream;
   WS<3> W((char*)workspace, L, c->g);
   int64_t launches = 0;
-  const int64_t plane = c->g.sz;
   k_set_round<<<1, 32, 0, s>>>(W.ls, (unsigned long long)round);
   st = round_phase<3>(c, f, fhat, o, W, g_out, W.units, &W.dc->n_units, W.units2, &W.dc->n_units2, nullptr, 0,
                       sl->own_z0, sl->own_z1, sl->own_z0, sl->own_z1, false, ~0ull,

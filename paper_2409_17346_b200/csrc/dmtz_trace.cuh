@@ -70,6 +70,14 @@ __device__ __forceinline__ void coords_of(const Grid& g, int64_t v, int64_t& x, 
 }
 
 template <int D>
+__device__ __forceinline__ bool link_in_grid_xyz(const Grid& g, int64_t x, int64_t y, int64_t z, int t, int s) {
+  x += t_link<D>(t, s, 0);
+  y += t_link<D>(t, s, 1);
+  z += t_link<D>(t, s, 2);
+  return x >= 0 && y >= 0 && z >= 0 && x < g.nx && y < g.ny && z < g.nz;
+}
+
+template <int D>
 __device__ __forceinline__ bool link_in_grid(const Grid& g, int64_t a, int t, int s) {
   int64_t x, y, z;
   coords_of(g, a, x, y, z);
@@ -98,7 +106,7 @@ __device__ __forceinline__ int paired_facet(const void* codes, const Grid& g, in
 
 // ----------------------------------------------------------------------------- counting / emission
 template <int D>
-__device__ __forceinline__ int branch_count(const Grid& g, int kind, uint32_t cm, int64_t a) {
+__device__ __forceinline__ int branch_count(const Grid& g, int kind, uint32_t cm, int64_t x, int64_t y, int64_t z) {
   const int top = Tr<D>::TOP;
   if (kind == 1) {  // DESC: two branches per critical edge
     const uint32_t em = ((1u << t_first_of_dim<D>(2)) - 1u) & ~1u;
@@ -108,7 +116,7 @@ __device__ __forceinline__ int branch_count(const Grid& g, int kind, uint32_t cm
     int n = 0;
     for (int t = t_first_of_dim<D>(top - 1); t < t_first_of_dim<D>(top); t++) {
       if (!((cm >> t) & 1u)) continue;
-      for (int s = 0; s < t_nlink<D>(t); s++) n += link_in_grid<D>(g, a, t, s) ? 1 : 0;
+      for (int s = 0; s < t_nlink<D>(t); s++) n += link_in_grid_xyz<D>(g, x, y, z, t, s) ? 1 : 0;
     }
     return n;
   }
@@ -122,7 +130,7 @@ template <int D>
 __global__ void k_branch_count(const uint32_t* __restrict__ crit, long long* __restrict__ cnt_out, Grid g, int kind) {
   DMTZ_FOR_ANCHORS(g, 0, g.nz) {
     const int64_t a = x + y * g.sy + z * g.sz;
-    cnt_out[a] = branch_count<D>(g, kind, crit[a], a);
+    cnt_out[a] = branch_count<D>(g, kind, crit[a], x, y, z);
   }
 }
 
@@ -153,11 +161,23 @@ __global__ void k_scan_local(long long* __restrict__ a, int64_t n, unsigned long
 }
 
 __global__ void k_scan_top(unsigned long long* __restrict__ bsum, int64_t nb, unsigned long long* __restrict__ total) {
-  if (threadIdx.x == 0) {
-    unsigned long long acc = 0;
-    for (int64_t i = 0; i < nb; i++) { const unsigned long long v = bsum[i]; bsum[i] = acc; acc += v; }
-    *total = acc;
+  // exclusive scan of nb block sums by one block of 1024 threads (contiguous ranges)
+  __shared__ unsigned long long part[1024];
+  const int64_t per = (nb + 1023) / 1024;
+  const int64_t lo = threadIdx.x * per, hi = lo + per < nb ? lo + per : nb;
+  unsigned long long acc = 0;
+  for (int64_t i = lo; i < hi; i++) acc += bsum[i];
+  part[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const unsigned long long v = threadIdx.x >= (unsigned)o ? part[threadIdx.x - o] : 0ull;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
   }
+  unsigned long long run = part[threadIdx.x] - acc;
+  for (int64_t i = lo; i < hi; i++) { const unsigned long long v = bsum[i]; bsum[i] = run; run += v; }
+  if (threadIdx.x == 1023) *total = part[1023];
 }
 
 __global__ void k_scan_add(long long* __restrict__ a, int64_t n, const unsigned long long* __restrict__ bsum) {
@@ -183,7 +203,7 @@ __global__ void k_branch_emit(const uint32_t* __restrict__ crit, const long long
       for (int t = t_first_of_dim<D>(top - 1); t < t_first_of_dim<D>(top); t++) {
         if (!((cm >> t) & 1u)) continue;
         for (int s = 0; s < t_nlink<D>(t); s++) {
-          if (!link_in_grid<D>(g, a, t, s)) continue;
+          if (!link_in_grid_xyz<D>(g, x, y, z, t, s)) continue;
           origin[b] = cell_id<D>(a, t); kout[b] = 2; jout[b] = (uint64_t)s; b++;
         }
       }
@@ -534,7 +554,7 @@ inline cudaError_t scan_i64(long long* a, int64_t n, unsigned long long* bsum, u
   const int64_t nb = (n + SCAN_CHUNK - 1) / SCAN_CHUNK;
   if (n > 0) {
     k_scan_local<<<(unsigned)nb, 1024, 0, s>>>(a, n, bsum);
-    k_scan_top<<<1, 32, 0, s>>>(bsum, nb, total);
+    k_scan_top<<<1, 1024, 0, s>>>(bsum, nb, total);
     k_scan_add<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, n, bsum);
   } else {
     TCK(cudaMemsetAsync(total, 0, 8, s));
@@ -594,12 +614,12 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   unsigned long long* sc = A.bfs;
   const int64_t words = (int64_t)(A.bfs_bytes / 8);
   // a connector visits at most the 12 N triangles; small grids get small slots
-  const int64_t slot_q = 12 * g.N + 16 < 256 ? 12 * g.N + 16 : 256;
+  const int64_t slot_q = 12 * g.N + 16 < 64 ? 12 * g.N + 16 : 64;
   int64_t slot_h = 1;
   while (slot_h < 2 * slot_q) slot_h *= 2;
   const int threads = 128;
   int64_t nslots = words / (slot_q + slot_h);
-  if (nslots > 65536) nslots = 65536;
+  if (nslots > 148 * 2048) nslots = 148 * 2048;  // one slot per resident thread
   nslots = nslots / threads * threads;
   const int64_t conn_base = nbk[0] + nbk[1];
   const int64_t ovf_words = (nbk[2] + 31) / 32;
