@@ -260,16 +260,17 @@ def main():
             need = sizes["n_branches"] * 33 + sizes["n_cells"] * 8
             free = torch.cuda.mem_get_info()[0]
             if need < 0.8 * free:
+                bufs = ctx.trace_buffers(sizes["n_branches"], sizes["n_cells"], dev)
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                tr = ctx.trace_separatrices(codes, cap_branches=sizes["n_branches"], cap_cells=sizes["n_cells"])
+                tr = ctx.trace_separatrices(codes, out=bufs)
                 e1.record(stream)
                 torch.cuda.synchronize()
                 kinds = torch.bincount(tr["kind"].long(), minlength=5).tolist()
                 trace = {"trace_ms": e0.elapsed_time(e1), "n_branches": sizes["n_branches"],
                          "n_cells": sizes["n_cells"], "desc": kinds[1], "asc": kinds[2], "conn": kinds[4]}
-                del tr
+                del tr, bufs
             else:
                 trace = {"skipped": f"needs {need / 1e9:.1f} GB of outputs", **sizes}
         except Exception as e:  # noqa: BLE001

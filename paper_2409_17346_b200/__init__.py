@@ -237,18 +237,25 @@ class Context:
             _check(st)
         return {"n_branches": n_b, "n_cells": nc.value}
 
+    @staticmethod
+    def trace_buffers(cap_branches: int, cap_cells: int, device):
+        """Output buffers for trace_separatrices(out=...)."""
+        return dict(offsets=torch.empty(cap_branches + 1, dtype=torch.int64, device=device),
+                    cells=torch.empty(max(cap_cells, 1), dtype=torch.int64, device=device),
+                    origin=torch.empty(max(cap_branches, 1), dtype=torch.int64, device=device),
+                    terminal=torch.empty(max(cap_branches, 1), dtype=torch.int64, device=device),
+                    kind=torch.empty(max(cap_branches, 1), dtype=torch.uint8, device=device))
+
     def trace_separatrices(self, codes: torch.Tensor, kinds: int = KIND_DESC | KIND_ASC | KIND_CONN,
-                           cap_branches: int | None = None, cap_cells: int | None = None, stream=None):
-        """V-path traces -> dict of CUDA tensors (CSR)."""
+                           cap_branches: int | None = None, cap_cells: int | None = None, stream=None,
+                           out: dict | None = None):
+        """V-path traces -> dict of CUDA tensors (CSR).  ``out`` (from
+        trace_buffers) avoids allocating the outputs."""
         _need_cuda(codes)
         dev = codes.device
 
         def run(cb, cc):
-            bufs = dict(offsets=torch.empty(cb + 1, dtype=torch.int64, device=dev),
-                        cells=torch.empty(max(cc, 1), dtype=torch.int64, device=dev),
-                        origin=torch.empty(max(cb, 1), dtype=torch.int64, device=dev),
-                        terminal=torch.empty(max(cb, 1), dtype=torch.int64, device=dev),
-                        kind=torch.empty(max(cb, 1), dtype=torch.uint8, device=dev))
+            bufs = out if out is not None else self.trace_buffers(cb, cc, dev)
             seps = _Seps(*(ctypes.c_void_p(bufs[k].data_ptr()) for k in ("offsets", "cells", "origin", "terminal", "kind")))
             nb, nc = ctypes.c_int64(), ctypes.c_int64()
             st = _lib.dmtz_trace_separatrices(self._h, ctypes.c_void_p(codes.data_ptr()), kinds,
@@ -257,11 +264,14 @@ class Context:
                                               _stream_ptr(stream))
             return st, nb.value, nc.value, bufs
 
-        cb = cap_branches if cap_branches is not None else 1 << 16
-        cc = cap_cells if cap_cells is not None else 1 << 20
+        if out is not None:
+            cb, cc = out["origin"].shape[0], out["cells"].shape[0]
+        else:
+            cb = cap_branches if cap_branches is not None else 1 << 16
+            cc = cap_cells if cap_cells is not None else 1 << 20
         st, nb, nc, bufs = run(cb, cc)
         tries = 0
-        while st == E_CAPACITY and cap_branches is None and cap_cells is None and tries < 2:
+        while st == E_CAPACITY and cap_branches is None and cap_cells is None and out is None and tries < 2:
             # the branch count is known first; the cell count once the branches fit
             cb, cc = max(nb, cb), max(nc, cc)
             st, nb, nc, bufs = run(cb, cc)

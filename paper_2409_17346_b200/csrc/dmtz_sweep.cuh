@@ -116,7 +116,8 @@ __device__ __forceinline__ uint64_t cand_of(const float (&s)[27]) {
 template <int D>
 __global__ void __launch_bounds__(256)
 k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg, uint32_t* __restrict__ ebits,
-         uint32_t* __restrict__ vchg, int64_t vwords, int use_skip, const uint32_t* __restrict__ units,
+         uint32_t* __restrict__ vchg, int64_t vwords, uint32_t* __restrict__ uchg, int64_t uwords, int use_skip,
+         const uint32_t* __restrict__ units,
          const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg, const LoopState* __restrict__ ls,
          Counters* __restrict__ cnt) {
   const int lane = threadIdx.x & 31;
@@ -128,12 +129,32 @@ k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg
   const uint32_t* vprev = vchg + (int64_t)((round - 1) & 1) * vwords;
   uint32_t* vcur = vchg + (int64_t)(round & 1) * vwords;
   const bool skip = use_skip && !first_round;
+  // units with a changed vertex in the previous round / this round's (cleared here)
+  const uint32_t* uprev = uchg + (int64_t)((round - 1) & 1) * uwords;
+  uint32_t* ucur = uchg + (int64_t)(round & 1) * uwords;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < uwords; i += (int64_t)gridDim.x * blockDim.x)
+    ucur[i] = 0u;
   unsigned long long swept = 0, recomputed = 0;
   WORK_LOOP_BEGIN
     // need(u): a vertex of u's 3x3x3 box changed -> the code may change; else it provably
     // did not (a code is a function of that box) and the memoized one stays.
     uint32_t need = 0xffffffffu;
+    bool unit_changed = true;
     if (skip) {
+      // coarse test first: a changed vertex in the units holding rows y-1..y+1 of planes z-1..z+1
+      uint32_t uc = 0;
+      if (lane < 9) {
+        const int64_t yy = y + (lane % 3) - 1, zz = D == 3 ? z + (lane / 3) - 1 : z;
+        if (yy >= 0 && yy < g.ny && zz >= 0 && zz < g.nz && (D == 3 || lane / 3 == 1)) {
+          const int64_t un = zz * rg.ub + yy / UY;
+          uc = (__ldg(uprev + (un >> 5)) >> (un & 31)) & 1u;
+        }
+      }
+      unit_changed = __any_sync(0xffffffffu, uc != 0);
+    }
+    if (skip && !unit_changed) {
+      need = 0u;
+    } else if (skip) {
       uint32_t contrib = 0;
       if (lane < 27) {
         const int dx = lane / 9 - 1, r9 = lane % 9;
@@ -436,8 +457,9 @@ __global__ void k_edit_rows(uint32_t* __restrict__ tbits, int64_t nwords, const 
                             const float* __restrict__ lb, float* __restrict__ gf, uint32_t* __restrict__ state,
                             Counters* __restrict__ cnt, float step, int q_cap, uint32_t* __restrict__ next_frontier,
                             Grid g, RowGeom rg, int fwords_smem, uint32_t* __restrict__ vchg, int64_t vwords,
-                            const LoopState* __restrict__ ls) {
+                            uint32_t* __restrict__ uchg, int64_t uwords, const LoopState* __restrict__ ls) {
   uint32_t* vcur = vchg ? vchg + (int64_t)(ls->round & 1) * vwords : nullptr;
+  uint32_t* ucur = vchg ? uchg + (int64_t)(ls->round & 1) * uwords : nullptr;
   extern __shared__ uint32_t sfr[];
   for (int i = threadIdx.x; i < fwords_smem; i += blockDim.x) sfr[i] = 0;
   __syncthreads();
@@ -474,7 +496,11 @@ __global__ void k_edit_rows(uint32_t* __restrict__ tbits, int64_t nwords, const 
       const uint32_t st = state[v];
       if (st >> 16) continue;  // lossless: no-op, but its cells stay in the frontier
       changed++;
-      if (vcur) atomicOr(vcur + dword_index(g, rg, vy, vz, vx >> 5), 1u << (vx & 31));
+      if (vcur) {
+        atomicOr(vcur + dword_index(g, rg, vy, vz, vx >> 5), 1u << (vx & 31));
+        const int64_t un = vz * rg.ub + vy / UY;
+        atomicOr(ucur + (un >> 5), 1u << (un & 31));
+      }
       const uint32_t q = st & 0xFFFFu;
       if ((int)q + 1 <= q_cap) {
         // g' = RN(fhat - RN((q+1) * step)): two roundings, never fused
