@@ -20,9 +20,6 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdmtz.so")
 
-if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2409_17346_b200.build` "
-                      "(or __graft_entry__.build()); there is no CPU fallback")
 
 OK, E_ARG, E_DIMS, E_NONFINITE, E_BOUND, E_CAPACITY, E_ITER_CAP, E_STUCK, E_CUDA, E_NCCL, E_OOM, \
     E_INTERNAL = range(12)
@@ -63,6 +60,9 @@ class _Seps(ctypes.Structure):
 
 
 def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python paper_2409_17346_b200/build.py` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
     L = ctypes.CDLL(LIB_PATH)
     P, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
     L.dmtz_ctx_create.argtypes = [ctypes.POINTER(P), ctypes.POINTER(_Dims), i32, i32, P, i32]
@@ -89,14 +89,28 @@ def _load():
     return L
 
 
-_lib = _load()
+class _LazyLib:
+    """libdmtz.so, loaded on first use (so that the package can be imported to build it);
+    every call raises if the library is missing -- there is no CPU fallback."""
+
+    _L = None
+
+    def __getattr__(self, name):
+        if _LazyLib._L is None:
+            _LazyLib._L = _load()
+        return getattr(_LazyLib._L, name)
+
+
+_lib = _LazyLib()
 EXPORTED = ("dmtz_ctx_create", "dmtz_ctx_destroy", "dmtz_workspace_bytes", "dmtz_compute_gradient",
             "dmtz_critical_mask", "dmtz_correct", "dmtz_trace_separatrices", "dmtz_status_string",
             "dmtz_last_error", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end")
 
 
 def lib():
-    return _lib
+    if _LazyLib._L is None:
+        _LazyLib._L = _load()
+    return _LazyLib._L
 
 
 def _check(st):

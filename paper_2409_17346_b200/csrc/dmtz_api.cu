@@ -77,8 +77,8 @@ inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 // Workspace layout (offsets from the base, each 256-B aligned)
 struct Layout {
-  size_t cand_f, cand_g, crit_f, crit_g, lowpos, lb, state, tbits, counters, edit_bc, ebits, fmark, vchg, uchg,
-      units, units2, frontier, trace, total;
+  size_t cand_f, cand_g, crit_f, crit_g, lowpos, lb, state, tbits, counters, edit_bc, ebits, fmark, needw, vchg,
+      uchg, units, units2, frontier, trace, total;
   int64_t fwords;  // frontier bitmap words (one bit per row-block unit)
 };
 
@@ -103,6 +103,7 @@ Layout layout_for(const dmtz_ctx* c) {
   L.fwords = (rg.units + 31) / 32;
   L.ebits = o; o += align_up((size_t)(c->g.nz * c->g.ny * rg.wpr) * 4 + 64);
   L.fmark = o; o += align_up((size_t)(c->g.nz * c->g.ny * rg.wpr) * 4 + 64);
+  L.needw = o; o += align_up((size_t)(c->g.nz * c->g.ny * rg.wpr) * 4 + 64);
   L.vchg = o; o += align_up(2 * (size_t)(c->g.nz * c->g.ny * rg.wpr) * 4 + 64);
   L.uchg = o; o += align_up(2 * (size_t)((rg.units + 31) / 32) * 4 + 64);
   L.units = o; o += align_up((size_t)rg.units * 4);
@@ -141,7 +142,7 @@ struct WS {
   using code_t = typename Tr<D>::code_t;
   code_t* cand_f;
   code_t* cand_g;            // codes of g, memoized across rounds
-  uint32_t *crit_f, *crit_g, *state, *tbits, *ebits, *fmark, *vchg, *uchg, *units, *units2, *fbits;
+  uint32_t *crit_f, *crit_g, *state, *tbits, *ebits, *fmark, *needw, *vchg, *uchg, *units, *units2, *fbits;
   int64_t vwords, uwords;
   unsigned long long* lowpos;
   float* lb;
@@ -163,6 +164,7 @@ struct WS {
     bc = (unsigned long long*)(ws + L.edit_bc);
     ebits = (uint32_t*)(ws + L.ebits);
     fmark = (uint32_t*)(ws + L.fmark);
+    needw = (uint32_t*)(ws + L.needw);
     vchg = (uint32_t*)(ws + L.vchg);
     uchg = (uint32_t*)(ws + L.uchg);
     units = (uint32_t*)(ws + L.units);
@@ -245,8 +247,12 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
   if (!use_cond) CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));  // else: k_loop_check
   if (fbits) CK(cudaMemsetAsync(W.ebits, 0, W.rowbit_bytes, s));  // rewritten for every active unit
   if (profile) CK(cudaEventRecord(c->ev[0], s));
-  k_screen<D><<<sweep_blocks, 256, 0, s>>>(g_out, W.cand_g, W.ebits, W.vchg, W.vwords, W.uchg, W.uwords, use_skip,
-                                           units, n_units, g, rg, W.ls, W.dc);
+  if (use_skip) {
+    k_need<D><<<sweep_blocks, 256, 0, s>>>(W.needw, W.vchg, W.vwords, W.uchg, W.uwords, units, n_units, g, rg, W.ls);
+    *launches += 1;
+  }
+  k_screen<D><<<sweep_blocks, 256, 0, s>>>(g_out, W.cand_g, W.ebits, W.needw, use_skip, units, n_units, g, rg, W.ls,
+                                           W.dc);
   if (profile) CK(cudaEventRecord(c->ev[1], s));
   k_decode<D><<<sweep_blocks * 2, DECODE_THREADS, 0, s>>>(
       f, W.cand_f, W.crit_f, W.cand_g, W.ebits, W.fmark, W.tbits, dunits, n_dunits, g, rg,
