@@ -85,8 +85,9 @@ typedef struct {
                           "q < q_max" is q_cap = q_max (reading A6) */
   int32_t tier;        /* 1: extrema only (dims 0 and top), 2: all critical cells */
   int64_t max_rounds;  /* 0 = N * (q_cap + 1), the bound of the progress argument */
-  int32_t full_sweeps; /* 1: every round re-evaluates every anchor; 0: only the dirty frontier
-                          (bit-identical results) */
+  int32_t full_sweeps; /* 1: reference mode -- every round recomputes the code of every anchor and
+                          classifies every anchor; 0 (default): only the dirty frontier, and within
+                          it only codes whose 3x3x3 box changed (exact, bit-identical) */
   int32_t profile;     /* 1: time each round's sweep with CUDA events on `stream` (stats.sweep_ms) */
 } dmtz_correct_opts;
 

@@ -77,8 +77,8 @@ inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 // Workspace layout (offsets from the base, each 256-B aligned)
 struct Layout {
-  size_t cand_f, cand_g, crit_f, crit_g, lowpos, lb, state, tbits, counters, edit_bc, ebits, fmark, needw, vchg,
-      uchg, units, units2, frontier, trace, total;
+  size_t cand_f, cand_g, crit_f, crit_g, lowpos, lb, state, tbits, counters, edit_bc, ebits, fmark, vchg, units,
+      units2, frontier, trace, total;
   int64_t fwords;  // frontier bitmap words (one bit per row-block unit)
 };
 
@@ -103,9 +103,7 @@ Layout layout_for(const dmtz_ctx* c) {
   L.fwords = (rg.units + 31) / 32;
   L.ebits = o; o += align_up((size_t)(c->g.nz * c->g.ny * rg.wpr) * 4 + 64);
   L.fmark = o; o += align_up((size_t)(c->g.nz * c->g.ny * rg.wpr) * 4 + 64);
-  L.needw = o; o += align_up((size_t)(c->g.nz * c->g.ny * rg.wpr) * 4 + 64);
   L.vchg = o; o += align_up(2 * (size_t)(c->g.nz * c->g.ny * rg.wpr) * 4 + 64);
-  L.uchg = o; o += align_up(2 * (size_t)((rg.units + 31) / 32) * 4 + 64);
   L.units = o; o += align_up((size_t)rg.units * 4);
   L.units2 = o; o += align_up((size_t)rg.units * 4);
   L.frontier = o; o += align_up(L.fwords * 4 + 64);
@@ -142,8 +140,8 @@ struct WS {
   using code_t = typename Tr<D>::code_t;
   code_t* cand_f;
   code_t* cand_g;            // codes of g, memoized across rounds
-  uint32_t *crit_f, *crit_g, *state, *tbits, *ebits, *fmark, *needw, *vchg, *uchg, *units, *units2, *fbits;
-  int64_t vwords, uwords;
+  uint32_t *crit_f, *crit_g, *state, *tbits, *ebits, *fmark, *vchg, *units, *units2, *fbits;
+  int64_t vwords;
   unsigned long long* lowpos;
   float* lb;
   Counters* dc;
@@ -164,16 +162,13 @@ struct WS {
     bc = (unsigned long long*)(ws + L.edit_bc);
     ebits = (uint32_t*)(ws + L.ebits);
     fmark = (uint32_t*)(ws + L.fmark);
-    needw = (uint32_t*)(ws + L.needw);
     vchg = (uint32_t*)(ws + L.vchg);
-    uchg = (uint32_t*)(ws + L.uchg);
     units = (uint32_t*)(ws + L.units);
     units2 = (uint32_t*)(ws + L.units2);
     fbits = (uint32_t*)(ws + L.frontier);
     const RowGeom rg = row_geom(g);
     rowbit_bytes = (size_t)(g.nz * g.ny * rg.wpr) * 4;
     vwords = g.nz * g.ny * rg.wpr;
-    uwords = (rg.units + 31) / 32;
   }
 };
 
@@ -195,7 +190,6 @@ dmtz_status setup_phase(dmtz_ctx* c, const float* f, const float* fhat, const dm
   CK(cudaMemsetAsync(W.tbits, 0, nwords * 4, s));
   CK(cudaMemsetAsync(W.fmark, 0, W.rowbit_bytes, s));
   CK(cudaMemsetAsync(W.vchg, 0, 2 * W.rowbit_bytes, s));
-  CK(cudaMemsetAsync(W.uchg, 0, 2 * (size_t)W.uwords * 4, s));
   k_setup<<<clamp_blocks(g.N, 256), 256, 0, s>>>(f, fhat, o->xi, g.N, W.lb, g_out, W.state, W.dc);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(hc, W.dc, sizeof(Counters), cudaMemcpyDeviceToHost, s));
@@ -247,12 +241,8 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
   if (!use_cond) CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));  // else: k_loop_check
   if (fbits) CK(cudaMemsetAsync(W.ebits, 0, W.rowbit_bytes, s));  // rewritten for every active unit
   if (profile) CK(cudaEventRecord(c->ev[0], s));
-  if (use_skip) {
-    k_need<D><<<sweep_blocks, 256, 0, s>>>(W.needw, W.vchg, W.vwords, W.uchg, W.uwords, units, n_units, g, rg, W.ls);
-    *launches += 1;
-  }
-  k_screen<D><<<sweep_blocks, 256, 0, s>>>(g_out, W.cand_g, W.ebits, W.needw, use_skip, units, n_units, g, rg, W.ls,
-                                           W.dc);
+  k_screen<D><<<sweep_blocks, 256, 0, s>>>(g_out, W.cand_g, W.ebits, W.vchg, W.vwords, use_skip, units, n_units, g,
+                                           rg, W.ls, W.dc);
   if (profile) CK(cudaEventRecord(c->ev[1], s));
   k_decode<D><<<sweep_blocks * 2, DECODE_THREADS, 0, s>>>(
       f, W.cand_f, W.crit_f, W.cand_g, W.ebits, W.fmark, W.tbits, dunits, n_dunits, g, rg,
@@ -260,7 +250,7 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
   if (profile) CK(cudaEventRecord(c->ev[2], s));
   k_edit_rows<D><<<clamp_blocks(nwords, 256), 256, fwords_smem * 4, s>>>(
       W.tbits, nwords, fhat, W.lb, g_out, W.state, W.dc, step, o->q_cap, fbits, g, rg, fwords_smem,
-      use_skip ? W.vchg : nullptr, W.vwords, W.uchg, W.uwords, W.ls);
+      use_skip ? W.vchg : nullptr, W.vwords, W.ls);
   k_loop_check<<<1, 32, 0, s>>>(W.dc, W.ls, max_rounds, h, use_cond, fbits ? n_units : nullptr);
   *launches += 4;
   if (fbits) {
@@ -336,7 +326,7 @@ dmtz_status build_loop_graph(dmtz_ctx* c, LoopGraph& G, const float* f, const fl
   int64_t launches = 0;
   dmtz_status st = enqueue_round<D>(c, f, fhat, o, W, g_out, W.units, &W.dc->n_units, W.units, &W.dc->n_units,
                                     frontier_mode ? W.fbits : nullptr, (int)L.fwords, 0, c->g.nz, 0, c->g.nz, false,
-                                    max_rounds, h, 1, 1, &launches, cs);
+                                    max_rounds, h, 1, frontier_mode ? 1 : 0, &launches, cs);
   cudaGraph_t captured;
   cudaError_t e = cudaStreamEndCapture(cs, &captured);
   if (st) return st;
@@ -388,7 +378,7 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
       (void)round;
       status = round_phase<D>(c, f, fhat, o, W, g_out, W.units, n_units, W.units, n_units,
                               frontier_mode ? W.fbits : nullptr, (int)L.fwords, 0, g.nz, 0, g.nz, o->profile != 0,
-                              max_rounds, 1, hls, &st->launches, s);
+                              max_rounds, frontier_mode ? 1 : 0, hls, &st->launches, s);
       if (status != DMTZ_OK) break;
       if (o->profile) {
         float ms0 = 0.f, ms1 = 0.f;

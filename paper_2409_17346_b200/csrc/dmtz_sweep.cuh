@@ -113,73 +113,42 @@ __device__ __forceinline__ uint64_t cand_of(const float (&s)[27]) {
 // ---------------------------------------------------------------------------
 // k_screen: codes of g; e(u) = code changed.  One warp per 32-anchor row chunk.
 // ---------------------------------------------------------------------------
-// k_need: which anchors of each active row chunk may have a new code -- those with
-// a changed vertex (previous round's edits) in their 3x3x3 box; a code is a
-// function of that box, so every other code provably stays.  One word per chunk.
-// Also clears this round's change bitmaps (written by the edit kernel).
 template <int D>
 __global__ void __launch_bounds__(256)
-k_need(uint32_t* __restrict__ needw, uint32_t* __restrict__ vchg, int64_t vwords, uint32_t* __restrict__ uchg,
-       int64_t uwords, const uint32_t* __restrict__ units, const unsigned long long* __restrict__ n_units_p, Grid g,
-       RowGeom rg, const LoopState* __restrict__ ls) {
+k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg, uint32_t* __restrict__ ebits,
+         uint32_t* __restrict__ vchg, int64_t vwords, int use_skip, const uint32_t* __restrict__ units,
+         const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg, const LoopState* __restrict__ ls,
+         Counters* __restrict__ cnt) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const unsigned long long round = ls->round;
+  const bool first_round = round == 1;
+  // vertices whose value changed in the previous round (its edits) / this round's (cleared here)
   const uint32_t* vprev = vchg + (int64_t)((round - 1) & 1) * vwords;
   uint32_t* vcur = vchg + (int64_t)(round & 1) * vwords;
-  const uint32_t* uprev = uchg + (int64_t)((round - 1) & 1) * uwords;
-  uint32_t* ucur = uchg + (int64_t)(round & 1) * uwords;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < uwords; i += (int64_t)gridDim.x * blockDim.x)
-    ucur[i] = 0u;
+  const bool skip = use_skip && !first_round;
+  unsigned long long swept = 0, recomputed = 0;
   WORK_LOOP_BEGIN
-    // coarse test: a changed vertex in the units holding rows y-1..y+1 of planes z-1..z+1
-    uint32_t uc = 0;
-    if (lane < 9) {
-      const int64_t yy = y + (lane % 3) - 1, zz = D == 3 ? z + (lane / 3) - 1 : z;
-      if (yy >= 0 && yy < g.ny && zz >= 0 && zz < g.nz && (D == 3 || lane / 3 == 1)) {
-        const int64_t un = zz * rg.ub + yy / UY;
-        uc = (__ldg(uprev + (un >> 5)) >> (un & 31)) & 1u;
-      }
-    }
-    uint32_t need = 0;
-    if (__any_sync(0xffffffffu, uc != 0)) {
+    // need(u): a vertex of u's 3x3x3 box changed -> the code may change; else it provably
+    // did not (a code is a function of that box) and the memoized one stays.
+    uint32_t need = 0xffffffffu;
+    if (skip) {
       uint32_t contrib = 0;
       if (lane < 27) {
         const int dx = lane / 9 - 1, r9 = lane % 9;
         const int64_t yy = y + (r9 % 3) - 1, zz = D == 3 ? z + (r9 / 3) - 1 : z;
         const int64_t cc = c + dx;
-        if (yy >= 0 && yy < g.ny && zz >= 0 && zz < g.nz && cc >= 0 && cc < rg.wpr && (D == 3 || r9 / 3 == 1)) {
+        const bool ok_row = yy >= 0 && yy < g.ny && zz >= 0 && zz < g.nz && cc >= 0 && cc < rg.wpr &&
+                            (D == 3 || r9 / 3 == 1);
+        if (ok_row) {
           const uint32_t w = __ldg(vprev + dword_index(g, rg, yy, zz, cc));
           contrib = dx < 0 ? (w >> 31) : dx > 0 ? (w << 31) : (w | (w << 1) | (w >> 1));
         }
       }
       need = __reduce_or_sync(0xffffffffu, contrib);
     }
-    if (lane == 0) {
-      const int64_t wi = dword_index(g, rg, y, z, c);
-      needw[wi] = need;
-      vcur[wi] = 0u;
-    }
-  WORK_LOOP_END
-}
-
-// k_screen: codes of g where needed; e(u) = code changed.  One warp per 32-anchor row chunk.
-template <int D>
-__global__ void __launch_bounds__(256)
-k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg, uint32_t* __restrict__ ebits,
-         const uint32_t* __restrict__ needw, int use_skip, const uint32_t* __restrict__ units,
-         const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg, const LoopState* __restrict__ ls,
-         Counters* __restrict__ cnt) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const bool first_round = ls->round == 1;
-  const bool skip = use_skip && !first_round;
-  unsigned long long swept = 0, recomputed = 0;
-  WORK_LOOP_BEGIN
-    const int64_t wi = dword_index(g, rg, y, z, c);
-    const uint32_t need = skip ? __ldg(needw + wi) : 0xffffffffu;
+    if (lane == 0) vcur[dword_index(g, rg, y, z, c)] = 0u;
     const int64_t x = c * 32 + lane;
     bool e = false;
     if (x < g.nx) {
@@ -196,7 +165,7 @@ k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg
       }
     }
     const unsigned bal = __ballot_sync(0xffffffffu, e);
-    if (lane == 0) ebits[wi] = bal;
+    if (lane == 0) ebits[dword_index(g, rg, y, z, c)] = bal;
   WORK_LOOP_END
   warp_add(&cnt->n_swept, swept);
   warp_add(&cnt->n_recomputed, recomputed);
@@ -467,9 +436,8 @@ __global__ void k_edit_rows(uint32_t* __restrict__ tbits, int64_t nwords, const 
                             const float* __restrict__ lb, float* __restrict__ gf, uint32_t* __restrict__ state,
                             Counters* __restrict__ cnt, float step, int q_cap, uint32_t* __restrict__ next_frontier,
                             Grid g, RowGeom rg, int fwords_smem, uint32_t* __restrict__ vchg, int64_t vwords,
-                            uint32_t* __restrict__ uchg, int64_t uwords, const LoopState* __restrict__ ls) {
+                            const LoopState* __restrict__ ls) {
   uint32_t* vcur = vchg ? vchg + (int64_t)(ls->round & 1) * vwords : nullptr;
-  uint32_t* ucur = vchg ? uchg + (int64_t)(ls->round & 1) * uwords : nullptr;
   extern __shared__ uint32_t sfr[];
   for (int i = threadIdx.x; i < fwords_smem; i += blockDim.x) sfr[i] = 0;
   __syncthreads();
@@ -506,11 +474,7 @@ __global__ void k_edit_rows(uint32_t* __restrict__ tbits, int64_t nwords, const 
       const uint32_t st = state[v];
       if (st >> 16) continue;  // lossless: no-op, but its cells stay in the frontier
       changed++;
-      if (vcur) {
-        atomicOr(vcur + dword_index(g, rg, vy, vz, vx >> 5), 1u << (vx & 31));
-        const int64_t un = vz * rg.ub + vy / UY;
-        atomicOr(ucur + (un >> 5), 1u << (un & 31));
-      }
+      if (vcur) atomicOr(vcur + dword_index(g, rg, vy, vz, vx >> 5), 1u << (vx & 31));
       const uint32_t q = st & 0xFFFFu;
       if ((int)q + 1 <= q_cap) {
         // g' = RN(fhat - RN((q+1) * step)): two roundings, never fused
