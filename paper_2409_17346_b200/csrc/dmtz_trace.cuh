@@ -408,9 +408,39 @@ __device__ __forceinline__ int64_t bfs_find(const unsigned long long* keys, int6
   return -1;
 }
 
+// set bits of words [w0, w1) -> list of bit indices (any order), words cleared; one atomic per warp
+__global__ void k_bits_compact(uint32_t* __restrict__ bits, int64_t w0, int64_t w1, uint32_t* __restrict__ list,
+                               unsigned long long* __restrict__ n_out) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = w0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) - lane; base < w1;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = base + lane;
+    uint32_t word = 0u;
+    if (w < w1) {
+      word = bits[w];
+      if (word) bits[w] = 0u;
+    }
+    const int c = __popc(word);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    unsigned long long pos = 0;
+    if (lane == 31 && incl) pos = atomicAdd(n_out, (unsigned long long)incl);
+    pos = __shfl_sync(0xffffffffu, pos, 31) + (unsigned long long)(incl - c);
+    while (word) {
+      const int b = __ffs(word) - 1;
+      word &= word - 1u;
+      list[pos++] = (uint32_t)(w * 32 + b);
+    }
+  }
+}
+
 template <int D>
 __global__ void __launch_bounds__(BFS_THREADS)
-k_walk_block(const void* codes, const uint32_t* __restrict__ crit, Grid g, const long long* __restrict__ list,
+k_walk_block(const void* codes, const uint32_t* __restrict__ crit, Grid g, const uint32_t* __restrict__ list,
              int64_t nlist, int64_t conn_base, const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
              long long* __restrict__ off, uint64_t* __restrict__ cells, bool write,
              unsigned long long* __restrict__ scratch, int64_t qcap, int64_t hcap,
@@ -625,14 +655,13 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   const int64_t ovf_words = (nbk[2] + 31) / 32;
   const int64_t pre_words = (int64_t)(A.pre_bytes / 8);
   if (nbk[2] && (ovf_words + 2) * 4 + 64 * 8 > pre_words * 8) return cudaErrorMemoryAllocation;
-  const int64_t list_cap = (pre_words * 8 - (ovf_words + 2) * 4) / 8;
+  const int64_t list_cap = (pre_words * 8 - (ovf_words + 2) * 4) / 4;
   if (nbk[2] && nslots < threads) return cudaErrorMemoryAllocation;
   const int64_t blocks_path = conn_base > 0 ? (conn_base + threads - 1) / threads : 0;
   int64_t blocks_conn = (nbk[2] + threads - 1) / threads;
   if (blocks_conn * threads > nslots) blocks_conn = nslots / threads;
   long long* off = (long long*)A.out_offsets;
   TCK(cudaMemsetAsync(sc, 0, A.bfs_bytes, s));
-  std::vector<int> hov;
   for (int pass = 0; pass < 2; pass++) {
     const bool write = pass == 1;
     TCK(cudaMemsetAsync(ovf, 0, (size_t)ovf_words * 4 + 4, s));
@@ -646,36 +675,52 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
                                                           slot_h, nslots, ovf, conn_base, dc);
     TCK(cudaGetLastError());
     if (nbk[2]) {  // connectors that outgrew their slot: retry with 16x bigger slots, fewer threads
+      // the overflow bitmask is compacted into a list on the device, in word chunks that fit the list area
       int64_t q = slot_q;
-      long long* dlist = (long long*)(ovf + ((ovf_words + 3) & ~(int64_t)1));  // 8-byte aligned
+      uint32_t* dlist = (uint32_t*)(ovf + ovf_words + 1);
+      unsigned long long* dn = &dc->pad[1];
+      const int64_t chunk_words = list_cap / 32 > 0 ? list_cap / 32 : 1;
       for (int level = 0; level < 8; level++) {
-        hov.assign((size_t)ovf_words + 1, 0);
-        TCK(cudaMemcpyAsync(hov.data(), ovf, (size_t)ovf_words * 4, cudaMemcpyDeviceToHost, s));
-        TCK(cudaStreamSynchronize(s));
-        std::vector<long long> lst;
-        for (int64_t cb = 0; cb < nbk[2]; cb++)
-          if ((hov[(size_t)(cb >> 5)] >> (cb & 31)) & 1) lst.push_back(cb);
-        if (lst.empty()) break;
-        if (q >= words / 5) { A.n_internal += (int64_t)lst.size(); break; }  // larger than all scratch
-        q = q * 16 < words / 5 ? q * 16 : words / 5;
+        if (q >= words / 5) {  // larger than all scratch: count what is left as internal failures
+          TCK(cudaMemsetAsync(dn, 0, 8, s));
+          k_bits_compact<<<(unsigned)((ovf_words + 255) / 256 < 148 * 16 ? (ovf_words + 255) / 256 : 148 * 16), 256, 0,
+                           s>>>((uint32_t*)ovf, 0, ovf_words, dlist, dn);  // (list unused beyond the count)
+          TCK(cudaMemcpyAsync(&hc->pad[1], dn, 8, cudaMemcpyDeviceToHost, s));
+          TCK(cudaStreamSynchronize(s));
+          A.n_internal += (int64_t)hc->pad[1];
+          break;
+        }
+        const int64_t qn = q * 16 < words / 5 ? q * 16 : words / 5;
         int64_t h = 1;
-        while (h < 2 * q) h *= 2;
-        while (q + 2 * h > words) h /= 2;
-        int64_t ns = words / (q + 2 * h);
+        while (h < 2 * qn) h *= 2;
+        while (qn + 2 * h > words) h /= 2;
+        int64_t ns = words / (qn + 2 * h);
         if (ns < 1) ns = 1;
         if (ns > 4096) ns = 4096;
-        TCK(cudaMemsetAsync(sc, 0, A.bfs_bytes, s));
-        TCK(cudaMemsetAsync(ovf, 0, (size_t)ovf_words * 4 + 4, s));
-        for (int64_t c0 = 0; c0 < (int64_t)lst.size(); c0 += list_cap) {
-          const int64_t cn = (int64_t)lst.size() - c0 < list_cap ? (int64_t)lst.size() - c0 : list_cap;
-          TCK(cudaMemcpyAsync(dlist, lst.data() + c0, (size_t)cn * 8, cudaMemcpyHostToDevice, s));
+        bool any = false, cleared = false;
+        for (int64_t w0 = 0; w0 < ovf_words; w0 += chunk_words) {
+          const int64_t w1 = w0 + chunk_words < ovf_words ? w0 + chunk_words : ovf_words;
+          TCK(cudaMemsetAsync(dn, 0, 8, s));
+          const int64_t cb = (w1 - w0 + 255) / 256;
+          k_bits_compact<<<(unsigned)(cb < 148 * 16 ? cb : 148 * 16), 256, 0, s>>>((uint32_t*)ovf, w0, w1, dlist, dn);
+          TCK(cudaGetLastError());
+          TCK(cudaMemcpyAsync(&hc->pad[1], dn, 8, cudaMemcpyDeviceToHost, s));
+          TCK(cudaStreamSynchronize(s));
+          const int64_t cn = (int64_t)hc->pad[1];
+          if (!cn) continue;
+          any = true;
+          if (!cleared) {  // level-0 slots self-clean; bigger slots overlay them, so clear once per level
+            TCK(cudaMemsetAsync(sc, 0, A.bfs_bytes, s));
+            cleared = true;
+          }
           const int64_t nblk = cn < ns ? cn : ns;
           k_walk_block<D><<<(unsigned)nblk, BFS_THREADS, 0, s>>>(A.codes, A.crit, g, dlist, cn, conn_base,
                                                                  A.out_origin, A.out_terminal, off, A.out_cells,
-                                                                 write, sc, q, h, (unsigned int*)ovf, dc);
+                                                                 write, sc, qn, h, (unsigned int*)ovf, dc);
           TCK(cudaGetLastError());
-          TCK(cudaStreamSynchronize(s));  // lst is pageable host memory
         }
+        if (!any) break;
+        q = qn;
       }
       TCK(cudaMemsetAsync(sc, 0, A.bfs_bytes, s));
     }
