@@ -87,12 +87,12 @@ Layout layout_for(const dmtz_ctx* c) {
   const size_t cs = c->D == 3 ? 8 : 2;
   Layout L;
   size_t o = 0;
-  L.cand_f = o; o += align_up(N * cs);
   // u64 even in 2D: the trace reuses it as int64 scratch (>= 1 MiB for small grids)
   L.cand_g = o; o += align_up(N * 8 > (size_t)(1 << 20) ? N * 8 : (size_t)(1 << 20));
-  L.crit_f = o; o += align_up(N * 4);
   L.crit_g = o; o += align_up(N * 4);
-  // lowpos doubles as the trace's connector-BFS scratch: at least 128 slots of 3 x 1024 words
+  // [cand_f, tbits] is the trace's connector-BFS scratch (lowpos: at least 128 slots of 3 x 1024 words)
+  L.cand_f = o; o += align_up(N * cs);
+  L.crit_f = o; o += align_up(N * 4);
   L.lowpos = o; o += align_up(N * 8 > (size_t)128 * 3072 * 8 ? N * 8 : (size_t)128 * 3072 * 8);
   L.lb = o; o += align_up(N * 4);
   L.state = o; o += align_up(N * 4);
@@ -633,9 +633,10 @@ dmtz_status dmtz_trace_separatrices(dmtz_ctx* c, const void* codes, uint32_t kin
   a.codes = codes;
   a.kinds = kinds;
   a.pre = (long long*)(ws + L.cand_g);
-  a.pre_bytes = L.crit_f - L.cand_g;
-  a.bfs = (unsigned long long*)(ws + L.lowpos);
-  a.bfs_bytes = L.lb - L.lowpos;  // the lowpos region, which lb follows
+  a.pre_bytes = L.crit_g - L.cand_g;
+  a.bfs = (unsigned long long*)(ws + L.cand_f);
+  a.bfs_bytes = L.counters - L.cand_f;  // cand_f, crit_f, lowpos, lb, state, tbits: free during a trace
+  a.verbose = c->verbose;
   a.crit = (uint32_t*)(ws + L.crit_g);
   a.bsum = (unsigned long long*)(ws + L.edit_bc);
   a.cnt = (Counters*)(ws + L.counters);

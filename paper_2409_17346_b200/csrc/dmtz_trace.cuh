@@ -28,7 +28,7 @@ struct TraceArgs {
   uint32_t kinds;
   long long* pre;            // >= N x 8 B workspace region: per-anchor branch counts, then overflow flags
   size_t pre_bytes;
-  unsigned long long* bfs;   // N x 8 B workspace region: connector BFS slots (zeroed, self-cleaning)
+  unsigned long long* bfs;   // >= N x 8 B workspace region: connector BFS slots (zeroed, self-cleaning)
   size_t bfs_bytes;
   uint32_t* crit;            // N x 4 B workspace region
   unsigned long long* bsum;  // scan block sums (>= N / 8192 + 2 entries)
@@ -40,6 +40,7 @@ struct TraceArgs {
   uint64_t* out_terminal;
   uint8_t* out_kind;
   int64_t cap_b, cap_c;
+  int verbose = 0;
   int64_t n_branches = 0, n_cells = 0, n_internal = 0;
 };
 
@@ -714,6 +715,9 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
             cleared = true;
           }
           const int64_t nblk = cn < ns ? cn : ns;
+          if (A.verbose)
+            fprintf(stderr, "dmtz trace pass %d level %d: %lld connectors, q %lld, %lld blocks\n", pass, level + 1,
+                    (long long)cn, (long long)qn, (long long)nblk);
           k_walk_block<D><<<(unsigned)nblk, BFS_THREADS, 0, s>>>(A.codes, A.crit, g, dlist, cn, conn_base,
                                                                  A.out_origin, A.out_terminal, off, A.out_cells,
                                                                  write, sc, qn, h, (unsigned int*)ovf, dc);
