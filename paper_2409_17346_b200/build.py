@@ -35,7 +35,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         subprocess.check_call([sys.executable, gen])
     if force or _stale():
         nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-        cmd = [nvcc] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + \
+        extra = os.environ.get("DMTZ_NVCC_EXTRA", "").split()  # e.g. -DDMTZ_INSTR (instrumented build)
+        cmd = [nvcc] + NVCC_FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + \
               ["-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES]
         subprocess.check_call(cmd, cwd=CSRC)
     return LIB

@@ -77,7 +77,7 @@ inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 // Workspace layout (offsets from the base, each 256-B aligned)
 struct Layout {
-  size_t cand_f, cand_g, crit_f, crit_g, lowpos, lb, state, tbits, counters, edit_bc, ebits, fmark, vchg, units,
+  size_t cand_f, cand_g, crit_f, crit_g, lowpos, lb, state, tcache, ncache, tbits, counters, edit_bc, ebits, fmark, vchg, units,
       units2, frontier, trace, total;
   int64_t fwords;  // frontier bitmap words (one bit per row-block unit)
 };
@@ -96,6 +96,8 @@ Layout layout_for(const dmtz_ctx* c) {
   L.lowpos = o; o += align_up(N * 8 > (size_t)128 * 3072 * 8 ? N * 8 : (size_t)128 * 3072 * 8);
   L.lb = o; o += align_up(N * 4);
   L.state = o; o += align_up(N * 4);
+  L.tcache = o; o += align_up(N * 8);  // per anchor: target offsets of its false cells (last evaluation)
+  L.ncache = o; o += align_up(N);      // per anchor: number of those false cells
   L.tbits = o; o += align_up((size_t)(c->g.nz * c->g.ny * ((c->g.nx + 31) / 32)) * 4 + 64);  // row-padded
   L.counters = o; o += align_up(sizeof(Counters) * 2);
   L.edit_bc = o; o += align_up(((N + EDIT_CHUNK - 1) / EDIT_CHUNK + 2) * 8);
@@ -143,6 +145,8 @@ struct WS {
   uint32_t *crit_f, *crit_g, *state, *tbits, *ebits, *fmark, *vchg, *units, *units2, *fbits;
   int64_t vwords;
   unsigned long long* lowpos;
+  unsigned long long* tcache;
+  uint8_t* ncache;
   float* lb;
   Counters* dc;
   LoopState* ls;             // second 256 B block of the counters region
@@ -155,6 +159,8 @@ struct WS {
     crit_g = (uint32_t*)(ws + L.crit_g);
     lowpos = (unsigned long long*)(ws + L.lowpos);
     lb = (float*)(ws + L.lb);
+    tcache = (unsigned long long*)(ws + L.tcache);
+    ncache = (uint8_t*)(ws + L.ncache);
     state = (uint32_t*)(ws + L.state);
     tbits = (uint32_t*)(ws + L.tbits);
     dc = (Counters*)(ws + L.counters);
@@ -239,6 +245,7 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
   const float step = ldexpf(o->xi, -o->q_max);  // xi / 2^q_max, exact
   const int fwords_smem = fbits && fwords * 4 <= 32768 ? fwords : 0;
   if (!use_cond) CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));  // else: k_loop_check
+  if (!use_cond && c->verbose) CK(cudaMemsetAsync(&W.dc->pad[2], 0, 4 * 8, s));
   if (fbits) CK(cudaMemsetAsync(W.ebits, 0, W.rowbit_bytes, s));  // rewritten for every active unit
   if (profile) CK(cudaEventRecord(c->ev[0], s));
   k_screen<D><<<sweep_blocks, 256, 0, s>>>(g_out, W.cand_g, W.ebits, W.vchg, W.vwords, use_skip, units, n_units, g,
@@ -246,7 +253,7 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
   if (profile) CK(cudaEventRecord(c->ev[1], s));
   k_decode<D><<<sweep_blocks * 2, DECODE_THREADS, 0, s>>>(
       f, W.cand_f, W.crit_f, W.cand_g, W.ebits, W.fmark, W.tbits, dunits, n_dunits, g, rg,
-      tier_mask<D>(o->tier), W.lowpos, W.ls, own_z0, own_z1, count_z0, count_z1, W.dc);
+      tier_mask<D>(o->tier), W.lowpos, W.tcache, W.ncache, W.ls, own_z0, own_z1, count_z0, count_z1, W.dc);
   if (profile) CK(cudaEventRecord(c->ev[2], s));
   k_edit_rows<D><<<clamp_blocks(nwords, 256), 256, fwords_smem * 4, s>>>(
       W.tbits, nwords, fhat, W.lb, g_out, W.state, W.dc, step, o->q_cap, fbits, g, rg, fwords_smem,
@@ -274,7 +281,7 @@ dmtz_status round_phase(dmtz_ctx* c, const float* f, const float* fhat, const dm
                                     own_z1, count_z0, count_z1, profile, max_rounds, cudaGraphConditionalHandle(), 0,
                                     use_skip, launches, s);
   if (st) return st;
-  CK(cudaMemcpyAsync(c->host_cnt, W.dc, offsetof(Counters, first_nonfinite), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(c->host_cnt, W.dc, sizeof(Counters), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(hls, W.ls, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return DMTZ_OK;
@@ -390,8 +397,10 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
         if (ms0 > 0 && (int64_t)hc->n_recomputed == g.N) { st->screen_ms_full += ms0; st->n_screen_full++; }
       }
       if (c->verbose)
-        fprintf(stderr, "dmtz round %llu: swept %llu false %llu targets %llu changed %llu\n", hls->sweeps,
-                hc->n_swept, hc->n_false, hc->n_targets, hc->n_changed);
+        fprintf(stderr, "dmtz round %llu: units %llu recomputed %llu swept %llu false %llu targets %llu changed %llu"
+                " | act_chg %llu act_had %llu had_false %llu chg_false %llu\n",
+                hls->sweeps, hc->n_units, hc->n_recomputed, hc->n_swept, hc->n_false, hc->n_targets, hc->n_changed,
+                hc->pad[2], hc->pad[3], hc->pad[4], hc->pad[5]);
       const bool go = hls->status == 0 && hls->rounds == hls->sweeps;  // check advanced the round
       if (!go) break;
     }
@@ -635,7 +644,7 @@ dmtz_status dmtz_trace_separatrices(dmtz_ctx* c, const void* codes, uint32_t kin
   a.pre = (long long*)(ws + L.cand_g);
   a.pre_bytes = L.crit_g - L.cand_g;
   a.bfs = (unsigned long long*)(ws + L.cand_f);
-  a.bfs_bytes = L.counters - L.cand_f;  // cand_f, crit_f, lowpos, lb, state, tbits: free during a trace
+  a.bfs_bytes = L.counters - L.cand_f;  // cand_f .. tbits: free during a trace
   a.verbose = c->verbose;
   a.crit = (uint32_t*)(ws + L.crit_g);
   a.bsum = (unsigned long long*)(ws + L.edit_bc);

@@ -259,19 +259,54 @@ __device__ __forceinline__ uint32_t target_del(const TargetTables& T, int t, boo
 }
 
 // ---------------------------------------------------------------------------
-// k_decode: classification.  crit_f is precomputed once per call; anchors are
-// revisited only where a code of u + {0,1}^D changed or false cells remain.
+// k_decode: classification.  crit_f is precomputed once per call.  Work item =
+// (unit, row, group of DG 32-anchor chunks); an anchor is visited only if a code
+// of u + {0,1}^D changed this round ("chg") or it had false cells last round.
+//  * had false cells, no code changed: same false cells, same targets (both are
+//    functions of those codes, f and fixed tables) -> replay the cached target
+//    offsets (tcache) and false-cell count (ncache);
+//  * code changed: decode.  The anchors to decode are compacted into full warps
+//    (lane = one anchor) so that sparse rows do not pay 32 lanes per anchor.
+// Targets go to a shared-memory window over the group's rows y-1..y+2, planes
+// z-1..z+2 (x from the group start - 32), flushed with one atomicOr per
+// non-empty word into the row-padded target bitmap.
 // ---------------------------------------------------------------------------
 constexpr int DECODE_THREADS = 128;
+constexpr int DG = 16;                  // chunks per work item (512 anchors of a row)
+constexpr int TWW = DG + 2;             // window words per row
 struct DecodeWarpSmem {
   uint2 cf[8 * 32];
   uint2 cg[8 * 32];
   unsigned long long lowpos[32];
   unsigned long long dp[32];
-  uint32_t tw[48];   // target window of a 32-anchor chunk: z-1..z+2 x y-1..y+2 rows x 3 words (x0-32 .. x0+63)
+  unsigned long long tm[32];   // per slot: target offsets of its false cells (bit = packed delta)
+  uint32_t tw[16 * TWW];       // target window: 16 rows (dz+1)*4+(dy+1) x TWW words
   uint32_t critf[32];
+  uint32_t fm[DG];             // new false-cell marks of the group's chunks
+  uint16_t sx[32];             // per slot: anchor offset in the group (chunk * 32 + lane)
+  uint16_t list[DG * 32];      // compacted anchor offsets
   uint16_t items[32 * 26];
 };
+
+// anchors of the group whose bit is set in the lanes' chunk masks -> W.list (ascending); count
+__device__ __forceinline__ int compact_group(uint32_t m, int lane, uint16_t* list) {
+  const int n = __popc(m);
+  int pre = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, pre, o);
+    if (lane >= o) pre += v;
+  }
+  const int total = __shfl_sync(0xffffffffu, pre, 31);
+  pre -= n;
+  while (m) {
+    const int b = __ffs(m) - 1;
+    m &= m - 1;
+    list[pre++] = (uint16_t)(lane * 32 + b);
+  }
+  __syncwarp();
+  return total;
+}
 
 template <int D>
 __global__ void __launch_bounds__(DECODE_THREADS, 6)
@@ -280,7 +315,8 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
          const uint32_t* __restrict__ ebits, uint32_t* __restrict__ fmark,
          uint32_t* __restrict__ tbits, const uint32_t* __restrict__ units,
          const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg, uint32_t tier_mask,
-         const unsigned long long* __restrict__ lowpos_f, const LoopState* __restrict__ ls, int64_t own_z0,
+         const unsigned long long* __restrict__ lowpos_f, unsigned long long* __restrict__ tcache,
+         uint8_t* __restrict__ ncache, const LoopState* __restrict__ ls, int64_t own_z0,
          int64_t own_z1, int64_t count_z0, int64_t count_z1, Counters* __restrict__ cnt) {
   const bool count_kinds = ls->round == 1;  // kinds are reported for round 1 only
   __shared__ TargetTables T;
@@ -290,16 +326,10 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
   DecodeWarpSmem& W = WS[threadIdx.x >> 5];
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  __shared__ unsigned int kcs[8];
-  if (threadIdx.x < 8) kcs[threadIdx.x] = 0;
-  __syncthreads();
-  unsigned int* kc = kcs;  // kind counts of round 1 (shared-memory histogram)
   unsigned long long nfalse = 0, nint = 0;
-  // items = (unit, row, group of 32 row chunks); lane j of the warp first scans
-  // chunk c0 + j (changed-code words of u + {0,1}^D and the false-cell mark),
-  // then the warp processes the chunks that need work, lanes = the 32 anchors.
+  unsigned int kacc = 0;  // round 1: lane k < 8 counts false cells of kind k
   const uint32_t n_units_ = (uint32_t)*n_units_p;
-  const uint32_t ngr = (uint32_t)((rg.wpr + 31) / 32);
+  const uint32_t ngr = (uint32_t)((rg.wpr + DG - 1) / DG);
   const uint32_t per_unit_ = (uint32_t)UY * ngr;
   const uint32_t total_ = n_units_ * per_unit_;
   for (uint32_t it_ = (uint32_t)warp; it_ < total_; it_ += (uint32_t)nwarps) {
@@ -309,119 +339,153 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
     const int64_t z = unit_ / ub_;
     const int64_t y = (int64_t)(unit_ - (uint32_t)z * ub_) * UY + rem_ / ngr;
     if (y >= g.ny) continue;  // warp-uniform
-    const int64_t cbase = (int64_t)(rem_ % ngr) * 32;
+    const int64_t cbase = (int64_t)(rem_ % ngr) * DG;
+    // lane j < DG scans chunk cbase + j: changed-code words of u + {0,1}^D and the false-cell mark
     uint32_t chg_l = 0, had_l = 0;
-    {
-      const int64_t cl = cbase + lane;
-      if (cl < rg.wpr) {
+    const int64_t cl = cbase + lane;
+    if (lane < DG && cl < rg.wpr) {
 #pragma unroll
-        for (int r = 0; r < (D == 3 ? 4 : 2); r++) {
-          const int64_t yy = y + (r & 1), zz = z + (r >> 1);
-          if (yy >= g.ny || zz >= g.nz) continue;
-          const int64_t wi = dword_index(g, rg, yy, zz, cl);
-          const uint32_t w0 = __ldg(ebits + wi);
-          const uint32_t w1 = (cl + 1 < rg.wpr) ? __ldg(ebits + wi + 1) : 0u;
-          chg_l |= w0 | (w0 >> 1) | (w1 << 31);
-        }
-        had_l = fmark[dword_index(g, rg, y, z, cl)];
+      for (int r = 0; r < (D == 3 ? 4 : 2); r++) {
+        const int64_t yy = y + (r & 1), zz = z + (r >> 1);
+        if (yy >= g.ny || zz >= g.nz) continue;
+        const int64_t wi = dword_index(g, rg, yy, zz, cl);
+        const uint32_t w0 = __ldg(ebits + wi);
+        const uint32_t w1 = (cl + 1 < rg.wpr) ? __ldg(ebits + wi + 1) : 0u;
+        chg_l |= w0 | (w0 >> 1) | (w1 << 31);
       }
+      had_l = fmark[dword_index(g, rg, y, z, cl)];
+      const int64_t rem = g.nx - cl * 32;
+      if (rem < 32) chg_l &= (1u << rem) - 1u;
     }
-    unsigned todo = __ballot_sync(0xffffffffu, (chg_l | had_l) != 0);
-    while (todo) {
-      const int j = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const int64_t c = cbase + j;
-      const uint32_t chg = __shfl_sync(0xffffffffu, chg_l, j);
-      const uint32_t had = __shfl_sync(0xffffffffu, had_l, j);
-      const int64_t fwi = dword_index(g, rg, y, z, c);
-    const int64_t x = c * 32 + lane;
-    const int64_t u = x + y * g.sy + z * g.sz;
-    const bool active = x < g.nx && (((chg | had) >> lane) & 1u);
-    uint32_t diff = 0, critf = 0;
-    uint64_t dp = 0;
-    uint64_t cf[Tr<D>::NDELTA], cgv[Tr<D>::NDELTA];
-#pragma unroll
-    for (int dm = 0; dm < Tr<D>::NDELTA; dm++) cf[dm] = cgv[dm] = Tr<D>::ALL_NONE;
-    if (active) {
-      const int ok = axes_ok(g, x, y, z);
-#pragma unroll
-      for (int dm = 0; dm < Tr<D>::NDELTA; dm++) {
-        if ((dm & ~ok) != 0) { cf[dm] = cgv[dm] = Tr<D>::ALL_NONE; continue; }
-        const int64_t w = u + mask_delta(g, dm);
-        cf[dm] = (uint64_t)__ldg(cand_f + w);
-        cgv[dm] = (uint64_t)__ldg(cg + w);
-      }
-      const uint32_t cgm = decode_crit_dp<D>(cgv, ok, &dp);
-      critf = __ldg(crit_f + u);
-      diff = (critf ^ cgm) & tier_mask;
-    }
-    const unsigned fb = __ballot_sync(0xffffffffu, diff != 0);
-    if (lane == 0 && fb != had) fmark[fwi] = fb;
-    if (!fb) continue;  // warp-uniform (next chunk of this row)
-    // warp work list of the false cells (source lane, type): all lanes then share them
-    const int nmine = __popc(diff);
+    if (!__any_sync(0xffffffffu, (chg_l | had_l) != 0)) continue;  // warp-uniform
     const bool counted = z >= count_z0 && z < count_z1;  // slab mode: each anchor counted by its owner
-    if (counted) nfalse += nmine;
-    int pre = nmine;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, pre, o);
-      if (lane >= o) pre += v;
+    const int64_t row0 = y * g.sy + z * g.sz + cbase * 32;  // anchor index of the group's first x
+    for (int i = lane; i < 16 * TWW; i += 32) W.tw[i] = 0u;
+    const uint32_t cached_l = had_l & ~chg_l;
+    if (lane < DG) W.fm[lane] = cached_l;
+    // (1) replay: false cells and targets unchanged since the last evaluation
+    {
+      const int n = compact_group(cached_l, lane, W.list);
+      for (int b0 = 0; b0 < n; b0 += 32) {
+        if (b0 + lane < n) {
+          const int o = W.list[b0 + lane];
+          const int64_t u = row0 + o;
+          unsigned long long tmc = tcache[u];
+          if (counted) nfalse += ncache[u];
+          while (tmc) {
+            const int del = __ffsll((long long)tmc) - 1;
+            tmc &= tmc - 1ull;
+            const int X = 32 + o + (del & 3) - 1;
+            const int row = ((del >> 4) & 3) * 4 + ((del >> 2) & 3);
+            atomicOr(&W.tw[row * TWW + (X >> 5)], 1u << (X & 31));
+          }
+        }
+      }
     }
-    const int total = __shfl_sync(0xffffffffu, pre, 31);
-    pre -= nmine;
-    W.tw[lane] = 0u;
-    if (lane < 16) W.tw[32 + lane] = 0u;
-    if (diff) {
+    // (2) decode the anchors whose codes changed, 32 per pass
+    const int ndec = compact_group(chg_l, lane, W.list);
+    for (int b0 = 0; b0 < ndec; b0 += 32) {
+      const bool act = b0 + lane < ndec;
+      const int o = act ? W.list[b0 + lane] : 0;
+      const int64_t x = cbase * 32 + o;
+      const int64_t u = row0 + o;
+      uint32_t diff = 0, critf = 0;
+      uint64_t dp = 0;
+      uint64_t cf[Tr<D>::NDELTA], cgv[Tr<D>::NDELTA];
 #pragma unroll
-      for (int dm = 0; dm < Tr<D>::NDELTA; dm++) {
-        W.cf[dm * 32 + lane] = make_uint2((uint32_t)cf[dm], (uint32_t)(cf[dm] >> 32));
-        W.cg[dm * 32 + lane] = make_uint2((uint32_t)cgv[dm], (uint32_t)(cgv[dm] >> 32));
+      for (int dm = 0; dm < Tr<D>::NDELTA; dm++) cf[dm] = cgv[dm] = Tr<D>::ALL_NONE;
+      if (act) {
+        const int ok = axes_ok(g, x, y, z);
+#pragma unroll
+        for (int dm = 0; dm < Tr<D>::NDELTA; dm++) {
+          if ((dm & ~ok) != 0) continue;
+          const int64_t w = u + mask_delta(g, dm);
+          cf[dm] = (uint64_t)__ldg(cand_f + w);
+          cgv[dm] = (uint64_t)__ldg(cg + w);
+        }
+        const uint32_t cgm = decode_crit_dp<D>(cgv, ok, &dp);
+        critf = __ldg(crit_f + u);
+        diff = (critf ^ cgm) & tier_mask;
       }
-      W.critf[lane] = critf;
-      W.dp[lane] = dp;
-      W.lowpos[lane] = __ldg(lowpos_f + u);
-      uint32_t dd = diff;
-      for (int k = 0; dd; k++) {
-        const int t = __ffs(dd) - 1;
-        dd &= dd - 1;
-        W.items[pre + k] = (uint16_t)(lane | (t << 5));
+      if (!__any_sync(0xffffffffu, diff != 0)) continue;  // warp-uniform
+      if (diff) atomicOr(&W.fm[o >> 5], 1u << (o & 31));
+      // work list of the false cells (slot, type): all lanes then share them
+      const int nmine = __popc(diff);
+      if (counted) nfalse += nmine;
+      int pre = nmine;
+#pragma unroll
+      for (int k = 1; k < 32; k <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, pre, k);
+        if (lane >= k) pre += v;
       }
+      const int total = __shfl_sync(0xffffffffu, pre, 31);
+      pre -= nmine;
+      W.tm[lane] = 0ull;
+      if (diff) {
+#pragma unroll
+        for (int dm = 0; dm < Tr<D>::NDELTA; dm++) {
+          W.cf[dm * 32 + lane] = make_uint2((uint32_t)cf[dm], (uint32_t)(cf[dm] >> 32));
+          W.cg[dm * 32 + lane] = make_uint2((uint32_t)cgv[dm], (uint32_t)(cgv[dm] >> 32));
+        }
+        W.critf[lane] = critf;
+        W.dp[lane] = dp;
+        W.lowpos[lane] = __ldg(lowpos_f + u);
+        W.sx[lane] = (uint16_t)o;
+        uint32_t dd = diff;
+        for (int k = 0; dd; k++) {
+          const int t = __ffs(dd) - 1;
+          dd &= dd - 1;
+          W.items[pre + k] = (uint16_t)(lane | (t << 5));
+        }
+      }
+      __syncwarp();
+      // targets -> window (x relative to the group start - 32)
+      for (int i0 = 0; i0 < total; i0 += 32) {
+        const int i = i0 + lane;
+        const bool live = i < total;
+        const int item = live ? W.items[i] : 0;
+        const int src = item & 31, t = item >> 5;
+        const bool fn = (W.critf[src] >> t) & 1u;
+        if (count_kinds && counted) {
+          const int dim = T.tinfo[t] & 3;
+          const int key = live ? 2 * ((dim == Tr<D>::TOP) ? 3 : dim) + (fn ? 1 : 0) : 8;
+#pragma unroll
+          for (int k = 0; k < 8; k++) {
+            const unsigned bk = __ballot_sync(0xffffffffu, key == k);
+            if (lane == k) kacc += __popc(bk);
+          }
+        }
+        if (!live) continue;
+        const uint32_t del = target_del<D>(T, t, fn, W.lowpos[src], W.dp[src], W.cf, W.cg, src);
+        if (del == 0xFFFFFFFFu) { nint++; continue; }
+        const int X = 32 + W.sx[src] + (int)(del & 3) - 1;
+        const int row = (int)((del >> 4) & 3) * 4 + (int)((del >> 2) & 3);   // (dz+1) * 4 + (dy+1)
+        atomicOr(&W.tw[row * TWW + (X >> 5)], 1u << (X & 31));
+        atomicOr((uint32_t*)&W.tm[src] + ((del >> 5) & 1), 1u << (del & 31));   // native 32-bit smem atomic
+      }
+      __syncwarp();
+      if (diff) {  // evaluated anchors refresh their cache entry
+        tcache[u] = W.tm[lane];
+        ncache[u] = (uint8_t)nmine;
+      }
+      __syncwarp();
     }
     __syncwarp();
-    // targets -> the chunk's target window in shared memory (x relative to x0 - 32)
-    for (int i = lane; i < total; i += 32) {
-      const int item = W.items[i];
-      const int src = item & 31, t = item >> 5;
-      const bool fn = (W.critf[src] >> t) & 1u;
-      if (count_kinds && counted) {
-        const int dim = T.tinfo[t] & 3;
-        const int cls = (dim == Tr<D>::TOP) ? 3 : dim;
-        atomicAdd(kc + 2 * cls + (fn ? 1 : 0), 1u);
-      }
-      const uint32_t del = target_del<D>(T, t, fn, W.lowpos[src], W.dp[src], W.cf, W.cg, src);
-      if (del == 0xFFFFFFFFu) { nint++; continue; }
-      const int X = 32 + src + (int)(del & 3) - 1;              // 31 .. 65
-      const int row = (int)((del >> 4) & 3) * 4 + (int)((del >> 2) & 3);   // (dz+1) * 4 + (dy+1)
-      atomicOr(&W.tw[row * 3 + (X >> 5)], 1u << (X & 31));
-    }
-    __syncwarp();
+    if (lane < DG && cl < rg.wpr && W.fm[lane] != had_l) fmark[dword_index(g, rg, y, z, cl)] = W.fm[lane];
     // flush the window: one aligned atomicOr per non-empty word (row-padded target bitmap)
-    for (int i = lane; i < 48; i += 32) {
+    for (int i = lane; i < 16 * TWW; i += 32) {
       const uint32_t wv = W.tw[i];
       if (!wv) continue;
-      const int row = i / 3, wd = i - (i / 3) * 3;
-      const int64_t ty = y + (row & 3) - 1, tz = z + (row >> 2) - 1, tc = c + wd - 1;
+      const int row = i / TWW, wd = i - row * TWW;
+      const int64_t ty = y + (row & 3) - 1, tz = z + (row >> 2) - 1, tc = cbase + wd - 1;
       if (tz < own_z0 || tz >= own_z1) continue;   // slab mode: only the owned vertices
       atomicOr(tbits + dword_index(g, rg, ty, tz, tc), wv);
     }
     __syncwarp();
-    }
   }
   warp_add(&cnt->n_false, nfalse);
   warp_add(&cnt->n_internal, nint);
-  __syncthreads();
-  if (count_kinds && threadIdx.x < 8 && kcs[threadIdx.x]) atomicAdd(&cnt->kinds[threadIdx.x], (unsigned long long)kcs[threadIdx.x]);
+  if (count_kinds && lane < 8 && kacc) atomicAdd(&cnt->kinds[lane], (unsigned long long)kacc);
 }
 
 // ---------------------------------------------------------------------------
