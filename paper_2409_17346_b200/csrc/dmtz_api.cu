@@ -248,7 +248,7 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
   if (!use_cond && c->verbose) CK(cudaMemsetAsync(&W.dc->pad[2], 0, 4 * 8, s));
   if (fbits) CK(cudaMemsetAsync(W.ebits, 0, W.rowbit_bytes, s));  // rewritten for every active unit
   if (profile) CK(cudaEventRecord(c->ev[0], s));
-  k_screen<D><<<sweep_blocks, 256, 0, s>>>(g_out, W.cand_g, W.ebits, W.vchg, W.vwords, use_skip, units, n_units, g,
+  k_screen<D><<<sweep_blocks, SCREEN_THREADS, 0, s>>>(g_out, W.cand_g, W.ebits, W.vchg, W.vwords, use_skip, units, n_units, g,
                                            rg, W.ls, W.dc);
   if (profile) CK(cudaEventRecord(c->ev[1], s));
   k_decode<D><<<sweep_blocks * 2, DECODE_THREADS, 0, s>>>(

@@ -44,6 +44,7 @@ __host__ __device__ inline RowGeom row_geom(const Grid& g) {
 // Work decomposition of the active units: item = (unit, row, group of CG row
 // chunks of 32 anchors); warps stride over items, 32-bit index arithmetic.
 constexpr int CG = 4;
+constexpr int DG = 16;  // k_screen / k_decode: chunks per work item (512 anchors of a row)
 #define WORK_LOOP_BEGIN                                                                          \
   {                                                                                              \
     const uint32_t n_units_ = (uint32_t)*n_units_p;                                              \
@@ -111,15 +112,24 @@ __device__ __forceinline__ uint64_t cand_of(const float (&s)[27]) {
 }
 
 // ---------------------------------------------------------------------------
-// k_screen: codes of g; e(u) = code changed.  One warp per 32-anchor row chunk.
+// k_screen: codes of g; e(u) = code changed.  Work item = (unit, row, group of DG
+// 32-anchor chunks).  need(u): a vertex of u's 3^D box changed in the previous
+// round -> the code may change; else it provably did not (a code is a function
+// of that box) and the memoized one stays.  The anchors that need a recompute
+// are compacted into full warps (lane = one anchor).
 // ---------------------------------------------------------------------------
+constexpr int SCREEN_THREADS = 256;
 template <int D>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(SCREEN_THREADS)
 k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg, uint32_t* __restrict__ ebits,
          uint32_t* __restrict__ vchg, int64_t vwords, int use_skip, const uint32_t* __restrict__ units,
          const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg, const LoopState* __restrict__ ls,
          Counters* __restrict__ cnt) {
-  const int lane = threadIdx.x & 31;
+  __shared__ uint16_t s_list[SCREEN_THREADS / 32][DG * 32];
+  __shared__ uint32_t s_e[SCREEN_THREADS / 32][DG];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint16_t* list = s_list[wib];
+  uint32_t* se = s_e[wib];
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const unsigned long long round = ls->round;
@@ -129,44 +139,91 @@ k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg
   uint32_t* vcur = vchg + (int64_t)(round & 1) * vwords;
   const bool skip = use_skip && !first_round;
   unsigned long long swept = 0, recomputed = 0;
-  WORK_LOOP_BEGIN
-    // need(u): a vertex of u's 3x3x3 box changed -> the code may change; else it provably
-    // did not (a code is a function of that box) and the memoized one stays.
-    uint32_t need = 0xffffffffu;
-    if (skip) {
-      uint32_t contrib = 0;
-      if (lane < 27) {
-        const int dx = lane / 9 - 1, r9 = lane % 9;
-        const int64_t yy = y + (r9 % 3) - 1, zz = D == 3 ? z + (r9 / 3) - 1 : z;
-        const int64_t cc = c + dx;
-        const bool ok_row = yy >= 0 && yy < g.ny && zz >= 0 && zz < g.nz && cc >= 0 && cc < rg.wpr &&
-                            (D == 3 || r9 / 3 == 1);
-        if (ok_row) {
-          const uint32_t w = __ldg(vprev + dword_index(g, rg, yy, zz, cc));
-          contrib = dx < 0 ? (w >> 31) : dx > 0 ? (w << 31) : (w | (w << 1) | (w >> 1));
-        }
+  const uint32_t n_units_ = (uint32_t)*n_units_p;
+  const uint32_t ngr = (uint32_t)((rg.wpr + DG - 1) / DG);
+  const uint32_t per_unit_ = (uint32_t)UY * ngr;
+  const uint32_t total_ = n_units_ * per_unit_;
+  for (uint32_t it_ = (uint32_t)warp; it_ < total_; it_ += (uint32_t)nwarps) {
+    const uint32_t ui_ = it_ / per_unit_, rem_ = it_ - ui_ * per_unit_;
+    const uint32_t unit_ = units[ui_];
+    const uint32_t ub_ = (uint32_t)rg.ub;
+    const int64_t z = unit_ / ub_;
+    const int64_t y = (int64_t)(unit_ - (uint32_t)z * ub_) * UY + rem_ / ngr;
+    if (y >= g.ny) continue;  // warp-uniform
+    const int64_t cbase = (int64_t)(rem_ % ngr) * DG;
+    const int64_t cl = cbase + lane;
+    const bool inrow = lane < DG && cl < rg.wpr;
+    uint32_t valid = 0, need = 0;
+    if (inrow) {
+      const int64_t rem = g.nx - cl * 32;
+      valid = rem < 32 ? (1u << rem) - 1u : 0xffffffffu;
+      need = valid;
+      if (skip) {  // OR of the previous round's change words over the 3^D rows, then dilate in x
+        uint32_t A = 0, B = 0, C = 0;
+#pragma unroll
+        for (int dz = (D == 3 ? -1 : 0); dz <= (D == 3 ? 1 : 0); dz++)
+#pragma unroll
+          for (int dy = -1; dy <= 1; dy++) {
+            const int64_t yy = y + dy, zz = z + dz;
+            if (yy < 0 || yy >= g.ny || zz < 0 || zz >= g.nz) continue;
+            const int64_t wi = dword_index(g, rg, yy, zz, cl);
+            B |= __ldg(vprev + wi);
+            if (cl > 0) A |= __ldg(vprev + wi - 1);
+            if (cl + 1 < rg.wpr) C |= __ldg(vprev + wi + 1);
+          }
+        need &= (A >> 31) | B | (B << 1) | (B >> 1) | (C << 31);
       }
-      need = __reduce_or_sync(0xffffffffu, contrib);
+      vcur[dword_index(g, rg, y, z, cl)] = 0u;
+      swept += __popc(valid);
+      se[lane] = 0u;
     }
-    if (lane == 0) vcur[dword_index(g, rg, y, z, c)] = 0u;
-    const int64_t x = c * 32 + lane;
-    bool e = false;
-    if (x < g.nx) {
-      swept++;
-      if ((need >> lane) & 1u) {
-        const int64_t v = x + y * g.sy + z * g.sz;
-        float s[27];
-        load_stencil<D>(gfld, g, v, x, y, z, s);
+    const bool dense = __all_sync(0xffffffffu, need == valid);
+    int n;
+    if (dense) {
+      n = (int)(__shfl_sync(0xffffffffu, (int)(g.nx - cbase * 32 < DG * 32 ? g.nx - cbase * 32 : DG * 32), 0));
+    } else {
+      const int c = __popc(need);
+      int pre = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre += v;
+      }
+      n = __shfl_sync(0xffffffffu, pre, 31);
+      pre -= c;
+      uint32_t m = need;
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        list[pre++] = (uint16_t)(lane * 32 + b);
+      }
+    }
+    __syncwarp();
+    const int64_t row0 = y * g.sy + z * g.sz + cbase * 32;
+    for (int b0 = 0; b0 < n; b0 += 32) {
+      const bool act = b0 + lane < n;
+      const int o = act ? (dense ? b0 + lane : (int)list[b0 + lane]) : 0;
+      bool e = false;
+      if (act) {
+        const int64_t x = cbase * 32 + o;
+        const int64_t v = row0 + o;
+        float sv[27];
+        load_stencil<D>(gfld, g, v, x, y, z, sv);
         const int ok = axes_ok(g, x, y, z);
-        const uint64_t code = cand_of<D>(s) | t_nonex_fill<D>(ok);
+        const uint64_t code = cand_of<D>(sv) | t_nonex_fill<D>(ok);
         e = first_round || code != (uint64_t)cg[v];
         if (e) cg[v] = (typename Tr<D>::code_t)code;
         recomputed++;
       }
+      // changed-code bits per chunk (the batch's lanes are in ascending anchor order)
+      const unsigned grp = __match_any_sync(0xffffffffu, act ? (o >> 5) : -1);
+      const uint32_t bits = __reduce_or_sync(grp, e ? 1u << (o & 31) : 0u);
+      if (act && lane == __ffs(grp) - 1 && bits) se[o >> 5] |= bits;
+      __syncwarp();
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, e);
-    if (lane == 0) ebits[dword_index(g, rg, y, z, c)] = bal;
-  WORK_LOOP_END
+    if (inrow) ebits[dword_index(g, rg, y, z, cl)] = se[lane];
+    __syncwarp();
+  }
   warp_add(&cnt->n_swept, swept);
   warp_add(&cnt->n_recomputed, recomputed);
 }
@@ -272,7 +329,6 @@ __device__ __forceinline__ uint32_t target_del(const TargetTables& T, int t, boo
 // non-empty word into the row-padded target bitmap.
 // ---------------------------------------------------------------------------
 constexpr int DECODE_THREADS = 128;
-constexpr int DG = 16;                  // chunks per work item (512 anchors of a row)
 constexpr int TWW = DG + 2;             // window words per row
 struct DecodeWarpSmem {
   uint2 cf[8 * 32];
@@ -502,59 +558,77 @@ __global__ void k_edit_rows(uint32_t* __restrict__ tbits, int64_t nwords, const 
                             Grid g, RowGeom rg, int fwords_smem, uint32_t* __restrict__ vchg, int64_t vwords,
                             const LoopState* __restrict__ ls) {
   uint32_t* vcur = vchg ? vchg + (int64_t)(ls->round & 1) * vwords : nullptr;
+  // each block takes a contiguous word range, so its frontier units span a few planes
+  const int64_t per_block = ((nwords + gridDim.x - 1) / gridDim.x + 31) / 32 * 32;
+  const int64_t w_begin = (int64_t)blockIdx.x * per_block;
+  const int64_t w_end = w_begin + per_block < nwords ? w_begin + per_block : nwords;
+  if (w_begin >= w_end) return;  // block-uniform
+  // frontier words this block can touch: units of planes z_first - 2 .. z_last + 1
+  const int64_t z_first = (w_begin / rg.wpr) / g.ny, z_last = ((w_end - 1) / rg.wpr) / g.ny;
+  const int64_t fz0 = z_first >= 2 ? z_first - 2 : 0, fz1 = z_last + 1 < g.nz ? z_last + 1 : g.nz - 1;
+  const int64_t fw0 = (fz0 * rg.ub) >> 5, fw1 = (((fz1 + 1) * rg.ub - 1) >> 5) + 1;
   extern __shared__ uint32_t sfr[];
-  for (int i = threadIdx.x; i < fwords_smem; i += blockDim.x) sfr[i] = 0;
+  const bool use_smem = fwords_smem && fw1 - fw0 <= fwords_smem;
+  if (use_smem)
+    for (int64_t i = threadIdx.x; i < fw1 - fw0; i += blockDim.x) sfr[i] = 0;
   __syncthreads();
-  uint32_t* fr = fwords_smem ? sfr : next_frontier;
   unsigned long long changed = 0, targets = 0;
   const int lane = threadIdx.x & 31;
-  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t base = warp0 * 32; base < nwords; base += nwarps * 32) {
+  const int wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+  for (int64_t base = w_begin + (int64_t)wib * 32; base < w_end; base += (int64_t)nwb * 32) {
     const int64_t wi = base + lane;
-    uint32_t word = wi < nwords ? tbits[wi] : 0u;
+    uint32_t word = wi < w_end ? tbits[wi] : 0u;
     if (word) tbits[wi] = 0;
     unsigned nz = __ballot_sync(0xffffffffu, word != 0);
     while (nz) {
       const int src = __ffs(nz) - 1;
       nz &= nz - 1;
       const uint32_t wv = __shfl_sync(0xffffffffu, word, src);
-      if (!((wv >> lane) & 1u)) continue;
-      // row-padded target bitmap: word = (z * ny + y) * wpr + x / 32
+      // row-padded target bitmap: word = (z * ny + y) * wpr + x / 32; all its targets share (y, z)
       const int64_t wrow = (base + src) / rg.wpr;
-      const int64_t vx = ((base + src) - wrow * rg.wpr) * 32 + lane;
       const int64_t vy = wrow % g.ny, vz = wrow / g.ny;
-      const int64_t v = vx + vy * g.sy + vz * g.sz;
-      targets++;
-      if (next_frontier) {
+      if (next_frontier && lane < 8) {  // the units meeting (y, z) + [-2, 1]: <= 4 planes x 2 row blocks
         const int64_t y0 = vy >= 2 ? vy - 2 : 0, y1 = vy + 1 < g.ny ? vy + 1 : g.ny - 1;
-        const int64_t z0 = vz >= 2 ? vz - 2 : 0, z1 = vz + 1 < g.nz ? vz + 1 : g.nz - 1;
-        for (int64_t zz = z0; zz <= z1; zz++)
-          for (int64_t b = y0 / UY; b <= y1 / UY; b++) {
-            const int64_t unit = zz * rg.ub + b;
-            atomicOr(fr + (unit >> 5), 1u << (unit & 31));
+        const int64_t zz = (vz >= 2 ? vz - 2 : 0) + (lane >> 1), z1 = vz + 1 < g.nz ? vz + 1 : g.nz - 1;
+        const int64_t b = y0 / UY + (lane & 1);
+        if (zz <= z1 && b <= y1 / UY) {
+          const int64_t unit = zz * rg.ub + b;
+          if (use_smem) atomicOr(sfr + ((unit >> 5) - fw0), 1u << (unit & 31));
+          else atomicOr(next_frontier + (unit >> 5), 1u << (unit & 31));
+        }
+      }
+      bool ch = false;
+      if ((wv >> lane) & 1u) {
+        const int64_t vx = ((base + src) - wrow * rg.wpr) * 32 + lane;
+        const int64_t v = vx + vy * g.sy + vz * g.sz;
+        targets++;
+        const uint32_t st = state[v];
+        if (!(st >> 16)) {  // lossless targets are no-ops, but their cells stay in the frontier
+          ch = true;
+          changed++;
+          const uint32_t q = st & 0xFFFFu;
+          bool done = false;
+          if ((int)q + 1 <= q_cap) {
+            // g' = RN(fhat - RN((q+1) * step)): two roundings, never fused
+            const float gp = __fsub_rn(fhat[v], __fmul_rn((float)(q + 1), step));
+            if (gp >= lb[v]) { state[v] = q + 1; gf[v] = gp; done = true; }
           }
+          if (!done) {
+            gf[v] = lb[v];              // clamp to the lower bound, stored losslessly
+            state[v] = q | (1u << 16);
+          }
+        }
       }
-      const uint32_t st = state[v];
-      if (st >> 16) continue;  // lossless: no-op, but its cells stay in the frontier
-      changed++;
-      if (vcur) atomicOr(vcur + dword_index(g, rg, vy, vz, vx >> 5), 1u << (vx & 31));
-      const uint32_t q = st & 0xFFFFu;
-      if ((int)q + 1 <= q_cap) {
-        // g' = RN(fhat - RN((q+1) * step)): two roundings, never fused
-        const float gp = __fsub_rn(fhat[v], __fmul_rn((float)(q + 1), step));
-        if (gp >= lb[v]) { state[v] = q + 1; gf[v] = gp; continue; }
-      }
-      gf[v] = lb[v];              // clamp to the lower bound, stored losslessly
-      state[v] = q | (1u << 16);
+      const unsigned cb = __ballot_sync(0xffffffffu, ch);
+      if (vcur && lane == 0 && cb) atomicOr(vcur + base + src, cb);   // same row-padded word index
     }
   }
   warp_add(&cnt->n_changed, changed);
   warp_add(&cnt->n_targets, targets);
-  if (fwords_smem) {
+  if (use_smem) {
     __syncthreads();
-    for (int i = threadIdx.x; i < fwords_smem; i += blockDim.x)
-      if (sfr[i]) atomicOr(next_frontier + i, sfr[i]);
+    for (int64_t i = threadIdx.x; i < fw1 - fw0; i += blockDim.x)
+      if (sfr[i]) atomicOr(next_frontier + fw0 + i, sfr[i]);
   }
 }
 
