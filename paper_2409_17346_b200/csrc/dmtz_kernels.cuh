@@ -120,6 +120,16 @@ __global__ void k_loop_check(Counters* cnt, LoopState* ls, unsigned long long ma
 // table accessors (constant-folded when t is a compile-time constant after unrolling)
 #define DMTZ_TAB(D, name) ((D) == 3 ? k3d::name : k2d::name)
 template <int D> __device__ __forceinline__ int t_dim(int t) { return D == 3 ? k3d::DIM[t] : k2d::DIM[t]; }
+// types of kind class c (0 = minima, 1 = 1-saddles, 2 = 2-saddles, 3 = maxima = top dimension)
+template <int D> __device__ __forceinline__ uint32_t t_dimclass_mask(int c) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int t = 0; t < Tr<D>::NT; t++) {
+    const int d = t_dim<D>(t);
+    m |= ((d == Tr<D>::TOP ? 3 : d) == c ? 1u : 0u) << t;
+  }
+  return m;
+}
 template <int D> __device__ __forceinline__ int t_nv(int t) { return D == 3 ? k3d::NV[t] : k2d::NV[t]; }
 template <int D> __device__ __forceinline__ int t_shift(int t) { return D == 3 ? k3d::SHIFT[t] : k2d::SHIFT[t]; }
 template <int D> __device__ __forceinline__ int t_none(int t) { return D == 3 ? k3d::NONE[t] : k2d::NONE[t]; }

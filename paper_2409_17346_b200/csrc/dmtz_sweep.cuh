@@ -290,29 +290,27 @@ __device__ __forceinline__ uint32_t mask_del(int m) { return 0x15u + (m & 1) + (
 template <int D>
 __device__ __forceinline__ uint32_t target_del(const TargetTables& T, int t, bool fn, uint64_t lowpos, uint64_t dp,
                                                const uint2* cfs, const uint2* cgs, int src) {
+  // straight-line (no divergence between the rules inside a warp): every operand is
+  // read, the rule is picked with selects
   const uint32_t ti = T.tinfo[t];
   const int dim = ti & 3, shift = (ti >> 5) & 63;
   const uint32_t none = (ti >> 11) & 15;
   // m = the cell's f-lowest vertex (SoS), precomputed per anchor and type
   const int mp = (int)(lowpos >> (2 * t)) & 3;
   const uint32_t m_del = mask_del((T.vm[t] >> (3 * mp)) & 7);
-  const bool has_cand = dim < Tr<D>::TOP;
-  if (!fn) {                                        // FP: paired in f, critical in g (R1)
-    const uint32_t sl = has_cand ? field2(cfs[src], shift, none) : none;
-    return sl != none ? T.ldel[t][sl] : m_del;      // paired up: its cofacet's vertex; down: m
-  }
-  if (has_cand && field2(cgs[src], shift, none) != none) return m_del;   // R2
-  // paired down in g with gamma = the facet j that points at it (R3a / R3b)
+  // R1 reads the f-pairing, R2 the g-pairing of the same cell
+  const uint32_t a = dim < Tr<D>::TOP ? field2(fn ? cgs[src] : cfs[src], shift, none) : none;
+  const uint32_t r1 = a != none ? (uint32_t)T.ldel[t][a < 14 ? a : 0] : m_del;   // FP: cofacet vertex or m
+  // R3a / R3b: paired down in g with gamma = the facet j that points at it
   const int j = (int)(dp >> (2 * t)) & 3;
   const uint32_t fc = T.fac[t][j];
   const int dm = fc & 7, ft = (fc >> 3) & 31, k = (fc >> 12) & 3;
-  if (mp != k) return m_del;                        // R3a: y = the vertex gamma omits != m
   const uint32_t fti = T.tinfo[ft];
-  const int fsh = (fti >> 5) & 63;
   const uint32_t fno = (fti >> 11) & 15;
-  const uint32_t s2 = field2(cfs[dm * 32 + src], fsh, fno);   // R3b: gamma's f-pair vertex
-  if (s2 == fno) return 0xFFFFFFFFu;
-  return mask_del(dm) + T.ldel[ft][s2] - 0x15u;
+  const uint32_t s2 = field2(cfs[dm * 32 + src], (fti >> 5) & 63, fno);     // gamma's f-pair vertex
+  const uint32_t r3b = s2 != fno ? mask_del(dm) + T.ldel[ft][s2 < 14 ? s2 : 0] - 0x15u : 0xFFFFFFFFu;
+  const uint32_t r3 = mp != k ? m_del : r3b;      // R3a: y = the vertex gamma omits != m
+  return !fn ? r1 : (a != none ? m_del : r3);     // R2: paired up in g -> m
 }
 
 // ---------------------------------------------------------------------------
@@ -465,6 +463,14 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
       }
       if (!__any_sync(0xffffffffu, diff != 0)) continue;  // warp-uniform
       if (diff) atomicOr(&W.fm[o >> 5], 1u << (o & 31));
+      if (count_kinds && counted) {  // round 1: false cells by (dim class, FP / FN)
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          const uint32_t cls = (uint32_t)t_dimclass_mask<D>(k >> 1);
+          const uint32_t n = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(diff & cls & ((k & 1) ? critf : ~critf)));
+          if (lane == k) kacc += n;
+        }
+      }
       // work list of the false cells (slot, type): all lanes then share them
       const int nmine = __popc(diff);
       if (counted) nfalse += nmine;
@@ -502,15 +508,6 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
         const int item = live ? W.items[i] : 0;
         const int src = item & 31, t = item >> 5;
         const bool fn = (W.critf[src] >> t) & 1u;
-        if (count_kinds && counted) {
-          const int dim = T.tinfo[t] & 3;
-          const int key = live ? 2 * ((dim == Tr<D>::TOP) ? 3 : dim) + (fn ? 1 : 0) : 8;
-#pragma unroll
-          for (int k = 0; k < 8; k++) {
-            const unsigned bk = __ballot_sync(0xffffffffu, key == k);
-            if (lane == k) kacc += __popc(bk);
-          }
-        }
         if (!live) continue;
         const uint32_t del = target_del<D>(T, t, fn, W.lowpos[src], W.dp[src], W.cf, W.cg, src);
         if (del == 0xFFFFFFFFu) { nint++; continue; }
