@@ -577,47 +577,66 @@ __global__ void k_edit_rows(uint32_t* __restrict__ tbits, int64_t nwords, const 
     uint32_t word = wi < w_end ? tbits[wi] : 0u;
     if (word) tbits[wi] = 0;
     unsigned nz = __ballot_sync(0xffffffffu, word != 0);
+    // two target words per pass: their loads are independent, one memory round trip for both
     while (nz) {
-      const int src = __ffs(nz) - 1;
+      int src[2];
+      src[0] = __ffs(nz) - 1;
       nz &= nz - 1;
-      const uint32_t wv = __shfl_sync(0xffffffffu, word, src);
-      // row-padded target bitmap: word = (z * ny + y) * wpr + x / 32; all its targets share (y, z)
-      const int64_t wrow = (base + src) / rg.wpr;
-      const int64_t vy = wrow % g.ny, vz = wrow / g.ny;
-      if (next_frontier && lane < 8) {  // the units meeting (y, z) + [-2, 1]: <= 4 planes x 2 row blocks
-        const int64_t y0 = vy >= 2 ? vy - 2 : 0, y1 = vy + 1 < g.ny ? vy + 1 : g.ny - 1;
-        const int64_t zz = (vz >= 2 ? vz - 2 : 0) + (lane >> 1), z1 = vz + 1 < g.nz ? vz + 1 : g.nz - 1;
-        const int64_t b = y0 / UY + (lane & 1);
-        if (zz <= z1 && b <= y1 / UY) {
-          const int64_t unit = zz * rg.ub + b;
-          if (use_smem) atomicOr(sfr + ((unit >> 5) - fw0), 1u << (unit & 31));
-          else atomicOr(next_frontier + (unit >> 5), 1u << (unit & 31));
+      src[1] = nz ? __ffs(nz) - 1 : -1;
+      if (nz) nz &= nz - 1;
+      uint32_t st[2] = {0u, 0u};
+      float fh[2] = {0.f, 0.f}, lbv[2] = {0.f, 0.f};
+      int64_t v[2] = {0, 0};
+      bool mine[2];
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int sw = src[h] < 0 ? src[0] : src[h];
+        const uint32_t wv = __shfl_sync(0xffffffffu, word, sw);
+        mine[h] = src[h] >= 0 && ((wv >> lane) & 1u);
+        if (src[h] < 0) continue;  // warp-uniform
+        // row-padded target bitmap: word = (z * ny + y) * wpr + x / 32; all its targets share (y, z)
+        const int64_t wrow = (base + sw) / rg.wpr;
+        const int64_t vy = wrow % g.ny, vz = wrow / g.ny;
+        if (next_frontier && lane < 8) {  // the units meeting (y, z) + [-2, 1]: <= 4 planes x 2 row blocks
+          const int64_t y0 = vy >= 2 ? vy - 2 : 0, y1 = vy + 1 < g.ny ? vy + 1 : g.ny - 1;
+          const int64_t zz = (vz >= 2 ? vz - 2 : 0) + (lane >> 1), z1 = vz + 1 < g.nz ? vz + 1 : g.nz - 1;
+          const int64_t b = y0 / UY + (lane & 1);
+          if (zz <= z1 && b <= y1 / UY) {
+            const int64_t unit = zz * rg.ub + b;
+            if (use_smem) atomicOr(sfr + ((unit >> 5) - fw0), 1u << (unit & 31));
+            else atomicOr(next_frontier + (unit >> 5), 1u << (unit & 31));
+          }
+        }
+        if (mine[h]) {
+          v[h] = ((base + sw) - wrow * rg.wpr) * 32 + lane + vy * g.sy + vz * g.sz;
+          st[h] = state[v[h]];
+          fh[h] = __ldg(fhat + v[h]);
+          lbv[h] = __ldg(lb + v[h]);
         }
       }
-      bool ch = false;
-      if ((wv >> lane) & 1u) {
-        const int64_t vx = ((base + src) - wrow * rg.wpr) * 32 + lane;
-        const int64_t v = vx + vy * g.sy + vz * g.sz;
-        targets++;
-        const uint32_t st = state[v];
-        if (!(st >> 16)) {  // lossless targets are no-ops, but their cells stay in the frontier
-          ch = true;
-          changed++;
-          const uint32_t q = st & 0xFFFFu;
-          bool done = false;
-          if ((int)q + 1 <= q_cap) {
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        bool ch = false;
+        if (mine[h]) {
+          targets++;
+          if (!(st[h] >> 16)) {  // lossless targets are no-ops, but their cells stay in the frontier
+            ch = true;
+            changed++;
+            const uint32_t q = st[h] & 0xFFFFu;
             // g' = RN(fhat - RN((q+1) * step)): two roundings, never fused
-            const float gp = __fsub_rn(fhat[v], __fmul_rn((float)(q + 1), step));
-            if (gp >= lb[v]) { state[v] = q + 1; gf[v] = gp; done = true; }
-          }
-          if (!done) {
-            gf[v] = lb[v];              // clamp to the lower bound, stored losslessly
-            state[v] = q | (1u << 16);
+            const float gp = __fsub_rn(fh[h], __fmul_rn((float)(q + 1), step));
+            if ((int)q + 1 <= q_cap && gp >= lbv[h]) {
+              state[v[h]] = q + 1;
+              gf[v[h]] = gp;
+            } else {
+              gf[v[h]] = lbv[h];        // clamp to the lower bound, stored losslessly
+              state[v[h]] = q | (1u << 16);
+            }
           }
         }
+        const unsigned cb = __ballot_sync(0xffffffffu, ch);
+        if (vcur && lane == 0 && cb) atomicOr(vcur + base + src[h], cb);   // same row-padded word index
       }
-      const unsigned cb = __ballot_sync(0xffffffffu, ch);
-      if (vcur && lane == 0 && cb) atomicOr(vcur + base + src, cb);   // same row-padded word index
     }
   }
   warp_add(&cnt->n_changed, changed);
