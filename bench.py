@@ -45,8 +45,13 @@ sys.path.insert(0, ROOT)
 import dmtz_inputs as di  # noqa: E402
 
 METRIC = "C-loop Mvoxels/s per iteration"
-ALU_OPS_PER_ANCHOR = {3: 210, 2: 30}      # 2 x SoS compares per anchor (105 in 3D, 15 in 2D)
+ALU_OPS_PER_ANCHOR = {3: 210, 2: 30}      # k_screen: 2 x SoS compares per anchor (105 in 3D, 15 in 2D)
 BYTES_PER_ANCHOR = {3: 12, 2: 6}          # g f32 + stored code (u64 3D / u16 2D)
+# k_decode: per decoded anchor, crit(c) for every cell type = cand(c) == NONE (20 / 4 tests) and no
+# facet pointing at c (74 / 12 tests), each a field extract + compare (2 ops); per false cell, one
+# target rule R1 / R2 / R3 (three field tests + two selects, 6 ops)  -- DESIGN.md section 7
+DECODE_OPS_PER_ANCHOR = {3: 2 * (20 + 74), 2: 2 * (4 + 12)}
+RULE_OPS_PER_CELL = 6
 
 
 def _peaks():
@@ -60,7 +65,8 @@ def _ncu_traffic(kernel: str, workload: str):
     """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        e = d.get(workload, {}).get(kernel)
+        w = d.get(workload, {})
+        e = w.get(kernel + "@step") or w.get(kernel)   # mean over the step's launches, else one capture
         return e["dram_bytes"] if e else None
     except Exception:
         return None
@@ -225,6 +231,7 @@ def main():
             fr_t.append(e0.elapsed_time(e1))
         # once more with per-kernel CUDA events (host-driven rounds) for the roofline
         rp = step(full=True, profile=True)
+        rpd = step(profile=True)   # default mode, per-kernel events
     assert rfull.n_edits == r.n_edits and rfull.stats["rounds"] == r.stats["rounds"]
     ms = float(np.median(times))
     sweeps = int(np.median([s["sweeps"] for s in stats]))
@@ -233,25 +240,38 @@ def main():
     full_recompute = {"value": N * rfull.stats["sweeps"] / (fr_ms * 1e-3) / 1e6, "unit": "Mvoxels/s",
                       "ms_per_step": fr_ms, "mode": "full_sweeps=1: every code recomputed, every anchor classified"}
 
-    # roofline of the dominant kernel: k_screen on rounds that recompute every code, live CUDA events
+    # roofline of the dominant kernel of the default step (live CUDA events on the launching stream,
+    # one extra host-driven step): k_decode; k_screen's on the rounds that recompute every code
     peaks = _peaks()
     hbm = peaks.get("hbm_gbs") or 6650.0
     sm_mhz = peaks.get("sm_max_mhz") or 1965.0
+    alu_peak = 148 * 64 * sm_mhz * 1e6 / 1e9          # Gop/s: 148 SMs x 4 SMSP x 16-lane ALU pipe
+    workload = f"{cfg.name} {'x'.join(map(str, f.shape))}"
+    ds = rpd.stats
+    dec_ops = DECODE_OPS_PER_ANCHOR[D] * ds["anchors_decoded"] + RULE_OPS_PER_CELL * ds["cells_evaluated"]
+    dec_s = ds["decode_ms"] * 1e-3
+    dec_ach = dec_ops / dec_s / 1e9
+    roof = {"bound": "alu", "achieved": dec_ach, "peak": alu_peak, "unit": "Gop/s", "frac": dec_ach / alu_peak,
+            "traffic": _ncu_traffic("k_decode", workload),
+            "kernel": "k_decode (criticality of g, critical-cell diff, target rules; default step)",
+            "decode_ms_per_step": ds["decode_ms"], "screen_ms_per_step": ds["screen_ms"],
+            "share_of_step": ds["decode_ms"] / ms, "launches_per_step": ds["sweeps"],
+            "anchors_decoded": ds["anchors_decoded"], "cells_evaluated": ds["cells_evaluated"],
+            "anchors_replayed": ds["anchors_replayed"],
+            "ops_per_decoded_anchor": DECODE_OPS_PER_ANCHOR[D], "ops_per_false_cell": RULE_OPS_PER_CELL,
+            "peak_source": "ALU: 148 SMs x 64 lanes/clk x MEASURED_PEAKS sm_max_mhz (DESIGN.md section 7)",
+            "traffic_note": "ncu dram bytes per launch, mean over one step's launches (profiles/ncu_summary.json)"}
     ps = rp.stats
     t_launch = ps["screen_ms_full"] / max(ps["n_screen_full"], 1) * 1e-3
-    alu_peak = 148 * 64 * sm_mhz * 1e6 / 1e9          # Gop/s: 148 SMs x 4 SMSP x 16-lane ALU pipe
     alu_achieved = ALU_OPS_PER_ANCHOR[D] * N / t_launch / 1e9
     gbs = BYTES_PER_ANCHOR[D] * N / t_launch / 1e9
-    workload = f"{cfg.name} {'x'.join(map(str, f.shape))}"
-    traffic = _ncu_traffic("k_screen", workload)
-    roof = {"bound": "alu", "achieved": alu_achieved, "peak": alu_peak, "unit": "Gop/s",
-            "frac": alu_achieved / alu_peak, "traffic": traffic,
-            "kernel": "k_screen (gradient codes of g, every anchor recomputed)", "launch_ms": t_launch * 1e3,
-            "alu_ops_per_anchor": ALU_OPS_PER_ANCHOR[D], "bytes_per_anchor": BYTES_PER_ANCHOR[D],
-            "hbm_achieved_gbs": gbs, "hbm_peak_gbs": hbm, "hbm_frac": gbs / hbm,
-            "peak_source": ("ALU: 148 SMs x 64 lanes/clk x MEASURED_PEAKS sm_max_mhz; HBM: MEASURED_PEAKS hbm_gbs"),
-            "share_of_full_recompute_step": ps["screen_ms"] / fr_ms, "decode_ms_full_recompute": ps["decode_ms"],
-            "screen_ms_full_recompute": ps["screen_ms"]}
+    roof_screen = {"bound": "alu", "achieved": alu_achieved, "peak": alu_peak, "unit": "Gop/s",
+                   "frac": alu_achieved / alu_peak, "traffic": _ncu_traffic("k_screen", workload),
+                   "kernel": "k_screen (gradient codes of g, a launch that recomputes every anchor)",
+                   "launch_ms": t_launch * 1e3, "alu_ops_per_anchor": ALU_OPS_PER_ANCHOR[D],
+                   "bytes_per_anchor": BYTES_PER_ANCHOR[D], "hbm_achieved_gbs": gbs, "hbm_peak_gbs": hbm,
+                   "hbm_frac": gbs / hbm, "screen_ms_per_step": ds["screen_ms"],
+                   "share_of_step": ds["screen_ms"] / ms}
 
     # time-to-fixed-point (the second half of BASELINE's metric): the timed default step
     frontier = {"time_to_fixed_point_ms": ms, "rounds": r.stats["rounds"], "sweeps": r.stats["sweeps"],
@@ -324,7 +344,7 @@ def main():
                    "xi": xi, "q_max": 6, "q_cap": 6, "tier": 2, "sweeps_per_step": sweeps, "rounds": st["rounds"],
                    "mode": "default: dirty frontier + exact change skipping (bit-identical to full_sweeps=1)",
                    "l2": "inputs larger than L2 (2 x 537 MB)", "parallelism": "1 GPU"},
-        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "time_to_fixed_point": frontier,
+        "roofline": roof, "roofline_screen": roof_screen, "cpu_baseline": cpu, "e2e": e2e, "time_to_fixed_point": frontier,
         "full_recompute": full_recompute, "trace": trace,
         "gpu_launches": st["launches"],
         "clocks": clk.summary(),

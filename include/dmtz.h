@@ -118,6 +118,10 @@ typedef struct {
   int64_t n_screen_full;   /* number of such rounds */
   int64_t anchors_recomputed; /* sum over sweeps of anchors whose code was recomputed (the rest
                                  provably kept theirs: no vertex of their 3x3x3 box changed) */
+  int64_t anchors_decoded;    /* sum over sweeps of anchors whose criticality was decoded (a code of
+                                 u + {0,1}^D changed) */
+  int64_t cells_evaluated;    /* sum over sweeps of false cells whose target rule was evaluated */
+  int64_t anchors_replayed;   /* sum over sweeps of anchors whose unchanged targets were replayed */
 } dmtz_stats;
 
 typedef struct dmtz_ctx dmtz_ctx;

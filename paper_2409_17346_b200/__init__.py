@@ -51,7 +51,8 @@ class _Stats(ctypes.Structure):
                 ("pad", ctypes.c_int32), ("sweeps", ctypes.c_int64), ("anchors_swept", ctypes.c_int64),
                 ("launches", ctypes.c_int64), ("sweep_ms", ctypes.c_double), ("screen_ms", ctypes.c_double),
                 ("decode_ms", ctypes.c_double), ("screen_ms_full", ctypes.c_double), ("n_screen_full", ctypes.c_int64),
-                ("anchors_recomputed", ctypes.c_int64)]
+                ("anchors_recomputed", ctypes.c_int64), ("anchors_decoded", ctypes.c_int64),
+                ("cells_evaluated", ctypes.c_int64), ("anchors_replayed", ctypes.c_int64)]
 
 
 class _Seps(ctypes.Structure):
@@ -217,7 +218,8 @@ class Context:
                      status=status, sweeps=st.sweeps, anchors_swept=st.anchors_swept, launches=st.launches,
                      sweep_ms=st.sweep_ms, screen_ms=st.screen_ms, decode_ms=st.decode_ms,
                      screen_ms_full=st.screen_ms_full, n_screen_full=st.n_screen_full,
-                     anchors_recomputed=st.anchors_recomputed)
+                     anchors_recomputed=st.anchors_recomputed, anchors_decoded=st.anchors_decoded,
+                     cells_evaluated=st.cells_evaluated, anchors_replayed=st.anchors_replayed)
         msg = _lib.dmtz_last_error().decode() if status != OK else ""
         if raise_on_error and status not in (OK, E_STUCK, E_ITER_CAP, E_CAPACITY):
             raise DmtzError(status, msg)

@@ -409,6 +409,9 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
   st->sweeps = (int64_t)hls->sweeps;
   st->anchors_swept = (int64_t)hls->anchors_swept;
   st->anchors_recomputed = (int64_t)hls->recomputed;
+  st->anchors_decoded = (int64_t)hls->decoded;
+  st->cells_evaluated = (int64_t)hls->items;
+  st->anchors_replayed = (int64_t)hls->replayed;
   st->rounds = (int64_t)hls->rounds;
   st->n_false_round0 = (int64_t)hls->n_false0;
   for (int k = 0; k < 8; k++) st->false_by_kind_round0[k] = (int64_t)hls->kinds0[k];

@@ -25,13 +25,16 @@ struct Counters {                 // device-side round counters (one 256 B block
   unsigned long long n_internal;  // invariant violations (expected 0)
   unsigned long long n_swept;     // anchors evaluated by the round's sweep
   unsigned long long n_recomputed;  // of which their code was recomputed (stencil changed)
+  unsigned long long n_decoded;   // anchors whose criticality was decoded this round
+  unsigned long long n_items;     // false cells whose target rule was evaluated this round
+  unsigned long long n_replayed;  // anchors whose cached targets were replayed this round
   unsigned long long first_nonfinite;
   unsigned long long first_bound;
   unsigned long long n_edits;
   unsigned long long n_lossless;  // lossless entries of the edit list
   unsigned long long n_units;     // active units of the current round (frontier list length)
   unsigned long long n_units2;    // slab mode: units whose cells are classified
-  unsigned long long pad[12];
+  unsigned long long pad[9];
 };
 static_assert(sizeof(Counters) == 256, "counters are one 256 B block");
 
@@ -47,7 +50,8 @@ struct LoopState {
   unsigned long long status;         // dmtz_status of the loop (0 while running / OK)
   unsigned long long last_false, last_changed, last_targets, last_swept;
   unsigned long long recomputed;     // anchors whose code was recomputed, summed over sweeps
-  unsigned long long pad[13];
+  unsigned long long decoded, items, replayed;  // k_decode work, summed over sweeps
+  unsigned long long pad[10];
 };
 static_assert(sizeof(LoopState) == 256, "loop state is one 256 B block");
 
@@ -87,6 +91,9 @@ __global__ void k_loop_check(Counters* cnt, LoopState* ls, unsigned long long ma
   ls->sweeps++;
   ls->anchors_swept += cnt->n_swept;
   ls->recomputed += cnt->n_recomputed;
+  ls->decoded += cnt->n_decoded;
+  ls->items += cnt->n_items;
+  ls->replayed += cnt->n_replayed;
   ls->last_false = cnt->n_false;
   ls->last_changed = cnt->n_changed;
   ls->last_targets = cnt->n_targets;

@@ -380,7 +380,7 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
   DecodeWarpSmem& W = WS[threadIdx.x >> 5];
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long nfalse = 0, nint = 0;
+  unsigned long long nfalse = 0, nint = 0, c_dec = 0, c_items = 0, c_rep = 0;
   unsigned int kacc = 0;  // round 1: lane k < 8 counts false cells of kind k
   const uint32_t n_units_ = (uint32_t)*n_units_p;
   const uint32_t ngr = (uint32_t)((rg.wpr + DG - 1) / DG);
@@ -424,6 +424,7 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
         if (b0 + lane < n) {
           const int o = W.list[b0 + lane];
           const int64_t u = row0 + o;
+          c_rep++;
           unsigned long long tmc = tcache[u];
           if (counted) nfalse += ncache[u];
           while (tmc) {
@@ -460,6 +461,7 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
         const uint32_t cgm = decode_crit_dp<D>(cgv, ok, &dp);
         critf = __ldg(crit_f + u);
         diff = (critf ^ cgm) & tier_mask;
+        c_dec++;
       }
       if (!__any_sync(0xffffffffu, diff != 0)) continue;  // warp-uniform
       if (diff) atomicOr(&W.fm[o >> 5], 1u << (o & 31));
@@ -474,6 +476,7 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
       // work list of the false cells (slot, type): all lanes then share them
       const int nmine = __popc(diff);
       if (counted) nfalse += nmine;
+      c_items += nmine;
       int pre = nmine;
 #pragma unroll
       for (int k = 1; k < 32; k <<= 1) {
@@ -538,6 +541,9 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
   }
   warp_add(&cnt->n_false, nfalse);
   warp_add(&cnt->n_internal, nint);
+  warp_add(&cnt->n_decoded, c_dec);
+  warp_add(&cnt->n_items, c_items);
+  warp_add(&cnt->n_replayed, c_rep);
   if (count_kinds && lane < 8 && kacc) atomicAdd(&cnt->kinds[lane], (unsigned long long)kacc);
 }
 
