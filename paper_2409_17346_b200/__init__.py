@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdmtz.so")
+LIB_PATH = os.environ.get("DMTZ_LIB") or os.path.join(_HERE, "libdmtz.so")   # DMTZ_LIB: experiment builds
 
 
 OK, E_ARG, E_DIMS, E_NONFINITE, E_BOUND, E_CAPACITY, E_ITER_CAP, E_STUCK, E_CUDA, E_NCCL, E_OOM, \

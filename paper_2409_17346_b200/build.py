@@ -36,8 +36,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if force or _stale():
         nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
         extra = os.environ.get("DMTZ_NVCC_EXTRA", "").split()  # e.g. -DDMTZ_INSTR (instrumented build)
+        out = os.environ.get("DMTZ_LIB_OUT", LIB)                # variant builds for experiments
         cmd = [nvcc] + NVCC_FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + \
-              ["-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES]
+              ["-o", out] + [os.path.join(CSRC, s) for s in SOURCES]
         subprocess.check_call(cmd, cwd=CSRC)
     return LIB
 

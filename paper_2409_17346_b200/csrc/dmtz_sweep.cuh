@@ -329,8 +329,8 @@ __device__ __forceinline__ uint32_t target_del(const TargetTables& T, int t, boo
 constexpr int DECODE_THREADS = 128;
 constexpr int TWW = DG + 2;             // window words per row
 struct DecodeWarpSmem {
-  uint2 cf[8 * 32];
-  uint2 cg[8 * 32];
+  uint2 cf[8 * 32];            // per slot: f codes of u + {0,1}^D
+  uint2 cg[32];                // per slot: g code of u
   unsigned long long lowpos[32];
   unsigned long long dp[32];
   unsigned long long tm[32];   // per slot: target offsets of its false cells (bit = packed delta)
@@ -362,8 +362,11 @@ __device__ __forceinline__ int compact_group(uint32_t m, int lane, uint16_t* lis
   return total;
 }
 
+#ifndef DMTZ_DECODE_MINB
+#define DMTZ_DECODE_MINB 8
+#endif
 template <int D>
-__global__ void __launch_bounds__(DECODE_THREADS, 6)
+__global__ void __launch_bounds__(DECODE_THREADS, DMTZ_DECODE_MINB)
 k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__ cand_f,
          const uint32_t* __restrict__ crit_f, const typename Tr<D>::code_t* __restrict__ cg,
          const uint32_t* __restrict__ ebits, uint32_t* __restrict__ fmark,
@@ -445,19 +448,15 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
       const int64_t x = cbase * 32 + o;
       const int64_t u = row0 + o;
       uint32_t diff = 0, critf = 0;
-      uint64_t dp = 0;
-      uint64_t cf[Tr<D>::NDELTA], cgv[Tr<D>::NDELTA];
-#pragma unroll
-      for (int dm = 0; dm < Tr<D>::NDELTA; dm++) cf[dm] = cgv[dm] = Tr<D>::ALL_NONE;
+      uint64_t dp = 0, cg0 = 0;
+      int ok = 0;
       if (act) {
-        const int ok = axes_ok(g, x, y, z);
+        uint64_t cgv[Tr<D>::NDELTA];
+        ok = axes_ok(g, x, y, z);
 #pragma unroll
-        for (int dm = 0; dm < Tr<D>::NDELTA; dm++) {
-          if ((dm & ~ok) != 0) continue;
-          const int64_t w = u + mask_delta(g, dm);
-          cf[dm] = (uint64_t)__ldg(cand_f + w);
-          cgv[dm] = (uint64_t)__ldg(cg + w);
-        }
+        for (int dm = 0; dm < Tr<D>::NDELTA; dm++)
+          cgv[dm] = (dm & ~ok) == 0 ? (uint64_t)__ldg(cg + u + mask_delta(g, dm)) : Tr<D>::ALL_NONE;
+        cg0 = cgv[0];
         const uint32_t cgm = decode_crit_dp<D>(cgv, ok, &dp);
         critf = __ldg(crit_f + u);
         diff = (critf ^ cgm) & tier_mask;
@@ -486,12 +485,13 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
       const int total = __shfl_sync(0xffffffffu, pre, 31);
       pre -= nmine;
       W.tm[lane] = 0ull;
-      if (diff) {
+      if (diff) {  // the f codes are read only for anchors with false cells
 #pragma unroll
         for (int dm = 0; dm < Tr<D>::NDELTA; dm++) {
-          W.cf[dm * 32 + lane] = make_uint2((uint32_t)cf[dm], (uint32_t)(cf[dm] >> 32));
-          W.cg[dm * 32 + lane] = make_uint2((uint32_t)cgv[dm], (uint32_t)(cgv[dm] >> 32));
+          const uint64_t cfv = (dm & ~ok) == 0 ? (uint64_t)__ldg(cand_f + u + mask_delta(g, dm)) : Tr<D>::ALL_NONE;
+          W.cf[dm * 32 + lane] = make_uint2((uint32_t)cfv, (uint32_t)(cfv >> 32));
         }
+        W.cg[lane] = make_uint2((uint32_t)cg0, (uint32_t)(cg0 >> 32));
         W.critf[lane] = critf;
         W.dp[lane] = dp;
         W.lowpos[lane] = __ldg(lowpos_f + u);
