@@ -284,74 +284,11 @@ __device__ int64_t walk_asc(const void* codes, const Grid& g, int64_t a, int t, 
   return n;
 }
 
-// Connector BFS from critical triangle (a, t), private queue + visited hash set.
-// Returns the event count, -2 if the scratch slot was too small, -1 on error.
 template <int D>
-__device__ int64_t bfs_conn(const void* codes, const uint32_t* __restrict__ crit, const Grid& g, int64_t a, int t,
-                            bool write, uint64_t* cells, unsigned long long* queue, int64_t qcap,
-                            unsigned long long* hset, int64_t hcap /* power of 2 */) {
-  // hset starts all-zero; every inserted key is also in the queue, and the
-  // clean-up below removes exactly those, so the slot is zero again on exit
-  auto key = [](int64_t an, int ty) { return (unsigned long long)(an * 32 + ty) + 1ull; };
-  auto slot_of = [&](unsigned long long k) { return (k * 0x9E3779B97F4A7C15ull) >> 20; };
-  auto insert = [&](unsigned long long k) -> int {  // 1 inserted, 0 present, -1 full
-    const unsigned long long h = slot_of(k);
-    for (int64_t p = 0; p < hcap / 2; p++) {
-      const int64_t i = (int64_t)((h + p) & (unsigned long long)(hcap - 1));
-      if (hset[i] == k) return 0;
-      if (hset[i] == 0ull) { hset[i] = k; return 1; }
-    }
-    return -1;
-  };
-  int64_t head = 0, tail = 0, n = 0, result = 0;
-  queue[tail++] = key(a, t);
-  insert(key(a, t));
-  while (head < tail && result == 0) {
-    const unsigned long long cur = queue[head++] - 1ull;
-    const int64_t B = (int64_t)(cur / 32);
-    const int bt = (int)(cur % 32);
-    for (int j = 0; j < t_nfacet<D>(bt); j++) {
-      const int dm = t_facet<D>(bt, j, 0), et = t_facet<D>(bt, j, 1);
-      const int64_t E = B + mask_delta(g, dm);
-      if ((crit[E] >> et) & 1u) {  // critical edge: a reached 1-saddle
-        if (write) cells[n] = cell_id<D>(E, et);
-        n++;
-        continue;
-      }
-      const uint32_t s = field_of<D>(code_at<D>(codes, E), et);
-      if (s == (uint32_t)t_none<D>(et)) continue;  // paired down with a vertex: the path stops
-      const int64_t Nb = cof_anchor<D>(g, E, et, (int)s);
-      const int nt = t_cof_type<D>(et, (int)s);
-      if (Nb == B && nt == bt) continue;
-      if (tail >= qcap) { result = -2; break; }
-      const int ins = insert(key(Nb, nt));
-      if (ins < 0) { result = -2; break; }
-      if (ins == 0) continue;
-      if (write) cells[n] = cell_id<D>(Nb, nt);
-      n++;
-      queue[tail++] = key(Nb, nt);
-    }
-  }
-  // clean the visited set in reverse insertion order: linear-probing chains of the
-  // keys still present stay intact, so every key is found and removed
-  for (int64_t q = tail - 1; q >= 0; q--) {
-    const unsigned long long k = queue[q], h = slot_of(k);
-    for (int64_t p = 0; p < hcap; p++) {
-      const int64_t i = (int64_t)((h + p) & (unsigned long long)(hcap - 1));
-      if (hset[i] == k) { hset[i] = 0ull; break; }
-      if (hset[i] == 0ull) break;
-    }
-  }
-  return result ? result : n;
-}
-
-template <int D>
-__global__ void k_walk(const void* codes, const uint32_t* __restrict__ crit, Grid g, int64_t b0, int64_t nb,
+__global__ void k_walk(const void* codes, Grid g, int64_t b0, int64_t nb,
                        const uint64_t* __restrict__ origin, const uint8_t* __restrict__ kind,
                        uint64_t* __restrict__ jterm, long long* __restrict__ off, uint64_t* __restrict__ cells,
-                       bool write, unsigned long long* __restrict__ scratch, int64_t slot_q, int64_t slot_h,
-                       int64_t nslots, int* __restrict__ overflow, int64_t conn_base,
-                       Counters* __restrict__ cnt) {
+                       bool write, Counters* __restrict__ cnt) {
   const int64_t cap_steps = g.N * 26 + 1;
   for (int64_t b = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
        b += (int64_t)gridDim.x * blockDim.x) {
@@ -364,20 +301,80 @@ __global__ void k_walk(const void* codes, const uint32_t* __restrict__ crit, Gri
     uint64_t term = CELL_BOUNDARY;
     if (k == 1) n = walk_desc<D>(codes, g, a, t, (int)jterm[b], write, out, &term, cap_steps);
     else if (k == 2) n = walk_asc<D>(codes, g, a, t, (int)jterm[b], write, out, &term, cap_steps);
-    else {
-      // connector: slots are handed out per thread; overflowing saddles go to the big pass
-      const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // < nslots by launch
-      unsigned long long* q = scratch + slot * (slot_q + slot_h);
-      n = bfs_conn<D>(codes, crit, g, a, t, write, out, q, slot_q, q + slot_q, slot_h);
-      if (n == -2) {  // overflow bit of connector branch b - conn_base
-        const int64_t cb = b - conn_base;
-        atomicOr((unsigned int*)overflow + (cb >> 5), 1u << (cb & 31));
-        continue;
-      }
-    }
+    else n = -1;  // connectors run in k_conn_small / k_walk_block
     if (n < 0) { atomicAdd(&cnt->n_internal, 1ull); n = 0; }
     if (!write) off[b] = n;
     else jterm[b] = term;
+  }
+}
+
+// Connector BFS, small case: one thread per 2-saddle, its queue (= its visited set:
+// every visited triangle is enqueued exactly once) in shared memory, keys relative
+// to the origin anchor (7 bits per axis + type; BFS depth <= CQ bounds the offsets),
+// membership by a linear scan.  Saddles that reach more than CQ triangles set their
+// overflow bit and go to the block-parallel pass.
+#ifndef DMTZ_CQ
+#define DMTZ_CQ 64
+#endif
+constexpr int CQ = DMTZ_CQ;
+constexpr int CONN_THREADS = 128;
+template <int D>
+__global__ void __launch_bounds__(CONN_THREADS)
+k_conn_small(const void* codes, const uint32_t* __restrict__ crit, Grid g, int64_t b0, int64_t nb,
+             const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm, long long* __restrict__ off,
+             uint64_t* __restrict__ cells, bool write, unsigned int* __restrict__ overflow, int64_t conn_base) {
+  __shared__ uint32_t sq[CQ][CONN_THREADS];
+  uint32_t* q = &sq[0][threadIdx.x];   // q[k * CONN_THREADS]: conflict-free columns
+  auto key = [](int dx, int dy, int dz, int ty) {
+    return (uint32_t)(dx + 64) | ((uint32_t)(dy + 64) << 7) | ((uint32_t)(dz + 64) << 14) | ((uint32_t)ty << 21);
+  };
+  for (int64_t b = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a;
+    int t;
+    id_cell<D>(origin[b], a, t);
+    uint64_t* out = write ? cells + off[b] : nullptr;
+    int head = 0, tail = 1;
+    int64_t n = 0;
+    bool ovf = false;
+    q[0] = key(0, 0, 0, t);
+    while (head < tail && !ovf) {
+      const uint32_t cur = q[(head++) * CONN_THREADS];
+      const int bx = (int)(cur & 127) - 64, by = (int)((cur >> 7) & 127) - 64, bz = (int)((cur >> 14) & 127) - 64;
+      const int bt = (int)(cur >> 21);
+      const int64_t B = a + bx + by * g.sy + bz * g.sz;
+      for (int j = 0; j < t_nfacet<D>(bt); j++) {
+        const int dm = t_facet<D>(bt, j, 0), et = t_facet<D>(bt, j, 1);
+        const int64_t E = B + mask_delta(g, dm);
+        if ((__ldg(crit + E) >> et) & 1u) {  // critical edge: a reached 1-saddle
+          if (write) out[n] = cell_id<D>(E, et);
+          n++;
+          continue;
+        }
+        const uint32_t s = field_of<D>(code_at<D>(codes, E), et);
+        if (s == (uint32_t)t_none<D>(et)) continue;  // paired down with a vertex: the path stops
+        const int nt = t_cof_type<D>(et, (int)s);
+        const int ex = bx + (dm & 1), ey = by + ((dm >> 1) & 1), ez = bz + ((dm >> 2) & 1);
+        const int nx_ = ex + t_cof_anchor<D>(et, (int)s, 0), ny_ = ey + t_cof_anchor<D>(et, (int)s, 1),
+                  nz_ = ez + t_cof_anchor<D>(et, (int)s, 2);
+        const uint32_t k = key(nx_, ny_, nz_, nt);
+        if (k == cur) continue;
+        bool seen = false;
+        for (int i = 0; i < tail; i++) seen |= q[i * CONN_THREADS] == k;
+        if (seen) continue;
+        if (tail == CQ) { ovf = true; break; }
+        q[(tail++) * CONN_THREADS] = k;
+        if (write) out[n] = cell_id<D>(a + nx_ + ny_ * g.sy + nz_ * g.sz, nt);
+        n++;
+      }
+    }
+    if (ovf) {
+      const int64_t cb = b - conn_base;
+      atomicOr(overflow + (cb >> 5), 1u << (cb & 31));
+      continue;
+    }
+    if (!write) off[b] = n;
+    else jterm[b] = CELL_BOUNDARY;
   }
 }
 
@@ -388,7 +385,6 @@ __global__ void k_walk(const void* codes, const uint32_t* __restrict__ crit, Gri
 // occurrence in (entry, facet) order within the batch -- decided by an atomic
 // max of ~(batch << 32 | candidate) on the visited slot's owner word.  A block
 // scan then places events and new queue entries in that order.
-constexpr int BFS_THREADS = 256;
 
 __device__ __forceinline__ int64_t bfs_find_or_insert(unsigned long long* keys, int64_t hcap, unsigned long long k) {
   const unsigned long long h = (k * 0x9E3779B97F4A7C15ull) >> 20;
@@ -439,14 +435,14 @@ __global__ void k_bits_compact(uint32_t* __restrict__ bits, int64_t w0, int64_t 
   }
 }
 
-template <int D>
+template <int D, int BFS_THREADS>
 __global__ void __launch_bounds__(BFS_THREADS)
 k_walk_block(const void* codes, const uint32_t* __restrict__ crit, Grid g, const uint32_t* __restrict__ list,
              int64_t nlist, int64_t conn_base, const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
              long long* __restrict__ off, uint64_t* __restrict__ cells, bool write,
              unsigned long long* __restrict__ scratch, int64_t qcap, int64_t hcap,
              unsigned int* __restrict__ overflow, Counters* __restrict__ cnt) {
-  __shared__ int s_warp[BFS_THREADS / 32];
+  __shared__ int s_warp[32];
   __shared__ int s_flag;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   unsigned long long* queue = scratch + (int64_t)blockIdx.x * (qcap + 2 * hcap);
@@ -645,35 +641,27 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   unsigned long long* sc = A.bfs;
   const int64_t words = (int64_t)(A.bfs_bytes / 8);
   // a connector visits at most the 12 N triangles; small grids get small slots
-  const int64_t slot_q = 12 * g.N + 16 < 64 ? 12 * g.N + 16 : 64;
-  int64_t slot_h = 1;
-  while (slot_h < 2 * slot_q) slot_h *= 2;
+  const int64_t slot_q = CQ;  // level 0: k_conn_small's shared-memory queues
   const int threads = 128;
-  int64_t nslots = words / (slot_q + slot_h);
-  if (nslots > 148 * 2048) nslots = 148 * 2048;  // one slot per resident thread
-  nslots = nslots / threads * threads;
   const int64_t conn_base = nbk[0] + nbk[1];
   const int64_t ovf_words = (nbk[2] + 31) / 32;
   const int64_t pre_words = (int64_t)(A.pre_bytes / 8);
   if (nbk[2] && (ovf_words + 2) * 4 + 64 * 8 > pre_words * 8) return cudaErrorMemoryAllocation;
   const int64_t list_cap = (pre_words * 8 - (ovf_words + 2) * 4) / 4;
-  if (nbk[2] && nslots < threads) return cudaErrorMemoryAllocation;
   const int64_t blocks_path = conn_base > 0 ? (conn_base + threads - 1) / threads : 0;
-  int64_t blocks_conn = (nbk[2] + threads - 1) / threads;
-  if (blocks_conn * threads > nslots) blocks_conn = nslots / threads;
   long long* off = (long long*)A.out_offsets;
-  TCK(cudaMemsetAsync(sc, 0, A.bfs_bytes, s));
   for (int pass = 0; pass < 2; pass++) {
     const bool write = pass == 1;
     TCK(cudaMemsetAsync(ovf, 0, (size_t)ovf_words * 4 + 4, s));
     if (blocks_path)  // descending / ascending paths: one thread per branch
-      k_walk<D><<<(unsigned)blocks_path, threads, 0, s>>>(A.codes, A.crit, g, 0, conn_base, A.out_origin, A.out_kind,
-                                                          A.out_terminal, off, A.out_cells, write, sc, slot_q,
-                                                          slot_h, nslots, ovf, conn_base, dc);
-    if (blocks_conn)  // connectors: one scratch slot per thread
-      k_walk<D><<<(unsigned)blocks_conn, threads, 0, s>>>(A.codes, A.crit, g, conn_base, nb, A.out_origin, A.out_kind,
-                                                          A.out_terminal, off, A.out_cells, write, sc, slot_q,
-                                                          slot_h, nslots, ovf, conn_base, dc);
+      k_walk<D><<<(unsigned)blocks_path, threads, 0, s>>>(A.codes, g, 0, conn_base, A.out_origin, A.out_kind,
+                                                          A.out_terminal, off, A.out_cells, write, dc);
+    if (nbk[2]) {  // connectors: one thread per 2-saddle, small queues in shared memory
+      const int64_t nbc = (nbk[2] + CONN_THREADS - 1) / CONN_THREADS;
+      k_conn_small<D><<<(unsigned)(nbc < 148 * 64 ? nbc : 148 * 64), CONN_THREADS, 0, s>>>(
+          A.codes, A.crit, g, conn_base, nb, A.out_origin, A.out_terminal, off, A.out_cells, write,
+          (unsigned int*)ovf, conn_base);
+    }
     TCK(cudaGetLastError());
     if (nbk[2]) {  // connectors that outgrew their slot: retry with 16x bigger slots, fewer threads
       // the overflow bitmask is compacted into a list on the device, in word chunks that fit the list area
@@ -718,15 +706,14 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
           if (A.verbose)
             fprintf(stderr, "dmtz trace pass %d level %d: %lld connectors, q %lld, %lld blocks\n", pass, level + 1,
                     (long long)cn, (long long)qn, (long long)nblk);
-          k_walk_block<D><<<(unsigned)nblk, BFS_THREADS, 0, s>>>(A.codes, A.crit, g, dlist, cn, conn_base,
-                                                                 A.out_origin, A.out_terminal, off, A.out_cells,
-                                                                 write, sc, qn, h, (unsigned int*)ovf, dc);
+          k_walk_block<D, 256><<<(unsigned)nblk, 256, 0, s>>>(A.codes, A.crit, g, dlist, cn, conn_base,
+                                                              A.out_origin, A.out_terminal, off, A.out_cells,
+                                                              write, sc, qn, h, (unsigned int*)ovf, dc);
           TCK(cudaGetLastError());
         }
         if (!any) break;
         q = qn;
       }
-      TCK(cudaMemsetAsync(sc, 0, A.bfs_bytes, s));
     }
     if (!write) {
       TCK(cudaMemsetAsync(off + nb, 0, 8, s));
