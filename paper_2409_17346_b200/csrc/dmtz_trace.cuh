@@ -378,6 +378,146 @@ k_conn_small(const void* codes, const uint32_t* __restrict__ crit, Grid g, int64
   }
 }
 
+// Connector BFS, mid-size case: one warp per 2-saddle, queue (WQ entries) and a
+// visited hash set (WH slots) in shared memory.  Same batch rule as the block
+// kernel below (the batch = the next <= 32 queue entries; a discovered triangle is
+// new iff it was not seen before the batch and this is its first occurrence in
+// (entry, facet) order, decided by an atomicMin of batch << 7 | candidate on its
+// slot's owner word), so the events come out in the sequential FIFO order.
+constexpr int WQ = 512, WH = 1024, CONNW_WARPS = 4;
+constexpr size_t CONNW_SMEM = (size_t)CONNW_WARPS * (WQ * 8 + WH * 8 + WH * 4);
+template <int D>
+__global__ void __launch_bounds__(CONNW_WARPS * 32)
+k_conn_warp(const void* codes, const uint32_t* __restrict__ crit, Grid g, const uint32_t* __restrict__ list,
+            int64_t nlist, int64_t conn_base, const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
+            long long* __restrict__ off, uint64_t* __restrict__ cells, bool write,
+            unsigned int* __restrict__ overflow) {
+  extern __shared__ unsigned long long smw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long* queue = smw + (size_t)wid * (WQ + WH + WH / 2);
+  unsigned long long* keys = queue + WQ;
+  uint32_t* owner = (uint32_t*)(keys + WH);
+  for (int i = lane; i < WH; i += 32) { keys[i] = 0ull; owner[i] = 0xFFFFFFFFu; }
+  __syncwarp();
+  auto key = [](int64_t an, int ty) { return (unsigned long long)(an * 32 + ty) + 1ull; };
+  auto hslot = [](unsigned long long k) { return (int)((k * 0x9E3779B97F4A7C15ull) >> 54); };  // 10 bits
+  auto find_or_insert = [&](unsigned long long k) -> int {
+    const int h = hslot(k);
+    for (int p = 0; p < WH / 2; p++) {
+      const int i = (h + p) & (WH - 1);
+      const unsigned long long v = atomicCAS(keys + i, 0ull, k);
+      if (v == 0ull || v == k) return i;
+    }
+    return -1;
+  };
+  for (int64_t li = (int64_t)blockIdx.x * CONNW_WARPS + wid; li < nlist; li += (int64_t)gridDim.x * CONNW_WARPS) {
+    const int64_t cb = list[li], b = conn_base + cb;
+    int64_t a0;
+    int t0;
+    id_cell<D>(origin[b], a0, t0);
+    uint64_t* out = write ? cells + off[b] : nullptr;
+    if (lane == 0) {
+      queue[0] = key(a0, t0);
+      owner[find_or_insert(key(a0, t0))] = 0u;  // seen before every batch
+    }
+    __syncwarp();
+    int head = 0, tail = 1;
+    int64_t nev = 0;
+    uint32_t batch = 1;
+    bool ovf = false;
+    while (head < tail) {
+      const int K = tail - head < 32 ? tail - head : 32;
+      int ckind[3] = {0, 0, 0}, cslot[3] = {-1, -1, -1};
+      uint64_t cid[3] = {0, 0, 0};
+      unsigned long long ckey[3] = {0, 0, 0};
+      bool bad = false;
+      if (lane < K) {
+        const unsigned long long cur = queue[head + lane] - 1ull;
+        const int64_t B = (int64_t)(cur / 32);
+        const int bt = (int)(cur % 32);
+#pragma unroll
+        for (int j = 0; j < 3; j++) {
+          const int dm = t_facet<D>(bt, j, 0), et = t_facet<D>(bt, j, 1);
+          const int64_t E = B + mask_delta(g, dm);
+          if ((__ldg(crit + E) >> et) & 1u) { ckind[j] = 1; cid[j] = cell_id<D>(E, et); continue; }
+          const uint32_t sl = field_of<D>(code_at<D>(codes, E), et);
+          if (sl == (uint32_t)t_none<D>(et)) continue;
+          const int64_t Nb = cof_anchor<D>(g, E, et, (int)sl);
+          const int nt = t_cof_type<D>(et, (int)sl);
+          if (Nb == B && nt == bt) continue;
+          ckind[j] = 2;
+          cid[j] = cell_id<D>(Nb, nt);
+          ckey[j] = key(Nb, nt);
+          const int slot = find_or_insert(ckey[j]);
+          if (slot < 0) { bad = true; continue; }
+          cslot[j] = slot;
+          atomicMin(owner + slot, (batch << 7) | (uint32_t)(lane * 3 + j));
+        }
+      }
+      __syncwarp();
+      if (__any_sync(0xffffffffu, bad)) { ovf = true; break; }
+      int ne = 0, nq = 0;
+      bool isnew[3] = {false, false, false};
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        if (ckind[j] == 2 && owner[cslot[j]] == ((batch << 7) | (uint32_t)(lane * 3 + j))) { isnew[j] = true; nq++; }
+        if (ckind[j] == 1 || isnew[j]) ne++;
+      }
+      int v = ne | (nq << 16), incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      const int tot = __shfl_sync(0xffffffffu, incl, 31);
+      const int tot_e = tot & 0xFFFF, tot_q = tot >> 16;
+      if (tail + tot_q > WQ) { ovf = true; break; }
+      int pe = (incl - v) & 0xFFFF, pq = (incl - v) >> 16;
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        if (ckind[j] == 1 || isnew[j]) {
+          if (write) out[nev + pe] = cid[j];
+          pe++;
+        }
+        if (isnew[j]) { queue[tail + pq] = ckey[j]; pq++; }
+      }
+      __syncwarp();
+      nev += tot_e;
+      tail += tot_q;
+      head += K;
+      batch++;
+    }
+    __syncwarp();
+    if (ovf) {  // keys of the failing batch are not all queued: wipe the table
+      for (int i = lane; i < WH; i += 32) { keys[i] = 0ull; owner[i] = 0xFFFFFFFFu; }
+      if (lane == 0) atomicOr(overflow + (cb >> 5), 1u << (cb & 31));
+    } else {
+      // clean the visited set: find every queued key's slot first, then clear
+      for (int i = lane; i < tail; i += 32) {
+        const unsigned long long k = queue[i];
+        const int h = hslot(k);
+        int sl = -1;
+        for (int p = 0; p < WH; p++) {
+          const int j = (h + p) & (WH - 1);
+          if (keys[j] == k) { sl = j; break; }
+          if (keys[j] == 0ull) break;
+        }
+        queue[i] = (unsigned long long)(long long)sl;
+      }
+      __syncwarp();
+      for (int i = lane; i < tail; i += 32) {
+        const long long sl = (long long)queue[i];
+        if (sl >= 0) { keys[sl] = 0ull; owner[sl] = 0xFFFFFFFFu; }
+      }
+      if (lane == 0) {
+        if (!write) off[b] = nev;
+        else jterm[b] = CELL_BOUNDARY;
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // Block-parallel connector BFS for the saddles that outgrew a per-thread slot.
 // Reproduces the sequential FIFO order exactly: a batch = the next (up to 256)
 // queue entries, each producing its facet events in facet order; a discovered
@@ -670,7 +810,8 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
       unsigned long long* dn = &dc->pad[1];
       const int64_t chunk_words = list_cap / 32 > 0 ? list_cap / 32 : 1;
       for (int level = 0; level < 8; level++) {
-        if (q >= words / 5) {  // larger than all scratch: count what is left as internal failures
+        const bool warp_level = level == 0;  // mid-size: one warp per saddle, shared memory only
+        if (!warp_level && q >= words / 5) {  // larger than all scratch: count what is left as internal failures
           TCK(cudaMemsetAsync(dn, 0, 8, s));
           k_bits_compact<<<(unsigned)((ovf_words + 255) / 256 < 148 * 16 ? (ovf_words + 255) / 256 : 148 * 16), 256, 0,
                            s>>>((uint32_t*)ovf, 0, ovf_words, dlist, dn);  // (list unused beyond the count)
@@ -679,7 +820,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
           A.n_internal += (int64_t)hc->pad[1];
           break;
         }
-        const int64_t qn = q * 16 < words / 5 ? q * 16 : words / 5;
+        const int64_t qn = warp_level ? WQ : (q * 16 < words / 5 ? q * 16 : words / 5);
         int64_t h = 1;
         while (h < 2 * qn) h *= 2;
         while (qn + 2 * h > words) h /= 2;
@@ -698,7 +839,19 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
           const int64_t cn = (int64_t)hc->pad[1];
           if (!cn) continue;
           any = true;
-          if (!cleared) {  // level-0 slots self-clean; bigger slots overlay them, so clear once per level
+          if (warp_level) {
+            const int64_t nbw = (cn + CONNW_WARPS - 1) / CONNW_WARPS;
+            if (A.verbose)
+              fprintf(stderr, "dmtz trace pass %d level %d: %lld connectors, warp queues of %d\n", pass, level + 1,
+                      (long long)cn, WQ);
+            TCK(cudaFuncSetAttribute(k_conn_warp<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CONNW_SMEM));
+            k_conn_warp<D><<<(unsigned)(nbw < 148 * 12 ? nbw : 148 * 12), CONNW_WARPS * 32, CONNW_SMEM, s>>>(
+                A.codes, A.crit, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write,
+                (unsigned int*)ovf);
+            TCK(cudaGetLastError());
+            continue;
+          }
+          if (!cleared) {  // block-BFS slots: zero once per level (the kernel leaves them zero)
             TCK(cudaMemsetAsync(sc, 0, A.bfs_bytes, s));
             cleared = true;
           }
