@@ -235,8 +235,12 @@ def test_full_size_cloop_properties(dmtz, name):
     monotone edits, edit list replays g, and no false critical cell at exit -- checked
     by the oracle on sampled crops of f and g."""
     f, fh, xi, cfg = di.config_inputs(name)
-    r = dmtz.correct(_cuda(f), _cuda(fh), xi, full_sweeps=True)
+    r = dmtz.correct(_cuda(f), _cuda(fh), xi)                    # default mode (what bench.py times)
+    rf = dmtz.correct(_cuda(f), _cuda(fh), xi, full_sweeps=True)  # reference mode: every code, every round
     assert r.status == dmtz.OK and r.stats["rounds"] > 0
+    assert r.stats["rounds"] == rf.stats["rounds"] and r.n_edits == rf.n_edits
+    assert torch.equal(r.g.view(torch.int32), rf.g.view(torch.int32))
+    assert torch.equal(r.edits, rf.edits)
     g = r.g.cpu().numpy()
     F, FH, G = f.astype(np.float64), fh.astype(np.float64), g.astype(np.float64)
     assert np.all(G <= FH) and np.all(np.abs(G - F) <= np.float64(np.float32(xi)))
@@ -274,3 +278,32 @@ def test_iter_cap_matches_oracle(dmtz, full_sweeps):
     assert r.status == dmtz.E_ITER_CAP and r.stats["rounds"] == 3 == ref["stats"]["rounds"]
     assert np.array_equal(r.g.cpu().numpy().view(np.uint32), ref["g"].view(np.uint32))
     assert np.array_equal(r.edits_numpy()["v"], ref["edits"]["v"])
+
+
+def test_full_size_cloop_C5_one_gpu(dmtz):
+    """BASELINE config C5 (3D 1024^3, nominally 8 GPUs) fits one B200: the default-mode
+    C-loop to its fixed point, every property checked on the device -- exact error bound,
+    edits only lower g, the edit list replays g bit for bit, and crit(g) == crit(f)
+    everywhere (P:115, P:138, P:141)."""
+    f, fh, xi, cfg = di.config_inputs("C5")
+    ft, fht = _cuda(f), _cuda(fh)
+    del f, fh
+    r = dmtz.correct(ft, fht, xi)
+    assert r.status == dmtz.OK and r.stats["rounds"] > 0
+    g = r.g
+    x32 = torch.tensor(np.float32(xi), device=g.device)
+    assert bool((g <= fht).all()) and bool(((g.double() - ft.double()).abs() <= x32.double()).all())
+    e = r.edits.view(-1, 16)
+    v = e[:, 0:8].contiguous().view(torch.int64).view(-1)
+    q = e[:, 8:10].contiguous().view(torch.int16).view(-1).to(torch.int64) & 0xFFFF
+    ll = e[:, 10] != 0
+    val = e[:, 12:16].contiguous().view(torch.float32).view(-1)
+    assert bool((v[1:] > v[:-1]).all())
+    rec = fht.reshape(-1).clone()
+    step = torch.tensor(np.float32(xi) * np.float32(2.0 ** -6), device=g.device)
+    rec[v[~ll]] = fht.reshape(-1)[v[~ll]] - (q[~ll].to(torch.float32) * step)
+    rec[v[ll]] = val[ll]
+    assert torch.equal(rec.view(torch.int32), g.reshape(-1).view(torch.int32))
+    cf = dmtz.critical_mask(dmtz.compute_gradient(ft))
+    cg = dmtz.critical_mask(dmtz.compute_gradient(g))
+    assert torch.equal(cf, cg)
