@@ -226,6 +226,13 @@ dmtz_status dmtz_slab_begin(dmtz_ctx* ctx, const float* f, const float* fhat, co
 dmtz_status dmtz_slab_round(dmtz_ctx* ctx, const float* f, const float* fhat, const dmtz_correct_opts* opts,
                             const dmtz_slab* slab, void* workspace, size_t workspace_bytes, float* g,
                             int64_t round, int64_t* counters, int64_t* kinds, dmtz_stream_t stream);
+/* Halo refresh between rounds: replace the local planes [z_begin, z_end) of g with
+ * `planes` (device, (z_end - z_begin) * ny * nx f32, the neighbour's values after
+ * round `round`), and record every vertex whose value changed, so that round + 1
+ * re-screens exactly the anchors whose 3x3x3 box holds such a vertex and its frontier
+ * contains the cells they can affect (the same rule as for this rank's own edits). */
+dmtz_status dmtz_slab_halo(dmtz_ctx* ctx, const dmtz_slab* slab, void* workspace, size_t workspace_bytes, float* g,
+                           const float* planes, int64_t z_begin, int64_t z_end, int64_t round, dmtz_stream_t stream);
 /* The owned edits (global vertex indices, sorted). */
 dmtz_status dmtz_slab_end(dmtz_ctx* ctx, const dmtz_slab* slab, void* workspace, size_t workspace_bytes,
                           const float* g, dmtz_edit* edits, int64_t edits_capacity, int64_t* n_edits /* host */,

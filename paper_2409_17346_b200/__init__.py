@@ -81,11 +81,13 @@ def _load():
     L.dmtz_slab_begin.argtypes = [P, P, P, ctypes.POINTER(_Opts), P, P, SZ, P, P]
     L.dmtz_slab_round.argtypes = [P, P, P, ctypes.POINTER(_Opts), P, P, SZ, P, i64, P, P, P]
     L.dmtz_slab_end.argtypes = [P, P, P, SZ, P, P, i64, ctypes.POINTER(i64), ctypes.POINTER(i64), P]
+    L.dmtz_slab_halo.argtypes = [P, P, P, SZ, P, P, i64, i64, i64, P]
     L.dmtz_status_string.argtypes = [i32]
     L.dmtz_status_string.restype = ctypes.c_char_p
     L.dmtz_last_error.restype = ctypes.c_char_p
     for fn in ("dmtz_ctx_create", "dmtz_compute_gradient", "dmtz_critical_mask", "dmtz_correct",
-               "dmtz_trace_separatrices", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end"):
+               "dmtz_trace_separatrices", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end",
+               "dmtz_slab_halo"):
         getattr(L, fn).restype = ctypes.c_int
     return L
 
@@ -105,7 +107,8 @@ class _LazyLib:
 _lib = _LazyLib()
 EXPORTED = ("dmtz_ctx_create", "dmtz_ctx_destroy", "dmtz_workspace_bytes", "dmtz_compute_gradient",
             "dmtz_critical_mask", "dmtz_correct", "dmtz_trace_separatrices", "dmtz_status_string",
-            "dmtz_last_error", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end")
+            "dmtz_last_error", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end",
+            "dmtz_slab_halo")
 
 
 def lib():

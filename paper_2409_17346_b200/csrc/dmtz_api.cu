@@ -229,13 +229,20 @@ inline cudaError_t units_range(const RowGeom& rg, int64_t z0, int64_t z1, uint32
 // body of the CUDA-graph WHILE node.  The screen runs over `units`/`n_units`, the
 // decode over `dunits`/`n_dunits`; targets outside [own_lo, own_hi) are dropped
 // and only anchors in planes [count_z0, count_z1) are counted (slab mode).
+// slab mode: classified planes, false-cell unit marks, unit list built by the caller
+struct RoundExtra {
+  int64_t anchor_z0 = 0, anchor_z1 = INT64_MAX;
+  uint32_t* decode_marks = nullptr;
+  bool list_after = true;
+};
+
 template <int D>
 dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o, WS<D>& W,
                           float* g_out, const uint32_t* units, unsigned long long* n_units, const uint32_t* dunits,
                           unsigned long long* n_dunits, uint32_t* fbits, int fwords, int64_t own_z0, int64_t own_z1,
                           int64_t count_z0, int64_t count_z1, bool profile, unsigned long long max_rounds,
                           cudaGraphConditionalHandle h, int use_cond, int use_skip, int64_t* launches,
-                          cudaStream_t s) {
+                          cudaStream_t s, const RoundExtra& X = RoundExtra()) {
   const Grid& g = c->g;
   const RowGeom rg = row_geom(g);
   const int64_t nwords = (int64_t)(W.rowbit_bytes / 4);  // row-padded target bitmap
@@ -253,14 +260,15 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
   if (profile) CK(cudaEventRecord(c->ev[1], s));
   k_decode<D><<<sweep_blocks * 2, DECODE_THREADS, 0, s>>>(
       f, W.cand_f, W.crit_f, W.cand_g, W.ebits, W.fmark, W.tbits, dunits, n_dunits, g, rg,
-      tier_mask<D>(o->tier), W.lowpos, W.tcache, W.ncache, W.ls, own_z0, own_z1, count_z0, count_z1, W.dc);
+      tier_mask<D>(o->tier), W.lowpos, W.tcache, W.ncache, W.ls, own_z0, own_z1, count_z0, count_z1, X.anchor_z0,
+      X.anchor_z1, X.decode_marks, W.dc);
   if (profile) CK(cudaEventRecord(c->ev[2], s));
   k_edit_rows<D><<<clamp_blocks(nwords, 256), 256, fwords_smem * 4, s>>>(
       W.tbits, nwords, fhat, W.lb, g_out, W.state, W.dc, step, o->q_cap, fbits, g, rg, fwords_smem,
       use_skip ? W.vchg : nullptr, W.vwords, W.ls);
-  k_loop_check<<<1, 32, 0, s>>>(W.dc, W.ls, max_rounds, h, use_cond, fbits ? n_units : nullptr);
+  k_loop_check<<<1, 32, 0, s>>>(W.dc, W.ls, max_rounds, h, use_cond, fbits && X.list_after ? n_units : nullptr);
   *launches += 4;
-  if (fbits) {
+  if (fbits && X.list_after) {
     // next round's unit list (after the check read this round's counters); clears fbits
     if (!use_cond) CK(cudaMemsetAsync(n_units, 0, 8, s));
     k_units_from_bits<<<clamp_blocks(rg.units, 256, 4096), 256, 0, s>>>(fbits, rg.units, (uint32_t*)units, n_units);
@@ -276,10 +284,11 @@ dmtz_status round_phase(dmtz_ctx* c, const float* f, const float* fhat, const dm
                         float* g_out, const uint32_t* units, unsigned long long* n_units, const uint32_t* dunits,
                         unsigned long long* n_dunits, uint32_t* fbits, int fwords, int64_t own_z0, int64_t own_z1,
                         int64_t count_z0, int64_t count_z1, bool profile, unsigned long long max_rounds,
-                        int use_skip, LoopState* hls, int64_t* launches, cudaStream_t s) {
+                        int use_skip, LoopState* hls, int64_t* launches, cudaStream_t s,
+                        const RoundExtra& X = RoundExtra()) {
   dmtz_status st = enqueue_round<D>(c, f, fhat, o, W, g_out, units, n_units, dunits, n_dunits, fbits, fwords, own_z0,
                                     own_z1, count_z0, count_z1, profile, max_rounds, cudaGraphConditionalHandle(), 0,
-                                    use_skip, launches, s);
+                                    use_skip, launches, s, X);
   if (st) return st;
   CK(cudaMemcpyAsync(c->host_cnt, W.dc, sizeof(Counters), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(hls, W.ls, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
@@ -583,8 +592,10 @@ dmtz_status dmtz_slab_begin(dmtz_ctx* c, const float* f, const float* fhat, cons
   st = setup_phase<3>(c, f, fhat, o, W, g_out, sl->z_offset * c->g.sz, &launches, s);
   if (st) return st;
   const RowGeom rg = row_geom(c->g);
+  // round 1 sweeps every local unit; later rounds the frontier (own edits, halo
+  // changes, units with false cells)
   CK(units_range(rg, 0, c->g.nz, W.units, &W.dc->n_units, s));
-  CK(units_range(rg, sl->anchor_z0, sl->anchor_z1, W.units2, &W.dc->n_units2, s));
+  CK(cudaMemsetAsync(W.fbits, 0, (size_t)L.fwords * 4 + 64, s));
   CK(cudaStreamSynchronize(s));
   return DMTZ_OK;
 }
@@ -600,9 +611,19 @@ dmtz_status dmtz_slab_round(dmtz_ctx* c, const float* f, const float* fhat, cons
   WS<3> W((char*)workspace, L, c->g);
   int64_t launches = 0;
   k_set_round<<<1, 32, 0, s>>>(W.ls, (unsigned long long)round);
-  st = round_phase<3>(c, f, fhat, o, W, g_out, W.units, &W.dc->n_units, W.units2, &W.dc->n_units2, nullptr, 0,
-                      sl->own_z0, sl->own_z1, sl->own_z0, sl->own_z1, false, ~0ull,
-                      0 /* halos change outside this rank's edits: no change skipping */, c->host_ls, &launches, s);
+  const RowGeom rg = row_geom(c->g);
+  if (round > 1) {  // this round's unit list: the frontier marked by the last round and the halo refresh
+    CK(cudaMemsetAsync(&W.dc->n_units, 0, 8, s));
+    k_units_from_bits<<<clamp_blocks(rg.units, 256, 4096), 256, 0, s>>>(W.fbits, rg.units, W.units, &W.dc->n_units);
+  }
+  RoundExtra X;
+  X.anchor_z0 = sl->anchor_z0;
+  X.anchor_z1 = sl->anchor_z1;
+  X.decode_marks = W.fbits;
+  X.list_after = false;
+  st = round_phase<3>(c, f, fhat, o, W, g_out, W.units, &W.dc->n_units, W.units, &W.dc->n_units, W.fbits,
+                      (int)L.fwords, sl->own_z0, sl->own_z1, sl->own_z0, sl->own_z1, false, ~0ull, 1, c->host_ls,
+                      &launches, s, X);
   if (st) return st;
   Counters* hc = c->host_cnt;
   counters[0] = (int64_t)hc->n_false;
@@ -610,6 +631,25 @@ dmtz_status dmtz_slab_round(dmtz_ctx* c, const float* f, const float* fhat, cons
   counters[2] = (int64_t)hc->n_targets;
   counters[3] = (int64_t)hc->n_internal;
   for (int k = 0; k < 8; k++) kinds[k] = round == 1 ? (int64_t)hc->kinds[k] : 0;
+  return DMTZ_OK;
+}
+
+dmtz_status dmtz_slab_halo(dmtz_ctx* c, const dmtz_slab* sl, void* workspace, size_t wsb, float* g,
+                           const float* planes, int64_t z_begin, int64_t z_end, int64_t round, dmtz_stream_t stream) {
+  Layout L;
+  dmtz_status st = slab_check(c, sl, workspace, wsb, &L);
+  if (st) return st;
+  if (!g || !planes || z_begin < 0 || z_end > c->g.nz || z_begin > z_end || round < 1) {
+    set_err("invalid argument");
+    return DMTZ_E_ARG;
+  }
+  if (z_begin == z_end) return DMTZ_OK;
+  WS<3> W((char*)workspace, L, c->g);
+  const RowGeom rg = row_geom(c->g);
+  const int64_t items = (z_end - z_begin) * c->g.ny * rg.wpr;
+  k_halo<<<clamp_blocks(items * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+      g, planes, z_begin, z_end, c->g, rg, W.vchg + (int64_t)(round & 1) * W.vwords, W.fbits);
+  CK(cudaGetLastError());
   return DMTZ_OK;
 }
 

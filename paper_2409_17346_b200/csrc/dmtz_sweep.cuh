@@ -374,7 +374,8 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
          const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg, uint32_t tier_mask,
          const unsigned long long* __restrict__ lowpos_f, unsigned long long* __restrict__ tcache,
          uint8_t* __restrict__ ncache, const LoopState* __restrict__ ls, int64_t own_z0,
-         int64_t own_z1, int64_t count_z0, int64_t count_z1, Counters* __restrict__ cnt) {
+         int64_t own_z1, int64_t count_z0, int64_t count_z1, int64_t anchor_z0, int64_t anchor_z1,
+         uint32_t* __restrict__ mark_units, Counters* __restrict__ cnt) {
   const bool count_kinds = ls->round == 1;  // kinds are reported for round 1 only
   __shared__ TargetTables T;
   __shared__ DecodeWarpSmem WS[DECODE_THREADS / 32];
@@ -395,7 +396,7 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
     const uint32_t ub_ = (uint32_t)rg.ub;
     const int64_t z = unit_ / ub_;
     const int64_t y = (int64_t)(unit_ - (uint32_t)z * ub_) * UY + rem_ / ngr;
-    if (y >= g.ny) continue;  // warp-uniform
+    if (y >= g.ny || z < anchor_z0 || z >= anchor_z1) continue;  // warp-uniform (slab: classified planes)
     const int64_t cbase = (int64_t)(rem_ % ngr) * DG;
     // lane j < DG scans chunk cbase + j: changed-code words of u + {0,1}^D and the false-cell mark
     uint32_t chg_l = 0, had_l = 0;
@@ -528,6 +529,11 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
     }
     __syncwarp();
     if (lane < DG && cl < rg.wpr && W.fm[lane] != had_l) fmark[dword_index(g, rg, y, z, cl)] = W.fm[lane];
+    // slab mode: a unit with false cells stays in the frontier (its targets may be another rank's)
+    if (mark_units && __any_sync(0xffffffffu, lane < DG && W.fm[lane & (DG - 1)] != 0u) && lane == 0) {
+      const int64_t unit = z * rg.ub + y / UY;
+      atomicOr(mark_units + (unit >> 5), 1u << (unit & 31));
+    }
     // flush the window: one aligned atomicOr per non-empty word (row-padded target bitmap)
     for (int i = lane; i < 16 * TWW; i += 32) {
       const uint32_t wv = W.tw[i];
@@ -545,6 +551,42 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
   warp_add(&cnt->n_items, c_items);
   warp_add(&cnt->n_replayed, c_rep);
   if (count_kinds && lane < 8 && kacc) atomicAdd(&cnt->kinds[lane], (unsigned long long)kacc);
+}
+
+// ---------------------------------------------------------------------------
+// Slab halo refresh: new values of planes [z0, z1) from a neighbour rank; changed
+// vertices go to the change bitmap the next screen reads and mark the frontier
+// units meeting v + [-2,1]^3, exactly as this rank's own edits do.  One warp per
+// 32-vertex row chunk.
+// ---------------------------------------------------------------------------
+__global__ void k_halo(float* __restrict__ gf, const float* __restrict__ planes, int64_t z0, int64_t z1, Grid g,
+                       RowGeom rg, uint32_t* __restrict__ vchg_round, uint32_t* __restrict__ frontier) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nitems = (z1 - z0) * g.ny * rg.wpr;
+  for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < nitems;
+       it += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t c = it % rg.wpr, row = it / rg.wpr;
+    const int64_t y = row % g.ny, z = z0 + row / g.ny;
+    const int64_t x = c * 32 + lane;
+    bool ch = false;
+    if (x < g.nx) {
+      const int64_t v = x + y * g.sy + z * g.sz;
+      const float nv = planes[v - z0 * g.sz];
+      if (__float_as_uint(nv) != __float_as_uint(gf[v])) { gf[v] = nv; ch = true; }
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, ch);
+    if (!b) continue;  // warp-uniform
+    if (lane == 0) atomicOr(vchg_round + dword_index(g, rg, y, z, c), b);
+    if (lane < 8) {
+      const int64_t y0 = y >= 2 ? y - 2 : 0, y1 = y + 1 < g.ny ? y + 1 : g.ny - 1;
+      const int64_t zz = (z >= 2 ? z - 2 : 0) + (lane >> 1), zt = z + 1 < g.nz ? z + 1 : g.nz - 1;
+      const int64_t bb = y0 / UY + (lane & 1);
+      if (zz <= zt && bb <= y1 / UY) {
+        const int64_t unit = zz * rg.ub + bb;
+        atomicOr(frontier + (unit >> 5), 1u << (unit & 31));
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------

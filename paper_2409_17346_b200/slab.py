@@ -134,6 +134,14 @@ class CudaSlabEngine:
                                               self._stream_ptr()))
         return np.array(c[:], np.int64), np.array(k[:], np.int64)
 
+    def halo(self, r: int, a: int, b: int, planes):
+        """Local planes [a, b) of g <- `planes` (the neighbour's values after round r);
+        the library records the changed vertices for round r + 1's screen and frontier."""
+        planes = planes.contiguous()
+        self._check(self._lib.dmtz_slab_halo(self.ctx._h, ctypes.byref(self.slab), self._P(self.ctx.workspace),
+                                             self.ctx.ws_bytes, self._P(self.g), self._P(planes), a, b, r,
+                                             self._stream_ptr()))
+
     def end(self):
         o0, o1 = self.p.own_local
         cap = (o1 - o0) * self.shape[1] * self.shape[2]
@@ -175,12 +183,16 @@ def run_distributed(engine, f, fhat, xi, q_max=6, q_cap=None, tier=2, max_rounds
     while status is None:
         r += 1
         if r > 1 and pairs:
-            ops = []
+            ops, bufs = [], []
             for peer, (sa, sb), (ra, rb) in pairs:
+                buf = torch.empty_like(engine.g[ra:rb])
+                bufs.append((ra, rb, buf))
                 ops.append(dist.P2POp(dist.isend, engine.g[sa:sb].contiguous(), peer, group))
-                ops.append(dist.P2POp(dist.irecv, engine.g[ra:rb], peer, group))
+                ops.append(dist.P2POp(dist.irecv, buf, peer, group))
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
+            for ra, rb, buf in bufs:   # apply + record the changed halo vertices
+                engine.halo(r - 1, ra, rb, buf)
         c, k = engine.round(r)
         tot = torch.tensor(np.concatenate([c, k]), dtype=torch.int64, device=dev)
         dist.all_reduce(tot, group=group)
@@ -211,7 +223,7 @@ def run_emulated(engines, fs, fhats, xi, q_max=6, q_cap=None, tier=2, max_rounds
                     src = engines[peer]
                     # the peer's planes that this rank keeps as halo = peer's send range towards us
                     (_, (psa, psb), _) = [x for x in halo_pairs(src.p) if x[0] == e.p.rank][0]
-                    e.g[ra:rb] = src.g[psa:psb]
+                    e.halo(r - 1, ra, rb, src.g[psa:psb].clone())
         tot = np.zeros(12, np.int64)
         for e in engines:
             c, k = e.round(r)

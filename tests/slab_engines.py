@@ -24,6 +24,9 @@ class OracleSlabEngine:
                                                self.tier)
         return np.array([nF, nch, nt, 0], np.int64), (kinds if r == 1 else np.zeros(8, np.int64))
 
+    def halo(self, r, a, b, planes):
+        self.g[a:b] = torch.as_tensor(planes)
+
     def end(self):
         o0, o1 = self.p.own_local
         plane = self.f.shape[1] * self.f.shape[2]
