@@ -168,6 +168,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-trace", action="store_true")
+    ap.add_argument("--slab", action="store_true", help="run the multi-GPU slab path even with one rank")
     args = ap.parse_args()
     if args.impl == "dmtz":
         args.warmup = max(args.warmup, 3)
@@ -185,12 +186,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.slab:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2409_17346_b200 as dmtz
-    if world > 1:
+    if world > 1 or args.slab:
         from paper_2409_17346_b200 import slab
-        return slab.bench_main(args, f, fh, xi, cfg, world, rank, local)
+        return slab.bench_main(args, f, fh, xi, cfg, world, rank, local, clocks_cls=Clocks)
 
     dev = torch.device("cuda", local)
     D = len(f.shape)

@@ -111,6 +111,7 @@ class CudaSlabEngine:
         a0, a1 = p.anchor_local
         self.slab = _Slab(p.lz0, o0, o1, a0, a1)
         self.device = torch.device(device)
+        self.launches = 0   # kernels launched by the library calls below (fixed per call)
 
     def _P(self, t):
         return ctypes.c_void_p(t.data_ptr())
@@ -123,6 +124,7 @@ class CudaSlabEngine:
                                               ctypes.byref(self.opts), ctypes.byref(self.slab),
                                               self._P(self.ctx.workspace), self.ctx.ws_bytes, self._P(self.g),
                                               self._stream_ptr()))
+        self.launches += 5   # k_setup, k_codes, k_critmask, k_lowpos, k_units_all
 
     def round(self, r: int):
         c = (ctypes.c_int64 * 4)()
@@ -132,6 +134,7 @@ class CudaSlabEngine:
                                               self._P(self.ctx.workspace), self.ctx.ws_bytes, self._P(self.g), r,
                                               ctypes.cast(c, ctypes.c_void_p), ctypes.cast(k, ctypes.c_void_p),
                                               self._stream_ptr()))
+        self.launches += 5 + (r > 1)  # set_round, [units_from_bits], screen, decode, edit_rows, loop_check
         return np.array(c[:], np.int64), np.array(k[:], np.int64)
 
     def halo(self, r: int, a: int, b: int, planes):
@@ -141,6 +144,7 @@ class CudaSlabEngine:
         self._check(self._lib.dmtz_slab_halo(self.ctx._h, ctypes.byref(self.slab), self._P(self.ctx.workspace),
                                              self.ctx.ws_bytes, self._P(self.g), self._P(planes), a, b, r,
                                              self._stream_ptr()))
+        self.launches += 1 if b > a else 0
 
     def end(self):
         o0, o1 = self.p.own_local
@@ -150,6 +154,7 @@ class CudaSlabEngine:
         self._check(self._lib.dmtz_slab_end(self.ctx._h, ctypes.byref(self.slab), self._P(self.ctx.workspace),
                                             self.ctx.ws_bytes, self._P(self.g), self._P(edits), cap,
                                             ctypes.byref(ne), ctypes.byref(nl), self._stream_ptr()))
+        self.launches += 3   # edit count, scan, write
         return edits[:ne.value], nl.value
 
     def owned_g(self):
@@ -244,12 +249,14 @@ def local_inputs(f: np.ndarray, fhat: np.ndarray, p: SlabPlan):
     return (np.ascontiguousarray(f[p.lz0:p.lz1]), np.ascontiguousarray(fhat[p.lz0:p.lz1]))
 
 
-def bench_main(args, f, fh, xi, cfg, world, rank, local):
-    """bench.py --gpus N (torchrun): strong scaling of the slab C-loop on the config."""
+def bench_main(args, f, fh, xi, cfg, world, rank, local, clocks_cls=None):
+    """bench.py --gpus N (torchrun): strong scaling of the slab C-loop on the config.
+    Device time of a step = max over ranks (CUDA events, barrier + sync on both sides)."""
     import json
 
     import torch.distributed as dist
     dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
     p = plan(f.shape[0], world, rank)
     lf, lfh = local_inputs(f, fh, p)
     eng = CudaSlabEngine(p, f.shape[1], f.shape[2], dev)
@@ -258,29 +265,67 @@ def bench_main(args, f, fh, xi, cfg, world, rank, local):
         run_distributed(eng, ft, fht, xi)
     torch.cuda.synchronize()
     dist.barrier()
-    times = []
-    for _ in range(args.steps):
+
+    def timed(fn):
         dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        edits, nl, st = run_distributed(eng, ft, fht, xi)
+        out = fn()
         e1.record()
         torch.cuda.synchronize()
         t = torch.tensor([e0.elapsed_time(e1)], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        times.append(float(t.item()))
+        return float(t.item()), out
+
+    times = []
+    clk = clocks_cls(local) if clocks_cls else None
+    if clk:
+        clk.__enter__()
+    l0 = eng.launches
+    for _ in range(args.steps):
+        t, (edits, nl, st) = timed(lambda: run_distributed(eng, ft, fht, xi))
+        times.append(t)
+    launches = (eng.launches - l0) // max(args.steps, 1)
+    if clk:
+        clk.__exit__()
     ms = float(np.median(times))
     sweeps = st["rounds"] + 1
     value = f.size * sweeps / (ms * 1e-3) / 1e6
+    # end to end: this rank's inputs from pinned host memory, its owned g and edit list back
+    fp, fhp = torch.from_numpy(lf).pin_memory(), torch.from_numpy(lfh).pin_memory()
+    o0, o1 = p.own_local
+    gh = torch.empty((o1 - o0,) + tuple(f.shape[1:]), dtype=torch.float32).pin_memory()
+    eh = torch.empty((max(gh.numel(), 1), 16), dtype=torch.uint8).pin_memory()
+
+    def e2e_step():
+        ft.copy_(fp, non_blocking=True)
+        fht.copy_(fhp, non_blocking=True)
+        e, n, s = run_distributed(eng, ft, fht, xi)
+        gh.copy_(eng.owned_g(), non_blocking=True)
+        eh[:e.shape[0]].copy_(e, non_blocking=True)
+        torch.cuda.synchronize()
+        return e.numel()
+    ems, ebytes = timed(e2e_step)
+    d2h = torch.tensor([gh.numel() * 4 + ebytes], device=dev, dtype=torch.int64)
+    h2d = torch.tensor([lf.nbytes + lfh.nbytes], device=dev, dtype=torch.int64)
+    dist.all_reduce(d2h)
+    dist.all_reduce(h2d)
     if rank == 0:
         line = {"metric": "C-loop Mvoxels/s per iteration", "value": value, "unit": "Mvoxels/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": f"{cfg.name} {cfg.family} {'x'.join(map(str, f.shape))} rel eps {cfg.eps}",
-                           "parallelism": f"z-slabs x{world} (NCCL halo send/recv + counter all-reduce)",
-                           "sweeps_per_step": sweeps, "rounds": st["rounds"], "mode": "full sweeps per slab"},
-                "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": None,
+                           "parallelism": f"z-slabs x{world} (NCCL halo send/recv + counter all-reduce per round)",
+                           "sweeps_per_step": sweeps, "rounds": st["rounds"],
+                           "mode": "frontier + exact change skipping per slab (bit-identical to 1 GPU)",
+                           "l2": "inputs larger than L2"},
+                "roofline": None, "roofline_note": "kernel rooflines: the N=1 line (same kernels per slab)",
+                "cpu_baseline": None,
+                "e2e": {"value": f.size * sweeps / (ems * 1e-3) / 1e6, "unit": "Mvoxels/s", "ms_per_step": ems,
+                        "h2d_bytes_per_step": int(h2d.item()),
+                        "d2h_bytes_per_step": int(d2h.item())},
+                "gpu_launches": launches, "clocks": clk.summary() if clk else None,
                 "stats": st}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
