@@ -265,7 +265,7 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
   if (profile) CK(cudaEventRecord(c->ev[2], s));
   k_edit_rows<D><<<clamp_blocks(nwords, 256), 256, fwords_smem * 4, s>>>(
       W.tbits, nwords, fhat, W.lb, g_out, W.state, W.dc, step, o->q_cap, fbits, g, rg, fwords_smem,
-      use_skip ? W.vchg : nullptr, W.vwords, W.ls);
+      use_skip ? W.vchg : nullptr, W.vwords, W.ls, FastDiv((uint32_t)rg.wpr), FastDiv((uint32_t)g.ny));
   k_loop_check<<<1, 32, 0, s>>>(W.dc, W.ls, max_rounds, h, use_cond, fbits && X.list_after ? n_units : nullptr);
   *launches += 4;
   if (fbits && X.list_after) {
@@ -471,6 +471,12 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
   if (!out || !d) { set_err("NULL argument"); return DMTZ_E_ARG; }
   *out = nullptr;
   if (d->nx < 2 || d->ny < 2 || d->nz < 1) { set_err("dims %lld x %lld x %lld", (long long)d->nx, (long long)d->ny, (long long)d->nz); return DMTZ_E_DIMS; }
+  // 32-bit work indices: row-padded bitmap words and frontier units must fit in 32 bits
+  if ((d->nz * d->ny) * ((d->nx + 31) / 32) >= (1ll << 31)) {
+    set_err("grid %lld x %lld x %lld too large for one context (use slabs)", (long long)d->nx, (long long)d->ny,
+            (long long)d->nz);
+    return DMTZ_E_DIMS;
+  }
   if (world != 1 || rank != 0 || nccl_id != nullptr) { set_err("world must be 1 (slab layer drives per-rank contexts)"); return DMTZ_E_ARG; }
   CK(cudaSetDevice(cuda_device));
   dmtz_ctx* c = new (std::nothrow) dmtz_ctx();

@@ -17,6 +17,22 @@ struct Grid {
   int64_t nx, ny, nz, N, sy, sz;  // sy = nx, sz = nx*ny
 };
 
+// n / d for a divisor fixed at launch (round-up method: m = 2^32 (2^s - d) / d + 1,
+// q = (umulhi(m, n) + n) >> s, exact for every 32-bit n); replaces the ~60-instruction
+// 64-bit division in per-element index arithmetic
+struct FastDiv {
+  uint32_t d, m, s;
+  FastDiv() = default;
+  __host__ explicit FastDiv(uint32_t dv) : d(dv) {
+    s = 0;
+    while ((1ull << s) < dv) s++;
+    m = (uint32_t)(((1ull << 32) * ((1ull << s) - dv)) / dv + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return (uint32_t)(((uint64_t)__umulhi(m, n) + n) >> s);
+  }
+};
+
 struct Counters {                 // device-side round counters (one 256 B block)
   unsigned long long n_false;
   unsigned long long kinds[8];

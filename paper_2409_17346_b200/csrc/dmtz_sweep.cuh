@@ -601,7 +601,7 @@ __global__ void k_edit_rows(uint32_t* __restrict__ tbits, int64_t nwords, const 
                             const float* __restrict__ lb, float* __restrict__ gf, uint32_t* __restrict__ state,
                             Counters* __restrict__ cnt, float step, int q_cap, uint32_t* __restrict__ next_frontier,
                             Grid g, RowGeom rg, int fwords_smem, uint32_t* __restrict__ vchg, int64_t vwords,
-                            const LoopState* __restrict__ ls) {
+                            const LoopState* __restrict__ ls, FastDiv div_wpr, FastDiv div_ny) {
   uint32_t* vcur = vchg ? vchg + (int64_t)(ls->round & 1) * vwords : nullptr;
   // each block takes a contiguous word range, so its frontier units span a few planes
   const int64_t per_block = ((nwords + gridDim.x - 1) / gridDim.x + 31) / 32 * 32;
@@ -643,8 +643,9 @@ __global__ void k_edit_rows(uint32_t* __restrict__ tbits, int64_t nwords, const 
         mine[h] = src[h] >= 0 && ((wv >> lane) & 1u);
         if (src[h] < 0) continue;  // warp-uniform
         // row-padded target bitmap: word = (z * ny + y) * wpr + x / 32; all its targets share (y, z)
-        const int64_t wrow = (base + sw) / rg.wpr;
-        const int64_t vy = wrow % g.ny, vz = wrow / g.ny;
+        const uint32_t wrow32 = div_wpr.div((uint32_t)(base + sw));   // word indices < 2^32 (host check)
+        const uint32_t vz32 = div_ny.div(wrow32);
+        const int64_t wrow = wrow32, vz = vz32, vy = (int64_t)(wrow32 - vz32 * (uint32_t)g.ny);
         if (next_frontier && lane < 8) {  // the units meeting (y, z) + [-2, 1]: <= 4 planes x 2 row blocks
           const int64_t y0 = vy >= 2 ? vy - 2 : 0, y1 = vy + 1 < g.ny ? vy + 1 : g.ny - 1;
           const int64_t zz = (vz >= 2 ? vz - 2 : 0) + (lane >> 1), z1 = vz + 1 < g.nz ? vz + 1 : g.nz - 1;
