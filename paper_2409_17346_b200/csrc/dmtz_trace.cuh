@@ -314,7 +314,7 @@ __global__ void k_walk(const void* codes, Grid g, int64_t b0, int64_t nb,
 // membership by a linear scan.  Saddles that reach more than CQ triangles set their
 // overflow bit and go to the block-parallel pass.
 #ifndef DMTZ_CQ
-#define DMTZ_CQ 64
+#define DMTZ_CQ 48
 #endif
 constexpr int CQ = DMTZ_CQ;
 constexpr int CONN_THREADS = 128;
