@@ -227,10 +227,67 @@ __device__ __forceinline__ void id_cell(uint64_t id, int64_t& a, int& t) {
   t = t_first_of_dim<D>(d) + (int)(r - a * Td);
 }
 
+// ----------------------------------------------------------------------------- compact views
+// Built once per trace from the codes and criticality, so that a walk step reads
+// one small word instead of several 8-byte codes:
+//  vnib: 4 bits per vertex = its cand slot (NONE = critical), 64 MB for 512^3 (L2-resident);
+//  tpair: per anchor, 3 bits per top cell type = the facet j paired with it, 7 if critical;
+//  eview (3D): per anchor, 4 bits per edge type = cand slot | critical << 3.
+struct TraceViews {
+  uint8_t* vnib;
+  uint32_t* tpair;
+  uint32_t* eview;
+};
+
+template <int D>
+__global__ void k_trace_views(const void* codes, const uint32_t* __restrict__ crit, Grid g, TraceViews V) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 2 * p < g.N; p += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t nib = 0;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int64_t u = 2 * p + h;
+      if (u >= g.N) break;
+      const uint64_t c = code_at<D>(codes, u);
+      nib |= (field_of<D>(c, 0) & 15u) << (4 * h);
+      int64_t x, y, z;
+      coords_of(g, u, x, y, z);
+      const int ok = axes_ok(g, x, y, z);
+      const int tt0 = t_first_of_dim<D>(Tr<D>::TOP);
+      uint32_t tp = 0;
+#pragma unroll
+      for (int t = tt0; t < Tr<D>::NT; t++) {
+        uint32_t j = 7;
+        if (((t_exist<D>(ok) >> t) & 1u) && !((crit[u] >> t) & 1u)) {
+#pragma unroll
+          for (int jj = 0; jj < 4; jj++) {
+            if (jj < t_nfacet<D>(t)) {
+              const int dm = t_facet<D>(t, jj, 0), ft = t_facet<D>(t, jj, 1), sl = t_facet<D>(t, jj, 2);
+              if (field_of<D>(code_at<D>(codes, u + mask_delta(g, dm)), ft) == (uint32_t)sl) j = (uint32_t)jj;
+            }
+          }
+        }
+        tp |= j << (3 * (t - tt0));
+      }
+      V.tpair[u] = tp;
+      if (D == 3) {
+        const uint32_t cm = crit[u];
+        uint32_t ev = 0;
+#pragma unroll
+        for (int e = 0; e < 7; e++) {
+          const int et = t_first_of_dim<D>(1) + e;
+          ev |= ((field_of<D>(c, et) & 7u) | (((cm >> et) & 1u) << 3)) << (4 * e);
+        }
+        V.eview[u] = ev;
+      }
+    }
+    V.vnib[p] = (uint8_t)nib;
+  }
+}
+
 // ----------------------------------------------------------------------------- walks
 // write == false: count cells only.  Returns the cell count or -1 on a cycle.
 template <int D>
-__device__ int64_t walk_desc(const void* codes, const Grid& g, int64_t a, int t, int j, bool write,
+__device__ int64_t walk_desc(const TraceViews& V, const Grid& g, int64_t a, int t, int j, bool write,
                              uint64_t* cells, uint64_t* term, int64_t cap_steps) {
   int64_t v = a + mask_delta(g, t_vmask<D>(t, j));
   int64_t n = 0;
@@ -238,7 +295,7 @@ __device__ int64_t walk_desc(const void* codes, const Grid& g, int64_t a, int t,
   n++;
   for (int64_t step = 0;; step++) {
     if (step > cap_steps) return -1;
-    const uint32_t s = field_of<D>(code_at<D>(codes, v), 0);
+    const uint32_t s = (__ldg(V.vnib + (v >> 1)) >> (4 * (v & 1))) & 15u;
     if (s == (uint32_t)t_none<D>(0)) break;  // critical vertex (a vertex has no facets)
     const int64_t w = v + t_link<D>(0, s, 0) + t_link<D>(0, s, 1) * g.sy + t_link<D>(0, s, 2) * g.sz;
     if (write) {
@@ -253,29 +310,40 @@ __device__ int64_t walk_desc(const void* codes, const Grid& g, int64_t a, int t,
 }
 
 template <int D>
-__device__ int64_t walk_asc(const void* codes, const Grid& g, int64_t a, int t, int s0, bool write,
+__device__ int64_t walk_asc(const TraceViews& V, const Grid& g, int64_t a, int t, int s0, bool write,
                             uint64_t* cells, uint64_t* term, int64_t cap_steps) {
-  int64_t B = cof_anchor<D>(g, a, t, s0);
+  int64_t x, y, z;
+  coords_of(g, a, x, y, z);   // once per branch; every step below moves by table offsets
+  x += t_cof_anchor<D>(t, s0, 0);
+  y += t_cof_anchor<D>(t, s0, 1);
+  z += t_cof_anchor<D>(t, s0, 2);
+  int64_t B = x + y * g.sy + z * g.sz;
   int bt = t_cof_type<D>(t, s0);
+  const int tt0 = t_first_of_dim<D>(Tr<D>::TOP);
   int64_t n = 0;
   uint64_t terminal = CELL_BOUNDARY;
   for (int64_t step = 0;; step++) {
     if (step > cap_steps) return -1;
     if (write) cells[n] = cell_id<D>(B, bt);
     n++;
-    int64_t ca;
-    int ct;
-    if (paired_facet<D>(codes, g, B, bt, ca, ct) < 0) { terminal = cell_id<D>(B, bt); break; }  // maximum
+    const int j = (int)(__ldg(V.tpair + B) >> (3 * (bt - tt0))) & 7;
+    if (j == 7) { terminal = cell_id<D>(B, bt); break; }  // maximum
+    const int dm = t_facet<D>(bt, j, 0), ct = t_facet<D>(bt, j, 1);
+    const int64_t cx = x + (dm & 1), cy = y + ((dm >> 1) & 1), cz = z + ((dm >> 2) & 1);
+    const int64_t ca = B + mask_delta(g, dm);
     if (write) cells[n] = cell_id<D>(ca, ct);
     n++;
     // the other top cofacet of (ca, ct)
     bool moved = false;
     for (int s = 0; s < t_nlink<D>(ct); s++) {
-      if (!link_in_grid<D>(g, ca, ct, s)) continue;
-      const int64_t nb = cof_anchor<D>(g, ca, ct, s);
+      const int64_t lx = cx + t_link<D>(ct, s, 0), ly = cy + t_link<D>(ct, s, 1), lz = cz + t_link<D>(ct, s, 2);
+      if (lx < 0 || ly < 0 || lz < 0 || lx >= g.nx || ly >= g.ny || lz >= g.nz) continue;
       const int nt = t_cof_type<D>(ct, s);
+      const int64_t nx_ = cx + t_cof_anchor<D>(ct, s, 0), ny_ = cy + t_cof_anchor<D>(ct, s, 1),
+                    nz_ = cz + t_cof_anchor<D>(ct, s, 2);
+      const int64_t nb = nx_ + ny_ * g.sy + nz_ * g.sz;
       if (nb == B && nt == bt) continue;
-      B = nb; bt = nt; moved = true;
+      B = nb; bt = nt; x = nx_; y = ny_; z = nz_; moved = true;
       break;
     }
     if (!moved) break;  // boundary facet: the path leaves the domain
@@ -285,7 +353,7 @@ __device__ int64_t walk_asc(const void* codes, const Grid& g, int64_t a, int t, 
 }
 
 template <int D>
-__global__ void k_walk(const void* codes, Grid g, int64_t b0, int64_t nb,
+__global__ void k_walk(TraceViews V, Grid g, int64_t b0, int64_t nb,
                        const uint64_t* __restrict__ origin, const uint8_t* __restrict__ kind,
                        uint64_t* __restrict__ jterm, long long* __restrict__ off, uint64_t* __restrict__ cells,
                        bool write, Counters* __restrict__ cnt) {
@@ -299,8 +367,8 @@ __global__ void k_walk(const void* codes, Grid g, int64_t b0, int64_t nb,
     int64_t n;
     uint64_t* out = write ? cells + off[b] : nullptr;
     uint64_t term = CELL_BOUNDARY;
-    if (k == 1) n = walk_desc<D>(codes, g, a, t, (int)jterm[b], write, out, &term, cap_steps);
-    else if (k == 2) n = walk_asc<D>(codes, g, a, t, (int)jterm[b], write, out, &term, cap_steps);
+    if (k == 1) n = walk_desc<D>(V, g, a, t, (int)jterm[b], write, out, &term, cap_steps);
+    else if (k == 2) n = walk_asc<D>(V, g, a, t, (int)jterm[b], write, out, &term, cap_steps);
     else n = -1;  // connectors run in k_conn_small / k_walk_block
     if (n < 0) { atomicAdd(&cnt->n_internal, 1ull); n = 0; }
     if (!write) off[b] = n;
@@ -320,7 +388,7 @@ constexpr int CQ = DMTZ_CQ;
 constexpr int CONN_THREADS = 128;
 template <int D>
 __global__ void __launch_bounds__(CONN_THREADS)
-k_conn_small(const void* codes, const uint32_t* __restrict__ crit, Grid g, int64_t b0, int64_t nb,
+k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
              const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm, long long* __restrict__ off,
              uint64_t* __restrict__ cells, bool write, unsigned int* __restrict__ overflow, int64_t conn_base) {
   __shared__ uint32_t sq[CQ][CONN_THREADS];
@@ -346,12 +414,13 @@ k_conn_small(const void* codes, const uint32_t* __restrict__ crit, Grid g, int64
       for (int j = 0; j < t_nfacet<D>(bt); j++) {
         const int dm = t_facet<D>(bt, j, 0), et = t_facet<D>(bt, j, 1);
         const int64_t E = B + mask_delta(g, dm);
-        if ((__ldg(crit + E) >> et) & 1u) {  // critical edge: a reached 1-saddle
+        const uint32_t ev = (__ldg(eview + E) >> (4 * (et - t_first_of_dim<D>(1)))) & 15u;
+        if (ev & 8u) {  // critical edge: a reached 1-saddle
           if (write) out[n] = cell_id<D>(E, et);
           n++;
           continue;
         }
-        const uint32_t s = field_of<D>(code_at<D>(codes, E), et);
+        const uint32_t s = ev & 7u;
         if (s == (uint32_t)t_none<D>(et)) continue;  // paired down with a vertex: the path stops
         const int nt = t_cof_type<D>(et, (int)s);
         const int ex = bx + (dm & 1), ey = by + ((dm >> 1) & 1), ez = bz + ((dm >> 2) & 1);
@@ -388,7 +457,7 @@ constexpr int WQ = 512, WH = 1024, CONNW_WARPS = 4;
 constexpr size_t CONNW_SMEM = (size_t)CONNW_WARPS * (WQ * 8 + WH * 8 + WH * 4);
 template <int D>
 __global__ void __launch_bounds__(CONNW_WARPS * 32)
-k_conn_warp(const void* codes, const uint32_t* __restrict__ crit, Grid g, const uint32_t* __restrict__ list,
+k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restrict__ list,
             int64_t nlist, int64_t conn_base, const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
             long long* __restrict__ off, uint64_t* __restrict__ cells, bool write,
             unsigned int* __restrict__ overflow) {
@@ -439,8 +508,9 @@ k_conn_warp(const void* codes, const uint32_t* __restrict__ crit, Grid g, const 
         for (int j = 0; j < 3; j++) {
           const int dm = t_facet<D>(bt, j, 0), et = t_facet<D>(bt, j, 1);
           const int64_t E = B + mask_delta(g, dm);
-          if ((__ldg(crit + E) >> et) & 1u) { ckind[j] = 1; cid[j] = cell_id<D>(E, et); continue; }
-          const uint32_t sl = field_of<D>(code_at<D>(codes, E), et);
+          const uint32_t ev = (__ldg(eview + E) >> (4 * (et - t_first_of_dim<D>(1)))) & 15u;
+          if (ev & 8u) { ckind[j] = 1; cid[j] = cell_id<D>(E, et); continue; }
+          const uint32_t sl = ev & 7u;
           if (sl == (uint32_t)t_none<D>(et)) continue;
           const int64_t Nb = cof_anchor<D>(g, E, et, (int)sl);
           const int nt = t_cof_type<D>(et, (int)sl);
@@ -577,7 +647,7 @@ __global__ void k_bits_compact(uint32_t* __restrict__ bits, int64_t w0, int64_t 
 
 template <int D, int BFS_THREADS>
 __global__ void __launch_bounds__(BFS_THREADS)
-k_walk_block(const void* codes, const uint32_t* __restrict__ crit, Grid g, const uint32_t* __restrict__ list,
+k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restrict__ list,
              int64_t nlist, int64_t conn_base, const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
              long long* __restrict__ off, uint64_t* __restrict__ cells, bool write,
              unsigned long long* __restrict__ scratch, int64_t qcap, int64_t hcap,
@@ -618,8 +688,9 @@ k_walk_block(const void* codes, const uint32_t* __restrict__ crit, Grid g, const
         for (int j = 0; j < 3; j++) {
           const int dm = t_facet<D>(bt, j, 0), et = t_facet<D>(bt, j, 1);
           const int64_t E = B + mask_delta(g, dm);
-          if ((crit[E] >> et) & 1u) { ckind[j] = 1; cid[j] = cell_id<D>(E, et); continue; }
-          const uint32_t sl = field_of<D>(code_at<D>(codes, E), et);
+          const uint32_t ev = (__ldg(eview + E) >> (4 * (et - t_first_of_dim<D>(1)))) & 15u;
+          if (ev & 8u) { ckind[j] = 1; cid[j] = cell_id<D>(E, et); continue; }
+          const uint32_t sl = ev & 7u;
           if (sl == (uint32_t)t_none<D>(et)) continue;
           const int64_t Nb = cof_anchor<D>(g, E, et, (int)sl);
           const int nt = t_cof_type<D>(et, (int)sl);
@@ -745,6 +816,24 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   TCK(cudaMemsetAsync(dc, 0, sizeof(Counters), s));
   k_critmask<D><<<trace_anchor_grid(g), 128, 0, s>>>((const typename Tr<D>::code_t*)A.codes, A.crit, g);
   TCK(cudaGetLastError());
+  // compact views at the front of the BFS scratch (the block BFS gets the rest)
+  TraceViews V;
+  {
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    char* p = (char*)A.bfs;
+    const size_t nb_nib = al((size_t)(g.N + 1) / 2), nb_w = al((size_t)g.N * 4);
+    const size_t need = nb_nib + nb_w * (D == 3 ? 2 : 1);
+    if (need + 64 * 1024 > A.bfs_bytes) return cudaErrorMemoryAllocation;
+    V.vnib = (uint8_t*)p;
+    V.tpair = (uint32_t*)(p + nb_nib);
+    V.eview = D == 3 ? (uint32_t*)(p + nb_nib + nb_w) : nullptr;
+    A.bfs = (unsigned long long*)(p + need);
+    A.bfs_bytes -= need;
+    const int64_t pairs = (g.N + 1) / 2;
+    k_trace_views<D><<<(unsigned)((pairs + 255) / 256 < 148 * 32 ? (pairs + 255) / 256 : 148 * 32), 256, 0, s>>>(
+        A.codes, A.crit, g, V);
+    TCK(cudaGetLastError());
+  }
   long long* pre = A.pre;
   unsigned long long* total = &dc->pad[0];
   const int kinds_list[3] = {1, 2, 4};
@@ -794,12 +883,12 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
     const bool write = pass == 1;
     TCK(cudaMemsetAsync(ovf, 0, (size_t)ovf_words * 4 + 4, s));
     if (blocks_path)  // descending / ascending paths: one thread per branch
-      k_walk<D><<<(unsigned)blocks_path, threads, 0, s>>>(A.codes, g, 0, conn_base, A.out_origin, A.out_kind,
+      k_walk<D><<<(unsigned)blocks_path, threads, 0, s>>>(V, g, 0, conn_base, A.out_origin, A.out_kind,
                                                           A.out_terminal, off, A.out_cells, write, dc);
     if (nbk[2]) {  // connectors: one thread per 2-saddle, small queues in shared memory
       const int64_t nbc = (nbk[2] + CONN_THREADS - 1) / CONN_THREADS;
       k_conn_small<D><<<(unsigned)(nbc < 148 * 64 ? nbc : 148 * 64), CONN_THREADS, 0, s>>>(
-          A.codes, A.crit, g, conn_base, nb, A.out_origin, A.out_terminal, off, A.out_cells, write,
+          V.eview, g, conn_base, nb, A.out_origin, A.out_terminal, off, A.out_cells, write,
           (unsigned int*)ovf, conn_base);
     }
     TCK(cudaGetLastError());
@@ -846,7 +935,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
                       (long long)cn, WQ);
             TCK(cudaFuncSetAttribute(k_conn_warp<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CONNW_SMEM));
             k_conn_warp<D><<<(unsigned)(nbw < 148 * 12 ? nbw : 148 * 12), CONNW_WARPS * 32, CONNW_SMEM, s>>>(
-                A.codes, A.crit, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write,
+                V.eview, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write,
                 (unsigned int*)ovf);
             TCK(cudaGetLastError());
             continue;
@@ -859,7 +948,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
           if (A.verbose)
             fprintf(stderr, "dmtz trace pass %d level %d: %lld connectors, q %lld, %lld blocks\n", pass, level + 1,
                     (long long)cn, (long long)qn, (long long)nblk);
-          k_walk_block<D, 256><<<(unsigned)nblk, 256, 0, s>>>(A.codes, A.crit, g, dlist, cn, conn_base,
+          k_walk_block<D, 256><<<(unsigned)nblk, 256, 0, s>>>(V.eview, g, dlist, cn, conn_base,
                                                               A.out_origin, A.out_terminal, off, A.out_cells,
                                                               write, sc, qn, h, (unsigned int*)ovf, dc);
           TCK(cudaGetLastError());
