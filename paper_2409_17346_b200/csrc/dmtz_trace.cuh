@@ -127,14 +127,6 @@ __device__ __forceinline__ int branch_count(const Grid& g, int kind, uint32_t cm
   return __popc(cm & tm);
 }
 
-template <int D>
-__global__ void k_branch_count(const uint32_t* __restrict__ crit, long long* __restrict__ cnt_out, Grid g, int kind) {
-  DMTZ_FOR_ANCHORS(g, 0, g.nz) {
-    const int64_t a = x + y * g.sy + z * g.sz;
-    cnt_out[a] = branch_count<D>(g, kind, crit[a], x, y, z);
-  }
-}
-
 // exclusive scan helpers (int64, in place); block sums -> one-block scan -> apply
 __global__ void k_scan_local(long long* __restrict__ a, int64_t n, unsigned long long* __restrict__ bsum) {
   __shared__ long long part[1024];
@@ -186,32 +178,95 @@ __global__ void k_scan_add(long long* __restrict__ a, int64_t n, const unsigned 
   if (i < n) a[i] += (long long)bsum[i / SCAN_CHUNK];
 }
 
+// Branch origins without an N-sized count array: a block owns BT_TILE consecutive
+// anchors (BT_PER per thread); pass 1 writes the block's branch total, the block
+// totals are scanned, pass 2 recomputes the counts, scans them inside the block and
+// emits in (anchor, type, branch) order.
+constexpr int BT_THREADS = 256, BT_PER = 8, BT_TILE = BT_THREADS * BT_PER;
+
 template <int D>
-__global__ void k_branch_emit(const uint32_t* __restrict__ crit, const long long* __restrict__ pre, Grid g, int kind,
-                              int64_t base, uint64_t* __restrict__ origin, uint8_t* __restrict__ kout,
-                              uint64_t* __restrict__ jout) {
-  DMTZ_FOR_ANCHORS(g, 0, g.nz) {
-    const int64_t a = x + y * g.sy + z * g.sz;
-    const uint32_t cm = crit[a];
-    int64_t b = base + pre[a];
-    const int top = Tr<D>::TOP;
+__device__ __forceinline__ int tile_counts(const uint32_t* __restrict__ crit, const Grid& g, int kind, int64_t a0,
+                                           int (&c)[BT_PER]) {
+  int64_t x, y, z;
+  coords_of(g, a0 < g.N ? a0 : 0, x, y, z);
+  int tot = 0;
+#pragma unroll
+  for (int k = 0; k < BT_PER; k++) {
+    const int64_t a = a0 + k;
+    c[k] = a < g.N ? branch_count<D>(g, kind, __ldg(crit + a), x, y, z) : 0;
+    tot += c[k];
+    if (++x == g.nx) { x = 0; if (++y == g.ny) { y = 0; ++z; } }
+  }
+  return tot;
+}
+
+__device__ __forceinline__ long long block_exclusive_scan(long long v, long long* total) {
+  __shared__ long long ws[BT_THREADS / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  long long incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  if (lane == 31) ws[wid] = incl;
+  __syncthreads();
+  long long wbase = 0, tot = 0;
+  for (int w = 0; w < BT_THREADS / 32; w++) {
+    const long long x = ws[w];
+    if (w < wid) wbase += x;
+    tot += x;
+  }
+  __syncthreads();
+  *total = tot;
+  return wbase + incl - v;
+}
+
+template <int D>
+__global__ void __launch_bounds__(BT_THREADS)
+k_branch_tiles(const uint32_t* __restrict__ crit, Grid g, int kind, unsigned long long* __restrict__ bsum) {
+  int c[BT_PER];
+  const int t = tile_counts<D>(crit, g, kind, (int64_t)blockIdx.x * BT_TILE + threadIdx.x * BT_PER, c);
+  long long tot;
+  block_exclusive_scan(t, &tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = (unsigned long long)tot;
+}
+
+template <int D>
+__global__ void __launch_bounds__(BT_THREADS)
+k_branch_tiles_emit(const uint32_t* __restrict__ crit, Grid g, int kind, const unsigned long long* __restrict__ bscan,
+                    int64_t base, uint64_t* __restrict__ origin, uint8_t* __restrict__ kout,
+                    uint64_t* __restrict__ jout) {
+  int c[BT_PER];
+  const int64_t a0 = (int64_t)blockIdx.x * BT_TILE + threadIdx.x * BT_PER;
+  const int t = tile_counts<D>(crit, g, kind, a0, c);
+  long long tot;
+  int64_t b = base + (int64_t)bscan[blockIdx.x] + block_exclusive_scan(t, &tot);
+  if (!t) return;
+  int64_t x, y, z;
+  coords_of(g, a0, x, y, z);
+  const int top = Tr<D>::TOP;
+  for (int k = 0; k < BT_PER; k++, (++x == g.nx ? (x = 0, (++y == g.ny ? (y = 0, ++z) : 0)) : 0)) {
+    if (!c[k]) continue;
+    const int64_t a = a0 + k;
+    const uint32_t cm = __ldg(crit + a);
     if (kind == 1) {
-      for (int t = 1; t < t_first_of_dim<D>(2); t++) {
-        if (!((cm >> t) & 1u)) continue;
-        for (int j = 0; j < 2; j++) { origin[b] = cell_id<D>(a, t); kout[b] = 1; jout[b] = (uint64_t)j; b++; }
+      for (int tt = 1; tt < t_first_of_dim<D>(2); tt++) {
+        if (!((cm >> tt) & 1u)) continue;
+        for (int j = 0; j < 2; j++) { origin[b] = cell_id<D>(a, tt); kout[b] = 1; jout[b] = (uint64_t)j; b++; }
       }
     } else if (kind == 2) {
-      for (int t = t_first_of_dim<D>(top - 1); t < t_first_of_dim<D>(top); t++) {
-        if (!((cm >> t) & 1u)) continue;
-        for (int s = 0; s < t_nlink<D>(t); s++) {
-          if (!link_in_grid_xyz<D>(g, x, y, z, t, s)) continue;
-          origin[b] = cell_id<D>(a, t); kout[b] = 2; jout[b] = (uint64_t)s; b++;
+      for (int tt = t_first_of_dim<D>(top - 1); tt < t_first_of_dim<D>(top); tt++) {
+        if (!((cm >> tt) & 1u)) continue;
+        for (int s = 0; s < t_nlink<D>(tt); s++) {
+          if (!link_in_grid_xyz<D>(g, x, y, z, tt, s)) continue;
+          origin[b] = cell_id<D>(a, tt); kout[b] = 2; jout[b] = (uint64_t)s; b++;
         }
       }
     } else if (D == 3) {
-      for (int t = t_first_of_dim<D>(2); t < t_first_of_dim<D>(3); t++) {
-        if (!((cm >> t) & 1u)) continue;
-        origin[b] = cell_id<D>(a, t); kout[b] = 4; jout[b] = 0; b++;
+      for (int tt = t_first_of_dim<D>(2); tt < t_first_of_dim<D>(3); tt++) {
+        if (!((cm >> tt) & 1u)) continue;
+        origin[b] = cell_id<D>(a, tt); kout[b] = 4; jout[b] = 0; b++;
       }
     }
   }
@@ -838,13 +893,23 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   unsigned long long* total = &dc->pad[0];
   const int kinds_list[3] = {1, 2, 4};
   int64_t nbk[3] = {0, 0, 0};
+  // origins: per kind, block totals of BT_TILE-anchor tiles (kept, scanned) -> emission
+  const int64_t ntiles = (g.N + BT_TILE - 1) / BT_TILE;
+  if ((3 * ntiles + 8) * 8 > (int64_t)A.pre_bytes) return cudaErrorMemoryAllocation;
+  unsigned long long* tsum[3] = {(unsigned long long*)pre, (unsigned long long*)pre + ntiles,
+                                 (unsigned long long*)pre + 2 * ntiles};
   for (int ki = 0; ki < 3; ki++) {
     const int kind = kinds_list[ki];
     if (!(A.kinds & (uint32_t)kind) || (kind == 4 && D != 3)) continue;
-    k_branch_count<D><<<trace_anchor_grid(g), 128, 0, s>>>(A.crit, pre, g, kind);
+    k_branch_tiles<D><<<(unsigned)ntiles, BT_THREADS, 0, s>>>(A.crit, g, kind, tsum[ki]);
+    k_scan_top<<<1, 1024, 0, s>>>(tsum[ki], ntiles, total + ki);
     TCK(cudaGetLastError());
-    TCK(scan_i64(pre, g.N, A.bsum, total, &hc->pad[0], s));
-    nbk[ki] = (int64_t)hc->pad[0];
+  }
+  TCK(cudaMemcpyAsync(&hc->pad[0], total, 3 * 8, cudaMemcpyDeviceToHost, s));
+  TCK(cudaStreamSynchronize(s));
+  for (int ki = 0; ki < 3; ki++) {
+    const int kind = kinds_list[ki];
+    nbk[ki] = (!(A.kinds & (uint32_t)kind) || (kind == 4 && D != 3)) ? 0 : (int64_t)hc->pad[ki];
   }
   const int64_t nb = nbk[0] + nbk[1] + nbk[2];
   A.n_branches = nb;
@@ -858,10 +923,8 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   for (int ki = 0; ki < 3; ki++) {
     const int kind = kinds_list[ki];
     if (!nbk[ki]) continue;
-    k_branch_count<D><<<trace_anchor_grid(g), 128, 0, s>>>(A.crit, pre, g, kind);
-    TCK(scan_i64(pre, g.N, A.bsum, total, &hc->pad[0], s));
-    k_branch_emit<D><<<trace_anchor_grid(g), 128, 0, s>>>(A.crit, pre, g, kind, base, A.out_origin, A.out_kind,
-                                                          A.out_terminal);
+    k_branch_tiles_emit<D><<<(unsigned)ntiles, BT_THREADS, 0, s>>>(A.crit, g, kind, tsum[ki], base, A.out_origin,
+                                                                   A.out_kind, A.out_terminal);
     TCK(cudaGetLastError());
     base += nbk[ki];
   }
