@@ -171,6 +171,9 @@ template <int D> __device__ __forceinline__ uint32_t t_exist(int ok) { return D 
 template <int D> __device__ __forceinline__ uint64_t t_nonex_fill(int ok) {
   return D == 3 ? k3d::NONEX_FILL[ok] : k2d::NONEX_FILL[ok];
 }
+template <int D> __host__ __device__ constexpr int t_first_of_dim_c(int d) {
+  return D == 3 ? (d == 0 ? 0 : d == 1 ? 1 : d == 2 ? 8 : d == 3 ? 20 : 26) : (d == 0 ? 0 : d == 1 ? 1 : d == 2 ? 4 : 6);
+}
 template <int D> __device__ __forceinline__ int t_first_of_dim(int d) {
   return D == 3 ? k3d::FIRST_OF_DIM[d] : k2d::FIRST_OF_DIM[d];
 }

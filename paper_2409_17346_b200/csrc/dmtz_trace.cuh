@@ -448,6 +448,29 @@ k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
              uint64_t* __restrict__ cells, bool write, unsigned int* __restrict__ overflow, int64_t conn_base) {
   __shared__ uint32_t sq[CQ][CONN_THREADS];
   uint32_t* q = &sq[0][threadIdx.x];   // q[k * CONN_THREADS]: conflict-free columns
+  // triangle -> facet edges (dm | edge index << 3); edge slot -> cofacet (type | anchor delta + 1)
+  constexpr int T0 = t_first_of_dim_c<D>(2), E0 = t_first_of_dim_c<D>(1);
+  __shared__ uint8_t s_tf[12 * 3];
+  __shared__ uint16_t s_ec[7 * 8];
+  if constexpr (D == 3) {
+    if (threadIdx.x == 0) {
+#pragma unroll
+    for (int tt = 0; tt < 12; tt++)
+#pragma unroll
+      for (int j = 0; j < 3; j++)
+        s_tf[tt * 3 + j] = (uint8_t)(t_facet<D>(T0 + tt, j, 0) | ((t_facet<D>(T0 + tt, j, 1) - E0) << 3));
+#pragma unroll
+    for (int e = 0; e < 7; e++)
+#pragma unroll
+      for (int sl = 0; sl < 8; sl++)
+        s_ec[e * 8 + sl] = sl < t_nlink<D>(E0 + e)
+                               ? (uint16_t)(t_cof_type<D>(E0 + e, sl) | ((t_cof_anchor<D>(E0 + e, sl, 0) + 1) << 5) |
+                                            ((t_cof_anchor<D>(E0 + e, sl, 1) + 1) << 7) |
+                                            ((t_cof_anchor<D>(E0 + e, sl, 2) + 1) << 9))
+                               : (uint16_t)0;
+    }
+  }
+  __syncthreads();
   auto key = [](int dx, int dy, int dz, int ty) {
     return (uint32_t)(dx + 64) | ((uint32_t)(dy + 64) << 7) | ((uint32_t)(dz + 64) << 14) | ((uint32_t)ty << 21);
   };
@@ -466,21 +489,29 @@ k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
       const int bx = (int)(cur & 127) - 64, by = (int)((cur >> 7) & 127) - 64, bz = (int)((cur >> 14) & 127) - 64;
       const int bt = (int)(cur >> 21);
       const int64_t B = a + bx + by * g.sy + bz * g.sz;
-      for (int j = 0; j < t_nfacet<D>(bt); j++) {
-        const int dm = t_facet<D>(bt, j, 0), et = t_facet<D>(bt, j, 1);
-        const int64_t E = B + mask_delta(g, dm);
-        const uint32_t ev = (__ldg(eview + E) >> (4 * (et - t_first_of_dim<D>(1)))) & 15u;
-        if (ev & 8u) {  // critical edge: a reached 1-saddle
-          if (write) out[n] = cell_id<D>(E, et);
+      // the triangle's 3 facet edges: all three views read at once (independent loads)
+      uint32_t tf[3], ev[3];
+      int64_t E[3];
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        tf[j] = s_tf[(bt - T0) * 3 + j];
+        E[j] = B + mask_delta(g, (int)(tf[j] & 7));
+        ev[j] = (__ldg(eview + E[j]) >> (4 * (int)(tf[j] >> 3))) & 15u;
+      }
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        const int dm = (int)(tf[j] & 7), e = (int)(tf[j] >> 3);
+        if (ev[j] & 8u) {  // critical edge: a reached 1-saddle
+          if (write) out[n] = cell_id<D>(E[j], E0 + e);
           n++;
           continue;
         }
-        const uint32_t s = ev & 7u;
-        if (s == (uint32_t)t_none<D>(et)) continue;  // paired down with a vertex: the path stops
-        const int nt = t_cof_type<D>(et, (int)s);
-        const int ex = bx + (dm & 1), ey = by + ((dm >> 1) & 1), ez = bz + ((dm >> 2) & 1);
-        const int nx_ = ex + t_cof_anchor<D>(et, (int)s, 0), ny_ = ey + t_cof_anchor<D>(et, (int)s, 1),
-                  nz_ = ez + t_cof_anchor<D>(et, (int)s, 2);
+        const uint32_t sl = ev[j] & 7u;
+        if (sl == 7u) continue;  // paired down with a vertex: the path stops
+        const uint32_t ec = s_ec[e * 8 + sl];
+        const int nt = (int)(ec & 31);
+        const int nx_ = bx + (dm & 1) + (int)((ec >> 5) & 3) - 1, ny_ = by + ((dm >> 1) & 1) + (int)((ec >> 7) & 3) - 1,
+                  nz_ = bz + ((dm >> 2) & 1) + (int)((ec >> 9) & 3) - 1;
         const uint32_t k = key(nx_, ny_, nz_, nt);
         if (k == cur) continue;
         bool seen = false;
