@@ -431,6 +431,69 @@ __global__ void k_walk(TraceViews V, Grid g, int64_t b0, int64_t nb,
   }
 }
 
+// Connector tables in shared memory: triangle type -> its 3 facet edges (dm | edge
+// index << 3); edge (index, slot) -> cofacet triangle (type | (anchor delta + 1) << 5, 7, 9).
+struct ConnTab {
+  uint8_t tf[12 * 3];
+  uint16_t ec[7 * 8];
+};
+template <int D>
+__device__ __forceinline__ void conn_tables_init(ConnTab& T) {
+  if constexpr (D == 3) {
+    constexpr int T0 = t_first_of_dim_c<D>(2), E0 = t_first_of_dim_c<D>(1);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int tt = 0; tt < 12; tt++)
+#pragma unroll
+        for (int j = 0; j < 3; j++)
+          T.tf[tt * 3 + j] = (uint8_t)(t_facet<D>(T0 + tt, j, 0) | ((t_facet<D>(T0 + tt, j, 1) - E0) << 3));
+#pragma unroll
+      for (int e = 0; e < 7; e++)
+#pragma unroll
+        for (int sl = 0; sl < 8; sl++)
+          T.ec[e * 8 + sl] = sl < t_nlink<D>(E0 + e)
+                                 ? (uint16_t)(t_cof_type<D>(E0 + e, sl) | ((t_cof_anchor<D>(E0 + e, sl, 0) + 1) << 5) |
+                                              ((t_cof_anchor<D>(E0 + e, sl, 1) + 1) << 7) |
+                                              ((t_cof_anchor<D>(E0 + e, sl, 2) + 1) << 9))
+                                 : (uint16_t)0;
+    }
+  }
+  __syncthreads();
+}
+
+// the 3 facet events of triangle (B, bt): kind 1 = critical edge (id), 2 = next triangle
+// (id, key = anchor * 32 + type + 1), 0 = nothing; the three view reads are issued together
+template <int D>
+__device__ __forceinline__ void conn_expand(const ConnTab& T, const uint32_t* __restrict__ eview, const Grid& g,
+                                            int64_t B, int bt, int (&ck)[3], uint64_t (&cid)[3],
+                                            unsigned long long (&ckey)[3]) {
+  constexpr int T0 = t_first_of_dim_c<D>(2), E0 = t_first_of_dim_c<D>(1);
+  uint32_t tf[3], ev[3];
+  int64_t E[3];
+#pragma unroll
+  for (int j = 0; j < 3; j++) {
+    tf[j] = T.tf[(bt - T0) * 3 + j];
+    E[j] = B + mask_delta(g, (int)(tf[j] & 7));
+    ev[j] = (__ldg(eview + E[j]) >> (4 * (int)(tf[j] >> 3))) & 15u;
+  }
+#pragma unroll
+  for (int j = 0; j < 3; j++) {
+    ck[j] = 0;
+    const int e = (int)(tf[j] >> 3);
+    if (ev[j] & 8u) { ck[j] = 1; cid[j] = cell_id<D>(E[j], E0 + e); continue; }
+    const uint32_t sl = ev[j] & 7u;
+    if (sl == 7u) continue;
+    const uint32_t ec = T.ec[e * 8 + sl];
+    const int nt = (int)(ec & 31);
+    const int64_t Nb = E[j] + ((int)((ec >> 5) & 3) - 1) + ((int)((ec >> 7) & 3) - 1) * g.sy +
+                       ((int)((ec >> 9) & 3) - 1) * g.sz;
+    if (Nb == B && nt == bt) continue;
+    ck[j] = 2;
+    cid[j] = cell_id<D>(Nb, nt);
+    ckey[j] = (unsigned long long)(Nb * 32 + nt) + 1ull;
+  }
+}
+
 // Connector BFS, small case: one thread per 2-saddle, its queue (= its visited set:
 // every visited triangle is enqueued exactly once) in shared memory, keys relative
 // to the origin anchor (7 bits per axis + type; BFS depth <= CQ bounds the offsets),
@@ -548,6 +611,8 @@ k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restri
             long long* __restrict__ off, uint64_t* __restrict__ cells, bool write,
             unsigned int* __restrict__ overflow) {
   extern __shared__ unsigned long long smw[];
+  __shared__ ConnTab CT;
+  conn_tables_init<D>(CT);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   unsigned long long* queue = smw + (size_t)wid * (WQ + WH + WH / 2);
   unsigned long long* keys = queue + WQ;
@@ -590,20 +655,10 @@ k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restri
         const unsigned long long cur = queue[head + lane] - 1ull;
         const int64_t B = (int64_t)(cur / 32);
         const int bt = (int)(cur % 32);
+        conn_expand<D>(CT, eview, g, B, bt, ckind, cid, ckey);
 #pragma unroll
         for (int j = 0; j < 3; j++) {
-          const int dm = t_facet<D>(bt, j, 0), et = t_facet<D>(bt, j, 1);
-          const int64_t E = B + mask_delta(g, dm);
-          const uint32_t ev = (__ldg(eview + E) >> (4 * (et - t_first_of_dim<D>(1)))) & 15u;
-          if (ev & 8u) { ckind[j] = 1; cid[j] = cell_id<D>(E, et); continue; }
-          const uint32_t sl = ev & 7u;
-          if (sl == (uint32_t)t_none<D>(et)) continue;
-          const int64_t Nb = cof_anchor<D>(g, E, et, (int)sl);
-          const int nt = t_cof_type<D>(et, (int)sl);
-          if (Nb == B && nt == bt) continue;
-          ckind[j] = 2;
-          cid[j] = cell_id<D>(Nb, nt);
-          ckey[j] = key(Nb, nt);
+          if (ckind[j] != 2) continue;
           const int slot = find_or_insert(ckey[j]);
           if (slot < 0) { bad = true; continue; }
           cslot[j] = slot;
@@ -740,6 +795,8 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
              unsigned int* __restrict__ overflow, Counters* __restrict__ cnt) {
   __shared__ int s_warp[32];
   __shared__ int s_flag;
+  __shared__ ConnTab CT;
+  conn_tables_init<D>(CT);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   unsigned long long* queue = scratch + (int64_t)blockIdx.x * (qcap + 2 * hcap);
   unsigned long long* keys = queue + qcap;
@@ -771,19 +828,10 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
         const unsigned long long cur = queue[head + tid] - 1ull;
         const int64_t B = (int64_t)(cur / 32);
         const int bt = (int)(cur % 32);
+        conn_expand<D>(CT, eview, g, B, bt, ckind, cid, ckey);
+#pragma unroll
         for (int j = 0; j < 3; j++) {
-          const int dm = t_facet<D>(bt, j, 0), et = t_facet<D>(bt, j, 1);
-          const int64_t E = B + mask_delta(g, dm);
-          const uint32_t ev = (__ldg(eview + E) >> (4 * (et - t_first_of_dim<D>(1)))) & 15u;
-          if (ev & 8u) { ckind[j] = 1; cid[j] = cell_id<D>(E, et); continue; }
-          const uint32_t sl = ev & 7u;
-          if (sl == (uint32_t)t_none<D>(et)) continue;
-          const int64_t Nb = cof_anchor<D>(g, E, et, (int)sl);
-          const int nt = t_cof_type<D>(et, (int)sl);
-          if (Nb == B && nt == bt) continue;
-          ckind[j] = 2;
-          cid[j] = cell_id<D>(Nb, nt);
-          ckey[j] = key(Nb, nt);
+          if (ckind[j] != 2) continue;
           const int64_t slot = bfs_find_or_insert(keys, hcap, ckey[j]);
           if (slot < 0) { s_flag = 1; continue; }
           cslot[j] = slot;
