@@ -197,6 +197,15 @@ dmtz_status dmtz_trace_separatrices(dmtz_ctx* ctx, const void* codes, uint32_t k
                                     int64_t cap_branches, int64_t cap_cells,
                                     int64_t* n_branches /* host */, int64_t* n_cells /* host */,
                                     dmtz_stream_t stream);
+/* The same restricted to the branches whose origin cell is anchored in the z-planes
+ * [z_begin, z_end) (codes cover the whole grid): within each kind these are a
+ * contiguous run of dmtz_trace_separatrices' branches, so ranks that own disjoint
+ * plane ranges (with the gradient replicated, slab.trace_distributed) produce, kind by
+ * kind and in rank order, exactly its output. */
+dmtz_status dmtz_trace_separatrices_range(dmtz_ctx* ctx, const void* codes, uint32_t kinds, int64_t z_begin,
+                                          int64_t z_end, void* workspace, size_t workspace_bytes, dmtz_seps* out,
+                                          int64_t cap_branches, int64_t cap_cells, int64_t* n_branches /* host */,
+                                          int64_t* n_cells /* host */, dmtz_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * Slab mode (multi-GPU z-slab decomposition).  One context per

@@ -82,12 +82,15 @@ def _load():
     L.dmtz_slab_round.argtypes = [P, P, P, ctypes.POINTER(_Opts), P, P, SZ, P, i64, P, P, P]
     L.dmtz_slab_end.argtypes = [P, P, P, SZ, P, P, i64, ctypes.POINTER(i64), ctypes.POINTER(i64), P]
     L.dmtz_slab_halo.argtypes = [P, P, P, SZ, P, P, i64, i64, i64, P]
+    L.dmtz_trace_separatrices_range.argtypes = [P, P, ctypes.c_uint32, i64, i64, P, ctypes.c_size_t,
+                                                ctypes.POINTER(_Seps), i64, i64, ctypes.POINTER(i64),
+                                                ctypes.POINTER(i64), P]
     L.dmtz_status_string.argtypes = [i32]
     L.dmtz_status_string.restype = ctypes.c_char_p
     L.dmtz_last_error.restype = ctypes.c_char_p
     for fn in ("dmtz_ctx_create", "dmtz_compute_gradient", "dmtz_critical_mask", "dmtz_correct",
                "dmtz_trace_separatrices", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end",
-               "dmtz_slab_halo"):
+               "dmtz_slab_halo", "dmtz_trace_separatrices_range"):
         getattr(L, fn).restype = ctypes.c_int
     return L
 
@@ -108,7 +111,7 @@ _lib = _LazyLib()
 EXPORTED = ("dmtz_ctx_create", "dmtz_ctx_destroy", "dmtz_workspace_bytes", "dmtz_compute_gradient",
             "dmtz_critical_mask", "dmtz_correct", "dmtz_trace_separatrices", "dmtz_status_string",
             "dmtz_last_error", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end",
-            "dmtz_slab_halo")
+            "dmtz_slab_halo", "dmtz_trace_separatrices_range")
 
 
 def lib():
@@ -230,17 +233,28 @@ class Context:
                       message=msg)
 
     # ---------------------------------------------------------------- traces
-    def trace_sizes(self, codes: torch.Tensor, kinds: int = KIND_DESC | KIND_ASC | KIND_CONN, stream=None):
-        """Branch and cell counts of the traces (two sizing calls: branches, then cells)."""
+    def _trace(self, codes, kinds, seps, cb, cc, nb, nc, stream, z_range):
+        if z_range is None:
+            return _lib.dmtz_trace_separatrices(self._h, ctypes.c_void_p(codes.data_ptr()), kinds,
+                                                ctypes.c_void_p(self.workspace.data_ptr()), self.ws_bytes,
+                                                ctypes.byref(seps), cb, cc, ctypes.byref(nb), ctypes.byref(nc),
+                                                _stream_ptr(stream))
+        return _lib.dmtz_trace_separatrices_range(self._h, ctypes.c_void_p(codes.data_ptr()), kinds,
+                                                  int(z_range[0]), int(z_range[1]),
+                                                  ctypes.c_void_p(self.workspace.data_ptr()), self.ws_bytes,
+                                                  ctypes.byref(seps), cb, cc, ctypes.byref(nb), ctypes.byref(nc),
+                                                  _stream_ptr(stream))
+
+    def trace_sizes(self, codes: torch.Tensor, kinds: int = KIND_DESC | KIND_ASC | KIND_CONN, stream=None,
+                    z_range=None):
+        """Branch and cell counts of the traces (two sizing calls: branches, then cells);
+        z_range = (z0, z1): only branches whose origin is anchored in those planes."""
         _need_cuda(codes)
         nb, nc = ctypes.c_int64(), ctypes.c_int64()
         seps = _Seps(None, None, None, None, None)
         one = torch.empty(8, dtype=torch.int64, device=codes.device)
         seps.branch_offsets = ctypes.c_void_p(one.data_ptr())
-        st = _lib.dmtz_trace_separatrices(self._h, ctypes.c_void_p(codes.data_ptr()), kinds,
-                                          ctypes.c_void_p(self.workspace.data_ptr()), self.ws_bytes,
-                                          ctypes.byref(seps), 0, 0, ctypes.byref(nb), ctypes.byref(nc),
-                                          _stream_ptr(stream))
+        st = self._trace(codes, kinds, seps, 0, 0, nb, nc, stream, z_range)
         if st not in (OK, E_CAPACITY):
             _check(st)
         n_b = nb.value
@@ -248,10 +262,7 @@ class Context:
         kb = torch.empty(max(n_b, 1), dtype=torch.uint8, device=codes.device)
         seps = _Seps(ctypes.c_void_p(bufs[0].data_ptr()), None, ctypes.c_void_p(bufs[1].data_ptr()),
                      ctypes.c_void_p(bufs[2].data_ptr()), ctypes.c_void_p(kb.data_ptr()))
-        st = _lib.dmtz_trace_separatrices(self._h, ctypes.c_void_p(codes.data_ptr()), kinds,
-                                          ctypes.c_void_p(self.workspace.data_ptr()), self.ws_bytes,
-                                          ctypes.byref(seps), n_b, 0, ctypes.byref(nb), ctypes.byref(nc),
-                                          _stream_ptr(stream))
+        st = self._trace(codes, kinds, seps, n_b, 0, nb, nc, stream, z_range)
         if st not in (OK, E_CAPACITY):
             _check(st)
         return {"n_branches": n_b, "n_cells": nc.value}
@@ -267,7 +278,7 @@ class Context:
 
     def trace_separatrices(self, codes: torch.Tensor, kinds: int = KIND_DESC | KIND_ASC | KIND_CONN,
                            cap_branches: int | None = None, cap_cells: int | None = None, stream=None,
-                           out: dict | None = None):
+                           out: dict | None = None, z_range=None):
         """V-path traces -> dict of CUDA tensors (CSR).  ``out`` (from
         trace_buffers) avoids allocating the outputs."""
         _need_cuda(codes)
@@ -277,10 +288,7 @@ class Context:
             bufs = out if out is not None else self.trace_buffers(cb, cc, dev)
             seps = _Seps(*(ctypes.c_void_p(bufs[k].data_ptr()) for k in ("offsets", "cells", "origin", "terminal", "kind")))
             nb, nc = ctypes.c_int64(), ctypes.c_int64()
-            st = _lib.dmtz_trace_separatrices(self._h, ctypes.c_void_p(codes.data_ptr()), kinds,
-                                              ctypes.c_void_p(self.workspace.data_ptr()), self.ws_bytes,
-                                              ctypes.byref(seps), cb, cc, ctypes.byref(nb), ctypes.byref(nc),
-                                              _stream_ptr(stream))
+            st = self._trace(codes, kinds, seps, cb, cc, nb, nc, stream, z_range)
             return st, nb.value, nc.value, bufs
 
         if out is not None:

@@ -679,10 +679,20 @@ dmtz_status dmtz_slab_end(dmtz_ctx* c, const dmtz_slab* sl, void* workspace, siz
 dmtz_status dmtz_trace_separatrices(dmtz_ctx* c, const void* codes, uint32_t kinds, void* workspace,
                                     size_t workspace_bytes, dmtz_seps* out, int64_t cap_b, int64_t cap_c,
                                     int64_t* n_b, int64_t* n_c, dmtz_stream_t stream) {
+  if (!c) { set_err("NULL argument"); return DMTZ_E_ARG; }
+  return dmtz_trace_separatrices_range(c, codes, kinds, 0, c->g.nz, workspace, workspace_bytes, out, cap_b, cap_c,
+                                       n_b, n_c, stream);
+}
+
+dmtz_status dmtz_trace_separatrices_range(dmtz_ctx* c, const void* codes, uint32_t kinds, int64_t z_begin,
+                                          int64_t z_end, void* workspace, size_t workspace_bytes, dmtz_seps* out,
+                                          int64_t cap_b, int64_t cap_c, int64_t* n_b, int64_t* n_c,
+                                          dmtz_stream_t stream) {
   if (!c || !codes || !workspace || !out || !n_b || !n_c || cap_b < 0 || cap_c < 0) {
     set_err("NULL argument");
     return DMTZ_E_ARG;
   }
+  if (z_begin < 0 || z_end > c->g.nz || z_begin > z_end) { set_err("bad plane range"); return DMTZ_E_ARG; }
   Layout L = layout_for(c);
   if (workspace_bytes < L.total) { set_err("workspace %zu < %zu bytes", workspace_bytes, L.total); return DMTZ_E_OOM; }
   char* ws = (char*)workspace;
@@ -706,6 +716,8 @@ dmtz_status dmtz_trace_separatrices(dmtz_ctx* c, const void* codes, uint32_t kin
   a.out_kind = out->kind;
   a.cap_b = cap_b;
   a.cap_c = cap_c;
+  a.a_lo = z_begin * c->g.sz;
+  a.a_hi = z_end * c->g.sz;
   cudaError_t e = c->D == 3 ? run_trace<3>(a, (cudaStream_t)stream) : run_trace<2>(a, (cudaStream_t)stream);
   if (e != cudaSuccess) { set_err("trace: %s", cudaGetErrorString(e)); return DMTZ_E_CUDA; }
   *n_b = a.n_branches;

@@ -40,6 +40,7 @@ struct TraceArgs {
   uint64_t* out_terminal;
   uint8_t* out_kind;
   int64_t cap_b, cap_c;
+  int64_t a_lo = 0, a_hi = INT64_MAX;   // origin anchors traced: [a_lo, a_hi)
   int verbose = 0;
   int64_t n_branches = 0, n_cells = 0, n_internal = 0;
 };
@@ -186,14 +187,14 @@ constexpr int BT_THREADS = 256, BT_PER = 8, BT_TILE = BT_THREADS * BT_PER;
 
 template <int D>
 __device__ __forceinline__ int tile_counts(const uint32_t* __restrict__ crit, const Grid& g, int kind, int64_t a0,
-                                           int (&c)[BT_PER]) {
+                                           int64_t a_lo, int64_t a_hi, int (&c)[BT_PER]) {
   int64_t x, y, z;
   coords_of(g, a0 < g.N ? a0 : 0, x, y, z);
   int tot = 0;
 #pragma unroll
   for (int k = 0; k < BT_PER; k++) {
     const int64_t a = a0 + k;
-    c[k] = a < g.N ? branch_count<D>(g, kind, __ldg(crit + a), x, y, z) : 0;
+    c[k] = a < g.N && a >= a_lo && a < a_hi ? branch_count<D>(g, kind, __ldg(crit + a), x, y, z) : 0;
     tot += c[k];
     if (++x == g.nx) { x = 0; if (++y == g.ny) { y = 0; ++z; } }
   }
@@ -224,9 +225,10 @@ __device__ __forceinline__ long long block_exclusive_scan(long long v, long long
 
 template <int D>
 __global__ void __launch_bounds__(BT_THREADS)
-k_branch_tiles(const uint32_t* __restrict__ crit, Grid g, int kind, unsigned long long* __restrict__ bsum) {
+k_branch_tiles(const uint32_t* __restrict__ crit, Grid g, int kind, int64_t a_lo, int64_t a_hi,
+               unsigned long long* __restrict__ bsum) {
   int c[BT_PER];
-  const int t = tile_counts<D>(crit, g, kind, (int64_t)blockIdx.x * BT_TILE + threadIdx.x * BT_PER, c);
+  const int t = tile_counts<D>(crit, g, kind, (int64_t)blockIdx.x * BT_TILE + threadIdx.x * BT_PER, a_lo, a_hi, c);
   long long tot;
   block_exclusive_scan(t, &tot);
   if (threadIdx.x == 0) bsum[blockIdx.x] = (unsigned long long)tot;
@@ -234,12 +236,12 @@ k_branch_tiles(const uint32_t* __restrict__ crit, Grid g, int kind, unsigned lon
 
 template <int D>
 __global__ void __launch_bounds__(BT_THREADS)
-k_branch_tiles_emit(const uint32_t* __restrict__ crit, Grid g, int kind, const unsigned long long* __restrict__ bscan,
-                    int64_t base, uint64_t* __restrict__ origin, uint8_t* __restrict__ kout,
-                    uint64_t* __restrict__ jout) {
+k_branch_tiles_emit(const uint32_t* __restrict__ crit, Grid g, int kind, int64_t a_lo, int64_t a_hi,
+                    const unsigned long long* __restrict__ bscan, int64_t base, uint64_t* __restrict__ origin,
+                    uint8_t* __restrict__ kout, uint64_t* __restrict__ jout) {
   int c[BT_PER];
   const int64_t a0 = (int64_t)blockIdx.x * BT_TILE + threadIdx.x * BT_PER;
-  const int t = tile_counts<D>(crit, g, kind, a0, c);
+  const int t = tile_counts<D>(crit, g, kind, a0, a_lo, a_hi, c);
   long long tot;
   int64_t b = base + (int64_t)bscan[blockIdx.x] + block_exclusive_scan(t, &tot);
   if (!t) return;
@@ -980,7 +982,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   for (int ki = 0; ki < 3; ki++) {
     const int kind = kinds_list[ki];
     if (!(A.kinds & (uint32_t)kind) || (kind == 4 && D != 3)) continue;
-    k_branch_tiles<D><<<(unsigned)ntiles, BT_THREADS, 0, s>>>(A.crit, g, kind, tsum[ki]);
+    k_branch_tiles<D><<<(unsigned)ntiles, BT_THREADS, 0, s>>>(A.crit, g, kind, A.a_lo, A.a_hi, tsum[ki]);
     k_scan_top<<<1, 1024, 0, s>>>(tsum[ki], ntiles, total + ki);
     TCK(cudaGetLastError());
   }
@@ -1002,8 +1004,8 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   for (int ki = 0; ki < 3; ki++) {
     const int kind = kinds_list[ki];
     if (!nbk[ki]) continue;
-    k_branch_tiles_emit<D><<<(unsigned)ntiles, BT_THREADS, 0, s>>>(A.crit, g, kind, tsum[ki], base, A.out_origin,
-                                                                   A.out_kind, A.out_terminal);
+    k_branch_tiles_emit<D><<<(unsigned)ntiles, BT_THREADS, 0, s>>>(A.crit, g, kind, A.a_lo, A.a_hi, tsum[ki], base,
+                                                                   A.out_origin, A.out_kind, A.out_terminal);
     TCK(cudaGetLastError());
     base += nbk[ki];
   }

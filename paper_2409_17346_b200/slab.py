@@ -244,6 +244,46 @@ def run_emulated(engines, fs, fhats, xi, q_max=6, q_cap=None, tier=2, max_rounds
     return outs, stats
 
 
+# ----------------------------------------------------------------------------- traces
+# The traces do not shard along z without exchanging path segments (a V-path or a
+# connector BFS can cross any number of slabs).  Instead the gradient is replicated:
+# every rank computes the codes of its owned planes (its local grid holds the 1-plane
+# stencil halo they need), the codes are all-gathered (C4: 1.07 GB, C5: 8.6 GB -- a
+# small fraction of 180 GB of HBM), and each rank traces the branches whose origin
+# cell is anchored in its owned planes (dmtz_trace_separatrices_range).  Per kind,
+# the ranks' branches in rank order are exactly the one-GPU output.
+
+def gather_planes(owned: torch.Tensor, nz: int, world: int, group=None) -> torch.Tensor:
+    """All-gather the ranks' owned planes (partition(nz, world)) into the full array
+    (uneven slabs: padded to the largest, then trimmed)."""
+    import torch.distributed as dist
+    parts = partition(nz, world)
+    mx = max(b - a for a, b in parts)
+    plane = tuple(owned.shape[1:])
+    pad = torch.zeros((mx,) + plane, dtype=owned.dtype, device=owned.device)
+    pad[:owned.shape[0]] = owned
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    return torch.cat([bufs[r][:b - a] for r, (a, b) in enumerate(parts)], dim=0)
+
+
+def owned_codes(engine) -> torch.Tensor:
+    """Gradient codes of the rank's owned planes, from its local g (owned + halos)."""
+    codes = engine.ctx.compute_gradient(engine.g)
+    o0, o1 = engine.p.own_local
+    return codes[o0:o1]
+
+
+def trace_distributed(engine, kinds=7, group=None, ctx=None):
+    """One rank of the multi-GPU trace after run_distributed: returns (its CSR dict,
+    the global Context used).  Kinds are DESC | ASC | CONN bits."""
+    from . import Context
+    p = engine.p
+    full = gather_planes(owned_codes(engine), p.nz, p.world, group)
+    ctx = ctx or Context(tuple(full.shape), engine.device)
+    return ctx.trace_separatrices(full, kinds, z_range=(p.z0, p.z1)), ctx
+
+
 def local_inputs(f: np.ndarray, fhat: np.ndarray, p: SlabPlan):
     """The rank's local arrays (owned planes + halos) of global inputs."""
     return (np.ascontiguousarray(f[p.lz0:p.lz1]), np.ascontiguousarray(fhat[p.lz0:p.lz1]))

@@ -119,3 +119,67 @@ def test_slab_cuda_emulated_matches_single_gpu(name, shape, world):
     assert torch.equal(e, ref.edits)
     g = torch.cat([eng.owned_g() for eng in engines])
     assert torch.equal(g.view(torch.int32), ref.g.view(torch.int32))
+
+
+# ----------------------------------------------------------------------------- multi-GPU trace
+def _gather_worker(rank, world, port, nz, d):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    a, b = slab.partition(nz, world)[rank]
+    full = torch.arange(nz * 3 * 2, dtype=torch.int64).reshape(nz, 3, 2)
+    got = slab.gather_planes(full[a:b].clone(), nz, world)
+    np.save(os.path.join(d, f"g{rank}.npy"), got.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nz,world", [(7, 2), (11, 3)])
+def test_gather_planes_gloo(nz, world):
+    """The trace's gradient replication: uneven slabs all-gathered back into the grid."""
+    with tempfile.TemporaryDirectory() as d:
+        port = 29700 + (os.getpid() % 200) + nz
+        mp.spawn(_gather_worker, args=(world, port, nz, d), nprocs=world, join=True)
+        full = np.arange(nz * 3 * 2, dtype=np.int64).reshape(nz, 3, 2)
+        for r in range(world):
+            assert np.array_equal(np.load(os.path.join(d, f"g{r}.npy")), full)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,shape,world", [("C4", (40, 37, 33), 3), ("C3", (30, 60, 70), 2)])
+def test_trace_distributed_emulated(name, shape, world):
+    """Multi-GPU trace, ranks emulated on one GPU: each rank's owned-plane codes (from its
+    local g) concatenate to the one-GPU gradient of g, and the ranks' range traces
+    concatenate, kind by kind, to the one-GPU trace."""
+    import paper_2409_17346_b200 as dmtz
+    f, fh, xi, _ = di.config_inputs(name, shape=shape)
+    dev = torch.device("cuda", 0)
+    ref = dmtz.correct(torch.from_numpy(f).to(dev), torch.from_numpy(fh).to(dev), xi)
+    codes = dmtz.compute_gradient(ref.g)
+    full = dmtz.trace_separatrices(codes)
+    plans = [slab.plan(shape[0], world, r) for r in range(world)]
+    engines = [slab.CudaSlabEngine(p, shape[1], shape[2], dev) for p in plans]
+    loc = [slab.local_inputs(f, fh, p) for p in plans]
+    slab.run_emulated(engines, [torch.from_numpy(a).to(dev) for a, _ in loc],
+                      [torch.from_numpy(b).to(dev) for _, b in loc], xi)
+    gathered = torch.cat([slab.owned_codes(e) for e in engines])
+    assert torch.equal(gathered, codes)
+    ctx = dmtz.Context(shape, dev)
+    parts = [ctx.trace_separatrices(gathered, z_range=(p.z0, p.z1)) for p in plans]
+
+    def cells_of(tr, i):
+        return tr["cells"][tr["offsets"][i]:tr["offsets"][i + 1]]
+
+    for kind in (dmtz.KIND_DESC, dmtz.KIND_ASC, dmtz.KIND_CONN):
+        sel = (full["kind"] == kind).nonzero().flatten()
+        got_o, got_t, got_len, got_c = [], [], [], []
+        for tr in parts:
+            s = (tr["kind"] == kind).nonzero().flatten()
+            got_o.append(tr["origin"][s])
+            got_t.append(tr["terminal"][s])
+            got_len.append(tr["offsets"][s + 1] - tr["offsets"][s])
+            got_c += [cells_of(tr, int(i)) for i in s]
+        assert torch.equal(torch.cat(got_o), full["origin"][sel])
+        assert torch.equal(torch.cat(got_t), full["terminal"][sel])
+        assert torch.equal(torch.cat(got_len), full["offsets"][sel + 1] - full["offsets"][sel])
+        exp = [cells_of(full, int(i)) for i in sel[:: max(1, len(sel) // 200)]]
+        sub = got_c[:: max(1, len(sel) // 200)]
+        assert all(torch.equal(a, b) for a, b in zip(sub, exp))
