@@ -347,6 +347,30 @@ def bench_main(args, f, fh, xi, cfg, world, rank, local, clocks_cls=None):
         torch.cuda.synchronize()
         return e.numel()
     ems, ebytes = timed(e2e_step)
+    # traces of the converged field: codes all-gathered, branches split by origin plane
+    trace = None
+    if not getattr(args, "no_trace", False):
+        try:
+            from . import Context
+            full = gather_planes(owned_codes(eng), p.nz, world)
+            tctx = Context(tuple(full.shape), dev)
+            zr = (p.z0, p.z1)
+            sz = tctx.trace_sizes(full, 7, z_range=zr)
+            bufs = tctx.trace_buffers(sz["n_branches"], sz["n_cells"], dev)
+            del full
+
+            def tr_step():   # gradient of the owned planes, all-gather, this rank's branches
+                fc = gather_planes(owned_codes(eng), p.nz, world)
+                return tctx.trace_separatrices(fc, 7, out=bufs, z_range=zr)
+            tr_step()
+            tms, tr = timed(tr_step)
+            nbr = torch.tensor([tr["origin"].shape[0], tr["cells"].shape[0]], device=dev, dtype=torch.int64)
+            dist.all_reduce(nbr)
+            trace = {"trace_ms": tms, "n_branches": int(nbr[0].item()), "n_cells": int(nbr[1].item()),
+                     "mode": "owned-plane codes all-gathered, branches split by origin plane (max over ranks)"}
+            del tr, bufs
+        except Exception as ex:  # noqa: BLE001
+            trace = {"error": str(ex)[:200]}
     d2h = torch.tensor([gh.numel() * 4 + ebytes], device=dev, dtype=torch.int64)
     h2d = torch.tensor([lf.nbytes + lfh.nbytes], device=dev, dtype=torch.int64)
     dist.all_reduce(d2h)
@@ -365,7 +389,7 @@ def bench_main(args, f, fh, xi, cfg, world, rank, local, clocks_cls=None):
                 "e2e": {"value": f.size * sweeps / (ems * 1e-3) / 1e6, "unit": "Mvoxels/s", "ms_per_step": ems,
                         "h2d_bytes_per_step": int(h2d.item()),
                         "d2h_bytes_per_step": int(d2h.item())},
-                "gpu_launches": launches, "clocks": clk.summary() if clk else None,
+                "trace": trace, "gpu_launches": launches, "clocks": clk.summary() if clk else None,
                 "stats": st}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

@@ -68,12 +68,31 @@ def run(name, world):
             status = slab._stop(r, tot, 0)
         outs = [e.end() for e in engines]
     n_edits = sum(int(o[0].shape[0]) for o in outs)
+    # traces: owned-plane codes (concatenated = the all-gather), each rank's range trace
+    full = torch.cat([slab.owned_codes(e) for e in engines])
+    tctx = dmtz.Context(tuple(full.shape), dev)
+    t_ranks = []
+    for p in plans:
+        sz = tctx.trace_sizes(full, 7, z_range=(p.z0, p.z1))
+        bufs = tctx.trace_buffers(sz["n_branches"], sz["n_cells"], dev)
+        tctx.trace_separatrices(full, 7, out=bufs, z_range=(p.z0, p.z1))
+        e0, e1 = ev(), ev()
+        e0.record()
+        tctx.trace_separatrices(full, 7, out=bufs, z_range=(p.z0, p.z1))
+        e1.record()
+        torch.cuda.synchronize()
+        t_ranks.append(e0.elapsed_time(e1))
+        del bufs
+    gather_ms = full.numel() * 8 * (world - 1) / world / 400e9 * 1e3   # NVLink all-gather at ~400 GB/s per GPU
+    del full, tctx
     proj_ms = sum(max(t) for t in per_round) + len(per_round) * ALLREDUCE_US * 1e-3
     sweeps = r + 1
     return {"config": name, "world": world, "rounds": r, "status": status, "n_edits": n_edits,
             "projected_ms": proj_ms, "sum_rank_ms": sum(sum(t) for t in per_round),
             "projected_value_mvox_s": f.size * sweeps / (proj_ms * 1e-3) / 1e6,
-            "note": "one-GPU emulation; per-round max over ranks + fixed all-reduce latency"}
+            "trace_rank_ms": t_ranks, "trace_projected_ms": max(t_ranks) + gather_ms,
+            "note": "one-GPU emulation; per-round max over ranks + fixed all-reduce latency; trace: max over "
+                    "ranks of the range trace + codes all-gather at 400 GB/s"}
 
 
 if __name__ == "__main__":
