@@ -36,6 +36,13 @@ class _Stats(ctypes.Structure):
                 ("status", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
+class _SStats(ctypes.Structure):
+    _fields_ = [("c_rounds", ctypes.c_int64), ("s_rounds", ctypes.c_int64),
+                ("troublemakers", ctypes.c_int64), ("tm_by_kind", ctypes.c_int64 * 3),
+                ("sep_branches", ctypes.c_int64), ("sep_cells", ctypes.c_int64),
+                ("tm_round1", ctypes.c_int64), ("pad", ctypes.c_int64 * 7)]
+
+
 def build(force: bool = False) -> str:
     """Compile the oracle (gcc, OpenMP, no FMA contraction, honoured rounding modes)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
@@ -60,11 +67,15 @@ def lib():
         L.dmtz_oracle_correct.argtypes = [P, P, P, ctypes.c_float, ctypes.c_int32, ctypes.c_int32,
                                           ctypes.c_int32, i64, P, P, P, i64, P,
                                           ctypes.POINTER(_Stats)]
+        L.dmtz_oracle_preserve.argtypes = [P, P, P, ctypes.c_float, ctypes.c_int32, ctypes.c_int32,
+                                           ctypes.c_int32, i64, P, P, P, i64, P,
+                                           ctypes.POINTER(_Stats), ctypes.POINTER(_SStats)]
         L.dmtz_oracle_trace.argtypes = [P, P, ctypes.c_uint32, i64, i64, P, P, P, P, P, P, P]
         L.dmtz_oracle_slab_round.argtypes = [P, P, P, ctypes.c_float, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                              i64, i64, i64, i64, P, P, P, P]
         for fn in ("dmtz_oracle_gradient", "dmtz_oracle_complex_info", "dmtz_oracle_cell_counts",
-                   "dmtz_oracle_correct", "dmtz_oracle_trace", "dmtz_oracle_num_threads", "dmtz_oracle_slab_round"):
+                   "dmtz_oracle_correct", "dmtz_oracle_trace", "dmtz_oracle_num_threads", "dmtz_oracle_slab_round",
+                   "dmtz_oracle_preserve"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -142,6 +153,37 @@ def correct(f: np.ndarray, fhat: np.ndarray, xi: float, q_max: int = 6, q_cap: i
     out = {k: getattr(stats, k) for k in STATS_FIELDS}
     out["false_by_kind_round0"] = list(stats.false_by_kind_round0)
     out["status"] = st
+    return dict(status=st, g=g, state=state, edits=edits[:min(ne.value, cap)].copy(),
+                n_edits=ne.value, stats=out)
+
+
+def preserve(f: np.ndarray, fhat: np.ndarray, xi: float, tier: int = 4, q_max: int = 6,
+             q_cap: int | None = None, max_rounds: int = 0, edits_capacity: int | None = None):
+    """Literal alternating C-/S-loop workflow (tiers 1-4).  Returns dict(status, g, state,
+    edits, stats) with stats also holding c_rounds, s_rounds, troublemakers, tm_by_kind,
+    sep_branches, sep_cells, tm_round1."""
+    f = np.ascontiguousarray(f, dtype=np.float32)
+    fhat = np.ascontiguousarray(fhat, dtype=np.float32)
+    assert f.shape == fhat.shape
+    if q_cap is None:
+        q_cap = q_max
+    d = _dims(f.shape)
+    n = f.size
+    cap = n if edits_capacity is None else edits_capacity
+    g = np.empty_like(f)
+    state = np.zeros(f.shape, dtype=np.uint32)
+    edits = np.zeros(max(cap, 1), dtype=EDIT_DTYPE)
+    ne = ctypes.c_int64()
+    stats, ss = _Stats(), _SStats()
+    st = lib().dmtz_oracle_preserve(_p(d), _p(f), _p(fhat), ctypes.c_float(xi), q_max, q_cap, tier,
+                                    max_rounds, _p(g), _p(state), _p(edits), cap,
+                                    ctypes.byref(ne), ctypes.byref(stats), ctypes.byref(ss))
+    out = {k: getattr(stats, k) for k in STATS_FIELDS}
+    out["false_by_kind_round0"] = list(stats.false_by_kind_round0)
+    out["status"] = st
+    for k in ("c_rounds", "s_rounds", "troublemakers", "sep_branches", "sep_cells", "tm_round1"):
+        out[k] = getattr(ss, k)
+    out["tm_by_kind"] = list(ss.tm_by_kind)
     return dict(status=st, g=g, state=state, edits=edits[:min(ne.value, cap)].copy(),
                 n_edits=ne.value, stats=out)
 

@@ -652,18 +652,41 @@ static int top_cofacets(const cx_t* cx, int64_t A, int ti, int64_t* Bs, int* bts
   return n;
 }
 
-int dmtz_oracle_trace(const int64_t* dims, const float* field, uint32_t kinds,
-                      int64_t cap_branches, int64_t cap_cells, int64_t* branch_offsets,
-                      uint64_t* cells, uint64_t* origin, uint64_t* terminal, uint8_t* kind,
-                      int64_t* n_branches, int64_t* n_cells) {
-  int st = check_dims(dims);
-  if (st) return st;
-  cx_t cx; build_complex(&cx, dims[0], dims[1], dims[2]);
-  grad_t G;
-  if (!grad_alloc(&cx, &G)) return OR_E_ARG;
-  gradient(&cx, field, &G);
-  csr_t o = {cap_branches, cap_cells, 0, 0, branch_offsets, cells, origin, terminal, kind};
-  if (cap_branches > 0) branch_offsets[0] = 0;
+/* Growable CSR for the oracle's internal traces (the exported trace writes into
+ * caller buffers with fixed capacities instead). */
+static int csr_grow(csr_t* o) {
+  if (o->nb + 1 >= o->cap_b) {
+    int64_t nb = o->cap_b ? 2 * o->cap_b : 1024;
+    o->off = (int64_t*)realloc(o->off, sizeof(int64_t) * (nb + 1));
+    o->origin = (uint64_t*)realloc(o->origin, sizeof(uint64_t) * nb);
+    o->terminal = (uint64_t*)realloc(o->terminal, sizeof(uint64_t) * nb);
+    o->kind = (uint8_t*)realloc(o->kind, nb);
+    if (!o->off || !o->origin || !o->terminal || !o->kind) return 0;
+    o->cap_b = nb;
+  }
+  if (o->nc + 4 >= o->cap_c) {
+    int64_t nc = o->cap_c ? 2 * o->cap_c : 65536;
+    o->cells = (uint64_t*)realloc(o->cells, sizeof(uint64_t) * nc);
+    if (!o->cells) return 0;
+    o->cap_c = nc;
+  }
+  return 1;
+}
+static void csr_free(csr_t* o) {
+  free(o->off); free(o->cells); free(o->origin); free(o->terminal); free(o->kind);
+  memset(o, 0, sizeof *o);
+}
+#define CSR_ROOM(o) do { if (grow && !csr_grow(o)) return OR_E_ARG; } while (0)
+
+/* The traces of gradient G into o (grow = 1: o is reallocated as needed).
+ * Returns OR_OK, or OR_E_INTERNAL on a cycle (never expected: paths strictly
+ * decrease the extended function). */
+static int trace_grad(const cx_t* cxp, const grad_t* Gp, uint32_t kinds, csr_t* op, int grow) {
+  const cx_t cx = *cxp;
+  const grad_t G = *Gp;
+  csr_t* po = op;
+#define o (*po)
+  if (o.cap_b > 0) o.off[0] = 0;
   int64_t maxsteps = cx.N * cx.T + 1;
   int err = 0;
   int T = cx.T;
@@ -676,17 +699,17 @@ int dmtz_oracle_trace(const int64_t* dims, const float* field, uint32_t kinds,
         int64_t ev[2];
         cell_vertices(&cx, A, ti, ev);
         for (int b = 0; b < 2; b++) {
-          csr_begin(&o, cell_id(&cx, A, ti), KIND_DESC);
+          CSR_ROOM(&o); csr_begin(&o, cell_id(&cx, A, ti), KIND_DESC);
           int64_t v = ev[b];
-          csr_push(&o, cell_id(&cx, v, 0));
+          CSR_ROOM(&o); csr_push(&o, cell_id(&cx, v, 0));
           int64_t steps = 0;
           while (G.up[(size_t)v * T + 0] >= 0) {
             int s = G.up[(size_t)v * T + 0], bt;
             int64_t E = cofacet_cell(&cx, v, 0, s, &bt);
             co_t c = coords(&cx, v);
             int64_t w = vid(&cx, c.x + cx.t[0].link[s][0], c.y + cx.t[0].link[s][1], c.z + cx.t[0].link[s][2]);
-            csr_push(&o, cell_id(&cx, E, bt));
-            csr_push(&o, cell_id(&cx, w, 0));
+            CSR_ROOM(&o); csr_push(&o, cell_id(&cx, E, bt));
+            CSR_ROOM(&o); csr_push(&o, cell_id(&cx, w, 0));
             v = w;
             if (++steps > maxsteps) { err = 1; break; }
           }
@@ -705,18 +728,18 @@ int dmtz_oracle_trace(const int64_t* dims, const float* field, uint32_t kinds,
         int64_t Bs[2]; int bts[2];
         int nb = top_cofacets(&cx, A, ti, Bs, bts);
         for (int b = 0; b < nb; b++) {
-          csr_begin(&o, cell_id(&cx, A, ti), KIND_ASC);
+          CSR_ROOM(&o); csr_begin(&o, cell_id(&cx, A, ti), KIND_ASC);
           int64_t B = Bs[b]; int bt = bts[b];
           uint64_t term = BOUNDARY_ID;
           int64_t steps = 0;
           for (;;) {
-            csr_push(&o, cell_id(&cx, B, bt));
+            CSR_ROOM(&o); csr_push(&o, cell_id(&cx, B, bt));
             if (is_crit(&cx, &G, B, bt)) { term = cell_id(&cx, B, bt); break; }
             int k = G.dn[(size_t)B * T + bt];
             if (k < 0) { err = 1; break; }
             int ct;
             int64_t C = facet_cell(&cx, B, bt, k, &ct);
-            csr_push(&o, cell_id(&cx, C, ct));
+            CSR_ROOM(&o); csr_push(&o, cell_id(&cx, C, ct));
             int64_t Cs[2]; int cts[2];
             int nc = top_cofacets(&cx, C, ct, Cs, cts);
             int moved = 0;
@@ -740,7 +763,7 @@ int dmtz_oracle_trace(const int64_t* dims, const float* field, uint32_t kinds,
     for (int64_t A = 0; A < cx.N && !err; A++)
       for (int ti = cx.first_of_dim[2]; ti < cx.first_of_dim[3] && !err; ti++) {
         if (!is_crit(&cx, &G, A, ti)) continue;
-        csr_begin(&o, cell_id(&cx, A, ti), KIND_CONN);
+        CSR_ROOM(&o); csr_begin(&o, cell_id(&cx, A, ti), KIND_CONN);
         int64_t head = 0, tail = 0;
         qa[tail] = A; qt[tail] = ti; tail++;
         seen[(size_t)A * T + ti] = 1;
@@ -749,7 +772,7 @@ int dmtz_oracle_trace(const int64_t* dims, const float* field, uint32_t kinds,
           for (int k = 0; k < 3; k++) {
             int et;
             int64_t E = facet_cell(&cx, B, bt, k, &et);
-            if (is_crit(&cx, &G, E, et)) { csr_push(&o, cell_id(&cx, E, et)); continue; }
+            if (is_crit(&cx, &G, E, et)) { CSR_ROOM(&o); csr_push(&o, cell_id(&cx, E, et)); continue; }
             int s = G.up[(size_t)E * T + et];
             if (s < 0) continue;  /* paired down with a vertex: the path stops */
             int nt;
@@ -757,7 +780,7 @@ int dmtz_oracle_trace(const int64_t* dims, const float* field, uint32_t kinds,
             if (Nb == B && nt == bt) continue;
             if (seen[(size_t)Nb * T + nt]) continue;
             seen[(size_t)Nb * T + nt] = 1;
-            csr_push(&o, cell_id(&cx, Nb, nt));
+            CSR_ROOM(&o); csr_push(&o, cell_id(&cx, Nb, nt));
             if (tail == qcap) {
               qcap *= 2;
               qa = (int64_t*)realloc(qa, sizeof(int64_t) * qcap);
@@ -771,12 +794,261 @@ int dmtz_oracle_trace(const int64_t* dims, const float* field, uint32_t kinds,
       }
     free(qa); free(qt); free(seen);
   }
+#undef o
+  return err ? OR_E_INTERNAL : OR_OK;
+}
+
+int dmtz_oracle_trace(const int64_t* dims, const float* field, uint32_t kinds,
+                      int64_t cap_branches, int64_t cap_cells, int64_t* branch_offsets,
+                      uint64_t* cells, uint64_t* origin, uint64_t* terminal, uint8_t* kind,
+                      int64_t* n_branches, int64_t* n_cells) {
+  int st = check_dims(dims);
+  if (st) return st;
+  cx_t cx; build_complex(&cx, dims[0], dims[1], dims[2]);
+  grad_t G;
+  if (!grad_alloc(&cx, &G)) return OR_E_ARG;
+  gradient(&cx, field, &G);
+  csr_t o = {cap_branches, cap_cells, 0, 0, branch_offsets, cells, origin, terminal, kind};
+  if (cap_branches > 0) branch_offsets[0] = 0;
+  int err = trace_grad(&cx, &G, kinds, &o, 0);
   grad_free(&G);
   *n_branches = o.nb;
   *n_cells = o.nc;
-  if (err) return OR_E_INTERNAL;
+  if (err) return err;
   if (o.nb > cap_branches || o.nc > cap_cells) return OR_E_CAPACITY;
   return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* S-loops and the alternating C/S driver (Fig. 2).         */
+/* ------------------------------------------------------------------------- */
+
+/* (anchor, type) of a cell id */
+static void id_to_cell(const cx_t* cx, uint64_t id, int64_t* A, int* ti) {
+  int d = (int)(id >> 56);
+  int Td = cx->first_of_dim[d + 1] - cx->first_of_dim[d];
+  int64_t r = (int64_t)(id & ((1ull << 56) - 1));
+  *A = r / Td;
+  *ti = cx->first_of_dim[d] + (int)(r % Td);
+}
+
+/* "whose pairing partner differs": the cell's pair in Gg is not its pair in Gf
+ * (pairs up: the same cofacet slot; pairs down: the same facet). */
+static int pair_differs(const cx_t* cx, const grad_t* Gf, const grad_t* Gg, int64_t A, int ti) {
+  size_t i = (size_t)A * cx->T + ti;
+  return Gf->up[i] != Gg->up[i] || Gf->dn[i] != Gg->dn[i];
+}
+
+/* The troublemaker of branch b of the original separatrices Sf: the
+ * first cell along the branch, in its walk order, whose pairing in g differs from
+ * the original pairing.  Cells examined (the critical cells at the ends are the
+ * C-loop's business and are skipped):
+ *   DESC (cells v0 e1 v1 ... v_min): the vertices before the minimum -- a
+ *        0-dimensional troublemaker "paired with an incorrect 1-cell";
+ *   ASC  (cells t0 c1 t1 c2 ...): the (top-1)-cells c_k -- the 2-cell (3D) "paired
+ *        with an incorrect 3-cell", or in 2D the edge paired with a triangle;
+ *   CONN (breadth-first event log): the triangles in queue order (the origin,
+ *        then the logged triangles), and of each its facet edges in facet order,
+ *        f-critical edges skipped -- the 1-cell "paired with an incorrect 2-cell".
+ * Returns 1 and the cell, or 0. */
+static int troublemaker(const cx_t* cx, const grad_t* Gf, const grad_t* Gg, const csr_t* S, int64_t b,
+                        int64_t* tA, int* tt) {
+  int64_t i0 = S->off[b], i1 = S->off[b + 1];
+  int kind = S->kind[b];
+  if (kind == KIND_DESC) {
+    for (int64_t i = i0; i + 1 < i1; i += 2) {   /* v0, v1, ... ; the last cell is the minimum */
+      int64_t A; int ti;
+      id_to_cell(cx, S->cells[i], &A, &ti);
+      if (pair_differs(cx, Gf, Gg, A, ti)) { *tA = A; *tt = ti; return 1; }
+    }
+    return 0;
+  }
+  if (kind == KIND_ASC) {
+    for (int64_t i = i0 + 1; i < i1; i += 2) {   /* c1, c2, ... */
+      int64_t A; int ti;
+      id_to_cell(cx, S->cells[i], &A, &ti);
+      if (pair_differs(cx, Gf, Gg, A, ti)) { *tA = A; *tt = ti; return 1; }
+    }
+    return 0;
+  }
+  /* CONN */
+  int64_t B; int bt;
+  id_to_cell(cx, S->origin[b], &B, &bt);
+  for (int64_t i = i0 - 1; i < i1; i++) {
+    if (i >= i0) {
+      if ((int)(S->cells[i] >> 56) != 2) continue;      /* logged critical edge */
+      id_to_cell(cx, S->cells[i], &B, &bt);
+    }
+    for (int k = 0; k < 3; k++) {
+      int et;
+      int64_t E = facet_cell(cx, B, bt, k, &et);
+      if (is_crit(cx, Gf, E, et)) continue;
+      if (pair_differs(cx, Gf, Gg, E, et)) { *tA = E; *tt = et; return 1; }
+    }
+  }
+  return 0;
+}
+
+static int cmp_u64(const void* a, const void* b) {
+  uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+  return x < y ? -1 : x > y;
+}
+
+/* Tier 3: does branch b of Sg reach the same extremum / the same multiset
+ * of 1-saddles (connectors, reading A14) as branch b of Sf?  Both are traced from
+ * the same critical cells (F = empty), so their branch lists correspond 1:1. */
+static int same_ends(const csr_t* Sf, const csr_t* Sg, int64_t b) {
+  if (Sf->kind[b] != KIND_CONN) return Sf->terminal[b] == Sg->terminal[b];
+  int64_t n[2] = {0, 0};
+  uint64_t* e[2];
+  const csr_t* S[2] = {Sf, Sg};
+  for (int s = 0; s < 2; s++) {
+    int64_t i0 = S[s]->off[b], i1 = S[s]->off[b + 1];
+    e[s] = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(i1 - i0 + 1));
+    for (int64_t i = i0; i < i1; i++)
+      if ((int)(S[s]->cells[i] >> 56) == 1) e[s][n[s]++] = S[s]->cells[i];
+    qsort(e[s], (size_t)n[s], sizeof(uint64_t), cmp_u64);
+  }
+  int same = n[0] == n[1] && (n[0] == 0 || memcmp(e[0], e[1], sizeof(uint64_t) * (size_t)n[0]) == 0);
+  free(e[0]); free(e[1]);
+  return same;
+}
+
+typedef struct {
+  int64_t c_rounds, s_rounds, troublemakers, tm_by_kind[3];  /* DESC ASC CONN */
+  int64_t sep_branches, sep_cells;                           /* of the original field */
+  int64_t tm_round1;                                         /* troublemakers of the first S-round */
+  int64_t pad[7];
+} or_sstats;
+
+/* The DMTz workflow for tiers 1-4 (Fig. 2): C-loops and S-loops
+ * alternate until no false critical cell and no false separatrix is left.
+ * Synchronous rounds (reading A7, A17):
+ *   every round recomputes the gradient of g;
+ *   F != empty (tiers >= 3 use tier 2's F)  -> C-round: T = targets of F (R1-R3b);
+ *   else, tier >= 3                          -> S-round: T = { R1 target of the
+ *        troublemaker of b : b an original separatrix branch, checked when
+ *        tier 4 -- always; tier 3 -- when b's traced end in g differs };
+ *        T = empty -> done;
+ *   else done;
+ *   each non-lossless v in T takes one Eq. 2 step.
+ * A troublemaker's target is "the vertex of its original partner it does not
+ * share" (decrease j / k / l), i.e. rule R1 of the C-loop. */
+int dmtz_oracle_preserve(const int64_t* dims, const float* f, const float* fhat, float xi,
+                         int32_t q_max, int32_t q_cap, int32_t tier, int64_t max_rounds,
+                         float* g_out, uint32_t* state_out, or_edit* edits, int64_t edits_capacity,
+                         int64_t* n_edits, or_stats* stats, or_sstats* ss) {
+  memset(stats, 0, sizeof *stats);
+  memset(ss, 0, sizeof *ss);
+  *n_edits = 0;
+  int st = check_dims(dims);
+  if (st) { stats->status = st; return st; }
+  if (!(xi > 0.0f) || !isfinite(xi) || q_max < 0 || q_max > 30 || q_cap < 1 || q_cap > 65535 ||
+      tier < 1 || tier > 4 || max_rounds < 0) {
+    stats->status = OR_E_ARG; return OR_E_ARG;
+  }
+  cx_t cx; build_complex(&cx, dims[0], dims[1], dims[2]);
+  int64_t N = cx.N;
+  for (int64_t v = 0; v < N; v++)
+    if (!isfinite(f[v]) || !isfinite(fhat[v])) { stats->status = OR_E_NONFINITE; return OR_E_NONFINITE; }
+  for (int64_t v = 0; v < N; v++)
+    if (fhat[v] < lower_bound_ru(f[v], xi) || fhat[v] > upper_bound_rd(f[v], xi)) {
+      stats->status = OR_E_BOUND; return OR_E_BOUND;
+    }
+  if (max_rounds == 0) max_rounds = N * (int64_t)(q_cap + 1);
+  float step = ldexpf(xi, -q_max);
+  float* lb = (float*)malloc(sizeof(float) * N);
+  uint16_t* q = (uint16_t*)calloc(N, sizeof(uint16_t));
+  uint8_t* lossless = (uint8_t*)calloc(N, 1);
+  uint8_t* T = (uint8_t*)calloc(N, 1);
+  grad_t Gf, Gg;
+  if (!lb || !q || !lossless || !T || !grad_alloc(&cx, &Gf) || !grad_alloc(&cx, &Gg)) {
+    stats->status = OR_E_ARG; return OR_E_ARG;
+  }
+  for (int64_t v = 0; v < N; v++) { lb[v] = lower_bound_ru(f[v], xi); g_out[v] = fhat[v]; }
+  gradient(&cx, f, &Gf);
+  const uint32_t all = KIND_DESC | KIND_ASC | KIND_CONN;
+  csr_t Sf = {0}, Sg = {0};
+  int status = OR_OK;
+  if (tier >= 3) {
+    status = trace_grad(&cx, &Gf, all, &Sf, 1);
+    ss->sep_branches = Sf.nb;
+    ss->sep_cells = Sf.nc;
+  }
+  const int ctier = tier >= 2 ? 2 : 1;
+  for (int64_t round = 1; status == OR_OK; round++) {
+    gradient(&cx, g_out, &Gg);
+    memset(T, 0, N);
+    int64_t kinds[8] = {0};
+    int64_t nF = classify(&cx, f, &Gf, &Gg, ctier, T, kinds);
+    if (nF < 0) { status = OR_E_INTERNAL; break; }
+    if (round == 1) {
+      stats->n_false_round0 = nF;
+      memcpy(stats->false_by_kind_round0, kinds, sizeof kinds);
+    }
+    if (nF > 0) {
+      ss->c_rounds++;
+    } else if (tier >= 3) {
+      if (tier == 3) {
+        Sg.nb = Sg.nc = 0;
+        status = trace_grad(&cx, &Gg, all, &Sg, 1);
+        if (status) break;
+        if (Sg.nb != Sf.nb) { status = OR_E_INTERNAL; break; }
+      }
+      int64_t ntm = 0, bad = 0;
+      for (int64_t b = 0; b < Sf.nb; b++) {
+        if (tier == 3 && same_ends(&Sf, &Sg, b)) continue;
+        int64_t A; int ti;
+        if (!troublemaker(&cx, &Gf, &Gg, &Sf, b, &A, &ti)) continue;
+        int64_t v = target_of(&cx, f, &Gf, &Gg, A, ti, 0);
+        if (v < 0) { bad++; continue; }
+        T[v] = 1;
+        ntm++;
+        ss->tm_by_kind[Sf.kind[b] == KIND_DESC ? 0 : Sf.kind[b] == KIND_ASC ? 1 : 2]++;
+      }
+      if (bad) { status = OR_E_INTERNAL; break; }
+      if (ntm == 0) break;
+      if (ss->s_rounds == 0) ss->tm_round1 = ntm;
+      ss->s_rounds++;
+      ss->troublemakers += ntm;
+    } else {
+      break;
+    }
+    int changed = 0;
+    for (int64_t v = 0; v < N; v++) {
+      if (!T[v] || lossless[v]) continue;
+      changed = 1;
+      if (q[v] + 1 <= q_cap) {
+        float s = (float)(q[v] + 1) * step;
+        float gp = fhat[v] - s;
+        if (gp >= lb[v]) { q[v]++; g_out[v] = gp; continue; }
+      }
+      g_out[v] = lb[v];
+      lossless[v] = 1;
+    }
+    if (!changed) { status = OR_E_STUCK; break; }
+    if (round == max_rounds) { status = OR_E_ITER_CAP; break; }
+  }
+  stats->rounds = ss->c_rounds;
+  int64_t ne = 0;
+  for (int64_t v = 0; v < N; v++) {
+    if (state_out) state_out[v] = (uint32_t)q[v] | ((uint32_t)lossless[v] << 16);
+    if (q[v] == 0 && !lossless[v]) continue;
+    stats->n_edited++;
+    if (lossless[v]) stats->n_lossless++; else stats->n_quantized++;
+    if (edits && ne < edits_capacity) {
+      edits[ne].v = (uint64_t)v; edits[ne].q = q[v]; edits[ne].lossless = lossless[v];
+      edits[ne].pad = 0; edits[ne].value = g_out[v];
+    }
+    ne++;
+  }
+  *n_edits = ne;
+  if (status == OR_OK && edits && ne > edits_capacity) status = OR_E_CAPACITY;
+  stats->status = status;
+  free(lb); free(q); free(lossless); free(T);
+  grad_free(&Gf); grad_free(&Gg);
+  csr_free(&Sf); csr_free(&Sg);
+  return status;
 }
 
 int dmtz_oracle_num_threads(void) {

@@ -238,3 +238,108 @@ def trace(C: Complex, f):
                         visited.append(pair[e])
             out.append(("conn", s, visited[1:], reached))
     return out
+
+
+def cs_loop(C: Complex, f, fhat, xi, q_max=6, q_cap=None, tier=4, max_rounds=100000):
+    """Alternating C-/S-loop in synchronous rounds, written
+    independently of the oracle: a round with false critical cells is a C-round
+    (rules R1-R3b); otherwise (tier >= 3) every separatrix of f is re-checked in the
+    gradient of g (tier 4: all; tier 3: those whose end differs in g's trace) and its
+    troublemaker -- the first cell along it whose partner differs -- has the vertex of
+    its original partner that it does not share decreased.
+    Returns (status, g, q, lossless, stats)."""
+    if q_cap is None:
+        q_cap = q_max
+    f = np.asarray(f, np.float32).ravel()
+    fhat = np.asarray(fhat, np.float32).ravel()
+    xi32 = np.float32(xi)
+    step = np.float32(float(Fraction(float(xi32)) / 2 ** q_max))
+    lb = np.array([ru32(Fraction(float(v)) - Fraction(float(xi32))) for v in f], np.float32)
+    g = fhat.copy()
+    q = np.zeros(f.size, np.int64)
+    lossless = np.zeros(f.size, bool)
+    pf = gradient(C, f)
+    cf = critical(C, pf)
+    sep_f = trace(C, f) if tier >= 3 else []
+    stats = dict(c_rounds=0, s_rounds=0, troublemakers=0)
+
+    def partner_vertex(a):
+        b = pf[a]
+        big, small = (b, a) if len(b) > len(a) else (a, b)
+        (v,) = big - small
+        return v
+
+    def first_differing(kind, origin, cells, pg):
+        if kind == "desc":
+            seq = cells[0:-1:2]
+        elif kind == "asc":
+            seq = cells[1::2]
+        else:
+            seq = [e for t in [origin] + cells for e in (t - {p} for p in sorted(t, key=C.vid))
+                   if e not in cf]
+        for a in seq:
+            if pf.get(a) != pg.get(a):
+                return a
+        return None
+
+    rnd = 0
+    while True:
+        rnd += 1
+        pg = gradient(C, g)
+        cg = critical(C, pg)
+        F = cf ^ cg
+        T = set()
+        if F:
+            stats["c_rounds"] += 1
+            for a in F:
+                lowest_f = min(a, key=lambda p: sos_key(f, p, C))
+                if a in cg:
+                    v = partner_vertex(a)
+                elif len(pg[a]) > len(a):
+                    v = lowest_f
+                else:
+                    gamma = pg[a]
+                    (y,) = a - gamma
+                    if lowest_f != y:
+                        v = lowest_f
+                    else:
+                        (v,) = pf[gamma] - gamma
+                T.add(C.vid(v))
+        elif tier >= 3:
+            sep_g = trace(C, g) if tier == 3 else None
+            n = 0
+            for b, (kind, origin, cells, term) in enumerate(sep_f):
+                if tier == 3:
+                    kg, og, cg_, tg = sep_g[b]
+                    assert (kg, og) == (kind, origin)
+                    same = (sorted(map(sorted, tg)) == sorted(map(sorted, term))) if kind == "conn" else tg == term
+                    if same:
+                        continue
+                a = first_differing(kind, origin, cells, pg)
+                if a is None:
+                    continue
+                n += 1
+                T.add(C.vid(partner_vertex(a)))
+            if not T:
+                return "OK", g, q, lossless, stats
+            stats["s_rounds"] += 1
+            stats["troublemakers"] += n
+        else:
+            return "OK", g, q, lossless, stats
+        changed = False
+        for v in sorted(T):
+            if lossless[v]:
+                continue
+            changed = True
+            if q[v] + 1 <= q_cap:
+                gp = np.float32(fhat[v] - np.float32(np.float32(q[v] + 1) * step))
+                if gp >= lb[v]:
+                    q[v] += 1
+                    g[v] = gp
+                    continue
+            g[v] = lb[v]
+            lossless[v] = True
+        if not changed:
+            return "STUCK", g, q, lossless, stats
+        if rnd == max_rounds:
+            return "ITER_CAP", g, q, lossless, stats
