@@ -208,6 +208,54 @@ dmtz_status dmtz_trace_separatrices_range(dmtz_ctx* ctx, const void* codes, uint
                                           int64_t* n_cells /* host */, dmtz_stream_t stream);
 
 /* ------------------------------------------------------------------------
+ * Tiers 3-4: S-loops and the alternating C/S workflow.
+ * P:150 / Fig. 2: "C-loops and S-loops alternate until no false critical cells
+ * or separatrices exist"; an S-loop iteration (1) traces the
+ * separatrices, (2) identifies the TROUBLEMAKER of each -- the first cell along it
+ * whose gradient pairing differs from the original one -- and (3)
+ * decreases the vertex of the original partner the troublemaker does not share
+ * ("decrease j" / "k" / "l").  Rounds are synchronous (DESIGN.md
+ * readings A7, A17): each round recomputes the gradient of g; false critical cells
+ * (tier 2's F) make it a C-round; otherwise the separatrices of f are checked --
+ * tier 4: every branch (same paths); tier 3: the branches whose traced end in
+ * g differs (same extrema; connectors: the same multiset of 1-saddles) --
+ * and the set of their troublemakers' targets takes one Eq. 2 step; none left ->
+ * done.  Each branch is walked in the order of dmtz_trace_separatrices' cells:
+ * DESC the vertices before the minimum, ASC the (top-1)-cells, CONN the facet
+ * edges (facet order, f-critical ones skipped) of the triangles in queue order.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int64_t c_rounds;        /* rounds that fixed false critical cells */
+  int64_t s_rounds;        /* rounds that fixed troublemakers */
+  int64_t troublemakers;   /* summed over the S-rounds */
+  int64_t tm_by_kind[3];   /* of which on DESC / ASC / CONN branches */
+  int64_t sep_branches;    /* separatrices of f (branches / CSR cells) */
+  int64_t sep_cells;
+  int64_t tm_round1;       /* troublemakers of the first S-round */
+  double trace_ms;         /* device time: trace of f + its cell -> branch map */
+  double s_ms;             /* device time summed over the S-rounds (search + edit; tier 3: + trace of g) */
+  int64_t pad[5];
+} dmtz_sloop_stats;
+
+/* Device bytes dmtz_preserve needs in `sep_ws` for separatrix CSRs of at most
+ * cap_branches branches / cap_cells cells (size them with a
+ * dmtz_trace_separatrices call of capacity 0 on the codes of f: it returns
+ * DMTZ_E_CAPACITY with the exact counts; tier 3 also traces g, whose paths may
+ * be longer: give it headroom).  0 for tiers 1-2. */
+size_t dmtz_preserve_sep_bytes(const dmtz_ctx* ctx, const dmtz_correct_opts* opts, int64_t cap_branches,
+                               int64_t cap_cells);
+
+/* The workflow for opts->tier in 1..4 (tiers 1-2: exactly dmtz_correct; sep_ws may
+ * be NULL).  Same inputs, outputs and errors as dmtz_correct, plus sstats (host);
+ * DMTZ_E_CAPACITY also when a separatrix CSR exceeds the caps (sstats->sep_* hold
+ * the needed counts).  ITER_CAP counts C- and S-rounds together. */
+dmtz_status dmtz_preserve(dmtz_ctx* ctx, const float* f, const float* fhat, const dmtz_correct_opts* opts,
+                          void* workspace, size_t workspace_bytes, void* sep_ws, size_t sep_ws_bytes,
+                          int64_t cap_branches, int64_t cap_cells, float* g_out, dmtz_edit* edits,
+                          int64_t edits_capacity, int64_t* n_edits /* host */, dmtz_stats* stats /* host */,
+                          dmtz_sloop_stats* sstats /* host */, dmtz_stream_t stream);
+
+/* ------------------------------------------------------------------------
  * Slab mode (multi-GPU z-slab decomposition).  One context per
  * rank, created for its LOCAL grid: the owned z-planes plus up to 3 halo planes
  * below and above (nz_local = own + halos).  The caller drives the rounds and,

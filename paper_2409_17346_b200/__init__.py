@@ -55,6 +55,13 @@ class _Stats(ctypes.Structure):
                 ("cells_evaluated", ctypes.c_int64), ("anchors_replayed", ctypes.c_int64)]
 
 
+class _SStats(ctypes.Structure):
+    _fields_ = [("c_rounds", ctypes.c_int64), ("s_rounds", ctypes.c_int64), ("troublemakers", ctypes.c_int64),
+                ("tm_by_kind", ctypes.c_int64 * 3), ("sep_branches", ctypes.c_int64), ("sep_cells", ctypes.c_int64),
+                ("tm_round1", ctypes.c_int64), ("trace_ms", ctypes.c_double), ("s_ms", ctypes.c_double),
+                ("pad", ctypes.c_int64 * 5)]
+
+
 class _Seps(ctypes.Structure):
     _fields_ = [("branch_offsets", ctypes.c_void_p), ("cells", ctypes.c_void_p), ("origin", ctypes.c_void_p),
                 ("terminal", ctypes.c_void_p), ("kind", ctypes.c_void_p)]
@@ -85,12 +92,16 @@ def _load():
     L.dmtz_trace_separatrices_range.argtypes = [P, P, ctypes.c_uint32, i64, i64, P, ctypes.c_size_t,
                                                 ctypes.POINTER(_Seps), i64, i64, ctypes.POINTER(i64),
                                                 ctypes.POINTER(i64), P]
+    L.dmtz_preserve_sep_bytes.argtypes = [P, ctypes.POINTER(_Opts), i64, i64]
+    L.dmtz_preserve_sep_bytes.restype = ctypes.c_size_t
+    L.dmtz_preserve.argtypes = [P, P, P, ctypes.POINTER(_Opts), P, SZ, P, SZ, i64, i64, P, P, i64,
+                                ctypes.POINTER(i64), ctypes.POINTER(_Stats), ctypes.POINTER(_SStats), P]
     L.dmtz_status_string.argtypes = [i32]
     L.dmtz_status_string.restype = ctypes.c_char_p
     L.dmtz_last_error.restype = ctypes.c_char_p
     for fn in ("dmtz_ctx_create", "dmtz_compute_gradient", "dmtz_critical_mask", "dmtz_correct",
                "dmtz_trace_separatrices", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end",
-               "dmtz_slab_halo", "dmtz_trace_separatrices_range"):
+               "dmtz_slab_halo", "dmtz_trace_separatrices_range", "dmtz_preserve"):
         getattr(L, fn).restype = ctypes.c_int
     return L
 
@@ -111,7 +122,7 @@ _lib = _LazyLib()
 EXPORTED = ("dmtz_ctx_create", "dmtz_ctx_destroy", "dmtz_workspace_bytes", "dmtz_compute_gradient",
             "dmtz_critical_mask", "dmtz_correct", "dmtz_trace_separatrices", "dmtz_status_string",
             "dmtz_last_error", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end",
-            "dmtz_slab_halo", "dmtz_trace_separatrices_range")
+            "dmtz_slab_halo", "dmtz_trace_separatrices_range", "dmtz_preserve_sep_bytes", "dmtz_preserve")
 
 
 def lib():
@@ -142,6 +153,16 @@ def _need_cuda(*ts):
     for t in ts:
         if not (isinstance(t, torch.Tensor) and t.is_cuda):
             raise TypeError("dmtz needs CUDA tensors (no CPU fallback)")
+
+
+def _stats_dict(st, status):
+    return dict(rounds=st.rounds, n_edited=st.n_edited, n_quantized=st.n_quantized, n_lossless=st.n_lossless,
+                n_false_round0=st.n_false_round0, false_by_kind_round0=list(st.false_by_kind_round0),
+                status=status, sweeps=st.sweeps, anchors_swept=st.anchors_swept, launches=st.launches,
+                sweep_ms=st.sweep_ms, screen_ms=st.screen_ms, decode_ms=st.decode_ms,
+                screen_ms_full=st.screen_ms_full, n_screen_full=st.n_screen_full,
+                anchors_recomputed=st.anchors_recomputed, anchors_decoded=st.anchors_decoded,
+                cells_evaluated=st.cells_evaluated, anchors_replayed=st.anchors_replayed)
 
 
 class Context:
@@ -219,13 +240,55 @@ class Context:
                                    self.ws_bytes, ctypes.c_void_p(g_out.data_ptr()),
                                    ctypes.c_void_p(edits.data_ptr()), cap, ctypes.byref(ne), ctypes.byref(st),
                                    _stream_ptr(stream))
-        stats = dict(rounds=st.rounds, n_edited=st.n_edited, n_quantized=st.n_quantized, n_lossless=st.n_lossless,
-                     n_false_round0=st.n_false_round0, false_by_kind_round0=list(st.false_by_kind_round0),
-                     status=status, sweeps=st.sweeps, anchors_swept=st.anchors_swept, launches=st.launches,
-                     sweep_ms=st.sweep_ms, screen_ms=st.screen_ms, decode_ms=st.decode_ms,
-                     screen_ms_full=st.screen_ms_full, n_screen_full=st.n_screen_full,
-                     anchors_recomputed=st.anchors_recomputed, anchors_decoded=st.anchors_decoded,
-                     cells_evaluated=st.cells_evaluated, anchors_replayed=st.anchors_replayed)
+        stats = _stats_dict(st, status)
+        msg = _lib.dmtz_last_error().decode() if status != OK else ""
+        if raise_on_error and status not in (OK, E_STUCK, E_ITER_CAP, E_CAPACITY):
+            raise DmtzError(status, msg)
+        return Result(status=status, g=g_out, edits=edits[:min(ne.value, cap)], n_edits=ne.value, stats=stats,
+                      message=msg)
+
+    # ---------------------------------------------------------------- tiers 3-4
+    def preserve(self, f: torch.Tensor, fhat: torch.Tensor, xi: float, tier: int = 4, q_max: int = 6,
+                 q_cap: int | None = None, max_rounds: int = 0, full_sweeps: bool = False,
+                 g_out: torch.Tensor | None = None, edits_capacity: int | None = None, sep_caps=None, stream=None,
+                 raise_on_error: bool = True):
+        """The alternating C-/S-loop workflow for tiers 1-4.  The
+        separatrix CSR of f is sized with a trace of f's gradient (sep_caps = (branches,
+        cells) overrides; tier 3 also traces g and gets 50 % headroom on the cells)."""
+        _need_cuda(f, fhat)
+        for t in (f, fhat):
+            assert t.dtype == torch.float32 and tuple(t.shape) == self.shape and t.is_contiguous()
+        if g_out is None:
+            g_out = torch.empty_like(f)
+        cap = self.N if edits_capacity is None else int(edits_capacity)
+        edits = torch.empty((max(cap, 1), 16), dtype=torch.uint8, device=f.device)
+        opts = _Opts(float(xi), int(q_max), int(q_max if q_cap is None else q_cap), int(tier), int(max_rounds),
+                     1 if full_sweeps else 0, 0)
+        cb = cc = 0
+        sep = None
+        if tier >= 3:
+            if sep_caps is None:
+                sz = self.trace_sizes(self.compute_gradient(f), stream=stream)
+                cb, cc = sz["n_branches"], sz["n_cells"]
+                if tier == 3:
+                    cc = cc + cc // 2 + 1024
+            else:
+                cb, cc = (int(x) for x in sep_caps)
+            nbytes = int(_lib.dmtz_preserve_sep_bytes(self._h, ctypes.byref(opts), cb, cc))
+            sep = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=f.device)
+        else:
+            nbytes = 0
+        ne = ctypes.c_int64()
+        st, ss = _Stats(), _SStats()
+        status = _lib.dmtz_preserve(self._h, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(fhat.data_ptr()),
+                                    ctypes.byref(opts), ctypes.c_void_p(self.workspace.data_ptr()), self.ws_bytes,
+                                    ctypes.c_void_p(sep.data_ptr()) if sep is not None else None, nbytes, cb, cc,
+                                    ctypes.c_void_p(g_out.data_ptr()), ctypes.c_void_p(edits.data_ptr()), cap,
+                                    ctypes.byref(ne), ctypes.byref(st), ctypes.byref(ss), _stream_ptr(stream))
+        stats = _stats_dict(st, status)
+        stats.update(c_rounds=ss.c_rounds, s_rounds=ss.s_rounds, troublemakers=ss.troublemakers,
+                     tm_by_kind=list(ss.tm_by_kind), sep_branches=ss.sep_branches, sep_cells=ss.sep_cells,
+                     tm_round1=ss.tm_round1, trace_ms=ss.trace_ms, s_ms=ss.s_ms)
         msg = _lib.dmtz_last_error().decode() if status != OK else ""
         if raise_on_error and status not in (OK, E_STUCK, E_ITER_CAP, E_CAPACITY):
             raise DmtzError(status, msg)
@@ -342,6 +405,10 @@ def critical_mask(codes: torch.Tensor, stream=None):
 
 def correct(f: torch.Tensor, fhat: torch.Tensor, xi: float, **kw) -> Result:
     return context(f.shape, f.device).correct(f, fhat, xi, **kw)
+
+
+def preserve(f: torch.Tensor, fhat: torch.Tensor, xi: float, **kw) -> Result:
+    return context(f.shape, f.device).preserve(f, fhat, xi, **kw)
 
 
 def trace_separatrices(codes: torch.Tensor, kinds: int = KIND_DESC | KIND_ASC | KIND_CONN, **kw):

@@ -17,6 +17,7 @@
 #include "dmtz_kernels.cuh"
 #include "dmtz_sweep.cuh"
 #include "dmtz_trace.cuh"
+#include "dmtz_sloop.cuh"
 
 using namespace dmtz;
 
@@ -131,7 +132,7 @@ void launch_codes(const Grid& g, const float* fld, void* codes, int64_t z0, int6
 
 template <int D>
 uint32_t tier_mask(int tier) {
-  if (tier == 2) return 0xFFFFFFFFu;
+  if (tier >= 2) return 0xFFFFFFFFu;  // tiers 3-4 build on tier 2
   // dims 0 and top only
   return D == 3 ? (1u | (0x3Fu << 20)) : (1u | (0x3u << 4));
 }
@@ -353,27 +354,28 @@ dmtz_status build_loop_graph(dmtz_ctx* c, LoopGraph& G, const float* f, const fl
   return DMTZ_OK;
 }
 
+// Run C-loop rounds (a3-a7) until the loop check stops them.  first: start a new
+// loop (round 1 over every unit); else resume at the round and unit list the caller
+// prepared (after an S-round).  On return hls holds the loop state.
 template <int D>
-dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
-                         char* ws, const Layout& L, float* g_out, dmtz_edit* edits, int64_t cap,
-                         int64_t* n_edits, dmtz_stats* st, cudaStream_t s) {
+dmtz_status run_cloop(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o, WS<D>& W,
+                      char* ws, const Layout& L, float* g_out, unsigned long long max_rounds, bool first,
+                      dmtz_stats* st, cudaStream_t s) {
   const Grid& g = c->g;
-  WS<D> W(ws, L, g);
   Counters* hc = c->host_cnt;
   LoopState* hls = c->host_ls;
-  dmtz_status status = setup_phase<D>(c, f, fhat, o, W, g_out, 0, &st->launches, s);
-  if (status != DMTZ_OK) { st->status = status; return status; }
-  const unsigned long long max_rounds =
-      o->max_rounds > 0 ? (unsigned long long)o->max_rounds : (unsigned long long)g.N * (unsigned long long)(o->q_cap + 1);
   const RowGeom rg = row_geom(g);
   unsigned long long* n_units = &W.dc->n_units;
   const bool frontier_mode = !o->full_sweeps;
-  // round 1 (and every round of a full sweep) processes every unit
-  CK(units_range(rg, 0, g.nz, W.units, n_units, s));
-  CK(cudaMemsetAsync(W.fbits, 0, (size_t)L.fwords * 4, s));
-  CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));
-  k_loop_reset<<<1, 32, 0, s>>>(W.ls);
-  st->launches += 2;
+  dmtz_status status = DMTZ_OK;
+  if (first) {
+    // round 1 (and every round of a full sweep) processes every unit
+    CK(units_range(rg, 0, g.nz, W.units, n_units, s));
+    CK(cudaMemsetAsync(W.fbits, 0, (size_t)L.fwords * 4, s));
+    CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));
+    k_loop_reset<<<1, 32, 0, s>>>(W.ls);
+    st->launches += 2;
+  }
   const bool use_graph = !o->profile && !c->verbose && !c->no_graph && c->cap_stream && c->graph;
   if (use_graph) {
     // a3-a7 on the device: one graph launch runs every round
@@ -382,16 +384,15 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
         G.q_max != o->q_max || G.q_cap != o->q_cap || G.tier != o->tier || G.frontier != (int)frontier_mode ||
         G.max_rounds != (long long)max_rounds) {
       status = build_loop_graph<D>(c, G, f, fhat, o, W, g_out, ws, L, max_rounds, frontier_mode, s);
-      if (status != DMTZ_OK) { st->status = status; return status; }
+      if (status != DMTZ_OK) return status;
     }
+    const unsigned long long sw0 = first ? 0ull : hls->sweeps;
     CK(cudaGraphLaunch(G.exec, s));
     CK(cudaMemcpyAsync(hls, W.ls, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    st->launches += 5 * (int64_t)hls->sweeps;
+    st->launches += 5 * (int64_t)(hls->sweeps - sw0);
   } else {
     for (;;) {
-      const int64_t round = (int64_t)hls->round;
-      (void)round;
       status = round_phase<D>(c, f, fhat, o, W, g_out, W.units, n_units, W.units, n_units,
                               frontier_mode ? W.fbits : nullptr, (int)L.fwords, 0, g.nz, 0, g.nz, o->profile != 0,
                               max_rounds, frontier_mode ? 1 : 0, hls, &st->launches, s);
@@ -410,11 +411,16 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
                 " | act_chg %llu act_had %llu had_false %llu chg_false %llu\n",
                 hls->sweeps, hc->n_units, hc->n_recomputed, hc->n_swept, hc->n_false, hc->n_targets, hc->n_changed,
                 hc->pad[2], hc->pad[3], hc->pad[4], hc->pad[5]);
-      const bool go = hls->status == 0 && hls->rounds == hls->sweeps;  // check advanced the round
+      const bool go = hls->status == 0 && hls->last_false != 0;  // the check advanced the round
       if (!go) break;
     }
   }
-  if (status == DMTZ_E_CUDA) { st->status = status; return status; }
+  return status;
+}
+
+template <int D>
+void loop_stats(dmtz_ctx* c, dmtz_stats* st) {
+  LoopState* hls = c->host_ls;
   st->sweeps = (int64_t)hls->sweeps;
   st->anchors_swept = (int64_t)hls->anchors_swept;
   st->anchors_recomputed = (int64_t)hls->recomputed;
@@ -424,13 +430,18 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
   st->rounds = (int64_t)hls->rounds;
   st->n_false_round0 = (int64_t)hls->n_false0;
   for (int k = 0; k < 8; k++) st->false_by_kind_round0[k] = (int64_t)hls->kinds0[k];
-  status = (dmtz_status)hls->status;
+  const dmtz_status status = (dmtz_status)hls->status;
   if (status == DMTZ_E_INTERNAL) set_err("gradient invariant violated (round %llu)", hls->round);
   else if (status == DMTZ_E_STUCK) set_err("no target could move (round %llu)", hls->round);
   else if (status == DMTZ_E_ITER_CAP) set_err("round cap %llu reached", hls->round);
+}
+
+template <int D>
+dmtz_status finish_edits(dmtz_ctx* c, WS<D>& W, float* g_out, dmtz_status status, dmtz_edit* edits, int64_t cap,
+                         int64_t* n_edits, dmtz_stats* st, cudaStream_t s) {
   // a8: edit list
   int64_t nl = 0;
-  dmtz_status es = edits_phase<D>(c, W, g_out, 0, g.N, 0, edits, cap, n_edits, &nl, &st->launches, s);
+  dmtz_status es = edits_phase<D>(c, W, g_out, 0, c->g.N, 0, edits, cap, n_edits, &nl, &st->launches, s);
   if (es != DMTZ_OK) { st->status = es; return es; }
   st->n_edited = *n_edits;
   st->n_lossless = nl;
@@ -438,6 +449,235 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
   if (status == DMTZ_OK && *n_edits > cap) { status = DMTZ_E_CAPACITY; set_err("edit list needs %lld entries", (long long)*n_edits); }
   st->status = status;
   return status;
+}
+
+template <int D>
+dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
+                         char* ws, const Layout& L, float* g_out, dmtz_edit* edits, int64_t cap,
+                         int64_t* n_edits, dmtz_stats* st, cudaStream_t s) {
+  const Grid& g = c->g;
+  WS<D> W(ws, L, g);
+  dmtz_status status = setup_phase<D>(c, f, fhat, o, W, g_out, 0, &st->launches, s);
+  if (status != DMTZ_OK) { st->status = status; return status; }
+  const unsigned long long max_rounds =
+      o->max_rounds > 0 ? (unsigned long long)o->max_rounds : (unsigned long long)g.N * (unsigned long long)(o->q_cap + 1);
+  status = run_cloop<D>(c, f, fhat, o, W, ws, L, g_out, max_rounds, true, st, s);
+  if (status == DMTZ_E_CUDA) { st->status = status; return status; }
+  if (status == DMTZ_OK) {
+    loop_stats<D>(c, st);
+    status = (dmtz_status)c->host_ls->status;
+  }
+  return finish_edits<D>(c, W, g_out, status, edits, cap, n_edits, st, s);
+}
+
+// ----------------------------------------------------------------------------- tiers 3-4
+// sep_ws layout: codes scratch (N x code), tier 3: saved lb + state (N x 8), the CSR
+// of f's separatrices, per-branch first-mismatch keys, cell -> branch map, and for
+// tier 3 the CSR of g's separatrices + per-branch end flags.
+struct SepLayout {
+  size_t codes, save, off, cells, origin, term, kind, first, cb, goff, gcells, gorigin, gterm, gkind, flag, total;
+};
+
+SepLayout sep_layout(const dmtz_ctx* c, int tier, int64_t cap_b, int64_t cap_c) {
+  SepLayout S = {};
+  const size_t N = (size_t)c->g.N;
+  const size_t cs = c->D == 3 ? 8 : 2;
+  size_t o = 0;
+  S.codes = o; o += align_up(N * cs);
+  if (tier == 3) { S.save = o; o += align_up(N * 8); }
+  S.off = o; o += align_up(((size_t)cap_b + 1) * 8);
+  S.cells = o; o += align_up((size_t)cap_c * 8 + 8);
+  S.origin = o; o += align_up((size_t)cap_b * 8 + 8);
+  S.term = o; o += align_up((size_t)cap_b * 8 + 8);
+  S.kind = o; o += align_up((size_t)cap_b + 8);
+  S.first = o; o += align_up((size_t)cap_b * 4 + 8);
+  S.cb = o; o += align_up((size_t)cap_c * 4 + 8);
+  if (tier == 3) {
+    S.goff = o; o += align_up(((size_t)cap_b + 1) * 8);
+    S.gcells = o; o += align_up((size_t)cap_c * 8 + 8);
+    S.gorigin = o; o += align_up((size_t)cap_b * 8 + 8);
+    S.gterm = o; o += align_up((size_t)cap_b * 8 + 8);
+    S.gkind = o; o += align_up((size_t)cap_b + 8);
+    S.flag = o; o += align_up((size_t)cap_b + 8);
+  }
+  S.total = o;
+  return S;
+}
+
+// trace of `codes` into (off, cells, origin, term, kind) with the workspace scratch
+template <int D>
+dmtz_status trace_into(dmtz_ctx* c, char* ws, const Layout& L, const void* codes, char* sw, size_t off, size_t cells,
+                       size_t origin, size_t term, size_t kind, int64_t cap_b, int64_t cap_c, int64_t* nb,
+                       int64_t* nc, cudaStream_t s) {
+  TraceArgs a;
+  a.g = c->g;
+  a.codes = codes;
+  a.kinds = 7u;
+  a.pre = (long long*)(ws + L.cand_g);
+  a.pre_bytes = L.crit_g - L.cand_g;
+  a.bfs = (unsigned long long*)(ws + L.cand_f);
+  a.bfs_bytes = L.counters - L.cand_f;
+  a.verbose = c->verbose;
+  a.crit = (uint32_t*)(ws + L.crit_g);
+  a.bsum = (unsigned long long*)(ws + L.edit_bc);
+  a.cnt = (Counters*)(ws + L.counters);
+  a.host_cnt = c->host_cnt;
+  a.out_offsets = (int64_t*)(sw + off);
+  a.out_cells = (uint64_t*)(sw + cells);
+  a.out_origin = (uint64_t*)(sw + origin);
+  a.out_terminal = (uint64_t*)(sw + term);
+  a.out_kind = (uint8_t*)(sw + kind);
+  a.cap_b = cap_b;
+  a.cap_c = cap_c;
+  cudaError_t e = run_trace<D>(a, s);
+  if (e != cudaSuccess) { set_err("trace: %s", cudaGetErrorString(e)); return DMTZ_E_CUDA; }
+  *nb = a.n_branches;
+  *nc = a.n_cells;
+  if (a.n_internal) { set_err("trace: cycle or inconsistent gradient"); return DMTZ_E_INTERNAL; }
+  if (a.n_branches > cap_b || a.n_cells > cap_c) {
+    set_err("separatrices need %lld branches / %lld cells", (long long)a.n_branches, (long long)a.n_cells);
+    return DMTZ_E_CAPACITY;
+  }
+  if (a.n_branches >= (1ll << 32) || 3 * (a.n_cells + 1) >= (1ll << 32) - 2) { set_err("separatrix CSR too large"); return DMTZ_E_CAPACITY; }
+  return DMTZ_OK;
+}
+
+template <int D>
+dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o, char* ws,
+                          const Layout& L, char* sw, int64_t cap_b, int64_t cap_c, float* g_out, dmtz_edit* edits,
+                          int64_t cap, int64_t* n_edits, dmtz_stats* st, dmtz_sloop_stats* ss, cudaStream_t s) {
+  const Grid& g = c->g;
+  WS<D> W(ws, L, g);
+  const SepLayout S = sep_layout(c, o->tier, cap_b, cap_c);
+  const RowGeom rg = row_geom(g);
+  const size_t cs = D == 3 ? 8 : 2;
+  Counters* hc = c->host_cnt;
+  LoopState* hls = c->host_ls;
+  cudaEvent_t e0 = c->ev[0], e1 = c->ev[1];
+  int64_t nb = 0, nc = 0;
+  // the separatrices of f, once (the trace borrows the loop's workspace: before setup)
+  CK(cudaEventRecord(e0, s));
+  launch_codes<D>(g, f, sw + S.codes, 0, g.nz, s);
+  CK(cudaGetLastError());
+  dmtz_status status = trace_into<D>(c, ws, L, sw + S.codes, sw, S.off, S.cells, S.origin, S.term, S.kind, cap_b,
+                                     cap_c, &nb, &nc, s);
+  ss->sep_branches = nb;
+  ss->sep_cells = nc;
+  if (status != DMTZ_OK) { st->status = status; return status; }
+  const long long* off = (const long long*)(sw + S.off);
+  const uint64_t* cells = (const uint64_t*)(sw + S.cells);
+  const uint64_t* origin = (const uint64_t*)(sw + S.origin);
+  const uint8_t* kind = (const uint8_t*)(sw + S.kind);
+  uint32_t* first = (uint32_t*)(sw + S.first);
+  uint32_t* cb = (uint32_t*)(sw + S.cb);
+  if (nb > 0) {
+    CK(cudaMemsetAsync(&W.dc->pad[2], 0, 8, s));
+    k_cell_branch_short<<<clamp_blocks(nb, 256), 256, 0, s>>>(off, nb, cb, first, &W.dc->pad[2]);
+    k_cell_branch_long<<<148 * 8, 256, 0, s>>>(off, first, &W.dc->pad[2], cb);
+    k_fill_u32<<<clamp_blocks(nb, 256), 256, 0, s>>>(first, nb, TM_NONE);
+    CK(cudaGetLastError());
+    st->launches += 3;
+  }
+  CK(cudaEventRecord(e1, s));
+  CK(cudaEventSynchronize(e1));
+  {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    ss->trace_ms = ms;
+  }
+  status = setup_phase<D>(c, f, fhat, o, W, g_out, 0, &st->launches, s);
+  if (status != DMTZ_OK) { st->status = status; return status; }
+  const unsigned long long max_rounds =
+      o->max_rounds > 0 ? (unsigned long long)o->max_rounds : (unsigned long long)g.N * (unsigned long long)(o->q_cap + 1);
+  const bool frontier_mode = !o->full_sweeps;
+  const int64_t nwords = (int64_t)(W.rowbit_bytes / 4);
+  const float step = ldexpf(o->xi, -o->q_max);
+  const int fwords_smem = frontier_mode && L.fwords * 4 <= 32768 ? (int)L.fwords : 0;
+  int64_t c_rounds = 0;
+  unsigned long long sw_before = 0;
+  for (bool first_call = true;; first_call = false) {
+    status = run_cloop<D>(c, f, fhat, o, W, ws, L, g_out, max_rounds, first_call, st, s);
+    if (status != DMTZ_OK) { st->status = status; return status; }
+    status = (dmtz_status)hls->status;
+    c_rounds += (int64_t)(hls->sweeps - sw_before) - (status == DMTZ_OK ? 1 : 0);
+    sw_before = hls->sweeps;
+    if (status != DMTZ_OK || nb == 0) break;
+    // S-round in round r: the last sweep found no false critical cell
+    const unsigned long long r = hls->round;
+    CK(cudaEventRecord(e0, s));
+    const uint8_t* flag = nullptr;
+    if (o->tier == 3) {
+      // trace g (its codes are current) with the loop's workspace, then restore the loop state
+      CK(cudaMemcpyAsync(sw + S.codes, W.cand_g, (size_t)g.N * cs, cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(sw + S.save, W.lb, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(sw + S.save + (size_t)g.N * 4, W.state, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
+      int64_t gnb = 0, gnc = 0;
+      status = trace_into<D>(c, ws, L, sw + S.codes, sw, S.goff, S.gcells, S.gorigin, S.gterm, S.gkind, cap_b, cap_c,
+                             &gnb, &gnc, s);
+      if (status == DMTZ_OK && gnb != nb) { set_err("tier 3: %lld branches in g, %lld in f", (long long)gnb, (long long)nb); status = DMTZ_E_INTERNAL; }
+      if (status != DMTZ_OK) { st->status = status; return status; }
+      k_t3_flags<<<clamp_blocks(nb * 32, T3_WARPS * 32), T3_WARPS * 32, 0, s>>>(
+          off, cells, (const uint64_t*)(sw + S.term), kind, (const long long*)(sw + S.goff),
+          (const uint64_t*)(sw + S.gcells), (const uint64_t*)(sw + S.gterm), nb, (uint8_t*)(sw + S.flag));
+      CK(cudaMemcpyAsync(W.lb, sw + S.save, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(W.state, sw + S.save + (size_t)g.N * 4, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(W.cand_g, sw + S.codes, (size_t)g.N * cs, cudaMemcpyDeviceToDevice, s));
+      launch_codes<D>(g, f, W.cand_f, 0, g.nz, s);
+      k_critmask<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(W.cand_f, W.crit_f, g);
+      k_lowpos<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(f, W.lowpos, g);
+      CK(cudaMemsetAsync(W.tbits, 0, nwords * 4, s));
+      CK(cudaMemsetAsync(W.fmark, 0, W.rowbit_bytes, s));
+      CK(cudaMemsetAsync(W.vchg, 0, 2 * W.rowbit_bytes, s));
+      CK(cudaMemsetAsync(W.fbits, 0, (size_t)L.fwords * 4, s));
+      CK(cudaGetLastError());
+      st->launches += 4;
+      flag = (const uint8_t*)(sw + S.flag);
+    }
+    CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));
+    CK(cudaMemsetAsync(&W.dc->pad[3], 0, 4 * 8, s));
+    if (nc > 0)
+      k_tm_cells<D><<<clamp_blocks(nc, 256, 148 * 64), 256, 0, s>>>(cells, nc, cb, off, kind, W.cand_f, W.cand_g,
+                                                                    W.crit_f, g, first);
+    k_tm_targets<D><<<clamp_blocks(nb, 256, 148 * 64), 256, 0, s>>>(cells, off, kind, origin, nb, W.cand_f, W.cand_g,
+                                                                    W.crit_f, g, rg, first, flag, W.tbits, W.dc);
+    k_edit_rows<D><<<clamp_blocks(nwords, 256), 256, fwords_smem * 4, s>>>(
+        W.tbits, nwords, fhat, W.lb, g_out, W.state, W.dc, step, o->q_cap, frontier_mode ? W.fbits : nullptr, g, rg,
+        fwords_smem, frontier_mode ? W.vchg : nullptr, W.vwords, W.ls, FastDiv((uint32_t)rg.wpr),
+        FastDiv((uint32_t)g.ny));
+    CK(cudaGetLastError());
+    st->launches += 3;
+    CK(cudaEventRecord(e1, s));
+    CK(cudaMemcpyAsync(hc, W.dc, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      ss->s_ms += ms;
+    }
+    if (hc->n_internal) { set_err("troublemaker without an original partner"); status = DMTZ_E_INTERNAL; break; }
+    const int64_t ntm = (int64_t)hc->pad[3];
+    if (ntm == 0) break;  // no false separatrix (and no false critical cell): done
+    if (ss->s_rounds == 0) ss->tm_round1 = ntm;
+    ss->s_rounds++;
+    ss->troublemakers += ntm;
+    for (int k = 0; k < 3; k++) ss->tm_by_kind[k] += (int64_t)hc->pad[4 + k];
+    if (hc->n_changed == 0) { set_err("no target could move (round %llu)", r); status = DMTZ_E_STUCK; break; }
+    if (r == max_rounds) { set_err("round cap %llu reached", r); status = DMTZ_E_ITER_CAP; break; }
+    // resume the C-loop at round r + 1 over the units the edits marked
+    k_set_round<<<1, 32, 0, s>>>(W.ls, r + 1);
+    if (frontier_mode) {
+      CK(cudaMemsetAsync(&W.dc->n_units, 0, 8, s));
+      k_units_from_bits<<<clamp_blocks(rg.units, 256, 4096), 256, 0, s>>>(W.fbits, rg.units, W.units, &W.dc->n_units);
+      st->launches += 1;
+    }
+    CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));
+    CK(cudaGetLastError());
+    st->launches += 1;
+  }
+  loop_stats<D>(c, st);
+  st->rounds = c_rounds;
+  ss->c_rounds = c_rounds;
+  return finish_edits<D>(c, W, g_out, status, edits, cap, n_edits, st, s);
 }
 
 }  // namespace
@@ -725,6 +965,56 @@ dmtz_status dmtz_trace_separatrices_range(dmtz_ctx* c, const void* codes, uint32
   if (a.n_internal) { set_err("trace: cycle or inconsistent gradient"); return DMTZ_E_INTERNAL; }
   if (a.n_branches > cap_b || a.n_cells > cap_c) { set_err("trace needs %lld branches / %lld cells", (long long)a.n_branches, (long long)a.n_cells); return DMTZ_E_CAPACITY; }
   return DMTZ_OK;
+}
+
+
+size_t dmtz_preserve_sep_bytes(const dmtz_ctx* c, const dmtz_correct_opts* o, int64_t cap_b, int64_t cap_c) {
+  if (!c || !o || o->tier < 3 || cap_b < 0 || cap_c < 0) return 0;
+  return sep_layout(c, o->tier, cap_b, cap_c).total;
+}
+
+dmtz_status dmtz_preserve(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
+                          void* workspace, size_t workspace_bytes, void* sep_ws, size_t sep_ws_bytes,
+                          int64_t cap_b, int64_t cap_c, float* g_out, dmtz_edit* edits, int64_t edits_capacity,
+                          int64_t* n_edits, dmtz_stats* st, dmtz_sloop_stats* ss, dmtz_stream_t stream) {
+  if (!c || !f || !fhat || !o || !workspace || !g_out || !n_edits || !st || !ss ||
+      (edits_capacity > 0 && !edits) || edits_capacity < 0 || cap_b < 0 || cap_c < 0) {
+    set_err("NULL argument");
+    return DMTZ_E_ARG;
+  }
+  memset(ss, 0, sizeof *ss);
+  if (o->tier >= 1 && o->tier <= 2)
+    return dmtz_correct(c, f, fhat, o, workspace, workspace_bytes, g_out, edits, edits_capacity, n_edits, st, stream);
+  memset(st, 0, sizeof *st);
+  *n_edits = 0;
+  if (!(o->xi > 0.0f) || !isfinite(o->xi) || o->q_max < 0 || o->q_max > 30 || o->q_cap < 1 ||
+      o->q_cap > 65535 || o->tier < 3 || o->tier > 4 || o->max_rounds < 0) {
+    set_err("invalid options (xi=%g q_max=%d q_cap=%d tier=%d)", (double)o->xi, o->q_max, o->q_cap, o->tier);
+    st->status = DMTZ_E_ARG;
+    return DMTZ_E_ARG;
+  }
+  Layout L = layout_for(c);
+  if (workspace_bytes < L.total) {
+    set_err("workspace %zu < %zu bytes", workspace_bytes, L.total);
+    st->status = DMTZ_E_OOM;
+    return DMTZ_E_OOM;
+  }
+  const size_t need = sep_layout(c, o->tier, cap_b, cap_c).total;
+  if (!sep_ws || sep_ws_bytes < need) {
+    set_err("separatrix workspace %zu < %zu bytes", sep_ws_bytes, need);
+    st->status = DMTZ_E_OOM;
+    return DMTZ_E_OOM;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  dmtz_status r;
+  if (c->D == 3)
+    r = preserve_impl<3>(c, f, fhat, o, (char*)workspace, L, (char*)sep_ws, cap_b, cap_c, g_out, edits,
+                         edits_capacity, n_edits, st, ss, s);
+  else
+    r = preserve_impl<2>(c, f, fhat, o, (char*)workspace, L, (char*)sep_ws, cap_b, cap_c, g_out, edits,
+                         edits_capacity, n_edits, st, ss, s);
+  if (r == DMTZ_E_CUDA) st->status = r;
+  return r;
 }
 
 }  // extern "C"
