@@ -629,8 +629,10 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
       CK(cudaMemsetAsync(W.fmark, 0, W.rowbit_bytes, s));
       CK(cudaMemsetAsync(W.vchg, 0, 2 * W.rowbit_bytes, s));
       CK(cudaMemsetAsync(W.fbits, 0, (size_t)L.fwords * 4, s));
+      // the trace cleared the counters, the full-sweep unit count among them
+      if (!frontier_mode) CK(units_range(rg, 0, g.nz, W.units, &W.dc->n_units, s));
       CK(cudaGetLastError());
-      st->launches += 4;
+      st->launches += 5;
       flag = (const uint8_t*)(sw + S.flag);
     }
     CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));
