@@ -234,7 +234,9 @@ typedef struct {
   int64_t tm_round1;       /* troublemakers of the first S-round */
   double trace_ms;         /* device time: trace of f + its cell -> branch map */
   double s_ms;             /* device time summed over the S-rounds (search + edit; tier 3: + trace of g) */
-  int64_t pad[5];
+  int64_t cells_checked;   /* CSR cells whose pairing was re-evaluated, summed over the S-rounds (after
+                              the first, only cells with a code changed since the last S-round) */
+  int64_t pad[4];
 } dmtz_sloop_stats;
 
 /* Device bytes dmtz_preserve needs in `sep_ws` for separatrix CSRs of at most

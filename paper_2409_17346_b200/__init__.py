@@ -59,7 +59,7 @@ class _SStats(ctypes.Structure):
     _fields_ = [("c_rounds", ctypes.c_int64), ("s_rounds", ctypes.c_int64), ("troublemakers", ctypes.c_int64),
                 ("tm_by_kind", ctypes.c_int64 * 3), ("sep_branches", ctypes.c_int64), ("sep_cells", ctypes.c_int64),
                 ("tm_round1", ctypes.c_int64), ("trace_ms", ctypes.c_double), ("s_ms", ctypes.c_double),
-                ("pad", ctypes.c_int64 * 5)]
+                ("cells_checked", ctypes.c_int64), ("pad", ctypes.c_int64 * 4)]
 
 
 class _Seps(ctypes.Structure):
@@ -288,7 +288,8 @@ class Context:
         stats = _stats_dict(st, status)
         stats.update(c_rounds=ss.c_rounds, s_rounds=ss.s_rounds, troublemakers=ss.troublemakers,
                      tm_by_kind=list(ss.tm_by_kind), sep_branches=ss.sep_branches, sep_cells=ss.sep_cells,
-                     tm_round1=ss.tm_round1, trace_ms=ss.trace_ms, s_ms=ss.s_ms)
+                     tm_round1=ss.tm_round1, trace_ms=ss.trace_ms, s_ms=ss.s_ms,
+                     cells_checked=ss.cells_checked)
         msg = _lib.dmtz_last_error().decode() if status != OK else ""
         if raise_on_error and status not in (OK, E_STUCK, E_ITER_CAP, E_CAPACITY):
             raise DmtzError(status, msg)

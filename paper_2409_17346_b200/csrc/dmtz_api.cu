@@ -27,7 +27,7 @@ struct LoopGraph {
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr;
   // key: everything the captured body depends on
-  const void *f = nullptr, *fhat = nullptr, *g = nullptr, *ws = nullptr;
+  const void *f = nullptr, *fhat = nullptr, *g = nullptr, *ws = nullptr, *sdirty = nullptr;
   float xi = 0.f;
   int q_max = -1, q_cap = -1, tier = -1, frontier = -1;
   long long max_rounds = -1;
@@ -52,6 +52,7 @@ struct dmtz_ctx {
   LoopState* host_ls;  // pinned
   struct LoopGraph* graph;
   cudaStream_t cap_stream;  // private stream the loop body is captured on (the caller's may be the legacy stream)
+  uint32_t* sdirty = nullptr;  // dmtz_preserve: per-anchor "code changed since the last S-round" bits
 };
 
 namespace {
@@ -258,6 +259,10 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
   if (profile) CK(cudaEventRecord(c->ev[0], s));
   k_screen<D><<<sweep_blocks, SCREEN_THREADS, 0, s>>>(g_out, W.cand_g, W.ebits, W.vchg, W.vwords, use_skip, units, n_units, g,
                                            rg, W.ls, W.dc);
+  if (c->sdirty) {  // dmtz_preserve: accumulate the changed codes for the next S-round
+    k_sdirty_or<<<clamp_blocks(nwords, 256), 256, 0, s>>>(W.ebits, nwords, g, rg, c->sdirty);
+    *launches += 1;
+  }
   if (profile) CK(cudaEventRecord(c->ev[1], s));
   k_decode<D><<<sweep_blocks * 2, DECODE_THREADS, 0, s>>>(
       f, W.cand_f, W.crit_f, W.cand_g, W.ebits, W.fmark, W.tbits, dunits, n_dunits, g, rg,
@@ -350,7 +355,7 @@ dmtz_status build_loop_graph(dmtz_ctx* c, LoopGraph& G, const float* f, const fl
   CK(e);
   CK(cudaGraphInstantiate(&G.exec, G.graph, 0));
   G.f = f; G.fhat = fhat; G.g = g_out; G.ws = ws; G.xi = o->xi; G.q_max = o->q_max; G.q_cap = o->q_cap;
-  G.tier = o->tier; G.frontier = frontier_mode; G.max_rounds = (long long)max_rounds;
+  G.tier = o->tier; G.frontier = frontier_mode; G.max_rounds = (long long)max_rounds; G.sdirty = c->sdirty;
   return DMTZ_OK;
 }
 
@@ -382,7 +387,7 @@ dmtz_status run_cloop(dmtz_ctx* c, const float* f, const float* fhat, const dmtz
     LoopGraph& G = *c->graph;
     if (!G.exec || G.f != f || G.fhat != fhat || G.g != g_out || G.ws != ws || G.xi != o->xi ||
         G.q_max != o->q_max || G.q_cap != o->q_cap || G.tier != o->tier || G.frontier != (int)frontier_mode ||
-        G.max_rounds != (long long)max_rounds) {
+        G.max_rounds != (long long)max_rounds || G.sdirty != (const void*)c->sdirty) {
       status = build_loop_graph<D>(c, G, f, fhat, o, W, g_out, ws, L, max_rounds, frontier_mode, s);
       if (status != DMTZ_OK) return status;
     }
@@ -472,10 +477,12 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
 
 // ----------------------------------------------------------------------------- tiers 3-4
 // sep_ws layout: codes scratch (N x code), tier 3: saved lb + state (N x 8), the CSR
-// of f's separatrices, per-branch first-mismatch keys, cell -> branch map, and for
-// tier 3 the CSR of g's separatrices + per-branch end flags.
+// of f's separatrices, a per-branch scratch, the per-cell descriptors, the per-cell
+// mismatch bits, the per-anchor changed-code bits, and for tier 3 the CSR of g's
+// separatrices + per-branch end flags.
 struct SepLayout {
-  size_t codes, save, off, cells, origin, term, kind, first, cb, goff, gcells, gorigin, gterm, gkind, flag, total;
+  size_t codes, save, off, cells, origin, term, kind, first, cb, mbits, sdirty, sdil, goff, gcells, gorigin, gterm, gkind,
+      flag, total;
 };
 
 SepLayout sep_layout(const dmtz_ctx* c, int tier, int64_t cap_b, int64_t cap_c) {
@@ -491,7 +498,10 @@ SepLayout sep_layout(const dmtz_ctx* c, int tier, int64_t cap_b, int64_t cap_c) 
   S.term = o; o += align_up((size_t)cap_b * 8 + 8);
   S.kind = o; o += align_up((size_t)cap_b + 8);
   S.first = o; o += align_up((size_t)cap_b * 4 + 8);
-  S.cb = o; o += align_up((size_t)cap_c * 4 + 8);
+  S.cb = o; o += align_up((size_t)cap_c + 8);  // per-cell descriptors
+  S.mbits = o; o += align_up((size_t)cap_c / 8 + 8);
+  S.sdirty = o; o += align_up(N / 8 + 8);
+  S.sdil = o; o += align_up(N / 8 + 8);
   if (tier == 3) {
     S.goff = o; o += align_up(((size_t)cap_b + 1) * 8);
     S.gcells = o; o += align_up((size_t)cap_c * 8 + 8);
@@ -538,7 +548,7 @@ dmtz_status trace_into(dmtz_ctx* c, char* ws, const Layout& L, const void* codes
     set_err("separatrices need %lld branches / %lld cells", (long long)a.n_branches, (long long)a.n_cells);
     return DMTZ_E_CAPACITY;
   }
-  if (a.n_branches >= (1ll << 32) || 3 * (a.n_cells + 1) >= (1ll << 32) - 2) { set_err("separatrix CSR too large"); return DMTZ_E_CAPACITY; }
+  if (a.n_branches >= (1ll << 32)) { set_err("more than 2^32 separatrix branches"); return DMTZ_E_CAPACITY; }
   return DMTZ_OK;
 }
 
@@ -568,15 +578,18 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
   const uint64_t* cells = (const uint64_t*)(sw + S.cells);
   const uint64_t* origin = (const uint64_t*)(sw + S.origin);
   const uint8_t* kind = (const uint8_t*)(sw + S.kind);
-  uint32_t* first = (uint32_t*)(sw + S.first);
-  uint32_t* cb = (uint32_t*)(sw + S.cb);
+  uint32_t* first = (uint32_t*)(sw + S.first);  // the list of long branches, then per-branch origin mismatches
+  uint32_t* mbits = (uint32_t*)(sw + S.mbits);
+  uint32_t* sdirty = (uint32_t*)(sw + S.sdirty);
+  uint32_t* sdil = (uint32_t*)(sw + S.sdil);
+  const int64_t dwords = (g.N + 31) / 32;
+  uint8_t* desc = (uint8_t*)(sw + S.cb);
   if (nb > 0) {
     CK(cudaMemsetAsync(&W.dc->pad[2], 0, 8, s));
-    k_cell_branch_short<<<clamp_blocks(nb, 256), 256, 0, s>>>(off, nb, cb, first, &W.dc->pad[2]);
-    k_cell_branch_long<<<148 * 8, 256, 0, s>>>(off, first, &W.dc->pad[2], cb);
-    k_fill_u32<<<clamp_blocks(nb, 256), 256, 0, s>>>(first, nb, TM_NONE);
+    k_cell_desc_short<<<clamp_blocks(nb, 256), 256, 0, s>>>(off, kind, cells, nb, desc, first, &W.dc->pad[2]);
+    k_cell_desc_long<<<148 * 8, 256, 0, s>>>(off, kind, cells, first, &W.dc->pad[2], desc);
     CK(cudaGetLastError());
-    st->launches += 3;
+    st->launches += 2;
   }
   CK(cudaEventRecord(e1, s));
   CK(cudaEventSynchronize(e1));
@@ -595,6 +608,11 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
   const int fwords_smem = frontier_mode && L.fwords * 4 <= 32768 ? (int)L.fwords : 0;
   int64_t c_rounds = 0;
   unsigned long long sw_before = 0;
+  if (nb > 0) {
+    CK(cudaMemsetAsync(sdirty, 0, (size_t)g.N / 8 + 8, s));
+    c->sdirty = sdirty;
+  }
+  struct Reset { dmtz_ctx* c; ~Reset() { c->sdirty = nullptr; } } reset{c};
   for (bool first_call = true;; first_call = false) {
     status = run_cloop<D>(c, f, fhat, o, W, ws, L, g_out, max_rounds, first_call, st, s);
     if (status != DMTZ_OK) { st->status = status; return status; }
@@ -636,12 +654,22 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
       flag = (const uint8_t*)(sw + S.flag);
     }
     CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));
-    CK(cudaMemsetAsync(&W.dc->pad[3], 0, 4 * 8, s));
-    if (nc > 0)
-      k_tm_cells<D><<<clamp_blocks(nc, 256, 148 * 64), 256, 0, s>>>(cells, nc, cb, off, kind, W.cand_f, W.cand_g,
-                                                                    W.crit_f, g, first);
+    CK(cudaMemsetAsync(&W.dc->pad[3], 0, 5 * 8, s));
+    const int full = ss->s_rounds == 0 ? 1 : 0;
+    if (!full) {
+      k_sdirty_dilate<<<clamp_blocks(dwords, 256), 256, 0, s>>>(sdirty, dwords, g.sy, g.sz, sdil);
+      st->launches += 1;
+    }
+    if (nc > 0) {
+      const int64_t nblk = ((nc + 31) / 32 + 8 * TM_U - 1) / (8 * TM_U);  // 8 warps x TM_U words per block
+      k_tm_cells<D><<<(unsigned)nblk, 256, 0, s>>>(cells, nc, desc, W.cand_f, W.cand_g, W.crit_f, g, sdil, full,
+                                                   mbits, W.dc);
+    }
     k_tm_targets<D><<<clamp_blocks(nb, 256, 148 * 64), 256, 0, s>>>(cells, off, kind, origin, nb, W.cand_f, W.cand_g,
-                                                                    W.crit_f, g, rg, first, flag, W.tbits, W.dc);
+                                                                    W.crit_f, g, rg, mbits, flag, sdil, full,
+                                                                    (uint8_t*)first,
+                                                                    W.tbits, W.dc);
+    CK(cudaMemsetAsync(sdirty, 0, (size_t)g.N / 8 + 8, s));
     k_edit_rows<D><<<clamp_blocks(nwords, 256), 256, fwords_smem * 4, s>>>(
         W.tbits, nwords, fhat, W.lb, g_out, W.state, W.dc, step, o->q_cap, frontier_mode ? W.fbits : nullptr, g, rg,
         fwords_smem, frontier_mode ? W.vchg : nullptr, W.vwords, W.ls, FastDiv((uint32_t)rg.wpr),
@@ -663,6 +691,7 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
     ss->s_rounds++;
     ss->troublemakers += ntm;
     for (int k = 0; k < 3; k++) ss->tm_by_kind[k] += (int64_t)hc->pad[4 + k];
+    ss->cells_checked += (int64_t)hc->pad[7];
     if (hc->n_changed == 0) { set_err("no target could move (round %llu)", r); status = DMTZ_E_STUCK; break; }
     if (r == max_rounds) { set_err("round cap %llu reached", r); status = DMTZ_E_ITER_CAP; break; }
     // resume the C-loop at round r + 1 over the units the edits marked

@@ -14,10 +14,10 @@
 //   CONN  event log of the BFS     : the triangles in queue order (the origin, then the
 //         logged triangles), and of each its 3 facet edges in facet order, f-critical
 //         edges skipped.
-// "First" is found cell-parallel: k_tm_cells (one thread per CSR cell) takes an
-// atomicMin of the cell's position key into its branch's slot; k_tm_targets (one
-// thread per branch) turns the winning key into the target.  The branch of each
-// CSR cell is precomputed once (k_cell_branch_*).
+// "First" is found in two steps: k_tm_cells keeps one mismatch bit per CSR cell
+// (re-evaluating only cells whose codes changed since the last S-round), and
+// k_tm_targets (one thread per branch) takes the first set bit of its range.  Which
+// cells are examined is precomputed once per CSR cell (k_cell_desc_*).
 #pragma once
 
 #include "dmtz_kernels.cuh"
@@ -26,32 +26,42 @@
 
 namespace dmtz {
 
-constexpr uint32_t TM_NONE = 0xFFFFFFFFu;
+// ----------------------------------------------------------------------------- per-cell descriptors
+// desc[i] (one byte per CSR cell, built once): 0 = not examined; else the branch
+// kind (1 DESC vertex before the minimum, 2 ASC (top-1)-cell, 4 CONN logged
+// triangle).  Branches of at most 32 cells are done by their own thread; longer ones
+// are listed (long_list) and done by a warp each.
+__device__ __forceinline__ uint8_t cell_desc(int k, int64_t pos, int64_t len, uint64_t id) {
+  if (k == 1) return (!(pos & 1) && pos + 1 < len) ? 1 : 0;
+  if (k == 2) return (pos & 1) ? 2 : 0;
+  return (id >> 56) == 2 ? 4 : 0;
+}
 
-// ----------------------------------------------------------------------------- cell -> branch
-// Branches of at most 32 cells are filled by their own thread; longer ones are
-// listed (long_list) and filled by a warp each.
-__global__ void k_cell_branch_short(const long long* __restrict__ off, int64_t nb, uint32_t* __restrict__ cb,
-                                    uint32_t* __restrict__ long_list, unsigned long long* __restrict__ n_long) {
+__global__ void k_cell_desc_short(const long long* __restrict__ off, const uint8_t* __restrict__ kind,
+                                  const uint64_t* __restrict__ cells, int64_t nb, uint8_t* __restrict__ desc,
+                                  uint32_t* __restrict__ long_list, unsigned long long* __restrict__ n_long) {
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i0 = off[b], i1 = off[b + 1];
+    const int k = kind[b];
     if (i1 - i0 <= 32) {
-      for (int64_t i = i0; i < i1; i++) cb[i] = (uint32_t)b;
+      for (int64_t i = i0; i < i1; i++) desc[i] = cell_desc(k, i - i0, i1 - i0, cells[i]);
     } else {
       long_list[atomicAdd(n_long, 1ull)] = (uint32_t)b;
     }
   }
 }
 
-__global__ void k_cell_branch_long(const long long* __restrict__ off, const uint32_t* __restrict__ long_list,
-                                   const unsigned long long* __restrict__ n_long, uint32_t* __restrict__ cb) {
+__global__ void k_cell_desc_long(const long long* __restrict__ off, const uint8_t* __restrict__ kind,
+                                 const uint64_t* __restrict__ cells, const uint32_t* __restrict__ long_list,
+                                 const unsigned long long* __restrict__ n_long, uint8_t* __restrict__ desc) {
   const int lane = threadIdx.x & 31;
   const int64_t n = (int64_t)*n_long;
   for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n;
        w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const uint32_t b = long_list[w];
     const int64_t i0 = off[b], i1 = off[b + 1];
-    for (int64_t i = i0 + lane; i < i1; i += 32) cb[i] = b;
+    const int k = kind[b];
+    for (int64_t i = i0 + lane; i < i1; i += 32) desc[i] = cell_desc(k, i - i0, i1 - i0, cells[i]);
   }
 }
 
@@ -96,84 +106,151 @@ __device__ __forceinline__ int64_t r1_target(const void* cf, const Grid& g, int6
   return A + mask_delta(g, t_vmask<D>(t, t_facet<D>(t, j, 3)));  // facet j omits vertex t_facet(t, j, 3)
 }
 
-// ----------------------------------------------------------------------------- per-cell keys
-// key of a mismatch: DESC / ASC: the cell's position in its branch; CONN: 3 * (queue
-// position) + facet, queue position 0 = the origin (k_tm_targets), logged triangle at
-// branch position p -> queue position p + 1.
+// ----------------------------------------------------------------------------- per-cell mismatch bits
+// mbits (one bit per CSR cell, persistent across S-rounds): the cell is examined
+// (see the header) and its pairing in g differs from f's -- for a CONN triangle:
+// one of its facet edges that is not critical in f does.  A cell's bit depends
+// only on the codes of g at a few anchors (DESC vertex v: v; ASC cell: its anchor;
+// CONN triangle at B: each facet edge's anchor and second vertex, all in
+// B + {0,1,2}^3), so after the first S-round (full = 1) only cells whose anchor has
+// a changed code in that window since the last S-round (sdirty, fed by every round's
+// changed-code bits, dilated by k_sdirty_dilate) are re-evaluated; the others keep
+// their bit exactly.
+// id_cell with compile-time divisors (multiply-high instead of a 64-bit division)
 template <int D>
-__global__ void k_tm_cells(const uint64_t* __restrict__ cells, int64_t n_cells, const uint32_t* __restrict__ cb,
-                           const long long* __restrict__ off, const uint8_t* __restrict__ kind,
-                           const void* __restrict__ cf, const void* __restrict__ cg,
-                           const uint32_t* __restrict__ crit_f, Grid g, uint32_t* __restrict__ first) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_cells;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t b = cb[i];
-    const int k = kind[b];
-    const int64_t i0 = off[b];
-    const int64_t pos = i - i0;
-    const uint64_t id = cells[i];
-    const int d = (int)(id >> 56);
-    uint32_t key = TM_NONE;
-    if (k == 1) {  // DESC: vertices at even positions, not the minimum at the end
-      if ((pos & 1) || i + 1 >= off[b + 1]) continue;
-      int64_t A; int t;
-      id_cell<D>(id, A, t);
-      if (pair_differs<D>(cf, cg, g, A, t)) key = (uint32_t)pos;
-    } else if (k == 2) {  // ASC: (top-1)-cells at odd positions
-      if (!(pos & 1)) continue;
-      int64_t A; int t;
-      id_cell<D>(id, A, t);
-      if (pair_differs<D>(cf, cg, g, A, t)) key = (uint32_t)pos;
-    } else {  // CONN: the facet edges of a logged triangle
-      if (d != 2) continue;
-      int64_t B; int bt;
-      id_cell<D>(id, B, bt);
-      for (int j = 0; j < 3; j++) {
-        const int64_t E = B + mask_delta(g, t_facet<D>(bt, j, 0));
-        const int et = t_facet<D>(bt, j, 1);
-        if ((__ldg(crit_f + E) >> et) & 1u) continue;
-        if (pair_differs<D>(cf, cg, g, E, et)) { key = (uint32_t)(3 * (pos + 1) + j); break; }
-      }
-    }
-    if (key != TM_NONE && key < first[b]) atomicMin(first + b, key);
+__device__ __forceinline__ void id_cell_fast(uint64_t id, int64_t& a, int& t) {
+  const int d = (int)(id >> 56);
+  const uint64_t r = id & ((1ull << 56) - 1);
+  uint64_t q;
+  if (D == 3) q = d == 0 ? r : d == 1 ? r / 7u : d == 2 ? r / 12u : r / 6u;
+  else q = d == 0 ? r : d == 1 ? r / 3u : r / 2u;
+  a = (int64_t)q;
+  t = t_first_of_dim_c<D>(d) + (int)(r - q * (uint64_t)types_of_dim<D>(d));
+}
+
+__device__ __forceinline__ bool dbit(const uint32_t* __restrict__ d, int64_t v) {
+  return (__ldg(d + (v >> 5)) >> (v & 31)) & 1u;
+}
+
+template <int D>
+__device__ __forceinline__ bool conn_tri_differs(const void* cf, const void* cg, const uint32_t* __restrict__ crit_f,
+                                                 const Grid& g, int64_t B, int bt, int* jfirst) {
+  for (int j = 0; j < 3; j++) {
+    const int64_t E = B + mask_delta(g, t_facet<D>(bt, j, 0));
+    const int et = t_facet<D>(bt, j, 1);
+    if ((__ldg(crit_f + E) >> et) & 1u) continue;
+    if (pair_differs<D>(cf, cg, g, E, et)) { *jfirst = j; return true; }
   }
+  return false;
+}
+
+// A warp takes TM_U consecutive mbits words (32 x TM_U cells, one per lane per word)
+// and issues every load of the batch before using any (the kernel is bound by the
+// latency of its dependent loads otherwise).
+constexpr int TM_U = 4;
+template <int D>
+__global__ void __launch_bounds__(256)
+k_tm_cells(const uint64_t* __restrict__ cells, int64_t n_cells, const uint8_t* __restrict__ desc,
+           const void* __restrict__ cf, const void* __restrict__ cg, const uint32_t* __restrict__ crit_f, Grid g,
+           const uint32_t* __restrict__ sdirty /* dilated */, int full, uint32_t* __restrict__ mbits,
+           Counters* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * TM_U;  // first word of the warp
+  int k[TM_U];
+  uint64_t id[TM_U];
+#pragma unroll
+  for (int u = 0; u < TM_U; u++) {
+    const int64_t i = (w0 + u) * 32 + lane;
+    k[u] = i < n_cells ? __ldg(desc + i) : 0;
+  }
+#pragma unroll
+  for (int u = 0; u < TM_U; u++) {
+    const int64_t i = (w0 + u) * 32 + lane;
+    id[u] = k[u] ? __ldg(cells + i) : 0ull;
+  }
+  int64_t A[TM_U];
+  int t[TM_U];
+  bool dirty[TM_U];
+#pragma unroll
+  for (int u = 0; u < TM_U; u++) {
+    id_cell_fast<D>(id[u], A[u], t[u]);
+    dirty[u] = full ? ((w0 + u) * 32 + lane < n_cells) : (k[u] && dbit(sdirty, A[u]));
+  }
+  unsigned long long nre = 0;
+#pragma unroll
+  for (int u = 0; u < TM_U; u++) {
+    bool mis = false;
+    if (k[u] && dirty[u]) {
+      nre++;
+      int j;
+      mis = k[u] == 4 ? conn_tri_differs<D>(cf, cg, crit_f, g, A[u], t[u], &j) : pair_differs<D>(cf, cg, g, A[u], t[u]);
+    }
+    const unsigned dm = __ballot_sync(0xffffffffu, dirty[u]), mm = __ballot_sync(0xffffffffu, mis);
+    if (lane == 0 && dm) {
+      uint32_t* w = mbits + w0 + u;
+      *w = (*w & ~dm) | mm;
+    }
+  }
+  warp_add(&cnt->pad[7], nre);
+}
+
+// first set bit of mbits in [i0, i1), or -1
+__device__ __forceinline__ int64_t first_bit(const uint32_t* __restrict__ mbits, int64_t i0, int64_t i1) {
+  for (int64_t w = i0 >> 5; (w << 5) < i1; w++) {
+    uint32_t m = mbits[w];
+    const int64_t lo = w << 5;
+    if (lo < i0) m &= ~0u << (i0 - lo);
+    if (lo + 32 > i1) m &= (i1 - lo) >= 32 ? ~0u : ((1u << (i1 - lo)) - 1u);
+    if (m) return lo + __ffs(m) - 1;
+  }
+  return -1;
 }
 
 // ----------------------------------------------------------------------------- per-branch targets
-// cnt->pad[3] += troublemakers, cnt->pad[4 + kind index] += per kind; first[] reset.
+// One thread per branch: its troublemaker = the first set mismatch bit (CONN: the
+// origin's facets first), its target -> the round's target bitmap.
+// cnt->pad[3] += troublemakers, cnt->pad[4 + kind index] += per kind.
 // flag (tier 3, else nullptr): only branches with flag[b] != 0 count.
 template <int D>
 __global__ void k_tm_targets(const uint64_t* __restrict__ cells, const long long* __restrict__ off,
                              const uint8_t* __restrict__ kind, const uint64_t* __restrict__ origin, int64_t nb,
                              const void* __restrict__ cf, const void* __restrict__ cg,
-                             const uint32_t* __restrict__ crit_f, Grid g, RowGeom rg, uint32_t* __restrict__ first,
-                             const uint8_t* __restrict__ flag, uint32_t* __restrict__ tbits,
-                             Counters* __restrict__ cnt) {
+                             const uint32_t* __restrict__ crit_f, Grid g, RowGeom rg,
+                             const uint32_t* __restrict__ mbits, const uint8_t* __restrict__ flag,
+                             const uint32_t* __restrict__ sdirty, int full, uint8_t* __restrict__ omis,
+                             uint32_t* __restrict__ tbits, Counters* __restrict__ cnt) {
   unsigned long long ntm = 0, nk[3] = {0, 0, 0}, bad = 0;
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t key = first[b];
-    if (key != TM_NONE) first[b] = TM_NONE;
-    if (flag && !flag[b]) continue;  // tier 3: this branch ends where it ends in f
     const int k = kind[b];
     int64_t A = -1;
     int t = 0;
     if (k == 4) {
       int64_t B; int bt;
-      id_cell<D>(origin[b], B, bt);
-      for (int j = 0; j < 3; j++) {  // the origin's facets come first (queue position 0)
-        const int64_t E = B + mask_delta(g, t_facet<D>(bt, j, 0));
-        const int et = t_facet<D>(bt, j, 1);
-        if ((__ldg(crit_f + E) >> et) & 1u) continue;
-        if (pair_differs<D>(cf, cg, g, E, et)) { key = (uint32_t)j; break; }
+      id_cell_fast<D>(origin[b], B, bt);
+      int j = -1;
+      // the origin's facets come first; their mismatch (omis) is kept like mbits
+      bool om;
+      if (full || dbit(sdirty, B)) {
+        om = conn_tri_differs<D>(cf, cg, crit_f, g, B, bt, &j);
+        omis[b] = om;
+      } else {
+        om = omis[b] != 0;
+        if (om && !conn_tri_differs<D>(cf, cg, crit_f, g, B, bt, &j)) { bad++; continue; }
       }
-      if (key == TM_NONE) continue;
-      const uint32_t qp = key / 3, j = key - qp * 3;
-      if (qp > 0) id_cell<D>(cells[off[b] + qp - 1], B, bt);
-      A = B + mask_delta(g, t_facet<D>(bt, (int)j, 0));
-      t = t_facet<D>(bt, (int)j, 1);
+      if (flag && !flag[b]) continue;  // tier 3: this branch ends where it ends in f
+      if (!om) {
+        const int64_t i = first_bit(mbits, off[b], off[b + 1]);
+        if (i < 0) continue;
+        id_cell_fast<D>(cells[i], B, bt);
+        if (!conn_tri_differs<D>(cf, cg, crit_f, g, B, bt, &j)) { bad++; continue; }
+      }
+      A = B + mask_delta(g, t_facet<D>(bt, j, 0));
+      t = t_facet<D>(bt, j, 1);
     } else {
-      if (key == TM_NONE) continue;
-      id_cell<D>(cells[off[b] + key], A, t);
+      if (flag && !flag[b]) continue;  // tier 3: this branch ends where it ends in f
+      const int64_t i = first_bit(mbits, off[b], off[b + 1]);
+      if (i < 0) continue;
+      id_cell_fast<D>(cells[i], A, t);
     }
     const int64_t v = r1_target<D>(cf, g, A, t);
     if (v < 0) { bad++; continue; }
@@ -188,6 +265,52 @@ __global__ void k_tm_targets(const uint64_t* __restrict__ cells, const long long
   warp_add(&cnt->pad[5], nk[1]);
   warp_add(&cnt->pad[6], nk[2]);
   warp_add(&cnt->n_internal, bad);
+}
+
+// dil(A) = OR of changed(A + dx + dy*nx + dz*nx*ny) over (dx, dy, dz) in {0,1,2}^3, in the
+// linear bit space (offsets that wrap across a row or plane only add positions): a
+// superset of every anchor a cell's mismatch bit reads (DESC/ASC: the cell's anchor;
+// CONN: facet edges at A + {0,1}^3 and their second vertices), so one bit decides
+// whether a cell must be re-evaluated.
+__global__ void k_sdirty_dilate(const uint32_t* __restrict__ chg, int64_t nwords, int64_t sy, int64_t sz,
+                                uint32_t* __restrict__ dil) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t acc = 0;
+#pragma unroll
+    for (int dz = 0; dz < 3; dz++)
+#pragma unroll
+      for (int dy = 0; dy < 3; dy++) {
+        const int64_t o = dy * sy + dz * sz;       // bits w*32 + o + (0..2) + lane
+        const int64_t b = w * 32 + o;
+        const int64_t q = b >> 5;
+        const int r = (int)(b & 31);
+        const uint32_t lo = q < nwords ? __ldg(chg + q) : 0u, hi = q + 1 < nwords ? __ldg(chg + q + 1) : 0u;
+        const uint32_t h2 = q + 1 < nwords && r > 29 ? (q + 2 < nwords ? __ldg(chg + q + 2) : 0u) : 0u;
+        // 64-bit window starting at bit b: bits b .. b + 63 (enough for + 0..2 when r <= 29)
+        const unsigned long long win = ((unsigned long long)hi << 32 | lo) >> r;
+        const unsigned long long ext = r > 29 ? (unsigned long long)h2 << (64 - r) : 0ull;
+        const unsigned long long x = win | ext;
+        acc |= (uint32_t)(x | (x >> 1) | (x >> 2));
+      }
+    dil[w] = acc;
+  }
+}
+
+// changed-code bits of a round (row-padded words) -> the linear per-anchor bitmap sdirty
+__global__ void k_sdirty_or(const uint32_t* __restrict__ ebits, int64_t nwords, Grid g, RowGeom rg,
+                            uint32_t* __restrict__ sdirty) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t m = ebits[w];
+    if (!m) continue;
+    const int64_t row = w / rg.wpr, c = w - row * rg.wpr;
+    const int64_t v0 = row * g.nx + c * 32;
+    while (m) {
+      const int bit = __ffs(m) - 1;
+      m &= m - 1;
+      const int64_t v = v0 + bit;
+      atomicOr(sdirty + (v >> 5), 1u << (v & 31));
+    }
+  }
 }
 
 }  // namespace dmtz
