@@ -156,6 +156,56 @@ def run_reference(args, cfg, f, fh, xi):
     print(json.dumps(line), flush=True)
 
 
+def sloop_line(name, dev, stream, with_cpu):
+    """Tiers 3-4: the alternating C/S workflow to its fixed point on
+    one config, device-resident inputs, CUDA events on the launching stream (1 warm-up,
+    median of 2), and the oracle's workflow on a crop of the same config."""
+    import torch
+    import paper_2409_17346_b200 as dmtz
+    f, fh, xi, cfg = di.config_inputs(name)
+    ft, fht = torch.from_numpy(f).to(dev), torch.from_numpy(fh).to(dev)
+    ctx = dmtz.Context(f.shape, dev)
+    out = {"workload": f"{cfg.name} {cfg.family} {'x'.join(map(str, f.shape))} rel eps {cfg.eps}"}
+    for tier in (4, 3):
+        ctx.preserve(ft, fht, xi, tier=tier)
+        ts = []
+        for _ in range(2):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = ctx.preserve(ft, fht, xi, tier=tier)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = float(np.median(ts))
+        s = r.stats
+        rounds = s["c_rounds"] + s["s_rounds"]
+        out[f"tier{tier}"] = {
+            "status": r.status, "time_to_fixed_point_ms": ms,
+            "value": f.size * (rounds + 1) / (ms * 1e-3) / 1e6, "unit": "Mvoxels/s (voxels x rounds / time)",
+            "c_rounds": s["c_rounds"], "s_rounds": s["s_rounds"], "troublemakers": s["troublemakers"],
+            "tm_by_kind": s["tm_by_kind"], "n_edited": r.n_edits, "sep_branches": s["sep_branches"],
+            "sep_cells": s["sep_cells"], "trace_of_f_ms": s["trace_ms"], "s_rounds_ms": s["s_ms"],
+            "cells_rechecked": s["cells_checked"]}
+    del ctx
+    torch.cuda.empty_cache()
+    if with_cpu:
+        import oracle
+        crop = tuple(min(n, 96) for n in f.shape) if len(f.shape) == 3 else tuple(min(n, 240) for n in f.shape)
+        sl = tuple(slice(0, n) for n in crop)
+        fc, fhc = np.ascontiguousarray(f[sl]), np.ascontiguousarray(fh[sl])
+        t0 = time.perf_counter()
+        ro = oracle.preserve(fc, fhc, xi, tier=4)
+        dt = time.perf_counter() - t0
+        so = ro["stats"]
+        n = fc.size * (so["c_rounds"] + so["s_rounds"] + 1)
+        out["cpu_baseline"] = {"value": n / dt / 1e6, "unit": "Mvoxels/s (voxels x rounds / time)",
+                               "cores": oracle.num_threads(), "kind": "oracle",
+                               "sample": f"oracle tier-4 workflow on the {list(crop)} crop of {cfg.name} "
+                                         f"({so['c_rounds']} C- + {so['s_rounds']} S-rounds in {dt:.1f} s)"}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -169,6 +219,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-trace", action="store_true")
     ap.add_argument("--slab", action="store_true", help="run the multi-GPU slab path even with one rank")
+    ap.add_argument("--sloop-config", default="C2", help="config of the tier-3/4 workflow line ('none' skips it)")
     args = ap.parse_args()
     if args.impl == "dmtz":
         args.warmup = max(args.warmup, 3)
@@ -336,6 +387,12 @@ def main():
                "sample": f"oracle C-loop to its fixed point on the {s['shape']} crop of {cfg.name} "
                          f"({s['sweeps']} sweeps in {s['seconds']:.1f} s)"}
 
+    sloop = None
+    if args.sloop_config != "none":
+        del ctx
+        torch.cuda.empty_cache()
+        sloop = sloop_line(args.sloop_config, dev, stream, not args.no_cpu_baseline)
+
     st = r.stats
     line = {
         "metric": METRIC, "value": value, "unit": "Mvoxels/s", "n_gpus": world,
@@ -346,7 +403,7 @@ def main():
                    "mode": "default: dirty frontier + exact change skipping (bit-identical to full_sweeps=1)",
                    "l2": "inputs larger than L2 (2 x 537 MB)", "parallelism": "1 GPU"},
         "roofline": roof, "roofline_screen": roof_screen, "cpu_baseline": cpu, "e2e": e2e, "time_to_fixed_point": frontier,
-        "full_recompute": full_recompute, "trace": trace,
+        "full_recompute": full_recompute, "trace": trace, "sloop": sloop,
         "gpu_launches": st["launches"],
         "clocks": clk.summary(),
         "stats": {k: st[k] for k in ("rounds", "sweeps", "n_edited", "n_quantized", "n_lossless", "n_false_round0",
