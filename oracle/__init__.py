@@ -70,6 +70,8 @@ def lib():
         L.dmtz_oracle_preserve.argtypes = [P, P, P, ctypes.c_float, ctypes.c_int32, ctypes.c_int32,
                                            ctypes.c_int32, i64, P, P, P, i64, P,
                                            ctypes.POINTER(_Stats), ctypes.POINTER(_SStats)]
+        L.dmtz_oracle_persistence0.argtypes = [P, P, P, i64]
+        L.dmtz_oracle_persistence0.restype = ctypes.c_int64
         L.dmtz_oracle_trace.argtypes = [P, P, ctypes.c_uint32, i64, i64, P, P, P, P, P, P, P]
         L.dmtz_oracle_slab_round.argtypes = [P, P, P, ctypes.c_float, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                              i64, i64, i64, i64, P, P, P, P]
@@ -159,7 +161,7 @@ def correct(f: np.ndarray, fhat: np.ndarray, xi: float, q_max: int = 6, q_cap: i
 
 def preserve(f: np.ndarray, fhat: np.ndarray, xi: float, tier: int = 4, q_max: int = 6,
              q_cap: int | None = None, max_rounds: int = 0, edits_capacity: int | None = None):
-    """Literal alternating C-/S-loop workflow (tiers 1-4).  Returns dict(status, g, state,
+    """Literal alternating C-/S-loop workflow (tiers 1-5; 5 = pre-clamp + tier 4).  Returns dict(status, g, state,
     edits, stats) with stats also holding c_rounds, s_rounds, troublemakers, tm_by_kind,
     sep_branches, sep_cells, tm_round1."""
     f = np.ascontiguousarray(f, dtype=np.float32)
@@ -186,6 +188,16 @@ def preserve(f: np.ndarray, fhat: np.ndarray, xi: float, tier: int = 4, q_max: i
     out["tm_by_kind"] = list(ss.tm_by_kind)
     return dict(status=st, g=g, state=state, edits=edits[:min(ne.value, cap)].copy(),
                 n_edits=ne.value, stats=out)
+
+
+def persistence0(field: np.ndarray) -> np.ndarray:
+    """0-dim sublevel persistence pairs (birth vertex, death vertex), union-find + elder rule."""
+    field = np.ascontiguousarray(field, dtype=np.float32)
+    d = _dims(field.shape)
+    n = lib().dmtz_oracle_persistence0(_p(d), _p(field), None, 0)
+    out = np.zeros((max(n, 1), 2), np.int64)
+    lib().dmtz_oracle_persistence0(_p(d), _p(field), _p(out), n)
+    return out[:n]
 
 
 def trace(field: np.ndarray, kinds: int = KIND_DESC | KIND_ASC | KIND_CONN,

@@ -944,7 +944,7 @@ int dmtz_oracle_preserve(const int64_t* dims, const float* f, const float* fhat,
   int st = check_dims(dims);
   if (st) { stats->status = st; return st; }
   if (!(xi > 0.0f) || !isfinite(xi) || q_max < 0 || q_max > 30 || q_cap < 1 || q_cap > 65535 ||
-      tier < 1 || tier > 4 || max_rounds < 0) {
+      tier < 1 || tier > 5 || max_rounds < 0) {
     stats->status = OR_E_ARG; return OR_E_ARG;
   }
   cx_t cx; build_complex(&cx, dims[0], dims[1], dims[2]);
@@ -967,6 +967,19 @@ int dmtz_oracle_preserve(const int64_t* dims, const float* f, const float* fhat,
   }
   for (int64_t v = 0; v < N; v++) { lb[v] = lower_bound_ru(f[v], xi); g_out[v] = fhat[v]; }
   gradient(&cx, f, &Gf);
+  if (tier == 5) {
+    /* T5: "we edit the scalar values of all vertices that constitute the
+     * critical cells in the original data to their lower bound f - xi before the
+     * iterative process begins"; stored losslessly.  Then the tier-4 workflow. */
+    for (int64_t A = 0; A < N; A++)
+      for (int ti = 0; ti < cx.T; ti++) {
+        if (!is_crit(&cx, &Gf, A, ti)) continue;
+        int64_t vs[4];
+        cell_vertices(&cx, A, ti, vs);
+        for (int k = 0; k <= cx.t[ti].dim; k++) { g_out[vs[k]] = lb[vs[k]]; lossless[vs[k]] = 1; }
+      }
+    tier = 4;
+  }
   const uint32_t all = KIND_DESC | KIND_ASC | KIND_CONN;
   csr_t Sf = {0}, Sg = {0};
   int status = OR_OK;
@@ -1049,6 +1062,59 @@ int dmtz_oracle_preserve(const int64_t* dims, const float* f, const float* fhat,
   grad_free(&Gf); grad_free(&Gg);
   csr_free(&Sf); csr_free(&Sg);
   return status;
+}
+
+/* ------------------------------------------------------------------------- */
+/* 0-dimensional persistence of the sublevel filtration (tier 5's check,       */
+/* P:143 "persistence diagram"): vertices in SoS order, union-find   */
+/* over the edges of the complex, elder rule.  pairs[2k], pairs[2k+1] = (birth  */
+/* vertex, death vertex) of each finite pair; returns the number of pairs.      */
+/* ------------------------------------------------------------------------- */
+static int64_t uf_find(int64_t* parent, int64_t x) {
+  while (parent[x] != x) { parent[x] = parent[parent[x]]; x = parent[x]; }
+  return x;
+}
+static const float* g_sort_f;
+static int cmp_sos(const void* a, const void* b) {
+  int64_t u = *(const int64_t*)a, v = *(const int64_t*)b;
+  return sos_less(g_sort_f, u, v) ? -1 : sos_less(g_sort_f, v, u) ? 1 : 0;
+}
+int64_t dmtz_oracle_persistence0(const int64_t* dims, const float* field, int64_t* pairs, int64_t cap) {
+  if (check_dims(dims)) return -1;
+  cx_t cx; build_complex(&cx, dims[0], dims[1], dims[2]);
+  int64_t N = cx.N;
+  int64_t* order = (int64_t*)malloc(sizeof(int64_t) * N);
+  int64_t* parent = (int64_t*)malloc(sizeof(int64_t) * N);
+  int64_t* root_birth = (int64_t*)malloc(sizeof(int64_t) * N);  /* oldest vertex of a root's component */
+  uint8_t* in = (uint8_t*)calloc(N, 1);
+  for (int64_t v = 0; v < N; v++) { order[v] = v; parent[v] = v; root_birth[v] = v; }
+  g_sort_f = field;
+  qsort(order, (size_t)N, sizeof(int64_t), cmp_sos);
+  int64_t np = 0;
+  for (int64_t i = 0; i < N; i++) {
+    int64_t v = order[i];
+    in[v] = 1;
+    co_t c = coords(&cx, v);
+    const ctype_t* vt = &cx.t[0];
+    for (int s = 0; s < vt->nlink; s++) {        /* edges {v, w}: the vertex's link */
+      int64_t x = c.x + vt->link[s][0], y = c.y + vt->link[s][1], z = c.z + vt->link[s][2];
+      if (!inside(&cx, x, y, z)) continue;
+      int64_t w = vid(&cx, x, y, z);
+      if (!in[w]) continue;
+      int64_t a = uf_find(parent, v), b = uf_find(parent, w);
+      if (a == b) continue;
+      int64_t ba = root_birth[a], bb = root_birth[b];
+      /* elder rule: the younger component (later birth) dies at v */
+      int64_t young = sos_less(field, ba, bb) ? b : a, old = young == a ? b : a;
+      if (root_birth[young] != v) {              /* v's own singleton merging is not a pair */
+        if (np < cap) { pairs[2 * np] = root_birth[young]; pairs[2 * np + 1] = v; }
+        np++;
+      }
+      parent[young] = old;
+    }
+  }
+  free(order); free(parent); free(root_birth); free(in);
+  return np;
 }
 
 int dmtz_oracle_num_threads(void) {

@@ -260,6 +260,13 @@ def cs_loop(C: Complex, f, fhat, xi, q_max=6, q_cap=None, tier=4, max_rounds=100
     lossless = np.zeros(f.size, bool)
     pf = gradient(C, f)
     cf = critical(C, pf)
+    if tier == 5:   # every vertex of every critical cell of f to its lower bound, losslessly
+        for c in cf:
+            for p in c:
+                v = C.vid(p)
+                g[v] = lb[v]
+                lossless[v] = True
+        tier = 4
     sep_f = trace(C, f) if tier >= 3 else []
     stats = dict(c_rounds=0, s_rounds=0, troublemakers=0)
 
@@ -343,3 +350,48 @@ def cs_loop(C: Complex, f, fhat, xi, q_max=6, q_cap=None, tier=4, max_rounds=100
             return "STUCK", g, q, lossless, stats
         if rnd == max_rounds:
             return "ITER_CAP", g, q, lossless, stats
+
+
+def persistence0(C: Complex, f):
+    """0-dim sublevel persistence pairs (birth vertex, death vertex) from scratch: add the
+    vertices in SoS order, recompute the components of the induced subgraph each time;
+    when v merges components, all but the eldest (earliest-born) die at v."""
+    fl = np.asarray(f, np.float32).ravel()
+    verts = sorted((c for c in C.by_dim[0]), key=lambda c: sos_key(fl, next(iter(c)), C))
+    nbrs = {}
+    for e in C.by_dim[1]:
+        a, b = tuple(e)
+        nbrs.setdefault(a, []).append(b)
+        nbrs.setdefault(b, []).append(a)
+    rank = {}
+    comps_prev = {}
+    pairs = []
+    present = set()
+    for i, c in enumerate(verts):
+        (p,) = tuple(c)
+        rank[p] = i
+        present.add(p)
+        # components containing p's present neighbours, before p was added
+        roots = {comps_prev[q] for q in nbrs.get(p, []) if q in present and q != p}
+        if len(roots) > 1:
+            eldest = min(roots, key=lambda r: rank[r])
+            pairs += [(C.vid(r), C.vid(p)) for r in roots if r != eldest]
+        # recompute components (labels = eldest vertex) from scratch
+        comps_prev = {}
+        seen = set()
+        for s0 in present:
+            if s0 in seen:
+                continue
+            stack, comp = [s0], []
+            seen.add(s0)
+            while stack:
+                x = stack.pop()
+                comp.append(x)
+                for y in nbrs.get(x, []):
+                    if y in present and y not in seen:
+                        seen.add(y)
+                        stack.append(y)
+            root = min(comp, key=lambda r: rank[r])
+            for x in comp:
+                comps_prev[x] = root
+    return sorted(pairs)

@@ -105,7 +105,49 @@ def test_identity_needs_no_edit(tier):
 
 def test_preserve_errors():
     f, fh, xi = di.random_case((5, 5), 1)
-    assert oracle.preserve(f, fh, xi, tier=5)["status"] == oracle.E_ARG
+    assert oracle.preserve(f, fh, xi, tier=6)["status"] == oracle.E_ARG
     bad = fh.copy()
     bad[0, 0] = f[0, 0] + np.float32(3 * xi)
     assert oracle.preserve(f, bad, xi, tier=4)["status"] == oracle.E_BOUND
+
+
+# ----------------------------------------------------------------------------- tier 5
+def test_persistence0_double_well_golden():
+    """a double well on a 5x2 strip -- minima at x=0 (f=0) and x=2 (f=1) merge at
+    x=1 (f=4): exactly one finite pair, (vertex 2, vertex 1)."""
+    f = np.array([[0, 4, 1, 5, 6], [0.5, 4.5, 1.5, 5.5, 6.5]], np.float32)
+    assert oracle.persistence0(f).tolist() == [[2, 1]]
+    assert bf.persistence0(_complex(f.shape), f) == [(2, 1)]
+
+
+@pytest.mark.parametrize("shape,seed,ties", [((6, 7), 1, False), ((8, 8), 2, True), ((4, 4, 4), 3, False),
+                                             ((3, 5, 4), 4, True)])
+def test_persistence0_matches_bruteforce(shape, seed, ties):
+    f, _, _ = di.random_case(shape, seed, ties=ties)
+    po = sorted(map(tuple, oracle.persistence0(f).tolist()))
+    assert po == bf.persistence0(_complex(shape), f)
+    # one essential class: finite pairs = minima - 1 (every minimum but the global one dies)
+    assert len(po) == int(np.count_nonzero(oracle.gradient(f)[1].ravel() & 1)) - 1
+
+
+@pytest.mark.parametrize("family,shape,seed,eps,perturb", [("lognormal", (10, 10), 4, 0.05, "lorenzo"),
+                                                           ("multiscale", (5, 6, 6), 3, 0.05, "lorenzo"),
+                                                           ("gauss2d", (12, 12), 1, 0.05, "noise")])
+def test_tier5_matches_bruteforce_and_keeps_the_diagram(family, shape, seed, eps, perturb):
+    """P:272 / P:327: T5 pre-clamps every vertex of every critical cell of f to its lower
+    bound, then runs the tier-4 workflow.  Post-conditions: the T4 ones, and the 0-dim
+    persistence pairs of g are those of f with both ends at f - xi (reading A18)."""
+    f, fh, xi = di.random_case(shape, seed, eps=eps, family=family, perturb=perturb)
+    r = oracle.preserve(f, fh, xi, tier=5)
+    st, g, q, ll, stats = bf.cs_loop(_complex(shape), f, fh, xi, 6, 6, 5)
+    assert st == "OK" and r["status"] == 0
+    assert np.array_equal(r["g"].ravel().view(np.uint32), g.view(np.uint32))
+    assert np.array_equal((r["state"].ravel() >> 16).astype(bool), ll)
+    C = _complex(shape)
+    assert bf.trace(C, f) == bf.trace(C, r["g"])
+    pf, pg = oracle.persistence0(f), oracle.persistence0(r["g"])
+    assert sorted(map(tuple, pf.tolist())) == sorted(map(tuple, pg.tolist()))
+    lb = np.array([bf.ru32(bf.Fraction(float(v)) - bf.Fraction(float(np.float32(xi)))) for v in f.ravel()],
+                  np.float32)
+    ends = np.unique(pf.ravel())
+    assert np.array_equal(r["g"].ravel()[ends].view(np.uint32), lb[ends].view(np.uint32))
