@@ -166,7 +166,7 @@ def sloop_line(name, dev, stream, with_cpu):
     ft, fht = torch.from_numpy(f).to(dev), torch.from_numpy(fh).to(dev)
     ctx = dmtz.Context(f.shape, dev)
     out = {"workload": f"{cfg.name} {cfg.family} {'x'.join(map(str, f.shape))} rel eps {cfg.eps}"}
-    for tier in (4, 3):
+    for tier in (4, 3, 5):
         ctx.preserve(ft, fht, xi, tier=tier)
         ts = []
         for _ in range(2):

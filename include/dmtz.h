@@ -247,8 +247,9 @@ typedef struct {
 size_t dmtz_preserve_sep_bytes(const dmtz_ctx* ctx, const dmtz_correct_opts* opts, int64_t cap_branches,
                                int64_t cap_cells);
 
-/* The workflow for opts->tier in 1..4 (tiers 1-2: exactly dmtz_correct; sep_ws may
- * be NULL).  Same inputs, outputs and errors as dmtz_correct, plus sstats (host);
+/* The workflow for opts->tier in 1..5 (tiers 1-2: exactly dmtz_correct; sep_ws may
+ * be NULL; tier 5: every vertex of every critical cell of f is first
+ * set to its lower bound (a lossless edit), then the tier-4 workflow runs).  Same inputs, outputs and errors as dmtz_correct, plus sstats (host);
  * DMTZ_E_CAPACITY also when a separatrix CSR exceeds the caps (sstats->sep_* hold
  * the needed counts).  ITER_CAP counts C- and S-rounds together. */
 dmtz_status dmtz_preserve(dmtz_ctx* ctx, const float* f, const float* fhat, const dmtz_correct_opts* opts,

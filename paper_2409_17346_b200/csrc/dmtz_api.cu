@@ -600,6 +600,11 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
   }
   status = setup_phase<D>(c, f, fhat, o, W, g_out, 0, &st->launches, s);
   if (status != DMTZ_OK) { st->status = status; return status; }
+  if (o->tier == 5) {  // pre-clamp f's critical cells, then the tier-4 workflow
+    k_t5_clamp<D><<<clamp_blocks(g.N, 256), 256, 0, s>>>(W.crit_f, W.lb, g_out, W.state, g);
+    CK(cudaGetLastError());
+    st->launches += 1;
+  }
   const unsigned long long max_rounds =
       o->max_rounds > 0 ? (unsigned long long)o->max_rounds : (unsigned long long)g.N * (unsigned long long)(o->q_cap + 1);
   const bool frontier_mode = !o->full_sweeps;
@@ -1019,7 +1024,7 @@ dmtz_status dmtz_preserve(dmtz_ctx* c, const float* f, const float* fhat, const 
   memset(st, 0, sizeof *st);
   *n_edits = 0;
   if (!(o->xi > 0.0f) || !isfinite(o->xi) || o->q_max < 0 || o->q_max > 30 || o->q_cap < 1 ||
-      o->q_cap > 65535 || o->tier < 3 || o->tier > 4 || o->max_rounds < 0) {
+      o->q_cap > 65535 || o->tier < 3 || o->tier > 5 || o->max_rounds < 0) {
     set_err("invalid options (xi=%g q_max=%d q_cap=%d tier=%d)", (double)o->xi, o->q_max, o->q_cap, o->tier);
     st->status = DMTZ_E_ARG;
     return DMTZ_E_ARG;

@@ -387,3 +387,27 @@ k_t3_flags(const long long* __restrict__ foff, const uint64_t* __restrict__ fcel
 }
 
 }  // namespace dmtz
+
+namespace dmtz {
+
+// Tier 5: every vertex of every critical cell of f goes to its lower
+// bound before the loop, stored losslessly.  Several anchors may write the
+// same vertex: the writes are identical.
+template <int D>
+__global__ void k_t5_clamp(const uint32_t* __restrict__ crit_f, const float* __restrict__ lb, float* __restrict__ gf,
+                           uint32_t* __restrict__ state, Grid g) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < g.N; v += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t m = crit_f[v];
+    while (m) {
+      const int t = __ffs(m) - 1;
+      m &= m - 1;
+      for (int k = 0; k < t_nv<D>(t); k++) {
+        const int64_t w = v + mask_delta(g, t_vmask<D>(t, k));
+        gf[w] = lb[w];
+        state[w] = 1u << 16;
+      }
+    }
+  }
+}
+
+}  // namespace dmtz

@@ -50,6 +50,9 @@ CASES = [  # (family, shape, seed, eps, perturb, tier, q_cap)
     ("noise", (33, 40, 37), 2, 0.05, "lorenzo", 4, 6),
     ("lognormal", (20, 31, 45), 3, 0.05, "lorenzo", 3, 6),
     ("noise", (97, 131), 5, 0.1, "noise", 4, 6),
+    ("lognormal", (10, 10), 4, 0.05, "lorenzo", 5, 6),
+    ("multiscale", (5, 6, 6), 3, 0.05, "lorenzo", 5, 65535),
+    ("lognormal", (20, 31, 45), 3, 0.05, "lorenzo", 5, 6),
 ]
 
 
@@ -68,7 +71,7 @@ def test_preserve_full_sweeps(dmtz, tier):
 
 @pytest.mark.parametrize("name,shape,tier", [("C1", None, 4), ("C2", (120, 240), 4), ("C3", (20, 50, 50), 4),
                                              ("C4", (24, 24, 24), 4), ("C4", (20, 22, 24), 3),
-                                             ("C5", (20, 24, 28), 4)])
+                                             ("C5", (20, 24, 28), 4), ("C4", (24, 24, 24), 5)])
 def test_preserve_config_crops(dmtz, name, shape, tier):
     f, fh, xi, _ = di.config_inputs(name, shape=shape)
     _compare(dmtz, f, fh, xi, tier)
@@ -120,3 +123,19 @@ def test_preserve_postconditions_mid_size(dmtz, name, shape, tier):
         nb = tf["origin"].shape[0]
         assert tg["origin"].shape[0] == nb and torch.equal(tf["origin"], tg["origin"])
         assert _ends(tf, nb) == _ends(tg, nb)
+
+
+@pytest.mark.parametrize("name,shape", [("C4", (48, 48, 48)), ("C2", (300, 600))])
+def test_tier5_keeps_the_persistence_diagram(dmtz, name, shape):
+    """P:143 / P:272: after tier 5 the 0-dim persistence pairs of g (oracle union-find)
+    are those of f, and their vertices sit at their lower bounds (reading A18)."""
+    f, fh, xi, _ = di.config_inputs(name, shape=shape)
+    r = dmtz.preserve(_cuda(f), _cuda(fh), xi, tier=5)
+    assert r.status == 0, r.message
+    g = r.g.cpu().numpy()
+    pf, pg = oracle.persistence0(f), oracle.persistence0(g)
+    assert sorted(map(tuple, pf.tolist())) == sorted(map(tuple, pg.tolist()))
+    e = r.edits_numpy()
+    ends = np.unique(pf.ravel())
+    clamped = e["v"][e["lossless"] > 0]
+    assert np.isin(ends, clamped).all()
