@@ -96,12 +96,19 @@ def _load():
     L.dmtz_preserve_sep_bytes.restype = ctypes.c_size_t
     L.dmtz_preserve.argtypes = [P, P, P, ctypes.POINTER(_Opts), P, SZ, P, SZ, i64, i64, P, P, i64,
                                 ctypes.POINTER(i64), ctypes.POINTER(_Stats), ctypes.POINTER(_SStats), P]
+    L.dmtz_edit_stream_bound.argtypes = [i64]
+    L.dmtz_edit_stream_bound.restype = SZ
+    L.dmtz_encode_edits.argtypes = [P, P, i64, ctypes.c_float, i32, P, SZ, P, SZ, ctypes.POINTER(SZ), P]
+    L.dmtz_decode_edits.argtypes = [P, P, SZ, P, i64, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_float),
+                                    ctypes.POINTER(i32), P, SZ, P]
+    L.dmtz_apply_edits.argtypes = [P, P, ctypes.c_float, i32, P, i64, P, P, SZ, P]
     L.dmtz_status_string.argtypes = [i32]
     L.dmtz_status_string.restype = ctypes.c_char_p
     L.dmtz_last_error.restype = ctypes.c_char_p
     for fn in ("dmtz_ctx_create", "dmtz_compute_gradient", "dmtz_critical_mask", "dmtz_correct",
                "dmtz_trace_separatrices", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end",
-               "dmtz_slab_halo", "dmtz_trace_separatrices_range", "dmtz_preserve"):
+               "dmtz_slab_halo", "dmtz_trace_separatrices_range", "dmtz_preserve",
+               "dmtz_encode_edits", "dmtz_decode_edits", "dmtz_apply_edits"):
         getattr(L, fn).restype = ctypes.c_int
     return L
 
@@ -122,7 +129,8 @@ _lib = _LazyLib()
 EXPORTED = ("dmtz_ctx_create", "dmtz_ctx_destroy", "dmtz_workspace_bytes", "dmtz_compute_gradient",
             "dmtz_critical_mask", "dmtz_correct", "dmtz_trace_separatrices", "dmtz_status_string",
             "dmtz_last_error", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end",
-            "dmtz_slab_halo", "dmtz_trace_separatrices_range", "dmtz_preserve_sep_bytes", "dmtz_preserve")
+            "dmtz_slab_halo", "dmtz_trace_separatrices_range", "dmtz_preserve_sep_bytes", "dmtz_preserve",
+            "dmtz_edit_stream_bound", "dmtz_encode_edits", "dmtz_decode_edits", "dmtz_apply_edits")
 
 
 def lib():
@@ -295,6 +303,45 @@ class Context:
             raise DmtzError(status, msg)
         return Result(status=status, g=g_out, edits=edits[:min(ne.value, cap)], n_edits=ne.value, stats=stats,
                       message=msg)
+
+    # ---------------------------------------------------------------- edits as an artifact
+    def encode_edits(self, edits: torch.Tensor, xi: float, q_max: int = 6, stream=None) -> torch.Tensor:
+        """Edit list (n, 16) uint8 rows -> the version-1 edit stream (uint8 CUDA tensor)."""
+        _need_cuda(edits)
+        n = int(edits.shape[0])
+        cap = int(_lib.dmtz_edit_stream_bound(n))
+        out = torch.empty(max(cap, 1), dtype=torch.uint8, device=edits.device)
+        nb = ctypes.c_size_t()
+        _check(_lib.dmtz_encode_edits(self._h, ctypes.c_void_p(edits.data_ptr()) if n else None, n, float(xi),
+                                      int(q_max), ctypes.c_void_p(self.workspace.data_ptr()), self.ws_bytes,
+                                      ctypes.c_void_p(out.data_ptr()), cap, ctypes.byref(nb), _stream_ptr(stream)))
+        return out[:nb.value]
+
+    def decode_edits(self, stream_bytes: torch.Tensor, stream=None):
+        """Edit stream (uint8 CUDA tensor) -> (edits (n, 16) uint8, xi, q_max)."""
+        _need_cuda(stream_bytes)
+        cap = self.N
+        edits = torch.empty((max(cap, 1), 16), dtype=torch.uint8, device=stream_bytes.device)
+        n, xi, qm = ctypes.c_int64(), ctypes.c_float(), ctypes.c_int32()
+        _check(_lib.dmtz_decode_edits(self._h, ctypes.c_void_p(stream_bytes.data_ptr()), int(stream_bytes.numel()),
+                                      ctypes.c_void_p(edits.data_ptr()), cap, ctypes.byref(n), ctypes.byref(xi),
+                                      ctypes.byref(qm), ctypes.c_void_p(self.workspace.data_ptr()), self.ws_bytes,
+                                      _stream_ptr(stream)))
+        return edits[:n.value], xi.value, qm.value
+
+    def apply_edits(self, fhat: torch.Tensor, xi: float, edits: torch.Tensor, q_max: int = 6,
+                    g_out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """Decompression side: fhat with the edits applied (bit-exact with correct()'s g)."""
+        _need_cuda(fhat, edits)
+        assert fhat.dtype == torch.float32 and tuple(fhat.shape) == self.shape and fhat.is_contiguous()
+        if g_out is None:
+            g_out = torch.empty_like(fhat)
+        n = int(edits.shape[0])
+        _check(_lib.dmtz_apply_edits(self._h, ctypes.c_void_p(fhat.data_ptr()), float(xi), int(q_max),
+                                     ctypes.c_void_p(edits.data_ptr()) if n else None, n,
+                                     ctypes.c_void_p(g_out.data_ptr()), ctypes.c_void_p(self.workspace.data_ptr()),
+                                     self.ws_bytes, _stream_ptr(stream)))
+        return g_out
 
     # ---------------------------------------------------------------- traces
     def _trace(self, codes, kinds, seps, cb, cc, nb, nc, stream, z_range):

@@ -18,6 +18,7 @@
 #include "dmtz_sweep.cuh"
 #include "dmtz_trace.cuh"
 #include "dmtz_sloop.cuh"
+#include "dmtz_codec.cuh"
 
 using namespace dmtz;
 
@@ -1051,6 +1052,103 @@ dmtz_status dmtz_preserve(dmtz_ctx* c, const float* f, const float* fhat, const 
                          edits_capacity, n_edits, st, ss, s);
   if (r == DMTZ_E_CUDA) st->status = r;
   return r;
+}
+
+
+size_t dmtz_edit_stream_bound(int64_t n) {
+  if (n < 0) return 0;
+  const size_t nb = (size_t)((n + EC_BLOCK - 1) / EC_BLOCK);
+  return EC_HEADER + 8 * nb + (size_t)n * (10 + 3 + 4);
+}
+
+dmtz_status dmtz_encode_edits(dmtz_ctx* c, const dmtz_edit* edits, int64_t n, float xi, int32_t q_max, void* ws,
+                              size_t wsb, uint8_t* out, size_t cap, size_t* nbytes, dmtz_stream_t stream) {
+  if (!c || (n > 0 && !edits) || !ws || !out || !nbytes || n < 0) { set_err("NULL argument"); return DMTZ_E_ARG; }
+  if (n > c->g.N) { set_err("%lld edits for %lld vertices", (long long)n, (long long)c->g.N); return DMTZ_E_ARG; }
+  const Layout L = layout_for(c);
+  if (wsb < L.total) { set_err("workspace %zu < %zu bytes", wsb, L.total); return DMTZ_E_OOM; }
+  cudaStream_t s = (cudaStream_t)stream;
+  char* w = (char*)ws;
+  long long* len = (long long*)(w + L.cand_g);
+  unsigned long long* bsum = (unsigned long long*)(w + L.edit_bc);
+  Counters* dc = (Counters*)(w + L.counters);
+  Counters* hc = c->host_cnt;
+  CK(cudaMemsetAsync(dc, 0, sizeof(Counters), s));
+  k_ec_len<<<clamp_blocks(n + 1, 256), 256, 0, s>>>((const EditRec*)edits, n, len, &dc->pad[1]);
+  CK(cudaGetLastError());
+  CK(scan_i64(len, n + 1, bsum, &dc->pad[0], &hc->pad[0], s));  // synchronises: hc->pad[0] = payload bytes
+  CK(cudaMemcpyAsync(&hc->pad[1], &dc->pad[1], 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (hc->pad[1]) { set_err("edit list not strictly ascending"); return DMTZ_E_ARG; }
+  const size_t nb = (size_t)((n + EC_BLOCK - 1) / EC_BLOCK);
+  *nbytes = EC_HEADER + 8 * nb + (size_t)hc->pad[0];
+  if (*nbytes > cap) { set_err("edit stream needs %zu bytes", *nbytes); return DMTZ_E_CAPACITY; }
+  k_ec_write<<<clamp_blocks(n > 0 ? n : 1, 256), 256, 0, s>>>((const EditRec*)edits, n, len, xi, q_max, out);
+  CK(cudaGetLastError());
+  return DMTZ_OK;
+}
+
+dmtz_status dmtz_decode_edits(dmtz_ctx* c, const uint8_t* in, size_t nbytes, dmtz_edit* edits, int64_t cap,
+                              int64_t* n_edits, float* xi, int32_t* q_max, void* ws, size_t wsb,
+                              dmtz_stream_t stream) {
+  if (!c || !in || !n_edits || !xi || !q_max || !ws || cap < 0 || (cap > 0 && !edits)) {
+    set_err("NULL argument");
+    return DMTZ_E_ARG;
+  }
+  if (nbytes < EC_HEADER) { set_err("edit stream of %zu bytes", nbytes); return DMTZ_E_ARG; }
+  const Layout L = layout_for(c);
+  if (wsb < L.total) { set_err("workspace %zu < %zu bytes", wsb, L.total); return DMTZ_E_OOM; }
+  cudaStream_t s = (cudaStream_t)stream;
+  uint8_t h[EC_HEADER];
+  CK(cudaMemcpyAsync(h, in, EC_HEADER, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  auto u32 = [&](int o) { uint32_t x = 0; for (int k = 0; k < 4; k++) x |= (uint32_t)h[o + k] << (8 * k); return x; };
+  uint64_t n = 0;
+  for (int k = 0; k < 8; k++) n |= (uint64_t)h[8 + k] << (8 * k);
+  const uint32_t ver = u32(4), blk = u32(16), nblocks = u32(28), xib = u32(24);
+  if (memcmp(h, "DMTE", 4) != 0 || ver != 1 || blk != (uint32_t)EC_BLOCK ||
+      (uint64_t)nblocks != (n + EC_BLOCK - 1) / EC_BLOCK || EC_HEADER + 8 * (size_t)nblocks > nbytes) {
+    set_err("not a version-1 edit stream");
+    return DMTZ_E_ARG;
+  }
+  *n_edits = (int64_t)n;
+  memcpy(xi, &xib, 4);
+  *q_max = (int32_t)u32(20);
+  if ((int64_t)n > cap) { set_err("stream holds %llu edits", (unsigned long long)n); return DMTZ_E_CAPACITY; }
+  Counters* dc = (Counters*)((char*)ws + L.counters);
+  Counters* hc = c->host_cnt;
+  CK(cudaMemsetAsync(&dc->pad[1], 0, 8, s));
+  if (nblocks)
+    k_ec_decode<<<clamp_blocks(nblocks, 128), 128, 0, s>>>(in, nbytes, (int64_t)n, nblocks, c->g.N, (EditRec*)edits,
+                                                           &dc->pad[1]);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(&hc->pad[1], &dc->pad[1], 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (hc->pad[1]) { set_err("malformed edit stream (%llu bad blocks)", hc->pad[1]); return DMTZ_E_ARG; }
+  return DMTZ_OK;
+}
+
+dmtz_status dmtz_apply_edits(dmtz_ctx* c, const float* fhat, float xi, int32_t q_max, const dmtz_edit* edits,
+                             int64_t n, float* g_out, void* ws, size_t wsb, dmtz_stream_t stream) {
+  if (!c || !fhat || !g_out || !ws || n < 0 || (n > 0 && !edits) || !(xi > 0.0f) || q_max < 0 || q_max > 30) {
+    set_err("invalid argument");
+    return DMTZ_E_ARG;
+  }
+  const Layout L = layout_for(c);
+  if (wsb < L.total) { set_err("workspace %zu < %zu bytes", wsb, L.total); return DMTZ_E_OOM; }
+  cudaStream_t s = (cudaStream_t)stream;
+  Counters* dc = (Counters*)((char*)ws + L.counters);
+  Counters* hc = c->host_cnt;
+  CK(cudaMemsetAsync(&dc->pad[1], 0, 8, s));
+  if (g_out != fhat) CK(cudaMemcpyAsync(g_out, fhat, (size_t)c->g.N * 4, cudaMemcpyDeviceToDevice, s));
+  if (n > 0)
+    k_apply_edits<<<clamp_blocks(n, 256), 256, 0, s>>>(fhat, (const EditRec*)edits, n, c->g.N, ldexpf(xi, -q_max),
+                                                       g_out, &dc->pad[1]);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(&hc->pad[1], &dc->pad[1], 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (hc->pad[1]) { set_err("%llu edits outside the grid", hc->pad[1]); return DMTZ_E_ARG; }
+  return DMTZ_OK;
 }
 
 }  // extern "C"

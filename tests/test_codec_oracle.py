@@ -1,0 +1,65 @@
+"""Pins of the plain-Python edit-stream codec (oracle/edit_codec.py)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import dmtz_inputs as di
+import oracle
+from oracle import edit_codec as ec
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "edit_stream_small.json")
+
+
+def _edits(rows):
+    e = np.zeros(len(rows), oracle.EDIT_DTYPE)
+    for i, (v, q, ll, val) in enumerate(rows):
+        e[i] = (v, q, ll, 0, val)
+    return e
+
+
+def test_golden_bytes():
+    g = json.load(open(GOLD))
+    b = ec.encode(_edits(g["edits"]), g["xi"], g["q_max"])
+    assert b.hex() == g["hex"].replace(" ", "")
+    d, xi, qm = ec.decode(b)
+    assert (xi, qm) == (g["xi"], g["q_max"]) and d.tolist() == _edits(g["edits"]).tolist()
+
+
+@pytest.mark.parametrize("n,seed", [(0, 0), (1, 1), (4095, 2), (4097, 3), (9000, 4)])
+def test_roundtrip(n, seed):
+    rng = np.random.default_rng(seed)
+    v = np.sort(rng.choice(10 ** 7, size=n, replace=False)) if n else np.zeros(0, np.int64)
+    e = np.zeros(n, oracle.EDIT_DTYPE)
+    e["v"] = v
+    e["q"] = rng.integers(0, 65536, n)
+    e["lossless"] = rng.integers(0, 2, n)
+    e["value"] = np.where(e["lossless"] > 0, rng.standard_normal(n).astype(np.float32), 0)
+    d, xi, qm = ec.decode(ec.encode(e, 0.125, 6))
+    assert d.tobytes() == e.tobytes() and xi == 0.125 and qm == 6
+
+
+def test_quantized_is_smaller():
+    """10 quantized entries < 10 x 12 B key-value floats; the quantized
+    stream of a C-loop result is no larger than the all-lossless stream of the same edits."""
+    e = _edits([(1000 + 7 * i, 5, 0, 0.0) for i in range(10)])
+    assert len(ec.encode(e, 0.1, 6)) - 32 - 8 < 10 * 12
+    f, fh, xi, _ = di.config_inputs("C1")
+    r = oracle.correct(f, fh, xi, q_cap=65535)
+    q = ec.encode(r["edits"], xi, 6)
+    ll = r["edits"].copy()
+    ll["lossless"] = 1
+    ll["value"] = r["g"].ravel()[ll["v"]]
+    assert len(q) <= len(ec.encode(ll, xi, 6))
+
+
+@pytest.mark.parametrize("q_cap", [6, 65535])
+def test_apply_replays_the_cloop(q_cap):
+    """Fig. 2: the decompression side rebuilds the editor's g bit for bit from fhat and the
+    decoded edits."""
+    f, fh, xi = di.random_case((9, 10, 11), 4, eps=0.05, family="lognormal")
+    r = oracle.correct(f, fh, xi, q_cap=q_cap)
+    d, x2, qm = ec.decode(ec.encode(r["edits"], xi, 6))
+    g = ec.apply(fh, d, x2, qm)
+    assert np.array_equal(g.view(np.uint32), r["g"].view(np.uint32))
