@@ -18,6 +18,15 @@ def dmtz():
     return d
 
 
+def _same_edits(d, e):
+    """decoded vs original: v, q, lossless; value bits of the lossless entries (quantized
+    entries carry no value in the stream -- apply_edits recomputes it from fhat)."""
+    a, b = d.cpu().numpy().view(oracle.EDIT_DTYPE).ravel(), e.cpu().numpy().view(oracle.EDIT_DTYPE).ravel()
+    ll = b["lossless"] > 0
+    return (len(a) == len(b) and all(np.array_equal(a[k], b[k]) for k in ("v", "q", "lossless")) and
+            np.array_equal(a["value"][ll].view(np.uint32), b["value"][ll].view(np.uint32)))
+
+
 def _cuda(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
@@ -35,7 +44,7 @@ def test_encode_decode_apply(dmtz, name, shape, q_cap):
     assert s.cpu().numpy().tobytes() == ref
     d, x2, qm = ctx.decode_edits(s)
     assert (x2, qm) == (np.float32(xi), 6)
-    assert torch.equal(d, r.edits)
+    assert _same_edits(d, r.edits)
     g = ctx.apply_edits(fht, x2, d, q_max=qm)
     assert torch.equal(g.view(torch.int32), r.g.view(torch.int32))
     assert s.numel() < 12 * max(r.n_edits, 1) + 64   # below the 12 B key-value float records
@@ -50,7 +59,7 @@ def test_multi_block_and_errors(dmtz):
     s = ctx.encode_edits(r.edits, xi, 6)
     assert s.cpu().numpy().tobytes() == ec.encode(r.edits_numpy(), xi, 6)
     d, _, _ = ctx.decode_edits(s)
-    assert torch.equal(d, r.edits)
+    assert _same_edits(d, r.edits)
     bad = s.clone()
     bad[0] = ord("X")
     with pytest.raises(dmtz.DmtzError):
