@@ -387,6 +387,32 @@ def main():
                "sample": f"oracle C-loop to its fixed point on the {s['shape']} crop of {cfg.name} "
                          f"({s['sweeps']} sweeps in {s['seconds']:.1f} s)"}
 
+    # the edit list as an artifact (NEXT-2): encode / decode / apply on the device
+    codec = None
+    try:
+        ev = r.edits[:r.n_edits]
+        def _t(fn):
+            fn()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            out = fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            return out, e0.elapsed_time(e1)
+        sb, enc_ms = _t(lambda: ctx.encode_edits(ev, xi, 6))
+        (dec, _, _), dec_ms = _t(lambda: ctx.decode_edits(sb))
+        ga, app_ms = _t(lambda: ctx.apply_edits(fht, xi, dec))
+        nbytes = int(sb.numel())
+        codec = {"n_edits": r.n_edits, "stream_bytes": nbytes, "bytes_per_edit": nbytes / max(r.n_edits, 1),
+                 "keyvalue_float_bytes": 12 * r.n_edits, "edit_ratio": r.n_edits / N,
+                 "stream_fraction_of_original": nbytes / (4 * N),
+                 "encode_ms": enc_ms, "decode_ms": dec_ms, "apply_ms": app_ms,
+                 "apply_matches_g": bool(torch.equal(ga.view(torch.int32), g.view(torch.int32)))}
+        del sb, dec, ga
+    except Exception as e:  # noqa: BLE001
+        codec = {"error": str(e)[:200]}
+
     sloop = None
     if args.sloop_config != "none":
         del ctx
@@ -403,7 +429,7 @@ def main():
                    "mode": "default: dirty frontier + exact change skipping (bit-identical to full_sweeps=1)",
                    "l2": "inputs larger than L2 (2 x 537 MB)", "parallelism": "1 GPU"},
         "roofline": roof, "roofline_screen": roof_screen, "cpu_baseline": cpu, "e2e": e2e, "time_to_fixed_point": frontier,
-        "full_recompute": full_recompute, "trace": trace, "sloop": sloop,
+        "full_recompute": full_recompute, "trace": trace, "sloop": sloop, "codec": codec,
         "gpu_launches": st["launches"],
         "clocks": clk.summary(),
         "stats": {k: st[k] for k in ("rounds", "sweeps", "n_edited", "n_quantized", "n_lossless", "n_false_round0",

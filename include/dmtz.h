@@ -296,6 +296,25 @@ dmtz_status dmtz_apply_edits(dmtz_ctx* ctx, const float* fhat, float xi, int32_t
                              dmtz_stream_t stream);
 
 /* ------------------------------------------------------------------------
+ * Evaluation metrics (§5.1).  Recall = n_match /
+ * n_orig, precision = n_match / n_rec (1 when the denominator is 0).
+ * ------------------------------------------------------------------------ */
+typedef struct { int64_t n_orig, n_rec, n_match; } dmtz_prf;
+/* Critical cells: masks (uint32[N] per anchor, bit = type, as dmtz_critical_mask
+ * writes them) of the original and the reconstructed field; a cell matches when it is
+ * critical in both ("retained").  Synchronises the stream. */
+dmtz_status dmtz_critical_prf(dmtz_ctx* ctx, const uint32_t* crit_orig, const uint32_t* crit_rec,
+                              dmtz_prf* out /* host */, void* workspace, size_t workspace_bytes,
+                              dmtz_stream_t stream);
+/* Separatrices: two outputs of dmtz_trace_separatrices (device CSRs with nb_orig /
+ * nb_rec branches).  The unit is a branch, identified by (kind, origin cell, ordinal
+ * among its origin's branches); it matches when both traces hold it with the same
+ * terminal and the same cell sequence.  Synchronises the stream. */
+dmtz_status dmtz_separatrix_prf(dmtz_ctx* ctx, const dmtz_seps* orig, int64_t nb_orig, const dmtz_seps* rec,
+                                int64_t nb_rec, dmtz_prf* out /* host */, void* workspace,
+                                size_t workspace_bytes, dmtz_stream_t stream);
+
+/* ------------------------------------------------------------------------
  * Slab mode (multi-GPU z-slab decomposition).  One context per
  * rank, created for its LOCAL grid: the owned z-planes plus up to 3 halo planes
  * below and above (nz_local = own + halos).  The caller drives the rounds and,

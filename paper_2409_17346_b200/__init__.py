@@ -62,6 +62,16 @@ class _SStats(ctypes.Structure):
                 ("cells_checked", ctypes.c_int64), ("pad", ctypes.c_int64 * 4)]
 
 
+class _Prf(ctypes.Structure):
+    _fields_ = [("n_orig", ctypes.c_int64), ("n_rec", ctypes.c_int64), ("n_match", ctypes.c_int64)]
+
+
+def _prf(p):
+    return dict(n_orig=p.n_orig, n_rec=p.n_rec, n_match=p.n_match,
+                recall=p.n_match / p.n_orig if p.n_orig else 1.0,
+                precision=p.n_match / p.n_rec if p.n_rec else 1.0)
+
+
 class _Seps(ctypes.Structure):
     _fields_ = [("branch_offsets", ctypes.c_void_p), ("cells", ctypes.c_void_p), ("origin", ctypes.c_void_p),
                 ("terminal", ctypes.c_void_p), ("kind", ctypes.c_void_p)]
@@ -102,13 +112,17 @@ def _load():
     L.dmtz_decode_edits.argtypes = [P, P, SZ, P, i64, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_float),
                                     ctypes.POINTER(i32), P, SZ, P]
     L.dmtz_apply_edits.argtypes = [P, P, ctypes.c_float, i32, P, i64, P, P, SZ, P]
+    L.dmtz_critical_prf.argtypes = [P, P, P, ctypes.POINTER(_Prf), P, SZ, P]
+    L.dmtz_separatrix_prf.argtypes = [P, ctypes.POINTER(_Seps), i64, ctypes.POINTER(_Seps), i64,
+                                      ctypes.POINTER(_Prf), P, SZ, P]
     L.dmtz_status_string.argtypes = [i32]
     L.dmtz_status_string.restype = ctypes.c_char_p
     L.dmtz_last_error.restype = ctypes.c_char_p
     for fn in ("dmtz_ctx_create", "dmtz_compute_gradient", "dmtz_critical_mask", "dmtz_correct",
                "dmtz_trace_separatrices", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end",
                "dmtz_slab_halo", "dmtz_trace_separatrices_range", "dmtz_preserve",
-               "dmtz_encode_edits", "dmtz_decode_edits", "dmtz_apply_edits"):
+               "dmtz_encode_edits", "dmtz_decode_edits", "dmtz_apply_edits",
+               "dmtz_critical_prf", "dmtz_separatrix_prf"):
         getattr(L, fn).restype = ctypes.c_int
     return L
 
@@ -130,7 +144,8 @@ EXPORTED = ("dmtz_ctx_create", "dmtz_ctx_destroy", "dmtz_workspace_bytes", "dmtz
             "dmtz_critical_mask", "dmtz_correct", "dmtz_trace_separatrices", "dmtz_status_string",
             "dmtz_last_error", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end",
             "dmtz_slab_halo", "dmtz_trace_separatrices_range", "dmtz_preserve_sep_bytes", "dmtz_preserve",
-            "dmtz_edit_stream_bound", "dmtz_encode_edits", "dmtz_decode_edits", "dmtz_apply_edits")
+            "dmtz_edit_stream_bound", "dmtz_encode_edits", "dmtz_decode_edits", "dmtz_apply_edits",
+            "dmtz_critical_prf", "dmtz_separatrix_prf")
 
 
 def lib():
@@ -342,6 +357,28 @@ class Context:
                                      ctypes.c_void_p(g_out.data_ptr()), ctypes.c_void_p(self.workspace.data_ptr()),
                                      self.ws_bytes, _stream_ptr(stream)))
         return g_out
+
+    # ---------------------------------------------------------------- metrics (§5.1)
+    def critical_prf(self, crit_orig: torch.Tensor, crit_rec: torch.Tensor, stream=None) -> dict:
+        """Critical-cell recall / precision from two critical masks."""
+        _need_cuda(crit_orig, crit_rec)
+        p = _Prf()
+        _check(_lib.dmtz_critical_prf(self._h, ctypes.c_void_p(crit_orig.data_ptr()),
+                                      ctypes.c_void_p(crit_rec.data_ptr()), ctypes.byref(p),
+                                      ctypes.c_void_p(self.workspace.data_ptr()), self.ws_bytes, _stream_ptr(stream)))
+        return _prf(p)
+
+    def separatrix_prf(self, tr_orig: dict, tr_rec: dict, stream=None) -> dict:
+        """Separatrix recall / precision from two trace_separatrices() results."""
+        def seps(t):
+            return _Seps(*(ctypes.c_void_p(t[k].data_ptr()) for k in ("offsets", "cells", "origin", "terminal", "kind")))
+        a, b = seps(tr_orig), seps(tr_rec)
+        p = _Prf()
+        _check(_lib.dmtz_separatrix_prf(self._h, ctypes.byref(a), int(tr_orig["origin"].shape[0]), ctypes.byref(b),
+                                        int(tr_rec["origin"].shape[0]), ctypes.byref(p),
+                                        ctypes.c_void_p(self.workspace.data_ptr()), self.ws_bytes,
+                                        _stream_ptr(stream)))
+        return _prf(p)
 
     # ---------------------------------------------------------------- traces
     def _trace(self, codes, kinds, seps, cb, cc, nb, nc, stream, z_range):

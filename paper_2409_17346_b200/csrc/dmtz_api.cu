@@ -19,6 +19,7 @@
 #include "dmtz_trace.cuh"
 #include "dmtz_sloop.cuh"
 #include "dmtz_codec.cuh"
+#include "dmtz_metrics.cuh"
 
 using namespace dmtz;
 
@@ -1148,6 +1149,48 @@ dmtz_status dmtz_apply_edits(dmtz_ctx* c, const float* fhat, float xi, int32_t q
   CK(cudaMemcpyAsync(&hc->pad[1], &dc->pad[1], 8, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (hc->pad[1]) { set_err("%llu edits outside the grid", hc->pad[1]); return DMTZ_E_ARG; }
+  return DMTZ_OK;
+}
+
+
+dmtz_status dmtz_critical_prf(dmtz_ctx* c, const uint32_t* a, const uint32_t* b, dmtz_prf* out, void* ws,
+                              size_t wsb, dmtz_stream_t stream) {
+  if (!c || !a || !b || !out || !ws) { set_err("NULL argument"); return DMTZ_E_ARG; }
+  const Layout L = layout_for(c);
+  if (wsb < L.total) { set_err("workspace %zu < %zu bytes", wsb, L.total); return DMTZ_E_OOM; }
+  cudaStream_t s = (cudaStream_t)stream;
+  Counters* dc = (Counters*)((char*)ws + L.counters);
+  Counters* hc = c->host_cnt;
+  CK(cudaMemsetAsync(dc->pad, 0, 3 * 8, s));
+  k_crit_prf<<<clamp_blocks(c->g.N, 256), 256, 0, s>>>(a, b, c->g.N, dc->pad);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(hc->pad, dc->pad, 3 * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  out->n_orig = (int64_t)hc->pad[0];
+  out->n_rec = (int64_t)hc->pad[1];
+  out->n_match = (int64_t)hc->pad[2];
+  return DMTZ_OK;
+}
+
+dmtz_status dmtz_separatrix_prf(dmtz_ctx* c, const dmtz_seps* A, int64_t na, const dmtz_seps* B, int64_t nb,
+                                dmtz_prf* out, void* ws, size_t wsb, dmtz_stream_t stream) {
+  if (!c || !A || !B || !out || !ws || na < 0 || nb < 0) { set_err("NULL argument"); return DMTZ_E_ARG; }
+  const Layout L = layout_for(c);
+  if (wsb < L.total) { set_err("workspace %zu < %zu bytes", wsb, L.total); return DMTZ_E_OOM; }
+  cudaStream_t s = (cudaStream_t)stream;
+  Counters* dc = (Counters*)((char*)ws + L.counters);
+  Counters* hc = c->host_cnt;
+  CK(cudaMemsetAsync(dc->pad, 0, 8, s));
+  if (na > 0 && nb > 0)
+    k_sep_match<<<clamp_blocks(na, 256), 256, 0, s>>>(
+        (const long long*)A->branch_offsets, A->cells, A->origin, A->terminal, A->kind, na,
+        (const long long*)B->branch_offsets, B->cells, B->origin, B->terminal, B->kind, nb, dc->pad);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(hc->pad, dc->pad, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  out->n_orig = na;
+  out->n_rec = nb;
+  out->n_match = (int64_t)hc->pad[0];
   return DMTZ_OK;
 }
 
