@@ -404,8 +404,8 @@ dmtz_status run_cloop(dmtz_ctx* c, const float* f, const float* fhat, const dmtz
                               frontier_mode ? W.fbits : nullptr, (int)L.fwords, 0, g.nz, 0, g.nz, o->profile != 0,
                               max_rounds, frontier_mode ? 1 : 0, hls, &st->launches, s);
       if (status != DMTZ_OK) break;
+      float ms0 = 0.f, ms1 = 0.f;
       if (o->profile) {
-        float ms0 = 0.f, ms1 = 0.f;
         CK(cudaEventElapsedTime(&ms0, c->ev[0], c->ev[1]));
         CK(cudaEventElapsedTime(&ms1, c->ev[1], c->ev[2]));
         st->sweep_ms += ms0 + ms1;
@@ -415,9 +415,9 @@ dmtz_status run_cloop(dmtz_ctx* c, const float* f, const float* fhat, const dmtz
       }
       if (c->verbose)
         fprintf(stderr, "dmtz round %llu: units %llu recomputed %llu swept %llu false %llu targets %llu changed %llu"
-                " | act_chg %llu act_had %llu had_false %llu chg_false %llu\n",
+                " decoded %llu items %llu replayed %llu | screen %.3f ms decode %.3f ms\n",
                 hls->sweeps, hc->n_units, hc->n_recomputed, hc->n_swept, hc->n_false, hc->n_targets, hc->n_changed,
-                hc->pad[2], hc->pad[3], hc->pad[4], hc->pad[5]);
+                hc->n_decoded, hc->n_items, hc->n_replayed, ms0, ms1);
       const bool go = hls->status == 0 && hls->last_false != 0;  // the check advanced the round
       if (!go) break;
     }
