@@ -483,7 +483,7 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
 // mismatch bits, the per-anchor changed-code bits, and for tier 3 the CSR of g's
 // separatrices + per-branch end flags.
 struct SepLayout {
-  size_t codes, save, off, cells, origin, term, kind, first, cb, mbits, sdirty, sdil, goff, gcells, gorigin, gterm, gkind,
+  size_t codes, save, off, cells, origin, term, kind, first, cb, canc, mbits, sdirty, sdil, goff, gcells, gorigin, gterm, gkind,
       flag, total;
 };
 
@@ -501,6 +501,7 @@ SepLayout sep_layout(const dmtz_ctx* c, int tier, int64_t cap_b, int64_t cap_c) 
   S.kind = o; o += align_up((size_t)cap_b + 8);
   S.first = o; o += align_up((size_t)cap_b * 4 + 8);
   S.cb = o; o += align_up((size_t)cap_c + 8);  // per-cell descriptors
+  S.canc = o; o += align_up((size_t)cap_c * 4 + 8);  // anchors of the examined cells
   S.mbits = o; o += align_up((size_t)cap_c / 8 + 8);
   S.sdirty = o; o += align_up(N / 8 + 8);
   S.sdil = o; o += align_up(N / 8 + 8);
@@ -586,10 +587,12 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
   uint32_t* sdil = (uint32_t*)(sw + S.sdil);
   const int64_t dwords = (g.N + 31) / 32;
   uint8_t* desc = (uint8_t*)(sw + S.cb);
+  uint32_t* canc = (uint32_t*)(sw + S.canc);
   if (nb > 0) {
     CK(cudaMemsetAsync(&W.dc->pad[2], 0, 8, s));
-    k_cell_desc_short<<<clamp_blocks(nb, 256), 256, 0, s>>>(off, kind, cells, nb, desc, first, &W.dc->pad[2]);
-    k_cell_desc_long<<<148 * 8, 256, 0, s>>>(off, kind, cells, first, &W.dc->pad[2], desc);
+    k_cell_desc_short<D><<<clamp_blocks(nb, 256), 256, 0, s>>>(off, kind, cells, nb, desc, canc, first,
+                                                               &W.dc->pad[2]);
+    k_cell_desc_long<D><<<148 * 8, 256, 0, s>>>(off, kind, cells, first, &W.dc->pad[2], desc, canc);
     CK(cudaGetLastError());
     st->launches += 2;
   }
@@ -669,8 +672,8 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
     }
     if (nc > 0) {
       const int64_t nblk = ((nc + 31) / 32 + 8 * TM_U - 1) / (8 * TM_U);  // 8 warps x TM_U words per block
-      k_tm_cells<D><<<(unsigned)nblk, 256, 0, s>>>(cells, nc, desc, W.cand_f, W.cand_g, W.crit_f, g, sdil, full,
-                                                   mbits, W.dc);
+      k_tm_cells<D><<<(unsigned)nblk, 256, 0, s>>>(cells, nc, desc, canc, W.cand_f, W.cand_g, W.crit_f, g, sdil,
+                                                   full, mbits, W.dc);
     }
     k_tm_targets<D><<<clamp_blocks(nb, 256, 148 * 64), 256, 0, s>>>(cells, off, kind, origin, nb, W.cand_f, W.cand_g,
                                                                     W.crit_f, g, rg, mbits, flag, sdil, full,
@@ -1037,6 +1040,7 @@ dmtz_status dmtz_preserve(dmtz_ctx* c, const float* f, const float* fhat, const 
     st->status = DMTZ_E_OOM;
     return DMTZ_E_OOM;
   }
+  if (c->g.N >= (1ll << 32)) { set_err("tiers 3-5 need fewer than 2^32 vertices per context"); return DMTZ_E_DIMS; }
   const size_t need = sep_layout(c, o->tier, cap_b, cap_c).total;
   if (!sep_ws || sep_ws_bytes < need) {
     set_err("separatrix workspace %zu < %zu bytes", sep_ws_bytes, need);

@@ -37,23 +37,31 @@ __device__ __forceinline__ uint8_t cell_desc(int k, int64_t pos, int64_t len, ui
   return (id >> 56) == 2 ? 4 : 0;
 }
 
+template <int D>
+__device__ __forceinline__ void put_desc(int k, int64_t pos, int64_t len, uint64_t id, uint8_t* desc, uint32_t* anc,
+                                         int64_t i);
+
+template <int D>
 __global__ void k_cell_desc_short(const long long* __restrict__ off, const uint8_t* __restrict__ kind,
                                   const uint64_t* __restrict__ cells, int64_t nb, uint8_t* __restrict__ desc,
-                                  uint32_t* __restrict__ long_list, unsigned long long* __restrict__ n_long) {
+                                  uint32_t* __restrict__ anc, uint32_t* __restrict__ long_list,
+                                  unsigned long long* __restrict__ n_long) {
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i0 = off[b], i1 = off[b + 1];
     const int k = kind[b];
     if (i1 - i0 <= 32) {
-      for (int64_t i = i0; i < i1; i++) desc[i] = cell_desc(k, i - i0, i1 - i0, cells[i]);
+      for (int64_t i = i0; i < i1; i++) put_desc<D>(k, i - i0, i1 - i0, cells[i], desc, anc, i);
     } else {
       long_list[atomicAdd(n_long, 1ull)] = (uint32_t)b;
     }
   }
 }
 
+template <int D>
 __global__ void k_cell_desc_long(const long long* __restrict__ off, const uint8_t* __restrict__ kind,
                                  const uint64_t* __restrict__ cells, const uint32_t* __restrict__ long_list,
-                                 const unsigned long long* __restrict__ n_long, uint8_t* __restrict__ desc) {
+                                 const unsigned long long* __restrict__ n_long, uint8_t* __restrict__ desc,
+                                 uint32_t* __restrict__ anc) {
   const int lane = threadIdx.x & 31;
   const int64_t n = (int64_t)*n_long;
   for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n;
@@ -61,7 +69,7 @@ __global__ void k_cell_desc_long(const long long* __restrict__ off, const uint8_
     const uint32_t b = long_list[w];
     const int64_t i0 = off[b], i1 = off[b + 1];
     const int k = kind[b];
-    for (int64_t i = i0 + lane; i < i1; i += 32) desc[i] = cell_desc(k, i - i0, i1 - i0, cells[i]);
+    for (int64_t i = i0 + lane; i < i1; i += 32) put_desc<D>(k, i - i0, i1 - i0, cells[i], desc, anc, i);
   }
 }
 
@@ -128,6 +136,19 @@ __device__ __forceinline__ void id_cell_fast(uint64_t id, int64_t& a, int& t) {
   t = t_first_of_dim_c<D>(d) + (int)(r - q * (uint64_t)types_of_dim<D>(d));
 }
 
+// desc[i] and, for examined cells, anc[i] = the cell's anchor (grids below 2^32 vertices)
+template <int D>
+__device__ __forceinline__ void put_desc(int k, int64_t pos, int64_t len, uint64_t id, uint8_t* desc, uint32_t* anc,
+                                         int64_t i) {
+  const uint8_t d = cell_desc(k, pos, len, id);
+  desc[i] = d;
+  if (d) {
+    int64_t A; int t;
+    id_cell_fast<D>(id, A, t);
+    anc[i] = (uint32_t)A;
+  }
+}
+
 __device__ __forceinline__ bool dbit(const uint32_t* __restrict__ d, int64_t v) {
   return (__ldg(d + (v >> 5)) >> (v & 31)) & 1u;
 }
@@ -151,13 +172,13 @@ constexpr int TM_U = 4;
 template <int D>
 __global__ void __launch_bounds__(256)
 k_tm_cells(const uint64_t* __restrict__ cells, int64_t n_cells, const uint8_t* __restrict__ desc,
-           const void* __restrict__ cf, const void* __restrict__ cg, const uint32_t* __restrict__ crit_f, Grid g,
-           const uint32_t* __restrict__ sdirty /* dilated */, int full, uint32_t* __restrict__ mbits,
-           Counters* __restrict__ cnt) {
+           const uint32_t* __restrict__ anc, const void* __restrict__ cf, const void* __restrict__ cg,
+           const uint32_t* __restrict__ crit_f, Grid g, const uint32_t* __restrict__ sdirty /* dilated */, int full,
+           uint32_t* __restrict__ mbits, Counters* __restrict__ cnt) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * TM_U;  // first word of the warp
   int k[TM_U];
-  uint64_t id[TM_U];
+  uint32_t a[TM_U];
 #pragma unroll
   for (int u = 0; u < TM_U; u++) {
     const int64_t i = (w0 + u) * 32 + lane;
@@ -166,24 +187,22 @@ k_tm_cells(const uint64_t* __restrict__ cells, int64_t n_cells, const uint8_t* _
 #pragma unroll
   for (int u = 0; u < TM_U; u++) {
     const int64_t i = (w0 + u) * 32 + lane;
-    id[u] = k[u] ? __ldg(cells + i) : 0ull;
+    a[u] = k[u] ? __ldg(anc + i) : 0u;
   }
-  int64_t A[TM_U];
-  int t[TM_U];
   bool dirty[TM_U];
 #pragma unroll
-  for (int u = 0; u < TM_U; u++) {
-    id_cell_fast<D>(id[u], A[u], t[u]);
-    dirty[u] = full ? ((w0 + u) * 32 + lane < n_cells) : (k[u] && dbit(sdirty, A[u]));
-  }
+  for (int u = 0; u < TM_U; u++)
+    dirty[u] = full ? ((w0 + u) * 32 + lane < n_cells) : (k[u] && dbit(sdirty, (int64_t)a[u]));
   unsigned long long nre = 0;
 #pragma unroll
   for (int u = 0; u < TM_U; u++) {
     bool mis = false;
     if (k[u] && dirty[u]) {
       nre++;
+      int64_t A; int t;
+      id_cell_fast<D>(__ldg(cells + (w0 + u) * 32 + lane), A, t);
       int j;
-      mis = k[u] == 4 ? conn_tri_differs<D>(cf, cg, crit_f, g, A[u], t[u], &j) : pair_differs<D>(cf, cg, g, A[u], t[u]);
+      mis = k[u] == 4 ? conn_tri_differs<D>(cf, cg, crit_f, g, A, t, &j) : pair_differs<D>(cf, cg, g, A, t);
     }
     const unsigned dm = __ballot_sync(0xffffffffu, dirty[u]), mm = __ballot_sync(0xffffffffu, mis);
     if (lane == 0 && dm) {
