@@ -379,6 +379,27 @@ def main():
         ems = float(np.median(et))
         e2e = {"value": N * r2.stats["sweeps"] / (ems * 1e-3) / 1e6, "unit": "Mvoxels/s",
                "h2d_bytes_per_step": 2 * 4 * N, "d2h_bytes_per_step": 4 * N + 16 * r2.n_edits, "ms_per_step": ems}
+        # variant: the compressor-side artifact only -- the encoded edit stream comes back
+        # (the decompressor rebuilds g from fhat + stream, dmtz_apply_edits)
+        sh = torch.empty(int(dmtz.lib().dmtz_edit_stream_bound(N)), dtype=torch.uint8).pin_memory()
+        et2 = []
+        for _ in range(2):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ft.copy_(fp, non_blocking=True)
+            fht.copy_(fhp, non_blocking=True)
+            r3 = step()
+            sb = ctx.encode_edits(edits[:r3.n_edits], xi, 6)
+            sh[:sb.numel()].copy_(sb, non_blocking=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            et2.append(e0.elapsed_time(e1))
+        ems2 = float(np.median(et2))
+        e2e["stream_variant"] = {"value": N * r3.stats["sweeps"] / (ems2 * 1e-3) / 1e6, "unit": "Mvoxels/s",
+                                 "h2d_bytes_per_step": 2 * 4 * N, "d2h_bytes_per_step": int(sb.numel()),
+                                 "ms_per_step": ems2, "result": "encoded edit stream (dmtz_encode_edits)"}
+        del sb
 
     cpu = None
     if not args.no_cpu_baseline:
