@@ -363,7 +363,7 @@ __device__ __forceinline__ int compact_group(uint32_t m, int lane, uint16_t* lis
 }
 
 #ifndef DMTZ_DECODE_MINB
-#define DMTZ_DECODE_MINB 8
+#define DMTZ_DECODE_MINB 7
 #endif
 template <int D>
 __global__ void __launch_bounds__(DECODE_THREADS, DMTZ_DECODE_MINB)
