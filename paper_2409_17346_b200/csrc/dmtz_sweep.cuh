@@ -119,8 +119,13 @@ __device__ __forceinline__ uint64_t cand_of(const float (&s)[27]) {
 // are compacted into full warps (lane = one anchor).
 // ---------------------------------------------------------------------------
 constexpr int SCREEN_THREADS = 256;
+#ifdef DMTZ_SCREEN_MINB
+#define DMTZ_SCREEN_LB __launch_bounds__(SCREEN_THREADS, DMTZ_SCREEN_MINB)
+#else
+#define DMTZ_SCREEN_LB __launch_bounds__(SCREEN_THREADS)
+#endif
 template <int D>
-__global__ void __launch_bounds__(SCREEN_THREADS)
+__global__ void DMTZ_SCREEN_LB
 k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg, uint32_t* __restrict__ ebits,
          uint32_t* __restrict__ vchg, int64_t vwords, int use_skip, const uint32_t* __restrict__ units,
          const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg, const LoopState* __restrict__ ls,
