@@ -156,8 +156,8 @@ def run_reference(args, cfg, f, fh, xi):
     print(json.dumps(line), flush=True)
 
 
-def sloop_line(name, dev, stream, with_cpu):
-    """Tiers 3-4: the alternating C/S workflow to its fixed point on
+def sloop_line(name, tiers, dev, stream, with_cpu):
+    """Tiers 3-5: the alternating C/S workflow to its fixed point on
     one config, device-resident inputs, CUDA events on the launching stream (1 warm-up,
     median of 2), and the oracle's workflow on a crop of the same config."""
     import torch
@@ -166,7 +166,7 @@ def sloop_line(name, dev, stream, with_cpu):
     ft, fht = torch.from_numpy(f).to(dev), torch.from_numpy(fh).to(dev)
     ctx = dmtz.Context(f.shape, dev)
     out = {"workload": f"{cfg.name} {cfg.family} {'x'.join(map(str, f.shape))} rel eps {cfg.eps}"}
-    for tier in (4, 3, 5):
+    for tier in tiers:
         ctx.preserve(ft, fht, xi, tier=tier)
         ts = []
         for _ in range(2):
@@ -186,22 +186,25 @@ def sloop_line(name, dev, stream, with_cpu):
             "c_rounds": s["c_rounds"], "s_rounds": s["s_rounds"], "troublemakers": s["troublemakers"],
             "tm_by_kind": s["tm_by_kind"], "n_edited": r.n_edits, "sep_branches": s["sep_branches"],
             "sep_cells": s["sep_cells"], "trace_of_f_ms": s["trace_ms"], "s_rounds_ms": s["s_ms"],
-            "cells_rechecked": s["cells_checked"]}
+            "cells_rechecked": s["cells_checked"],
+            "note": "includes sizing the separatrix CSR (a trace of f) in the binding" }
+        del r
+        torch.cuda.empty_cache()
     del ctx
     torch.cuda.empty_cache()
     if with_cpu:
         import oracle
-        crop = tuple(min(n, 96) for n in f.shape) if len(f.shape) == 3 else tuple(min(n, 240) for n in f.shape)
+        crop = tuple(min(n, 64) for n in f.shape) if len(f.shape) == 3 else tuple(min(n, 240) for n in f.shape)
         sl = tuple(slice(0, n) for n in crop)
         fc, fhc = np.ascontiguousarray(f[sl]), np.ascontiguousarray(fh[sl])
         t0 = time.perf_counter()
-        ro = oracle.preserve(fc, fhc, xi, tier=4)
+        ro = oracle.preserve(fc, fhc, xi, tier=max(tiers))
         dt = time.perf_counter() - t0
         so = ro["stats"]
         n = fc.size * (so["c_rounds"] + so["s_rounds"] + 1)
         out["cpu_baseline"] = {"value": n / dt / 1e6, "unit": "Mvoxels/s (voxels x rounds / time)",
                                "cores": oracle.num_threads(), "kind": "oracle",
-                               "sample": f"oracle tier-4 workflow on the {list(crop)} crop of {cfg.name} "
+                               "sample": f"oracle tier-{max(tiers)} workflow on the {list(crop)} crop of {cfg.name} "
                                          f"({so['c_rounds']} C- + {so['s_rounds']} S-rounds in {dt:.1f} s)"}
     return out
 
@@ -219,7 +222,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-trace", action="store_true")
     ap.add_argument("--slab", action="store_true", help="run the multi-GPU slab path even with one rank")
-    ap.add_argument("--sloop-config", default="C2", help="config of the tier-3/4 workflow line ('none' skips it)")
+    ap.add_argument("--sloop-config", default="C4:4,5;C2:3,4,5",
+                    help="configs:tiers of the tier-3/4/5 workflow lines, e.g. 'C4:4,5;C2:3,4,5' ('none' skips)")
     args = ap.parse_args()
     if args.impl == "dmtz":
         args.warmup = max(args.warmup, 3)
@@ -438,7 +442,10 @@ def main():
     if args.sloop_config != "none":
         del ctx
         torch.cuda.empty_cache()
-        sloop = sloop_line(args.sloop_config, dev, stream, not args.no_cpu_baseline)
+        sloop = {}
+        for item in args.sloop_config.split(";"):
+            name, tl = item.split(":")
+            sloop[name] = sloop_line(name, [int(t) for t in tl.split(",")], dev, stream, not args.no_cpu_baseline)
 
     st = r.stats
     line = {
