@@ -18,6 +18,8 @@
 
 #include <vector>
 
+#include <cstdlib>
+
 #include "dmtz_kernels.cuh"
 
 namespace dmtz {
@@ -506,11 +508,15 @@ __device__ __forceinline__ void conn_expand(const ConnTab& T, const uint32_t* __
 #endif
 constexpr int CQ = DMTZ_CQ;
 constexpr int CONN_THREADS = 128;
+constexpr int CONN_CHUNK = 1024;                       // pool entries taken per atomic
+constexpr uint64_t CONN_NOT_STORED = ~0ull - 1;        // terminal slot: events not in the pool
 template <int D>
 __global__ void __launch_bounds__(CONN_THREADS)
 k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
              const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm, long long* __restrict__ off,
-             uint64_t* __restrict__ cells, bool write, unsigned int* __restrict__ overflow, int64_t conn_base) {
+             uint64_t* __restrict__ cells, bool write, unsigned int* __restrict__ overflow, int64_t conn_base,
+             uint32_t* __restrict__ pool, unsigned long long* __restrict__ pool_top, int64_t pool_cap,
+             int64_t pool_limit) {
   __shared__ uint32_t sq[CQ][CONN_THREADS];
   uint32_t* q = &sq[0][threadIdx.x];   // q[k * CONN_THREADS]: conflict-free columns
   // triangle -> facet edges (dm | edge index << 3); edge slot -> cofacet (type | anchor delta + 1)
@@ -539,12 +545,42 @@ k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
   auto key = [](int dx, int dy, int dz, int ty) {
     return (uint32_t)(dx + 64) | ((uint32_t)(dy + 64) << 7) | ((uint32_t)(dz + 64) << 14) | ((uint32_t)ty << 21);
   };
+  // Event pool (count pass): each thread appends the events of its connectors to a
+  // chunk of the pool (taken with one atomic per CONN_CHUNK entries), and the branch's
+  // terminal slot keeps the pool position until the write pass, which then copies the
+  // events instead of redoing the BFS.  Event = 32-bit key relative to the origin
+  // anchor, bit 31 set for a reached critical edge.
+  uint32_t* chunk = nullptr;
+  int chunk_left = 0;
   for (int64_t b = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
        b += (int64_t)gridDim.x * blockDim.x) {
     int64_t a;
     int t;
     id_cell<D>(origin[b], a, t);
     uint64_t* out = write ? cells + off[b] : nullptr;
+    if (write) {
+      const uint64_t p = jterm[b];
+      const int64_t n0 = off[b + 1] - off[b];
+      if (p < CONN_NOT_STORED && (int64_t)p + n0 <= pool_limit) {  // stored by the count pass: copy
+        for (int64_t i = 0; i < n0; i++) {
+          const uint32_t e = pool[p + i];
+          const int ex = (int)(e & 127) - 64, ey = (int)((e >> 7) & 127) - 64, ez = (int)((e >> 14) & 127) - 64;
+          out[i] = cell_id<D>(a + ex + ey * g.sy + ez * g.sz, (int)((e >> 21) & 31));
+        }
+        jterm[b] = CELL_BOUNDARY;
+        continue;
+      }
+    }
+    // count pass: room for the connector's events (<= 3 per visited triangle)
+    uint32_t* ev_out = nullptr;
+    if (!write && pool) {
+      if (chunk_left < 3 * CQ) {
+        const unsigned long long p = atomicAdd(pool_top, (unsigned long long)CONN_CHUNK);
+        if ((int64_t)(p + CONN_CHUNK) <= pool_cap) { chunk = pool + p; chunk_left = CONN_CHUNK; }
+        else { chunk = nullptr; chunk_left = 0; }
+      }
+      ev_out = chunk;
+    }
     int head = 0, tail = 1;
     int64_t n = 0;
     bool ovf = false;
@@ -568,6 +604,7 @@ k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
         const int dm = (int)(tf[j] & 7), e = (int)(tf[j] >> 3);
         if (ev[j] & 8u) {  // critical edge: a reached 1-saddle
           if (write) out[n] = cell_id<D>(E[j], E0 + e);
+          else if (ev_out) ev_out[n] = key(bx + (dm & 1), by + ((dm >> 1) & 1), bz + ((dm >> 2) & 1), E0 + e) | 0x80000000u;
           n++;
           continue;
         }
@@ -585,16 +622,28 @@ k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
         if (tail == CQ) { ovf = true; break; }
         q[(tail++) * CONN_THREADS] = k;
         if (write) out[n] = cell_id<D>(a + nx_ + ny_ * g.sy + nz_ * g.sz, nt);
+        else if (ev_out) ev_out[n] = k;
         n++;
       }
     }
     if (ovf) {
       const int64_t cb = b - conn_base;
       atomicOr(overflow + (cb >> 5), 1u << (cb & 31));
+      if (!write) jterm[b] = CONN_NOT_STORED;
       continue;
     }
-    if (!write) off[b] = n;
-    else jterm[b] = CELL_BOUNDARY;
+    if (!write) {
+      off[b] = n;
+      if (ev_out) {
+        jterm[b] = (uint64_t)(ev_out - pool);
+        chunk += n;
+        chunk_left -= (int)n;
+      } else {
+        jterm[b] = CONN_NOT_STORED;
+      }
+    } else {
+      jterm[b] = CELL_BOUNDARY;
+    }
   }
 }
 
@@ -1023,17 +1072,26 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   const int64_t list_cap = (pre_words * 8 - (ovf_words + 2) * 4) / 4;
   const int64_t blocks_path = conn_base > 0 ? (conn_base + threads - 1) / threads : 0;
   long long* off = (long long*)A.out_offsets;
+  // connector event pool: the (still unused) output cell buffer during the count pass.
+  // The write pass copies the connectors first, then writes the paths over the pool;
+  // an event list is copied only if it lies below off[conn_base] (the paths' region),
+  // where the connectors' own output cannot overwrite it.
+  const char* pe = getenv("DMTZ_CONN_POOL");
+  uint32_t* pool = (A.out_cells && A.cap_c > 0 && nbk[2] && !(pe && pe[0] == '0')) ? (uint32_t*)A.out_cells : nullptr;
+  const int64_t pool_cap = pool ? 2 * A.cap_c : 0;
+  int64_t pool_limit = 0;
+  TCK(cudaMemsetAsync(&dc->pad[2], 0, 8, s));
   for (int pass = 0; pass < 2; pass++) {
     const bool write = pass == 1;
     TCK(cudaMemsetAsync(ovf, 0, (size_t)ovf_words * 4 + 4, s));
-    if (blocks_path)  // descending / ascending paths: one thread per branch
+    if (blocks_path && !write)  // descending / ascending paths: one thread per branch
       k_walk<D><<<(unsigned)blocks_path, threads, 0, s>>>(V, g, 0, conn_base, A.out_origin, A.out_kind,
                                                           A.out_terminal, off, A.out_cells, write, dc);
     if (nbk[2]) {  // connectors: one thread per 2-saddle, small queues in shared memory
       const int64_t nbc = (nbk[2] + CONN_THREADS - 1) / CONN_THREADS;
       k_conn_small<D><<<(unsigned)(nbc < 148 * 64 ? nbc : 148 * 64), CONN_THREADS, 0, s>>>(
           V.eview, g, conn_base, nb, A.out_origin, A.out_terminal, off, A.out_cells, write,
-          (unsigned int*)ovf, conn_base);
+          (unsigned int*)ovf, conn_base, pool, &dc->pad[2], pool_cap, pool_limit);
     }
     TCK(cudaGetLastError());
     if (nbk[2]) {  // connectors that outgrew their slot: retry with 16x bigger slots, fewer threads
@@ -1101,11 +1159,21 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
         q = qn;
       }
     }
+    if (blocks_path && write)  // after the connectors: the paths overwrite the event pool
+      k_walk<D><<<(unsigned)blocks_path, threads, 0, s>>>(V, g, 0, conn_base, A.out_origin, A.out_kind,
+                                                          A.out_terminal, off, A.out_cells, write, dc);
+    TCK(cudaGetLastError());
     if (!write) {
       TCK(cudaMemsetAsync(off + nb, 0, 8, s));
       TCK(scan_i64(off, nb + 1, A.bsum, total, &hc->pad[0], s));
       A.n_cells = (int64_t)hc->pad[0];
       if (A.n_cells > A.cap_c) break;
+      if (pool) {
+        long long oc = 0;
+        TCK(cudaMemcpyAsync(&oc, off + conn_base, 8, cudaMemcpyDeviceToHost, s));
+        TCK(cudaStreamSynchronize(s));
+        pool_limit = 2 * (int64_t)oc;
+      }
     }
   }
   TCK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, s));
