@@ -1078,7 +1078,11 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   // where the connectors' own output cannot overwrite it.
   const char* pe = getenv("DMTZ_CONN_POOL");
   uint32_t* pool = (A.out_cells && A.cap_c > 0 && nbk[2] && !(pe && pe[0] == '0')) ? (uint32_t*)A.out_cells : nullptr;
-  const int64_t pool_cap = pool ? 2 * A.cap_c : 0;
+  int64_t pool_cap = pool ? 2 * A.cap_c : 0;
+  if (const char* pc = getenv("DMTZ_CONN_POOL_CAP")) {  // tests: a small pool forces the fallback path
+    const long long c = atoll(pc);
+    if (c >= 0 && c < pool_cap) pool_cap = c;
+  }
   int64_t pool_limit = 0;
   TCK(cudaMemsetAsync(&dc->pad[2], 0, 8, s));
   for (int pass = 0; pass < 2; pass++) {

@@ -307,3 +307,15 @@ def test_full_size_cloop_C5_one_gpu(dmtz):
     cf = dmtz.critical_mask(dmtz.compute_gradient(ft))
     cg = dmtz.critical_mask(dmtz.compute_gradient(g))
     assert torch.equal(cf, cg)
+
+
+@pytest.mark.parametrize("cap", ["0", "2048", "5000"])
+def test_trace_connector_pool_fallback(dmtz, monkeypatch, cap):
+    """The connector events kept by the count pass (a pool in the output buffer) and the
+    BFS redone in the write pass give the same CSR: a pool too small for every connector
+    (DMTZ_CONN_POOL_CAP entries) mixes both paths; DMTZ_CONN_POOL=0 disables the pool."""
+    f, _, _ = di.random_case((20, 22, 24), 11, family="lognormal")
+    monkeypatch.setenv("DMTZ_CONN_POOL_CAP", cap)
+    _compare_trace(dmtz, f)
+    monkeypatch.setenv("DMTZ_CONN_POOL", "0")
+    _compare_trace(dmtz, f)
