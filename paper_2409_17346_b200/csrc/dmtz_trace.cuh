@@ -236,41 +236,65 @@ k_branch_tiles(const uint32_t* __restrict__ crit, Grid g, int kind, int64_t a_lo
   if (threadIdx.x == 0) bsum[blockIdx.x] = (unsigned long long)tot;
 }
 
+// Emission: warp w of the block takes anchors [w * 256, w * 256 + 256) of the tile in
+// 8 steps of 32 consecutive anchors (lane = anchor), so every step writes one dense
+// range of the outputs (coalesced) in (anchor, type, branch) order.
 template <int D>
 __global__ void __launch_bounds__(BT_THREADS)
 k_branch_tiles_emit(const uint32_t* __restrict__ crit, Grid g, int kind, int64_t a_lo, int64_t a_hi,
                     const unsigned long long* __restrict__ bscan, int64_t base, uint64_t* __restrict__ origin,
                     uint8_t* __restrict__ kout, uint64_t* __restrict__ jout) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t w0 = (int64_t)blockIdx.x * BT_TILE + (int64_t)wid * 32 * BT_PER;  // the warp's first anchor
   int c[BT_PER];
-  const int64_t a0 = (int64_t)blockIdx.x * BT_TILE + threadIdx.x * BT_PER;
-  const int t = tile_counts<D>(crit, g, kind, a0, a_lo, a_hi, c);
+  uint32_t cm[BT_PER];
+  int wtot = 0;
+#pragma unroll
+  for (int k = 0; k < BT_PER; k++) {
+    const int64_t a = w0 + k * 32 + lane;
+    int64_t x, y, z;
+    coords_of(g, a < g.N ? a : 0, x, y, z);
+    cm[k] = a < g.N && a >= a_lo && a < a_hi ? __ldg(crit + a) : 0u;
+    c[k] = cm[k] ? branch_count<D>(g, kind, cm[k], x, y, z) : 0;
+    wtot += __reduce_add_sync(0xffffffffu, (unsigned)c[k]);
+  }
   long long tot;
-  int64_t b = base + (int64_t)bscan[blockIdx.x] + block_exclusive_scan(t, &tot);
-  if (!t) return;
-  int64_t x, y, z;
-  coords_of(g, a0, x, y, z);
+  // exclusive scan of the warp totals in warp order = anchor order
+  const long long wbase = block_exclusive_scan(lane == 0 ? wtot : 0, &tot);
+  int64_t b = base + (int64_t)bscan[blockIdx.x] + __shfl_sync(0xffffffffu, wbase, 0);
   const int top = Tr<D>::TOP;
-  for (int k = 0; k < BT_PER; k++, (++x == g.nx ? (x = 0, (++y == g.ny ? (y = 0, ++z) : 0)) : 0)) {
+#pragma unroll 1
+  for (int k = 0; k < BT_PER; k++) {
+    int pre = c[k];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= o) pre += v;
+    }
+    const int stot = __shfl_sync(0xffffffffu, pre, 31);
+    int64_t p = b + pre - c[k];
+    b += stot;
     if (!c[k]) continue;
-    const int64_t a = a0 + k;
-    const uint32_t cm = __ldg(crit + a);
+    const int64_t a = w0 + k * 32 + lane;
     if (kind == 1) {
       for (int tt = 1; tt < t_first_of_dim<D>(2); tt++) {
-        if (!((cm >> tt) & 1u)) continue;
-        for (int j = 0; j < 2; j++) { origin[b] = cell_id<D>(a, tt); kout[b] = 1; jout[b] = (uint64_t)j; b++; }
+        if (!((cm[k] >> tt) & 1u)) continue;
+        for (int j = 0; j < 2; j++) { origin[p] = cell_id<D>(a, tt); kout[p] = 1; jout[p] = (uint64_t)j; p++; }
       }
     } else if (kind == 2) {
+      int64_t x, y, z;
+      coords_of(g, a, x, y, z);
       for (int tt = t_first_of_dim<D>(top - 1); tt < t_first_of_dim<D>(top); tt++) {
-        if (!((cm >> tt) & 1u)) continue;
+        if (!((cm[k] >> tt) & 1u)) continue;
         for (int s = 0; s < t_nlink<D>(tt); s++) {
           if (!link_in_grid_xyz<D>(g, x, y, z, tt, s)) continue;
-          origin[b] = cell_id<D>(a, tt); kout[b] = 2; jout[b] = (uint64_t)s; b++;
+          origin[p] = cell_id<D>(a, tt); kout[p] = 2; jout[p] = (uint64_t)s; p++;
         }
       }
     } else if (D == 3) {
       for (int tt = t_first_of_dim<D>(2); tt < t_first_of_dim<D>(3); tt++) {
-        if (!((cm >> tt) & 1u)) continue;
-        origin[b] = cell_id<D>(a, tt); kout[b] = 4; jout[b] = 0; b++;
+        if (!((cm[k] >> tt) & 1u)) continue;
+        origin[p] = cell_id<D>(a, tt); kout[p] = 4; jout[p] = 0; p++;
       }
     }
   }
