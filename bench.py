@@ -30,6 +30,7 @@ crop of the same workload on the host cores.
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import subprocess
@@ -130,7 +131,7 @@ def oracle_sample(f, fh, xi, edge):
     dt = time.perf_counter() - t0
     sweeps = r["stats"]["rounds"] + 1
     return dict(value=fc.size * sweeps / dt / 1e6, seconds=dt, sweeps=sweeps, shape=list(fc.shape),
-                rounds=r["stats"]["rounds"], threads=oracle.num_threads())
+                rounds=r["stats"]["rounds"], threads=oracle.num_threads(), ref=r, fc=fc, fhc=fhc)
 
 
 def run_reference(args, cfg, f, fh, xi):
@@ -294,7 +295,8 @@ def main():
     value = N * sweeps / (ms * 1e-3) / 1e6
     fr_ms = float(np.median(fr_t))
     full_recompute = {"value": N * rfull.stats["sweeps"] / (fr_ms * 1e-3) / 1e6, "unit": "Mvoxels/s",
-                      "ms_per_step": fr_ms, "mode": "full_sweeps=1: every code recomputed, every anchor classified"}
+                      "ms_per_step": fr_ms, "t_round_full_ms": fr_ms / rfull.stats["sweeps"],
+                      "mode": "full_sweeps=1: every code recomputed, every anchor classified"}
 
     # roofline of the dominant kernel of the default step (live CUDA events on the launching stream,
     # one extra host-driven step): k_decode; k_screen's on the rounds that recompute every code
@@ -353,7 +355,15 @@ def main():
                 kinds = torch.bincount(tr["kind"].long(), minlength=5).tolist()
                 trace = {"trace_ms": e0.elapsed_time(e1), "n_branches": sizes["n_branches"],
                          "n_cells": sizes["n_cells"], "desc": kinds[1], "asc": kinds[2], "conn": kinds[4]}
-                del tr, bufs
+                del tr
+                for kname, kb in (("desc_ms", 1), ("asc_ms", 2), ("conn_ms", 4)):   # one kind per call
+                    torch.cuda.synchronize()
+                    e0.record(stream)
+                    ctx.trace_separatrices(codes, kinds=kb, out=bufs)
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    trace[kname] = e0.elapsed_time(e1)
+                del bufs
             else:
                 trace = {"skipped": f"needs {need / 1e9:.1f} GB of outputs", **sizes}
         except Exception as e:  # noqa: BLE001
@@ -406,11 +416,29 @@ def main():
         del sb
 
     cpu = None
+    parity = None
     if not args.no_cpu_baseline:
         s = oracle_sample(f, fh, xi, args.ref_edge)
         cpu = {"value": s["value"], "unit": "Mvoxels/s", "cores": s["threads"], "kind": "oracle",
                "sample": f"oracle C-loop to its fixed point on the {s['shape']} crop of {cfg.name} "
                          f"({s['sweeps']} sweeps in {s['seconds']:.1f} s)"}
+        # parity on the same crop: the CUDA path against the oracle, bit for bit
+        import oracle
+        ref, fc, fhc = s["ref"], s["fc"], s["fhc"]
+        fct, fhct = torch.from_numpy(fc).to(dev), torch.from_numpy(fhc).to(dev)
+        rc = dmtz.correct(fct, fhct, xi)
+        oc, om = oracle.gradient(fc)
+        gc = dmtz.compute_gradient(fct)
+        e = rc.edits_numpy()
+        tr_o = oracle.trace(ref["g"])
+        tr_g = dmtz.trace_separatrices(dmtz.compute_gradient(rc.g))
+        parity = {"crop": s["shape"],
+                  "codes": bool(np.array_equal(gc.cpu().numpy().view(oc.dtype), oc)),
+                  "crit": bool(np.array_equal(dmtz.critical_mask(gc).cpu().numpy().view(np.uint32), om)),
+                  "g_bits": bool(np.array_equal(rc.g.cpu().numpy().view(np.uint32), ref["g"].view(np.uint32))),
+                  "edits": bool(np.array_equal(e["v"], ref["edits"]["v"]) and np.array_equal(e["q"], ref["edits"]["q"])),
+                  "rounds": rc.stats["rounds"] == ref["stats"]["rounds"],
+                  "csr": all(bool(np.array_equal(tr_g[k].cpu().numpy().view(tr_o[k].dtype), tr_o[k])) for k in tr_o)}
 
     # the edit list as an artifact (NEXT-2): encode / decode / apply on the device
     codec = None
@@ -463,6 +491,8 @@ def main():
         "stats": {k: st[k] for k in ("rounds", "sweeps", "n_edited", "n_quantized", "n_lossless", "n_false_round0",
                                      "false_by_kind_round0")},
         "gen_seconds": t_gen,
+        "parity_vs_oracle": parity,
+        "input_sha256": {"f": hashlib.sha256(f.tobytes()).hexdigest(), "fhat": hashlib.sha256(fh.tobytes()).hexdigest()},
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
