@@ -609,6 +609,7 @@ k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
     int64_t n = 0;
     bool ovf = false;
     q[0] = key(0, 0, 0, t);
+    uint64_t filt = 1ull << ((q[0] * 0x9E3779B1u) >> 26);
     while (head < tail && !ovf) {
       const uint32_t cur = q[(head++) * CONN_THREADS];
       const int bx = (int)(cur & 127) - 64, by = (int)((cur >> 7) & 127) - 64, bz = (int)((cur >> 14) & 127) - 64;
@@ -640,11 +641,17 @@ k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
                   nz_ = bz + ((dm >> 2) & 1) + (int)((ec >> 9) & 3) - 1;
         const uint32_t k = key(nx_, ny_, nz_, nt);
         if (k == cur) continue;
-        bool seen = false;
-        for (int i = 0; i < tail; i++) seen |= q[i * CONN_THREADS] == k;
-        if (seen) continue;
+        // membership: a 64-bit filter of the queued keys rules out most new keys without
+        // the linear scan of the queue (which stays exact for the rest)
+        const uint64_t fb = 1ull << ((k * 0x9E3779B1u) >> 26);
+        if (filt & fb) {
+          bool seen = false;
+          for (int i = tail - 1; i >= 0 && !seen; i--) seen = q[i * CONN_THREADS] == k;
+          if (seen) continue;
+        }
         if (tail == CQ) { ovf = true; break; }
         q[(tail++) * CONN_THREADS] = k;
+        filt |= fb;
         if (write) out[n] = cell_id<D>(a + nx_ + ny_ * g.sy + nz_ * g.sz, nt);
         else if (ev_out) ev_out[n] = k;
         n++;
