@@ -139,3 +139,18 @@ def test_tier5_keeps_the_persistence_diagram(dmtz, name, shape):
     ends = np.unique(pf.ravel())
     clamped = e["v"][e["lossless"] > 0]
     assert np.isin(ends, clamped).all()
+
+
+def test_preserve_capacity_and_errors(dmtz):
+    f, fh, xi, _ = di.config_inputs("C4", shape=(24, 24, 24))
+    ft, fht = _cuda(f), _cuda(fh)
+    r = dmtz.preserve(ft, fht, xi, tier=4, sep_caps=(10, 10), raise_on_error=False)
+    assert r.status == dmtz.E_CAPACITY
+    ref = oracle.preserve(f, fh, xi, tier=4)["stats"]
+    assert r.stats["sep_branches"] == ref["sep_branches"]
+    with pytest.raises(dmtz.DmtzError):
+        dmtz.preserve(ft, fht, xi, tier=6)
+    bad = fh.copy()
+    bad[3, 4, 5] = f[3, 4, 5] + np.float32(4 * xi)
+    r = dmtz.preserve(ft, _cuda(bad), xi, tier=4, raise_on_error=False)
+    assert r.status == dmtz.E_BOUND
