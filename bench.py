@@ -404,7 +404,7 @@ def main():
             ft.copy_(fp, non_blocking=True)
             fht.copy_(fhp, non_blocking=True)
             r3 = step()
-            sb = ctx.encode_edits(edits[:r3.n_edits], xi, 6)
+            sb = ctx.encode_edits(edits[:r3.n_edits], xi, 6, fhat=fht)
             sh[:sb.numel()].copy_(sb, non_blocking=True)
             e1.record(stream)
             torch.cuda.synchronize()
@@ -453,16 +453,18 @@ def main():
             e1.record(stream)
             torch.cuda.synchronize()
             return out, e0.elapsed_time(e1)
-        sb, enc_ms = _t(lambda: ctx.encode_edits(ev, xi, 6))
-        (dec, _, _), dec_ms = _t(lambda: ctx.decode_edits(sb))
+        sb1 = ctx.encode_edits(ev, xi, 6)
+        sb, enc_ms = _t(lambda: ctx.encode_edits(ev, xi, 6, fhat=fht))
+        (dec, _, _), dec_ms = _t(lambda: ctx.decode_edits(sb, fhat=fht))
         ga, app_ms = _t(lambda: ctx.apply_edits(fht, xi, dec))
         nbytes = int(sb.numel())
-        codec = {"n_edits": r.n_edits, "stream_bytes": nbytes, "bytes_per_edit": nbytes / max(r.n_edits, 1),
+        codec = {"format": "version 2 (lossless values relative to fhat)", "v1_stream_bytes": int(sb1.numel()),
+                 "n_edits": r.n_edits, "stream_bytes": nbytes, "bytes_per_edit": nbytes / max(r.n_edits, 1),
                  "keyvalue_float_bytes": 12 * r.n_edits, "edit_ratio": r.n_edits / N,
                  "stream_fraction_of_original": nbytes / (4 * N),
                  "encode_ms": enc_ms, "decode_ms": dec_ms, "apply_ms": app_ms,
                  "apply_matches_g": bool(torch.equal(ga.view(torch.int32), g.view(torch.int32)))}
-        del sb, dec, ga
+        del sb, sb1, dec, ga
     except Exception as e:  # noqa: BLE001
         codec = {"error": str(e)[:200]}
 

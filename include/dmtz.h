@@ -264,28 +264,32 @@ dmtz_status dmtz_preserve(dmtz_ctx* ctx, const float* f, const float* fhat, cons
  * rare lossless entries keep their value; Fig. 2: "the edits are applied to
  * the decompressed data ... in the decompression stage".
  *
- * Edit stream, version 1 (little-endian):
- *   0  char[4] "DMTE" | 4 uint32 version = 1 | 8 uint64 n_edits | 16 uint32 edits per
- *   block (4096) | 20 int32 q_max | 24 float xi | 28 uint32 n_blocks | 32 uint64
+ * Edit stream (little-endian):
+ *   0  char[4] "DMTE" | 4 uint32 version (1 or 2) | 8 uint64 n_edits | 16 uint32 edits
+ *   per block (4096) | 20 int32 q_max | 24 float xi | 28 uint32 n_blocks | 32 uint64
  *   block_offset[n_blocks] (byte offset of each block's first record in the payload) |
  *   payload: per edit, ascending v: varint(delta) varint(q << 1 | lossless)
- *   [uint32 value bits if lossless]; delta = v for a block's first edit, else
- *   v - v_prev - 1; varint = unsigned LEB128.
+ *   [lossless only -- version 1: uint32 value bits; version 2: varint(zigzag(d)),
+ *   d = int64(fhat bits as int32) - int64(value bits as int32): the stored value is
+ *   exact and, since fhat - 2 xi <= value <= fhat, d is a few thousand ulps at most];
+ *   delta = v for a block's first edit, else v - v_prev - 1; varint = unsigned LEB128.
  * ------------------------------------------------------------------------ */
 /* Upper bound of the stream size for n_edits edits. */
 size_t dmtz_edit_stream_bound(int64_t n_edits);
 /* Encode a sorted edit list (device, as dmtz_correct writes it) into `out` (device,
  * capacity cap bytes); *nbytes (host) = the stream size (DMTZ_E_CAPACITY if > cap).
- * Uses the workspace as scratch (n_edits <= the context's vertex count).
- * DMTZ_E_ARG if the list is not strictly ascending. */
+ * fhat (device, the decompressed field) != NULL writes version 2 (lossless values
+ * relative to fhat), NULL version 1.  Uses the workspace as scratch (n_edits <= the
+ * context's vertex count).  DMTZ_E_ARG if the list is not strictly ascending. */
 dmtz_status dmtz_encode_edits(dmtz_ctx* ctx, const dmtz_edit* edits, int64_t n_edits, float xi, int32_t q_max,
-                              void* workspace, size_t workspace_bytes, uint8_t* out, size_t cap,
+                              const float* fhat, void* workspace, size_t workspace_bytes, uint8_t* out, size_t cap,
                               size_t* nbytes /* host */, dmtz_stream_t stream);
 /* Decode a stream (device, nbytes) into edits (device, capacity cap); *n_edits, *xi,
- * *q_max (host) from its header.  DMTZ_E_ARG on a malformed stream (bad magic or
- * version, truncated, a vertex outside the context's grid). */
-dmtz_status dmtz_decode_edits(dmtz_ctx* ctx, const uint8_t* in, size_t nbytes, dmtz_edit* edits, int64_t cap,
-                              int64_t* n_edits /* host */, float* xi /* host */, int32_t* q_max /* host */,
+ * *q_max (host) from its header; fhat (device) is required for version 2 (ignored for
+ * version 1).  Quantized entries carry no value (apply recomputes it).  DMTZ_E_ARG on a
+ * malformed stream (bad magic or version, truncated, a vertex outside the grid). */
+dmtz_status dmtz_decode_edits(dmtz_ctx* ctx, const uint8_t* in, size_t nbytes, const float* fhat, dmtz_edit* edits,
+                              int64_t cap, int64_t* n_edits /* host */, float* xi /* host */, int32_t* q_max /* host */,
                               void* workspace, size_t workspace_bytes, dmtz_stream_t stream);
 /* Decompression side: g_out = fhat with every edit applied -- quantized:
  * RN(fhat - RN(q * xi 2^-q_max)) (Eq. 2 replayed from fhat), lossless: the

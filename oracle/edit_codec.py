@@ -25,8 +25,15 @@ def _varint(x: int) -> bytes:
             return bytes(out)
 
 
-def encode(edits: np.ndarray, xi: float, q_max: int) -> bytes:
-    """edits: structured array (v, q, lossless, value) sorted by v."""
+def _rel(fh: float, value: float) -> int:
+    """version 2: zigzag of int64(fhat bits as int32) - int64(value bits as int32)"""
+    d = int(np.float32(fh).view(np.int32)) - int(np.float32(value).view(np.int32))
+    return (d << 1) if d >= 0 else ((-d) << 1) - 1
+
+
+def encode(edits: np.ndarray, xi: float, q_max: int, fhat=None) -> bytes:
+    """edits: structured array (v, q, lossless, value) sorted by v; fhat given -> version 2
+    (lossless values relative to fhat), else version 1."""
     n = len(edits)
     nblocks = (n + BLOCK - 1) // BLOCK
     payload = bytearray()
@@ -42,18 +49,22 @@ def encode(edits: np.ndarray, xi: float, q_max: int) -> bytes:
             delta = v - prev - 1
         payload += _varint(delta) + _varint((q << 1) | ll)
         if ll:
-            payload += np.float32(edits["value"][i]).tobytes()
+            if fhat is None:
+                payload += np.float32(edits["value"][i]).tobytes()
+            else:
+                payload += _varint(_rel(np.asarray(fhat).ravel()[v], edits["value"][i]))
         prev = v
-    head = b"DMTE" + struct.pack("<IQIifI", 1, n, BLOCK, q_max, np.float32(xi), nblocks)
+    head = b"DMTE" + struct.pack("<IQIifI", 1 if fhat is None else 2, n, BLOCK, q_max, np.float32(xi), nblocks)
     return head + b"".join(struct.pack("<Q", o) for o in offsets) + bytes(payload)
 
 
-def decode(data: bytes):
-    """-> (edits structured array, xi, q_max)."""
+def decode(data: bytes, fhat=None):
+    """-> (edits structured array, xi, q_max); version 2 needs fhat."""
     from oracle import EDIT_DTYPE
     assert data[:4] == b"DMTE"
     ver, n, blk, q_max, xi, nblocks = struct.unpack("<IQIifI", data[4:32])
-    assert ver == 1 and blk == BLOCK and nblocks == (n + BLOCK - 1) // BLOCK
+    assert ver in (1, 2) and blk == BLOCK and nblocks == (n + BLOCK - 1) // BLOCK
+    assert ver == 1 or fhat is not None
     pos = 32 + 8 * nblocks
     out = np.zeros(n, EDIT_DTYPE)
     v = -1
@@ -75,8 +86,14 @@ def decode(data: bytes):
         code = get()
         out["v"][i], out["q"][i], out["lossless"][i] = v, code >> 1, code & 1
         if code & 1:
-            out["value"][i] = np.frombuffer(data[pos:pos + 4], "<f4")[0]
-            pos += 4
+            if ver == 1:
+                out["value"][i] = np.frombuffer(data[pos:pos + 4], "<f4")[0]
+                pos += 4
+            else:
+                z = get()
+                d = (z >> 1) if not z & 1 else -((z + 1) >> 1)
+                fb = int(np.float32(np.asarray(fhat).ravel()[v]).view(np.int32))
+                out["value"][i] = np.int32(fb - d).view(np.float32)
     assert pos == len(data)
     return out, float(xi), q_max
 

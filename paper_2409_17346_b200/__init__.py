@@ -108,8 +108,8 @@ def _load():
                                 ctypes.POINTER(i64), ctypes.POINTER(_Stats), ctypes.POINTER(_SStats), P]
     L.dmtz_edit_stream_bound.argtypes = [i64]
     L.dmtz_edit_stream_bound.restype = SZ
-    L.dmtz_encode_edits.argtypes = [P, P, i64, ctypes.c_float, i32, P, SZ, P, SZ, ctypes.POINTER(SZ), P]
-    L.dmtz_decode_edits.argtypes = [P, P, SZ, P, i64, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_float),
+    L.dmtz_encode_edits.argtypes = [P, P, i64, ctypes.c_float, i32, P, P, SZ, P, SZ, ctypes.POINTER(SZ), P]
+    L.dmtz_decode_edits.argtypes = [P, P, SZ, P, P, i64, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_float),
                                     ctypes.POINTER(i32), P, SZ, P]
     L.dmtz_apply_edits.argtypes = [P, P, ctypes.c_float, i32, P, i64, P, P, SZ, P]
     L.dmtz_critical_prf.argtypes = [P, P, P, ctypes.POINTER(_Prf), P, SZ, P]
@@ -320,25 +320,30 @@ class Context:
                       message=msg)
 
     # ---------------------------------------------------------------- edits as an artifact
-    def encode_edits(self, edits: torch.Tensor, xi: float, q_max: int = 6, stream=None) -> torch.Tensor:
-        """Edit list (n, 16) uint8 rows -> the version-1 edit stream (uint8 CUDA tensor)."""
+    def encode_edits(self, edits: torch.Tensor, xi: float, q_max: int = 6, fhat: torch.Tensor | None = None,
+                     stream=None) -> torch.Tensor:
+        """Edit list (n, 16) uint8 rows -> the edit stream (uint8 CUDA tensor); with fhat,
+        version 2 (lossless values relative to fhat), else version 1."""
         _need_cuda(edits)
         n = int(edits.shape[0])
         cap = int(_lib.dmtz_edit_stream_bound(n))
         out = torch.empty(max(cap, 1), dtype=torch.uint8, device=edits.device)
         nb = ctypes.c_size_t()
         _check(_lib.dmtz_encode_edits(self._h, ctypes.c_void_p(edits.data_ptr()) if n else None, n, float(xi),
-                                      int(q_max), ctypes.c_void_p(self.workspace.data_ptr()), self.ws_bytes,
+                                      int(q_max), ctypes.c_void_p(fhat.data_ptr()) if fhat is not None else None,
+                                      ctypes.c_void_p(self.workspace.data_ptr()), self.ws_bytes,
                                       ctypes.c_void_p(out.data_ptr()), cap, ctypes.byref(nb), _stream_ptr(stream)))
         return out[:nb.value]
 
-    def decode_edits(self, stream_bytes: torch.Tensor, stream=None):
-        """Edit stream (uint8 CUDA tensor) -> (edits (n, 16) uint8, xi, q_max)."""
+    def decode_edits(self, stream_bytes: torch.Tensor, fhat: torch.Tensor | None = None, stream=None):
+        """Edit stream (uint8 CUDA tensor) -> (edits (n, 16) uint8, xi, q_max); version 2
+        needs fhat."""
         _need_cuda(stream_bytes)
         cap = self.N
         edits = torch.empty((max(cap, 1), 16), dtype=torch.uint8, device=stream_bytes.device)
         n, xi, qm = ctypes.c_int64(), ctypes.c_float(), ctypes.c_int32()
         _check(_lib.dmtz_decode_edits(self._h, ctypes.c_void_p(stream_bytes.data_ptr()), int(stream_bytes.numel()),
+                                      ctypes.c_void_p(fhat.data_ptr()) if fhat is not None else None,
                                       ctypes.c_void_p(edits.data_ptr()), cap, ctypes.byref(n), ctypes.byref(xi),
                                       ctypes.byref(qm), ctypes.c_void_p(self.workspace.data_ptr()), self.ws_bytes,
                                       _stream_ptr(stream)))

@@ -1063,11 +1063,12 @@ dmtz_status dmtz_preserve(dmtz_ctx* c, const float* f, const float* fhat, const 
 size_t dmtz_edit_stream_bound(int64_t n) {
   if (n < 0) return 0;
   const size_t nb = (size_t)((n + EC_BLOCK - 1) / EC_BLOCK);
-  return EC_HEADER + 8 * nb + (size_t)n * (10 + 3 + 4);
+  return EC_HEADER + 8 * nb + (size_t)n * (10 + 3 + 5);
 }
 
-dmtz_status dmtz_encode_edits(dmtz_ctx* c, const dmtz_edit* edits, int64_t n, float xi, int32_t q_max, void* ws,
-                              size_t wsb, uint8_t* out, size_t cap, size_t* nbytes, dmtz_stream_t stream) {
+dmtz_status dmtz_encode_edits(dmtz_ctx* c, const dmtz_edit* edits, int64_t n, float xi, int32_t q_max,
+                              const float* fhat, void* ws, size_t wsb, uint8_t* out, size_t cap, size_t* nbytes,
+                              dmtz_stream_t stream) {
   if (!c || (n > 0 && !edits) || !ws || !out || !nbytes || n < 0) { set_err("NULL argument"); return DMTZ_E_ARG; }
   if (n > c->g.N) { set_err("%lld edits for %lld vertices", (long long)n, (long long)c->g.N); return DMTZ_E_ARG; }
   const Layout L = layout_for(c);
@@ -1079,7 +1080,7 @@ dmtz_status dmtz_encode_edits(dmtz_ctx* c, const dmtz_edit* edits, int64_t n, fl
   Counters* dc = (Counters*)(w + L.counters);
   Counters* hc = c->host_cnt;
   CK(cudaMemsetAsync(dc, 0, sizeof(Counters), s));
-  k_ec_len<<<clamp_blocks(n + 1, 256), 256, 0, s>>>((const EditRec*)edits, n, len, &dc->pad[1]);
+  k_ec_len<<<clamp_blocks(n + 1, 256), 256, 0, s>>>((const EditRec*)edits, n, fhat, len, &dc->pad[1]);
   CK(cudaGetLastError());
   CK(scan_i64(len, n + 1, bsum, &dc->pad[0], &hc->pad[0], s));  // synchronises: hc->pad[0] = payload bytes
   CK(cudaMemcpyAsync(&hc->pad[1], &dc->pad[1], 8, cudaMemcpyDeviceToHost, s));
@@ -1088,13 +1089,13 @@ dmtz_status dmtz_encode_edits(dmtz_ctx* c, const dmtz_edit* edits, int64_t n, fl
   const size_t nb = (size_t)((n + EC_BLOCK - 1) / EC_BLOCK);
   *nbytes = EC_HEADER + 8 * nb + (size_t)hc->pad[0];
   if (*nbytes > cap) { set_err("edit stream needs %zu bytes", *nbytes); return DMTZ_E_CAPACITY; }
-  k_ec_write<<<clamp_blocks(n > 0 ? n : 1, 256), 256, 0, s>>>((const EditRec*)edits, n, len, xi, q_max, out);
+  k_ec_write<<<clamp_blocks(n > 0 ? n : 1, 256), 256, 0, s>>>((const EditRec*)edits, n, len, xi, q_max, fhat, out);
   CK(cudaGetLastError());
   return DMTZ_OK;
 }
 
-dmtz_status dmtz_decode_edits(dmtz_ctx* c, const uint8_t* in, size_t nbytes, dmtz_edit* edits, int64_t cap,
-                              int64_t* n_edits, float* xi, int32_t* q_max, void* ws, size_t wsb,
+dmtz_status dmtz_decode_edits(dmtz_ctx* c, const uint8_t* in, size_t nbytes, const float* fhat, dmtz_edit* edits,
+                              int64_t cap, int64_t* n_edits, float* xi, int32_t* q_max, void* ws, size_t wsb,
                               dmtz_stream_t stream) {
   if (!c || !in || !n_edits || !xi || !q_max || !ws || cap < 0 || (cap > 0 && !edits)) {
     set_err("NULL argument");
@@ -1111,9 +1112,10 @@ dmtz_status dmtz_decode_edits(dmtz_ctx* c, const uint8_t* in, size_t nbytes, dmt
   uint64_t n = 0;
   for (int k = 0; k < 8; k++) n |= (uint64_t)h[8 + k] << (8 * k);
   const uint32_t ver = u32(4), blk = u32(16), nblocks = u32(28), xib = u32(24);
-  if (memcmp(h, "DMTE", 4) != 0 || ver != 1 || blk != (uint32_t)EC_BLOCK ||
+  if (ver == 2 && !fhat) { set_err("a version-2 edit stream needs fhat"); return DMTZ_E_ARG; }
+  if (memcmp(h, "DMTE", 4) != 0 || (ver != 1 && ver != 2) || blk != (uint32_t)EC_BLOCK ||
       (uint64_t)nblocks != (n + EC_BLOCK - 1) / EC_BLOCK || EC_HEADER + 8 * (size_t)nblocks > nbytes) {
-    set_err("not a version-1 edit stream");
+    set_err("not a version-1/2 edit stream");
     return DMTZ_E_ARG;
   }
   *n_edits = (int64_t)n;
@@ -1124,8 +1126,8 @@ dmtz_status dmtz_decode_edits(dmtz_ctx* c, const uint8_t* in, size_t nbytes, dmt
   Counters* hc = c->host_cnt;
   CK(cudaMemsetAsync(&dc->pad[1], 0, 8, s));
   if (nblocks)
-    k_ec_decode<<<clamp_blocks(nblocks, 128), 128, 0, s>>>(in, nbytes, (int64_t)n, nblocks, c->g.N, (EditRec*)edits,
-                                                           &dc->pad[1]);
+    k_ec_decode<<<clamp_blocks(nblocks, 128), 128, 0, s>>>(in, nbytes, (int64_t)n, nblocks, c->g.N,
+                                                           ver == 2 ? fhat : nullptr, (EditRec*)edits, &dc->pad[1]);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(&hc->pad[1], &dc->pad[1], 8, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));

@@ -63,3 +63,38 @@ def test_apply_replays_the_cloop(q_cap):
     d, x2, qm = ec.decode(ec.encode(r["edits"], xi, 6))
     g = ec.apply(fh, d, x2, qm)
     assert np.array_equal(g.view(np.uint32), r["g"].view(np.uint32))
+
+
+GOLD2 = os.path.join(os.path.dirname(__file__), "golden", "edit_stream_small_v2.json")
+
+
+def test_golden_bytes_v2():
+    g = json.load(open(GOLD2))
+    fhat = np.ones(301, np.float32)
+    fhat[6] = np.uint32(int(g["fhat_bits_at_6"], 16)).view(np.float32)
+    b = ec.encode(_edits(g["edits"]), g["xi"], g["q_max"], fhat=fhat)
+    assert b.hex() == g["hex"].replace(" ", "")
+    d, xi, qm = ec.decode(b, fhat=fhat)
+    assert d.tolist() == _edits(g["edits"]).tolist()
+
+
+@pytest.mark.parametrize("sign", [1.0, -1.0])
+def test_v2_roundtrip_and_size(sign):
+    """relative lossless values round-trip exactly (both signs, crossing zero) and the
+    C-loop's stream shrinks against version 1"""
+    rng = np.random.default_rng(5)
+    n = 5000
+    fhat = (sign * rng.uniform(0.5, 2.0, 10 ** 5)).astype(np.float32)
+    fhat[:10] = np.float32(1e-3) * sign
+    e = np.zeros(n, oracle.EDIT_DTYPE)
+    e["v"] = np.sort(rng.choice(10 ** 5, n, replace=False))
+    e["lossless"] = 1
+    e["value"] = (fhat[e["v"]] - np.float32(0.01)).astype(np.float32)
+    d, _, _ = ec.decode(ec.encode(e, 0.01, 6, fhat=fhat), fhat=fhat)
+    assert np.array_equal(d["value"].view(np.uint32), e["value"].view(np.uint32))
+    f, fh, xi, _ = di.config_inputs("C1")
+    r = oracle.correct(f, fh, xi)
+    v1, v2 = ec.encode(r["edits"], xi, 6), ec.encode(r["edits"], xi, 6, fhat=fh)
+    assert len(v2) < len(v1)
+    d2, _, _ = ec.decode(v2, fhat=fh)
+    assert np.array_equal(ec.apply(fh, d2, xi, 6).view(np.uint32), r["g"].view(np.uint32))

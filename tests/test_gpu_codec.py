@@ -48,6 +48,13 @@ def test_encode_decode_apply(dmtz, name, shape, q_cap):
     g = ctx.apply_edits(fht, x2, d, q_max=qm)
     assert torch.equal(g.view(torch.int32), r.g.view(torch.int32))
     assert s.numel() < 12 * max(r.n_edits, 1) + 64   # below the 12 B key-value float records
+    # version 2: lossless values relative to fhat
+    s2 = ctx.encode_edits(r.edits, xi, 6, fhat=fht)
+    assert s2.cpu().numpy().tobytes() == ec.encode(r.edits_numpy(), xi, 6, fhat=fh)
+    assert s2.numel() <= s.numel()
+    d2, _, _ = ctx.decode_edits(s2, fhat=fht)
+    assert _same_edits(d2, r.edits)
+    assert torch.equal(ctx.apply_edits(fht, xi, d2).view(torch.int32), r.g.view(torch.int32))
 
 
 def test_multi_block_and_errors(dmtz):
@@ -73,5 +80,7 @@ def test_multi_block_and_errors(dmtz):
     far[0, :8] = torch.tensor(list((f.size + 5).to_bytes(8, "little")), dtype=torch.uint8)
     with pytest.raises(dmtz.DmtzError):
         ctx.apply_edits(fht, xi, far)
+    with pytest.raises(dmtz.DmtzError):   # a version-2 stream without fhat
+        ctx.decode_edits(ctx.encode_edits(r.edits, xi, 6, fhat=fht))
     e0 = ctx.encode_edits(r.edits[:0], xi, 6)
     assert e0.numel() == 32 and ctx.decode_edits(e0)[0].shape[0] == 0
