@@ -331,6 +331,12 @@ def main():
                    "hbm_frac": gbs / hbm, "screen_ms_per_step": ds["screen_ms"],
                    "share_of_step": ds["screen_ms"] / ms}
 
+    # the north star's per-iteration HBM fraction: 12 B/voxel (g + cand_f) per sweep over the whole step
+    hbm_iter = {"algorithmic_bytes_per_voxel_sweep": BYTES_PER_ANCHOR[D],
+                "achieved_gbs": BYTES_PER_ANCHOR[D] * N * sweeps / (ms * 1e-3) / 1e9, "peak_gbs": hbm,
+                "frac": BYTES_PER_ANCHOR[D] * N * sweeps / (ms * 1e-3) / 1e9 / hbm,
+                "full_sweep_round_frac": BYTES_PER_ANCHOR[D] * N / (fr_ms / rfull.stats["sweeps"] * 1e-3) / 1e9 / hbm,
+                "note": "the path is ALU-bound (DESIGN.md section 7): 105 SoS compares per anchor per code"}
     # time-to-fixed-point (the second half of BASELINE's metric): the timed default step
     frontier = {"time_to_fixed_point_ms": ms, "rounds": r.stats["rounds"], "sweeps": r.stats["sweeps"],
                 "anchors_classified": r.stats["anchors_swept"], "codes_recomputed": r.stats["anchors_recomputed"],
@@ -486,7 +492,7 @@ def main():
                    "xi": xi, "q_max": 6, "q_cap": 6, "tier": 2, "sweeps_per_step": sweeps, "rounds": st["rounds"],
                    "mode": "default: dirty frontier + exact change skipping (bit-identical to full_sweeps=1)",
                    "l2": "inputs larger than L2 (2 x 537 MB)", "parallelism": "1 GPU"},
-        "roofline": roof, "roofline_screen": roof_screen, "cpu_baseline": cpu, "e2e": e2e, "time_to_fixed_point": frontier,
+        "roofline": roof, "roofline_screen": roof_screen, "hbm_per_iteration": hbm_iter, "cpu_baseline": cpu, "e2e": e2e, "time_to_fixed_point": frontier,
         "full_recompute": full_recompute, "trace": trace, "sloop": sloop, "codec": codec,
         "gpu_launches": st["launches"],
         "clocks": clk.summary(),

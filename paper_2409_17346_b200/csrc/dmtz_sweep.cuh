@@ -331,7 +331,10 @@ __device__ __forceinline__ uint32_t target_del(const TargetTables& T, int t, boo
 // z-1..z+2 (x from the group start - 32), flushed with one atomicOr per
 // non-empty word into the row-padded target bitmap.
 // ---------------------------------------------------------------------------
-constexpr int DECODE_THREADS = 128;
+#ifndef DMTZ_DECODE_THREADS
+#define DMTZ_DECODE_THREADS 128
+#endif
+constexpr int DECODE_THREADS = DMTZ_DECODE_THREADS;
 constexpr int TWW = DG + 2;             // window words per row
 struct DecodeWarpSmem {
   uint2 cf[8 * 32];            // per slot: f codes of u + {0,1}^D
