@@ -73,11 +73,6 @@ __global__ void k_cell_desc_long(const long long* __restrict__ off, const uint8_
   }
 }
 
-__global__ void k_fill_u32(uint32_t* __restrict__ a, int64_t n, uint32_t v) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    a[i] = v;
-}
-
 // ----------------------------------------------------------------------------- pairing comparison
 // The facet of cell (A, t) its code set points at it (down-pair), or -1.
 template <int D>
