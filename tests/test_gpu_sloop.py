@@ -154,3 +154,22 @@ def test_preserve_capacity_and_errors(dmtz):
     bad[3, 4, 5] = f[3, 4, 5] + np.float32(4 * xi)
     r = dmtz.preserve(ft, _cuda(bad), xi, tier=4, raise_on_error=False)
     assert r.status == dmtz.E_BOUND
+
+
+@pytest.mark.parametrize("tier", [4, 5])
+def test_full_size_C2_postconditions(dmtz, tier):
+    """C2 at full size (1800x3600): the tier post-conditions with the GPU's own traces
+     and, for tier 5, the 0-dim persistence pairs by the oracle's union-find."""
+    f, fh, xi, _ = di.config_inputs("C2")
+    ft, fht = _cuda(f), _cuda(fh)
+    r = dmtz.preserve(ft, fht, xi, tier=tier)
+    assert r.status == 0, r.message
+    assert bool((r.g <= fht).all()) and bool(((r.g.double() - ft.double()).abs() <= xi).all())
+    cf, cg = dmtz.compute_gradient(ft), dmtz.compute_gradient(r.g)
+    assert torch.equal(dmtz.critical_mask(cf), dmtz.critical_mask(cg))
+    tf, tg = dmtz.trace_separatrices(cf), dmtz.trace_separatrices(cg)
+    for k in tf:
+        assert torch.equal(tf[k], tg[k]), k
+    if tier == 5:
+        pf, pg = oracle.persistence0(f), oracle.persistence0(r.g.cpu().numpy())
+        assert sorted(map(tuple, pf.tolist())) == sorted(map(tuple, pg.tolist()))
