@@ -346,6 +346,13 @@ dmtz_status dmtz_slab_begin(dmtz_ctx* ctx, const float* f, const float* fhat, co
 dmtz_status dmtz_slab_round(dmtz_ctx* ctx, const float* f, const float* fhat, const dmtz_correct_opts* opts,
                             const dmtz_slab* slab, void* workspace, size_t workspace_bytes, float* g,
                             int64_t round, int64_t* counters, int64_t* kinds, dmtz_stream_t stream);
+/* The same round without any host synchronisation: the 12 counters (counters[4] then
+ * kinds[8]) go to dcounters (device, int64[12]) on the stream, so the caller can
+ * all-reduce them on the device and decide to stop a round later (a round after the
+ * fixed point or after STUCK changes nothing). */
+dmtz_status dmtz_slab_round_async(dmtz_ctx* ctx, const float* f, const float* fhat, const dmtz_correct_opts* opts,
+                                  const dmtz_slab* slab, void* workspace, size_t workspace_bytes, float* g,
+                                  int64_t round, int64_t* dcounters /* device, 12 */, dmtz_stream_t stream);
 /* Halo refresh between rounds: replace the local planes [z_begin, z_end) of g with
  * `planes` (device, (z_end - z_begin) * ny * nx f32, the neighbour's values after
  * round `round`), and record every vertex whose value changed, so that round + 1

@@ -97,6 +97,7 @@ def _load():
     SZ = ctypes.c_size_t
     L.dmtz_slab_begin.argtypes = [P, P, P, ctypes.POINTER(_Opts), P, P, SZ, P, P]
     L.dmtz_slab_round.argtypes = [P, P, P, ctypes.POINTER(_Opts), P, P, SZ, P, i64, P, P, P]
+    L.dmtz_slab_round_async.argtypes = [P, P, P, ctypes.POINTER(_Opts), P, P, SZ, P, i64, P, P]
     L.dmtz_slab_end.argtypes = [P, P, P, SZ, P, P, i64, ctypes.POINTER(i64), ctypes.POINTER(i64), P]
     L.dmtz_slab_halo.argtypes = [P, P, P, SZ, P, P, i64, i64, i64, P]
     L.dmtz_trace_separatrices_range.argtypes = [P, P, ctypes.c_uint32, i64, i64, P, ctypes.c_size_t,
@@ -120,7 +121,7 @@ def _load():
     L.dmtz_last_error.restype = ctypes.c_char_p
     for fn in ("dmtz_ctx_create", "dmtz_compute_gradient", "dmtz_critical_mask", "dmtz_correct",
                "dmtz_trace_separatrices", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end",
-               "dmtz_slab_halo", "dmtz_trace_separatrices_range", "dmtz_preserve",
+               "dmtz_slab_halo", "dmtz_trace_separatrices_range", "dmtz_preserve", "dmtz_slab_round_async",
                "dmtz_encode_edits", "dmtz_decode_edits", "dmtz_apply_edits",
                "dmtz_critical_prf", "dmtz_separatrix_prf"):
         getattr(L, fn).restype = ctypes.c_int
@@ -143,7 +144,8 @@ _lib = _LazyLib()
 EXPORTED = ("dmtz_ctx_create", "dmtz_ctx_destroy", "dmtz_workspace_bytes", "dmtz_compute_gradient",
             "dmtz_critical_mask", "dmtz_correct", "dmtz_trace_separatrices", "dmtz_status_string",
             "dmtz_last_error", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end",
-            "dmtz_slab_halo", "dmtz_trace_separatrices_range", "dmtz_preserve_sep_bytes", "dmtz_preserve",
+            "dmtz_slab_halo", "dmtz_trace_separatrices_range", "dmtz_slab_round_async", "dmtz_preserve_sep_bytes",
+            "dmtz_preserve",
             "dmtz_edit_stream_bound", "dmtz_encode_edits", "dmtz_decode_edits", "dmtz_apply_edits",
             "dmtz_critical_prf", "dmtz_separatrix_prf")
 

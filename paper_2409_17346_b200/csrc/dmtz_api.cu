@@ -921,6 +921,36 @@ dmtz_status dmtz_slab_round(dmtz_ctx* c, const float* f, const float* fhat, cons
   return DMTZ_OK;
 }
 
+dmtz_status dmtz_slab_round_async(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
+                                  const dmtz_slab* sl, void* workspace, size_t wsb, float* g_out, int64_t round,
+                                  int64_t* dcounters, dmtz_stream_t stream) {
+  Layout L;
+  dmtz_status st = slab_check(c, sl, workspace, wsb, &L);
+  if (st) return st;
+  if (!dcounters || round < 1) { set_err("invalid argument"); return DMTZ_E_ARG; }
+  cudaStream_t s = (cudaStream_t)stream;
+  WS<3> W((char*)workspace, L, c->g);
+  int64_t launches = 0;
+  k_set_round<<<1, 32, 0, s>>>(W.ls, (unsigned long long)round);
+  const RowGeom rg = row_geom(c->g);
+  if (round > 1) {
+    CK(cudaMemsetAsync(&W.dc->n_units, 0, 8, s));
+    k_units_from_bits<<<clamp_blocks(rg.units, 256, 4096), 256, 0, s>>>(W.fbits, rg.units, W.units, &W.dc->n_units);
+  }
+  RoundExtra X;
+  X.anchor_z0 = sl->anchor_z0;
+  X.anchor_z1 = sl->anchor_z1;
+  X.decode_marks = W.fbits;
+  X.list_after = false;
+  st = enqueue_round<3>(c, f, fhat, o, W, g_out, W.units, &W.dc->n_units, W.units, &W.dc->n_units, W.fbits,
+                        (int)L.fwords, sl->own_z0, sl->own_z1, sl->own_z0, sl->own_z1, false, ~0ull,
+                        cudaGraphConditionalHandle(), 0, 1, &launches, s, X);
+  if (st) return st;
+  k_counters_out<<<1, 32, 0, s>>>(W.dc, round, (long long*)dcounters);
+  CK(cudaGetLastError());
+  return DMTZ_OK;
+}
+
 dmtz_status dmtz_slab_halo(dmtz_ctx* c, const dmtz_slab* sl, void* workspace, size_t wsb, float* g,
                            const float* planes, int64_t z_begin, int64_t z_end, int64_t round, dmtz_stream_t stream) {
   Layout L;

@@ -140,6 +140,17 @@ __global__ void k_loop_check(Counters* cnt, LoopState* ls, unsigned long long ma
 }
 
 
+// the round counters of a slab round into a caller buffer (device): n_false, n_changed,
+// n_targets, n_internal, kinds[8] (round 1 only, else 0)
+__global__ void k_counters_out(const Counters* __restrict__ cnt, long long round, long long* __restrict__ out) {
+  const int i = threadIdx.x;
+  if (i == 0) out[0] = (long long)cnt->n_false;
+  if (i == 1) out[1] = (long long)cnt->n_changed;
+  if (i == 2) out[2] = (long long)cnt->n_targets;
+  if (i == 3) out[3] = (long long)cnt->n_internal;
+  if (i >= 4 && i < 12) out[i] = round == 1 ? (long long)cnt->kinds[i - 4] : 0ll;
+}
+
 // table accessors (constant-folded when t is a compile-time constant after unrolling)
 #define DMTZ_TAB(D, name) ((D) == 3 ? k3d::name : k2d::name)
 template <int D> __device__ __forceinline__ int t_dim(int t) { return D == 3 ? k3d::DIM[t] : k2d::DIM[t]; }

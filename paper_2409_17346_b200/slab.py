@@ -137,6 +137,16 @@ class CudaSlabEngine:
         self.launches += 5 + (r > 1)  # set_round, [units_from_bits], screen, decode, edit_rows, loop_check
         return np.array(c[:], np.int64), np.array(k[:], np.int64)
 
+    def round_async(self, r: int) -> torch.Tensor:
+        """The round with its 12 counters left on the device (no host synchronisation)."""
+        out = torch.empty(12, dtype=torch.int64, device=self.device)
+        self._check(self._lib.dmtz_slab_round_async(self.ctx._h, self._P(self.f), self._P(self.fhat),
+                                                    ctypes.byref(self.opts), ctypes.byref(self.slab),
+                                                    self._P(self.ctx.workspace), self.ctx.ws_bytes, self._P(self.g),
+                                                    r, self._P(out), self._stream_ptr()))
+        self.launches += 6 + (r > 1)  # set_round, [units_from_bits], screen, decode, edit_rows, loop_check, counters
+        return out
+
     def halo(self, r: int, a: int, b: int, planes):
         """Local planes [a, b) of g <- `planes` (the neighbour's values after round r);
         the library records the changed vertices for round r + 1's screen and frontier."""
@@ -176,38 +186,67 @@ def _stop(round_, tot, max_rounds):
 
 
 def run_distributed(engine, f, fhat, xi, q_max=6, q_cap=None, tier=2, max_rounds=0, group=None):
-    """One rank of the slab C-loop over torch.distributed (call on every rank)."""
+    """One rank of the slab C-loop over torch.distributed (call on every rank).
+
+    Pipelined by one round: round r's kernels, its halo exchange and its counter
+    all-reduce are all enqueued on the device before the host looks at round r - 1's
+    summed counters, so the host's stop decision never idles the GPU.  The one round
+    run past the stop is a no-op: after the fixed point (F empty) or STUCK (no target
+    can move) a round edits nothing, and no round is enqueued past max_rounds."""
     import torch.distributed as dist
     p = engine.p
     engine.begin(f, fhat, xi, q_max, q_cap, tier)
     pairs = halo_pairs(p)
-    dev = engine.g.device
     stats = dict(rounds=0, n_false_round0=0, false_by_kind_round0=[0] * 8)
     status = None
+    pending = None   # (round, host counters, event) of the last enqueued round
     r = 0
     while status is None:
-        r += 1
-        if r > 1 and pairs:
-            ops, bufs = [], []
-            for peer, (sa, sb), (ra, rb) in pairs:
-                buf = torch.empty_like(engine.g[ra:rb])
-                bufs.append((ra, rb, buf))
-                ops.append(dist.P2POp(dist.isend, engine.g[sa:sb].contiguous(), peer, group))
-                ops.append(dist.P2POp(dist.irecv, buf, peer, group))
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
-            for ra, rb, buf in bufs:   # apply + record the changed halo vertices
-                engine.halo(r - 1, ra, rb, buf)
-        c, k = engine.round(r)
-        tot = torch.tensor(np.concatenate([c, k]), dtype=torch.int64, device=dev)
-        dist.all_reduce(tot, group=group)
-        tot = tot.cpu().numpy()
-        if r == 1:
-            stats["n_false_round0"] = int(tot[0])
-            stats["false_by_kind_round0"] = [int(x) for x in tot[4:12]]
-        status = _stop(r, tot, max_rounds)
-        if status != OK:
-            stats["rounds"] = r
+        if not (max_rounds and r >= max_rounds):
+            r += 1
+            if r > 1 and pairs:
+                ops, bufs = [], []
+                for peer, (sa, sb), (ra, rb) in pairs:
+                    buf = torch.empty_like(engine.g[ra:rb])
+                    bufs.append((ra, rb, buf))
+                    ops.append(dist.P2POp(dist.isend, engine.g[sa:sb].contiguous(), peer, group))
+                    ops.append(dist.P2POp(dist.irecv, buf, peer, group))
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
+                for ra, rb, buf in bufs:   # apply + record the changed halo vertices
+                    engine.halo(r - 1, ra, rb, buf)
+            if hasattr(engine, "round_async"):
+                tot = engine.round_async(r)
+            else:
+                c, k = engine.round(r)
+                tot = torch.tensor(np.concatenate([c, k]), dtype=torch.int64, device=engine.g.device)
+            dist.all_reduce(tot, group=group)
+            if tot.is_cuda:
+                host = torch.empty(12, dtype=torch.int64).pin_memory()
+                host.copy_(tot, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record()
+            else:
+                host, ev = tot, None
+            nxt = (r, host, ev)
+        else:
+            nxt = None          # max_rounds reached: only the decision on the last round is left
+        if pending is not None:
+            pr, host_p, ev_p = pending
+            if ev_p is not None:
+                ev_p.synchronize()
+            t = host_p.numpy()
+            if pr == 1:
+                stats["n_false_round0"] = int(t[0])
+                stats["false_by_kind_round0"] = [int(x) for x in t[4:12]]
+            status = _stop(pr, t, max_rounds)
+            if status != OK:     # rounds that found false cells
+                stats["rounds"] = pr
+        pending = nxt
+        if pending is None and status is None:   # cannot happen: the cap round decides
+            status = E_ITER_CAP
+    if pending is not None and pending[2] is not None:
+        pending[2].synchronize()
     edits, nl = engine.end()
     stats["status"] = status
     return edits, nl, stats

@@ -44,8 +44,8 @@ def _case(shape, seed):
     return di.random_case(shape, seed, eps=0.05, perturb="noise", family="lognormal")
 
 
-def _check_against_oracle(f, fh, xi, outs, stats):
-    ref = oracle.correct(f, fh, xi)
+def _check_against_oracle(f, fh, xi, outs, stats, max_rounds=0):
+    ref = oracle.correct(f, fh, xi, max_rounds=max_rounds)
     assert stats["status"] == ref["status"]
     assert stats["rounds"] == ref["stats"]["rounds"]
     assert stats["n_false_round0"] == ref["stats"]["n_false_round0"]
@@ -68,14 +68,14 @@ def test_slab_emulated_oracle_engine(shape, world, seed):
     _check_against_oracle(f, fh, xi, outs, stats)
 
 
-def _gloo_worker(rank, world, port, shape, seed, outdir):
+def _gloo_worker(rank, world, port, shape, seed, outdir, max_rounds=0):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     f, fh, xi = _case(shape, seed)
     p = slab.plan(shape[0], world, rank)
     lf, lfh = slab.local_inputs(f, fh, p)
     eng = OracleSlabEngine(p, shape[1], shape[2])
-    edits, _, stats = slab.run_distributed(eng, torch.from_numpy(lf), torch.from_numpy(lfh), xi)
+    edits, _, stats = slab.run_distributed(eng, torch.from_numpy(lf), torch.from_numpy(lfh), xi, max_rounds=max_rounds)
     np.save(os.path.join(outdir, f"edits{rank}.npy"), edits)
     np.save(os.path.join(outdir, f"stats{rank}.npy"), np.array([stats["status"], stats["rounds"],
                                                                  stats["n_false_round0"]] +
@@ -83,18 +83,22 @@ def _gloo_worker(rank, world, port, shape, seed, outdir):
     dist.destroy_process_group()
 
 
-def test_slab_gloo_world2():
+@pytest.mark.parametrize("max_rounds", [0, 3])
+def test_slab_gloo_world2(max_rounds):
+    """The pipelined driver (stop decision one round behind) over gloo, world size 2;
+    max_rounds = 3 ends on ITER_CAP without running a round past the cap."""
     shape, seed, world = (14, 7, 8), 5, 2
     with tempfile.TemporaryDirectory() as d:
-        port = 29500 + (os.getpid() % 1000)
-        mp.spawn(_gloo_worker, args=(world, port, shape, seed, d), nprocs=world, join=True)
+        port = 29500 + (os.getpid() % 1000) + max_rounds
+        mp.spawn(_gloo_worker, args=(world, port, shape, seed, d, max_rounds), nprocs=world, join=True)
         outs = [(np.load(os.path.join(d, f"edits{r}.npy")), 0) for r in range(world)]
         st = [np.load(os.path.join(d, f"stats{r}.npy")) for r in range(world)]
     assert all(np.array_equal(st[0], s) for s in st)   # every rank took the same decisions
     stats = dict(status=int(st[0][0]), rounds=int(st[0][1]), n_false_round0=int(st[0][2]),
                  false_by_kind_round0=[int(x) for x in st[0][3:11]])
     f, fh, xi = _case(shape, seed)
-    _check_against_oracle(f, fh, xi, outs, stats)
+    _check_against_oracle(f, fh, xi, outs, stats, max_rounds)
+    assert stats["status"] == (6 if max_rounds else 0)
 
 
 @pytest.mark.gpu
