@@ -223,7 +223,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-trace", action="store_true")
     ap.add_argument("--slab", action="store_true", help="run the multi-GPU slab path even with one rank")
-    ap.add_argument("--sloop-config", default="C4:4,5;C2:3,4,5",
+    ap.add_argument("--sloop-config", default="C4:4,5,3;C2:3,4,5",
                     help="configs:tiers of the tier-3/4/5 workflow lines, e.g. 'C4:4,5;C2:3,4,5' ('none' skips)")
     args = ap.parse_args()
     if args.impl == "dmtz":

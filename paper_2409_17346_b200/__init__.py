@@ -279,7 +279,7 @@ class Context:
                  raise_on_error: bool = True):
         """The alternating C-/S-loop workflow for tiers 1-4.  The
         separatrix CSR of f is sized with a trace of f's gradient (sep_caps = (branches,
-        cells) overrides; tier 3 also traces g and gets 50 % headroom on the cells)."""
+        cells) overrides; tier 3 also traces its candidate branches in g and gets 12.5 % headroom on the cells)."""
         _need_cuda(f, fhat)
         for t in (f, fhat):
             assert t.dtype == torch.float32 and tuple(t.shape) == self.shape and t.is_contiguous()
@@ -296,7 +296,7 @@ class Context:
                 sz = self.trace_sizes(self.compute_gradient(f), stream=stream)
                 cb, cc = sz["n_branches"], sz["n_cells"]
                 if tier == 3:
-                    cc = cc + cc // 2 + 1024
+                    cc = cc + cc // 8 + 1024
             else:
                 cb, cc = (int(x) for x in sep_caps)
             nbytes = int(_lib.dmtz_preserve_sep_bytes(self._h, ctypes.byref(opts), cb, cc))

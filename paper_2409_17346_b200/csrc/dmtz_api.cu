@@ -484,7 +484,7 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
 // separatrices + per-branch end flags.
 struct SepLayout {
   size_t codes, save, off, cells, origin, term, kind, first, cb, canc, mbits, sdirty, sdil, goff, gcells, gorigin, gterm, gkind,
-      flag, total;
+      flag, cidx, cmap, cbsum, total;
 };
 
 SepLayout sep_layout(const dmtz_ctx* c, int tier, int64_t cap_b, int64_t cap_c) {
@@ -512,6 +512,9 @@ SepLayout sep_layout(const dmtz_ctx* c, int tier, int64_t cap_b, int64_t cap_c) 
     S.gterm = o; o += align_up((size_t)cap_b * 8 + 8);
     S.gkind = o; o += align_up((size_t)cap_b + 8);
     S.flag = o; o += align_up((size_t)cap_b + 8);
+    S.cidx = o; o += align_up(((size_t)cap_b + 1) * 8);        // candidate flags -> indices (scan)
+    S.cmap = o; o += align_up((size_t)cap_b * 4 + 8);          // candidate -> branch of f
+    S.cbsum = o; o += align_up(((size_t)cap_b / 8192 + 4) * 8);
   }
   S.total = o;
   return S;
@@ -521,8 +524,10 @@ SepLayout sep_layout(const dmtz_ctx* c, int tier, int64_t cap_b, int64_t cap_c) 
 template <int D>
 dmtz_status trace_into(dmtz_ctx* c, char* ws, const Layout& L, const void* codes, char* sw, size_t off, size_t cells,
                        size_t origin, size_t term, size_t kind, int64_t cap_b, int64_t cap_c, int64_t* nb,
-                       int64_t* nc, cudaStream_t s) {
+                       int64_t* nc, cudaStream_t s, const int64_t* given_nbk = nullptr) {
   TraceArgs a;
+  if (given_nbk)
+    for (int k = 0; k < 3; k++) a.given_nbk[k] = given_nbk[k];
   a.g = c->g;
   a.codes = codes;
   a.kinds = 7u;
@@ -634,35 +639,6 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
     const unsigned long long r = hls->round;
     CK(cudaEventRecord(e0, s));
     const uint8_t* flag = nullptr;
-    if (o->tier == 3) {
-      // trace g (its codes are current) with the loop's workspace, then restore the loop state
-      CK(cudaMemcpyAsync(sw + S.codes, W.cand_g, (size_t)g.N * cs, cudaMemcpyDeviceToDevice, s));
-      CK(cudaMemcpyAsync(sw + S.save, W.lb, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
-      CK(cudaMemcpyAsync(sw + S.save + (size_t)g.N * 4, W.state, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
-      int64_t gnb = 0, gnc = 0;
-      status = trace_into<D>(c, ws, L, sw + S.codes, sw, S.goff, S.gcells, S.gorigin, S.gterm, S.gkind, cap_b, cap_c,
-                             &gnb, &gnc, s);
-      if (status == DMTZ_OK && gnb != nb) { set_err("tier 3: %lld branches in g, %lld in f", (long long)gnb, (long long)nb); status = DMTZ_E_INTERNAL; }
-      if (status != DMTZ_OK) { st->status = status; return status; }
-      k_t3_flags<<<clamp_blocks(nb * 32, T3_WARPS * 32), T3_WARPS * 32, 0, s>>>(
-          off, cells, (const uint64_t*)(sw + S.term), kind, (const long long*)(sw + S.goff),
-          (const uint64_t*)(sw + S.gcells), (const uint64_t*)(sw + S.gterm), nb, (uint8_t*)(sw + S.flag));
-      CK(cudaMemcpyAsync(W.lb, sw + S.save, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
-      CK(cudaMemcpyAsync(W.state, sw + S.save + (size_t)g.N * 4, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
-      CK(cudaMemcpyAsync(W.cand_g, sw + S.codes, (size_t)g.N * cs, cudaMemcpyDeviceToDevice, s));
-      launch_codes<D>(g, f, W.cand_f, 0, g.nz, s);
-      k_critmask<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(W.cand_f, W.crit_f, g);
-      k_lowpos<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(f, W.lowpos, g);
-      CK(cudaMemsetAsync(W.tbits, 0, nwords * 4, s));
-      CK(cudaMemsetAsync(W.fmark, 0, W.rowbit_bytes, s));
-      CK(cudaMemsetAsync(W.vchg, 0, 2 * W.rowbit_bytes, s));
-      CK(cudaMemsetAsync(W.fbits, 0, (size_t)L.fwords * 4, s));
-      // the trace cleared the counters, the full-sweep unit count among them
-      if (!frontier_mode) CK(units_range(rg, 0, g.nz, W.units, &W.dc->n_units, s));
-      CK(cudaGetLastError());
-      st->launches += 5;
-      flag = (const uint8_t*)(sw + S.flag);
-    }
     CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));
     CK(cudaMemsetAsync(&W.dc->pad[3], 0, 5 * 8, s));
     const int full = ss->s_rounds == 0 ? 1 : 0;
@@ -674,6 +650,84 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
       const int64_t nblk = ((nc + 31) / 32 + 8 * TM_U - 1) / (8 * TM_U);  // 8 warps x TM_U words per block
       k_tm_cells<D><<<(unsigned)nblk, 256, 0, s>>>(cells, nc, desc, canc, W.cand_f, W.cand_g, W.crit_f, g, sdil,
                                                    full, mbits, W.dc);
+      st->launches += 1;
+    }
+    if (o->tier == 3) {
+      // the candidates (branches with a troublemaker) are traced in g; the others end as in f
+      long long* cidx = (long long*)(sw + S.cidx);
+      uint32_t* cmap = (uint32_t*)(sw + S.cmap);
+      k_t3_cand<D><<<clamp_blocks(nb + 1, 256, 148 * 64), 256, 0, s>>>(cells, off, kind, origin, nb, W.cand_f,
+                                                                       W.cand_g, W.crit_f, g, mbits, cidx, W.dc);
+      CK(cudaGetLastError());
+      CK(scan_i64(cidx, nb + 1, (unsigned long long*)(sw + S.cbsum), &W.dc->pad[0], &hc->pad[0], s));
+      const int64_t ncand = (int64_t)hc->pad[0];
+      CK(cudaMemcpyAsync(hc, W.dc, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      const int64_t nkc[3] = {(int64_t)hc->pad[4], (int64_t)hc->pad[5], (int64_t)hc->pad[6]};
+      ss->cells_checked += (int64_t)hc->pad[7];
+      CK(cudaMemsetAsync(sw + S.flag, 0, (size_t)nb, s));
+      st->launches += 4;
+      if (ncand > 0) {
+        k_t3_fill<D><<<clamp_blocks(nb, 256, 148 * 64), 256, 0, s>>>(
+            cells, off, kind, origin, nb, cidx, g, (uint64_t*)(sw + S.gorigin), (uint8_t*)(sw + S.gkind),
+            (uint64_t*)(sw + S.gterm), cmap);
+        // trace g with the loop's workspace (its codes are current), then restore the loop state
+        CK(cudaMemcpyAsync(sw + S.codes, W.cand_g, (size_t)g.N * cs, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(sw + S.save, W.lb, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(sw + S.save + (size_t)g.N * 4, W.state, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
+        // trace the candidates in chunks whose g-paths fit the CSR (halving a chunk that does not)
+        int64_t c0 = 0, chunk = ncand;
+        while (c0 < ncand) {
+          const int64_t c1 = c0 + chunk < ncand ? c0 + chunk : ncand;
+          int64_t knb[3];
+          int64_t kb = 0;
+          for (int k = 0; k < 3; k++) {   // candidates are grouped DESC, ASC, CONN
+            const int64_t lo = kb > c0 ? kb : c0, hi = kb + nkc[k] < c1 ? kb + nkc[k] : c1;
+            knb[k] = hi > lo ? hi - lo : 0;
+            kb += nkc[k];
+          }
+          int64_t gnb = 0, gnc = 0;
+          status = trace_into<D>(c, ws, L, sw + S.codes, sw, S.goff, S.gcells, S.gorigin + 8 * c0, S.gterm + 8 * c0,
+                                 S.gkind + c0, c1 - c0, cap_c, &gnb, &gnc, s, knb);
+          if (status == DMTZ_E_CAPACITY && c1 - c0 > 1 && gnb == c1 - c0) {
+            // k_t3_fill's j inputs of this chunk were consumed: refill them, retry half
+            k_t3_fill<D><<<clamp_blocks(nb, 256, 148 * 64), 256, 0, s>>>(
+                cells, off, kind, origin, nb, cidx, g, (uint64_t*)(sw + S.gorigin), (uint8_t*)(sw + S.gkind),
+                (uint64_t*)(sw + S.gterm), cmap);
+            chunk = (c1 - c0 + 1) / 2;
+            status = DMTZ_OK;
+            continue;
+          }
+          if (status == DMTZ_OK && gnb != c1 - c0) {
+            set_err("tier 3: %lld candidates traced, %lld given", (long long)gnb, (long long)(c1 - c0));
+            status = DMTZ_E_INTERNAL;
+          }
+          if (status != DMTZ_OK) { st->status = status; return status; }
+          k_t3_flags_cand<<<clamp_blocks((c1 - c0) * 32, T3_WARPS * 32), T3_WARPS * 32, 0, s>>>(
+              off, cells, (const uint64_t*)(sw + S.term), kind, (const long long*)(sw + S.goff),
+              (const uint64_t*)(sw + S.gcells), (const uint64_t*)(sw + S.gterm) + c0, cmap + c0, c1 - c0,
+              (uint8_t*)(sw + S.flag));
+          CK(cudaGetLastError());
+          c0 = c1;
+        }
+        CK(cudaMemcpyAsync(W.lb, sw + S.save, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(W.state, sw + S.save + (size_t)g.N * 4, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(W.cand_g, sw + S.codes, (size_t)g.N * cs, cudaMemcpyDeviceToDevice, s));
+        launch_codes<D>(g, f, W.cand_f, 0, g.nz, s);
+        k_critmask<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(W.cand_f, W.crit_f, g);
+        k_lowpos<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(f, W.lowpos, g);
+        CK(cudaMemsetAsync(W.tbits, 0, nwords * 4, s));
+        CK(cudaMemsetAsync(W.fmark, 0, W.rowbit_bytes, s));
+        CK(cudaMemsetAsync(W.vchg, 0, 2 * W.rowbit_bytes, s));
+        CK(cudaMemsetAsync(W.fbits, 0, (size_t)L.fwords * 4, s));
+        // the trace cleared the counters, the full-sweep unit count among them
+        if (!frontier_mode) CK(units_range(rg, 0, g.nz, W.units, &W.dc->n_units, s));
+        CK(cudaGetLastError());
+        st->launches += 6;
+      }
+      CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));
+      CK(cudaMemsetAsync(&W.dc->pad[3], 0, 5 * 8, s));
+      flag = (const uint8_t*)(sw + S.flag);
     }
     k_tm_targets<D><<<clamp_blocks(nb, 256, 148 * 64), 256, 0, s>>>(cells, off, kind, origin, nb, W.cand_f, W.cand_g,
                                                                     W.crit_f, g, rg, mbits, flag, sdil, full,

@@ -425,3 +425,130 @@ __global__ void k_t5_clamp(const uint32_t* __restrict__ crit_f, const float* __r
 }
 
 }  // namespace dmtz
+
+namespace dmtz {
+
+// ----------------------------------------------------------------------------- tier 3, candidates
+// A branch whose f-path shows no mismatch (no troublemaker) follows the same path in g
+// and ends the same; only the others (the candidates) are traced in g.
+// cidx[b] = 1 for a candidate (then exclusive-scanned into its index); cnt->pad[4 + kind
+// index] counts them per kind.
+template <int D>
+__global__ void k_t3_cand(const uint64_t* __restrict__ cells, const long long* __restrict__ off,
+                          const uint8_t* __restrict__ kind, const uint64_t* __restrict__ origin, int64_t nb,
+                          const void* __restrict__ cf, const void* __restrict__ cg, const uint32_t* __restrict__ crit_f,
+                          Grid g, const uint32_t* __restrict__ mbits, long long* __restrict__ cidx,
+                          Counters* __restrict__ cnt) {
+  unsigned long long nk[3] = {0, 0, 0};
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += (int64_t)gridDim.x * blockDim.x) {
+    if (b == nb) { cidx[nb] = 0; continue; }
+    const int k = kind[b];
+    bool c = first_bit(mbits, off[b], off[b + 1]) >= 0;
+    if (!c && k == 4) {
+      int64_t B; int bt; int j;
+      id_cell_fast<D>(origin[b], B, bt);
+      c = conn_tri_differs<D>(cf, cg, crit_f, g, B, bt, &j);
+    }
+    cidx[b] = c ? 1 : 0;
+    if (c) nk[k == 1 ? 0 : k == 2 ? 1 : 2]++;
+  }
+  warp_add(&cnt->pad[4], nk[0]);
+  warp_add(&cnt->pad[5], nk[1]);
+  warp_add(&cnt->pad[6], nk[2]);
+}
+
+// candidate i = cidx[b] (after the scan): its origin, kind, branch index j (DESC: which
+// endpoint; ASC: the raw cofacet slot of its first cell; CONN: 0) and cmap[i] = b
+template <int D>
+__global__ void k_t3_fill(const uint64_t* __restrict__ cells, const long long* __restrict__ off,
+                          const uint8_t* __restrict__ kind, const uint64_t* __restrict__ origin, int64_t nb,
+                          const long long* __restrict__ cidx, Grid g, uint64_t* __restrict__ corigin,
+                          uint8_t* __restrict__ ckind, uint64_t* __restrict__ cj, uint32_t* __restrict__ cmap) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const long long i = cidx[b];
+    if (cidx[b + 1] == i) continue;  // not a candidate
+    const int k = kind[b];
+    const uint64_t o = origin[b];
+    uint64_t j = 0;
+    if (k == 1) {
+      j = (b > 0 && origin[b - 1] == o && kind[b - 1] == 1) ? 1 : 0;
+    } else if (k == 2) {
+      int64_t A; int t;
+      id_cell_fast<D>(o, A, t);
+      const uint64_t t0 = cells[off[b]];
+      for (int sl = 0; sl < t_nlink<D>(t); sl++)
+        if (cell_id<D>(cof_anchor<D>(g, A, t, sl), t_cof_type<D>(t, sl)) == t0) { j = (uint64_t)sl; break; }
+    }
+    corigin[i] = o;
+    ckind[i] = (uint8_t)k;
+    cj[i] = j;
+    cmap[i] = (uint32_t)b;
+  }
+}
+
+// flag[b] for the candidates: like k_t3_flags, candidate i of the g-CSR against branch
+// cmap[i] of the f-CSR (the other branches keep flag 0)
+__global__ void __launch_bounds__(T3_WARPS * 32)
+k_t3_flags_cand(const long long* __restrict__ foff, const uint64_t* __restrict__ fcells,
+                const uint64_t* __restrict__ fterm, const uint8_t* __restrict__ kind,
+                const long long* __restrict__ goff, const uint64_t* __restrict__ gcells,
+                const uint64_t* __restrict__ gterm, const uint32_t* __restrict__ cmap, int64_t nc,
+                uint8_t* __restrict__ flag) {
+  __shared__ unsigned long long sl[T3_WARPS][2][T3_SMEM];
+  __shared__ int sn[T3_WARPS][2];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nc;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t b = cmap[i];
+    if (kind[b] != 4) {
+      if (lane == 0) flag[b] = fterm[b] != gterm[i];
+      continue;
+    }
+    const int64_t s0[2] = {foff[b], goff[i]}, s1[2] = {foff[b + 1], goff[i + 1]};
+    const uint64_t* cs[2] = {fcells, gcells};
+    if (lane < 2) sn[wib][lane] = 0;
+    __syncwarp();
+    int cnt[2];
+    for (int h = 0; h < 2; h++) {
+      int c = 0;
+      for (int64_t q = s0[h] + lane; q < s1[h]; q += 32) {
+        const uint64_t id = cs[h][q];
+        if ((id >> 56) != 1) continue;
+        c++;
+        const int p = atomicAdd(&sn[wib][h], 1);
+        if (p < T3_SMEM) sl[wib][h][p] = id;
+      }
+      cnt[h] = __reduce_add_sync(0xffffffffu, c);
+    }
+    __syncwarp();
+    bool differ = cnt[0] != cnt[1];
+    if (!differ && cnt[0] > 0) {
+      bool bad = false;
+      if (cnt[0] <= T3_SMEM) {
+        for (int q = lane; q < cnt[0]; q += 32) {
+          const unsigned long long x = sl[wib][0][q];
+          int a = 0, c = 0;
+          for (int r = 0; r < cnt[0]; r++) {
+            a += sl[wib][0][r] == x;
+            c += sl[wib][1][r] == x;
+          }
+          bad |= a != c;
+        }
+      } else {
+        for (int64_t q = s0[0] + lane; q < s1[0]; q += 32) {
+          const uint64_t x = fcells[q];
+          if ((x >> 56) != 1) continue;
+          int64_t a = 0, c = 0;
+          for (int64_t r = s0[0]; r < s1[0]; r++) a += fcells[r] == x;
+          for (int64_t r = s0[1]; r < s1[1]; r++) c += gcells[r] == x;
+          bad |= a != c;
+        }
+      }
+      differ = __any_sync(0xffffffffu, bad);
+    }
+    if (lane == 0) flag[b] = differ ? 1 : 0;
+    __syncwarp();
+  }
+}
+
+}  // namespace dmtz

@@ -43,6 +43,10 @@ struct TraceArgs {
   uint8_t* out_kind;
   int64_t cap_b, cap_c;
   int64_t a_lo = 0, a_hi = INT64_MAX;   // origin anchors traced: [a_lo, a_hi)
+  // given branches (given_nbk[0] >= 0): the caller filled out_origin / out_kind /
+  // out_terminal (= the branch index j) for given_nbk[k] branches of each kind, grouped
+  // DESC, ASC, CONN; only those are traced
+  int64_t given_nbk[3] = {-1, -1, -1};
   int verbose = 0;
   int64_t n_branches = 0, n_cells = 0, n_internal = 0;
 };
@@ -1059,18 +1063,23 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   if ((3 * ntiles + 8) * 8 > (int64_t)A.pre_bytes) return cudaErrorMemoryAllocation;
   unsigned long long* tsum[3] = {(unsigned long long*)pre, (unsigned long long*)pre + ntiles,
                                  (unsigned long long*)pre + 2 * ntiles};
-  for (int ki = 0; ki < 3; ki++) {
-    const int kind = kinds_list[ki];
-    if (!(A.kinds & (uint32_t)kind) || (kind == 4 && D != 3)) continue;
-    k_branch_tiles<D><<<(unsigned)ntiles, BT_THREADS, 0, s>>>(A.crit, g, kind, A.a_lo, A.a_hi, tsum[ki]);
-    k_scan_top<<<1, 1024, 0, s>>>(tsum[ki], ntiles, total + ki);
-    TCK(cudaGetLastError());
-  }
-  TCK(cudaMemcpyAsync(&hc->pad[0], total, 3 * 8, cudaMemcpyDeviceToHost, s));
-  TCK(cudaStreamSynchronize(s));
-  for (int ki = 0; ki < 3; ki++) {
-    const int kind = kinds_list[ki];
-    nbk[ki] = (!(A.kinds & (uint32_t)kind) || (kind == 4 && D != 3)) ? 0 : (int64_t)hc->pad[ki];
+  const bool given = A.given_nbk[0] >= 0;
+  if (given) {
+    for (int ki = 0; ki < 3; ki++) nbk[ki] = A.given_nbk[ki];
+  } else {
+    for (int ki = 0; ki < 3; ki++) {
+      const int kind = kinds_list[ki];
+      if (!(A.kinds & (uint32_t)kind) || (kind == 4 && D != 3)) continue;
+      k_branch_tiles<D><<<(unsigned)ntiles, BT_THREADS, 0, s>>>(A.crit, g, kind, A.a_lo, A.a_hi, tsum[ki]);
+      k_scan_top<<<1, 1024, 0, s>>>(tsum[ki], ntiles, total + ki);
+      TCK(cudaGetLastError());
+    }
+    TCK(cudaMemcpyAsync(&hc->pad[0], total, 3 * 8, cudaMemcpyDeviceToHost, s));
+    TCK(cudaStreamSynchronize(s));
+    for (int ki = 0; ki < 3; ki++) {
+      const int kind = kinds_list[ki];
+      nbk[ki] = (!(A.kinds & (uint32_t)kind) || (kind == 4 && D != 3)) ? 0 : (int64_t)hc->pad[ki];
+    }
   }
   const int64_t nb = nbk[0] + nbk[1] + nbk[2];
   A.n_branches = nb;
@@ -1081,7 +1090,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
     return cudaSuccess;
   }
   int64_t base = 0;
-  for (int ki = 0; ki < 3; ki++) {
+  for (int ki = 0; ki < 3 && !given; ki++) {
     const int kind = kinds_list[ki];
     if (!nbk[ki]) continue;
     k_branch_tiles_emit<D><<<(unsigned)ntiles, BT_THREADS, 0, s>>>(A.crit, g, kind, A.a_lo, A.a_hi, tsum[ki], base,
