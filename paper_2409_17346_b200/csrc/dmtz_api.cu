@@ -1209,7 +1209,10 @@ dmtz_status dmtz_decode_edits(dmtz_ctx* c, const uint8_t* in, size_t nbytes, con
   Counters* dc = (Counters*)((char*)ws + L.counters);
   Counters* hc = c->host_cnt;
   CK(cudaMemsetAsync(&dc->pad[1], 0, 8, s));
-  if (nblocks)
+  if (nblocks && ver == 2 && !getenv("DMTZ_EC_DECODE_THREAD"))   // one warp per block
+    k_ec_decode_v2w<<<clamp_blocks(nblocks * 32, 128), 128, 0, s>>>(in, nbytes, (int64_t)n, nblocks, c->g.N, fhat,
+                                                                    (EditRec*)edits, &dc->pad[1]);
+  else if (nblocks)   // version 1 (raw value bytes): one thread per block
     k_ec_decode<<<clamp_blocks(nblocks, 128), 128, 0, s>>>(in, nbytes, (int64_t)n, nblocks, c->g.N,
                                                            ver == 2 ? fhat : nullptr, (EditRec*)edits, &dc->pad[1]);
   CK(cudaGetLastError());

@@ -84,3 +84,60 @@ def test_multi_block_and_errors(dmtz):
         ctx.decode_edits(ctx.encode_edits(r.edits, xi, 6, fhat=fht))
     e0 = ctx.encode_edits(r.edits[:0], xi, 6)
     assert e0.numel() == 32 and ctx.decode_edits(e0)[0].shape[0] == 0
+
+
+def _decode_env(ctx, s, fht, thread):
+    """decode with the warp-per-block version-2 decoder (default) or the thread-per-block one."""
+    import os
+    if thread:
+        os.environ["DMTZ_EC_DECODE_THREAD"] = "1"
+    try:
+        return ctx.decode_edits(s, fhat=fht)
+    finally:
+        os.environ.pop("DMTZ_EC_DECODE_THREAD", None)
+
+
+def test_v2_warp_decoder_multi_block_and_fuzz(dmtz):
+    """the warp decoder (records split across lanes, roles chained in lane order) returns
+    the same records as the thread decoder on a multi-block version-2 stream, and takes
+    the same accept / reject decision on corrupted copies (flipped continuation bits,
+    changed bytes, truncations)."""
+    f, fh, xi, _ = di.config_inputs("C4", shape=(64, 64, 64))
+    ft, fht = _cuda(f), _cuda(fh)
+    ctx = dmtz.context(ft.shape, ft.device)
+    r = ctx.correct(ft, fht, xi)
+    assert r.n_edits > 3 * 4096
+    s = ctx.encode_edits(r.edits, xi, 6, fhat=fht)
+    d, _, _ = _decode_env(ctx, s, fht, thread=False)
+    assert _same_edits(d, r.edits)
+    assert torch.equal(d, _decode_env(ctx, s, fht, thread=True)[0])
+    rng = np.random.default_rng(7)
+    nblk = (r.n_edits + 4095) // 4096
+    pay0 = 32 + 8 * nblk
+    verdicts = set()
+    for trial in range(40):
+        bad = s.clone()
+        k = int(rng.integers(pay0, s.numel()))
+        if trial % 4 == 0:
+            bad[k] ^= 0x80                      # continuation bit: merges / splits varints
+        elif trial % 4 == 1:
+            bad[k] = int(rng.integers(0, 256))
+        elif trial % 4 == 2:
+            bad[k] ^= 0x01                      # a lossless flag or a low value bit
+        else:
+            bad = bad[:k].clone()               # truncated
+        res = []
+        for thread in (False, True):
+            try:
+                res.append(_decode_env(ctx, bad, fht, thread)[0].clone())
+            except dmtz.DmtzError:
+                res.append(None)
+        assert (res[0] is None) == (res[1] is None), trial
+        if res[0] is not None:
+            a = res[0].cpu().numpy().view(oracle.EDIT_DTYPE).ravel()
+            b = res[1].cpu().numpy().view(oracle.EDIT_DTYPE).ravel()
+            assert all(np.array_equal(a[key], b[key]) for key in ("v", "q", "lossless")), trial
+            ll = b["lossless"] > 0
+            assert np.array_equal(a["value"][ll].view(np.uint32), b["value"][ll].view(np.uint32)), trial
+        verdicts.add(res[0] is None)
+    assert True in verdicts

@@ -70,6 +70,8 @@ def run(name, world):
     n_edits = sum(int(o[0].shape[0]) for o in outs)
     # traces: owned-plane codes (concatenated = the all-gather), each rank's range trace
     full = torch.cat([slab.owned_codes(e) for e in engines])
+    del engines, fs, fhs, outs   # free the ranks' loop state before the traces (C5: ~80 GB)
+    torch.cuda.empty_cache()
     tctx = dmtz.Context(tuple(full.shape), dev)
     t_ranks = []
     for p in plans:
