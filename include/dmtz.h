@@ -164,6 +164,22 @@ dmtz_status dmtz_correct(dmtz_ctx* ctx, const float* f, const float* fhat,
                          int64_t* n_edits /* host */, dmtz_stats* stats /* host */,
                          dmtz_stream_t stream);
 
+/* dmtz_correct from HOST buffers (the end-to-end call): copies f_host and fhat_host
+ * (float[N]; pinned for full PCIe/C2C bandwidth, pageable works) into the caller's
+ * device buffers f_dev / fhat_dev, runs dmtz_correct on the device buffers, and
+ * copies g (float[N]) into g_host and the n = min(*n_edits, edits_capacity) edits
+ * into edits_host (dmtz_edit[edits_capacity]), all on `stream`; returns after the
+ * copies completed.  g_dev / edits_dev are device outputs as in dmtz_correct.
+ * g_host or edits_host may be NULL (that result is not copied back).  Same
+ * statuses as dmtz_correct; the host outputs are written when it returns
+ * DMTZ_OK, DMTZ_E_STUCK, DMTZ_E_ITER_CAP or DMTZ_E_CAPACITY. */
+dmtz_status dmtz_correct_host(dmtz_ctx* ctx, const float* f_host, const float* fhat_host,
+                              const dmtz_correct_opts* opts, void* workspace, size_t workspace_bytes,
+                              float* f_dev, float* fhat_dev, float* g_dev, dmtz_edit* edits_dev,
+                              int64_t edits_capacity, float* g_host, dmtz_edit* edits_host,
+                              int64_t* n_edits /* host */, dmtz_stats* stats /* host */,
+                              dmtz_stream_t stream);
+
 /* Separatrix traces of a gradient (P:82 gradient paths):
  *   DESC: from each endpoint (ascending index) of each critical edge, vertex ->
  *         paired edge -> its other vertex, until a critical vertex (minimum).

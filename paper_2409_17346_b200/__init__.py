@@ -92,6 +92,8 @@ def _load():
     L.dmtz_critical_mask.argtypes = [P, P, P, P]
     L.dmtz_correct.argtypes = [P, P, P, ctypes.POINTER(_Opts), P, ctypes.c_size_t, P, P, i64,
                                ctypes.POINTER(i64), ctypes.POINTER(_Stats), P]
+    L.dmtz_correct_host.argtypes = [P, P, P, ctypes.POINTER(_Opts), P, ctypes.c_size_t, P, P, P, P, i64, P, P,
+                                    ctypes.POINTER(i64), ctypes.POINTER(_Stats), P]
     L.dmtz_trace_separatrices.argtypes = [P, P, ctypes.c_uint32, P, ctypes.c_size_t, ctypes.POINTER(_Seps),
                                           i64, i64, ctypes.POINTER(i64), ctypes.POINTER(i64), P]
     SZ = ctypes.c_size_t
@@ -119,7 +121,7 @@ def _load():
     L.dmtz_status_string.argtypes = [i32]
     L.dmtz_status_string.restype = ctypes.c_char_p
     L.dmtz_last_error.restype = ctypes.c_char_p
-    for fn in ("dmtz_ctx_create", "dmtz_compute_gradient", "dmtz_critical_mask", "dmtz_correct",
+    for fn in ("dmtz_ctx_create", "dmtz_compute_gradient", "dmtz_critical_mask", "dmtz_correct", "dmtz_correct_host",
                "dmtz_trace_separatrices", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end",
                "dmtz_slab_halo", "dmtz_trace_separatrices_range", "dmtz_preserve", "dmtz_slab_round_async",
                "dmtz_encode_edits", "dmtz_decode_edits", "dmtz_apply_edits",
@@ -142,7 +144,7 @@ class _LazyLib:
 
 _lib = _LazyLib()
 EXPORTED = ("dmtz_ctx_create", "dmtz_ctx_destroy", "dmtz_workspace_bytes", "dmtz_compute_gradient",
-            "dmtz_critical_mask", "dmtz_correct", "dmtz_trace_separatrices", "dmtz_status_string",
+            "dmtz_critical_mask", "dmtz_correct", "dmtz_correct_host", "dmtz_trace_separatrices", "dmtz_status_string",
             "dmtz_last_error", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end",
             "dmtz_slab_halo", "dmtz_trace_separatrices_range", "dmtz_slab_round_async", "dmtz_preserve_sep_bytes",
             "dmtz_preserve",
@@ -271,6 +273,50 @@ class Context:
             raise DmtzError(status, msg)
         return Result(status=status, g=g_out, edits=edits[:min(ne.value, cap)], n_edits=ne.value, stats=stats,
                       message=msg)
+
+    def correct_host(self, f_host: torch.Tensor, fhat_host: torch.Tensor, xi: float, q_max: int = 6,
+                     q_cap: int | None = None, tier: int = 2, max_rounds: int = 0, full_sweeps: bool = False,
+                     bufs: dict | None = None, g_host: torch.Tensor | None = None,
+                     edits_host: torch.Tensor | None = None, stream=None, raise_on_error: bool = True):
+        """The end-to-end call (dmtz_correct_host): f and fhat from HOST tensors (pinned
+        for full bandwidth), g and the edit list back into host tensors, every copy
+        inside the library call.  ``bufs`` (from host_buffers) holds the device
+        buffers; g_host / edits_host default to new pinned tensors.  Returns a Result
+        whose g / edits are the HOST tensors."""
+        for t in (f_host, fhat_host):
+            assert t.device.type == "cpu" and t.dtype == torch.float32 and tuple(t.shape) == self.shape
+            assert t.is_contiguous()
+        dev = self.workspace.device
+        if bufs is None:
+            bufs = self.host_buffers(dev)
+        if g_host is None:
+            g_host = torch.empty(self.shape, dtype=torch.float32).pin_memory()
+        if edits_host is None:
+            edits_host = torch.empty((max(self.N, 1), 16), dtype=torch.uint8).pin_memory()
+        cap = min(bufs["edits"].shape[0], edits_host.shape[0])
+        opts = _Opts(float(xi), int(q_max), int(q_max if q_cap is None else q_cap), int(tier), int(max_rounds),
+                     1 if full_sweeps else 0, 0)
+        ne = ctypes.c_int64()
+        st = _Stats()
+        status = _lib.dmtz_correct_host(
+            self._h, ctypes.c_void_p(f_host.data_ptr()), ctypes.c_void_p(fhat_host.data_ptr()), ctypes.byref(opts),
+            ctypes.c_void_p(self.workspace.data_ptr()), self.ws_bytes, ctypes.c_void_p(bufs["f"].data_ptr()),
+            ctypes.c_void_p(bufs["fhat"].data_ptr()), ctypes.c_void_p(bufs["g"].data_ptr()),
+            ctypes.c_void_p(bufs["edits"].data_ptr()), cap, ctypes.c_void_p(g_host.data_ptr()),
+            ctypes.c_void_p(edits_host.data_ptr()), ctypes.byref(ne), ctypes.byref(st), _stream_ptr(stream))
+        stats = _stats_dict(st, status)
+        msg = _lib.dmtz_last_error().decode() if status != OK else ""
+        if raise_on_error and status not in (OK, E_STUCK, E_ITER_CAP, E_CAPACITY):
+            raise DmtzError(status, msg)
+        return Result(status=status, g=g_host, edits=edits_host[:min(ne.value, cap)], n_edits=ne.value,
+                      stats=stats, message=msg)
+
+    def host_buffers(self, device) -> dict:
+        """Device buffers of correct_host: f, fhat, g (float[N]) and the edit list."""
+        return dict(f=torch.empty(self.shape, dtype=torch.float32, device=device),
+                    fhat=torch.empty(self.shape, dtype=torch.float32, device=device),
+                    g=torch.empty(self.shape, dtype=torch.float32, device=device),
+                    edits=torch.empty((max(self.N, 1), 16), dtype=torch.uint8, device=device))
 
     # ---------------------------------------------------------------- tiers 3-4
     def preserve(self, f: torch.Tensor, fhat: torch.Tensor, xi: float, tier: int = 4, q_max: int = 6,
@@ -510,7 +556,7 @@ def trace_separatrices(codes: torch.Tensor, kinds: int = KIND_DESC | KIND_ASC | 
 def correct_host(f: np.ndarray, fhat: np.ndarray, xi: float, device="cuda", **kw):
     """End-to-end call from HOST arrays: H2D of f and fhat, the C-loop, D2H of g and
     the edit list.  Returns (g numpy, edits numpy, stats)."""
-    ft = torch.from_numpy(np.ascontiguousarray(f, np.float32)).pin_memory().to(device, non_blocking=True)
-    fht = torch.from_numpy(np.ascontiguousarray(fhat, np.float32)).pin_memory().to(device, non_blocking=True)
-    r = correct(ft, fht, xi, **kw)
-    return r.g.cpu().numpy(), r.edits_numpy(), r.stats
+    fp = torch.from_numpy(np.ascontiguousarray(f, np.float32)).pin_memory()
+    fhp = torch.from_numpy(np.ascontiguousarray(fhat, np.float32)).pin_memory()
+    r = context(f.shape, torch.device(device)).correct_host(fp, fhp, xi, **kw)
+    return r.g.numpy(), r.edits.numpy().view(EDIT_DTYPE).reshape(-1), r.stats

@@ -904,6 +904,30 @@ dmtz_status dmtz_correct(dmtz_ctx* c, const float* f, const float* fhat, const d
   return r;
 }
 
+dmtz_status dmtz_correct_host(dmtz_ctx* c, const float* f_host, const float* fhat_host, const dmtz_correct_opts* o,
+                              void* workspace, size_t workspace_bytes, float* f_dev, float* fhat_dev, float* g_dev,
+                              dmtz_edit* edits_dev, int64_t edits_capacity, float* g_host, dmtz_edit* edits_host,
+                              int64_t* n_edits, dmtz_stats* st, dmtz_stream_t stream) {
+  if (!c || !f_host || !fhat_host || !f_dev || !fhat_dev || !n_edits || !st ||
+      (edits_host && edits_capacity > 0 && !edits_dev)) {
+    set_err("NULL argument");
+    return DMTZ_E_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t fb = (size_t)c->g.N * sizeof(float);
+  CK(cudaMemcpyAsync(f_dev, f_host, fb, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(fhat_dev, fhat_host, fb, cudaMemcpyHostToDevice, s));
+  const dmtz_status r = dmtz_correct(c, f_dev, fhat_dev, o, workspace, workspace_bytes, g_dev, edits_dev,
+                                     edits_capacity, n_edits, st, stream);
+  if (r != DMTZ_OK && r != DMTZ_E_STUCK && r != DMTZ_E_ITER_CAP && r != DMTZ_E_CAPACITY) return r;
+  if (g_host) CK(cudaMemcpyAsync(g_host, g_dev, fb, cudaMemcpyDeviceToHost, s));
+  const int64_t ne = *n_edits < edits_capacity ? *n_edits : edits_capacity;
+  if (edits_host && ne > 0)
+    CK(cudaMemcpyAsync(edits_host, edits_dev, (size_t)ne * sizeof(dmtz_edit), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return r;
+}
+
 static dmtz_status slab_check(dmtz_ctx* c, const dmtz_slab* sl, void* ws, size_t wsb, Layout* L) {
   if (!c || !sl || !ws) { set_err("NULL argument"); return DMTZ_E_ARG; }
   if (c->D != 3) { set_err("slab mode needs a 3D grid"); return DMTZ_E_DIMS; }

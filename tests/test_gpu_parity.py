@@ -319,3 +319,22 @@ def test_trace_connector_pool_fallback(dmtz, monkeypatch, cap):
     _compare_trace(dmtz, f)
     monkeypatch.setenv("DMTZ_CONN_POOL", "0")
     _compare_trace(dmtz, f)
+
+
+@pytest.mark.parametrize("name,shape", [("C2", (90, 180)), ("C4", (40, 40, 40))])
+def test_correct_host_equals_device(dmtz, name, shape):
+    """dmtz_correct_host (host buffers in and out, the copies inside the C call) returns
+    the device call's g and edit list bit for bit; NULL host outputs are skipped."""
+    import torch
+    f, fh, xi, _ = di.config_inputs(name, shape=shape)
+    ctx = dmtz.context(f.shape, torch.device("cuda", 0))
+    r = ctx.correct(torch.from_numpy(f).cuda(), torch.from_numpy(fh).cuda(), xi)
+    rh = ctx.correct_host(torch.from_numpy(f).pin_memory(), torch.from_numpy(fh).pin_memory(), xi)
+    assert rh.status == r.status and rh.n_edits == r.n_edits > 0
+    assert rh.g.device.type == "cpu" and rh.edits.device.type == "cpu"
+    assert torch.equal(rh.g.view(torch.int32), r.g.cpu().view(torch.int32))
+    assert torch.equal(rh.edits, r.edits.cpu())
+    assert rh.stats["rounds"] == r.stats["rounds"]
+    g2, e2, st2 = dmtz.correct_host(f, fh, xi)   # pageable numpy in, numpy out
+    assert np.array_equal(g2.view(np.int32), r.g.cpu().numpy().view(np.int32))
+    assert np.array_equal(e2, r.edits_numpy())
