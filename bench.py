@@ -73,6 +73,19 @@ def _ncu_traffic(kernel: str, workload: str):
         return None
 
 
+def _ncu_issue(kernel: str, workload: str):
+    """issue-active and ALU-pipe % of `kernel` from the committed ncu --set full capture."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        e = d.get(workload, {}).get(kernel)
+        return {"issue_active_pct": e["smsp__issue_active.avg.pct_of_peak_sustained_active"],
+                "alu_pipe_pct": e["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"],
+                "warps_active_pct": e["sm__warps_active.avg.pct_of_peak_sustained_active"],
+                "report": e.get("report")} if e else None
+    except Exception:
+        return None
+
+
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
 
@@ -355,6 +368,7 @@ def main():
     dec_ach = dec_ops / dec_s / 1e9
     roof = {"bound": "alu", "achieved": dec_ach, "peak": alu_peak, "unit": "Gop/s", "frac": dec_ach / alu_peak,
             "traffic": _ncu_traffic("k_decode", workload),
+            "ncu_issue": _ncu_issue("k_decode", workload),
             "kernel": "k_decode (criticality of g, critical-cell diff, target rules; default step)",
             "decode_ms_per_step": ds["decode_ms"], "screen_ms_per_step": ds["screen_ms"],
             "share_of_step": ds["decode_ms"] / ms, "launches_per_step": ds["sweeps"],
@@ -369,6 +383,7 @@ def main():
     gbs = BYTES_PER_ANCHOR[D] * N / t_launch / 1e9
     roof_screen = {"bound": "alu", "achieved": alu_achieved, "peak": alu_peak, "unit": "Gop/s",
                    "frac": alu_achieved / alu_peak, "traffic": _ncu_traffic("k_screen", workload),
+                   "ncu_issue": _ncu_issue("k_screen", workload),
                    "kernel": "k_screen (gradient codes of g, a launch that recomputes every anchor)",
                    "launch_ms": t_launch * 1e3, "alu_ops_per_anchor": ALU_OPS_PER_ANCHOR[D],
                    "bytes_per_anchor": BYTES_PER_ANCHOR[D], "hbm_achieved_gbs": gbs, "hbm_peak_gbs": hbm,
