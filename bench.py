@@ -259,8 +259,19 @@ def chunked_trace(ctx, codes, dev, stream, budget, sizes):
         nb += tr["origin"].shape[0]
         nc += tr["cells"].shape[0]
         del tr
+    per_kind = {}
+    for kname, kb in (("desc_ms", 1), ("asc_ms", 2), ("conn_ms", 4)):   # one kind per call
+        per_kind[kname] = 0.0
+        for g in groups:
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ctx.trace_separatrices(codes, kinds=kb, out=bufs, z_range=(g[0], g[1]))
+            e1.record(stream)
+            torch.cuda.synchronize()
+            per_kind[kname] += e0.elapsed_time(e1)
     del bufs
-    return {"trace_ms": ms, "n_branches": nb, "n_cells": nc, "groups": len(groups),
+    return {"trace_ms": ms, **per_kind, "n_branches": nb, "n_cells": nc, "groups": len(groups),
             "mode": f"branches by origin plane in {len(groups)} groups of <= {budget / 1e9:.0f} GB of outputs "
                     "(outputs not kept); per-group sizing untimed",
             "full_csr_gb": (sizes["n_branches"] * 33 + sizes["n_cells"] * 8) / 1e9,

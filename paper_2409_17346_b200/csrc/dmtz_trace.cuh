@@ -463,6 +463,122 @@ __global__ void k_walk(TraceViews V, Grid g, int64_t b0, int64_t nb,
   }
 }
 
+// The same walks with dynamic lane refill: path lengths are heavy-tailed (C5: 36
+// cells per branch on average), so with one branch per thread a warp runs as long as
+// its longest path while the other lanes idle.  Here every lane advances its walk one
+// step per iteration and an idle lane takes the next branch at once (warp-aggregated
+// atomicAdd on *ctr, zeroed before the launch); persistent grid.  Same per-branch
+// results as k_walk (each branch writes only its own cells / count / terminal).
+template <int D>
+__global__ void __launch_bounds__(128)
+k_walk_dyn(TraceViews V, Grid g, int64_t b0, int64_t nb, const uint64_t* __restrict__ origin, const uint8_t* __restrict__ kind,
+           uint64_t* __restrict__ jterm, long long* __restrict__ off, uint64_t* __restrict__ cells, bool write,
+           Counters* __restrict__ cnt, unsigned long long* __restrict__ ctr) {
+  const int64_t cap_steps = g.N * 26 + 1;
+  const int lane = threadIdx.x & 31;
+  const int tt0 = t_first_of_dim<D>(Tr<D>::TOP);
+  int64_t b = -1;
+  bool drained = false;
+  int k = 0, bt = 0;
+  int64_t v = 0, x = 0, y = 0, z = 0, n = 0, step = 0;
+  uint64_t* out = nullptr;
+  uint64_t term = CELL_BOUNDARY;
+  for (;;) {
+    const unsigned idle = __ballot_sync(0xffffffffu, b < 0);
+    if (idle && !drained) {  // warp-uniform
+      const int leader = __ffs(idle) - 1;
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(ctr, (unsigned long long)__popc(idle));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if ((int64_t)(base + (unsigned long long)__popc(idle)) >= nb - b0) drained = true;
+      if (b < 0) {
+        const int64_t nbi = b0 + (int64_t)base + __popc(idle & ((1u << lane) - 1u));
+        if (nbi < nb) {
+          b = nbi;
+          int64_t a;
+          int t;
+          id_cell<D>(origin[b], a, t);
+          k = kind[b];
+          const int jj = (int)jterm[b];
+          n = 0;
+          step = 0;
+          out = write ? cells + off[b] : nullptr;
+          term = CELL_BOUNDARY;
+          if (k == 1) {
+            v = a + mask_delta(g, t_vmask<D>(t, jj));
+            if (write) out[0] = cell_id<D>(v, 0);
+            n = 1;
+          } else if (k == 2) {
+            coords_of(g, a, x, y, z);
+            x += t_cof_anchor<D>(t, jj, 0);
+            y += t_cof_anchor<D>(t, jj, 1);
+            z += t_cof_anchor<D>(t, jj, 2);
+            v = x + y * g.sy + z * g.sz;
+            bt = t_cof_type<D>(t, jj);
+          }
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, b < 0)) break;
+    if (b < 0) continue;
+    bool done = false;
+    if (k != 1 && k != 2) {
+      n = -1;  // connectors run in k_conn_small / k_walk_block
+      done = true;
+    } else if (step++ > cap_steps) {
+      n = -1;
+      done = true;
+    } else if (k == 1) {
+      const uint32_t s = (__ldg(V.vnib + (v >> 1)) >> (4 * (v & 1))) & 15u;
+      if (s == (uint32_t)t_none<D>(0)) {  // critical vertex
+        term = cell_id<D>(v, 0);
+        done = true;
+      } else {
+        const int64_t w = v + t_link<D>(0, s, 0) + t_link<D>(0, s, 1) * g.sy + t_link<D>(0, s, 2) * g.sz;
+        if (write) {
+          out[n] = cell_id<D>(cof_anchor<D>(g, v, 0, s), t_cof_type<D>(0, s));
+          out[n + 1] = cell_id<D>(w, 0);
+        }
+        n += 2;
+        v = w;
+      }
+    } else {
+      if (write) out[n] = cell_id<D>(v, bt);
+      n++;
+      const int j = (int)(__ldg(V.tpair + v) >> (3 * (bt - tt0))) & 7;
+      if (j == 7) {  // maximum
+        term = cell_id<D>(v, bt);
+        done = true;
+      } else {
+        const int dm = t_facet<D>(bt, j, 0), ct = t_facet<D>(bt, j, 1);
+        const int64_t cx = x + (dm & 1), cy = y + ((dm >> 1) & 1), cz = z + ((dm >> 2) & 1);
+        const int64_t ca = v + mask_delta(g, dm);
+        if (write) out[n] = cell_id<D>(ca, ct);
+        n++;
+        bool moved = false;  // the other top cofacet of (ca, ct)
+        for (int s = 0; s < t_nlink<D>(ct); s++) {
+          const int64_t lx = cx + t_link<D>(ct, s, 0), ly = cy + t_link<D>(ct, s, 1), lz = cz + t_link<D>(ct, s, 2);
+          if (lx < 0 || ly < 0 || lz < 0 || lx >= g.nx || ly >= g.ny || lz >= g.nz) continue;
+          const int nt = t_cof_type<D>(ct, s);
+          const int64_t nx_ = cx + t_cof_anchor<D>(ct, s, 0), ny_ = cy + t_cof_anchor<D>(ct, s, 1),
+                        nz_ = cz + t_cof_anchor<D>(ct, s, 2);
+          const int64_t nbb = nx_ + ny_ * g.sy + nz_ * g.sz;
+          if (nbb == v && nt == bt) continue;
+          v = nbb; bt = nt; x = nx_; y = ny_; z = nz_; moved = true;
+          break;
+        }
+        if (!moved) done = true;  // boundary facet: terminal stays BOUNDARY
+      }
+    }
+    if (done) {
+      if (n < 0) { atomicAdd(&cnt->n_internal, 1ull); n = 0; }
+      if (!write) off[b] = n;
+      else jterm[b] = term;
+      b = -1;
+    }
+  }
+}
+
 // Connector tables in shared memory: triangle type -> its 3 facet edges (dm | edge
 // index << 3); edge (index, slot) -> cofacet triangle (type | (anchor delta + 1) << 5, 7, 9).
 struct ConnTab {
@@ -1000,6 +1116,30 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
 
 inline size_t trace_scratch_bytes(const Grid&, int) { return 0; }  // reuses free workspace regions
 
+// walks of the descending branches [0, nasc0) and the ascending ones [nasc0, nb):
+// descending paths by k_walk (one thread per branch: short, cheap steps -- the refill
+// bookkeeping of k_walk_dyn doubled their time on C4), ascending ones by k_walk_dyn
+// (C4 76 -> 65 ms); DMTZ_WALK_STATIC=1: k_walk for both
+template <int D>
+cudaError_t launch_walk(const TraceViews& V, const Grid& g, int64_t nasc0, int64_t nb, const TraceArgs& A,
+                        long long* off, bool write, Counters* dc, int threads, cudaStream_t s) {
+  const char* ws = getenv("DMTZ_WALK_STATIC");
+  const bool stat = ws && ws[0] == '1';
+  const int64_t n_static = stat ? nb : nasc0;
+  if (n_static > 0)
+    k_walk<D><<<(unsigned)((n_static + threads - 1) / threads), threads, 0, s>>>(
+        V, g, 0, n_static, A.out_origin, A.out_kind, A.out_terminal, off, A.out_cells, write, dc);
+  if (n_static < nb) {
+    cudaError_t e = cudaMemsetAsync(&dc->pad[8], 0, 8, s);
+    if (e != cudaSuccess) return e;
+    const int64_t want = (nb - n_static + 127) / 128;
+    const unsigned grid = (unsigned)(want < 148 * 16 ? want : 148 * 16);
+    k_walk_dyn<D><<<grid, 128, 0, s>>>(V, g, n_static, nb, A.out_origin, A.out_kind, A.out_terminal, off,
+                                       A.out_cells, write, dc, &dc->pad[8]);
+  }
+  return cudaGetLastError();
+}
+
 // ----------------------------------------------------------------------------- driver
 #define TCK(x)                                  \
   do {                                          \
@@ -1128,9 +1268,8 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   for (int pass = 0; pass < 2; pass++) {
     const bool write = pass == 1;
     TCK(cudaMemsetAsync(ovf, 0, (size_t)ovf_words * 4 + 4, s));
-    if (blocks_path && !write)  // descending / ascending paths: one thread per branch
-      k_walk<D><<<(unsigned)blocks_path, threads, 0, s>>>(V, g, 0, conn_base, A.out_origin, A.out_kind,
-                                                          A.out_terminal, off, A.out_cells, write, dc);
+    if (blocks_path && !write)  // descending / ascending paths
+      TCK(launch_walk<D>(V, g, nbk[0], conn_base, A, off, write, dc, threads, s));
     if (nbk[2]) {  // connectors: one thread per 2-saddle, small queues in shared memory
       const int64_t nbc = (nbk[2] + CONN_THREADS - 1) / CONN_THREADS;
       k_conn_small<D><<<(unsigned)(nbc < 148 * 64 ? nbc : 148 * 64), CONN_THREADS, 0, s>>>(
@@ -1204,8 +1343,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
       }
     }
     if (blocks_path && write)  // after the connectors: the paths overwrite the event pool
-      k_walk<D><<<(unsigned)blocks_path, threads, 0, s>>>(V, g, 0, conn_base, A.out_origin, A.out_kind,
-                                                          A.out_terminal, off, A.out_cells, write, dc);
+      TCK(launch_walk<D>(V, g, nbk[0], conn_base, A, off, write, dc, threads, s));
     TCK(cudaGetLastError());
     if (!write) {
       TCK(cudaMemsetAsync(off + nb, 0, 8, s));

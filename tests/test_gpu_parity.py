@@ -338,3 +338,13 @@ def test_correct_host_equals_device(dmtz, name, shape):
     g2, e2, st2 = dmtz.correct_host(f, fh, xi)   # pageable numpy in, numpy out
     assert np.array_equal(g2.view(np.int32), r.g.cpu().numpy().view(np.int32))
     assert np.array_equal(e2, r.edits_numpy())
+
+
+@pytest.mark.parametrize("family,shape", [("lognormal", (20, 22, 24)), ("multiscale", (16, 40, 36)),
+                                          ("climate", (60, 90))])
+def test_trace_static_walk_kernel(dmtz, monkeypatch, family, shape):
+    """DMTZ_WALK_STATIC=1 (k_walk: one thread per branch) gives the oracle's CSR as the
+    default k_walk_dyn (lanes refilled as their paths end) does."""
+    f, _, _ = di.random_case(shape, 5, family=family)
+    monkeypatch.setenv("DMTZ_WALK_STATIC", "1")
+    _compare_trace(dmtz, f)
