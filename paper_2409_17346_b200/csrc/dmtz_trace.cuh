@@ -1300,7 +1300,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
         while (qn + 2 * h > words) h /= 2;
         int64_t ns = words / (qn + 2 * h);
         if (ns < 1) ns = 1;
-        if (ns > 4096) ns = 4096;
+        if (ns > 148 * 32) ns = 148 * 32;  // one resident 64-thread block-BFS per slot
         bool any = false, cleared = false;
         for (int64_t w0 = 0; w0 < ovf_words; w0 += chunk_words) {
           const int64_t w1 = w0 + chunk_words < ovf_words ? w0 + chunk_words : ovf_words;
@@ -1333,9 +1333,21 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
           if (A.verbose)
             fprintf(stderr, "dmtz trace pass %d level %d: %lld connectors, q %lld, %lld blocks\n", pass, level + 1,
                     (long long)cn, (long long)qn, (long long)nblk);
-          k_walk_block<D, 256><<<(unsigned)nblk, 256, 0, s>>>(V.eview, g, dlist, cn, conn_base,
-                                                              A.out_origin, A.out_terminal, off, A.out_cells,
-                                                              write, sc, qn, h, (unsigned int*)ovf, dc);
+          // block size of the BFS: DMTZ_BFS_THREADS=64|128|256|512|1024 (default 64: the
+          // connectors of a level are many, so saddles in flight beat threads per saddle --
+          // C5 origin planes [427, 597) 1475 -> 1105 ms, C3 342 -> 310 ms vs 256 threads)
+          const char* bt = getenv("DMTZ_BFS_THREADS");
+          const int bfs_t = bt ? atoi(bt) : 64;
+#define DMTZ_BFS_LAUNCH(T)                                                                             \
+  k_walk_block<D, T><<<(unsigned)nblk, T, 0, s>>>(V.eview, g, dlist, cn, conn_base, A.out_origin,      \
+                                                  A.out_terminal, off, A.out_cells, write, sc, qn, h, \
+                                                  (unsigned int*)ovf, dc)
+          if (bfs_t == 1024) DMTZ_BFS_LAUNCH(1024);
+          else if (bfs_t == 512) DMTZ_BFS_LAUNCH(512);
+          else if (bfs_t == 128) DMTZ_BFS_LAUNCH(128);
+          else if (bfs_t == 256) DMTZ_BFS_LAUNCH(256);
+          else DMTZ_BFS_LAUNCH(64);
+#undef DMTZ_BFS_LAUNCH
           TCK(cudaGetLastError());
         }
         if (!any) break;
