@@ -548,7 +548,11 @@ def main():
         sloop = {}
         for item in args.sloop_config.split(";"):
             name, tl = item.split(":")
-            sloop[name] = sloop_line(name, [int(t) for t in tl.split(",")], dev, stream, not args.no_cpu_baseline)
+            try:  # a failed extra line (e.g. out of memory next to C5's buffers) must not lose the main line
+                sloop[name] = sloop_line(name, [int(t) for t in tl.split(",")], dev, stream, not args.no_cpu_baseline)
+            except Exception as e:  # noqa: BLE001
+                sloop[name] = {"error": str(e)[:200]}
+                torch.cuda.empty_cache()
 
     st = r.stats
     line = {

@@ -47,5 +47,5 @@ for cname in a.configs:
             best = ms if best is None else min(best, ms)
         sig = (tr["cells"].shape[0], int(tr["cells"].sum().item()), int(tr["offsets"].sum().item()))
         ref = ref or sig
-        print(f"{cname} planes [{z0},{z1}) bfs_threads {bt}: conn {best:.1f} ms, cells {sig[0]}, "
+        print(f"{cname} planes [{z0},{z1}) bfs_threads {bt}: conn {best:.1f} ms, cells {sig[0]}, sum {sig[1]}, "
               f"same_output {sig == ref}", flush=True)
