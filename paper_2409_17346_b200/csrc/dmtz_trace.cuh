@@ -805,7 +805,10 @@ k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
 // (entry, facet) order, decided by an atomicMin of batch << 7 | candidate on its
 // slot's owner word), so the events come out in the sequential FIFO order.
 constexpr int WQ = 512, WH = 1024, CONNW_WARPS = 4;
-constexpr size_t CONNW_SMEM = (size_t)CONNW_WARPS * (WQ * 8 + WH * 8 + WH * 4);
+// per warp: hash keys (u64), owner words (u32), and the queue as hash slots (u16) --
+// 13 KB, so 4 blocks (16 warps) fit an SM (16 KB with a queue of keys: 3 blocks)
+constexpr size_t CONNW_WARP_BYTES = (size_t)WH * 8 + WH * 4 + WQ * 2;
+constexpr size_t CONNW_SMEM = (size_t)CONNW_WARPS * CONNW_WARP_BYTES;
 template <int D>
 __global__ void __launch_bounds__(CONNW_WARPS * 32)
 k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restrict__ list,
@@ -816,9 +819,9 @@ k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restri
   __shared__ ConnTab CT;
   conn_tables_init<D>(CT);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  unsigned long long* queue = smw + (size_t)wid * (WQ + WH + WH / 2);
-  unsigned long long* keys = queue + WQ;
+  unsigned long long* keys = smw + (size_t)wid * (CONNW_WARP_BYTES / 8);
   uint32_t* owner = (uint32_t*)(keys + WH);
+  uint16_t* queue = (uint16_t*)(owner + WH);  // queue entry = the hash slot of its key
   for (int i = lane; i < WH; i += 32) { keys[i] = 0ull; owner[i] = 0xFFFFFFFFu; }
   __syncwarp();
   auto key = [](int64_t an, int ty) { return (unsigned long long)(an * 32 + ty) + 1ull; };
@@ -839,8 +842,9 @@ k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restri
     id_cell<D>(origin[b], a0, t0);
     uint64_t* out = write ? cells + off[b] : nullptr;
     if (lane == 0) {
-      queue[0] = key(a0, t0);
-      owner[find_or_insert(key(a0, t0))] = 0u;  // seen before every batch
+      const int s0 = find_or_insert(key(a0, t0));
+      owner[s0] = 0u;  // seen before every batch
+      queue[0] = (uint16_t)s0;
     }
     __syncwarp();
     int head = 0, tail = 1;
@@ -854,7 +858,7 @@ k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restri
       unsigned long long ckey[3] = {0, 0, 0};
       bool bad = false;
       if (lane < K) {
-        const unsigned long long cur = queue[head + lane] - 1ull;
+        const unsigned long long cur = keys[queue[head + lane]] - 1ull;
         const int64_t B = (int64_t)(cur / 32);
         const int bt = (int)(cur % 32);
         conn_expand<D>(CT, eview, g, B, bt, ckind, cid, ckey);
@@ -892,7 +896,7 @@ k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restri
           if (write) out[nev + pe] = cid[j];
           pe++;
         }
-        if (isnew[j]) { queue[tail + pq] = ckey[j]; pq++; }
+        if (isnew[j]) { queue[tail + pq] = (uint16_t)cslot[j]; pq++; }
       }
       __syncwarp();
       nev += tot_e;
@@ -905,22 +909,11 @@ k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restri
       for (int i = lane; i < WH; i += 32) { keys[i] = 0ull; owner[i] = 0xFFFFFFFFu; }
       if (lane == 0) atomicOr(overflow + (cb >> 5), 1u << (cb & 31));
     } else {
-      // clean the visited set: find every queued key's slot first, then clear
+      // clean the visited set: the queue holds exactly the occupied slots
       for (int i = lane; i < tail; i += 32) {
-        const unsigned long long k = queue[i];
-        const int h = hslot(k);
-        int sl = -1;
-        for (int p = 0; p < WH; p++) {
-          const int j = (h + p) & (WH - 1);
-          if (keys[j] == k) { sl = j; break; }
-          if (keys[j] == 0ull) break;
-        }
-        queue[i] = (unsigned long long)(long long)sl;
-      }
-      __syncwarp();
-      for (int i = lane; i < tail; i += 32) {
-        const long long sl = (long long)queue[i];
-        if (sl >= 0) { keys[sl] = 0ull; owner[sl] = 0xFFFFFFFFu; }
+        const int sl = queue[i];
+        keys[sl] = 0ull;
+        owner[sl] = 0xFFFFFFFFu;
       }
       if (lane == 0) {
         if (!write) off[b] = nev;
