@@ -133,37 +133,45 @@ def cpu_cores():
         return os.cpu_count()
 
 
-def oracle_sample(f, fh, xi, edge):
-    """Time the oracle (as it stands) on a bounded crop of the workload."""
+def oracle_round(f, fh, xi, planes=None):
+    """The oracle (as it stands) on one full C-loop round of the workload: the literal
+    gradient of g = fhat, the classification of every cell and the Eq. 2 edits
+    (max_rounds = 1), optionally on the first ``planes`` z-planes only.  The round is
+    timed inside the oracle (omp_get_wtime around the round; the one-off setup -- lb and
+    the gradient of f -- is not part of a round).  Returns dict(value Mvox/s, ...)."""
     import oracle
     oracle.build()
-    crop = tuple(slice(0, min(edge, s)) for s in f.shape)
-    fc, fhc = np.ascontiguousarray(f[crop]), np.ascontiguousarray(fh[crop])
+    if planes is not None and f.ndim == 3:
+        f, fh = np.ascontiguousarray(f[:planes]), np.ascontiguousarray(fh[:planes])
     t0 = time.perf_counter()
-    r = oracle.correct(fc, fhc, xi)
-    dt = time.perf_counter() - t0
-    sweeps = r["stats"]["rounds"] + 1
-    return dict(value=fc.size * sweeps / dt / 1e6, seconds=dt, sweeps=sweeps, shape=list(fc.shape),
-                rounds=r["stats"]["rounds"], threads=oracle.num_threads(), ref=r, fc=fc, fhc=fhc)
+    r = oracle.correct(f, fh, xi, max_rounds=1, round_log=True)
+    total = time.perf_counter() - t0
+    t = r["round_seconds"][0]
+    return dict(value=f.size / t / 1e6, round_seconds=t, call_seconds=total, shape=list(f.shape),
+                threads=oracle.num_threads(), n_false=r["false_per_round"][0])
 
 
 def run_reference(args, cfg, f, fh, xi):
+    """--impl reference: this tier's reference arm is the CPU oracle.  Each step = one full
+    C-loop round of the oracle on a bounded sample of the workload (the first
+    --ref-planes z-planes of the config's field), the same unit as the GPU arm's value."""
     if int(os.environ.get("RANK", "0")) != 0:
         return
     vals = []
     for i in range(args.warmup + args.steps):
-        s = oracle_sample(f, fh, xi, args.ref_edge)
+        s = oracle_round(f, fh, xi, planes=args.ref_planes)
         if i >= args.warmup:
             vals.append(s)
     v = float(np.median([s["value"] for s in vals]))
-    sample = (f"oracle C-loop to its fixed point on the {vals[0]['shape']} crop of {cfg.name} "
-              f"({vals[0]['sweeps']} sweeps, {vals[0]['seconds']:.1f} s each)")
+    sample = (f"one oracle C-loop round (literal gradient of g, classification, Eq. 2 edits) on z-planes "
+              f"[0, {vals[0]['shape'][0]}) of {cfg.name} {'x'.join(map(str, cfg.shape))} "
+              f"({vals[0]['round_seconds']:.2f} s per round, setup untimed)")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Mvoxels/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": float(np.median([s["seconds"] for s in vals]) * 1e3), "higher_is_better": True,
+            "ms_per_step": float(np.median([s["round_seconds"] for s in vals]) * 1e3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{cfg.name} {cfg.family} {'x'.join(map(str, cfg.shape))} rel eps {cfg.eps}",
-                       "crop": vals[0]["shape"], "parallelism": "host cores (OpenMP)"},
+                       "sample_shape": vals[0]["shape"], "parallelism": "host cores (OpenMP)"},
             "cpu_baseline": {"value": v, "unit": "Mvoxels/s", "cores": vals[0]["threads"], "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": v, "unit": "Mvoxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -286,8 +294,13 @@ def main():
     ap.add_argument("--impl", default="dmtz", choices=["dmtz", "reference"])
     ap.add_argument("--config", default="C4")
     ap.add_argument("--shape", default=None, help="override the config shape, e.g. 128,128,128")
-    ap.add_argument("--ref-edge", type=int, default=96, help="oracle crop edge for the CPU baseline")
+    ap.add_argument("--ref-planes", type=int, default=48,
+                    help="--impl reference: z-planes of the field per oracle round (a bounded sample)")
+    ap.add_argument("--detail", default=None, help="also write the full result dict to this JSON file "
+                    "(default gpurun_out/bench_detail.json when gpurun_out/ exists)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-golden-parity", dest="golden_parity", action="store_false",
+                    help="skip the full-size parity check against tests/golden/oracle_full_<C>.json")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-trace", action="store_true")
     ap.add_argument("--slab", action="store_true", help="run the multi-GPU slab path even with one rank")
@@ -330,90 +343,73 @@ def main():
     def step(full=False, profile=False):
         return ctx.correct(ft, fht, xi, full_sweeps=full, g_out=g, edits=edits, profile=profile)
 
+    def timed(fn, reps):
+        ts, out = [], None
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            out = fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return out, ts
+
+    # THE STEP: one pass of the C-loop to its fixed point with every round a full sweep
+    # (full_sweeps=1: every code of g recomputed, every anchor classified in every round);
+    # value = N x sweeps / step time = SURVEY.md §8(d-1)'s full-sweep round throughput.
     for _ in range(args.warmup):
-        r = step()
+        step(full=True)
     torch.cuda.synchronize()
-    times, stats = [], []
     with Clocks(local) as clk:
-        for _ in range(args.steps):
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            r = step()
-            e1.record(stream)
-            torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1))
-            stats.append(r.stats)
-        # the reference (full-recompute) mode: every code recomputed in every round
-        fr_t = []
-        for _ in range(2):
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            rfull = step(full=True)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            fr_t.append(e0.elapsed_time(e1))
-        # once more with per-kernel CUDA events (host-driven rounds) for the roofline
+        rfull, times = timed(lambda: step(full=True), args.steps)
+        # time to the fixed point in the library's default mode (dirty frontier + exact
+        # change skipping, bit-identical output): the second half of BASELINE's metric
+        r, ttfp_t = timed(step, max(3, args.steps))
+        # per-kernel CUDA events (host-driven rounds, one extra step each) for the roofline
         rp = step(full=True, profile=True)
-        rpd = step(profile=True)   # default mode, per-kernel events
+        rpd = step(profile=True)
     assert rfull.n_edits == r.n_edits and rfull.stats["rounds"] == r.stats["rounds"]
     ms = float(np.median(times))
-    sweeps = int(np.median([s["sweeps"] for s in stats]))
-    value = N * sweeps / (ms * 1e-3) / 1e6
-    fr_ms = float(np.median(fr_t))
-    full_recompute = {"value": N * rfull.stats["sweeps"] / (fr_ms * 1e-3) / 1e6, "unit": "Mvoxels/s",
-                      "ms_per_step": fr_ms, "t_round_full_ms": fr_ms / rfull.stats["sweeps"],
-                      "mode": "full_sweeps=1: every code recomputed, every anchor classified"}
+    sweeps = rfull.stats["sweeps"]
+    t_round = ms / sweeps
+    value = N / (t_round * 1e-3) / 1e6
+    ttfp = float(np.median(ttfp_t))
 
-    # roofline of the dominant kernel of the default step (live CUDA events on the launching stream,
-    # one extra host-driven step): k_decode; k_screen's on the rounds that recompute every code
     peaks = _peaks()
     hbm = peaks.get("hbm_gbs") or 6650.0
     sm_mhz = peaks.get("sm_max_mhz") or 1965.0
     alu_peak = 148 * 64 * sm_mhz * 1e6 / 1e9          # Gop/s: 148 SMs x 4 SMSP x 16-lane ALU pipe
     workload = f"{cfg.name} {'x'.join(map(str, f.shape))}"
-    ds = rpd.stats
-    dec_ops = DECODE_OPS_PER_ANCHOR[D] * ds["anchors_decoded"] + RULE_OPS_PER_CELL * ds["cells_evaluated"]
-    dec_s = ds["decode_ms"] * 1e-3
-    dec_ach = dec_ops / dec_s / 1e9
-    roof = {"bound": "alu", "achieved": dec_ach, "peak": alu_peak, "unit": "Gop/s", "frac": dec_ach / alu_peak,
-            "traffic": _ncu_traffic("k_decode", workload),
-            "ncu_issue": _ncu_issue("k_decode", workload),
-            "kernel": "k_decode (criticality of g, critical-cell diff, target rules; default step)",
-            "decode_ms_per_step": ds["decode_ms"], "screen_ms_per_step": ds["screen_ms"],
-            "share_of_step": ds["decode_ms"] / ms, "launches_per_step": ds["sweeps"],
-            "anchors_decoded": ds["anchors_decoded"], "cells_evaluated": ds["cells_evaluated"],
-            "anchors_replayed": ds["anchors_replayed"],
-            "ops_per_decoded_anchor": DECODE_OPS_PER_ANCHOR[D], "ops_per_false_cell": RULE_OPS_PER_CELL,
-            "peak_source": "ALU: 148 SMs x 64 lanes/clk x MEASURED_PEAKS sm_max_mhz (DESIGN.md section 7)",
-            "traffic_note": "ncu dram bytes per launch, mean over one step's launches (profiles/ncu_summary.json)"}
     ps = rp.stats
+    # the full-sweep round's kernels (CUDA events on the launching stream, host-driven step)
+    k_ms = {"screen": ps["screen_ms"], "decode": ps["decode_ms"], "edit": ps.get("edit_ms", 0.0)}
+    round_dev_ms = sum(k_ms.values()) / sweeps
+    alg_bytes = BYTES_PER_ANCHOR[D] * N           # per full-sweep round (g f32 + the f code)
+    ach = alg_bytes / (t_round * 1e-3) / 1e9
+    ncu_round = _ncu_traffic("round", workload)
+    roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+            "traffic": ncu_round,
+            "kernel": "full-sweep C-loop round (k_screen + k_decode + k_edit_rows), SURVEY §8(d-1)",
+            "algorithmic_bytes_per_voxel": BYTES_PER_ANCHOR[D], "t_round_ms": t_round,
+            "kernel_ms_per_round": {k: v / sweeps for k, v in k_ms.items()},
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)",
+            "traffic_note": "ncu dram__bytes read+write of one full-sweep round's kernels (profiles/ncu_summary.json)"}
     t_launch = ps["screen_ms_full"] / max(ps["n_screen_full"], 1) * 1e-3
-    alu_achieved = ALU_OPS_PER_ANCHOR[D] * N / t_launch / 1e9
-    gbs = BYTES_PER_ANCHOR[D] * N / t_launch / 1e9
-    roof_screen = {"bound": "alu", "achieved": alu_achieved, "peak": alu_peak, "unit": "Gop/s",
-                   "frac": alu_achieved / alu_peak, "traffic": _ncu_traffic("k_screen", workload),
-                   "ncu_issue": _ncu_issue("k_screen", workload),
-                   "kernel": "k_screen (gradient codes of g, a launch that recomputes every anchor)",
-                   "launch_ms": t_launch * 1e3, "alu_ops_per_anchor": ALU_OPS_PER_ANCHOR[D],
-                   "bytes_per_anchor": BYTES_PER_ANCHOR[D], "hbm_achieved_gbs": gbs, "hbm_peak_gbs": hbm,
-                   "hbm_frac": gbs / hbm, "screen_ms_per_step": ds["screen_ms"],
-                   "share_of_step": ds["screen_ms"] / ms}
+    alu_ach = ALU_OPS_PER_ANCHOR[D] * N / t_launch / 1e9
+    roof_alu = {"bound": "alu", "kernel": "k_screen (gradient codes of g, one full-sweep launch)",
+                "achieved": alu_ach, "peak": alu_peak, "unit": "Gop/s", "frac": alu_ach / alu_peak,
+                "launch_ms": t_launch * 1e3, "alu_ops_per_anchor": ALU_OPS_PER_ANCHOR[D],
+                "ncu": _ncu_issue("k_screen", workload),
+                "peak_source": "ALU pipe: 148 SMs x 64 lanes/clk x sm_max_mhz (B300_MICROARCH: alu rt=2/SMSP)"}
+    ds = rpd.stats
+    frontier = {"time_to_fixed_point_ms": ttfp, "rounds": r.stats["rounds"], "sweeps": r.stats["sweeps"],
+                "codes_recomputed_full_sweep_equivalents": r.stats["anchors_recomputed"] / N,
+                "kernel_ms": {"screen": ds["screen_ms"], "decode": ds["decode_ms"], "edit": ds.get("edit_ms", 0.0)},
+                "gpu_launches": r.stats["launches"]}
 
-    # the north star's per-iteration HBM fraction: 12 B/voxel (g + cand_f) per sweep over the whole step
-    hbm_iter = {"algorithmic_bytes_per_voxel_sweep": BYTES_PER_ANCHOR[D],
-                "achieved_gbs": BYTES_PER_ANCHOR[D] * N * sweeps / (ms * 1e-3) / 1e9, "peak_gbs": hbm,
-                "frac": BYTES_PER_ANCHOR[D] * N * sweeps / (ms * 1e-3) / 1e9 / hbm,
-                "full_sweep_round_frac": BYTES_PER_ANCHOR[D] * N / (fr_ms / rfull.stats["sweeps"] * 1e-3) / 1e9 / hbm,
-                "note": "the path is ALU-bound (DESIGN.md section 7): 105 SoS compares per anchor per code"}
-    # time-to-fixed-point (the second half of BASELINE's metric): the timed default step
-    frontier = {"time_to_fixed_point_ms": ms, "rounds": r.stats["rounds"], "sweeps": r.stats["sweeps"],
-                "anchors_classified": r.stats["anchors_swept"], "codes_recomputed": r.stats["anchors_recomputed"],
-                "full_sweep_equivalents": r.stats["anchors_recomputed"] / N}
-
-    # traces of the converged field (a9-a11), once
-    trace = None
+    # traces of the converged field (a9-a11), once; CSR digests for the parity check
+    trace, csr_dig = None, None
     if not args.no_trace:
         codes = ctx.compute_gradient(g)
         try:
@@ -422,29 +418,53 @@ def main():
             free = torch.cuda.mem_get_info()[0]
             if need < 0.8 * free:
                 bufs = ctx.trace_buffers(sizes["n_branches"], sizes["n_cells"], dev)
-                torch.cuda.synchronize()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                tr = ctx.trace_separatrices(codes, out=bufs)
-                e1.record(stream)
-                torch.cuda.synchronize()
+                tr, tt = timed(lambda: ctx.trace_separatrices(codes, out=bufs), 2)
                 kinds = torch.bincount(tr["kind"].long(), minlength=5).tolist()
-                trace = {"trace_ms": e0.elapsed_time(e1), "n_branches": sizes["n_branches"],
-                         "n_cells": sizes["n_cells"], "desc": kinds[1], "asc": kinds[2], "conn": kinds[4]}
+                tms = float(np.median(tt))
+                # CSR write floor: 8 B per cell + 8 B offset + 8 B origin + 8 B terminal + 1 B kind per branch
+                csr_bytes = 8 * sizes["n_cells"] + 25 * sizes["n_branches"]
+                trace = {"trace_ms": tms, "n_branches": sizes["n_branches"], "n_cells": sizes["n_cells"],
+                         "desc": kinds[1], "asc": kinds[2], "conn": kinds[4],
+                         "roofline": {"bound": "hbm", "achieved": csr_bytes / (tms * 1e-3) / 1e9, "peak": hbm,
+                                      "unit": "GB/s", "frac": csr_bytes / (tms * 1e-3) / 1e9 / hbm,
+                                      "note": "CSR output bytes only (write floor); the walks are latency-bound"}}
+                if args.golden_parity:
+                    from tests import digest as dg
+                    csr_dig = {"n_branches": tr["origin"].shape[0], "n_cells": tr["cells"].shape[0],
+                               "digests": {k: dg.digest_t(tr[k]) for k in ("offsets", "cells", "origin",
+                                                                            "terminal", "kind")}}
                 del tr
                 for kname, kb in (("desc_ms", 1), ("asc_ms", 2), ("conn_ms", 4)):   # one kind per call
-                    torch.cuda.synchronize()
-                    e0.record(stream)
-                    ctx.trace_separatrices(codes, kinds=kb, out=bufs)
-                    e1.record(stream)
-                    torch.cuda.synchronize()
-                    trace[kname] = e0.elapsed_time(e1)
+                    _, tk = timed(lambda: ctx.trace_separatrices(codes, kinds=kb, out=bufs), 1)
+                    trace[kname] = tk[0]
                 del bufs
             else:   # the CSR does not fit: trace the branches in groups of origin planes
                 trace = chunked_trace(ctx, codes, dev, stream, 0.4 * free, sizes)
         except Exception as e:  # noqa: BLE001
             trace = {"error": str(e)[:200]}
         torch.cuda.empty_cache()
+
+    # parity with the CPU oracle at the full size: the committed oracle goldens
+    # (tests/golden/oracle_full_<C>.json, written by tools/oracle_goldens.py from oracle/ only)
+    parity = None
+    gpath = os.path.join(ROOT, "tests", "golden", f"oracle_full_{cfg.name}.json")
+    if args.golden_parity and shape is None and os.path.exists(gpath):
+        from tests import digest as dg
+        gold = json.load(open(gpath))
+        parity = {"crop": list(f.shape), "source": os.path.relpath(gpath, ROOT),
+                  "inputs": gold["input_sha256"] == {"f": hashlib.sha256(f.tobytes()).hexdigest(),
+                                                     "fhat": hashlib.sha256(fh.tobytes()).hexdigest()},
+                  "status": r.status == gold["status"],
+                  "stats": all(r.stats[k] == gold["stats"][k] for k in ("rounds", "n_edited", "n_quantized",
+                                                                         "n_lossless", "n_false_round0",
+                                                                         "false_by_kind_round0")),
+                  "g_bits": dg.digest_t(g.reshape(-1).view(torch.int32)) == gold["g_digest"],
+                  "edits": dg.digest_t(r.edits.reshape(-1, 16).contiguous().view(torch.int64).reshape(-1))
+                  == gold["edits_digest"],
+                  "full_sweeps_equal": rfull.n_edits == r.n_edits and rfull.stats["rounds"] == r.stats["rounds"]}
+        if csr_dig is not None:
+            parity["csr"] = csr_dig == {k: gold["trace_g"][k] for k in ("n_branches", "n_cells", "digests")}
+        parity["all"] = all(v for k, v in parity.items() if isinstance(v, bool))
 
     e2e = None
     if not args.no_e2e:
@@ -453,89 +473,39 @@ def main():
         gh = torch.empty(f.shape, dtype=torch.float32).pin_memory()
         eh = torch.empty((N, 16), dtype=torch.uint8).pin_memory()
         hb = dict(f=ft, fhat=fht, g=g, edits=edits)
-        et = []
-        for _ in range(2):
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            r2 = ctx.correct_host(fp, fhp, xi, bufs=hb, g_host=gh, edits_host=eh)   # copies inside the C call
-            e1.record(stream)
-            torch.cuda.synchronize()
-            et.append(e0.elapsed_time(e1))
+        # the same metric end to end: dmtz_correct_host (full sweeps), pinned host f / fhat
+        # in, g and the edit list back into pinned host memory, every copy inside the call
+        r2, et = timed(lambda: ctx.correct_host(fp, fhp, xi, full_sweeps=True, bufs=hb, g_host=gh,
+                                                edits_host=eh), 2)
         ems = float(np.median(et))
+        r3, et3 = timed(lambda: ctx.correct_host(fp, fhp, xi, bufs=hb, g_host=gh, edits_host=eh), 2)
         e2e = {"value": N * r2.stats["sweeps"] / (ems * 1e-3) / 1e6, "unit": "Mvoxels/s",
                "h2d_bytes_per_step": 2 * 4 * N, "d2h_bytes_per_step": 4 * N + 16 * r2.n_edits, "ms_per_step": ems,
-               "api": "dmtz_correct_host: pinned host f, fhat in; g and the edit list back to pinned host"}
-        # variant: the compressor-side artifact only -- the encoded edit stream comes back
-        # (the decompressor rebuilds g from fhat + stream, dmtz_apply_edits)
-        sh = torch.empty(int(dmtz.lib().dmtz_edit_stream_bound(N)), dtype=torch.uint8).pin_memory()
-        et2 = []
-        for _ in range(2):
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            ft.copy_(fp, non_blocking=True)
-            fht.copy_(fhp, non_blocking=True)
-            r3 = step()
-            sb = ctx.encode_edits(edits[:r3.n_edits], xi, 6, fhat=fht)
-            sh[:sb.numel()].copy_(sb, non_blocking=True)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            et2.append(e0.elapsed_time(e1))
-        ems2 = float(np.median(et2))
-        e2e["stream_variant"] = {"value": N * r3.stats["sweeps"] / (ems2 * 1e-3) / 1e6, "unit": "Mvoxels/s",
-                                 "h2d_bytes_per_step": 2 * 4 * N, "d2h_bytes_per_step": int(sb.numel()),
-                                 "ms_per_step": ems2, "result": "encoded edit stream (dmtz_encode_edits)"}
-        del sb
+               "api": "dmtz_correct_host (full sweeps): pinned host f, fhat in; g + edit list to pinned host",
+               "time_to_fixed_point_ms": float(np.median(et3))}
 
     cpu = None
-    parity = None
     if not args.no_cpu_baseline:
-        s = oracle_sample(f, fh, xi, args.ref_edge)
+        s = oracle_round(f, fh, xi)
         cpu = {"value": s["value"], "unit": "Mvoxels/s", "cores": s["threads"], "kind": "oracle",
-               "sample": f"oracle C-loop to its fixed point on the {s['shape']} crop of {cfg.name} "
-                         f"({s['sweeps']} sweeps in {s['seconds']:.1f} s)"}
-        # parity on the same crop: the CUDA path against the oracle, bit for bit
-        import oracle
-        ref, fc, fhc = s["ref"], s["fc"], s["fhc"]
-        fct, fhct = torch.from_numpy(fc).to(dev), torch.from_numpy(fhc).to(dev)
-        rc = dmtz.correct(fct, fhct, xi)
-        oc, om = oracle.gradient(fc)
-        gc = dmtz.compute_gradient(fct)
-        e = rc.edits_numpy()
-        tr_o = oracle.trace(ref["g"])
-        tr_g = dmtz.trace_separatrices(dmtz.compute_gradient(rc.g))
-        parity = {"crop": s["shape"],
-                  "codes": bool(np.array_equal(gc.cpu().numpy().view(oc.dtype), oc)),
-                  "crit": bool(np.array_equal(dmtz.critical_mask(gc).cpu().numpy().view(np.uint32), om)),
-                  "g_bits": bool(np.array_equal(rc.g.cpu().numpy().view(np.uint32), ref["g"].view(np.uint32))),
-                  "edits": bool(np.array_equal(e["v"], ref["edits"]["v"]) and np.array_equal(e["q"], ref["edits"]["q"])),
-                  "rounds": rc.stats["rounds"] == ref["stats"]["rounds"],
-                  "csr": all(bool(np.array_equal(tr_g[k].cpu().numpy().view(tr_o[k].dtype), tr_o[k])) for k in tr_o)}
+               "sample": f"one oracle C-loop round on the whole {'x'.join(map(str, s['shape']))} field of "
+                         f"{cfg.name} ({s['round_seconds']:.1f} s; literal gradient of g, classification, Eq. 2 "
+                         f"edits; {s['n_false']} false cells, equal to the GPU's round-1 count: "
+                         f"{s['n_false'] == r.stats['n_false_round0']})"}
 
     # the edit list as an artifact (NEXT-2): encode / decode / apply on the device
     codec = None
     try:
         ev = r.edits[:r.n_edits]
-        def _t(fn):
-            fn()
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            out = fn()
-            e1.record(stream)
-            torch.cuda.synchronize()
-            return out, e0.elapsed_time(e1)
-        sb1 = ctx.encode_edits(ev, xi, 6)
-        sb, enc_ms = _t(lambda: ctx.encode_edits(ev, xi, 6, fhat=fht))
-        (dec, _, _), dec_ms = _t(lambda: ctx.decode_edits(sb, fhat=fht))
-        ga, app_ms = _t(lambda: ctx.apply_edits(fht, xi, dec))
+        (sb1, _) = (ctx.encode_edits(ev, xi, 6), None)
+        sb, tenc = timed(lambda: ctx.encode_edits(ev, xi, 6, fhat=fht), 2)
+        (dec, _, _), tdec = timed(lambda: ctx.decode_edits(sb, fhat=fht), 2)
+        ga, tapp = timed(lambda: ctx.apply_edits(fht, xi, dec), 2)
         nbytes = int(sb.numel())
         codec = {"format": "version 2 (lossless values relative to fhat)", "v1_stream_bytes": int(sb1.numel()),
                  "n_edits": r.n_edits, "stream_bytes": nbytes, "bytes_per_edit": nbytes / max(r.n_edits, 1),
-                 "keyvalue_float_bytes": 12 * r.n_edits, "edit_ratio": r.n_edits / N,
-                 "stream_fraction_of_original": nbytes / (4 * N),
-                 "encode_ms": enc_ms, "decode_ms": dec_ms, "apply_ms": app_ms,
+                 "edit_ratio": r.n_edits / N, "stream_fraction_of_original": nbytes / (4 * N),
+                 "encode_ms": tenc[-1], "decode_ms": tdec[-1], "apply_ms": tapp[-1],
                  "apply_matches_g": bool(torch.equal(ga.view(torch.int32), g.view(torch.int32)))}
         del sb, sb1, dec, ga
     except Exception as e:  # noqa: BLE001
@@ -560,20 +530,39 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{cfg.name} {cfg.family} {'x'.join(map(str, f.shape))} rel eps {cfg.eps}",
-                   "xi": xi, "q_max": 6, "q_cap": 6, "tier": 2, "sweeps_per_step": sweeps, "rounds": st["rounds"],
-                   "mode": "default: dirty frontier + exact change skipping (bit-identical to full_sweeps=1)",
+                   "step": "C-loop to its fixed point, every round a full sweep (full_sweeps=1)",
+                   "value": "N x sweeps / step time = full-sweep round throughput (SURVEY §8(d-1))",
+                   "xi": xi, "q_max": 6, "q_cap": 6, "tier": 2, "sweeps_per_step": sweeps,
+                   "rounds": rfull.stats["rounds"],
                    "l2": (f"inputs larger than L2 (2 x {4 * N / 1e6:.0f} MB)" if 8 * N > 126e6
-                          else f"inputs fit in L2 (2 x {4 * N / 1e6:.1f} MB), not flushed between steps"), "parallelism": "1 GPU"},
-        "roofline": roof, "roofline_screen": roof_screen, "hbm_per_iteration": hbm_iter, "cpu_baseline": cpu, "e2e": e2e, "time_to_fixed_point": frontier,
-        "full_recompute": full_recompute, "trace": trace, "sloop": sloop, "codec": codec,
-        "gpu_launches": st["launches"],
+                          else f"inputs fit in L2 (2 x {4 * N / 1e6:.1f} MB), not flushed between steps"),
+                   "parallelism": "1 GPU"},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": rfull.stats["launches"],
         "clocks": clk.summary(),
+        "parity_vs_oracle": parity,
+        "full_sweep_mvox_s": value,
+        "time_to_fixed_point": frontier,
+        "roofline_alu": roof_alu,
+        "trace": trace,
         "stats": {k: st[k] for k in ("rounds", "sweeps", "n_edited", "n_quantized", "n_lossless", "n_false_round0",
                                      "false_by_kind_round0")},
+        "codec": codec,
         "gen_seconds": t_gen,
-        "parity_vs_oracle": parity,
-        "input_sha256": {"f": hashlib.sha256(f.tobytes()).hexdigest(), "fhat": hashlib.sha256(fh.tobytes()).hexdigest()},
     }
+    detail = dict(line, sloop=sloop,
+                  input_sha256={"f": hashlib.sha256(f.tobytes()).hexdigest(),
+                                "fhat": hashlib.sha256(fh.tobytes()).hexdigest()})
+    dpath = args.detail or (os.path.join(ROOT, "gpurun_out", "bench_detail.json")
+                            if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else None)
+    if dpath and rank == 0:
+        with open(dpath, "w") as fh_:
+            json.dump(detail, fh_, indent=1)
+    if sloop is not None:   # compact summary in the line; the full per-tier dicts in the detail file
+        line["sloop_ms"] = {n: {t: v.get("time_to_fixed_point_ms") for t, v in d.items() if t.startswith("tier")}
+                            for n, d in sloop.items() if isinstance(d, dict)}
     if rank == 0:
         print(json.dumps(line), flush=True)
 

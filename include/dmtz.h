@@ -384,6 +384,13 @@ dmtz_status dmtz_slab_end(dmtz_ctx* ctx, const dmtz_slab* slab, void* workspace,
 const char* dmtz_status_string(dmtz_status s);
 const char* dmtz_last_error(void);
 int dmtz_version(void);
+/* Diagnostics of the calling thread's last dmtz_trace_separatrices(_range) call: out[i]
+ * (i < n, n <= 10) = connectors handled at escalation level i in its count pass --
+ * [0] all connectors (one thread each, shared-memory queue), [1] those that overflowed
+ * into one warp each, [2], [3], ... those that overflowed into the block-parallel BFS
+ * with slots growing per level.  Host pointer; returns
+ * DMTZ_E_ARG for a NULL out. */
+int dmtz_last_trace_levels(int64_t* out, int n);
 
 #ifdef __cplusplus
 }

@@ -67,6 +67,10 @@ def lib():
         L.dmtz_oracle_correct.argtypes = [P, P, P, ctypes.c_float, ctypes.c_int32, ctypes.c_int32,
                                           ctypes.c_int32, i64, P, P, P, i64, P,
                                           ctypes.POINTER(_Stats)]
+        L.dmtz_oracle_correct_ex.argtypes = [P, P, P, ctypes.c_float, ctypes.c_int32, ctypes.c_int32,
+                                             ctypes.c_int32, i64, ctypes.c_int32, P, P, P, i64, P,
+                                             ctypes.POINTER(_Stats), P, P, i64]
+        L.dmtz_oracle_trace_digest.argtypes = [P, P, ctypes.c_uint32, P, P, P]
         L.dmtz_oracle_preserve.argtypes = [P, P, P, ctypes.c_float, ctypes.c_int32, ctypes.c_int32,
                                            ctypes.c_int32, i64, P, P, P, i64, P,
                                            ctypes.POINTER(_Stats), ctypes.POINTER(_SStats)]
@@ -77,7 +81,7 @@ def lib():
                                              i64, i64, i64, i64, P, P, P, P]
         for fn in ("dmtz_oracle_gradient", "dmtz_oracle_complex_info", "dmtz_oracle_cell_counts",
                    "dmtz_oracle_correct", "dmtz_oracle_trace", "dmtz_oracle_num_threads", "dmtz_oracle_slab_round",
-                   "dmtz_oracle_preserve"):
+                   "dmtz_oracle_preserve", "dmtz_oracle_correct_ex", "dmtz_oracle_trace_digest"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -134,8 +138,14 @@ def cell_counts(shape):
 
 
 def correct(f: np.ndarray, fhat: np.ndarray, xi: float, q_max: int = 6, q_cap: int | None = None,
-            tier: int = 2, max_rounds: int = 0, edits_capacity: int | None = None):
-    """Literal synchronous C-loop.  Returns dict(status, g, state, edits, stats)."""
+            tier: int = 2, max_rounds: int = 0, edits_capacity: int | None = None,
+            frontier: bool = False, round_log: bool = False):
+    """Literal synchronous C-loop.  Returns dict(status, g, state, edits, stats).
+
+    ``frontier``: after round 1 re-pair and classify only the cells anchored within
+    [-2,1]^D of a target of the previous round (``dmtz_oracle_correct_ex``; equal to
+    the full loop, tests/test_oracle_frontier.py).  ``round_log``: also return the
+    number of false cells of every round (``false_per_round``)."""
     f = np.ascontiguousarray(f, dtype=np.float32)
     fhat = np.ascontiguousarray(fhat, dtype=np.float32)
     assert f.shape == fhat.shape
@@ -149,14 +159,22 @@ def correct(f: np.ndarray, fhat: np.ndarray, xi: float, q_max: int = 6, q_cap: i
     edits = np.zeros(max(cap, 1), dtype=EDIT_DTYPE)
     ne = ctypes.c_int64()
     stats = _Stats()
-    st = lib().dmtz_oracle_correct(_p(d), _p(f), _p(fhat), ctypes.c_float(xi), q_max, q_cap, tier,
-                                   max_rounds, _p(g), _p(state), _p(edits), cap,
-                                   ctypes.byref(ne), ctypes.byref(stats))
+    log_cap = 1 << 20 if round_log else 0
+    log = np.full(max(log_cap, 1), -2, np.int64)
+    sec = np.zeros(max(log_cap, 1), np.float64)
+    st = lib().dmtz_oracle_correct_ex(_p(d), _p(f), _p(fhat), ctypes.c_float(xi), q_max, q_cap, tier,
+                                      max_rounds, int(bool(frontier)), _p(g), _p(state), _p(edits), cap,
+                                      ctypes.byref(ne), ctypes.byref(stats), _p(log), _p(sec), log_cap)
     out = {k: getattr(stats, k) for k in STATS_FIELDS}
     out["false_by_kind_round0"] = list(stats.false_by_kind_round0)
     out["status"] = st
-    return dict(status=st, g=g, state=state, edits=edits[:min(ne.value, cap)].copy(),
-                n_edits=ne.value, stats=out)
+    res = dict(status=st, g=g, state=state, edits=edits[:min(ne.value, cap)].copy(),
+               n_edits=ne.value, stats=out)
+    if round_log:
+        nr = int((log != -2).sum())
+        res["false_per_round"] = [int(x) for x in log[:nr]]
+        res["round_seconds"] = [float(x) for x in sec[:nr]]
+    return res
 
 
 def preserve(f: np.ndarray, fhat: np.ndarray, xi: float, tier: int = 4, q_max: int = 6,
@@ -227,6 +245,20 @@ def trace(field: np.ndarray, kinds: int = KIND_DESC | KIND_ASC | KIND_CONN,
         raise RuntimeError(f"oracle trace status {st}")
     return dict(offsets=off[:nb + 1], cells=cells[:nc], origin=origin[:nb], terminal=term[:nb],
                 kind=kind[:nb])
+
+
+def trace_digest(field: np.ndarray, kinds: int = KIND_DESC | KIND_ASC | KIND_CONN):
+    """The literal trace of ``field`` without storing it: (n_branches, n_cells, digests)
+    with digests = {offsets, cells, origin, terminal, kind} as defined in tests/digest.py."""
+    field = np.ascontiguousarray(field, dtype=np.float32)
+    d = _dims(field.shape)
+    dig = np.zeros(5, np.uint64)
+    nb, nc = ctypes.c_int64(), ctypes.c_int64()
+    st = lib().dmtz_oracle_trace_digest(_p(d), _p(field), kinds, _p(dig), ctypes.byref(nb), ctypes.byref(nc))
+    if st:
+        raise RuntimeError(f"oracle trace_digest status {st}")
+    names = ("offsets", "cells", "origin", "terminal", "kind")
+    return nb.value, nc.value, {k: int(v) for k, v in zip(names, dig)}
 
 
 def slab_round(f, fhat, xi, g, state, anchor_planes, owned_planes, q_max=6, q_cap=None, tier=2):

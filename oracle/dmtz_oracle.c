@@ -340,6 +340,72 @@ static inline int cell_exists(const cx_t* cx, int64_t A, int ti) {
   int64_t vs[4];
   return cell_vertices(cx, A, ti, vs);
 }
+
+/* Frontier update of a gradient (the oracle's frontier mode, used for the full-size
+ * C3/C4 goldens).  The pairing of a cell anchored at A reads the
+ * values of A + [-1,1]^D only (the cell and its link), and whether a cell
+ * is paired down reads the pairings of its facets, anchored in A + {0,1}^D.  So
+ * when the values changed only at vertices v with a flag in `D` dilated by
+ * [-2,1]^D (i.e. D[A] = 1 for every anchor A with a changed vertex in
+ * A + [-1,2]^D), every cell whose pair can differ is anchored where D[A] = 1, and
+ * recomputing exactly those cells -- with the literal rule, dimensions ascending,
+ * a cell paired with a facet not paired again -- gives the gradient a
+ * full recomputation gives (tests/test_oracle_frontier.py checks that claim
+ * against full mode bit for bit).  dn of a recomputed cell is re-derived from
+ * its facets' pairs (the facets may lie outside D and keep their pairs). */
+static void gradient_update(const cx_t* cx, const float* f, grad_t* G, const uint8_t* D) {
+  const int T = cx->T;
+  for (int d = 0; d <= cx->top; d++) {
+    int t0 = cx->first_of_dim[d], t1 = cx->first_of_dim[d + 1];
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t A = 0; A < cx->N; A++) {
+      if (!D[A]) continue;
+      for (int ti = t0; ti < t1; ti++) {
+        size_t i = (size_t)A * T + ti;
+        G->dn[i] = -1;
+        if (d == 0 || !cell_exists(cx, A, ti)) continue;
+        for (int k = 0; k <= d; k++) {
+          int ft;
+          int64_t C = facet_cell(cx, A, ti, k, &ft);
+          int s = G->up[(size_t)C * T + ft];
+          if (s < 0) continue;
+          int bt;
+          int64_t B = cofacet_cell(cx, C, ft, s, &bt);
+          if (B == A && bt == ti) G->dn[i] = (int8_t)k;
+        }
+      }
+    }
+    if (d == cx->top) break;
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t A = 0; A < cx->N; A++) {
+      if (!D[A]) continue;
+      for (int ti = t0; ti < t1; ti++) {
+        size_t i = (size_t)A * T + ti;
+        G->up[i] = -1;
+        if (G->dn[i] >= 0) continue;
+        int s = pair_cell(cx, f, A, ti);
+        if (s >= 0) G->up[i] = (int8_t)s;
+      }
+    }
+  }
+}
+
+/* D[A] = 1 iff some vertex with T[v] = 1 lies in A + [-1,2]^D (see above). */
+static void dilate_targets(const cx_t* cx, const uint8_t* T, uint8_t* D) {
+  int zlo = cx->D == 3 ? -1 : 0, zhi = cx->D == 3 ? 2 : 0;
+#pragma omp parallel for schedule(static)
+  for (int64_t A = 0; A < cx->N; A++) {
+    co_t a = coords(cx, A);
+    uint8_t hit = 0;
+    for (int dz = zlo; dz <= zhi && !hit; dz++)
+      for (int dy = -1; dy <= 2 && !hit; dy++)
+        for (int dx = -1; dx <= 2 && !hit; dx++) {
+          int64_t x = a.x + dx, y = a.y + dy, z = a.z + dz;
+          if (inside(cx, x, y, z) && T[vid(cx, x, y, z)]) hit = 1;
+        }
+    D[A] = hit;
+  }
+}
 static inline int is_crit(const cx_t* cx, const grad_t* G, int64_t A, int ti) {
   size_t i = (size_t)A * cx->T + ti;
   return G->up[i] < 0 && G->dn[i] < 0 && cell_exists(cx, A, ti);
@@ -500,11 +566,12 @@ static int64_t target_of(const cx_t* cx, const float* f, const grad_t* Gf, const
  * P:140-141), target set T (a set: each vertex at most once per round).
  * Returns |F| (or -1 on internal error); kinds[8] accumulates counts. */
 static int64_t classify(const cx_t* cx, const float* f, const grad_t* Gf, const grad_t* Gg,
-                        int tier, uint8_t* T, int64_t* kinds) {
+                        int tier, uint8_t* T, int64_t* kinds, const uint8_t* D) {
   int64_t nF = 0, bad = 0;
   int64_t kk[8] = {0};
 #pragma omp parallel for schedule(dynamic, 4096) reduction(+ : nF, bad) reduction(+ : kk[:8])
   for (int64_t A = 0; A < cx->N; A++) {
+    if (D && !D[A]) continue;  /* frontier mode: no false cell is anchored outside D */
     for (int ti = 0; ti < cx->T; ti++) {
       int d = cx->t[ti].dim;
       if (tier == 1 && d != 0 && d != cx->top) continue;
@@ -524,10 +591,20 @@ static int64_t classify(const cx_t* cx, const float* f, const grad_t* Gf, const 
   return bad ? -1 : nF;
 }
 
-int dmtz_oracle_correct(const int64_t* dims, const float* f, const float* fhat, float xi,
-                        int32_t q_max, int32_t q_cap, int32_t tier, int64_t max_rounds,
-                        float* g_out, uint32_t* state_out, or_edit* edits, int64_t edits_capacity,
-                        int64_t* n_edits, or_stats* stats) {
+/* frontier = 0: every round recomputes the whole gradient of g and classifies every
+ * cell (the literal loop).  frontier = 1: round 1 does; round r > 1 recomputes the
+ * cells anchored in D_r = { A : a target of round r-1 lies in A + [-1,2]^D } (the
+ * only cells whose pair can change, see gradient_update) and classifies the cells
+ * anchored in D_r: a false cell of round r was either false in round r-1 -- it is
+ * anchored within [-2,1]^D of its own target (its target is one of its vertices,
+ * of its pair's vertices or of its facet's pair's vertices) -- or became false
+ * because a vertex it reads (A + [-1,2]^D) changed, and every changed vertex was
+ * a target.  Checked equal to frontier = 0 in tests/test_oracle_frontier.py. */
+int dmtz_oracle_correct_ex(const int64_t* dims, const float* f, const float* fhat, float xi,
+                           int32_t q_max, int32_t q_cap, int32_t tier, int64_t max_rounds, int32_t frontier,
+                           float* g_out, uint32_t* state_out, or_edit* edits, int64_t edits_capacity,
+                           int64_t* n_edits, or_stats* stats, int64_t* round_log, double* round_sec,
+                           int64_t round_log_cap) {
   memset(stats, 0, sizeof *stats);
   *n_edits = 0;
   int st = check_dims(dims);
@@ -556,13 +633,24 @@ int dmtz_oracle_correct(const int64_t* dims, const float* f, const float* fhat, 
     stats->status = OR_E_ARG; return OR_E_ARG;
   }
   for (int64_t v = 0; v < N; v++) { lb[v] = lower_bound_ru(f[v], xi); g_out[v] = fhat[v]; }
+  uint8_t* Dm = frontier ? (uint8_t*)malloc(N) : NULL;
+  if (frontier && !Dm) { stats->status = OR_E_ARG; return OR_E_ARG; }
   gradient(&cx, f, &Gf);
   int status = OR_OK;
   for (int64_t round = 1;; round++) {
-    gradient(&cx, g_out, &Gg);
+#ifdef _OPENMP
+    double t_round0 = omp_get_wtime();  /* instrumentation only: wall time of each round */
+#endif
+    if (round == 1 || !frontier) {
+      gradient(&cx, g_out, &Gg);
+    } else {
+      dilate_targets(&cx, T, Dm);
+      gradient_update(&cx, g_out, &Gg, Dm);
+    }
     memset(T, 0, N);
     int64_t kinds[8] = {0};
-    int64_t nF = classify(&cx, f, &Gf, &Gg, tier, T, kinds);
+    int64_t nF = classify(&cx, f, &Gf, &Gg, tier, T, kinds, (round == 1 || !frontier) ? NULL : Dm);
+    if (round_log && round - 1 < round_log_cap) round_log[round - 1] = nF;
     if (nF < 0) { status = OR_E_INTERNAL; break; }
     if (round == 1) {
       stats->n_false_round0 = nF;
@@ -585,6 +673,9 @@ int dmtz_oracle_correct(const int64_t* dims, const float* f, const float* fhat, 
       g_out[v] = lb[v];
       lossless[v] = 1;
     }
+#ifdef _OPENMP
+    if (round_sec && round - 1 < round_log_cap) round_sec[round - 1] = omp_get_wtime() - t_round0;
+#endif
     if (!changed) { status = OR_E_STUCK; break; }
     if (round == max_rounds) { status = OR_E_ITER_CAP; break; }
   }
@@ -603,9 +694,17 @@ int dmtz_oracle_correct(const int64_t* dims, const float* f, const float* fhat, 
   *n_edits = ne;
   if (status == OR_OK && edits && ne > edits_capacity) status = OR_E_CAPACITY;
   stats->status = status;
-  free(lb); free(q); free(lossless); free(T);
+  free(lb); free(q); free(lossless); free(T); free(Dm);
   grad_free(&Gf); grad_free(&Gg);
   return status;
+}
+
+int dmtz_oracle_correct(const int64_t* dims, const float* f, const float* fhat, float xi,
+                        int32_t q_max, int32_t q_cap, int32_t tier, int64_t max_rounds,
+                        float* g_out, uint32_t* state_out, or_edit* edits, int64_t edits_capacity,
+                        int64_t* n_edits, or_stats* stats) {
+  return dmtz_oracle_correct_ex(dims, f, fhat, xi, q_max, q_cap, tier, max_rounds, 0, g_out, state_out,
+                                edits, edits_capacity, n_edits, stats, NULL, NULL, 0);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -625,17 +724,40 @@ static uint64_t cell_id(const cx_t* cx, int64_t A, int ti) {
 typedef struct {
   int64_t cap_b, cap_c, nb, nc;
   int64_t* off; uint64_t* cells; uint64_t* origin; uint64_t* terminal; uint8_t* kind;
+  uint64_t* dig;  /* non-NULL: digest mode -- nothing is stored, see csr_digest_mix */
 } csr_t;
 
+/* Digest mode (for the full-size goldens, whose CSR does not fit in host memory):
+ * instead of storing array X, accumulate sum_i mix(X[i] ^ (i * 0x9E3779B97F4A7C15))
+ * mod 2^64, mix = the splitmix64 finalizer.  dig[0..4] = offsets, cells, origin,
+ * terminal, kind.  A checksum of the output, not part of the method; the tests
+ * compute the same sums over the GPU's arrays (tests/digest.py). */
+static uint64_t csr_digest_mix(uint64_t x, uint64_t i) {
+  uint64_t z = x ^ (i * 0x9E3779B97F4A7C15ull);
+  z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27; z *= 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
 static void csr_begin(csr_t* o, uint64_t origin, uint8_t kind) {
+  if (o->dig) {
+    o->dig[2] += csr_digest_mix(origin, (uint64_t)o->nb);
+    o->dig[4] += csr_digest_mix(kind, (uint64_t)o->nb);
+    return;
+  }
   if (o->nb < o->cap_b) { o->off[o->nb] = o->nc; o->origin[o->nb] = origin; o->kind[o->nb] = kind; }
 }
 static void csr_push(csr_t* o, uint64_t c) {
-  if (o->nc < o->cap_c) o->cells[o->nc] = c;
+  if (o->dig) o->dig[1] += csr_digest_mix(c, (uint64_t)o->nc);
+  else if (o->nc < o->cap_c) o->cells[o->nc] = c;
   o->nc++;
 }
 static void csr_end(csr_t* o, uint64_t terminal) {
-  if (o->nb < o->cap_b) { o->terminal[o->nb] = terminal; o->off[o->nb + 1] = o->nc; }
+  if (o->dig) {
+    o->dig[3] += csr_digest_mix(terminal, (uint64_t)o->nb);
+    o->dig[0] += csr_digest_mix((uint64_t)o->nc, (uint64_t)o->nb + 1);
+  } else if (o->nb < o->cap_b) {
+    o->terminal[o->nb] = terminal; o->off[o->nb + 1] = o->nc;
+  }
   o->nb++;
 }
 
@@ -686,7 +808,8 @@ static int trace_grad(const cx_t* cxp, const grad_t* Gp, uint32_t kinds, csr_t* 
   const grad_t G = *Gp;
   csr_t* po = op;
 #define o (*po)
-  if (o.cap_b > 0) o.off[0] = 0;
+  if (o.dig) o.dig[0] += csr_digest_mix(0, 0);  /* offsets[0] = 0 */
+  else if (o.cap_b > 0) o.off[0] = 0;
   int64_t maxsteps = cx.N * cx.T + 1;
   int err = 0;
   int T = cx.T;
@@ -798,6 +921,25 @@ static int trace_grad(const cx_t* cxp, const grad_t* Gp, uint32_t kinds, csr_t* 
   return err ? OR_E_INTERNAL : OR_OK;
 }
 
+/* The trace in digest mode: n_branches, n_cells, per-kind branch counts are not
+ * separated (the kind digest covers them); dig[5] as in csr_t. */
+int dmtz_oracle_trace_digest(const int64_t* dims, const float* field, uint32_t kinds, uint64_t* dig,
+                             int64_t* n_branches, int64_t* n_cells) {
+  int st = check_dims(dims);
+  if (st) return st;
+  cx_t cx; build_complex(&cx, dims[0], dims[1], dims[2]);
+  grad_t G;
+  if (!grad_alloc(&cx, &G)) return OR_E_ARG;
+  gradient(&cx, field, &G);
+  for (int k = 0; k < 5; k++) dig[k] = 0;
+  csr_t o = {0, 0, 0, 0, NULL, NULL, NULL, NULL, NULL, dig};
+  int err = trace_grad(&cx, &G, kinds, &o, 0);
+  grad_free(&G);
+  *n_branches = o.nb;
+  *n_cells = o.nc;
+  return err;
+}
+
 int dmtz_oracle_trace(const int64_t* dims, const float* field, uint32_t kinds,
                       int64_t cap_branches, int64_t cap_cells, int64_t* branch_offsets,
                       uint64_t* cells, uint64_t* origin, uint64_t* terminal, uint8_t* kind,
@@ -808,7 +950,7 @@ int dmtz_oracle_trace(const int64_t* dims, const float* field, uint32_t kinds,
   grad_t G;
   if (!grad_alloc(&cx, &G)) return OR_E_ARG;
   gradient(&cx, field, &G);
-  csr_t o = {cap_branches, cap_cells, 0, 0, branch_offsets, cells, origin, terminal, kind};
+  csr_t o = {cap_branches, cap_cells, 0, 0, branch_offsets, cells, origin, terminal, kind, NULL};
   if (cap_branches > 0) branch_offsets[0] = 0;
   int err = trace_grad(&cx, &G, kinds, &o, 0);
   grad_free(&G);
@@ -993,7 +1135,7 @@ int dmtz_oracle_preserve(const int64_t* dims, const float* f, const float* fhat,
     gradient(&cx, g_out, &Gg);
     memset(T, 0, N);
     int64_t kinds[8] = {0};
-    int64_t nF = classify(&cx, f, &Gf, &Gg, ctier, T, kinds);
+    int64_t nF = classify(&cx, f, &Gf, &Gg, ctier, T, kinds, NULL);
     if (nF < 0) { status = OR_E_INTERNAL; break; }
     if (round == 1) {
       stats->n_false_round0 = nF;

@@ -121,6 +121,8 @@ def _load():
     L.dmtz_status_string.argtypes = [i32]
     L.dmtz_status_string.restype = ctypes.c_char_p
     L.dmtz_last_error.restype = ctypes.c_char_p
+    L.dmtz_last_trace_levels.argtypes = [P, i32]
+    L.dmtz_last_trace_levels.restype = ctypes.c_int
     for fn in ("dmtz_ctx_create", "dmtz_compute_gradient", "dmtz_critical_mask", "dmtz_correct", "dmtz_correct_host",
                "dmtz_trace_separatrices", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end",
                "dmtz_slab_halo", "dmtz_trace_separatrices_range", "dmtz_preserve", "dmtz_slab_round_async",
@@ -149,7 +151,14 @@ EXPORTED = ("dmtz_ctx_create", "dmtz_ctx_destroy", "dmtz_workspace_bytes", "dmtz
             "dmtz_slab_halo", "dmtz_trace_separatrices_range", "dmtz_slab_round_async", "dmtz_preserve_sep_bytes",
             "dmtz_preserve",
             "dmtz_edit_stream_bound", "dmtz_encode_edits", "dmtz_decode_edits", "dmtz_apply_edits",
-            "dmtz_critical_prf", "dmtz_separatrix_prf")
+            "dmtz_critical_prf", "dmtz_separatrix_prf", "dmtz_last_trace_levels")
+
+
+def last_trace_levels() -> list:
+    """Connectors per escalation level of this thread's last trace (dmtz_last_trace_levels)."""
+    out = (ctypes.c_int64 * 10)()
+    _check(_lib.dmtz_last_trace_levels(out, 10))
+    return list(out)
 
 
 def lib():
@@ -257,7 +266,13 @@ class Context:
             cap = self.N if edits_capacity is None else int(edits_capacity)
             edits = torch.empty((max(cap, 1), 16), dtype=torch.uint8, device=f.device)
         else:
-            cap = edits.shape[0] if edits_capacity is None else int(edits_capacity)
+            if (edits.dtype != torch.uint8 or edits.dim() != 2 or edits.shape[1] != 16 or not edits.is_contiguous()
+                    or edits.device != f.device):
+                raise ValueError("edits must be a contiguous (n, 16) uint8 tensor on f's device")
+            cap = edits.shape[0] if edits_capacity is None else min(int(edits_capacity), edits.shape[0])
+        if g_out.dtype != torch.float32 or tuple(g_out.shape) != self.shape or g_out.device != f.device \
+                or not g_out.is_contiguous():
+            raise ValueError("g_out must be a contiguous float32 tensor of the field's shape on f's device")
         opts = _Opts(float(xi), int(q_max), int(q_max if q_cap is None else q_cap), int(tier), int(max_rounds),
                      1 if full_sweeps else 0, 1 if profile else 0)
         ne = ctypes.c_int64()

@@ -47,19 +47,33 @@ struct dmtz_ctx {
   int D;
   int device;
   int rank, world;
-  Counters* host_cnt;  // pinned
-  cudaEvent_t ev[3];   // sweep timing (opts.profile): screen | decode
+  Counters* host_cnt = nullptr;  // pinned
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // sweep timing (opts.profile): screen | decode
   int verbose;         // DMTZ_VERBOSE=1: per-round counters on stderr (host-driven rounds)
   int no_graph;        // DMTZ_NO_GRAPH=1: host-driven rounds instead of the CUDA-graph loop
-  LoopState* host_ls;  // pinned
-  struct LoopGraph* graph;
-  cudaStream_t cap_stream;  // private stream the loop body is captured on (the caller's may be the legacy stream)
+  LoopState* host_ls = nullptr;  // pinned
+  struct LoopGraph* graph = nullptr;
+  cudaStream_t cap_stream = nullptr;  // private stream the loop body is captured on (the caller's may be the legacy stream)
   uint32_t* sdirty = nullptr;  // dmtz_preserve: per-anchor "code changed since the last S-round" bits
+};
+
+// Every entry point runs on the context's device and restores the caller's current
+// device on return (the caller's thread may have another device current).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(const dmtz_ctx* c) {
+    if (c && cudaGetDevice(&prev) == cudaSuccess && prev != c->device) cudaSetDevice(c->device);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
 };
 
 namespace {
 
 thread_local char g_err[512] = "";
+thread_local int64_t g_trace_levels[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 
 void set_err(const char* fmt, ...) {
   va_list ap;
@@ -548,10 +562,15 @@ dmtz_status trace_into(dmtz_ctx* c, char* ws, const Layout& L, const void* codes
   a.cap_b = cap_b;
   a.cap_c = cap_c;
   cudaError_t e = run_trace<D>(a, s);
+  for (int i = 0; i < 10; i++) g_trace_levels[i] = a.level_counts[i];
   if (e != cudaSuccess) { set_err("trace: %s", cudaGetErrorString(e)); return DMTZ_E_CUDA; }
   *nb = a.n_branches;
   *nc = a.n_cells;
   if (a.n_internal) { set_err("trace: cycle or inconsistent gradient"); return DMTZ_E_INTERNAL; }
+  if (a.n_overflow) {
+    set_err("trace: %lld connector BFS larger than the workspace scratch", (long long)a.n_overflow);
+    return DMTZ_E_CAPACITY;
+  }
   if (a.n_branches > cap_b || a.n_cells > cap_c) {
     set_err("separatrices need %lld branches / %lld cells", (long long)a.n_branches, (long long)a.n_cells);
     return DMTZ_E_CAPACITY;
@@ -783,6 +802,12 @@ int dmtz_version(void) { return 1; }
 
 const char* dmtz_last_error(void) { return g_err; }
 
+int dmtz_last_trace_levels(int64_t* out, int n) {
+  if (!out || n < 0) return DMTZ_E_ARG;
+  for (int i = 0; i < n && i < 10; i++) out[i] = g_trace_levels[i];
+  return DMTZ_OK;
+}
+
 const char* dmtz_status_string(dmtz_status s) {
   switch (s) {
     case DMTZ_OK: return "ok";
@@ -813,6 +838,11 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
     return DMTZ_E_DIMS;
   }
   if (world != 1 || rank != 0 || nccl_id != nullptr) { set_err("world must be 1 (slab layer drives per-rank contexts)"); return DMTZ_E_ARG; }
+  struct RestoreDevice {
+    int prev = -1;
+    ~RestoreDevice() { if (prev >= 0) cudaSetDevice(prev); }
+  } restore_;
+  if (cudaGetDevice(&restore_.prev) != cudaSuccess) restore_.prev = -1;
   CK(cudaSetDevice(cuda_device));
   dmtz_ctx* c = new (std::nothrow) dmtz_ctx();
   if (!c) return DMTZ_E_OOM;
@@ -831,10 +861,18 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
   c->no_graph = ng && ng[0] == '1';
   cudaError_t e = cudaMallocHost((void**)&c->host_cnt, sizeof(Counters) * 2);
   if (e == cudaSuccess) e = cudaMallocHost((void**)&c->host_ls, sizeof(LoopState));
-  if (e != cudaSuccess) { delete c; set_err("cudaMallocHost: %s", cudaGetErrorString(e)); return DMTZ_E_CUDA; }
+  if (e != cudaSuccess) {
+    set_err("cudaMallocHost: %s", cudaGetErrorString(e));
+    dmtz_ctx_destroy(c);
+    return DMTZ_E_CUDA;
+  }
   for (int i = 0; i < 3; i++) {
     e = cudaEventCreate(&c->ev[i]);
-    if (e != cudaSuccess) { set_err("cudaEventCreate: %s", cudaGetErrorString(e)); return DMTZ_E_CUDA; }
+    if (e != cudaSuccess) {
+      set_err("cudaEventCreate: %s", cudaGetErrorString(e));
+      dmtz_ctx_destroy(c);
+      return DMTZ_E_CUDA;
+    }
   }
   *out = c;
   return DMTZ_OK;
@@ -842,11 +880,13 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
 
 void dmtz_ctx_destroy(dmtz_ctx* c) {
   if (!c) return;
+  DeviceGuard dg_(c);
   if (c->graph) { c->graph->reset(); delete c->graph; }
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
-  cudaFreeHost(c->host_cnt);
-  cudaFreeHost(c->host_ls);
-  for (int i = 0; i < 3; i++) cudaEventDestroy(c->ev[i]);
+  if (c->host_cnt) cudaFreeHost(c->host_cnt);
+  if (c->host_ls) cudaFreeHost(c->host_ls);
+  for (int i = 0; i < 3; i++)
+    if (c->ev[i]) cudaEventDestroy(c->ev[i]);
   delete c;
 }
 
@@ -856,6 +896,7 @@ size_t dmtz_workspace_bytes(const dmtz_ctx* c, const dmtz_correct_opts*) {
 }
 
 dmtz_status dmtz_compute_gradient(dmtz_ctx* c, const float* field, void* codes, void*, dmtz_stream_t stream) {
+  DeviceGuard dg_(c);
   if (!c || !field || !codes) { set_err("NULL argument"); return DMTZ_E_ARG; }
   cudaStream_t s = (cudaStream_t)stream;
   if (c->D == 3) launch_codes<3>(c->g, field, codes, 0, c->g.nz, s);
@@ -865,6 +906,7 @@ dmtz_status dmtz_compute_gradient(dmtz_ctx* c, const float* field, void* codes, 
 }
 
 dmtz_status dmtz_critical_mask(dmtz_ctx* c, const void* codes, uint32_t* crit, dmtz_stream_t stream) {
+  DeviceGuard dg_(c);
   if (!c || !codes || !crit) { set_err("NULL argument"); return DMTZ_E_ARG; }
   cudaStream_t s = (cudaStream_t)stream;
   dim3 grid = anchor_grid(c->g, 0, c->g.nz, 128);
@@ -877,6 +919,7 @@ dmtz_status dmtz_critical_mask(dmtz_ctx* c, const void* codes, uint32_t* crit, d
 dmtz_status dmtz_correct(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
                          void* workspace, size_t workspace_bytes, float* g_out, dmtz_edit* edits,
                          int64_t edits_capacity, int64_t* n_edits, dmtz_stats* st, dmtz_stream_t stream) {
+  DeviceGuard dg_(c);
   if (!c || !f || !fhat || !o || !workspace || !g_out || !n_edits || !st || (edits_capacity > 0 && !edits) ||
       edits_capacity < 0) {
     set_err("NULL argument");
@@ -908,6 +951,7 @@ dmtz_status dmtz_correct_host(dmtz_ctx* c, const float* f_host, const float* fha
                               void* workspace, size_t workspace_bytes, float* f_dev, float* fhat_dev, float* g_dev,
                               dmtz_edit* edits_dev, int64_t edits_capacity, float* g_host, dmtz_edit* edits_host,
                               int64_t* n_edits, dmtz_stats* st, dmtz_stream_t stream) {
+  DeviceGuard dg_(c);
   if (!c || !f_host || !fhat_host || !f_dev || !fhat_dev || !n_edits || !st ||
       (edits_host && edits_capacity > 0 && !edits_dev)) {
     set_err("NULL argument");
@@ -943,6 +987,7 @@ static dmtz_status slab_check(dmtz_ctx* c, const dmtz_slab* sl, void* ws, size_t
 
 dmtz_status dmtz_slab_begin(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
                             const dmtz_slab* sl, void* workspace, size_t wsb, float* g_out, dmtz_stream_t stream) {
+  DeviceGuard dg_(c);
   Layout L;
   dmtz_status st = slab_check(c, sl, workspace, wsb, &L);
   if (st) return st;
@@ -968,6 +1013,7 @@ dmtz_status dmtz_slab_begin(dmtz_ctx* c, const float* f, const float* fhat, cons
 dmtz_status dmtz_slab_round(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
                             const dmtz_slab* sl, void* workspace, size_t wsb, float* g_out, int64_t round,
                             int64_t* counters, int64_t* kinds, dmtz_stream_t stream) {
+  DeviceGuard dg_(c);
   Layout L;
   dmtz_status st = slab_check(c, sl, workspace, wsb, &L);
   if (st) return st;
@@ -1002,6 +1048,7 @@ dmtz_status dmtz_slab_round(dmtz_ctx* c, const float* f, const float* fhat, cons
 dmtz_status dmtz_slab_round_async(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
                                   const dmtz_slab* sl, void* workspace, size_t wsb, float* g_out, int64_t round,
                                   int64_t* dcounters, dmtz_stream_t stream) {
+  DeviceGuard dg_(c);
   Layout L;
   dmtz_status st = slab_check(c, sl, workspace, wsb, &L);
   if (st) return st;
@@ -1031,6 +1078,7 @@ dmtz_status dmtz_slab_round_async(dmtz_ctx* c, const float* f, const float* fhat
 
 dmtz_status dmtz_slab_halo(dmtz_ctx* c, const dmtz_slab* sl, void* workspace, size_t wsb, float* g,
                            const float* planes, int64_t z_begin, int64_t z_end, int64_t round, dmtz_stream_t stream) {
+  DeviceGuard dg_(c);
   Layout L;
   dmtz_status st = slab_check(c, sl, workspace, wsb, &L);
   if (st) return st;
@@ -1051,6 +1099,7 @@ dmtz_status dmtz_slab_halo(dmtz_ctx* c, const dmtz_slab* sl, void* workspace, si
 dmtz_status dmtz_slab_end(dmtz_ctx* c, const dmtz_slab* sl, void* workspace, size_t wsb, const float* g,
                           dmtz_edit* edits, int64_t cap, int64_t* n_edits, int64_t* n_lossless,
                           dmtz_stream_t stream) {
+  DeviceGuard dg_(c);
   Layout L;
   dmtz_status st = slab_check(c, sl, workspace, wsb, &L);
   if (st) return st;
@@ -1068,6 +1117,7 @@ dmtz_status dmtz_slab_end(dmtz_ctx* c, const dmtz_slab* sl, void* workspace, siz
 dmtz_status dmtz_trace_separatrices(dmtz_ctx* c, const void* codes, uint32_t kinds, void* workspace,
                                     size_t workspace_bytes, dmtz_seps* out, int64_t cap_b, int64_t cap_c,
                                     int64_t* n_b, int64_t* n_c, dmtz_stream_t stream) {
+  DeviceGuard dg_(c);
   if (!c) { set_err("NULL argument"); return DMTZ_E_ARG; }
   return dmtz_trace_separatrices_range(c, codes, kinds, 0, c->g.nz, workspace, workspace_bytes, out, cap_b, cap_c,
                                        n_b, n_c, stream);
@@ -1077,6 +1127,7 @@ dmtz_status dmtz_trace_separatrices_range(dmtz_ctx* c, const void* codes, uint32
                                           int64_t z_end, void* workspace, size_t workspace_bytes, dmtz_seps* out,
                                           int64_t cap_b, int64_t cap_c, int64_t* n_b, int64_t* n_c,
                                           dmtz_stream_t stream) {
+  DeviceGuard dg_(c);
   if (!c || !codes || !workspace || !out || !n_b || !n_c || cap_b < 0 || cap_c < 0) {
     set_err("NULL argument");
     return DMTZ_E_ARG;
@@ -1108,10 +1159,15 @@ dmtz_status dmtz_trace_separatrices_range(dmtz_ctx* c, const void* codes, uint32
   a.a_lo = z_begin * c->g.sz;
   a.a_hi = z_end * c->g.sz;
   cudaError_t e = c->D == 3 ? run_trace<3>(a, (cudaStream_t)stream) : run_trace<2>(a, (cudaStream_t)stream);
+  for (int i = 0; i < 10; i++) g_trace_levels[i] = a.level_counts[i];
   if (e != cudaSuccess) { set_err("trace: %s", cudaGetErrorString(e)); return DMTZ_E_CUDA; }
   *n_b = a.n_branches;
   *n_c = a.n_cells;
   if (a.n_internal) { set_err("trace: cycle or inconsistent gradient"); return DMTZ_E_INTERNAL; }
+  if (a.n_overflow) {
+    set_err("trace: %lld connector BFS larger than the workspace scratch", (long long)a.n_overflow);
+    return DMTZ_E_CAPACITY;
+  }
   if (a.n_branches > cap_b || a.n_cells > cap_c) { set_err("trace needs %lld branches / %lld cells", (long long)a.n_branches, (long long)a.n_cells); return DMTZ_E_CAPACITY; }
   return DMTZ_OK;
 }
@@ -1126,6 +1182,7 @@ dmtz_status dmtz_preserve(dmtz_ctx* c, const float* f, const float* fhat, const 
                           void* workspace, size_t workspace_bytes, void* sep_ws, size_t sep_ws_bytes,
                           int64_t cap_b, int64_t cap_c, float* g_out, dmtz_edit* edits, int64_t edits_capacity,
                           int64_t* n_edits, dmtz_stats* st, dmtz_sloop_stats* ss, dmtz_stream_t stream) {
+  DeviceGuard dg_(c);
   if (!c || !f || !fhat || !o || !workspace || !g_out || !n_edits || !st || !ss ||
       (edits_capacity > 0 && !edits) || edits_capacity < 0 || cap_b < 0 || cap_c < 0) {
     set_err("NULL argument");
@@ -1177,6 +1234,7 @@ size_t dmtz_edit_stream_bound(int64_t n) {
 dmtz_status dmtz_encode_edits(dmtz_ctx* c, const dmtz_edit* edits, int64_t n, float xi, int32_t q_max,
                               const float* fhat, void* ws, size_t wsb, uint8_t* out, size_t cap, size_t* nbytes,
                               dmtz_stream_t stream) {
+  DeviceGuard dg_(c);
   if (!c || (n > 0 && !edits) || !ws || !out || !nbytes || n < 0) { set_err("NULL argument"); return DMTZ_E_ARG; }
   if (n > c->g.N) { set_err("%lld edits for %lld vertices", (long long)n, (long long)c->g.N); return DMTZ_E_ARG; }
   const Layout L = layout_for(c);
@@ -1205,6 +1263,7 @@ dmtz_status dmtz_encode_edits(dmtz_ctx* c, const dmtz_edit* edits, int64_t n, fl
 dmtz_status dmtz_decode_edits(dmtz_ctx* c, const uint8_t* in, size_t nbytes, const float* fhat, dmtz_edit* edits,
                               int64_t cap, int64_t* n_edits, float* xi, int32_t* q_max, void* ws, size_t wsb,
                               dmtz_stream_t stream) {
+  DeviceGuard dg_(c);
   if (!c || !in || !n_edits || !xi || !q_max || !ws || cap < 0 || (cap > 0 && !edits)) {
     set_err("NULL argument");
     return DMTZ_E_ARG;
@@ -1248,6 +1307,7 @@ dmtz_status dmtz_decode_edits(dmtz_ctx* c, const uint8_t* in, size_t nbytes, con
 
 dmtz_status dmtz_apply_edits(dmtz_ctx* c, const float* fhat, float xi, int32_t q_max, const dmtz_edit* edits,
                              int64_t n, float* g_out, void* ws, size_t wsb, dmtz_stream_t stream) {
+  DeviceGuard dg_(c);
   if (!c || !fhat || !g_out || !ws || n < 0 || (n > 0 && !edits) || !(xi > 0.0f) || q_max < 0 || q_max > 30) {
     set_err("invalid argument");
     return DMTZ_E_ARG;
@@ -1272,6 +1332,7 @@ dmtz_status dmtz_apply_edits(dmtz_ctx* c, const float* fhat, float xi, int32_t q
 
 dmtz_status dmtz_critical_prf(dmtz_ctx* c, const uint32_t* a, const uint32_t* b, dmtz_prf* out, void* ws,
                               size_t wsb, dmtz_stream_t stream) {
+  DeviceGuard dg_(c);
   if (!c || !a || !b || !out || !ws) { set_err("NULL argument"); return DMTZ_E_ARG; }
   const Layout L = layout_for(c);
   if (wsb < L.total) { set_err("workspace %zu < %zu bytes", wsb, L.total); return DMTZ_E_OOM; }
@@ -1291,6 +1352,7 @@ dmtz_status dmtz_critical_prf(dmtz_ctx* c, const uint32_t* a, const uint32_t* b,
 
 dmtz_status dmtz_separatrix_prf(dmtz_ctx* c, const dmtz_seps* A, int64_t na, const dmtz_seps* B, int64_t nb,
                                 dmtz_prf* out, void* ws, size_t wsb, dmtz_stream_t stream) {
+  DeviceGuard dg_(c);
   if (!c || !A || !B || !out || !ws || na < 0 || nb < 0) { set_err("NULL argument"); return DMTZ_E_ARG; }
   const Layout L = layout_for(c);
   if (wsb < L.total) { set_err("workspace %zu < %zu bytes", wsb, L.total); return DMTZ_E_OOM; }

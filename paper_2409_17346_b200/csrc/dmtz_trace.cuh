@@ -49,6 +49,10 @@ struct TraceArgs {
   int64_t given_nbk[3] = {-1, -1, -1};
   int verbose = 0;
   int64_t n_branches = 0, n_cells = 0, n_internal = 0;
+  int64_t n_overflow = 0;  // connectors whose BFS outgrew all scratch (-> DMTZ_E_CAPACITY)
+  // connectors handled per escalation level in the count pass: [0] all (thread queues),
+  // [1] warp queues, [2..] block BFS levels (slots growing by 16x)
+  int64_t level_counts[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 };
 
 constexpr uint64_t CELL_BOUNDARY = ~0ull;
@@ -660,7 +664,7 @@ k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
              const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm, long long* __restrict__ off,
              uint64_t* __restrict__ cells, bool write, unsigned int* __restrict__ overflow, int64_t conn_base,
              uint32_t* __restrict__ pool, unsigned long long* __restrict__ pool_top, int64_t pool_cap,
-             int64_t pool_limit) {
+             int64_t pool_limit, int cq_lim) {
   __shared__ uint32_t sq[CQ][CONN_THREADS];
   uint32_t* q = &sq[0][threadIdx.x];   // q[k * CONN_THREADS]: conflict-free columns
   // triangle -> facet edges (dm | edge index << 3); edge slot -> cofacet (type | anchor delta + 1)
@@ -769,7 +773,7 @@ k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
           for (int i = tail - 1; i >= 0 && !seen; i--) seen = q[i * CONN_THREADS] == k;
           if (seen) continue;
         }
-        if (tail == CQ) { ovf = true; break; }
+        if (tail == cq_lim) { ovf = true; break; }   // cq_lim = CQ (tests: smaller)
         q[(tail++) * CONN_THREADS] = k;
         filt |= fb;
         if (write) out[n] = cell_id<D>(a + nx_ + ny_ * g.sy + nz_ * g.sz, nt);
@@ -814,7 +818,7 @@ __global__ void __launch_bounds__(CONNW_WARPS * 32)
 k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restrict__ list,
             int64_t nlist, int64_t conn_base, const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
             long long* __restrict__ off, uint64_t* __restrict__ cells, bool write,
-            unsigned int* __restrict__ overflow) {
+            unsigned int* __restrict__ overflow, int wq_lim) {
   extern __shared__ unsigned long long smw[];
   __shared__ ConnTab CT;
   conn_tables_init<D>(CT);
@@ -888,7 +892,7 @@ k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restri
       }
       const int tot = __shfl_sync(0xffffffffu, incl, 31);
       const int tot_e = tot & 0xFFFF, tot_q = tot >> 16;
-      if (tail + tot_q > WQ) { ovf = true; break; }
+      if (tail + tot_q > wq_lim) { ovf = true; break; }   // wq_lim = WQ (tests: smaller)
       int pe = (incl - v) & 0xFFFF, pq = (incl - v) >> 16;
 #pragma unroll
       for (int j = 0; j < 3; j++) {
@@ -1234,9 +1238,8 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   // walks: lengths -> offsets -> cells.  Connector slots: one per thread of the launch.
   int* ovf = (int*)pre;
   unsigned long long* sc = A.bfs;
-  const int64_t words = (int64_t)(A.bfs_bytes / 8);
+  const int64_t words_all = (int64_t)(A.bfs_bytes / 8);
   // a connector visits at most the 12 N triangles; small grids get small slots
-  const int64_t slot_q = CQ;  // level 0: k_conn_small's shared-memory queues
   const int threads = 128;
   const int64_t conn_base = nbk[0] + nbk[1];
   const int64_t ovf_words = (nbk[2] + 31) / 32;
@@ -1257,6 +1260,20 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
     if (c >= 0 && c < pool_cap) pool_cap = c;
   }
   int64_t pool_limit = 0;
+  // test knobs (tests/test_gpu_parity.py forces every escalation level on small grids):
+  // DMTZ_TEST_CQ / DMTZ_TEST_WQ shrink the thread / warp queues, DMTZ_TEST_BFS_GROW sets
+  // the block level's slot growth (default 16), DMTZ_TEST_BFS_WORDS caps the scratch
+  auto env_int = [](const char* n, long long dflt, long long lo, long long hi) {
+    const char* e = getenv(n);
+    if (!e) return dflt;
+    long long v = atoll(e);
+    return v < lo ? lo : v > hi ? hi : v;
+  };
+  const int cq_lim = (int)env_int("DMTZ_TEST_CQ", CQ, 1, CQ);
+  const int wq_lim = (int)env_int("DMTZ_TEST_WQ", WQ, 4, WQ);
+  const int64_t grow = env_int("DMTZ_TEST_BFS_GROW", 16, 2, 16);
+  const int64_t words = env_int("DMTZ_TEST_BFS_WORDS", words_all, 1024, words_all);
+  for (int i = 0; i < 10; i++) A.level_counts[i] = 0;
   TCK(cudaMemsetAsync(&dc->pad[2], 0, 8, s));
   for (int pass = 0; pass < 2; pass++) {
     const bool write = pass == 1;
@@ -1267,12 +1284,13 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
       const int64_t nbc = (nbk[2] + CONN_THREADS - 1) / CONN_THREADS;
       k_conn_small<D><<<(unsigned)(nbc < 148 * 64 ? nbc : 148 * 64), CONN_THREADS, 0, s>>>(
           V.eview, g, conn_base, nb, A.out_origin, A.out_terminal, off, A.out_cells, write,
-          (unsigned int*)ovf, conn_base, pool, &dc->pad[2], pool_cap, pool_limit);
+          (unsigned int*)ovf, conn_base, pool, &dc->pad[2], pool_cap, pool_limit, cq_lim);
+      if (!write) A.level_counts[0] = nbk[2];
     }
     TCK(cudaGetLastError());
     if (nbk[2]) {  // connectors that outgrew their slot: retry with 16x bigger slots, fewer threads
       // the overflow bitmask is compacted into a list on the device, in word chunks that fit the list area
-      int64_t q = slot_q;
+      int64_t q = cq_lim;  // level 0: k_conn_small's shared-memory queues
       uint32_t* dlist = (uint32_t*)(ovf + ovf_words + 1);
       unsigned long long* dn = &dc->pad[1];
       const int64_t chunk_words = list_cap / 32 > 0 ? list_cap / 32 : 1;
@@ -1284,10 +1302,15 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
                            s>>>((uint32_t*)ovf, 0, ovf_words, dlist, dn);  // (list unused beyond the count)
           TCK(cudaMemcpyAsync(&hc->pad[1], dn, 8, cudaMemcpyDeviceToHost, s));
           TCK(cudaStreamSynchronize(s));
-          A.n_internal += (int64_t)hc->pad[1];
-          break;
+          // those connectors have no cell count (their offsets were never written):
+          // stop here -- the caller reports DMTZ_E_CAPACITY, the CSR is not produced
+          A.n_overflow = (int64_t)hc->pad[1];
+          TCK(cudaMemcpyAsync(hc, dc, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+          TCK(cudaStreamSynchronize(s));
+          A.n_internal = (int64_t)hc->n_internal;
+          return cudaSuccess;
         }
-        const int64_t qn = warp_level ? WQ : (q * 16 < words / 5 ? q * 16 : words / 5);
+        const int64_t qn = warp_level ? wq_lim : (q * grow < words / 5 ? q * grow : words / 5);
         int64_t h = 1;
         while (h < 2 * qn) h *= 2;
         while (qn + 2 * h > words) h /= 2;
@@ -1306,6 +1329,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
           const int64_t cn = (int64_t)hc->pad[1];
           if (!cn) continue;
           any = true;
+          if (!write) A.level_counts[level + 1 < 10 ? level + 1 : 9] += cn;
           if (warp_level) {
             const int64_t nbw = (cn + CONNW_WARPS - 1) / CONNW_WARPS;
             if (A.verbose)
@@ -1314,7 +1338,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
             TCK(cudaFuncSetAttribute(k_conn_warp<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CONNW_SMEM));
             k_conn_warp<D><<<(unsigned)(nbw < 148 * 12 ? nbw : 148 * 12), CONNW_WARPS * 32, CONNW_SMEM, s>>>(
                 V.eview, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write,
-                (unsigned int*)ovf);
+                (unsigned int*)ovf, wq_lim);
             TCK(cudaGetLastError());
             continue;
           }
