@@ -69,8 +69,9 @@ def lib():
                                           ctypes.POINTER(_Stats)]
         L.dmtz_oracle_correct_ex.argtypes = [P, P, P, ctypes.c_float, ctypes.c_int32, ctypes.c_int32,
                                              ctypes.c_int32, i64, ctypes.c_int32, P, P, P, i64, P,
-                                             ctypes.POINTER(_Stats), P, P, i64]
+                                             ctypes.POINTER(_Stats), P, P, i64, P]
         L.dmtz_oracle_trace_digest.argtypes = [P, P, ctypes.c_uint32, P, P, P]
+        L.dmtz_oracle_pairs_batch.argtypes = [P, i64, P, P, P, ctypes.c_int32]
         L.dmtz_oracle_preserve.argtypes = [P, P, P, ctypes.c_float, ctypes.c_int32, ctypes.c_int32,
                                            ctypes.c_int32, i64, P, P, P, i64, P,
                                            ctypes.POINTER(_Stats), ctypes.POINTER(_SStats)]
@@ -81,7 +82,8 @@ def lib():
                                              i64, i64, i64, i64, P, P, P, P]
         for fn in ("dmtz_oracle_gradient", "dmtz_oracle_complex_info", "dmtz_oracle_cell_counts",
                    "dmtz_oracle_correct", "dmtz_oracle_trace", "dmtz_oracle_num_threads", "dmtz_oracle_slab_round",
-                   "dmtz_oracle_preserve", "dmtz_oracle_correct_ex", "dmtz_oracle_trace_digest"):
+                   "dmtz_oracle_preserve", "dmtz_oracle_correct_ex", "dmtz_oracle_trace_digest",
+                   "dmtz_oracle_pairs_batch"):
             getattr(L, fn).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -139,13 +141,14 @@ def cell_counts(shape):
 
 def correct(f: np.ndarray, fhat: np.ndarray, xi: float, q_max: int = 6, q_cap: int | None = None,
             tier: int = 2, max_rounds: int = 0, edits_capacity: int | None = None,
-            frontier: bool = False, round_log: bool = False):
+            frontier: bool = False, round_log: bool = False, diag: bool = False):
     """Literal synchronous C-loop.  Returns dict(status, g, state, edits, stats).
 
     ``frontier``: after round 1 re-pair and classify only the cells anchored within
     [-2,1]^D of a target of the previous round (``dmtz_oracle_correct_ex``; equal to
     the full loop, tests/test_oracle_frontier.py).  ``round_log``: also return the
-    number of false cells of every round (``false_per_round``)."""
+    number of false cells of every round (``false_per_round``).  ``diag``: also return
+    ``diag`` = dict(targets_at_lb, r1, r2, r3a, r3b, targets) summed over the rounds."""
     f = np.ascontiguousarray(f, dtype=np.float32)
     fhat = np.ascontiguousarray(fhat, dtype=np.float32)
     assert f.shape == fhat.shape
@@ -162,14 +165,18 @@ def correct(f: np.ndarray, fhat: np.ndarray, xi: float, q_max: int = 6, q_cap: i
     log_cap = 1 << 20 if round_log else 0
     log = np.full(max(log_cap, 1), -2, np.int64)
     sec = np.zeros(max(log_cap, 1), np.float64)
+    dg = np.zeros(6, np.int64)
     st = lib().dmtz_oracle_correct_ex(_p(d), _p(f), _p(fhat), ctypes.c_float(xi), q_max, q_cap, tier,
                                       max_rounds, int(bool(frontier)), _p(g), _p(state), _p(edits), cap,
-                                      ctypes.byref(ne), ctypes.byref(stats), _p(log), _p(sec), log_cap)
+                                      ctypes.byref(ne), ctypes.byref(stats), _p(log), _p(sec), log_cap,
+                                      _p(dg) if diag else None)
     out = {k: getattr(stats, k) for k in STATS_FIELDS}
     out["false_by_kind_round0"] = list(stats.false_by_kind_round0)
     out["status"] = st
     res = dict(status=st, g=g, state=state, edits=edits[:min(ne.value, cap)].copy(),
                n_edits=ne.value, stats=out)
+    if diag:
+        res["diag"] = dict(zip(("targets_at_lb", "r1", "r2", "r3a", "r3b", "targets"), (int(x) for x in dg)))
     if round_log:
         nr = int((log != -2).sum())
         res["false_per_round"] = [int(x) for x in log[:nr]]
@@ -259,6 +266,21 @@ def trace_digest(field: np.ndarray, kinds: int = KIND_DESC | KIND_ASC | KIND_CON
         raise RuntimeError(f"oracle trace_digest status {st}")
     names = ("offsets", "cells", "origin", "terminal", "kind")
     return nb.value, nc.value, {k: int(v) for k, v in zip(names, dig)}
+
+
+def pairs_batch(fields: np.ndarray, cap: int = 48):
+    """Literal gradient pairs of many fields on one tiny grid (fields: (nf, *shape)).
+    Returns (pairs uint32 (nf, cap), count int32 (nf)); a pair is (cell mask << 16) |
+    (cofacet mask), vertex-id bitmasks, sorted per field."""
+    fields = np.ascontiguousarray(fields, dtype=np.float32)
+    d = _dims(fields.shape[1:])
+    nf = fields.shape[0]
+    out = np.zeros((nf, cap), np.uint32)
+    cnt = np.zeros(nf, np.int32)
+    st = lib().dmtz_oracle_pairs_batch(_p(d), nf, _p(fields), _p(out), _p(cnt), cap)
+    if st:
+        raise RuntimeError(f"oracle pairs_batch status {st}")
+    return out, cnt
 
 
 def slab_round(f, fhat, xi, g, state, anchor_planes, owned_planes, q_max=6, q_cap=None, tier=2):

@@ -535,13 +535,14 @@ static int64_t lowest_vertex(const float* f, int n, const int64_t* vs) {
  *        m == y                   -> the vertex c is paired with in f     (R3b)
  * Returns -1 on an internal inconsistency. */
 static int64_t target_of(const cx_t* cx, const float* f, const grad_t* Gf, const grad_t* Gg,
-                         int64_t A, int ti, int fn) {
+                         int64_t A, int ti, int fn, int* rule) {
   const ctype_t* ct = &cx->t[ti];
   int64_t av[4];
   cell_vertices(cx, A, ti, av);
   size_t i = (size_t)A * cx->T + ti;
   co_t a = coords(cx, A);
   if (!fn) {
+    *rule = 1;
     if (Gf->up[i] >= 0) {
       int s = Gf->up[i];
       return vid(cx, a.x + ct->link[s][0], a.y + ct->link[s][1], a.z + ct->link[s][2]);
@@ -549,10 +550,13 @@ static int64_t target_of(const cx_t* cx, const float* f, const grad_t* Gf, const
     return av[(int)Gf->dn[i]];
   }
   int64_t m = lowest_vertex(f, ct->nv, av);
+  *rule = 2;
   if (Gg->up[i] >= 0) return m;
   int k = Gg->dn[i];
   int64_t y = av[k];
+  *rule = 3;
   if (m != y) return m;
+  *rule = 4;
   int ft;
   int64_t C = facet_cell(cx, A, ti, k, &ft);
   int s = Gf->up[(size_t)C * cx->T + ft];
@@ -566,10 +570,10 @@ static int64_t target_of(const cx_t* cx, const float* f, const grad_t* Gf, const
  * P:140-141), target set T (a set: each vertex at most once per round).
  * Returns |F| (or -1 on internal error); kinds[8] accumulates counts. */
 static int64_t classify(const cx_t* cx, const float* f, const grad_t* Gf, const grad_t* Gg,
-                        int tier, uint8_t* T, int64_t* kinds, const uint8_t* D) {
+                        int tier, uint8_t* T, int64_t* kinds, const uint8_t* D, int64_t* rules) {
   int64_t nF = 0, bad = 0;
-  int64_t kk[8] = {0};
-#pragma omp parallel for schedule(dynamic, 4096) reduction(+ : nF, bad) reduction(+ : kk[:8])
+  int64_t kk[8] = {0}, rr[5] = {0};
+#pragma omp parallel for schedule(dynamic, 4096) reduction(+ : nF, bad) reduction(+ : kk[:8], rr[:5])
   for (int64_t A = 0; A < cx->N; A++) {
     if (D && !D[A]) continue;  /* frontier mode: no false cell is anchored outside D */
     for (int ti = 0; ti < cx->T; ti++) {
@@ -581,17 +585,23 @@ static int64_t classify(const cx_t* cx, const float* f, const grad_t* Gf, const 
       int fn = cf;  /* critical in f, paired in g: false negative */
       nF++;
       kk[kind_of(cx, d, fn)]++;
-      int64_t v = target_of(cx, f, Gf, Gg, A, ti, fn);
+      int rule = 0;
+      int64_t v = target_of(cx, f, Gf, Gg, A, ti, fn, &rule);
+      rr[rule]++;
       if (v < 0) { bad++; continue; }
 #pragma omp atomic write
       T[v] = 1;
     }
   }
   for (int k = 0; k < 8; k++) kinds[k] += kk[k];
+  if (rules) for (int k = 1; k < 5; k++) rules[k - 1] += rr[k];
   return bad ? -1 : nF;
 }
 
-/* frontier = 0: every round recomputes the whole gradient of g and classifies every
+/* diag (optional, int64[6], accumulated over the rounds; instrumentation for the
+ * progress-lemma pin): [0] targets whose g was not above lb when selected, [1..4]
+ * false cells resolved by rule R1 / R2 / R3a / R3b, [5] targets (set members).
+ * frontier = 0: every round recomputes the whole gradient of g and classifies every
  * cell (the literal loop).  frontier = 1: round 1 does; round r > 1 recomputes the
  * cells anchored in D_r = { A : a target of round r-1 lies in A + [-1,2]^D } (the
  * only cells whose pair can change, see gradient_update) and classifies the cells
@@ -604,7 +614,7 @@ int dmtz_oracle_correct_ex(const int64_t* dims, const float* f, const float* fha
                            int32_t q_max, int32_t q_cap, int32_t tier, int64_t max_rounds, int32_t frontier,
                            float* g_out, uint32_t* state_out, or_edit* edits, int64_t edits_capacity,
                            int64_t* n_edits, or_stats* stats, int64_t* round_log, double* round_sec,
-                           int64_t round_log_cap) {
+                           int64_t round_log_cap, int64_t* diag) {
   memset(stats, 0, sizeof *stats);
   *n_edits = 0;
   int st = check_dims(dims);
@@ -649,7 +659,8 @@ int dmtz_oracle_correct_ex(const int64_t* dims, const float* f, const float* fha
     }
     memset(T, 0, N);
     int64_t kinds[8] = {0};
-    int64_t nF = classify(&cx, f, &Gf, &Gg, tier, T, kinds, (round == 1 || !frontier) ? NULL : Dm);
+    int64_t nF = classify(&cx, f, &Gf, &Gg, tier, T, kinds, (round == 1 || !frontier) ? NULL : Dm,
+                          diag ? diag + 1 : NULL);
     if (round_log && round - 1 < round_log_cap) round_log[round - 1] = nF;
     if (nF < 0) { status = OR_E_INTERNAL; break; }
     if (round == 1) {
@@ -660,6 +671,10 @@ int dmtz_oracle_correct_ex(const int64_t* dims, const float* f, const float* fha
     stats->rounds = round;
     int changed = 0;
     for (int64_t v = 0; v < N; v++) {
+      if (diag && T[v]) {                 /* diagnostics: targets, and targets already at lb */
+        diag[5]++;
+        if (!(g_out[v] > lb[v])) diag[0]++;
+      }
       if (!T[v] || lossless[v]) continue;
       changed = 1;
       /* Eq. 2: one step of xi/2^q_max, recomputed from fhat:
@@ -704,7 +719,7 @@ int dmtz_oracle_correct(const int64_t* dims, const float* f, const float* fhat, 
                         float* g_out, uint32_t* state_out, or_edit* edits, int64_t edits_capacity,
                         int64_t* n_edits, or_stats* stats) {
   return dmtz_oracle_correct_ex(dims, f, fhat, xi, q_max, q_cap, tier, max_rounds, 0, g_out, state_out,
-                                edits, edits_capacity, n_edits, stats, NULL, NULL, 0);
+                                edits, edits_capacity, n_edits, stats, NULL, NULL, 0, NULL);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -1135,7 +1150,7 @@ int dmtz_oracle_preserve(const int64_t* dims, const float* f, const float* fhat,
     gradient(&cx, g_out, &Gg);
     memset(T, 0, N);
     int64_t kinds[8] = {0};
-    int64_t nF = classify(&cx, f, &Gf, &Gg, ctier, T, kinds, NULL);
+    int64_t nF = classify(&cx, f, &Gf, &Gg, ctier, T, kinds, NULL, NULL);
     if (nF < 0) { status = OR_E_INTERNAL; break; }
     if (round == 1) {
       stats->n_false_round0 = nF;
@@ -1155,7 +1170,8 @@ int dmtz_oracle_preserve(const int64_t* dims, const float* f, const float* fhat,
         if (tier == 3 && same_ends(&Sf, &Sg, b)) continue;
         int64_t A; int ti;
         if (!troublemaker(&cx, &Gf, &Gg, &Sf, b, &A, &ti)) continue;
-        int64_t v = target_of(&cx, f, &Gf, &Gg, A, ti, 0);
+        int rule_unused;
+        int64_t v = target_of(&cx, f, &Gf, &Gg, A, ti, 0, &rule_unused);
         if (v < 0) { bad++; continue; }
         T[v] = 1;
         ntm++;
@@ -1259,6 +1275,50 @@ int64_t dmtz_oracle_persistence0(const int64_t* dims, const float* field, int64_
   return np;
 }
 
+/* Test interface for the exhaustive-order pins (tests/test_oracle_orders.py): the
+ * literal gradient of each of nf fields on one tiny grid (<= 16 vertices), as the list
+ * of pairs (vertex-id bitmask of the cell, bitmask of its partner cofacet) sorted by
+ * the cell's bitmask; out[f * cap ...] holds field f's pairs, count[f] their number. */
+static int cmp_u32(const void* a, const void* b) {
+  uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+  return x < y ? -1 : x > y;
+}
+int dmtz_oracle_pairs_batch(const int64_t* dims, int64_t nf, const float* fields, uint32_t* out, int32_t* count,
+                            int32_t cap) {
+  int st = check_dims(dims);
+  if (st) return st;
+  cx_t cx; build_complex(&cx, dims[0], dims[1], dims[2]);
+  if (cx.N > 16) return OR_E_ARG;
+  int bad = 0;
+#pragma omp parallel for schedule(dynamic, 64) reduction(+ : bad)
+  for (int64_t k = 0; k < nf; k++) {
+    grad_t G;
+    if (!grad_alloc(&cx, &G)) { bad++; continue; }
+    gradient(&cx, fields + k * cx.N, &G);
+    int n = 0;
+    uint32_t* o = out + k * (int64_t)cap;
+    for (int64_t A = 0; A < cx.N; A++)
+      for (int ti = 0; ti < cx.T; ti++) {
+        int s = G.up[(size_t)A * cx.T + ti];
+        if (s < 0) continue;
+        int64_t vs[5];
+        cell_vertices(&cx, A, ti, vs);
+        uint32_t cm = 0;
+        for (int i = 0; i <= cx.t[ti].dim; i++) cm |= 1u << vs[i];
+        co_t a = coords(&cx, A);
+        const ctype_t* ct = &cx.t[ti];
+        int64_t w = vid(&cx, a.x + ct->link[s][0], a.y + ct->link[s][1], a.z + ct->link[s][2]);
+        if (n < cap) o[n] = (cm << 16) | cm | (1u << w);
+        n++;
+      }
+    if (n > cap) { bad++; n = cap; }
+    qsort(o, (size_t)n, sizeof(uint32_t), cmp_u32);
+    count[k] = n;
+    grad_free(&G);
+  }
+  return bad ? OR_E_CAPACITY : OR_OK;
+}
+
 int dmtz_oracle_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();
@@ -1311,7 +1371,8 @@ int dmtz_oracle_slab_round(const int64_t* dims, const float* f, const float* fha
         nF++;
         kinds[kind_of(&cx, d, cf)]++;
       }
-      int64_t v = target_of(&cx, f, &Gf, &Gg, A, ti, cf);
+      int rule_unused;
+      int64_t v = target_of(&cx, f, &Gf, &Gg, A, ti, cf, &rule_unused);
       if (v < 0) { bad++; continue; }
       if (v >= oz0 * plane && v < oz1 * plane) T[v] = 1;
     }

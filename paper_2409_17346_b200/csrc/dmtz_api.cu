@@ -51,6 +51,7 @@ struct dmtz_ctx {
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // sweep timing (opts.profile): screen | decode
   int verbose;         // DMTZ_VERBOSE=1: per-round counters on stderr (host-driven rounds)
   int no_graph;        // DMTZ_NO_GRAPH=1: host-driven rounds instead of the CUDA-graph loop
+  int no_keys;         // DMTZ_NO_KEYS=1: k_screen always uses the compare/select form of the gradient
   LoopState* host_ls = nullptr;  // pinned
   struct LoopGraph* graph = nullptr;
   cudaStream_t cap_stream = nullptr;  // private stream the loop body is captured on (the caller's may be the legacy stream)
@@ -96,7 +97,7 @@ inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 // Workspace layout (offsets from the base, each 256-B aligned)
 struct Layout {
   size_t cand_f, cand_g, crit_f, crit_g, lowpos, lb, state, tcache, ncache, tbits, counters, edit_bc, ebits, fmark, vchg, units,
-      units2, frontier, trace, total;
+      units2, frontier, keyinfo, trace, total;
   int64_t fwords;  // frontier bitmap words (one bit per row-block unit)
 };
 
@@ -127,6 +128,7 @@ Layout layout_for(const dmtz_ctx* c) {
   L.units = o; o += align_up((size_t)rg.units * 4);
   L.units2 = o; o += align_up((size_t)rg.units * 4);
   L.frontier = o; o += align_up(L.fwords * 4 + 64);
+  L.keyinfo = o; o += align_up(sizeof(KeyInfo));
   L.trace = o; o += align_up(trace_scratch_bytes(c->g, c->D));
   L.total = o;
   return L;
@@ -167,6 +169,7 @@ struct WS {
   uint8_t* ncache;
   float* lb;
   Counters* dc;
+  KeyInfo* ki;               // value range of the call (key form of the gradient)
   LoopState* ls;             // second 256 B block of the counters region
   unsigned long long* bc;
   size_t rowbit_bytes;
@@ -182,6 +185,7 @@ struct WS {
     state = (uint32_t*)(ws + L.state);
     tbits = (uint32_t*)(ws + L.tbits);
     dc = (Counters*)(ws + L.counters);
+    ki = (KeyInfo*)(ws + L.keyinfo);
     ls = (LoopState*)(ws + L.counters + sizeof(Counters));
     bc = (unsigned long long*)(ws + L.edit_bc);
     ebits = (uint32_t*)(ws + L.ebits);
@@ -214,7 +218,9 @@ dmtz_status setup_phase(dmtz_ctx* c, const float* f, const float* fhat, const dm
   CK(cudaMemsetAsync(W.tbits, 0, nwords * 4, s));
   CK(cudaMemsetAsync(W.fmark, 0, W.rowbit_bytes, s));
   CK(cudaMemsetAsync(W.vchg, 0, 2 * W.rowbit_bytes, s));
-  k_setup<<<clamp_blocks(g.N, 256), 256, 0, s>>>(f, fhat, o->xi, g.N, W.lb, g_out, W.state, W.dc);
+  CK(cudaMemsetAsync(W.ki, 0, sizeof(KeyInfo), s));
+  CK(cudaMemsetAsync(&W.ki->min_bits, 0x7F, 4, s));
+  k_setup<<<clamp_blocks(g.N, 256), 256, 0, s>>>(f, fhat, o->xi, g.N, W.lb, g_out, W.state, W.dc, W.ki);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(hc, W.dc, sizeof(Counters), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -274,7 +280,7 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
   if (fbits) CK(cudaMemsetAsync(W.ebits, 0, W.rowbit_bytes, s));  // rewritten for every active unit
   if (profile) CK(cudaEventRecord(c->ev[0], s));
   k_screen<D><<<sweep_blocks, SCREEN_THREADS, 0, s>>>(g_out, W.cand_g, W.ebits, W.vchg, W.vwords, use_skip, units, n_units, g,
-                                           rg, W.ls, W.dc);
+                                           rg, W.ls, W.dc, W.ki, c->no_keys ? 0 : 1);
   if (c->sdirty) {  // dmtz_preserve: accumulate the changed codes for the next S-round
     k_sdirty_or<<<clamp_blocks(nwords, 256), 256, 0, s>>>(W.ebits, nwords, g, rg, c->sdirty);
     *launches += 1;
@@ -859,6 +865,8 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
   c->verbose = vb && vb[0] == '1';
   const char* ng = getenv("DMTZ_NO_GRAPH");
   c->no_graph = ng && ng[0] == '1';
+  const char* nk = getenv("DMTZ_NO_KEYS");
+  c->no_keys = nk && nk[0] == '1';
   cudaError_t e = cudaMallocHost((void**)&c->host_cnt, sizeof(Counters) * 2);
   if (e == cudaSuccess) e = cudaMallocHost((void**)&c->host_ls, sizeof(LoopState));
   if (e != cudaSuccess) {

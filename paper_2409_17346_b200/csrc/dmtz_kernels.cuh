@@ -71,6 +71,22 @@ struct LoopState {
 };
 static_assert(sizeof(LoopState) == 256, "loop state is one 256 B block");
 
+// Range of the values a call's fields can take (f, and g in [lb, fhat]): the key
+// form of the gradient (dmtz_sweep.cuh load_keys) needs every value positive and the
+// float bit patterns within 2^25 of the smallest.  Filled by k_setup.
+struct KeyInfo {
+  int min_bits;           // min over lb (as signed int: <= 0 for a non-positive value)
+  unsigned int max_bits;  // max over f and fhat (as unsigned: a negative value is huge)
+  unsigned int pad[14];
+};
+constexpr unsigned KEY_RANGE = 1u << 25;
+__device__ __forceinline__ bool keys_ok(const KeyInfo* ki, uint32_t* base) {
+  const int mn = ki->min_bits;
+  const unsigned mx = ki->max_bits;
+  *base = (uint32_t)mn;
+  return mn > 0 && mx >= (unsigned)mn && mx - (unsigned)mn < KEY_RANGE;
+}
+
 __global__ void k_set_round(LoopState* ls, unsigned long long r) {
   if (threadIdx.x == 0) ls->round = r;
 }
@@ -335,7 +351,9 @@ __device__ __forceinline__ void warp_add(unsigned long long* dst, unsigned long 
 // --------------------------------------------------------------------------
 __global__ void k_setup(const float* __restrict__ f, const float* __restrict__ fhat, float xi, int64_t n,
                         float* __restrict__ lb, float* __restrict__ gf, uint32_t* __restrict__ state,
-                        Counters* __restrict__ cnt) {
+                        Counters* __restrict__ cnt, KeyInfo* __restrict__ ki) {
+  int mn = 0x7FFFFFFF;
+  unsigned mx = 0u;
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
     const float a = f[v], b = fhat[v];
     if (!isfinite(a) || !isfinite(b)) { atomicMin(&cnt->first_nonfinite, (unsigned long long)v); continue; }
@@ -344,6 +362,14 @@ __global__ void k_setup(const float* __restrict__ f, const float* __restrict__ f
     lb[v] = lo;
     gf[v] = b;
     state[v] = 0;
+    mn = min(mn, __float_as_int(lo));
+    mx = max(mx, max(__float_as_uint(a), __float_as_uint(b)));
+  }
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&ki->min_bits, mn);
+    atomicMax(&ki->max_bits, mx);
   }
 }
 

@@ -105,6 +105,43 @@ __device__ __forceinline__ void load_stencil(const float* __restrict__ fld, cons
   }
 }
 
+// Key form of the stencil (DESIGN.md §7 "key form"): W[p] = 32 (bits(g_p) - base) + p,
+// p = (dx+1) + 3 (dy+1) + 9 (dz+1) the stencil position (ascending global index).  When
+// every value of the call is positive and within 2^25 bit patterns of base (keys_ok),
+// W[p] < 2^30 + 32, and W[p] < W[q] <=> g_p < g_q or (g_p = g_q and p < q): the SoS
+// order on the stencil.  Read as float bit patterns the keys keep that order
+// (non-negative, finite), so the argmin of a type's set is one FMNMX3 tree and
+// key & 31 its position.  Outside the grid: a key above every valid one.
+constexpr uint32_t KEY_OUTSIDE = 0x7E000000u;
+template <int D>
+__device__ __forceinline__ void load_keys(const float* __restrict__ fld, const Grid& g, int64_t v, int64_t x,
+                                          int64_t y, int64_t z, uint32_t base, uint32_t (&W)[27]) {
+  const bool interior = x > 0 && x + 1 < g.nx && y > 0 && y + 1 < g.ny && (D == 2 || (z > 0 && z + 1 < g.nz));
+  const uint32_t c0 = 0u - 32u * base;
+#pragma unroll
+  for (int dz = -1; dz <= 1; dz++)
+#pragma unroll
+    for (int dy = -1; dy <= 1; dy++)
+#pragma unroll
+      for (int dx = -1; dx <= 1; dx++) {
+        const int p = (dx + 1) + 3 * (dy + 1) + 9 * (dz + 1);
+        if (D == 2 && dz != 0) { W[p] = KEY_OUTSIDE; continue; }
+        const bool in = interior || ((x + dx >= 0) && (x + dx < g.nx) && (y + dy >= 0) && (y + dy < g.ny) &&
+                                     (z + dz >= 0) && (z + dz < g.nz));
+        const uint32_t b = in ? __float_as_uint(__ldg(fld + v + dx + dy * g.sy + dz * g.sz)) : 0u;
+        // 32 * (b - base) + p, the multiply-add on the FMA pipe
+        uint32_t w;
+        asm("mad.lo.u32 %0, %1, 32, %2;" : "=r"(w) : "r"(b), "r"(c0 + (uint32_t)p));
+        W[p] = in ? w : KEY_OUTSIDE;
+      }
+}
+
+template <int D>
+__device__ __forceinline__ uint64_t cand_of_keys(const uint32_t (&W)[27], const uint8_t* lut) {
+  if constexpr (D == 3) return k3d::cand_code_keys(W, lut);
+  else return k2d::cand_code_keys(W, lut);
+}
+
 template <int D>
 __device__ __forceinline__ uint64_t cand_of(const float (&s)[27]) {
   if constexpr (D == 3) return k3d::cand_code(s);
@@ -129,9 +166,16 @@ __global__ void DMTZ_SCREEN_LB
 k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg, uint32_t* __restrict__ ebits,
          uint32_t* __restrict__ vchg, int64_t vwords, int use_skip, const uint32_t* __restrict__ units,
          const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg, const LoopState* __restrict__ ls,
-         Counters* __restrict__ cnt) {
+         Counters* __restrict__ cnt, const KeyInfo* __restrict__ ki, int use_keys) {
   __shared__ uint16_t s_list[SCREEN_THREADS / 32][DG * 32];
   __shared__ uint32_t s_e[SCREEN_THREADS / 32][DG];
+  constexpr int NF = D == 3 ? k3d::NFIELD : k2d::NFIELD;
+  __shared__ uint8_t s_lut[NF * 32];
+  for (int i = threadIdx.x; i < NF * 32; i += blockDim.x)
+    s_lut[i] = D == 3 ? (&k3d::KEYLUT[0][0])[i] : (&k2d::KEYLUT[0][0])[i];
+  __syncthreads();
+  uint32_t kbase = 0;
+  const bool keys = use_keys && keys_ok(ki, &kbase);  // uniform over the launch
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint16_t* list = s_list[wib];
   uint32_t* se = s_e[wib];
@@ -212,10 +256,17 @@ k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg
       if (act) {
         const int64_t x = cbase * 32 + o;
         const int64_t v = row0 + o;
-        float sv[27];
-        load_stencil<D>(gfld, g, v, x, y, z, sv);
         const int ok = axes_ok(g, x, y, z);
-        const uint64_t code = cand_of<D>(sv) | t_nonex_fill<D>(ok);
+        uint64_t code;
+        if (keys) {
+          uint32_t W[27];
+          load_keys<D>(gfld, g, v, x, y, z, kbase, W);
+          code = cand_of_keys<D>(W, s_lut) | t_nonex_fill<D>(ok);
+        } else {
+          float sv[27];
+          load_stencil<D>(gfld, g, v, x, y, z, sv);
+          code = cand_of<D>(sv) | t_nonex_fill<D>(ok);
+        }
         e = first_round || code != (uint64_t)cg[v];
         if (e) cg[v] = (typename Tr<D>::code_t)code;
         recomputed++;

@@ -181,9 +181,14 @@ def c_loop(C: Complex, f, fhat, xi, q_max=6, q_cap=None, tier=2, max_rounds=1000
             return "ITER_CAP", g, q, lossless, stats
 
 
-def trace(C: Complex, f):
+def trace(C: Complex, f, interleaved: bool = False):
     """Descending / ascending / connector traces, returned as python lists of
-    (kind, origin, [cells...], terminal) with cells as frozensets."""
+    (kind, origin, [cells...], terminal) with cells as frozensets.  Connectors:
+    cells = the visited triangles in BFS order, terminal = the reached 1-saddles in
+    order; with ``interleaved`` cells = the single event log instead -- for each
+    dequeued triangle, its facet edges in facet order (the facet omitting the k-th
+    vertex by index), a critical edge logged as reached, a new triangle logged when
+    it is enqueued (S:212)."""
     fl = np.asarray(f, np.float32).ravel()
     pair = gradient(C, fl)
     crit = critical(C, pair)
@@ -224,7 +229,7 @@ def trace(C: Complex, f):
             out.append(("asc", c, cells, term))
     if C.D == 3:
         for s in order(c for c in crit if len(c) == 3):
-            reached, visited = [], [s]
+            reached, visited, events = [], [s], []
             seen = {s}
             qi = 0
             while qi < len(visited):
@@ -233,10 +238,12 @@ def trace(C: Complex, f):
                 for e in (t - {p} for p in sorted(t, key=C.vid)):
                     if e in crit:
                         reached.append(e)
+                        events.append(e)
                     elif len(pair[e]) == 3 and pair[e] != t and pair[e] not in seen:
                         seen.add(pair[e])
                         visited.append(pair[e])
-            out.append(("conn", s, visited[1:], reached))
+                        events.append(pair[e])
+            out.append(("conn", s, events if interleaved else visited[1:], reached))
     return out
 
 
