@@ -118,22 +118,33 @@ __device__ __forceinline__ void load_keys(const float* __restrict__ fld, const G
                                           int64_t y, int64_t z, uint32_t base, uint32_t (&W)[27]) {
   const bool interior = x > 0 && x + 1 < g.nx && y > 0 && y + 1 < g.ny && (D == 2 || (z > 0 && z + 1 < g.nz));
   const uint32_t c0 = 0u - 32u * base;
+  if (interior) {  // straight-line: 27 loads, 27 multiply-adds (FMA pipe)
 #pragma unroll
-  for (int dz = -1; dz <= 1; dz++)
+    for (int dz = -1; dz <= 1; dz++)
 #pragma unroll
-    for (int dy = -1; dy <= 1; dy++)
+      for (int dy = -1; dy <= 1; dy++)
 #pragma unroll
-      for (int dx = -1; dx <= 1; dx++) {
-        const int p = (dx + 1) + 3 * (dy + 1) + 9 * (dz + 1);
-        if (D == 2 && dz != 0) { W[p] = KEY_OUTSIDE; continue; }
-        const bool in = interior || ((x + dx >= 0) && (x + dx < g.nx) && (y + dy >= 0) && (y + dy < g.ny) &&
-                                     (z + dz >= 0) && (z + dz < g.nz));
-        const uint32_t b = in ? __float_as_uint(__ldg(fld + v + dx + dy * g.sy + dz * g.sz)) : 0u;
-        // 32 * (b - base) + p, the multiply-add on the FMA pipe
-        uint32_t w;
-        asm("mad.lo.u32 %0, %1, 32, %2;" : "=r"(w) : "r"(b), "r"(c0 + (uint32_t)p));
-        W[p] = in ? w : KEY_OUTSIDE;
-      }
+        for (int dx = -1; dx <= 1; dx++) {
+          const int p = (dx + 1) + 3 * (dy + 1) + 9 * (dz + 1);
+          if (D == 2 && dz != 0) { W[p] = KEY_OUTSIDE; continue; }
+          const uint32_t b = __float_as_uint(__ldg(fld + v + dx + dy * g.sy + dz * g.sz));
+          asm("mad.lo.u32 %0, %1, 32, %2;" : "=r"(W[p]) : "r"(b), "r"(c0 + (uint32_t)p));
+        }
+  } else {
+#pragma unroll
+    for (int dz = -1; dz <= 1; dz++)
+#pragma unroll
+      for (int dy = -1; dy <= 1; dy++)
+#pragma unroll
+        for (int dx = -1; dx <= 1; dx++) {
+          const int p = (dx + 1) + 3 * (dy + 1) + 9 * (dz + 1);
+          if (D == 2 && dz != 0) { W[p] = KEY_OUTSIDE; continue; }
+          const bool in = (x + dx >= 0) && (x + dx < g.nx) && (y + dy >= 0) && (y + dy < g.ny) && (z + dz >= 0) &&
+                          (z + dz < g.nz);
+          W[p] = in ? 32u * (__float_as_uint(__ldg(fld + v + dx + dy * g.sy + dz * g.sz)) - base) + (uint32_t)p
+                    : KEY_OUTSIDE;
+        }
+  }
 }
 
 template <int D>
