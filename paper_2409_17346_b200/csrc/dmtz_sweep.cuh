@@ -302,27 +302,35 @@ k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg
 // false mask keeps the code small.
 // ---------------------------------------------------------------------------
 struct TargetTables {
-  uint32_t tinfo[26];      // dim | nv << 2 | shift << 5 | none << 11 | nfacet << 15
-  uint32_t vm[26];         // vertex delta masks, 3 bits each
-  uint32_t fac[26][4];     // dm | ft << 3 | slot << 8 | k << 12
+  uint2 tv[26];            // x: shift | none << 6 ; y: the packed delta of vertex k at 6 k (k < 4)
+  uint32_t fac[26][4];     // dm | ft << 3 | k << 8 | ft's shift << 10 | ft's none << 16 | dm's delta << 20
   uint8_t ldel[26][14];    // link slot -> packed (dx+1) | (dy+1) << 2 | (dz+1) << 4
 };
+
+// delta mask (dx = bit 0, dy = bit 1, dz = bit 2) -> packed (dx+1) | (dy+1) << 2 | (dz+1) << 4
+__host__ __device__ __forceinline__ uint32_t mask_del(int m) {
+  return 0x15u + (m & 1) + ((m & 2) << 1) + ((m & 4) << 2);
+}
 
 template <int D>
 __device__ __forceinline__ void init_target_tables(TargetTables& T, const Grid& g) {
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int t = 0; t < Tr<D>::NT; t++) {
-      T.tinfo[t] = (uint32_t)t_dim<D>(t) | ((uint32_t)t_nv<D>(t) << 2) | ((uint32_t)t_shift<D>(t) << 5) |
-                   ((uint32_t)t_none<D>(t) << 11) | ((uint32_t)t_nfacet<D>(t) << 15);
-      uint32_t vm = 0;
+      const uint32_t sh = t_dim<D>(t) < Tr<D>::TOP ? (uint32_t)t_shift<D>(t) : 0u;
+      const uint32_t no = t_dim<D>(t) < Tr<D>::TOP ? (uint32_t)t_none<D>(t) : 0u;
+      uint32_t md = 0;
 #pragma unroll
-      for (int k = 0; k < 4; k++) vm |= (uint32_t)t_vmask<D>(t, k) << (3 * k);
-      T.vm[t] = vm;
+      for (int k = 0; k < 4; k++) md |= mask_del(t_vmask<D>(t, k)) << (6 * k);
+      T.tv[t] = make_uint2(sh | (no << 6), md);
 #pragma unroll
-      for (int j = 0; j < 4; j++)
-        T.fac[t][j] = (uint32_t)t_facet<D>(t, j, 0) | ((uint32_t)t_facet<D>(t, j, 1) << 3) |
-                      ((uint32_t)t_facet<D>(t, j, 2) << 8) | ((uint32_t)t_facet<D>(t, j, 3) << 12);
+      for (int j = 0; j < 4; j++) {
+        const int dm = t_facet<D>(t, j, 0), ft = t_facet<D>(t, j, 1);
+        const uint32_t fsh = t_dim<D>(ft) < Tr<D>::TOP ? (uint32_t)t_shift<D>(ft) : 0u;
+        const uint32_t fno = t_dim<D>(ft) < Tr<D>::TOP ? (uint32_t)t_none<D>(ft) : 0u;
+        T.fac[t][j] = (uint32_t)dm | ((uint32_t)ft << 3) | ((uint32_t)t_facet<D>(t, j, 3) << 8) | (fsh << 10) |
+                      (fno << 16) | ((mask_del(dm) - 0x15u) << 20);
+      }
 #pragma unroll
       for (int q = 0; q < 14; q++)
         T.ldel[t][q] = (uint8_t)((t_link<D>(t, q, 0) + 1) | ((t_link<D>(t, q, 1) + 1) << 2) |
@@ -346,36 +354,39 @@ __device__ __forceinline__ uint32_t field2(uint2 c, int shift, uint32_t none) {
   return w & none;
 }
 
-// delta mask (dx = bit 0, dy = bit 1, dz = bit 2) -> packed (dx+1) | (dy+1) << 2 | (dz+1) << 4
-__device__ __forceinline__ uint32_t mask_del(int m) { return 0x15u + (m & 1) + ((m & 2) << 1) + ((m & 4) << 2); }
-
 // Rules R1 / R2 / R3a / R3b for the false cell (anchor u, type t):
 // returns the target's offset from the anchor as packed (dx+1) | (dy+1) << 2 |
-// (dz+1) << 4, each component in [-1, 2].  The anchor's codes at u + {0,1}^D come
-// from the warp's shared-memory copy (cfs[dm * 32 + src]); dp = the down-pair facet
-// indices of the cells in g (decode_crit_dp).  Returns 0xFFFFFFFF on an inconsistency.
+// (dz+1) << 4, each component in [-1, 2].  cf0 / cg0 = the anchor's own f / g codes,
+// lowpos its f-lowest vertex per type, dp the down-pair facet index per type in g
+// (decode_crit_dp); R3b reads the f code of the facet's anchor from global memory
+// (u + its delta).  Returns 0xFFFFFFFF on an inconsistency.
+//  FP (critical in g, paired in f):  paired up in f -> the cofacet's extra vertex;
+//     paired down in f -> m (the vertex the facet lacks is the cell's f-lowest, m).
+//  FN (critical in f, paired in g):  paired up in g -> m (R2); paired down with the
+//     facet gamma omitting y: y != m -> m (R3a), else the vertex gamma is paired with
+//     in f (R3b).
 template <int D>
 __device__ __forceinline__ uint32_t target_del(const TargetTables& T, int t, bool fn, uint64_t lowpos, uint64_t dp,
-                                               const uint2* cfs, const uint2* cgs, int src) {
+                                               uint2 cf0, uint2 cg0, const typename Tr<D>::code_t* __restrict__ cand_f,
+                                               int64_t u, const Grid& g) {
   // straight-line (no divergence between the rules inside a warp): every operand is
   // read, the rule is picked with selects
-  const uint32_t ti = T.tinfo[t];
-  const int dim = ti & 3, shift = (ti >> 5) & 63;
-  const uint32_t none = (ti >> 11) & 15;
-  // m = the cell's f-lowest vertex (SoS), precomputed per anchor and type
-  const int mp = (int)(lowpos >> (2 * t)) & 3;
-  const uint32_t m_del = mask_del((T.vm[t] >> (3 * mp)) & 7);
-  // R1 reads the f-pairing, R2 the g-pairing of the same cell
-  const uint32_t a = dim < Tr<D>::TOP ? field2(fn ? cgs[src] : cfs[src], shift, none) : none;
-  const uint32_t r1 = a != none ? (uint32_t)T.ldel[t][a < 14 ? a : 0] : m_del;   // FP: cofacet vertex or m
-  // R3a / R3b: paired down in g with gamma = the facet j that points at it
   const int j = (int)(dp >> (2 * t)) & 3;
   const uint32_t fc = T.fac[t][j];
-  const int dm = fc & 7, ft = (fc >> 3) & 31, k = (fc >> 12) & 3;
-  const uint32_t fti = T.tinfo[ft];
-  const uint32_t fno = (fti >> 11) & 15;
-  const uint32_t s2 = field2(cfs[dm * 32 + src], (fti >> 5) & 63, fno);     // gamma's f-pair vertex
-  const uint32_t r3b = s2 != fno ? mask_del(dm) + T.ldel[ft][s2 < 14 ? s2 : 0] - 0x15u : 0xFFFFFFFFu;
+  const int dm = fc & 7;
+  // R3b's operand first: its load latency overlaps the rest
+  const uint64_t cfg = (uint64_t)__ldg(cand_f + u + mask_delta(g, dm));
+  const uint2 tv = T.tv[t];
+  const int shift = tv.x & 63;
+  const uint32_t none = tv.x >> 6;
+  const int mp = (int)(lowpos >> (2 * t)) & 3;
+  const uint32_t m_del = (tv.y >> (6 * mp)) & 63;   // m = the cell's f-lowest vertex (SoS)
+  const uint32_t a = field2(fn ? cg0 : cf0, shift, none);   // top cells: none = 0 -> a = 0 = none
+  const uint32_t r1 = a != none ? (uint32_t)T.ldel[t][a < 14 ? a : 0] : m_del;
+  const int ft = (fc >> 3) & 31, k = (fc >> 8) & 3;
+  const uint32_t fno = (fc >> 16) & 15;
+  const uint32_t s2 = field2(make_uint2((uint32_t)cfg, (uint32_t)(cfg >> 32)), (fc >> 10) & 63, fno);
+  const uint32_t r3b = s2 != fno ? (fc >> 20) + T.ldel[ft][s2 < 14 ? s2 : 0] : 0xFFFFFFFFu;  // dm + slot
   const uint32_t r3 = mp != k ? m_del : r3b;      // R3a: y = the vertex gamma omits != m
   return !fn ? r1 : (a != none ? m_del : r3);     // R2: paired up in g -> m
 }
@@ -399,7 +410,7 @@ __device__ __forceinline__ uint32_t target_del(const TargetTables& T, int t, boo
 constexpr int DECODE_THREADS = DMTZ_DECODE_THREADS;
 constexpr int TWW = DG + 2;             // window words per row
 struct DecodeWarpSmem {
-  uint2 cf[8 * 32];            // per slot: f codes of u + {0,1}^D
+  uint2 cf[32];                // per slot: f code of u
   uint2 cg[32];                // per slot: g code of u
   unsigned long long lowpos[32];
   unsigned long long dp[32];
@@ -433,7 +444,7 @@ __device__ __forceinline__ int compact_group(uint32_t m, int lane, uint16_t* lis
 }
 
 #ifndef DMTZ_DECODE_MINB
-#define DMTZ_DECODE_MINB 7
+#define DMTZ_DECODE_MINB 8
 #endif
 template <int D>
 __global__ void __launch_bounds__(DECODE_THREADS, DMTZ_DECODE_MINB)
@@ -556,12 +567,9 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
       const int total = __shfl_sync(0xffffffffu, pre, 31);
       pre -= nmine;
       W.tm[lane] = 0ull;
-      if (diff) {  // the f codes are read only for anchors with false cells
-#pragma unroll
-        for (int dm = 0; dm < Tr<D>::NDELTA; dm++) {
-          const uint64_t cfv = (dm & ~ok) == 0 ? (uint64_t)__ldg(cand_f + u + mask_delta(g, dm)) : Tr<D>::ALL_NONE;
-          W.cf[dm * 32 + lane] = make_uint2((uint32_t)cfv, (uint32_t)(cfv >> 32));
-        }
+      if (diff) {  // the f code is read only for anchors with false cells
+        const uint64_t cfv = (uint64_t)__ldg(cand_f + u);
+        W.cf[lane] = make_uint2((uint32_t)cfv, (uint32_t)(cfv >> 32));
         W.cg[lane] = make_uint2((uint32_t)cg0, (uint32_t)(cg0 >> 32));
         W.critf[lane] = critf;
         W.dp[lane] = dp;
@@ -583,7 +591,8 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
         const int src = item & 31, t = item >> 5;
         const bool fn = (W.critf[src] >> t) & 1u;
         if (!live) continue;
-        const uint32_t del = target_del<D>(T, t, fn, W.lowpos[src], W.dp[src], W.cf, W.cg, src);
+        const uint32_t del = target_del<D>(T, t, fn, W.lowpos[src], W.dp[src], W.cf[src], W.cg[src], cand_f,
+                                           row0 + W.sx[src], g);
         if (del == 0xFFFFFFFFu) { nint++; continue; }
         const int X = 32 + W.sx[src] + (int)(del & 3) - 1;
         const int row = (int)((del >> 4) & 3) * 4 + (int)((del >> 2) & 3);   // (dz+1) * 4 + (dy+1)
