@@ -502,7 +502,16 @@ def main():
         (dec, _, _), tdec = timed(lambda: ctx.decode_edits(sb, fhat=fht), 2)
         ga, tapp = timed(lambda: ctx.apply_edits(fht, xi, dec), 2)
         nbytes = int(sb.numel())
-        codec = {"format": "version 2 (lossless values relative to fhat)", "v1_stream_bytes": int(sb1.numel()),
+        t0p = time.perf_counter()
+        packed = dmtz.pack_edit_stream(sb)
+        pack_s = time.perf_counter() - t0p
+        base = di.base_compressed_bytes(f, xi)
+        ocr = {"original_bytes": 4 * N, "base_bytes": base["bytes"], "base_model": base["model"],
+               "cr": 4 * N / base["bytes"], "edit_stream_bytes": nbytes, "edits_packed_bytes": len(packed),
+               "edits_coder": "zlib level 1 over the edit stream (host)", "pack_seconds": pack_s,
+               "ocr": 4 * N / (base["bytes"] + len(packed)), "edit_ratio": r.n_edits / N,
+               "definition": "CR = original / base; OCR = original / (base + packed edits) (P:291)"}
+        codec = {"ocr": ocr, "format": "version 2 (lossless values relative to fhat)", "v1_stream_bytes": int(sb1.numel()),
                  "n_edits": r.n_edits, "stream_bytes": nbytes, "bytes_per_edit": nbytes / max(r.n_edits, 1),
                  "edit_ratio": r.n_edits / N, "stream_fraction_of_original": nbytes / (4 * N),
                  "encode_ms": tenc[-1], "decode_ms": tdec[-1], "apply_ms": tapp[-1],

@@ -63,6 +63,7 @@ def _L():
         L.dmtz_gen_xi.argtypes = [P, i64, ctypes.c_double]
         L.dmtz_gen_xi.restype = ctypes.c_float
         L.dmtz_gen_lorenzo.argtypes = [P, i64, i64, i64, ctypes.c_float, P]
+        L.dmtz_gen_lorenzo_codes.argtypes = [P, i64, i64, i64, ctypes.c_float, P, P]
         L.dmtz_gen_uniform_noise.argtypes = [P, i64, ctypes.c_float, ctypes.c_uint64, P]
         _lib = L
     return _lib
@@ -102,6 +103,33 @@ def lorenzo(f: np.ndarray, xi: float) -> np.ndarray:
     out = np.empty_like(f)
     _L().dmtz_gen_lorenzo(_p(f), nx, ny, nz, ctypes.c_float(xi), _p(out))
     return out
+
+
+LORENZO_RAW = 0x7FFFFFFF
+
+
+def lorenzo_codes(f: np.ndarray, xi: float):
+    """(fhat, codes): the Lorenzo quantizer's integer codes (LORENZO_RAW = stored verbatim)."""
+    f = np.ascontiguousarray(f, np.float32)
+    nx, ny, nz = _nxyz(f.shape)
+    out = np.empty_like(f)
+    codes = np.empty(f.shape, np.int32)
+    _L().dmtz_gen_lorenzo_codes(_p(f), nx, ny, nz, ctypes.c_float(xi), _p(out), _p(codes))
+    return out, codes
+
+
+def base_compressed_bytes(f: np.ndarray, xi: float) -> dict:
+    """Size model of the SZ3 stand-in's compressed stream (for CR and OCR): the
+    entropy of its integer quantization codes (the ideal size of SZ3's Huffman stage)
+    plus the verbatim float32 values, plus a 4 B per distinct code table."""
+    _, codes = lorenzo_codes(f, xi)
+    raw = codes == LORENZO_RAW
+    _, cnt = np.unique(codes[~raw], return_counts=True)
+    p = cnt / max(cnt.sum(), 1)
+    bits = float(-(cnt * np.log2(p)).sum()) if cnt.size else 0.0
+    nbytes = int(np.ceil(bits / 8)) + 4 * int(raw.sum()) + 4 * int(cnt.size)
+    return {"bytes": nbytes, "n_verbatim": int(raw.sum()), "bits_per_value": bits / max(codes.size, 1),
+            "model": "entropy of the Lorenzo codes + verbatim floats + code table"}
 
 
 def uniform_noise(f: np.ndarray, xi: float, seed: int) -> np.ndarray:

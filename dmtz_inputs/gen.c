@@ -208,7 +208,17 @@ float dmtz_gen_xi(const float* f, int64_t N, double eps) {
  * reconstructed values, out-of-domain neighbours = 0:
  *   k = rint((f - pred) / 2xi); |k| > 32767 -> fhat = f (unpredictable)
  *   else fhat = RN32(pred + 2 xi k); post-check |fhat - f| <= xi, else fhat = f. */
+/* codes (optional): the quantization integer k of every vertex, or LORENZO_RAW when the
+ * value is stored verbatim (unpredictable, |k| > 32767, or the post-check failed) --
+ * what an SZ3-like compressor entropy-codes (used only for the CR / OCR size model). */
+#define LORENZO_RAW 0x7FFFFFFF
+int dmtz_gen_lorenzo_codes(const float* f, int64_t nx, int64_t ny, int64_t nz, float xi, float* fhat,
+                           int32_t* codes);
 int dmtz_gen_lorenzo(const float* f, int64_t nx, int64_t ny, int64_t nz, float xi, float* fhat) {
+  return dmtz_gen_lorenzo_codes(f, nx, ny, nz, xi, fhat, 0);
+}
+int dmtz_gen_lorenzo_codes(const float* f, int64_t nx, int64_t ny, int64_t nz, float xi, float* fhat,
+                           int32_t* codes) {
   double two_xi = 2.0 * (double)xi;
   for (int64_t z = 0; z < nz; z++)
     for (int64_t y = 0; y < ny; y++)
@@ -221,11 +231,13 @@ int dmtz_gen_lorenzo(const float* f, int64_t nx, int64_t ny, int64_t nz, float x
 #undef H
         double k = rint(((double)f[v] - pred) / two_xi);
         float out;
-        if (fabs(k) > 32767.0) out = f[v];
+        int32_t code = (int32_t)k;
+        if (fabs(k) > 32767.0) { out = f[v]; code = LORENZO_RAW; }
         else out = (float)(pred + two_xi * k);
         double e = (double)out - (double)f[v];
-        if (!(fabs(e) <= (double)xi)) out = f[v];
+        if (!(fabs(e) <= (double)xi)) { out = f[v]; code = LORENZO_RAW; }
         fhat[v] = out;
+        if (codes) codes[v] = code;
       }
   return 0;
 }

@@ -154,6 +154,22 @@ EXPORTED = ("dmtz_ctx_create", "dmtz_ctx_destroy", "dmtz_workspace_bytes", "dmtz
             "dmtz_critical_prf", "dmtz_separatrix_prf", "dmtz_last_trace_levels")
 
 
+def pack_edit_stream(stream: torch.Tensor, level: int = 1) -> bytes:
+    """The stored artifact of the edits ("the quantized edits are losslessly
+    compressed"): the device edit stream (dmtz_encode_edits) copied to the host and put
+    through a general-purpose lossless coder (zlib).  Not on the hot path."""
+    import zlib
+    return zlib.compress(stream.cpu().numpy().tobytes(), level)
+
+
+def unpack_edit_stream(blob: bytes, device=None) -> torch.Tensor:
+    """Inverse of pack_edit_stream: the edit stream as a uint8 tensor (for dmtz_decode_edits)."""
+    import zlib
+    a = np.frombuffer(zlib.decompress(blob), dtype=np.uint8).copy()
+    t = torch.from_numpy(a)
+    return t.to(device) if device is not None else t
+
+
 def last_trace_levels() -> list:
     """Connectors per escalation level of this thread's last trace (dmtz_last_trace_levels)."""
     out = (ctypes.c_int64 * 10)()

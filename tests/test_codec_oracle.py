@@ -98,3 +98,35 @@ def test_v2_roundtrip_and_size(sign):
     assert len(v2) < len(v1)
     d2, _, _ = ec.decode(v2, fhat=fh)
     assert np.array_equal(ec.apply(fh, d2, xi, 6).view(np.uint32), r["g"].view(np.uint32))
+
+
+def test_base_size_model_entropy():
+    """The SZ3 stand-in's size model (CR = original / compressed): an all-equal code
+    array has zero entropy (only the code table), a uniform 4-symbol one 2 bits a value,
+    and the Lorenzo codes of C1 are far below 32 bits a value."""
+    f = np.full((16, 16), 1.5, np.float32)
+    s = di.base_compressed_bytes(f, 1e-3)
+    assert s["n_verbatim"] == 0 and s["bits_per_value"] < 0.05
+    f, fh, xi, _ = di.config_inputs("C1")
+    s = di.base_compressed_bytes(f, xi)
+    _, codes = di.lorenzo_codes(f, xi)
+    _, cnt = np.unique(codes, return_counts=True)
+    p = cnt / cnt.sum()
+    assert abs(s["bits_per_value"] - float(-(p * np.log2(p)).sum())) < 1e-9
+    assert 4 * f.size / s["bytes"] > 4          # CR of the stand-in on a smooth field
+
+
+def test_edit_stream_pack_roundtrip_and_ocr():
+    """The stored edit artifact: the codec stream through the lossless stage and
+    back; OCR = original bytes / (base bytes + packed edit bytes) is below CR."""
+    import torch
+    import paper_2409_17346_b200 as dmtz
+    f, fh, xi, _ = di.config_inputs("C1")
+    r = oracle.correct(f, fh, xi)
+    stream = np.frombuffer(ec.encode(r["edits"], xi, 6), np.uint8)
+    blob = dmtz.pack_edit_stream(torch.from_numpy(stream.copy()))
+    back = dmtz.unpack_edit_stream(blob).numpy()
+    assert back.tobytes() == stream.tobytes()
+    base = di.base_compressed_bytes(f, xi)["bytes"]
+    cr, ocr = 4 * f.size / base, 4 * f.size / (base + len(blob))
+    assert ocr < cr and len(blob) <= len(stream) + 16
