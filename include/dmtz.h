@@ -122,16 +122,58 @@ typedef struct {
                                  u + {0,1}^D changed) */
   int64_t cells_evaluated;    /* sum over sweeps of false cells whose target rule was evaluated */
   int64_t anchors_replayed;   /* sum over sweeps of anchors whose unchanged targets were replayed */
+  int64_t halo_faces_sent;    /* world > 1: halo faces this rank sent over the rounds */
+  int64_t halo_faces_skipped; /* world > 1: faces skipped (no edit touched their 3 planes) */
 } dmtz_stats;
 
 typedef struct dmtz_ctx dmtz_ctx;
 
-/* Create a context for a global grid.  world == 1 only in this release (the
- * multi-GPU slab layer drives single-rank contexts over owned slabs);
- * nccl_unique_id must be NULL.  cuda_device: the device the caller's buffers live on. */
+/* Create a context for a global grid on `cuda_device` (the device the caller's
+ * buffers live on).
+ *   world == 1: the whole grid; nccl_unique_id must be NULL.
+ *   world > 1 (3D only, multi-GPU C-loop): rank `rank` of
+ *     `world` owns the z-planes [z0, z1) of dmtz_local_slab(nz, world, rank, ...); its
+ *     dmtz_correct takes and returns the OWNED planes only (f, fhat, g_out are
+ *     nx * ny * (z1 - z0) floats) and exchanges halo planes with ranks rank +- 1.
+ *     nccl_unique_id (128 bytes, the same on every rank, from dmtz_nccl_unique_id on one
+ *     rank) makes the context own an NCCL communicator (libnccl.so.2 is loaded at run
+ *     time); NULL leaves the transport to dmtz_ctx_set_transport.
+ *   world == 1 with an nccl_unique_id runs the same distributed driver on a one-rank
+ *     communicator (one slab, no halos): the NCCL path on one GPU.
+ * Errors: DMTZ_E_DIMS (an axis < 2, world > 1 with nz < 3 world or a 2D grid),
+ * DMTZ_E_ARG (rank out of range), DMTZ_E_NCCL (NCCL missing or its initialisation
+ * failed), DMTZ_E_CUDA. */
 dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* global, int rank, int world,
                             const void* nccl_unique_id, int cuda_device);
 void dmtz_ctx_destroy(dmtz_ctx* ctx);
+
+/* The z-slab partition of the multi-GPU C-loop: rank `rank` of `world`
+ * owns planes [*z0, *z1) (contiguous, balanced, at least 3 planes each); its local grid
+ * is [*lz0, *lz1) = the owned planes plus up to 3 halo planes below and above -- a
+ * target lies within [-1, 2]^3 of its false cell's anchor, so the cells that can
+ * target owned vertices are anchored in [z0 - 2, z1 + 1) and their criticality reads
+ * [z0 - 3, z1 + 3).  Host only; DMTZ_E_ARG if nz < 3 world or rank is out of range. */
+dmtz_status dmtz_local_slab(int64_t nz, int world, int rank, int64_t* z0, int64_t* z1, int64_t* lz0, int64_t* lz1);
+
+/* Transport of the multi-GPU C-loop.  Each callback returns 0 on success and must
+ * leave the data in place, ordered after the work already enqueued on `stream`, when
+ * it returns (an NCCL implementation enqueues on `stream`; a host-staged one
+ * synchronises it).  exchange: for i < n, send send_bytes[i] bytes at device pointer
+ * send[i] to rank peers[i] and receive recv_bytes[i] bytes from peers[i] into recv[i]
+ * (a rank appears at most once per call; both sides post matching pairs).
+ * allreduce_sum_i64: sum dev_buf[0 .. n) over all ranks, in place. */
+typedef struct {
+  void* user;
+  int (*exchange)(void* user, int n, const int* peers, const void* const* send, const size_t* send_bytes,
+                  void* const* recv, const size_t* recv_bytes, dmtz_stream_t stream);
+  int (*allreduce_sum_i64)(void* user, int64_t* dev_buf, int n, dmtz_stream_t stream);
+} dmtz_transport;
+/* Install (or, with NULL, remove) a transport for a world > 1 context that has no
+ * NCCL communicator.  The struct is copied. */
+dmtz_status dmtz_ctx_set_transport(dmtz_ctx* ctx, const dmtz_transport* transport);
+/* An NCCL unique id (128 bytes into `out`) for dmtz_ctx_create; DMTZ_E_NCCL if
+ * libnccl.so.2 cannot be loaded. */
+dmtz_status dmtz_nccl_unique_id(void* out);
 
 /* Bytes of device workspace dmtz_correct / dmtz_compute_gradient / trace need. */
 size_t dmtz_workspace_bytes(const dmtz_ctx* ctx, const dmtz_correct_opts* opts);
@@ -158,6 +200,15 @@ dmtz_status dmtz_critical_mask(dmtz_ctx* ctx, const void* codes, uint32_t* crit,
  * edits_capacity entries), *n_edits (host) and *stats (host).  On
  * DMTZ_E_CAPACITY g_out and *n_edits are valid and the list holds the first
  * edits_capacity entries. */
+/* Multi-GPU (world > 1 context): call on every rank with its OWNED planes of f, fhat
+ * and g_out; the edit list holds the rank's owned edits (global vertex indices,
+ * sorted), so the ranks' lists in rank order are the one-GPU list, and g_out the
+ * owned planes of the one-GPU g (bit-identical: the rounds are the same synchronous
+ * rounds).  Per round: the halo planes a neighbour changed are exchanged (faces whose
+ * 3 boundary planes no edit touched are skipped, both sides know it from the previous
+ * round's reduction), the round runs on the local grid, and the round counters plus
+ * per-face change flags are summed over the ranks; every rank applies the same stop
+ * rule.  stats are global (summed over ranks). */
 dmtz_status dmtz_correct(dmtz_ctx* ctx, const float* f, const float* fhat,
                          const dmtz_correct_opts* opts, void* workspace, size_t workspace_bytes,
                          float* g_out, dmtz_edit* edits, int64_t edits_capacity,

@@ -52,7 +52,8 @@ class _Stats(ctypes.Structure):
                 ("launches", ctypes.c_int64), ("sweep_ms", ctypes.c_double), ("screen_ms", ctypes.c_double),
                 ("decode_ms", ctypes.c_double), ("screen_ms_full", ctypes.c_double), ("n_screen_full", ctypes.c_int64),
                 ("anchors_recomputed", ctypes.c_int64), ("anchors_decoded", ctypes.c_int64),
-                ("cells_evaluated", ctypes.c_int64), ("anchors_replayed", ctypes.c_int64)]
+                ("cells_evaluated", ctypes.c_int64), ("anchors_replayed", ctypes.c_int64),
+                ("halo_faces_sent", ctypes.c_int64), ("halo_faces_skipped", ctypes.c_int64)]
 
 
 class _SStats(ctypes.Structure):
@@ -123,6 +124,12 @@ def _load():
     L.dmtz_last_error.restype = ctypes.c_char_p
     L.dmtz_last_trace_levels.argtypes = [P, i32]
     L.dmtz_last_trace_levels.restype = ctypes.c_int
+    L.dmtz_local_slab.argtypes = [i64, i32, i32, P, P, P, P]
+    L.dmtz_local_slab.restype = ctypes.c_int
+    L.dmtz_ctx_set_transport.argtypes = [P, P]
+    L.dmtz_ctx_set_transport.restype = ctypes.c_int
+    L.dmtz_nccl_unique_id.argtypes = [P]
+    L.dmtz_nccl_unique_id.restype = ctypes.c_int
     for fn in ("dmtz_ctx_create", "dmtz_compute_gradient", "dmtz_critical_mask", "dmtz_correct", "dmtz_correct_host",
                "dmtz_trace_separatrices", "dmtz_version", "dmtz_slab_begin", "dmtz_slab_round", "dmtz_slab_end",
                "dmtz_slab_halo", "dmtz_trace_separatrices_range", "dmtz_preserve", "dmtz_slab_round_async",
@@ -151,7 +158,8 @@ EXPORTED = ("dmtz_ctx_create", "dmtz_ctx_destroy", "dmtz_workspace_bytes", "dmtz
             "dmtz_slab_halo", "dmtz_trace_separatrices_range", "dmtz_slab_round_async", "dmtz_preserve_sep_bytes",
             "dmtz_preserve",
             "dmtz_edit_stream_bound", "dmtz_encode_edits", "dmtz_decode_edits", "dmtz_apply_edits",
-            "dmtz_critical_prf", "dmtz_separatrix_prf", "dmtz_last_trace_levels")
+            "dmtz_critical_prf", "dmtz_separatrix_prf", "dmtz_last_trace_levels", "dmtz_local_slab",
+            "dmtz_ctx_set_transport", "dmtz_nccl_unique_id")
 
 
 def pack_edit_stream(stream: torch.Tensor, level: int = 1) -> bytes:
@@ -214,7 +222,8 @@ def _stats_dict(st, status):
                 sweep_ms=st.sweep_ms, screen_ms=st.screen_ms, decode_ms=st.decode_ms,
                 screen_ms_full=st.screen_ms_full, n_screen_full=st.n_screen_full,
                 anchors_recomputed=st.anchors_recomputed, anchors_decoded=st.anchors_decoded,
-                cells_evaluated=st.cells_evaluated, anchors_replayed=st.anchors_replayed)
+                cells_evaluated=st.cells_evaluated, anchors_replayed=st.anchors_replayed,
+                halo_faces_sent=st.halo_faces_sent, halo_faces_skipped=st.halo_faces_skipped)
 
 
 class Context:

@@ -11,6 +11,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <algorithm>
+#include <vector>
 #include <utility>
 
 #include "../../include/dmtz.h"
@@ -56,7 +58,15 @@ struct dmtz_ctx {
   struct LoopGraph* graph = nullptr;
   cudaStream_t cap_stream = nullptr;  // private stream the loop body is captured on (the caller's may be the legacy stream)
   uint32_t* sdirty = nullptr;  // dmtz_preserve: per-anchor "code changed since the last S-round" bits
+  // multi-GPU (dist): this rank's z-slab of the global grid (g above is the LOCAL grid)
+  int dist = 0;
+  int64_t gnz = 0, z0 = 0, z1 = 0, lz0 = 0, lz1 = 0;
+  dmtz_transport tr = {nullptr, nullptr, nullptr};
+  int has_tr = 0;
+  void* nccl_comm = nullptr;
 };
+
+#include "dmtz_dist.cuh"  // needs the context above
 
 // Every entry point runs on the context's device and restores the caller's current
 // device on return (the caller's thread may have another device current).
@@ -97,7 +107,7 @@ inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 // Workspace layout (offsets from the base, each 256-B aligned)
 struct Layout {
   size_t cand_f, cand_g, crit_f, crit_g, lowpos, lb, state, tcache, ncache, tbits, counters, edit_bc, ebits, fmark, vchg, units,
-      units2, frontier, keyinfo, trace, total;
+      units2, frontier, keyinfo, dist, trace, total;
   int64_t fwords;  // frontier bitmap words (one bit per row-block unit)
 };
 
@@ -129,6 +139,11 @@ Layout layout_for(const dmtz_ctx* c) {
   L.units2 = o; o += align_up((size_t)rg.units * 4);
   L.frontier = o; o += align_up(L.fwords * 4 + 64);
   L.keyinfo = o; o += align_up(sizeof(KeyInfo));
+  L.dist = 0;
+  if (c->dist) {  // local f, fhat, g, halo staging (f32 each) + the reduced counters
+    L.dist = o;
+    o += align_up(4 * N * sizeof(float) + (size_t)(14 + 2 * c->world) * 8 * 2);
+  }
   L.trace = o; o += align_up(trace_scratch_bytes(c->g, c->D));
   L.total = o;
   return L;
@@ -802,6 +817,126 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
 
 }  // namespace
 
+// The multi-GPU C-loop (dmtz_dist.cuh): one rank's slab, its owned planes in and out.
+static dmtz_status correct_dist(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
+                                char* ws, size_t wsb, const Layout& L, float* g_out, dmtz_edit* edits, int64_t cap,
+                                int64_t* n_edits, dmtz_stats* st, cudaStream_t s) {
+  if (!c->has_tr || !c->tr.exchange || !c->tr.allreduce_sum_i64) {
+    set_err("multi-GPU context without a transport (NCCL id or dmtz_ctx_set_transport)");
+    st->status = DMTZ_E_NCCL;
+    return DMTZ_E_NCCL;
+  }
+  const Grid& g = c->g;  // the local grid
+  const int64_t N = g.N, sz = g.sz;
+  float* floc = (float*)(ws + L.dist);
+  float* fhloc = floc + N;
+  float* gloc = fhloc + N;
+  float* stage = gloc + N;
+  long long* dcnt = (long long*)(stage + N);
+  const int nout = 12 + 2 * c->world;
+  long long* hcnt = (long long*)c->host_cnt;  // pinned, 512 B >= 8 (14 + 2 world) for world <= 25
+  if (nout > 64) { set_err("world %d too large for the pinned counter block", c->world); return DMTZ_E_ARG; }
+  const int64_t oz0 = c->z0 - c->lz0, oz1 = c->z1 - c->lz0, nown = oz1 - oz0;
+  auto comm_fail = [&](const char* what) {
+    set_err("transport %s failed", what);
+    st->status = DMTZ_E_NCCL;
+    return DMTZ_E_NCCL;
+  };
+  // owned planes in; halo planes of f and fhat from the neighbours (once)
+  CK(cudaMemcpyAsync(floc + oz0 * sz, f, (size_t)(nown * sz) * 4, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(fhloc + oz0 * sz, fhat, (size_t)(nown * sz) * 4, cudaMemcpyDeviceToDevice, s));
+  for (float* a : {floc, fhloc}) {
+    HaloPlan h = halo_plan(c, g, a, a, 1, 1, 1, 1);
+    if (run_exchange(c, h, s)) return comm_fail("exchange");
+  }
+  dmtz_slab sl;
+  sl.z_offset = c->lz0;
+  sl.own_z0 = oz0;
+  sl.own_z1 = oz1;
+  sl.anchor_z0 = std::max<int64_t>(0, c->z0 - 2) - c->lz0;
+  sl.anchor_z1 = std::min<int64_t>(c->gnz, c->z1 + 1) - c->lz0;
+  dmtz_status bst = dmtz_slab_begin(c, floc, fhloc, o, &sl, ws, wsb, gloc, (dmtz_stream_t)s);
+  // every rank learns whether any rank failed its validation (no rank may enter the
+  // round loop alone: its exchanges would wait forever)
+  hcnt[0] = bst != DMTZ_OK ? 1 : 0;
+  CK(cudaMemcpyAsync(dcnt, hcnt, 8, cudaMemcpyHostToDevice, s));
+  if (c->tr.allreduce_sum_i64(c->tr.user, (int64_t*)dcnt, 1, (dmtz_stream_t)s)) return comm_fail("allreduce");
+  CK(cudaMemcpyAsync(hcnt, dcnt, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (bst != DMTZ_OK) { st->status = bst; return bst; }
+  if (hcnt[0]) { set_err("another rank failed its input validation"); st->status = DMTZ_E_BOUND; return DMTZ_E_BOUND; }
+  WS<3> W(ws, L, g);
+  const RowGeom rg = row_geom(g);
+  const int64_t per_plane = g.ny * rg.wpr;
+  const int64_t nface = std::min<int64_t>(3, nown);
+  const int64_t max_rounds = o->max_rounds ? o->max_rounds : c->dims.nx * c->dims.ny * c->gnz * (int64_t)(o->q_cap + 1);
+  long long* dround = dcnt + nout;  // slab_round_async's own 12 counters (unused beyond the kernel)
+  std::vector<long long> tot(nout, 0);
+  int status = -1;
+  int64_t r = 0;
+  while (status < 0) {
+    r++;
+    if (r > 1) {  // halo planes of g the neighbours changed in round r - 1
+      const int lo_peer = c->rank > 0 ? (int)tot[13 + 2 * (c->rank - 1)] : 0;          // its upper face
+      const int hi_peer = c->rank < c->world - 1 ? (int)tot[12 + 2 * (c->rank + 1)] : 0;  // its lower face
+      const int lo_me = (int)tot[12 + 2 * c->rank], hi_me = (int)tot[13 + 2 * c->rank];
+      HaloPlan h = halo_plan(c, g, gloc, stage, lo_me, lo_peer, hi_me, hi_peer);
+      for (int i = 0; i < h.n; i++) {
+        if (h.sbytes[i]) st->halo_faces_sent++;
+        else st->halo_faces_skipped++;
+      }
+      if (run_exchange(c, h, s)) return comm_fail("exchange");
+      for (int i = 0; i < h.n; i++)
+        if (h.rz1[i] > h.rz0[i]) {
+          const dmtz_status hs = dmtz_slab_halo(c, &sl, ws, wsb, gloc, stage + h.rz0[i] * sz, h.rz0[i], h.rz1[i], r - 1,
+                                                (dmtz_stream_t)s);
+          if (hs) return hs;
+        }
+    }
+    // this round's change bitmap rows of the owned face planes: cleared, so that after the
+    // round they hold exactly this round's edits there (the face flags)
+    uint32_t* vround = W.vchg + (int64_t)(r & 1) * W.vwords;
+    CK(cudaMemsetAsync(vround + oz0 * per_plane, 0, (size_t)(nface * per_plane) * 4, s));
+    CK(cudaMemsetAsync(vround + (oz1 - nface) * per_plane, 0, (size_t)(nface * per_plane) * 4, s));
+    const dmtz_status rs = dmtz_slab_round_async(c, floc, fhloc, o, &sl, ws, wsb, gloc, r, (int64_t*)dround,
+                                                 (dmtz_stream_t)s);
+    if (rs) return rs;
+    k_dist_counters<<<1, 256, 0, s>>>(W.dc, r, dcnt, nout, vround, g, rg, oz0, oz0 + nface, oz1 - nface, oz1,
+                                      c->rank);
+    CK(cudaGetLastError());
+    if (c->tr.allreduce_sum_i64(c->tr.user, (int64_t*)dcnt, nout, (dmtz_stream_t)s)) return comm_fail("allreduce");
+    CK(cudaMemcpyAsync(hcnt, dcnt, (size_t)nout * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int i = 0; i < nout; i++) tot[i] = hcnt[i];
+    if (r == 1) {
+      st->n_false_round0 = tot[0];
+      for (int k = 0; k < 8; k++) st->false_by_kind_round0[k] = tot[4 + k];
+    }
+    st->sweeps++;
+    status = dist_stop(r, tot.data(), max_rounds);
+    if (status != DMTZ_OK && status >= 0) st->rounds = r;
+    else if (status < 0) st->rounds = r;
+  }
+  if (status == DMTZ_E_INTERNAL) { set_err("internal invariant violated"); st->status = status; return DMTZ_E_INTERNAL; }
+  int64_t nl = 0;
+  const dmtz_status es = dmtz_slab_end(c, &sl, ws, wsb, gloc, edits, cap, n_edits, &nl, (dmtz_stream_t)s);
+  if (es != DMTZ_OK && es != DMTZ_E_CAPACITY) return es;
+  CK(cudaMemcpyAsync(g_out, gloc + oz0 * sz, (size_t)(nown * sz) * 4, cudaMemcpyDeviceToDevice, s));
+  // global edit counts
+  hcnt[0] = *n_edits;
+  hcnt[1] = nl;
+  CK(cudaMemcpyAsync(dcnt, hcnt, 16, cudaMemcpyHostToDevice, s));
+  if (c->tr.allreduce_sum_i64(c->tr.user, (int64_t*)dcnt, 2, (dmtz_stream_t)s)) return comm_fail("allreduce");
+  CK(cudaMemcpyAsync(hcnt, dcnt, 16, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  st->n_edited = hcnt[0];
+  st->n_lossless = hcnt[1];
+  st->n_quantized = hcnt[0] - hcnt[1];
+  const dmtz_status fin = es == DMTZ_E_CAPACITY && status == DMTZ_OK ? DMTZ_E_CAPACITY : (dmtz_status)status;
+  st->status = fin;
+  return fin;
+}
+
 extern "C" {
 
 int dmtz_version(void) { return 1; }
@@ -843,7 +978,16 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
             (long long)d->nz);
     return DMTZ_E_DIMS;
   }
-  if (world != 1 || rank != 0 || nccl_id != nullptr) { set_err("world must be 1 (slab layer drives per-rank contexts)"); return DMTZ_E_ARG; }
+  if (world < 1 || rank < 0 || rank >= world) { set_err("rank %d of world %d", rank, world); return DMTZ_E_ARG; }
+  const bool dist = world > 1 || nccl_id != nullptr;
+  int64_t z0 = 0, z1 = d->nz, lz0 = 0, lz1 = d->nz;
+  if (dist) {
+    if (d->nz == 1) { set_err("the multi-GPU C-loop needs a 3D grid"); return DMTZ_E_DIMS; }
+    if (local_slab(d->nz, world, rank, &z0, &z1, &lz0, &lz1) != DMTZ_OK) {
+      set_err("%lld planes cannot be split over %d ranks (>= 3 planes each)", (long long)d->nz, world);
+      return DMTZ_E_DIMS;
+    }
+  }
   struct RestoreDevice {
     int prev = -1;
     ~RestoreDevice() { if (prev >= 0) cudaSetDevice(prev); }
@@ -853,8 +997,10 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
   dmtz_ctx* c = new (std::nothrow) dmtz_ctx();
   if (!c) return DMTZ_E_OOM;
   c->dims = *d;
-  c->g.nx = d->nx; c->g.ny = d->ny; c->g.nz = d->nz;
-  c->g.N = d->nx * d->ny * d->nz;
+  c->dist = dist ? 1 : 0;
+  c->gnz = d->nz; c->z0 = z0; c->z1 = z1; c->lz0 = lz0; c->lz1 = lz1;
+  c->g.nx = d->nx; c->g.ny = d->ny; c->g.nz = lz1 - lz0;   // the local grid (the whole grid unless dist)
+  c->g.N = d->nx * d->ny * c->g.nz;
   c->g.sy = d->nx; c->g.sz = d->nx * d->ny;
   c->D = d->nz == 1 ? 2 : 3;
   c->device = cuda_device;
@@ -882,6 +1028,24 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
       return DMTZ_E_CUDA;
     }
   }
+  if (nccl_id) {  // the context's own NCCL communicator (a collective call over the world)
+    NcclApi* A = nccl_api();
+    if (!A) { set_err("libnccl.so.2 cannot be loaded"); dmtz_ctx_destroy(c); return DMTZ_E_NCCL; }
+    ncclUniqueId id;
+    memcpy(&id, nccl_id, sizeof id);
+    ncclComm_t comm = nullptr;
+    const ncclResult_t r = A->CommInitRank(&comm, world, id, rank);
+    if (r != ncclSuccess) {
+      set_err("ncclCommInitRank: %s", A->GetErrorString ? A->GetErrorString(r) : "error");
+      dmtz_ctx_destroy(c);
+      return DMTZ_E_NCCL;
+    }
+    c->nccl_comm = comm;
+    c->tr.user = comm;
+    c->tr.exchange = nccl_exchange;
+    c->tr.allreduce_sum_i64 = nccl_allreduce;
+    c->has_tr = 1;
+  }
   *out = c;
   return DMTZ_OK;
 }
@@ -889,6 +1053,9 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
 void dmtz_ctx_destroy(dmtz_ctx* c) {
   if (!c) return;
   DeviceGuard dg_(c);
+  if (c->nccl_comm) {
+    if (NcclApi* A = nccl_api()) A->CommDestroy((ncclComm_t)c->nccl_comm);
+  }
   if (c->graph) { c->graph->reset(); delete c->graph; }
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->host_cnt) cudaFreeHost(c->host_cnt);
@@ -949,6 +1116,8 @@ dmtz_status dmtz_correct(dmtz_ctx* c, const float* f, const float* fhat, const d
   }
   cudaStream_t s = (cudaStream_t)stream;
   dmtz_status r;
+  if (c->dist) return correct_dist(c, f, fhat, o, (char*)workspace, workspace_bytes, L, g_out, edits, edits_capacity,
+                                   n_edits, st, s);
   if (c->D == 3) r = correct_impl<3>(c, f, fhat, o, (char*)workspace, L, g_out, edits, edits_capacity, n_edits, st, s);
   else r = correct_impl<2>(c, f, fhat, o, (char*)workspace, L, g_out, edits, edits_capacity, n_edits, st, s);
   if (r == DMTZ_E_CUDA) st->status = r;
@@ -1378,6 +1547,36 @@ dmtz_status dmtz_separatrix_prf(dmtz_ctx* c, const dmtz_seps* A, int64_t na, con
   out->n_orig = na;
   out->n_rec = nb;
   out->n_match = (int64_t)hc->pad[0];
+  return DMTZ_OK;
+}
+
+dmtz_status dmtz_local_slab(int64_t nz, int world, int rank, int64_t* z0, int64_t* z1, int64_t* lz0, int64_t* lz1) {
+  if (!z0 || !z1 || !lz0 || !lz1) { set_err("NULL argument"); return DMTZ_E_ARG; }
+  const dmtz_status r = local_slab(nz, world, rank, z0, z1, lz0, lz1);
+  if (r) set_err("%lld planes cannot be split over %d ranks (rank %d)", (long long)nz, world, rank);
+  return r;
+}
+
+dmtz_status dmtz_ctx_set_transport(dmtz_ctx* c, const dmtz_transport* t) {
+  if (!c) { set_err("NULL argument"); return DMTZ_E_ARG; }
+  if (c->nccl_comm) { set_err("the context owns an NCCL communicator"); return DMTZ_E_ARG; }
+  if (!t) {
+    c->has_tr = 0;
+    return DMTZ_OK;
+  }
+  if (!t->exchange || !t->allreduce_sum_i64) { set_err("transport without callbacks"); return DMTZ_E_ARG; }
+  c->tr = *t;
+  c->has_tr = 1;
+  return DMTZ_OK;
+}
+
+dmtz_status dmtz_nccl_unique_id(void* out) {
+  if (!out) { set_err("NULL argument"); return DMTZ_E_ARG; }
+  NcclApi* A = nccl_api();
+  if (!A) { set_err("libnccl.so.2 cannot be loaded"); return DMTZ_E_NCCL; }
+  ncclUniqueId id;
+  if (A->GetUniqueId(&id) != ncclSuccess) { set_err("ncclGetUniqueId failed"); return DMTZ_E_NCCL; }
+  memcpy(out, &id, sizeof id);
   return DMTZ_OK;
 }
 

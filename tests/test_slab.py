@@ -187,3 +187,18 @@ def test_trace_distributed_emulated(name, shape, world):
         exp = [cells_of(full, int(i)) for i in sel[:: max(1, len(sel) // 200)]]
         sub = got_c[:: max(1, len(sel) // 200)]
         assert all(torch.equal(a, b) for a, b in zip(sub, exp))
+
+
+def test_library_local_slab_matches_plan():
+    """dmtz_local_slab (the library's partition, a host function) equals slab.plan."""
+    from paper_2409_17346_b200 import dist as dd
+    for nz in range(3, 60):
+        for w in range(1, nz // 3 + 1):
+            for r in range(w):
+                p = slab.plan(nz, w, r)
+                assert dd.local_slab(nz, w, r) == (p.z0, p.z1, p.lz0, p.lz1)
+    import paper_2409_17346_b200 as d
+    with pytest.raises(d.DmtzError):
+        dd.local_slab(8, 3, 0)     # fewer than 3 planes per rank
+    with pytest.raises(d.DmtzError):
+        dd.local_slab(30, 3, 3)    # rank out of range
