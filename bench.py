@@ -286,6 +286,93 @@ def chunked_trace(ctx, codes, dev, stream, budget, sizes):
             "counts_match_full_sizing": nb == sizes["n_branches"] and nc == sizes["n_cells"]}
 
 
+def dist_bench(args, f, fh, xi, cfg, world, rank, local):
+    """bench.py --gpus N (torchrun, one rank per GPU): the library's multi-GPU C-loop
+    (dmtz_correct on a world-N context with its own NCCL communicator; z-slabs, halo
+    exchange with face skipping, counter reduction per round).  Same step and metric
+    as N = 1: the C-loop to its fixed point with full-sweep rounds, value = global N x
+    sweeps / step time; device time = max over ranks (barrier + sync on both sides)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2409_17346_b200.dist import DistContext, nccl_unique_id
+    dev = torch.device("cuda", local)
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    ctx = DistContext(f.shape, rank, world, device=dev, nccl_id=obj[0])
+    own = (slice(ctx.z0, ctx.z1),)
+    ft = torch.from_numpy(np.ascontiguousarray(f[own])).to(dev)
+    fht = torch.from_numpy(np.ascontiguousarray(fh[own])).to(dev)
+
+    def timed(fn, reps):
+        ts, out = [], None
+        for _ in range(reps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            out = fn()
+            e1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1)], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ts.append(float(t.item()))
+        return out, ts
+
+    for _ in range(args.warmup):
+        ctx.correct(ft, fht, xi, full_sweeps=True)
+    with Clocks(local) as clk:
+        rfull, times = timed(lambda: ctx.correct(ft, fht, xi, full_sweeps=True), args.steps)
+        r, tt = timed(lambda: ctx.correct(ft, fht, xi), max(3, args.steps))
+    ms, ttfp = float(np.median(times)), float(np.median(tt))
+    sweeps = rfull.stats["sweeps"]
+    N = f.size
+    value = N * sweeps / (ms * 1e-3) / 1e6
+    peaks = _peaks()
+    hbm = (peaks.get("hbm_gbs") or 6650.0) * world
+    ach = BYTES_PER_ANCHOR[3] * N / (ms / sweeps * 1e-3) / 1e9
+    # end to end: the rank's owned planes from pinned host memory, its g planes and edits back
+    fp, fhp = torch.from_numpy(np.ascontiguousarray(f[own])).pin_memory(), \
+        torch.from_numpy(np.ascontiguousarray(fh[own])).pin_memory()
+    gh = torch.empty(tuple(ft.shape), dtype=torch.float32).pin_memory()
+    eh = torch.empty((ft.numel(), 16), dtype=torch.uint8).pin_memory()
+
+    def e2e_step():
+        ft.copy_(fp, non_blocking=True)
+        fht.copy_(fhp, non_blocking=True)
+        rr = ctx.correct(ft, fht, xi, full_sweeps=True)
+        gh.copy_(rr.g, non_blocking=True)
+        eh[:rr.n_edits].copy_(rr.edits, non_blocking=True)
+        torch.cuda.synchronize()
+        return rr.n_edits
+    ne, et = timed(e2e_step, 2)
+    ems = float(np.median(et))
+    nb = torch.tensor([ne * 16 + gh.numel() * 4, fp.numel() * 8], device=dev, dtype=torch.int64)
+    dist.all_reduce(nb)
+    st = r.stats
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "Mvoxels/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"{cfg.name} {cfg.family} {'x'.join(map(str, f.shape))} rel eps {cfg.eps}",
+                           "step": "C-loop to its fixed point, every round a full sweep (full_sweeps=1)",
+                           "parallelism": f"z-slabs x{world}: dmtz_correct on world-{world} contexts (NCCL)",
+                           "sweeps_per_step": sweeps, "rounds": rfull.stats["rounds"],
+                           "l2": "inputs larger than L2"},
+                "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                             "traffic": None, "kernel": "full-sweep C-loop round over all GPUs (12 B/voxel)",
+                             "peak_source": f"MEASURED_PEAKS.json hbm_gbs x {world}"},
+                "cpu_baseline": None,
+                "e2e": {"value": N * sweeps / (ems * 1e-3) / 1e6, "unit": "Mvoxels/s", "ms_per_step": ems,
+                        "h2d_bytes_per_step": int(nb[1].item()), "d2h_bytes_per_step": int(nb[0].item())},
+                "gpu_launches": rfull.stats["launches"], "clocks": clk.summary(),
+                "time_to_fixed_point": {"time_to_fixed_point_ms": ttfp, "rounds": st["rounds"],
+                                        "halo_faces_sent": st["halo_faces_sent"],
+                                        "halo_faces_skipped": st["halo_faces_skipped"]},
+                "stats": {k: st[k] for k in ("rounds", "n_edited", "n_quantized", "n_lossless", "n_false_round0")}}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -327,8 +414,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2409_17346_b200 as dmtz
     if world > 1 or args.slab:
-        from paper_2409_17346_b200 import slab
-        return slab.bench_main(args, f, fh, xi, cfg, world, rank, local, clocks_cls=Clocks)
+        return dist_bench(args, f, fh, xi, cfg, world, rank, local)
 
     dev = torch.device("cuda", local)
     D = len(f.shape)

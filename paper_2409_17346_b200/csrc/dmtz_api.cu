@@ -308,7 +308,7 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
   if (profile) CK(cudaEventRecord(c->ev[2], s));
   k_edit_rows<D><<<clamp_blocks(nwords, 256), 256, fwords_smem * 4, s>>>(
       W.tbits, nwords, fhat, W.lb, g_out, W.state, W.dc, step, o->q_cap, fbits, g, rg, fwords_smem,
-      use_skip ? W.vchg : nullptr, W.vwords, W.ls, FastDiv((uint32_t)rg.wpr), FastDiv((uint32_t)g.ny));
+      (use_skip || fbits) ? W.vchg : nullptr, W.vwords, W.ls, FastDiv((uint32_t)rg.wpr), FastDiv((uint32_t)g.ny));
   k_loop_check<<<1, 32, 0, s>>>(W.dc, W.ls, max_rounds, h, use_cond, fbits && X.list_after ? n_units : nullptr);
   *launches += 4;
   if (fbits && X.list_after) {
@@ -817,6 +817,10 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
 
 }  // namespace
 
+static dmtz_status slab_round_enqueue(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
+                                      const dmtz_slab* sl, char* ws, const Layout& L, float* g_out, int64_t round,
+                                      bool full, cudaStream_t s);
+
 // The multi-GPU C-loop (dmtz_dist.cuh): one rank's slab, its owned planes in and out.
 static dmtz_status correct_dist(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
                                 char* ws, size_t wsb, const Layout& L, float* g_out, dmtz_edit* edits, int64_t cap,
@@ -870,7 +874,6 @@ static dmtz_status correct_dist(dmtz_ctx* c, const float* f, const float* fhat, 
   const int64_t per_plane = g.ny * rg.wpr;
   const int64_t nface = std::min<int64_t>(3, nown);
   const int64_t max_rounds = o->max_rounds ? o->max_rounds : c->dims.nx * c->dims.ny * c->gnz * (int64_t)(o->q_cap + 1);
-  long long* dround = dcnt + nout;  // slab_round_async's own 12 counters (unused beyond the kernel)
   std::vector<long long> tot(nout, 0);
   int status = -1;
   int64_t r = 0;
@@ -898,11 +901,11 @@ static dmtz_status correct_dist(dmtz_ctx* c, const float* f, const float* fhat, 
     uint32_t* vround = W.vchg + (int64_t)(r & 1) * W.vwords;
     CK(cudaMemsetAsync(vround + oz0 * per_plane, 0, (size_t)(nface * per_plane) * 4, s));
     CK(cudaMemsetAsync(vround + (oz1 - nface) * per_plane, 0, (size_t)(nface * per_plane) * 4, s));
-    const dmtz_status rs = dmtz_slab_round_async(c, floc, fhloc, o, &sl, ws, wsb, gloc, r, (int64_t*)dround,
-                                                 (dmtz_stream_t)s);
+    const dmtz_status rs = slab_round_enqueue(c, floc, fhloc, o, &sl, ws, L, gloc, r, o->full_sweeps != 0, s);
     if (rs) return rs;
     k_dist_counters<<<1, 256, 0, s>>>(W.dc, r, dcnt, nout, vround, g, rg, oz0, oz0 + nface, oz1 - nface, oz1,
                                       c->rank);
+    st->launches += 6 + (r > 1 ? 1 : 0);  // set_round, [units], screen, decode, edit_rows, loop_check, counters
     CK(cudaGetLastError());
     if (c->tr.allreduce_sum_i64(c->tr.user, (int64_t*)dcnt, nout, (dmtz_stream_t)s)) return comm_fail("allreduce");
     CK(cudaMemcpyAsync(hcnt, dcnt, (size_t)nout * 8, cudaMemcpyDeviceToHost, s));
@@ -1222,6 +1225,34 @@ dmtz_status dmtz_slab_round(dmtz_ctx* c, const float* f, const float* fhat, cons
   return DMTZ_OK;
 }
 
+}  // extern "C"
+
+// one slab round enqueued on s (no host synchronisation); full: every local unit and
+// every code recomputed (the full-sweep mode), else the frontier with change skipping
+static dmtz_status slab_round_enqueue(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
+                                      const dmtz_slab* sl, char* ws, const Layout& L, float* g_out, int64_t round,
+                                      bool full, cudaStream_t s) {
+  WS<3> W(ws, L, c->g);
+  int64_t launches = 0;
+  k_set_round<<<1, 32, 0, s>>>(W.ls, (unsigned long long)round);
+  const RowGeom rg = row_geom(c->g);
+  if (round > 1) {
+    CK(cudaMemsetAsync(&W.dc->n_units, 0, 8, s));
+    k_units_from_bits<<<clamp_blocks(rg.units, 256, 4096), 256, 0, s>>>(W.fbits, rg.units, W.units, &W.dc->n_units);
+    if (full) CK(units_range(rg, 0, c->g.nz, W.units, &W.dc->n_units, s));  // the frontier is ignored
+  }
+  RoundExtra X;
+  X.anchor_z0 = sl->anchor_z0;
+  X.anchor_z1 = sl->anchor_z1;
+  X.decode_marks = W.fbits;
+  X.list_after = false;
+  return enqueue_round<3>(c, f, fhat, o, W, g_out, W.units, &W.dc->n_units, W.units, &W.dc->n_units, W.fbits,
+                          (int)L.fwords, sl->own_z0, sl->own_z1, sl->own_z0, sl->own_z1, false, ~0ull,
+                          cudaGraphConditionalHandle(), 0, full ? 0 : 1, &launches, s, X);
+}
+
+extern "C" {
+
 dmtz_status dmtz_slab_round_async(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
                                   const dmtz_slab* sl, void* workspace, size_t wsb, float* g_out, int64_t round,
                                   int64_t* dcounters, dmtz_stream_t stream) {
@@ -1231,23 +1262,9 @@ dmtz_status dmtz_slab_round_async(dmtz_ctx* c, const float* f, const float* fhat
   if (st) return st;
   if (!dcounters || round < 1) { set_err("invalid argument"); return DMTZ_E_ARG; }
   cudaStream_t s = (cudaStream_t)stream;
-  WS<3> W((char*)workspace, L, c->g);
-  int64_t launches = 0;
-  k_set_round<<<1, 32, 0, s>>>(W.ls, (unsigned long long)round);
-  const RowGeom rg = row_geom(c->g);
-  if (round > 1) {
-    CK(cudaMemsetAsync(&W.dc->n_units, 0, 8, s));
-    k_units_from_bits<<<clamp_blocks(rg.units, 256, 4096), 256, 0, s>>>(W.fbits, rg.units, W.units, &W.dc->n_units);
-  }
-  RoundExtra X;
-  X.anchor_z0 = sl->anchor_z0;
-  X.anchor_z1 = sl->anchor_z1;
-  X.decode_marks = W.fbits;
-  X.list_after = false;
-  st = enqueue_round<3>(c, f, fhat, o, W, g_out, W.units, &W.dc->n_units, W.units, &W.dc->n_units, W.fbits,
-                        (int)L.fwords, sl->own_z0, sl->own_z1, sl->own_z0, sl->own_z1, false, ~0ull,
-                        cudaGraphConditionalHandle(), 0, 1, &launches, s, X);
+  st = slab_round_enqueue(c, f, fhat, o, sl, (char*)workspace, L, g_out, round, false, s);
   if (st) return st;
+  WS<3> W((char*)workspace, L, c->g);
   k_counters_out<<<1, 32, 0, s>>>(W.dc, round, (long long*)dcounters);
   CK(cudaGetLastError());
   return DMTZ_OK;

@@ -126,14 +126,16 @@ class DistContext:
         _check(_lib.dmtz_ctx_set_transport(self._h, ctypes.byref(self._cb)))
 
     def correct(self, f: torch.Tensor, fhat: torch.Tensor, xi: float, q_max: int = 6, q_cap: int | None = None,
-                tier: int = 2, max_rounds: int = 0, stream=None, raise_on_error: bool = True) -> Result:
+                tier: int = 2, max_rounds: int = 0, full_sweeps: bool = False, stream=None,
+                raise_on_error: bool = True) -> Result:
         _need_cuda(f, fhat)
         for t in (f, fhat):
             assert t.dtype == torch.float32 and tuple(t.shape) == self.owned_shape and t.is_contiguous()
         g = torch.empty_like(f)
         cap = f.numel()
         edits = torch.empty((max(cap, 1), 16), dtype=torch.uint8, device=f.device)
-        opts = _Opts(float(xi), int(q_max), int(q_max if q_cap is None else q_cap), int(tier), int(max_rounds), 0, 0)
+        opts = _Opts(float(xi), int(q_max), int(q_max if q_cap is None else q_cap), int(tier), int(max_rounds),
+                     1 if full_sweeps else 0, 0)
         ne, st = ctypes.c_int64(), _Stats()
         status = _lib.dmtz_correct(self._h, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(fhat.data_ptr()),
                                    ctypes.byref(opts), ctypes.c_void_p(self.workspace.data_ptr()), self.ws_bytes,

@@ -39,7 +39,7 @@ def worker(rank, world, port, case, outdir):
     ft = torch.from_numpy(np.ascontiguousarray(f[ctx.z0:ctx.z1])).cuda()
     fht = torch.from_numpy(np.ascontiguousarray(fh[ctx.z0:ctx.z1])).cuda()
     r = ctx.correct(ft, fht, xi, q_cap=case.get("q_cap"), max_rounds=case.get("max_rounds", 0),
-                    raise_on_error=False)
+                    full_sweeps=case.get("full", False), raise_on_error=False)
     np.savez(os.path.join(outdir, f"rank{rank}.npz"), g=r.g.cpu().numpy(), edits=r.edits.cpu().numpy(),
              stats=json.dumps(r.stats), status=r.status, z=np.array([ctx.z0, ctx.z1]))
     dist.barrier()

@@ -50,6 +50,7 @@ def _run(case, world, tmp_path):
 CASES = [
     ({"kind": "config", "name": "C4", "shape": [40, 40, 40]}, 2),
     ({"kind": "config", "name": "C4", "shape": [36, 30, 34]}, 3),
+    ({"kind": "config", "name": "C4", "shape": [30, 32, 28], "full": True}, 3),
     ({"kind": "config", "name": "C3", "shape": [20, 60, 60]}, 2),
     ({"kind": "random", "shape": [12, 17, 19], "seed": 4, "eps": 4e-2, "q_cap": 65535}, 2),
     ({"kind": "random", "shape": [14, 16, 15], "seed": 6, "eps": 4e-2, "max_rounds": 4}, 2),
