@@ -54,6 +54,7 @@ struct dmtz_ctx {
   int verbose;         // DMTZ_VERBOSE=1: per-round counters on stderr (host-driven rounds)
   int no_graph;        // DMTZ_NO_GRAPH=1: host-driven rounds instead of the CUDA-graph loop
   int no_keys;         // DMTZ_NO_KEYS=1: k_screen always uses the compare/select form of the gradient
+  int no_tile;         // DMTZ_SCREEN_TILE=0: no shared-memory tile in k_screen's dense path
   LoopState* host_ls = nullptr;  // pinned
   struct LoopGraph* graph = nullptr;
   cudaStream_t cap_stream = nullptr;  // private stream the loop body is captured on (the caller's may be the legacy stream)
@@ -294,8 +295,9 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
   if (!use_cond && c->verbose) CK(cudaMemsetAsync(&W.dc->pad[2], 0, 4 * 8, s));
   if (fbits) CK(cudaMemsetAsync(W.ebits, 0, W.rowbit_bytes, s));  // rewritten for every active unit
   if (profile) CK(cudaEventRecord(c->ev[0], s));
-  k_screen<D><<<sweep_blocks, SCREEN_THREADS, 0, s>>>(g_out, W.cand_g, W.ebits, W.vchg, W.vwords, use_skip, units, n_units, g,
-                                           rg, W.ls, W.dc, W.ki, c->no_keys ? 0 : 1);
+  const int skeys = c->no_keys ? 0 : (c->no_tile ? 1 : 3);   // the tile's smem attribute: dmtz_ctx_create
+  k_screen<D><<<sweep_blocks, SCREEN_THREADS, (skeys & 2) ? SCREEN_TILE_BYTES : 0, s>>>(
+      g_out, W.cand_g, W.ebits, W.vchg, W.vwords, use_skip, units, n_units, g, rg, W.ls, W.dc, W.ki, skeys);
   if (c->sdirty) {  // dmtz_preserve: accumulate the changed codes for the next S-round
     k_sdirty_or<<<clamp_blocks(nwords, 256), 256, 0, s>>>(W.ebits, nwords, g, rg, c->sdirty);
     *launches += 1;
@@ -1016,6 +1018,12 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
   c->no_graph = ng && ng[0] == '1';
   const char* nk = getenv("DMTZ_NO_KEYS");
   c->no_keys = nk && nk[0] == '1';
+  const char* nt = getenv("DMTZ_SCREEN_TILE");
+  c->no_tile = nt && nt[0] == '0';
+  // k_screen's tiled dense path uses more than the default 48 KB of dynamic shared memory
+  // (set here, outside any stream capture)
+  CK(cudaFuncSetAttribute(k_screen<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCREEN_TILE_BYTES));
+  CK(cudaFuncSetAttribute(k_screen<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCREEN_TILE_BYTES));
   cudaError_t e = cudaMallocHost((void**)&c->host_cnt, sizeof(Counters) * 2);
   if (e == cudaSuccess) e = cudaMallocHost((void**)&c->host_ls, sizeof(LoopState));
   if (e != cudaSuccess) {

@@ -79,6 +79,7 @@ struct KeyInfo {
   unsigned int max_bits;  // max over f and fhat (as unsigned: a negative value is huge)
   unsigned int pad[14];
 };
+// 32 (max - min) + 26 stays below the outside-grid key 0x7E000000 (dmtz_sweep.cuh load_keys)
 constexpr unsigned KEY_RANGE = 1u << 25;
 __device__ __forceinline__ bool keys_ok(const KeyInfo* ki, uint32_t* base) {
   const int mn = ki->min_bits;

@@ -113,6 +113,8 @@ __device__ __forceinline__ void load_stencil(const float* __restrict__ fld, cons
 // (non-negative, finite), so the argmin of a type's set is one FMNMX3 tree and
 // key & 31 its position.  Outside the grid: a key above every valid one.
 constexpr uint32_t KEY_OUTSIDE = 0x7E000000u;
+constexpr int TSEG = 64, TROW = TSEG + 8;  // k_screen's tiled dense path: anchors per segment, floats per row
+constexpr int SCREEN_TILE_BYTES = (256 / 32) * 2 * 9 * TROW * 4;  // per CTA (SCREEN_THREADS = 256)
 template <int D>
 __device__ __forceinline__ void load_keys(const float* __restrict__ fld, const Grid& g, int64_t v, int64_t x,
                                           int64_t y, int64_t z, uint32_t base, uint32_t (&W)[27]) {
@@ -148,9 +150,9 @@ __device__ __forceinline__ void load_keys(const float* __restrict__ fld, const G
 }
 
 template <int D>
-__device__ __forceinline__ uint64_t cand_of_keys(const uint32_t (&W)[27], const uint8_t* lut) {
-  if constexpr (D == 3) return k3d::cand_code_keys(W, lut);
-  else return k2d::cand_code_keys(W, lut);
+__device__ __forceinline__ uint64_t cand_of_keys(const uint32_t (&W)[27], const uint8_t* lut, uint32_t kmask = 31u) {
+  if constexpr (D == 3) return k3d::cand_code_keys(W, lut, kmask);
+  else return k2d::cand_code_keys(W, lut, kmask);
 }
 
 template <int D>
@@ -167,11 +169,10 @@ __device__ __forceinline__ uint64_t cand_of(const float (&s)[27]) {
 // are compacted into full warps (lane = one anchor).
 // ---------------------------------------------------------------------------
 constexpr int SCREEN_THREADS = 256;
-#ifdef DMTZ_SCREEN_MINB
-#define DMTZ_SCREEN_LB __launch_bounds__(SCREEN_THREADS, DMTZ_SCREEN_MINB)
-#else
-#define DMTZ_SCREEN_LB __launch_bounds__(SCREEN_THREADS)
+#ifndef DMTZ_SCREEN_MINB
+#define DMTZ_SCREEN_MINB 4   // 4 CTAs (32 warps) per SM: <= 64 registers, the tile's shared memory fits
 #endif
+#define DMTZ_SCREEN_LB __launch_bounds__(SCREEN_THREADS, DMTZ_SCREEN_MINB)
 template <int D>
 __global__ void DMTZ_SCREEN_LB
 k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg, uint32_t* __restrict__ ebits,
@@ -187,6 +188,9 @@ k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg
   __syncthreads();
   uint32_t kbase = 0;
   const bool keys = use_keys && keys_ok(ki, &kbase);  // uniform over the launch
+  // tiled dense path: 16-byte aligned rows (nx % 4 == 0); DMTZ_SCREEN_TILE=0 (use_keys & 2) disables it
+  extern __shared__ __align__(16) float s_tile_dyn[];  // SCREEN_TILE_BYTES when launched tiled, else 0
+  const bool tiled = keys && (use_keys & 2) && (g.nx % 4) == 0;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint16_t* list = s_list[wib];
   uint32_t* se = s_e[wib];
@@ -260,33 +264,135 @@ k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg
     }
     __syncwarp();
     const int64_t row0 = y * g.sy + z * g.sz + cbase * 32;
-    for (int b0 = 0; b0 < n; b0 += 32) {
-      const bool act = b0 + lane < n;
-      const int o = act ? (dense ? b0 + lane : (int)list[b0 + lane]) : 0;
+    // the code's memo compare and the changed-code bits of a batch (lanes in ascending anchor order)
+    auto finish = [&](bool act, int o, uint64_t code, uint64_t old) {
       bool e = false;
       if (act) {
-        const int64_t x = cbase * 32 + o;
         const int64_t v = row0 + o;
-        const int ok = axes_ok(g, x, y, z);
-        uint64_t code;
-        if (keys) {
-          uint32_t W[27];
-          load_keys<D>(gfld, g, v, x, y, z, kbase, W);
-          code = cand_of_keys<D>(W, s_lut) | t_nonex_fill<D>(ok);
-        } else {
-          float sv[27];
-          load_stencil<D>(gfld, g, v, x, y, z, sv);
-          code = cand_of<D>(sv) | t_nonex_fill<D>(ok);
-        }
-        e = first_round || code != (uint64_t)cg[v];
+        e = first_round || code != old;
         if (e) cg[v] = (typename Tr<D>::code_t)code;
         recomputed++;
       }
-      // changed-code bits per chunk (the batch's lanes are in ascending anchor order)
       const unsigned grp = __match_any_sync(0xffffffffu, act ? (o >> 5) : -1);
       const uint32_t bits = __reduce_or_sync(grp, e ? 1u << (o & 31) : 0u);
       if (act && lane == __ffs(grp) - 1 && bits) se[o >> 5] |= bits;
       __syncwarp();
+    };
+    if (dense && tiled) {
+      // dense item, tiled: the stencil rows of 64-anchor segments are staged in shared
+      // memory with cp.async (double-buffered: segment k + 1 streams in while k is
+      // computed); an anchor forms its 27 keys from shared memory
+      float* tb = s_tile_dyn + wib * (2 * 9 * TROW);
+      const int nseg = (n + TSEG - 1) / TSEG;
+      // lane c < TROW / 4 copies 16-byte column chunk c of the 9 (3 in 2D) rows; row
+      // validity and the row's global offset are per item, the column's per segment
+      unsigned rowok = 0;
+#pragma unroll
+      for (int r = 0; r < 9; r++) {
+        const int64_t yy = y + r % 3 - 1, zz = z + r / 3 - 1;
+        if ((D == 3 || r / 3 == 1) && yy >= 0 && yy < g.ny && zz >= 0 && zz < g.nz) rowok |= 1u << r;
+      }
+      const int64_t rbase = (y - 1) * g.sy + (z - 1) * g.sz;   // row (dy, dz) = (-1, -1)
+      const unsigned sbase = (unsigned)__cvta_generic_to_shared(tb) + 16u * (unsigned)lane;
+      const unsigned allrows = D == 3 ? 0x1FFu : 0x38u;
+      auto fill = [&](int k) {
+        const int64_t x0 = cbase * 32 + (int64_t)k * TSEG - 4;   // 16-byte aligned (nx % 4 == 0)
+        const int64_t xx = x0 + 4 * lane;
+        if (lane < TROW / 4) {
+          const unsigned sb = sbase + (unsigned)((k & 1) * (9 * TROW * 4));
+          const float* p0 = gfld + rbase + xx;
+          if (rowok == allrows && x0 >= 0 && x0 + TROW <= g.nx) {  // warp-uniform: no checks
+#pragma unroll
+            for (int r = 0; r < 9; r++) {
+              if (D == 2 && r / 3 != 1) continue;
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + (unsigned)(r * TROW * 4)),
+                           "l"(p0 + (r / 3) * g.sz + (r % 3) * g.sy));
+            }
+          } else {
+            const bool xin = xx >= 0 && xx < g.nx;
+#pragma unroll
+            for (int r = 0; r < 9; r++) {
+              if (D == 2 && r / 3 != 1) continue;
+              const bool in = xin && ((rowok >> r) & 1u);
+              const float* src = in ? p0 + (r / 3) * g.sz + (r % 3) * g.sy : gfld;
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sb + (unsigned)(r * TROW * 4)),
+                           "l"(src), "r"(in ? 16 : 0));
+            }
+          }
+        }
+        asm volatile("cp.async.commit_group;");
+      };
+      fill(0);
+      for (int k = 0; k < nseg; k++) {
+        if (k + 1 < nseg) {
+          fill(k + 1);
+          asm volatile("cp.async.wait_group 1;");
+        } else {
+          asm volatile("cp.async.wait_group 0;");
+        }
+        __syncwarp();
+        const float* buf = tb + (k & 1) * (9 * TROW);
+        const int ne = n - k * TSEG < TSEG ? n - k * TSEG : TSEG;
+        for (int b0 = 0; b0 < ne; b0 += 32) {
+          const int a = b0 + lane;
+          const bool act = a < ne;
+          const int o = k * TSEG + a;
+          uint64_t code = 0, old = 0;
+          if (act) {
+            old = (uint64_t)cg[row0 + o];   // the memo code, loaded first: its latency overlaps the keys
+            const int64_t x = cbase * 32 + o;
+            const uint32_t c0 = 0u - 32u * kbase;
+            uint32_t W[27];
+            const bool interior = x > 0 && x + 1 < g.nx && y > 0 && y + 1 < g.ny && (D == 2 || (z > 0 && z + 1 < g.nz));
+#pragma unroll
+            for (int r = 0; r < 9; r++)
+#pragma unroll
+              for (int dx = -1; dx <= 1; dx++) {
+                const int p = (dx + 1) + 3 * r;
+                if (D == 2 && r / 3 != 1) { W[p] = KEY_OUTSIDE; continue; }
+                const uint32_t bv = __float_as_uint(buf[r * TROW + a + 4 + dx]);
+                asm("mad.lo.u32 %0, %1, 32, %2;" : "=r"(W[p]) : "r"(bv), "r"(c0 + (uint32_t)p));
+              }
+            if (!interior) {  // positions outside the grid (zero-filled in the tile)
+#pragma unroll
+              for (int r = 0; r < 9; r++)
+#pragma unroll
+                for (int dx = -1; dx <= 1; dx++) {
+                  const int p = (dx + 1) + 3 * r;
+                  const int dz = r / 3 - 1, dy = r % 3 - 1;
+                  const bool in = (x + dx >= 0) && (x + dx < g.nx) && (y + dy >= 0) && (y + dy < g.ny) &&
+                                  (z + dz >= 0) && (z + dz < g.nz) && (D == 3 || dz == 0);
+                  if (!in) W[p] = KEY_OUTSIDE;
+                }
+            }
+            code = cand_of_keys<D>(W, s_lut) | t_nonex_fill<D>(axes_ok(g, x, y, z));
+          }
+          finish(act, o, code, old);
+        }
+        __syncwarp();   // every lane is done with this buffer before it is refilled
+      }
+    } else {
+      for (int b0 = 0; b0 < n; b0 += 32) {
+        const bool act = b0 + lane < n;
+        const int o = act ? (dense ? b0 + lane : (int)list[b0 + lane]) : 0;
+        uint64_t code = 0, old = 0;
+        if (act) {
+          const int64_t x = cbase * 32 + o;
+          const int64_t v = row0 + o;
+          old = (uint64_t)cg[v];
+          const int ok = axes_ok(g, x, y, z);
+          if (keys) {
+            uint32_t W[27];
+            load_keys<D>(gfld, g, v, x, y, z, kbase, W);
+            code = cand_of_keys<D>(W, s_lut) | t_nonex_fill<D>(ok);
+          } else {
+            float sv[27];
+            load_stencil<D>(gfld, g, v, x, y, z, sv);
+            code = cand_of<D>(sv) | t_nonex_fill<D>(ok);
+          }
+        }
+        finish(act, o, code, old);
+      }
     }
     if (inrow) ebits[dword_index(g, rg, y, z, cl)] = se[lane];
     __syncwarp();
