@@ -297,7 +297,7 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
   if (profile) CK(cudaEventRecord(c->ev[0], s));
   const int skeys = c->no_keys ? 0 : (c->no_tile ? 1 : 3);   // the tile's smem attribute: dmtz_ctx_create
   k_screen<D><<<sweep_blocks, SCREEN_THREADS, (skeys & 2) ? SCREEN_TILE_BYTES : 0, s>>>(
-      g_out, W.cand_g, W.ebits, W.vchg, W.vwords, use_skip, units, n_units, g, rg, W.ls, W.dc, W.ki, skeys);
+      g_out, W.cand_g, W.ebits, W.vchg, W.vwords, use_skip, units, n_units, g, rg, W.ls, W.dc, W.ki, skeys, 32u);
   if (c->sdirty) {  // dmtz_preserve: accumulate the changed codes for the next S-round
     k_sdirty_or<<<clamp_blocks(nwords, 256), 256, 0, s>>>(W.ebits, nwords, g, rg, c->sdirty);
     *launches += 1;

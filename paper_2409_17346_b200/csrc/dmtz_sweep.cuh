@@ -150,9 +150,9 @@ __device__ __forceinline__ void load_keys(const float* __restrict__ fld, const G
 }
 
 template <int D>
-__device__ __forceinline__ uint64_t cand_of_keys(const uint32_t (&W)[27], const uint8_t* lut, uint32_t kmask = 31u) {
-  if constexpr (D == 3) return k3d::cand_code_keys(W, lut, kmask);
-  else return k2d::cand_code_keys(W, lut, kmask);
+__device__ __forceinline__ uint64_t cand_of_keys(const uint32_t (&W)[27], const uint8_t* lut) {
+  if constexpr (D == 3) return k3d::cand_code_keys(W, lut);
+  else return k2d::cand_code_keys(W, lut);
 }
 
 template <int D>
@@ -178,7 +178,9 @@ __global__ void DMTZ_SCREEN_LB
 k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg, uint32_t* __restrict__ ebits,
          uint32_t* __restrict__ vchg, int64_t vwords, int use_skip, const uint32_t* __restrict__ units,
          const unsigned long long* __restrict__ n_units_p, Grid g, RowGeom rg, const LoopState* __restrict__ ls,
-         Counters* __restrict__ cnt, const KeyInfo* __restrict__ ki, int use_keys) {
+         Counters* __restrict__ cnt, const KeyInfo* __restrict__ ki, int use_keys, uint32_t kmul) {
+  // kmul = 32, a launch parameter: a multiplier the compiler cannot see stays an IMAD (FMA
+  // pipe) instead of becoming a shift-add (ALU pipe, the limiting one here)
   __shared__ uint16_t s_list[SCREEN_THREADS / 32][DG * 32];
   __shared__ uint32_t s_e[SCREEN_THREADS / 32][DG];
   constexpr int NF = D == 3 ? k3d::NFIELD : k2d::NFIELD;
@@ -286,12 +288,12 @@ k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg
       const int nseg = (n + TSEG - 1) / TSEG;
       // lane c < TROW / 4 copies 16-byte column chunk c of the 9 (3 in 2D) rows; row
       // validity and the row's global offset are per item, the column's per segment
-      unsigned rowok = 0;
-#pragma unroll
-      for (int r = 0; r < 9; r++) {
-        const int64_t yy = y + r % 3 - 1, zz = z + r / 3 - 1;
-        if ((D == 3 || r / 3 == 1) && yy >= 0 && yy < g.ny && zz >= 0 && zz < g.nz) rowok |= 1u << r;
-      }
+      // rows (dy, dz) inside the grid: bit r = 3 (dz + 1) + (dy + 1)
+      const unsigned ymask = (y > 0 ? 1u : 0u) | 2u | (y + 1 < g.ny ? 4u : 0u);
+      const unsigned zmask = (z > 0 ? 1u : 0u) | 2u | (z + 1 < g.nz ? 4u : 0u);
+      const unsigned rowok = D == 2 ? ymask << 3
+                                    : ((zmask & 1u) ? ymask : 0u) | ((zmask & 2u) ? ymask << 3 : 0u) |
+                                          ((zmask & 4u) ? ymask << 6 : 0u);
       const int64_t rbase = (y - 1) * g.sy + (z - 1) * g.sz;   // row (dy, dz) = (-1, -1)
       const unsigned sbase = (unsigned)__cvta_generic_to_shared(tb) + 16u * (unsigned)lane;
       const unsigned allrows = D == 3 ? 0x1FFu : 0x38u;
@@ -343,15 +345,16 @@ k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg
             const int64_t x = cbase * 32 + o;
             const uint32_t c0 = 0u - 32u * kbase;
             uint32_t W[27];
-            const bool interior = x > 0 && x + 1 < g.nx && y > 0 && y + 1 < g.ny && (D == 2 || (z > 0 && z + 1 < g.nz));
+            const bool interior = rowok == allrows && x > 0 && x + 1 < g.nx;
+            const float* bp = buf + a + 3;   // column of dx = -1
 #pragma unroll
             for (int r = 0; r < 9; r++)
 #pragma unroll
               for (int dx = -1; dx <= 1; dx++) {
                 const int p = (dx + 1) + 3 * r;
                 if (D == 2 && r / 3 != 1) { W[p] = KEY_OUTSIDE; continue; }
-                const uint32_t bv = __float_as_uint(buf[r * TROW + a + 4 + dx]);
-                asm("mad.lo.u32 %0, %1, 32, %2;" : "=r"(W[p]) : "r"(bv), "r"(c0 + (uint32_t)p));
+                const uint32_t bv = __float_as_uint(bp[r * TROW + dx + 1]);
+                asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(W[p]) : "r"(bv), "r"(kmul), "r"(c0 + (uint32_t)p));
               }
             if (!interior) {  // positions outside the grid (zero-filled in the tile)
 #pragma unroll
