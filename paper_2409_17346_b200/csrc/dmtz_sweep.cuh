@@ -368,9 +368,18 @@ k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg
                   if (!in) W[p] = KEY_OUTSIDE;
                 }
             }
-            code = cand_of_keys<D>(W, s_lut) | t_nonex_fill<D>(axes_ok(g, x, y, z));
+            code = cand_of_keys<D>(W, s_lut);
+            if (!interior) code |= t_nonex_fill<D>(axes_ok(g, x, y, z));
           }
-          finish(act, o, code, old);
+          // the batch is one 32-anchor chunk (segments of 64 from a 32-aligned group start)
+          bool e = false;
+          if (act) {
+            e = first_round || code != old;
+            if (e) cg[row0 + o] = (typename Tr<D>::code_t)code;
+            recomputed++;
+          }
+          const uint32_t bits = __ballot_sync(0xffffffffu, e);
+          if (lane == 0 && bits) se[o >> 5] |= bits;
         }
         __syncwarp();   // every lane is done with this buffer before it is refilled
       }
