@@ -706,18 +706,9 @@ k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
     int t;
     id_cell<D>(origin[b], a, t);
     uint64_t* out = write ? cells + off[b] : nullptr;
-    if (write) {
+    if (write) {   // stored by the count pass: k_conn_copy writes it
       const uint64_t p = jterm[b];
-      const int64_t n0 = off[b + 1] - off[b];
-      if (p < CONN_NOT_STORED && (int64_t)p + n0 <= pool_limit) {  // stored by the count pass: copy
-        for (int64_t i = 0; i < n0; i++) {
-          const uint32_t e = pool[p + i];
-          const int ex = (int)(e & 127) - 64, ey = (int)((e >> 7) & 127) - 64, ez = (int)((e >> 14) & 127) - 64;
-          out[i] = cell_id<D>(a + ex + ey * g.sy + ez * g.sz, (int)((e >> 21) & 31));
-        }
-        jterm[b] = CELL_BOUNDARY;
-        continue;
-      }
+      if (p < CONN_NOT_STORED && (int64_t)p + (off[b + 1] - off[b]) <= pool_limit) continue;
     }
     // count pass: room for the connector's events (<= 3 per visited triangle)
     uint32_t* ev_out = nullptr;
@@ -799,6 +790,61 @@ k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
     } else {
       jterm[b] = CELL_BOUNDARY;
     }
+  }
+}
+
+// Write pass of the connectors stored by the count pass: a warp takes 32 consecutive
+// connector branches and copies their events (pool keys -> cell ids) cooperatively,
+// lane i handling event i of the 32 lists laid end to end, so the cell writes -- the
+// lists are contiguous in the CSR -- are coalesced.
+template <int D>
+__global__ void __launch_bounds__(256)
+k_conn_copy(Grid g, int64_t b0, int64_t nb, const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
+            const long long* __restrict__ off, uint64_t* __restrict__ cells, const uint32_t* __restrict__ pool,
+            int64_t pool_limit) {
+  __shared__ long long s_pre[8][33];
+  __shared__ long long s_pool[8][32], s_out[8][32], s_anc[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = b0 + warp * 32; base < nb; base += nwarps * 32) {
+    const int64_t b = base + lane;
+    long long len = 0;
+    if (b < nb) {
+      const uint64_t pp = jterm[b];
+      const long long o0 = off[b], o1 = off[b + 1];
+      if (pp < CONN_NOT_STORED && (int64_t)pp + (o1 - o0) <= pool_limit) {
+        len = o1 - o0;
+        int64_t an;
+        int t;
+        id_cell<D>(origin[b], an, t);
+        s_pool[w][lane] = (long long)pp;
+        s_out[w][lane] = o0;
+        s_anc[w][lane] = an;
+        jterm[b] = CELL_BOUNDARY;
+      }
+    }
+    long long inc = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    s_pre[w][lane + 1] = inc;
+    if (lane == 0) s_pre[w][0] = 0;
+    __syncwarp();
+    const long long total = s_pre[w][32];
+    for (long long i = lane; i < total; i += 32) {
+      int j = 0;   // the list holding event i: the last j with s_pre[j] <= i
+#pragma unroll
+      for (int st = 16; st > 0; st >>= 1)
+        if (s_pre[w][j + st] <= i) j += st;
+      const long long k = i - s_pre[w][j];
+      const uint32_t e = pool[s_pool[w][j] + k];
+      const int ex = (int)(e & 127) - 64, ey = (int)((e >> 7) & 127) - 64, ez = (int)((e >> 14) & 127) - 64;
+      cells[s_out[w][j] + k] = cell_id<D>(s_anc[w][j] + ex + ey * g.sy + ez * g.sz, (int)((e >> 21) & 31));
+    }
+    __syncwarp();
   }
 }
 
@@ -1285,6 +1331,12 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
       k_conn_small<D><<<(unsigned)(nbc < 148 * 64 ? nbc : 148 * 64), CONN_THREADS, 0, s>>>(
           V.eview, g, conn_base, nb, A.out_origin, A.out_terminal, off, A.out_cells, write,
           (unsigned int*)ovf, conn_base, pool, &dc->pad[2], pool_cap, pool_limit, cq_lim);
+      if (write && pool) {  // the stored event lists (skipped above): a cooperative copy, which
+                            // then marks them done -- after the BFS pass, which reads the marks
+        const int64_t nw = (nbk[2] + 31) / 32;
+        k_conn_copy<D><<<(unsigned)((nw + 7) / 8 < 148 * 16 ? (nw + 7) / 8 : 148 * 16), 256, 0, s>>>(
+            g, conn_base, nb, A.out_origin, A.out_terminal, off, A.out_cells, pool, pool_limit);
+      }
       if (!write) A.level_counts[0] = nbk[2];
     }
     TCK(cudaGetLastError());
