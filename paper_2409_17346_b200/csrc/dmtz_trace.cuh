@@ -658,7 +658,8 @@ constexpr int CQ = DMTZ_CQ;
 constexpr int CONN_THREADS = 128;
 constexpr int CONN_CHUNK = 1024;                       // pool entries taken per atomic
 constexpr uint64_t CONN_NOT_STORED = ~0ull - 1;        // terminal slot: events not in the pool
-template <int D>
+// IDX: int when the grid has < 2^31 vertices (32-bit index arithmetic), else int64_t
+template <int D, typename IDX>
 __global__ void __launch_bounds__(CONN_THREADS)
 k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
              const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm, long long* __restrict__ off,
@@ -689,7 +690,10 @@ k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
                                : (uint16_t)0;
     }
   }
+  __shared__ IDX s_dm[8];   // index offset of each corner delta of {0,1}^3
+  if (threadIdx.x < 8) s_dm[threadIdx.x] = (IDX)mask_delta(g, (int)threadIdx.x);
   __syncthreads();
+  const IDX sy = (IDX)g.sy, sz = (IDX)g.sz;
   auto key = [](int dx, int dy, int dz, int ty) {
     return (uint32_t)(dx + 64) | ((uint32_t)(dy + 64) << 7) | ((uint32_t)(dz + 64) << 14) | ((uint32_t)ty << 21);
   };
@@ -724,26 +728,29 @@ k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
     int64_t n = 0;
     bool ovf = false;
     q[0] = key(0, 0, 0, t);
-    uint64_t filt = 1ull << ((q[0] * 0x9E3779B1u) >> 26);
+    // membership filter of the queued keys: two 64-bit Bloom words with independent
+    // hashes rule out most new keys without the linear scan (which stays exact)
+    uint64_t filt0 = 1ull << ((q[0] * 0x9E3779B1u) >> 26), filt1 = 1ull << ((q[0] * 0x85EBCA6Bu) >> 26);
+    const IDX a_ = (IDX)a;
     while (head < tail && !ovf) {
       const uint32_t cur = q[(head++) * CONN_THREADS];
       const int bx = (int)(cur & 127) - 64, by = (int)((cur >> 7) & 127) - 64, bz = (int)((cur >> 14) & 127) - 64;
       const int bt = (int)(cur >> 21);
-      const int64_t B = a + bx + by * g.sy + bz * g.sz;
+      const IDX B = a_ + (IDX)bx + (IDX)by * sy + (IDX)bz * sz;
       // the triangle's 3 facet edges: all three views read at once (independent loads)
       uint32_t tf[3], ev[3];
-      int64_t E[3];
+      IDX E[3];
 #pragma unroll
       for (int j = 0; j < 3; j++) {
         tf[j] = s_tf[(bt - T0) * 3 + j];
-        E[j] = B + mask_delta(g, (int)(tf[j] & 7));
+        E[j] = B + s_dm[tf[j] & 7];
         ev[j] = (__ldg(eview + E[j]) >> (4 * (int)(tf[j] >> 3))) & 15u;
       }
 #pragma unroll
       for (int j = 0; j < 3; j++) {
         const int dm = (int)(tf[j] & 7), e = (int)(tf[j] >> 3);
         if (ev[j] & 8u) {  // critical edge: a reached 1-saddle
-          if (write) out[n] = cell_id<D>(E[j], E0 + e);
+          if (write) out[n] = cell_id<D>((int64_t)E[j], E0 + e);
           else if (ev_out) ev_out[n] = key(bx + (dm & 1), by + ((dm >> 1) & 1), bz + ((dm >> 2) & 1), E0 + e) | 0x80000000u;
           n++;
           continue;
@@ -758,16 +765,17 @@ k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
         if (k == cur) continue;
         // membership: a 64-bit filter of the queued keys rules out most new keys without
         // the linear scan of the queue (which stays exact for the rest)
-        const uint64_t fb = 1ull << ((k * 0x9E3779B1u) >> 26);
-        if (filt & fb) {
+        const uint64_t fb0 = 1ull << ((k * 0x9E3779B1u) >> 26), fb1 = 1ull << ((k * 0x85EBCA6Bu) >> 26);
+        if ((filt0 & fb0) && (filt1 & fb1)) {
           bool seen = false;
           for (int i = tail - 1; i >= 0 && !seen; i--) seen = q[i * CONN_THREADS] == k;
           if (seen) continue;
         }
         if (tail == cq_lim) { ovf = true; break; }   // cq_lim = CQ (tests: smaller)
         q[(tail++) * CONN_THREADS] = k;
-        filt |= fb;
-        if (write) out[n] = cell_id<D>(a + nx_ + ny_ * g.sy + nz_ * g.sz, nt);
+        filt0 |= fb0;
+        filt1 |= fb1;
+        if (write) out[n] = cell_id<D>((int64_t)(a_ + (IDX)nx_ + (IDX)ny_ * sy + (IDX)nz_ * sz), nt);
         else if (ev_out) ev_out[n] = k;
         n++;
       }
@@ -1328,9 +1336,15 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
       TCK(launch_walk<D>(V, g, nbk[0], conn_base, A, off, write, dc, threads, s));
     if (nbk[2]) {  // connectors: one thread per 2-saddle, small queues in shared memory
       const int64_t nbc = (nbk[2] + CONN_THREADS - 1) / CONN_THREADS;
-      k_conn_small<D><<<(unsigned)(nbc < 148 * 64 ? nbc : 148 * 64), CONN_THREADS, 0, s>>>(
-          V.eview, g, conn_base, nb, A.out_origin, A.out_terminal, off, A.out_cells, write,
-          (unsigned int*)ovf, conn_base, pool, &dc->pad[2], pool_cap, pool_limit, cq_lim);
+      const unsigned cgrid = (unsigned)(nbc < 148 * 64 ? nbc : 148 * 64);
+      if (g.N < (1ll << 31))
+        k_conn_small<D, int><<<cgrid, CONN_THREADS, 0, s>>>(
+            V.eview, g, conn_base, nb, A.out_origin, A.out_terminal, off, A.out_cells, write,
+            (unsigned int*)ovf, conn_base, pool, &dc->pad[2], pool_cap, pool_limit, cq_lim);
+      else
+        k_conn_small<D, int64_t><<<cgrid, CONN_THREADS, 0, s>>>(
+            V.eview, g, conn_base, nb, A.out_origin, A.out_terminal, off, A.out_cells, write,
+            (unsigned int*)ovf, conn_base, pool, &dc->pad[2], pool_cap, pool_limit, cq_lim);
       if (write && pool) {  // the stored event lists (skipped above): a cooperative copy, which
                             // then marks them done -- after the BFS pass, which reads the marks
         const int64_t nw = (nbk[2] + 31) / 32;
