@@ -1007,6 +1007,7 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
   c->g.nx = d->nx; c->g.ny = d->ny; c->g.nz = lz1 - lz0;   // the local grid (the whole grid unless dist)
   c->g.N = d->nx * d->ny * c->g.nz;
   c->g.sy = d->nx; c->g.sz = d->nx * d->ny;
+  c->g.set_fast();
   c->D = d->nz == 1 ? 2 : 3;
   c->device = cuda_device;
   c->graph = new (std::nothrow) LoopGraph();

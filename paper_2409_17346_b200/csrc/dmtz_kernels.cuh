@@ -13,10 +13,6 @@
 
 namespace dmtz {
 
-struct Grid {
-  int64_t nx, ny, nz, N, sy, sz;  // sy = nx, sz = nx*ny
-};
-
 // n / d for a divisor fixed at launch (round-up method: m = 2^32 (2^s - d) / d + 1,
 // q = (umulhi(m, n) + n) >> s, exact for every 32-bit n); replaces the ~60-instruction
 // 64-bit division in per-element index arithmetic
@@ -30,6 +26,17 @@ struct FastDiv {
   }
   __device__ __forceinline__ uint32_t div(uint32_t n) const {
     return (uint32_t)(((uint64_t)__umulhi(m, n) + n) >> s);
+  }
+};
+
+struct Grid {
+  int64_t nx, ny, nz, N, sy, sz;  // sy = nx, sz = nx*ny
+  // vertex index -> coordinates without 64-bit divisions when N < 2^32 (fast != 0)
+  FastDiv dnx, dsz;
+  int fast;
+  __host__ void set_fast() {
+    fast = N < (1ll << 32) && sz < (1ll << 32);
+    if (fast) { dnx = FastDiv((uint32_t)nx); dsz = FastDiv((uint32_t)sz); }
   }
 };
 

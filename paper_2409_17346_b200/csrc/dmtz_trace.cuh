@@ -75,6 +75,14 @@ __device__ __forceinline__ uint64_t code_at(const void* codes, int64_t a) {
 }
 
 __device__ __forceinline__ void coords_of(const Grid& g, int64_t v, int64_t& x, int64_t& y, int64_t& z) {
+  if (g.fast) {  // 32-bit multiply-high divisions
+    const uint32_t v32 = (uint32_t)v, z32 = g.dsz.div(v32), r = v32 - z32 * (uint32_t)g.sz;
+    const uint32_t y32 = g.dnx.div(r);
+    z = z32;
+    y = y32;
+    x = r - y32 * (uint32_t)g.nx;
+    return;
+  }
   z = v / g.sz;
   const int64_t r = v - z * g.sz;
   y = r / g.nx;
