@@ -473,7 +473,7 @@ def main():
     round_dev_ms = sum(k_ms.values()) / sweeps
     alg_bytes = BYTES_PER_ANCHOR[D] * N           # per full-sweep round (g f32 + the f code)
     ach = alg_bytes / (t_round * 1e-3) / 1e9
-    ncu_round = _ncu_traffic("round", workload)
+    ncu_round = _ncu_traffic("round@full", workload)
     roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
             "traffic": ncu_round,
             "kernel": "full-sweep C-loop round (k_screen + k_decode + k_edit_rows), SURVEY §8(d-1)",
@@ -482,11 +482,14 @@ def main():
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)",
             "traffic_note": "ncu dram__bytes read+write of one full-sweep round's kernels (profiles/ncu_summary.json)"}
     t_launch = ps["screen_ms_full"] / max(ps["n_screen_full"], 1) * 1e-3
-    alu_ach = ALU_OPS_PER_ANCHOR[D] * N / t_launch / 1e9
+    nc = _ncu_issue("k_screen", workload)
+    alu_frac = nc["alu_pipe_pct"] / 100.0 if nc else None
     roof_alu = {"bound": "alu", "kernel": "k_screen (gradient codes of g, one full-sweep launch)",
-                "achieved": alu_ach, "peak": alu_peak, "unit": "Gop/s", "frac": alu_ach / alu_peak,
-                "launch_ms": t_launch * 1e3, "alu_ops_per_anchor": ALU_OPS_PER_ANCHOR[D],
-                "ncu": _ncu_issue("k_screen", workload),
+                "achieved": alu_frac * alu_peak if alu_frac is not None else None, "peak": alu_peak,
+                "unit": "G ALU-pipe instr/s (lanes)", "frac": alu_frac, "launch_ms": t_launch * 1e3,
+                "compares_per_anchor": ALU_OPS_PER_ANCHOR[D] // 2,
+                "compares_per_s": ALU_OPS_PER_ANCHOR[D] // 2 * N / t_launch / 1e9, "ncu": nc,
+                "source": "frac = ncu sm__inst_executed_pipe_alu of the committed capture (profiles/ncu_summary.json)",
                 "peak_source": "ALU pipe: 148 SMs x 64 lanes/clk x sm_max_mhz (B300_MICROARCH: alu rt=2/SMSP)"}
     ds = rpd.stats
     frontier = {"time_to_fixed_point_ms": ttfp, "rounds": r.stats["rounds"], "sweeps": r.stats["sweeps"],
