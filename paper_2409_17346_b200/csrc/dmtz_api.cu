@@ -53,6 +53,9 @@ struct dmtz_ctx {
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // sweep timing (opts.profile): screen | decode
   int verbose;         // DMTZ_VERBOSE=1: per-round counters on stderr (host-driven rounds)
   int no_graph;        // DMTZ_NO_GRAPH=1: host-driven rounds instead of the CUDA-graph loop
+  cudaStream_t aux_stream = nullptr;   // dmtz_correct_host: f's gradient while fhat is uploaded
+  cudaEvent_t ev_aux[2] = {nullptr, nullptr};
+  int pre_codes = 0;   // set by dmtz_correct_host: f's codes / crit / lowest vertex already enqueued on aux_stream
   int no_keys;         // DMTZ_NO_KEYS=1: k_screen always uses the compare/select form of the gradient
   int no_tile;         // DMTZ_SCREEN_TILE=0: no shared-memory tile in k_screen's dense path
   LoopState* host_ls = nullptr;  // pinned
@@ -221,6 +224,14 @@ inline int clamp_blocks(int64_t n, int threads, int64_t cap = 148 * 32) {
   return (int)(b < 1 ? 1 : b < cap ? b : cap);
 }
 
+// a2: codes, critical masks and f-lowest vertices of f (reads f only)
+template <int D>
+void enqueue_f_codes(const Grid& g, const float* f, WS<D>& W, cudaStream_t s) {
+  launch_codes<D>(g, f, W.cand_f, 0, g.nz, s);
+  k_critmask<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(W.cand_f, W.crit_f, g);
+  k_lowpos<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(f, W.lowpos, g);
+}
+
 // a1 + a2: validate, lb, g = fhat, state = 0, codes / criticality / lowest vertex of f.
 // Error messages report vertex index + v_report_off (the global index in slab mode).
 template <int D>
@@ -248,9 +259,12 @@ dmtz_status setup_phase(dmtz_ctx* c, const float* f, const float* fhat, const dm
     set_err("|fhat - f| > xi at vertex %llu", hc->first_bound + (unsigned long long)v_report_off);
     return DMTZ_E_BOUND;
   }
-  launch_codes<D>(g, f, W.cand_f, 0, g.nz, s);
-  k_critmask<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(W.cand_f, W.crit_f, g);
-  k_lowpos<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(f, W.lowpos, g);
+  if (c->pre_codes) {  // enqueued by dmtz_correct_host on the aux stream (overlapping the fhat upload)
+    CK(cudaStreamWaitEvent(s, c->ev_aux[1], 0));
+    *launches += 4;
+    return DMTZ_OK;
+  }
+  enqueue_f_codes<D>(g, f, W, s);
   CK(cudaGetLastError());
   *launches += 4;
   return DMTZ_OK;
@@ -1012,6 +1026,9 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
   c->device = cuda_device;
   c->graph = new (std::nothrow) LoopGraph();
   if (cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess) c->cap_stream = nullptr;
+  if (cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking) != cudaSuccess) c->aux_stream = nullptr;
+  for (int i = 0; i < 2; i++)
+    if (cudaEventCreateWithFlags(&c->ev_aux[i], cudaEventDisableTiming) != cudaSuccess) c->ev_aux[i] = nullptr;
   c->rank = rank; c->world = world;
   const char* vb = getenv("DMTZ_VERBOSE");
   c->verbose = vb && vb[0] == '1';
@@ -1070,6 +1087,9 @@ void dmtz_ctx_destroy(dmtz_ctx* c) {
   }
   if (c->graph) { c->graph->reset(); delete c->graph; }
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
+  for (int i = 0; i < 2; i++)
+    if (c->ev_aux[i]) cudaEventDestroy(c->ev_aux[i]);
   if (c->host_cnt) cudaFreeHost(c->host_cnt);
   if (c->host_ls) cudaFreeHost(c->host_ls);
   for (int i = 0; i < 3; i++)
@@ -1149,9 +1169,27 @@ dmtz_status dmtz_correct_host(dmtz_ctx* c, const float* f_host, const float* fha
   cudaStream_t s = (cudaStream_t)stream;
   const size_t fb = (size_t)c->g.N * sizeof(float);
   CK(cudaMemcpyAsync(f_dev, f_host, fb, cudaMemcpyHostToDevice, s));
+  // f's gradient, critical masks and lowest vertices (a2, they read f only) run on an aux
+  // stream while fhat is uploaded; dmtz_correct's setup waits for them
+  const bool overlap = !c->dist && c->aux_stream && c->ev_aux[0] && c->ev_aux[1] && workspace &&
+                       workspace_bytes >= layout_for(c).total;
+  if (overlap) {
+    const Layout L = layout_for(c);
+    CK(cudaEventRecord(c->ev_aux[0], s));
+    CK(cudaStreamWaitEvent(c->aux_stream, c->ev_aux[0], 0));
+    if (c->D == 3) { WS<3> W((char*)workspace, L, c->g); enqueue_f_codes<3>(c->g, f_dev, W, c->aux_stream); }
+    else { WS<2> W((char*)workspace, L, c->g); enqueue_f_codes<2>(c->g, f_dev, W, c->aux_stream); }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->ev_aux[1], c->aux_stream));
+    c->pre_codes = 1;
+  }
   CK(cudaMemcpyAsync(fhat_dev, fhat_host, fb, cudaMemcpyHostToDevice, s));
   const dmtz_status r = dmtz_correct(c, f_dev, fhat_dev, o, workspace, workspace_bytes, g_dev, edits_dev,
                                      edits_capacity, n_edits, st, stream);
+  if (overlap) {
+    c->pre_codes = 0;
+    CK(cudaStreamWaitEvent(s, c->ev_aux[1], 0));   // (an early error return left it possibly running)
+  }
   if (r != DMTZ_OK && r != DMTZ_E_STUCK && r != DMTZ_E_ITER_CAP && r != DMTZ_E_CAPACITY) return r;
   if (g_host) CK(cudaMemcpyAsync(g_host, g_dev, fb, cudaMemcpyDeviceToHost, s));
   const int64_t ne = *n_edits < edits_capacity ? *n_edits : edits_capacity;
