@@ -666,6 +666,16 @@ constexpr int CQ = DMTZ_CQ;
 constexpr int CONN_THREADS = 128;
 constexpr int CONN_CHUNK = 1024;                       // pool entries taken per atomic
 constexpr uint64_t CONN_NOT_STORED = ~0ull - 1;        // terminal slot: events not in the pool
+// a pool list of full 64-bit cell ids (two u32 per event; the warp-level connectors,
+// whose extent can exceed the 7-bit relative keys of the thread level)
+constexpr uint64_t CONN_WIDE = 1ull << 62;
+// the terminal slot of connector b says its events are in the pool, below pool_limit
+// (u32 entries) -- the write pass copies them (k_conn_copy) instead of redoing the BFS
+__device__ __forceinline__ bool conn_stored(uint64_t p, long long len, int64_t pool_limit) {
+  if (p >= CONN_NOT_STORED) return false;
+  const int64_t w = (p & CONN_WIDE) ? 2 : 1;
+  return (int64_t)(p & ~CONN_WIDE) + w * len <= pool_limit;
+}
 // IDX: int when the grid has < 2^31 vertices (32-bit index arithmetic), else int64_t
 template <int D, typename IDX>
 __global__ void __launch_bounds__(CONN_THREADS)
@@ -720,7 +730,7 @@ k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
     uint64_t* out = write ? cells + off[b] : nullptr;
     if (write) {   // stored by the count pass: k_conn_copy writes it
       const uint64_t p = jterm[b];
-      if (p < CONN_NOT_STORED && (int64_t)p + (off[b + 1] - off[b]) <= pool_limit) continue;
+      if (conn_stored(p, off[b + 1] - off[b], pool_limit)) continue;
     }
     // count pass: room for the connector's events (<= 3 per visited triangle)
     uint32_t* ev_out = nullptr;
@@ -829,12 +839,13 @@ k_conn_copy(Grid g, int64_t b0, int64_t nb, const uint64_t* __restrict__ origin,
     if (b < nb) {
       const uint64_t pp = jterm[b];
       const long long o0 = off[b], o1 = off[b + 1];
-      if (pp < CONN_NOT_STORED && (int64_t)pp + (o1 - o0) <= pool_limit) {
+      if (conn_stored(pp, o1 - o0, pool_limit)) {
         len = o1 - o0;
         int64_t an;
         int t;
         id_cell<D>(origin[b], an, t);
-        s_pool[w][lane] = (long long)pp;
+        // wide lists: the position with bit 62 set (the flag survives as a sign-free marker)
+        s_pool[w][lane] = (pp & CONN_WIDE) ? -(long long)(pp & ~CONN_WIDE) - 1 : (long long)pp;
         s_out[w][lane] = o0;
         s_anc[w][lane] = an;
         jterm[b] = CELL_BOUNDARY;
@@ -856,9 +867,15 @@ k_conn_copy(Grid g, int64_t b0, int64_t nb, const uint64_t* __restrict__ origin,
       for (int st = 16; st > 0; st >>= 1)
         if (s_pre[w][j + st] <= i) j += st;
       const long long k = i - s_pre[w][j];
-      const uint32_t e = pool[s_pool[w][j] + k];
-      const int ex = (int)(e & 127) - 64, ey = (int)((e >> 7) & 127) - 64, ez = (int)((e >> 14) & 127) - 64;
-      cells[s_out[w][j] + k] = cell_id<D>(s_anc[w][j] + ex + ey * g.sy + ez * g.sz, (int)((e >> 21) & 31));
+      const long long pj = s_pool[w][j];
+      if (pj < 0) {   // wide list: the 64-bit cell ids
+        const long long q = -pj - 1 + 2 * k;
+        cells[s_out[w][j] + k] = (uint64_t)pool[q] | ((uint64_t)pool[q + 1] << 32);
+      } else {
+        const uint32_t e = pool[pj + k];
+        const int ex = (int)(e & 127) - 64, ey = (int)((e >> 7) & 127) - 64, ez = (int)((e >> 14) & 127) - 64;
+        cells[s_out[w][j] + k] = cell_id<D>(s_anc[w][j] + ex + ey * g.sy + ez * g.sz, (int)((e >> 21) & 31));
+      }
     }
     __syncwarp();
   }
@@ -880,7 +897,10 @@ __global__ void __launch_bounds__(CONNW_WARPS * 32)
 k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restrict__ list,
             int64_t nlist, int64_t conn_base, const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
             long long* __restrict__ off, uint64_t* __restrict__ cells, bool write,
-            unsigned int* __restrict__ overflow, int wq_lim) {
+            unsigned int* __restrict__ overflow, int wq_lim, uint64_t* __restrict__ stage,
+            uint32_t* __restrict__ pool, unsigned long long* __restrict__ pool_top, int64_t pool_cap) {
+  // count pass with a pool (stage != nullptr): the connector's events (cell ids) go to the
+  // warp's staging slot (3 WQ entries) and, once complete, to an exact-size pool list
   extern __shared__ unsigned long long smw[];
   __shared__ ConnTab CT;
   conn_tables_init<D>(CT);
@@ -906,7 +926,8 @@ k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restri
     int64_t a0;
     int t0;
     id_cell<D>(origin[b], a0, t0);
-    uint64_t* out = write ? cells + off[b] : nullptr;
+    uint64_t* stg = stage ? stage + (((int64_t)blockIdx.x * CONNW_WARPS + wid) * (3 * WQ)) : nullptr;
+    uint64_t* out = write ? cells + off[b] : stg;
     if (lane == 0) {
       const int s0 = find_or_insert(key(a0, t0));
       owner[s0] = 0u;  // seen before every batch
@@ -959,7 +980,7 @@ k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restri
 #pragma unroll
       for (int j = 0; j < 3; j++) {
         if (ckind[j] == 1 || isnew[j]) {
-          if (write) out[nev + pe] = cid[j];
+          if (out) out[nev + pe] = cid[j];
           pe++;
         }
         if (isnew[j]) { queue[tail + pq] = (uint16_t)cslot[j]; pq++; }
@@ -984,6 +1005,19 @@ k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restri
       if (lane == 0) {
         if (!write) off[b] = nev;
         else jterm[b] = CELL_BOUNDARY;
+      }
+      if (!write && stg) {  // the staged events -> an exact-size pool list (2 u32 per event)
+        unsigned long long p = 0;
+        if (lane == 0) p = atomicAdd(pool_top, (unsigned long long)(2 * nev));
+        p = __shfl_sync(0xffffffffu, p, 0);
+        const bool fits = (int64_t)(p + 2 * nev) <= pool_cap;
+        if (fits)
+          for (int64_t i = lane; i < nev; i += 32) {
+            const uint64_t c = stg[i];
+            pool[p + 2 * i] = (uint32_t)c;
+            pool[p + 2 * i + 1] = (uint32_t)(c >> 32);
+          }
+        if (lane == 0) jterm[b] = fits ? (p | CONN_WIDE) : CONN_NOT_STORED;
       }
     }
     __syncwarp();
@@ -1410,9 +1444,13 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
               fprintf(stderr, "dmtz trace pass %d level %d: %lld connectors, warp queues of %d\n", pass, level + 1,
                       (long long)cn, WQ);
             TCK(cudaFuncSetAttribute(k_conn_warp<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CONNW_SMEM));
-            k_conn_warp<D><<<(unsigned)(nbw < 148 * 12 ? nbw : 148 * 12), CONNW_WARPS * 32, CONNW_SMEM, s>>>(
+            const unsigned wgrid = (unsigned)(nbw < 148 * 12 ? nbw : 148 * 12);
+            // count pass with a pool: stage the events in the (still unused) BFS scratch
+            const size_t stage_bytes = (size_t)wgrid * CONNW_WARPS * 3 * WQ * 8;
+            uint64_t* stage = (!write && pool && stage_bytes <= A.bfs_bytes) ? (uint64_t*)sc : nullptr;
+            k_conn_warp<D><<<wgrid, CONNW_WARPS * 32, CONNW_SMEM, s>>>(
                 V.eview, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write,
-                (unsigned int*)ovf, wq_lim);
+                (unsigned int*)ovf, wq_lim, stage, pool, &dc->pad[2], pool_cap);
             TCK(cudaGetLastError());
             continue;
           }
