@@ -171,6 +171,18 @@ typedef struct {
 /* Install (or, with NULL, remove) a transport for a world > 1 context that has no
  * NCCL communicator.  The struct is copied. */
 dmtz_status dmtz_ctx_set_transport(dmtz_ctx* ctx, const dmtz_transport* transport);
+/* How a world > 1 context's dmtz_correct synchronises with the host (default 8):
+ *   rounds_per_sync == 1: every round ends on the host -- the summed counters are read
+ *     back, the stop rule runs there, and the next round exchanges only the faces whose
+ *     3 planes some edit touched (dmtz_stats.halo_faces_skipped counts the others);
+ *   rounds_per_sync  > 1: rounds are enqueued that many at a time with no host
+ *     synchronisation between them; the stop rule runs on the device on the all-reduced
+ *     counters and sets a stop flag after which the rest of the batch does no work, so
+ *     the per-rank round + counter all-reduce + stop decision is one stream of device
+ *     work with no host hop; every face is exchanged each round and a face the neighbour
+ *     did not change is not applied (halo_faces_skipped stays 0).
+ * Results are identical in both modes.  DMTZ_E_ARG outside [1, 1024]. */
+dmtz_status dmtz_ctx_set_dist_sync(dmtz_ctx* ctx, int rounds_per_sync);
 /* An NCCL unique id (128 bytes into `out`) for dmtz_ctx_create; DMTZ_E_NCCL if
  * libnccl.so.2 cannot be loaded. */
 dmtz_status dmtz_nccl_unique_id(void* out);

@@ -68,6 +68,7 @@ struct dmtz_ctx {
   dmtz_transport tr = {nullptr, nullptr, nullptr};
   int has_tr = 0;
   void* nccl_comm = nullptr;
+  int dist_sync = 8;  // rounds per host check of the device stop flag (1: host-synchronous rounds)
 };
 
 #include "dmtz_dist.cuh"  // needs the context above
@@ -146,7 +147,7 @@ Layout layout_for(const dmtz_ctx* c) {
   L.dist = 0;
   if (c->dist) {  // local f, fhat, g, halo staging (f32 each) + the reduced counters
     L.dist = o;
-    o += align_up(4 * N * sizeof(float) + (size_t)(14 + 2 * c->world) * 8 * 2);
+    o += align_up(4 * N * sizeof(float) + (size_t)(64 + DCTL_N) * 8);
   }
   L.trace = o; o += align_up(trace_scratch_bytes(c->g, c->D));
   L.total = o;
@@ -272,9 +273,9 @@ dmtz_status setup_phase(dmtz_ctx* c, const float* f, const float* fhat, const dm
 
 // unit list of the z-planes [z0, z1) into `list` (count -> *n)
 inline cudaError_t units_range(const RowGeom& rg, int64_t z0, int64_t z1, uint32_t* list, unsigned long long* n,
-                               cudaStream_t s) {
+                               cudaStream_t s, const long long* halt = nullptr) {
   const int64_t cnt = (z1 - z0) * rg.ub;
-  k_units_all<<<clamp_blocks(cnt > 0 ? cnt : 1, 256, 4096), 256, 0, s>>>(rg.ub, z0, z1, list, n);
+  k_units_all<<<clamp_blocks(cnt > 0 ? cnt : 1, 256, 4096), 256, 0, s>>>(rg.ub, z0, z1, list, n, halt);
   return cudaGetLastError();
 }
 
@@ -835,7 +836,7 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
 
 static dmtz_status slab_round_enqueue(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
                                       const dmtz_slab* sl, char* ws, const Layout& L, float* g_out, int64_t round,
-                                      bool full, cudaStream_t s);
+                                      bool full, cudaStream_t s, long long* ctl = nullptr);
 
 // The multi-GPU C-loop (dmtz_dist.cuh): one rank's slab, its owned planes in and out.
 static dmtz_status correct_dist(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
@@ -893,6 +894,52 @@ static dmtz_status correct_dist(dmtz_ctx* c, const float* f, const float* fhat, 
   std::vector<long long> tot(nout, 0);
   int status = -1;
   int64_t r = 0;
+  if (c->dist_sync > 1) {
+    // batched: rounds_per_sync rounds per host check; the stop rule and the halo gates
+    // live on the device (k_dist_stop), every face is exchanged, and a face whose planes
+    // the neighbour did not change is not applied (k_halo's gate)
+    long long* ctl = dcnt + 64;
+    long long* hctl = hcnt + 64 - DCTL_N;  // the pinned block's tail (nout <= 48 here)
+    if (nout > 64 - DCTL_N) { set_err("world %d too large for the batched mode", c->world); return DMTZ_E_ARG; }
+    CK(cudaMemsetAsync(ctl, 0, DCTL_N * 8, s));
+    for (;;) {
+      for (int b = 0; b < c->dist_sync; b++) {
+        r++;
+        if (r > 1) {
+          HaloPlan h = halo_plan(c, g, gloc, stage, 1, 1, 1, 1);
+          if (run_exchange(c, h, s)) return comm_fail("exchange");
+          for (int i = 0; i < h.n; i++)
+            if (h.rz1[i] > h.rz0[i]) {
+              const int64_t items = (h.rz1[i] - h.rz0[i]) * g.ny * rg.wpr;
+              k_halo<<<clamp_blocks(items * 32, 256), 256, 0, s>>>(
+                  gloc, stage + h.rz0[i] * sz, h.rz0[i], h.rz1[i], g, rg, W.vchg + (int64_t)((r - 1) & 1) * W.vwords,
+                  W.fbits, ctl, h.rz0[i] == 0 ? DCTL_GATE_LO : DCTL_GATE_HI);
+              st->launches++;
+            }
+        }
+        uint32_t* vround = W.vchg + (int64_t)(r & 1) * W.vwords;
+        CK(cudaMemsetAsync(vround + oz0 * per_plane, 0, (size_t)(nface * per_plane) * 4, s));
+        CK(cudaMemsetAsync(vround + (oz1 - nface) * per_plane, 0, (size_t)(nface * per_plane) * 4, s));
+        const dmtz_status rs = slab_round_enqueue(c, floc, fhloc, o, &sl, ws, L, gloc, r, o->full_sweeps != 0, s, ctl);
+        if (rs) return rs;
+        k_dist_counters<<<1, 256, 0, s>>>(W.dc, r, dcnt, nout, vround, g, rg, oz0, oz0 + nface, oz1 - nface, oz1,
+                                          c->rank, ctl);
+        CK(cudaGetLastError());
+        if (c->tr.allreduce_sum_i64(c->tr.user, (int64_t*)dcnt, nout, (dmtz_stream_t)s)) return comm_fail("allreduce");
+        k_dist_stop<<<1, 32, 0, s>>>(dcnt, ctl, max_rounds, c->rank, c->world);
+        st->launches += 7 + (r > 1 ? 1 : 0);  // begin, [units], screen, decode, edit_rows, loop_check, counters, stop
+      }
+      CK(cudaMemcpyAsync(hctl, ctl, DCTL_N * 8, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (hctl[DCTL_HALT]) break;
+    }
+    status = (int)hctl[DCTL_STATUS];
+    st->rounds = hctl[DCTL_ROUNDS];
+    st->sweeps = hctl[DCTL_SWEEPS];
+    st->n_false_round0 = hctl[DCTL_FALSE0];
+    for (int k = 0; k < 8; k++) st->false_by_kind_round0[k] = hctl[DCTL_FALSE0 + 1 + k];
+    st->halo_faces_sent = (int64_t)((c->rank > 0) + (c->rank < c->world - 1)) * (st->sweeps - 1);
+  }
   while (status < 0) {
     r++;
     if (r > 1) {  // halo planes of g the neighbours changed in round r - 1
@@ -920,7 +967,7 @@ static dmtz_status correct_dist(dmtz_ctx* c, const float* f, const float* fhat, 
     const dmtz_status rs = slab_round_enqueue(c, floc, fhloc, o, &sl, ws, L, gloc, r, o->full_sweeps != 0, s);
     if (rs) return rs;
     k_dist_counters<<<1, 256, 0, s>>>(W.dc, r, dcnt, nout, vround, g, rg, oz0, oz0 + nface, oz1 - nface, oz1,
-                                      c->rank);
+                                      c->rank, nullptr);
     st->launches += 6 + (r > 1 ? 1 : 0);  // set_round, [units], screen, decode, edit_rows, loop_check, counters
     CK(cudaGetLastError());
     if (c->tr.allreduce_sum_i64(c->tr.user, (int64_t*)dcnt, nout, (dmtz_stream_t)s)) return comm_fail("allreduce");
@@ -1278,15 +1325,19 @@ dmtz_status dmtz_slab_round(dmtz_ctx* c, const float* f, const float* fhat, cons
 // every code recomputed (the full-sweep mode), else the frontier with change skipping
 static dmtz_status slab_round_enqueue(dmtz_ctx* c, const float* f, const float* fhat, const dmtz_correct_opts* o,
                                       const dmtz_slab* sl, char* ws, const Layout& L, float* g_out, int64_t round,
-                                      bool full, cudaStream_t s) {
+                                      bool full, cudaStream_t s, long long* ctl) {
   WS<3> W(ws, L, c->g);
   int64_t launches = 0;
-  k_set_round<<<1, 32, 0, s>>>(W.ls, (unsigned long long)round);
+  // batched mode (ctl): the device counts the rounds, and once its stop flag is set the
+  // unit lists stay empty, so the screen / decode / edit kernels find no work
+  if (ctl) k_dist_begin<<<1, 32, 0, s>>>(ctl, W.ls);
+  else k_set_round<<<1, 32, 0, s>>>(W.ls, (unsigned long long)round);
   const RowGeom rg = row_geom(c->g);
   if (round > 1) {
     CK(cudaMemsetAsync(&W.dc->n_units, 0, 8, s));
-    k_units_from_bits<<<clamp_blocks(rg.units, 256, 4096), 256, 0, s>>>(W.fbits, rg.units, W.units, &W.dc->n_units);
-    if (full) CK(units_range(rg, 0, c->g.nz, W.units, &W.dc->n_units, s));  // the frontier is ignored
+    k_units_from_bits<<<clamp_blocks(rg.units, 256, 4096), 256, 0, s>>>(W.fbits, rg.units, W.units, &W.dc->n_units,
+                                                                       ctl);
+    if (full) CK(units_range(rg, 0, c->g.nz, W.units, &W.dc->n_units, s, ctl));  // the frontier is ignored
   }
   RoundExtra X;
   X.anchor_z0 = sl->anchor_z0;
@@ -1631,6 +1682,12 @@ dmtz_status dmtz_ctx_set_transport(dmtz_ctx* c, const dmtz_transport* t) {
   if (!t->exchange || !t->allreduce_sum_i64) { set_err("transport without callbacks"); return DMTZ_E_ARG; }
   c->tr = *t;
   c->has_tr = 1;
+  return DMTZ_OK;
+}
+
+dmtz_status dmtz_ctx_set_dist_sync(dmtz_ctx* c, int rounds_per_sync) {
+  if (!c || rounds_per_sync < 1 || rounds_per_sync > 1024) { set_err("invalid argument"); return DMTZ_E_ARG; }
+  c->dist_sync = rounds_per_sync;
   return DMTZ_OK;
 }
 

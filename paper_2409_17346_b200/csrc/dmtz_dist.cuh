@@ -98,13 +98,65 @@ inline int nccl_allreduce(void* user, int64_t* buf, int n, dmtz_stream_t stream)
   return A->AllReduce(buf, buf, (size_t)n, ncclInt64, ncclSum, (ncclComm_t)user, (cudaStream_t)stream) != ncclSuccess;
 }
 
+// The device control block of the batched mode (dmtz_ctx_set_dist_sync > 1): rounds are
+// enqueued rounds_per_sync at a time with no host synchronisation between them; the stop
+// rule runs on the device (k_dist_stop) on the all-reduced counters and sets HALT, after
+// which every kernel of the remaining enqueued rounds returns at once (their unit lists
+// stay empty, their halo updates and counters are no-ops).
+enum : int {
+  DCTL_HALT = 0,      // 1 once the stop rule fired
+  DCTL_STATUS = 1,    // its dmtz_status
+  DCTL_ROUND = 2,     // the round running (device count; frozen at the stop)
+  DCTL_ROUNDS = 3,    // dmtz_stats.rounds
+  DCTL_FALSE0 = 4,    // n_false_round0, kinds at 5 .. 12
+  DCTL_GATE_LO = 13,  // the lower neighbour changed its upper face planes last round
+  DCTL_GATE_HI = 14,  // the upper neighbour changed its lower face planes last round
+  DCTL_SWEEPS = 15,
+  DCTL_N = 16
+};
+
+// start of a batched round: the device round count and the loop state's round
+__global__ void k_dist_begin(long long* __restrict__ ctl, LoopState* __restrict__ ls) {
+  if (threadIdx.x == 0 && !ctl[DCTL_HALT]) ls->round = (unsigned long long)++ctl[DCTL_ROUND];
+}
+
+// the stop rule (as dist_stop below) on the summed counters, on the device; also the
+// halo gates of the next round from the neighbours' face flags
+__global__ void k_dist_stop(const long long* __restrict__ tot, long long* __restrict__ ctl, long long max_rounds,
+                            int rank, int world) {
+  if (threadIdx.x != 0 || ctl[DCTL_HALT]) return;
+  const long long r = ctl[DCTL_ROUND];
+  ctl[DCTL_SWEEPS]++;
+  if (r == 1) {
+    ctl[DCTL_FALSE0] = tot[0];
+    for (int k = 0; k < 8; k++) ctl[DCTL_FALSE0 + 1 + k] = tot[4 + k];
+  }
+  long long st = -1;
+  if (tot[3]) st = DMTZ_E_INTERNAL;
+  else if (tot[0] == 0) st = DMTZ_OK;
+  else if (tot[1] == 0) st = DMTZ_E_STUCK;
+  else if (r == max_rounds) st = DMTZ_E_ITER_CAP;
+  if (st != DMTZ_OK) ctl[DCTL_ROUNDS] = r;  // rounds that found false cells
+  if (st >= 0) {
+    ctl[DCTL_STATUS] = st;
+    ctl[DCTL_HALT] = 1;
+  }
+  ctl[DCTL_GATE_LO] = rank > 0 ? tot[13 + 2 * (rank - 1)] : 0;
+  ctl[DCTL_GATE_HI] = rank < world - 1 ? tot[12 + 2 * (rank + 1)] : 0;
+}
+
 // round counters for the distributed reduction: out[0..11] as k_counters_out, then two
 // face flags per rank at 12 + 2 rank (+1): "an owned vertex of the 3 planes next to the
 // lower (upper) face changed this round" -- from the round's change bitmap, whose rows
 // of those planes are cleared before the round (k_face_clear)
+// (ctl: the device stop flag of the batched mode -- once set, this writes zeros)
 __global__ void k_dist_counters(const Counters* __restrict__ cnt, long long round, long long* __restrict__ out,
                                 int nout, const uint32_t* __restrict__ vround, Grid g, RowGeom rg, int64_t lo0,
-                                int64_t lo1, int64_t hi0, int64_t hi1, int rank) {
+                                int64_t lo1, int64_t hi0, int64_t hi1, int rank, const long long* ctl) {
+  if (ctl && ctl[DCTL_HALT]) {
+    for (int i = threadIdx.x; i < nout; i += blockDim.x) out[i] = 0;
+    return;
+  }
   __shared__ unsigned s_flag[2];
   if (threadIdx.x < 2) s_flag[threadIdx.x] = 0u;
   __syncthreads();

@@ -756,8 +756,12 @@ k_decode(const float* __restrict__ f, const typename Tr<D>::code_t* __restrict__
 // units meeting v + [-2,1]^3, exactly as this rank's own edits do.  One warp per
 // 32-vertex row chunk.
 // ---------------------------------------------------------------------------
+// (ctl != nullptr: batched multi-GPU mode -- nothing to do once halted (ctl[0]) or when
+// the neighbour's face flag ctl[gate] says its planes did not change)
 __global__ void k_halo(float* __restrict__ gf, const float* __restrict__ planes, int64_t z0, int64_t z1, Grid g,
-                       RowGeom rg, uint32_t* __restrict__ vchg_round, uint32_t* __restrict__ frontier) {
+                       RowGeom rg, uint32_t* __restrict__ vchg_round, uint32_t* __restrict__ frontier,
+                       const long long* __restrict__ ctl = nullptr, int gate = 0) {
+  if (ctl && (ctl[0] || !ctl[gate])) return;
   const int lane = threadIdx.x & 31;
   const int64_t nitems = (z1 - z0) * g.ny * rg.wpr;
   for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < nitems;
@@ -930,7 +934,8 @@ __global__ void k_lowpos(const float* __restrict__ f, unsigned long long* __rest
 
 // active unit list from the frontier bitmap (ordered compaction), count -> *n_out
 __global__ void k_units_from_bits(uint32_t* __restrict__ fbits, int64_t n_units, uint32_t* __restrict__ list,
-                                  unsigned long long* __restrict__ n_out) {
+                                  unsigned long long* __restrict__ n_out, const long long* __restrict__ halt = nullptr) {
+  if (halt && *halt) return;  // batched multi-GPU rounds after the stop: empty list
   // single pass with one atomic per warp; order inside the list does not matter
   const int lane = threadIdx.x & 31;
   for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) - lane; base < n_units;
@@ -949,7 +954,8 @@ __global__ void k_units_from_bits(uint32_t* __restrict__ fbits, int64_t n_units,
 
 // units of the z-planes [z0, z1) (all units: z0 = 0, z1 = nz); unit = z * ub + y-block
 __global__ void k_units_all(int64_t ub, int64_t z0, int64_t z1, uint32_t* __restrict__ list,
-                            unsigned long long* __restrict__ n_out) {
+                            unsigned long long* __restrict__ n_out, const long long* __restrict__ halt = nullptr) {
+  if (halt && *halt) return;
   const int64_t n = (z1 - z0) * ub;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     list[i] = (uint32_t)(z0 * ub + i);

@@ -87,7 +87,8 @@ class DistContext:
     """One rank of the multi-GPU C-loop: a dmtz_ctx over the rank's slab of a global
     grid (numpy shape (nz, ny, nx)); correct() takes and returns the OWNED planes."""
 
-    def __init__(self, global_shape, rank: int, world: int, device=None, nccl_id: bytes | None = None):
+    def __init__(self, global_shape, rank: int, world: int, device=None, nccl_id: bytes | None = None,
+                 rounds_per_sync: int = 8):
         self.global_shape = tuple(int(x) for x in global_shape)
         nz, ny, nx = self.global_shape
         self.rank, self.world = int(rank), int(world)
@@ -100,6 +101,7 @@ class DistContext:
         _check(_lib.dmtz_ctx_create(ctypes.byref(h), ctypes.byref(d), self.rank, self.world, idbuf,
                                     self.device.index or 0))
         self._h = h
+        _check(_lib.dmtz_ctx_set_dist_sync(h, int(rounds_per_sync)))
         self.ws_bytes = int(_lib.dmtz_workspace_bytes(h, None))
         self.workspace = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
         self._cb = None

@@ -34,7 +34,7 @@ def worker(rank, world, port, case, outdir):
     torch.cuda.set_device(0)
     from paper_2409_17346_b200.dist import DistContext, gloo_transport
     f, fh, xi = make_case(case)
-    ctx = DistContext(f.shape, rank, world, device="cuda:0")
+    ctx = DistContext(f.shape, rank, world, device="cuda:0", rounds_per_sync=case.get("sync", 8))
     ctx.set_transport(*gloo_transport())
     ft = torch.from_numpy(np.ascontiguousarray(f[ctx.z0:ctx.z1])).cuda()
     fht = torch.from_numpy(np.ascontiguousarray(fh[ctx.z0:ctx.z1])).cuda()

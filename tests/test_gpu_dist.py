@@ -58,8 +58,13 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("sync", [1, 3, 8])
 @pytest.mark.parametrize("case,world", CASES)
-def test_dist_equals_single_gpu(case, world, tmp_path):
+def test_dist_equals_single_gpu(case, world, sync, tmp_path):
+    """sync = rounds per host check (dmtz_ctx_set_dist_sync): 1 = host-synchronous rounds
+    with halo-transfer skipping, > 1 = the device stop flag (batches that overrun the
+    stop by up to sync - 1 rounds, which must do nothing)."""
+    case = dict(case, sync=sync)
     ref = _single(case)
     g, edits, stats, status, parts = _run(case, world, tmp_path)
     assert all(s == ref.status for s in status), (status, ref.status, ref.message)
@@ -74,12 +79,14 @@ def test_dist_equals_single_gpu(case, world, tmp_path):
     skipped = sum(st["halo_faces_skipped"] for st in stats)
     # every round after the first decides each of the 2 (world - 1) faces once
     assert sent + skipped == 2 * (world - 1) * (stats[0]["sweeps"] - 1)
+    if sync > 1:
+        assert skipped == 0 and all(st["sweeps"] == stats[0]["sweeps"] for st in stats)
 
 
 def test_dist_halo_faces_are_skipped(tmp_path):
     """A field whose edits stay away from the slab faces in late rounds: the faces no
     edit touched are not exchanged, and the result is still the one-GPU result."""
-    case = {"kind": "config", "name": "C3", "shape": [24, 64, 64]}
+    case = {"kind": "config", "name": "C3", "shape": [24, 64, 64], "sync": 1}
     ref = _single(case)
     g, edits, stats, status, _ = _run(case, 2, tmp_path)
     assert np.array_equal(g.view(np.uint32), ref.g.cpu().numpy().view(np.uint32))
@@ -95,10 +102,14 @@ def test_dist_one_rank_nccl():
     case = {"kind": "config", "name": "C4", "shape": [32, 32, 32]}
     ref = _single(case)
     f, fh, xi = make_case(case)
-    ctx = DistContext(f.shape, 0, 1, device="cuda:0", nccl_id=nccl_unique_id())
-    r = ctx.correct(torch.from_numpy(f).cuda(), torch.from_numpy(fh).cuda(), xi)
-    assert r.status == ref.status == 0
-    assert torch.equal(r.g.view(torch.int32), ref.g.view(torch.int32))
-    assert torch.equal(r.edits, ref.edits)
-    for k in STAT_KEYS:
-        assert r.stats[k] == ref.stats[k], k
+    nid = nccl_unique_id()
+    for sync in (1, 8):
+        ctx = DistContext(f.shape, 0, 1, device="cuda:0", nccl_id=nid if sync == 1 else nccl_unique_id(),
+                          rounds_per_sync=sync)
+        r = ctx.correct(torch.from_numpy(f).cuda(), torch.from_numpy(fh).cuda(), xi)
+        assert r.status == ref.status == 0
+        assert torch.equal(r.g.view(torch.int32), ref.g.view(torch.int32))
+        assert torch.equal(r.edits, ref.edits)
+        for k in STAT_KEYS:
+            assert r.stats[k] == ref.stats[k], k
+        ctx.close()
