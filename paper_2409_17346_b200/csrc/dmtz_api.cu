@@ -311,8 +311,12 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
   if (fbits) CK(cudaMemsetAsync(W.ebits, 0, W.rowbit_bytes, s));  // rewritten for every active unit
   if (profile) CK(cudaEventRecord(c->ev[0], s));
   const int skeys = c->no_keys ? 0 : (c->no_tile ? 1 : 3);   // the tile's smem attribute: dmtz_ctx_create
-  k_screen<D><<<sweep_blocks, SCREEN_THREADS, (skeys & 2) ? SCREEN_TILE_BYTES : 0, s>>>(
-      g_out, W.cand_g, W.ebits, W.vchg, W.vwords, use_skip, units, n_units, g, rg, W.ls, W.dc, W.ki, skeys, 32u);
+  if (use_skip)
+    k_screen<D, true><<<sweep_blocks, SCREEN_THREADS, (skeys & 2) ? SCREEN_TILE_BYTES : 0, s>>>(
+        g_out, W.cand_g, W.ebits, W.vchg, W.vwords, use_skip, units, n_units, g, rg, W.ls, W.dc, W.ki, skeys, 32u);
+  else
+    k_screen<D, false><<<sweep_blocks, SCREEN_THREADS, (skeys & 2) ? SCREEN_TILE_BYTES : 0, s>>>(
+        g_out, W.cand_g, W.ebits, W.vchg, W.vwords, use_skip, units, n_units, g, rg, W.ls, W.dc, W.ki, skeys, 32u);
   if (c->sdirty) {  // dmtz_preserve: accumulate the changed codes for the next S-round
     k_sdirty_or<<<clamp_blocks(nwords, 256), 256, 0, s>>>(W.ebits, nwords, g, rg, c->sdirty);
     *launches += 1;
@@ -1087,8 +1091,10 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
   c->no_tile = nt && nt[0] == '0';
   // k_screen's tiled dense path uses more than the default 48 KB of dynamic shared memory
   // (set here, outside any stream capture)
-  CK(cudaFuncSetAttribute(k_screen<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCREEN_TILE_BYTES));
-  CK(cudaFuncSetAttribute(k_screen<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCREEN_TILE_BYTES));
+  CK(cudaFuncSetAttribute(k_screen<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCREEN_TILE_BYTES));
+  CK(cudaFuncSetAttribute(k_screen<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCREEN_TILE_BYTES));
+  CK(cudaFuncSetAttribute(k_screen<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCREEN_TILE_BYTES));
+  CK(cudaFuncSetAttribute(k_screen<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCREEN_TILE_BYTES));
   cudaError_t e = cudaMallocHost((void**)&c->host_cnt, sizeof(Counters) * 2);
   if (e == cudaSuccess) e = cudaMallocHost((void**)&c->host_ls, sizeof(LoopState));
   if (e != cudaSuccess) {

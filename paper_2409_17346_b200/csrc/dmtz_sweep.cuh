@@ -173,7 +173,8 @@ constexpr int SCREEN_THREADS = 256;
 #define DMTZ_SCREEN_MINB 4   // 4 CTAs (32 warps) per SM: <= 64 registers, the tile's shared memory fits
 #endif
 #define DMTZ_SCREEN_LB __launch_bounds__(SCREEN_THREADS, DMTZ_SCREEN_MINB)
-template <int D>
+// SKIP = false: the full-sweep instantiation (use_skip = 0), without the change-skip code
+template <int D, bool SKIP>
 __global__ void DMTZ_SCREEN_LB
 k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg, uint32_t* __restrict__ ebits,
          uint32_t* __restrict__ vchg, int64_t vwords, int use_skip, const uint32_t* __restrict__ units,
@@ -203,7 +204,7 @@ k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg
   // vertices whose value changed in the previous round (its edits) / this round's (cleared here)
   const uint32_t* vprev = vchg + (int64_t)((round - 1) & 1) * vwords;
   uint32_t* vcur = vchg + (int64_t)(round & 1) * vwords;
-  const bool skip = use_skip && !first_round;
+  const bool skip = SKIP && use_skip && !first_round;
   unsigned long long swept = 0, recomputed = 0;
   const uint32_t n_units_ = (uint32_t)*n_units_p;
   const uint32_t ngr = (uint32_t)((rg.wpr + DG - 1) / DG);
@@ -243,7 +244,13 @@ k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg
       swept += __popc(valid);
       se[lane] = 0u;
     }
-    const bool dense = __all_sync(0xffffffffu, need == valid);
+    // dense: every anchor of the item is recomputed -- also when the change skip leaves
+    // only most of them (>= 5/8): an anchor whose 3^D values did not change gets its
+    // memo code back (no change bit), and the tiled full pass is cheaper than the list
+    bool dense = __all_sync(0xffffffffu, need == valid);
+    if (skip && !dense)   // warp-uniform
+      dense = 8u * __reduce_add_sync(0xffffffffu, (unsigned)__popc(need)) >=
+              5u * __reduce_add_sync(0xffffffffu, (unsigned)__popc(valid));
     int n;
     if (dense) {
       n = (int)(__shfl_sync(0xffffffffu, (int)(g.nx - cbase * 32 < DG * 32 ? g.nx - cbase * 32 : DG * 32), 0));
