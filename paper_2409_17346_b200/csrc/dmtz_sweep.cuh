@@ -169,6 +169,9 @@ __device__ __forceinline__ uint64_t cand_of(const float (&s)[27]) {
 // are compacted into full warps (lane = one anchor).
 // ---------------------------------------------------------------------------
 constexpr int SCREEN_THREADS = 256;
+#ifndef DMTZ_SCREEN_DENSE8
+#define DMTZ_SCREEN_DENSE8 5u   // frontier mode: an item is swept whole when >= 5/8 of it needs a new code
+#endif
 #ifndef DMTZ_SCREEN_MINB
 #define DMTZ_SCREEN_MINB 4   // 4 CTAs (32 warps) per SM: <= 64 registers, the tile's shared memory fits
 #endif
@@ -250,7 +253,7 @@ k_screen(const float* __restrict__ gfld, typename Tr<D>::code_t* __restrict__ cg
     bool dense = __all_sync(0xffffffffu, need == valid);
     if (skip && !dense)   // warp-uniform
       dense = 8u * __reduce_add_sync(0xffffffffu, (unsigned)__popc(need)) >=
-              5u * __reduce_add_sync(0xffffffffu, (unsigned)__popc(valid));
+              DMTZ_SCREEN_DENSE8 * __reduce_add_sync(0xffffffffu, (unsigned)__popc(valid));
     int n;
     if (dense) {
       n = (int)(__shfl_sync(0xffffffffu, (int)(g.nx - cbase * 32 < DG * 32 ? g.nx - cbase * 32 : DG * 32), 0));
