@@ -4,6 +4,7 @@
 // C-loop (repeat gradient -> classify -> fix until no false
 // critical cell), status/error plumbing.  No device allocation happens here:
 // every buffer is the caller's.
+#include <chrono>
 #include <cuda_runtime.h>
 
 #include <cstdarg>
@@ -68,7 +69,8 @@ struct dmtz_ctx {
   dmtz_transport tr = {nullptr, nullptr, nullptr};
   int has_tr = 0;
   void* nccl_comm = nullptr;
-  int dist_sync = 8;  // rounds per host check of the device stop flag (1: host-synchronous rounds)
+  int dist_sync = 8;
+  int t3_log = 0;     // DMTZ_T3_LOG=1: per S-round candidate counts and trace time of tier 3 on stderr  // rounds per host check of the device stop flag (1: host-synchronous rounds)
 };
 
 #include "dmtz_dist.cuh"  // needs the context above
@@ -540,8 +542,11 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
 // separatrices + per-branch end flags.
 struct SepLayout {
   size_t codes, save, off, cells, origin, term, kind, first, cb, canc, mbits, sdirty, sdil, goff, gcells, gorigin, gterm, gkind,
-      flag, cidx, cmap, cbsum, total;
+      flag, cidx, cmap, cbsum, t3box, t3st, t3psum, t3hits, total;
 };
+
+// tier 3's end cache (k_t3_valid): 16-bit box coordinates, 32-bit prefix sums
+inline bool t3_cache_ok(const Grid& g) { return g.nx <= 65535 && g.ny <= 65535 && g.nz <= 65535 && g.N < (1ll << 31); }
 
 SepLayout sep_layout(const dmtz_ctx* c, int tier, int64_t cap_b, int64_t cap_c) {
   SepLayout S = {};
@@ -571,6 +576,12 @@ SepLayout sep_layout(const dmtz_ctx* c, int tier, int64_t cap_b, int64_t cap_c) 
     S.cidx = o; o += align_up(((size_t)cap_b + 1) * 8);        // candidate flags -> indices (scan)
     S.cmap = o; o += align_up((size_t)cap_b * 4 + 8);          // candidate -> branch of f
     S.cbsum = o; o += align_up(((size_t)cap_b / 8192 + 4) * 8);
+    if (t3_cache_ok(c->g)) {
+      S.t3box = o; o += align_up((size_t)cap_b * sizeof(T3Box) + 8);
+      S.t3st = o; o += align_up((size_t)cap_b + 8);
+      S.t3psum = o; o += align_up(N * 4);
+      S.t3hits = o; o += align_up(8);
+    }
   }
   S.total = o;
   return S;
@@ -688,6 +699,12 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
     CK(cudaMemsetAsync(sdirty, 0, (size_t)g.N / 8 + 8, s));
     c->sdirty = sdirty;
   }
+  // tier 3's end cache: per branch box + end comparison of its last trace in g
+  const bool t3c = o->tier == 3 && S.t3box != 0;
+  uint8_t* t3st = t3c ? (uint8_t*)(sw + S.t3st) : nullptr;
+  T3Box* t3box = t3c ? (T3Box*)(sw + S.t3box) : nullptr;
+  unsigned long long* t3hits = t3c ? (unsigned long long*)(sw + S.t3hits) : nullptr;
+  if (t3c && nb > 0) CK(cudaMemsetAsync(t3st, 0, (size_t)nb, s));
   struct Reset { dmtz_ctx* c; ~Reset() { c->sdirty = nullptr; } } reset{c};
   for (bool first_call = true;; first_call = false) {
     status = run_cloop<D>(c, f, fhat, o, W, ws, L, g_out, max_rounds, first_call, st, s);
@@ -717,8 +734,21 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
       // the candidates (branches with a troublemaker) are traced in g; the others end as in f
       long long* cidx = (long long*)(sw + S.cidx);
       uint32_t* cmap = (uint32_t*)(sw + S.cmap);
+      if (t3c) {
+        if (!full) {   // drop the cached ends whose box saw a changed code (sdil) since their trace
+          int32_t* P = (int32_t*)(sw + S.t3psum);
+          k_t3_psum_x<<<clamp_blocks(g.ny * g.nz * 32, 256), 256, 0, s>>>(sdil, g, P);
+          k_t3_psum_yz<<<clamp_blocks(g.nx * g.nz, 256), 256, 0, s>>>(g, 1, P);
+          k_t3_psum_yz<<<clamp_blocks(g.nx * g.ny, 256), 256, 0, s>>>(g, 2, P);
+          k_t3_valid<<<clamp_blocks(nb, 256), 256, 0, s>>>(P, g, nb, t3box, t3st);
+          st->launches += 4;
+        }
+        CK(cudaMemsetAsync(t3hits, 0, 8, s));
+      }
+      CK(cudaMemsetAsync(sw + S.flag, 0, (size_t)nb, s));
       k_t3_cand<D><<<clamp_blocks(nb + 1, 256, 148 * 64), 256, 0, s>>>(cells, off, kind, origin, nb, W.cand_f,
-                                                                       W.cand_g, W.crit_f, g, mbits, cidx, W.dc);
+                                                                       W.cand_g, W.crit_f, g, mbits, cidx, W.dc,
+                                                                       t3st, (uint8_t*)(sw + S.flag), t3hits);
       CK(cudaGetLastError());
       CK(scan_i64(cidx, nb + 1, (unsigned long long*)(sw + S.cbsum), &W.dc->pad[0], &hc->pad[0], s));
       const int64_t ncand = (int64_t)hc->pad[0];
@@ -726,7 +756,6 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
       CK(cudaStreamSynchronize(s));
       const int64_t nkc[3] = {(int64_t)hc->pad[4], (int64_t)hc->pad[5], (int64_t)hc->pad[6]};
       ss->cells_checked += (int64_t)hc->pad[7];
-      CK(cudaMemsetAsync(sw + S.flag, 0, (size_t)nb, s));
       st->launches += 4;
       if (ncand > 0) {
         k_t3_fill<D><<<clamp_blocks(nb, 256, 148 * 64), 256, 0, s>>>(
@@ -737,6 +766,8 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
         CK(cudaMemcpyAsync(sw + S.save, W.lb, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(sw + S.save + (size_t)g.N * 4, W.state, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
         // trace the candidates in chunks whose g-paths fit the CSR (halving a chunk that does not)
+        const auto t3_t0 = std::chrono::steady_clock::now();
+        int n_chunks = 0;
         int64_t c0 = 0, chunk = ncand;
         while (c0 < ncand) {
           const int64_t c1 = c0 + chunk < ncand ? c0 + chunk : ncand;
@@ -764,12 +795,26 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
             status = DMTZ_E_INTERNAL;
           }
           if (status != DMTZ_OK) { st->status = status; return status; }
-          k_t3_flags_cand<<<clamp_blocks((c1 - c0) * 32, T3_WARPS * 32), T3_WARPS * 32, 0, s>>>(
+          k_t3_flags_cand<D><<<clamp_blocks((c1 - c0) * 32, T3_WARPS * 32), T3_WARPS * 32, 0, s>>>(
               off, cells, (const uint64_t*)(sw + S.term), kind, (const long long*)(sw + S.goff),
               (const uint64_t*)(sw + S.gcells), (const uint64_t*)(sw + S.gterm) + c0, cmap + c0, c1 - c0,
-              (uint8_t*)(sw + S.flag));
+              (uint8_t*)(sw + S.flag), (const uint64_t*)(sw + S.gorigin) + c0, g, t3box, t3st);
           CK(cudaGetLastError());
           c0 = c1;
+          n_chunks++;
+        }
+        if (c->t3_log) {
+          unsigned long long hits = 0;
+          if (t3c) CK(cudaMemcpy(&hits, t3hits, 8, cudaMemcpyDeviceToHost));
+          fprintf(stderr, "t3 S-round %lld: %llu cached ends reused\n", (long long)ss->s_rounds, hits);
+          CK(cudaStreamSynchronize(s));
+          const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t3_t0).count();
+          fprintf(stderr, "t3 S-round %lld: candidates %lld (desc %lld asc %lld conn %lld), %d chunks, trace %.3f ms,"
+                  " connector levels %lld %lld %lld %lld %lld %lld\n",
+                  (long long)ss->s_rounds, (long long)ncand, (long long)nkc[0], (long long)nkc[1], (long long)nkc[2],
+                  n_chunks, ms, (long long)g_trace_levels[0], (long long)g_trace_levels[1],
+                  (long long)g_trace_levels[2], (long long)g_trace_levels[3], (long long)g_trace_levels[4],
+                  (long long)g_trace_levels[5]);
         }
         CK(cudaMemcpyAsync(W.lb, sw + S.save, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(W.state, sw + S.save + (size_t)g.N * 4, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
@@ -808,6 +853,7 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, e0, e1));
       ss->s_ms += ms;
+      if (c->t3_log) fprintf(stderr, "S-round %lld: %.3f ms\n", (long long)ss->s_rounds, ms);
     }
     if (hc->n_internal) { set_err("troublemaker without an original partner"); status = DMTZ_E_INTERNAL; break; }
     const int64_t ntm = (int64_t)hc->pad[3];
@@ -1083,6 +1129,8 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
   c->rank = rank; c->world = world;
   const char* vb = getenv("DMTZ_VERBOSE");
   c->verbose = vb && vb[0] == '1';
+  const char* t3l = getenv("DMTZ_T3_LOG");
+  c->t3_log = t3l && t3l[0] == '1';
   const char* ng = getenv("DMTZ_NO_GRAPH");
   c->no_graph = ng && ng[0] == '1';
   const char* nk = getenv("DMTZ_NO_KEYS");

@@ -433,13 +433,16 @@ namespace dmtz {
 // and ends the same; only the others (the candidates) are traced in g.
 // cidx[b] = 1 for a candidate (then exclusive-scanned into its index); cnt->pad[4 + kind
 // index] counts them per kind.
+// With the end cache (t3st != nullptr): a candidate whose cached end comparison is still
+// valid takes it (flag[b] = t3st[b] == 2) and is not traced; *hits counts them.
 template <int D>
 __global__ void k_t3_cand(const uint64_t* __restrict__ cells, const long long* __restrict__ off,
                           const uint8_t* __restrict__ kind, const uint64_t* __restrict__ origin, int64_t nb,
                           const void* __restrict__ cf, const void* __restrict__ cg, const uint32_t* __restrict__ crit_f,
                           Grid g, const uint32_t* __restrict__ mbits, long long* __restrict__ cidx,
-                          Counters* __restrict__ cnt) {
-  unsigned long long nk[3] = {0, 0, 0};
+                          Counters* __restrict__ cnt, const uint8_t* __restrict__ t3st, uint8_t* __restrict__ flag,
+                          unsigned long long* __restrict__ hits) {
+  unsigned long long nk[3] = {0, 0, 0}, nh = 0;
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += (int64_t)gridDim.x * blockDim.x) {
     if (b == nb) { cidx[nb] = 0; continue; }
     const int k = kind[b];
@@ -449,9 +452,18 @@ __global__ void k_t3_cand(const uint64_t* __restrict__ cells, const long long* _
       id_cell_fast<D>(origin[b], B, bt);
       c = conn_tri_differs<D>(cf, cg, crit_f, g, B, bt, &j);
     }
+    if (c && t3st) {
+      const uint8_t st = t3st[b];
+      if (st) {
+        flag[b] = st == 2 ? 1 : 0;
+        nh++;
+        c = false;
+      }
+    }
     cidx[b] = c ? 1 : 0;
     if (c) nk[k == 1 ? 0 : k == 2 ? 1 : 2]++;
   }
+  if (t3st) warp_add(hits, nh);
   warp_add(&cnt->pad[4], nk[0]);
   warp_add(&cnt->pad[5], nk[1]);
   warp_add(&cnt->pad[6], nk[2]);
@@ -486,22 +498,58 @@ __global__ void k_t3_fill(const uint64_t* __restrict__ cells, const long long* _
   }
 }
 
+// The box of the anchors a traced branch visited (its origin and every cell of its
+// g-CSR entry), for the end cache
+struct T3Box {
+  uint16_t lo[3], hi[3];
+};
+
 // flag[b] for the candidates: like k_t3_flags, candidate i of the g-CSR against branch
-// cmap[i] of the f-CSR (the other branches keep flag 0)
+// cmap[i] of the f-CSR (the other branches keep flag 0).  With the end cache (box !=
+// nullptr): box[b] and t3st[b] = 1 (same end) / 2 (another end).
+template <int D>
 __global__ void __launch_bounds__(T3_WARPS * 32)
 k_t3_flags_cand(const long long* __restrict__ foff, const uint64_t* __restrict__ fcells,
                 const uint64_t* __restrict__ fterm, const uint8_t* __restrict__ kind,
                 const long long* __restrict__ goff, const uint64_t* __restrict__ gcells,
                 const uint64_t* __restrict__ gterm, const uint32_t* __restrict__ cmap, int64_t nc,
-                uint8_t* __restrict__ flag) {
+                uint8_t* __restrict__ flag, const uint64_t* __restrict__ gorigin, Grid g, T3Box* __restrict__ box,
+                uint8_t* __restrict__ t3st) {
   __shared__ unsigned long long sl[T3_WARPS][2][T3_SMEM];
   __shared__ int sn[T3_WARPS][2];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nc;
        i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t b = cmap[i];
+    if (box) {
+      uint32_t lo[3] = {0xFFFFu, 0xFFFFu, 0xFFFFu}, hi[3] = {0u, 0u, 0u};
+      for (int64_t q = goff[i] + lane - 1; q < goff[i + 1]; q += 32) {
+        const uint64_t id = q < goff[i] ? gorigin[i] : gcells[q];
+        int64_t A; int t;
+        id_cell_fast<D>(id, A, t);
+        int64_t x, y, z;
+        coords_of(g, A, x, y, z);
+        const uint32_t c3[3] = {(uint32_t)x, (uint32_t)y, (uint32_t)z};
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+          lo[a] = c3[a] < lo[a] ? c3[a] : lo[a];
+          hi[a] = c3[a] > hi[a] ? c3[a] : hi[a];
+        }
+      }
+      T3Box bx;
+#pragma unroll
+      for (int a = 0; a < 3; a++) {
+        bx.lo[a] = (uint16_t)__reduce_min_sync(0xffffffffu, lo[a]);
+        bx.hi[a] = (uint16_t)__reduce_max_sync(0xffffffffu, hi[a]);
+      }
+      if (lane == 0) box[b] = bx;
+    }
     if (kind[b] != 4) {
-      if (lane == 0) flag[b] = fterm[b] != gterm[i];
+      if (lane == 0) {
+        const bool differ = fterm[b] != gterm[i];
+        flag[b] = differ;
+        if (box) t3st[b] = differ ? 2 : 1;
+      }
       continue;
     }
     const int64_t s0[2] = {foff[b], goff[i]}, s1[2] = {foff[b + 1], goff[i + 1]};
@@ -546,8 +594,73 @@ k_t3_flags_cand(const long long* __restrict__ foff, const uint64_t* __restrict__
       }
       differ = __any_sync(0xffffffffu, bad);
     }
-    if (lane == 0) flag[b] = differ ? 1 : 0;
+    if (lane == 0) {
+      flag[b] = differ ? 1 : 0;
+      if (box) t3st[b] = differ ? 2 : 1;
+    }
     __syncwarp();
+  }
+}
+
+// P = the inclusive 3D prefix sums of the per-anchor bits `bits` (x, then y, then z)
+__global__ void k_t3_psum_x(const uint32_t* __restrict__ bits, Grid g, int32_t* __restrict__ P) {
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = g.ny * g.nz;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t v0 = r * g.nx;
+    int32_t carry = 0;
+    for (int64_t x0 = 0; x0 < g.nx; x0 += 32) {
+      const int64_t v = v0 + x0 + lane;
+      int32_t s = x0 + lane < g.nx ? (int32_t)((bits[v >> 5] >> (v & 31)) & 1u) : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t u = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += u;
+      }
+      if (x0 + lane < g.nx) P[v] = carry + s;
+      carry += __shfl_sync(0xffffffffu, s, 31);
+    }
+  }
+}
+// axis 1: along y for every (x, z); axis 2: along z for every (x, y)
+__global__ void k_t3_psum_yz(Grid g, int axis, int32_t* __restrict__ P) {
+  const int64_t n_lines = axis == 1 ? g.nx * g.nz : g.nx * g.ny;
+  const int64_t len = axis == 1 ? g.ny : g.nz, stride = axis == 1 ? g.sy : g.sz;
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < n_lines; l += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = l % g.nx, o = l / g.nx;   // o = z (axis 1) or y (axis 2)
+    int64_t v = x + (axis == 1 ? o * g.sz : o * g.sy);
+    int32_t acc = 0;
+    for (int64_t k = 0; k < len; k++, v += stride) {
+      acc += P[v];
+      P[v] = acc;
+    }
+  }
+}
+
+__device__ __forceinline__ int64_t psum_at(const int32_t* P, const Grid& g, int64_t x, int64_t y, int64_t z) {
+  return (x < 0 || y < 0 || z < 0) ? 0 : (int64_t)P[x + y * g.sy + z * g.sz];
+}
+
+// the cached end comparisons still valid: no changed-code window (bits of sdil) within
+// the branch's box grown by 2 on every side; the others are dropped
+__global__ void k_t3_valid(const int32_t* __restrict__ P, Grid g, int64_t nb, const T3Box* __restrict__ box,
+                           uint8_t* __restrict__ t3st) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    if (!t3st[b]) continue;
+    const T3Box bx = box[b];
+    const int64_t n[3] = {g.nx, g.ny, g.nz};
+    int64_t lo[3], hi[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      lo[a] = (int64_t)bx.lo[a] - 2 > 0 ? (int64_t)bx.lo[a] - 2 : 0;
+      hi[a] = (int64_t)bx.hi[a] + 2 < n[a] - 1 ? (int64_t)bx.hi[a] + 2 : n[a] - 1;
+    }
+    const int64_t s = psum_at(P, g, hi[0], hi[1], hi[2]) - psum_at(P, g, lo[0] - 1, hi[1], hi[2]) -
+                      psum_at(P, g, hi[0], lo[1] - 1, hi[2]) - psum_at(P, g, hi[0], hi[1], lo[2] - 1) +
+                      psum_at(P, g, lo[0] - 1, lo[1] - 1, hi[2]) + psum_at(P, g, lo[0] - 1, hi[1], lo[2] - 1) +
+                      psum_at(P, g, hi[0], lo[1] - 1, lo[2] - 1) - psum_at(P, g, lo[0] - 1, lo[1] - 1, lo[2] - 1);
+    if (s) t3st[b] = 0;
   }
 }
 

@@ -13,6 +13,7 @@
 // private queue + open-addressing visited set in workspace scratch (saddles
 // whose search outgrows the slot are redone alone with the whole scratch).
 #pragma once
+#include <chrono>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -669,12 +670,16 @@ constexpr uint64_t CONN_NOT_STORED = ~0ull - 1;        // terminal slot: events 
 // a pool list of full 64-bit cell ids (two u32 per event; the warp-level connectors,
 // whose extent can exceed the 7-bit relative keys of the thread level)
 constexpr uint64_t CONN_WIDE = 1ull << 62;
+constexpr long long CONN_BIG = 8192;   // stored lists longer than this: k_conn_copy_big
 // the terminal slot of connector b says its events are in the pool, below pool_limit
-// (u32 entries) -- the write pass copies them (k_conn_copy) instead of redoing the BFS
-__device__ __forceinline__ bool conn_stored(uint64_t p, long long len, int64_t pool_limit) {
+// (u32 entries: the paths' region, written last) or at or above top_ok (2 x the CSR's
+// cell count: never written) -- the write pass copies them (k_conn_copy) instead of
+// redoing the BFS
+__device__ __forceinline__ bool conn_stored(uint64_t p, long long len, int64_t pool_limit, int64_t top_ok) {
   if (p >= CONN_NOT_STORED) return false;
   const int64_t w = (p & CONN_WIDE) ? 2 : 1;
-  return (int64_t)(p & ~CONN_WIDE) + w * len <= pool_limit;
+  const int64_t q = (int64_t)(p & ~CONN_WIDE);
+  return q + w * len <= pool_limit || q >= top_ok;
 }
 // IDX: int when the grid has < 2^31 vertices (32-bit index arithmetic), else int64_t
 template <int D, typename IDX>
@@ -683,7 +688,7 @@ k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
              const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm, long long* __restrict__ off,
              uint64_t* __restrict__ cells, bool write, unsigned int* __restrict__ overflow, int64_t conn_base,
              uint32_t* __restrict__ pool, unsigned long long* __restrict__ pool_top, int64_t pool_cap,
-             int64_t pool_limit, int cq_lim) {
+             int64_t pool_limit, int cq_lim, int64_t top_ok) {
   __shared__ uint32_t sq[CQ][CONN_THREADS];
   uint32_t* q = &sq[0][threadIdx.x];   // q[k * CONN_THREADS]: conflict-free columns
   // triangle -> facet edges (dm | edge index << 3); edge slot -> cofacet (type | anchor delta + 1)
@@ -730,7 +735,7 @@ k_conn_small(const uint32_t* __restrict__ eview, Grid g, int64_t b0, int64_t nb,
     uint64_t* out = write ? cells + off[b] : nullptr;
     if (write) {   // stored by the count pass: k_conn_copy writes it
       const uint64_t p = jterm[b];
-      if (conn_stored(p, off[b + 1] - off[b], pool_limit)) continue;
+      if (conn_stored(p, off[b + 1] - off[b], pool_limit, top_ok)) continue;
     }
     // count pass: room for the connector's events (<= 3 per visited triangle)
     uint32_t* ev_out = nullptr;
@@ -827,7 +832,8 @@ template <int D>
 __global__ void __launch_bounds__(256)
 k_conn_copy(Grid g, int64_t b0, int64_t nb, const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
             const long long* __restrict__ off, uint64_t* __restrict__ cells, const uint32_t* __restrict__ pool,
-            int64_t pool_limit) {
+            int64_t pool_limit, int64_t top_ok, uint32_t* __restrict__ big, unsigned long long* __restrict__ n_big,
+            int64_t big_cap) {
   __shared__ long long s_pre[8][33];
   __shared__ long long s_pool[8][32], s_out[8][32], s_anc[8][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -839,7 +845,15 @@ k_conn_copy(Grid g, int64_t b0, int64_t nb, const uint64_t* __restrict__ origin,
     if (b < nb) {
       const uint64_t pp = jterm[b];
       const long long o0 = off[b], o1 = off[b + 1];
-      if (conn_stored(pp, o1 - o0, pool_limit)) {
+      bool mine = conn_stored(pp, o1 - o0, pool_limit, top_ok);
+      if (mine && o1 - o0 > CONN_BIG && big) {   // a long list: k_conn_copy_big, many blocks on it
+        const unsigned long long k = atomicAdd(n_big, 1ull);
+        if ((int64_t)k < big_cap) {
+          big[k] = (uint32_t)(b - b0);
+          mine = false;
+        }
+      }
+      if (mine) {
         len = o1 - o0;
         int64_t an;
         int t;
@@ -879,6 +893,31 @@ k_conn_copy(Grid g, int64_t b0, int64_t nb, const uint64_t* __restrict__ origin,
     }
     __syncwarp();
   }
+}
+
+// the long stored lists k_conn_copy left (big[0 .. *n_big), connector indices from b0):
+// blockIdx.y strides over the lists, blockIdx.x over each list's events (always wide)
+template <int D>
+__global__ void __launch_bounds__(256)
+k_conn_copy_big(int64_t b0, uint64_t* __restrict__ jterm, const long long* __restrict__ off,
+                uint64_t* __restrict__ cells, const uint32_t* __restrict__ pool, const uint32_t* __restrict__ big,
+                const unsigned long long* __restrict__ n_big, int64_t big_cap) {
+  const int64_t n = (int64_t)*n_big < big_cap ? (int64_t)*n_big : big_cap;
+  for (int64_t it = blockIdx.y; it < n; it += gridDim.y) {
+    const int64_t b = b0 + big[it];
+    const uint64_t pp = jterm[b];
+    const long long o0 = off[b], len = off[b + 1] - o0;
+    const long long q = (long long)(pp & ~CONN_WIDE);
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < len; k += (long long)gridDim.x * blockDim.x)
+      cells[o0 + k] = (uint64_t)pool[q + 2 * k] | ((uint64_t)pool[q + 2 * k + 1] << 32);
+  }
+}
+
+__global__ void k_conn_big_done(int64_t b0, uint64_t* __restrict__ jterm, const uint32_t* __restrict__ big,
+                                const unsigned long long* __restrict__ n_big, int64_t big_cap) {
+  const int64_t n = (int64_t)*n_big < big_cap ? (int64_t)*n_big : big_cap;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    jterm[b0 + big[i]] = CELL_BOUNDARY;
 }
 
 // Connector BFS, mid-size case: one warp per 2-saddle, queue (WQ entries) and a
@@ -1087,9 +1126,18 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
              int64_t nlist, int64_t conn_base, const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
              long long* __restrict__ off, uint64_t* __restrict__ cells, bool write,
              unsigned long long* __restrict__ scratch, int64_t qcap, int64_t hcap,
-             unsigned int* __restrict__ overflow, Counters* __restrict__ cnt) {
+             unsigned int* __restrict__ overflow, Counters* __restrict__ cnt, uint32_t* __restrict__ pool,
+             int64_t pool_cap, const unsigned long long* __restrict__ bottom_top,
+             unsigned long long* __restrict__ top_used) {
+  // Count pass with a pool: each processed queue entry keeps its 3 facet outcomes in
+  // the key's top bits (2 bits per facet: 1 reached edge, 2 new triangle), and a
+  // completed BFS replays them into a wide event list taken from the top of the pool
+  // (growing down); the write pass copies it when it lies above the CSR's cells.
+  constexpr int QSH = 58;
+  constexpr unsigned long long QMASK = (1ull << QSH) - 1ull;
   __shared__ int s_warp[32];
   __shared__ int s_flag;
+  __shared__ long long s_base;
   __shared__ ConnTab CT;
   conn_tables_init<D>(CT);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -1145,6 +1193,12 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
           qmine++;
         }
       }
+      if (!write && pool && tid < K) {   // this entry's outcomes, for the replay into the pool
+        unsigned long long oc = 0;
+#pragma unroll
+        for (int j = 0; j < 3; j++) oc |= (unsigned long long)(ckind[j] == 1 ? 1 : isnew[j] ? 2 : 0) << (2 * j);
+        queue[head + tid] = (queue[head + tid] & QMASK) | (oc << QSH);
+      }
       // block exclusive scan of (events, enqueues) packed in one int
       int v = nmine | (qmine << 16), incl = v;
 #pragma unroll
@@ -1184,9 +1238,62 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
     }
     const bool ovf = s_flag != 0;
     __syncthreads();
+    bool stored = false;
+    if (!ovf && !write && pool) {
+      if (tid == 0) {
+        const unsigned long long need = 2ull * (unsigned long long)nev;
+        const unsigned long long old = atomicAdd(top_used, need);
+        const long long q = pool_cap - (long long)(old + need);
+        s_base = (nev > 0 && q >= (long long)*(volatile const unsigned long long*)bottom_top) ? q : -1;
+      }
+      __syncthreads();
+      const long long base = s_base;
+      stored = base >= 0;
+      if (stored) {
+        // the events in BFS order: entry by entry, its facets in order
+        long long pos = 0;
+        for (int64_t i0 = 0; i0 < tail; i0 += BFS_THREADS) {
+          const int64_t i = i0 + tid;
+          const unsigned long long qe = i < tail ? queue[i] : 0ull;
+          const unsigned oc = (unsigned)(qe >> QSH);
+          const int c = (oc & 3u ? 1 : 0) + ((oc >> 2) & 3u ? 1 : 0) + ((oc >> 4) & 3u ? 1 : 0);
+          int incl = c;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+          }
+          if (lane == 31) s_warp[wid] = incl;
+          __syncthreads();
+          int wbase = 0, tot = 0;
+          for (int w2 = 0; w2 < BFS_THREADS / 32; w2++) {
+            const int x = s_warp[w2];
+            if (w2 < wid) wbase += x;
+            tot += x;
+          }
+          if (c) {
+            const unsigned long long cur = (qe & QMASK) - 1ull;
+            int ck[3] = {0, 0, 0};
+            uint64_t cid[3] = {0, 0, 0};
+            unsigned long long ckey[3] = {0, 0, 0};
+            conn_expand<D>(CT, eview, g, (int64_t)(cur / 32), (int)(cur % 32), ck, cid, ckey);
+            long long p = base + 2 * (pos + wbase + incl - c);
+#pragma unroll
+            for (int j = 0; j < 3; j++)
+              if ((oc >> (2 * j)) & 3u) {
+                pool[p] = (uint32_t)cid[j];
+                pool[p + 1] = (uint32_t)(cid[j] >> 32);
+                p += 2;
+              }
+          }
+          pos += tot;
+          __syncthreads();
+        }
+      }
+    }
     // clean the visited set: find every queued key's slot first, then clear
     for (int64_t i = tid; i < tail; i += BFS_THREADS) {
-      const int64_t sl = bfs_find(keys, hcap, queue[i]);
+      const int64_t sl = bfs_find(keys, hcap, queue[i] & QMASK);
       queue[i] = (unsigned long long)sl;
     }
     __syncthreads();
@@ -1200,8 +1307,12 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
       for (int64_t i = tid; i < hcap; i += BFS_THREADS) { keys[i] = 0ull; owner[i] = 0ull; }
       if (tid == 0) atomicOr(overflow + (cb >> 5), 1u << (cb & 31));
     } else if (tid == 0) {
-      if (!write) off[b] = nev;
-      else jterm[b] = CELL_BOUNDARY;
+      if (!write) {
+        off[b] = nev;
+        jterm[b] = stored ? ((uint64_t)s_base | CONN_WIDE) : CONN_NOT_STORED;
+      } else {
+        jterm[b] = CELL_BOUNDARY;
+      }
     }
     __syncthreads();
   }
@@ -1266,6 +1377,25 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   const Grid& g = A.g;
   Counters* dc = A.cnt;
   Counters* hc = A.host_cnt;
+  // DMTZ_TRACE_TIMES=1: phase times on stderr (synchronising after each phase)
+  static const bool timing = [] { const char* e = getenv("DMTZ_TRACE_TIMES"); return e && e[0] == '1'; }();
+  char tlog[1024];
+  int tlen = 0;
+  auto t_prev = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!timing) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    if (tlen < 900)
+      tlen += snprintf(tlog + tlen, sizeof tlog - tlen, " %s %.2f", what,
+                       std::chrono::duration<double, std::milli>(now - t_prev).count());
+    t_prev = now;
+  };
+  struct Flush {
+    bool on; char* buf;
+    ~Flush() { if (on) fprintf(stderr, "trace ms:%s\n", buf); }
+  } flush_{timing, tlog};
+  tlog[0] = 0;
   TCK(cudaMemsetAsync(dc, 0, sizeof(Counters), s));
   k_critmask<D><<<trace_anchor_grid(g), 128, 0, s>>>((const typename Tr<D>::code_t*)A.codes, A.crit, g);
   TCK(cudaGetLastError());
@@ -1287,6 +1417,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
         A.codes, A.crit, g, V);
     TCK(cudaGetLastError());
   }
+  mark("views");
   long long* pre = A.pre;
   unsigned long long* total = &dc->pad[0];
   const int kinds_list[3] = {1, 2, 4};
@@ -1356,6 +1487,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
     if (c >= 0 && c < pool_cap) pool_cap = c;
   }
   int64_t pool_limit = 0;
+  int64_t top_ok = INT64_MAX;   // write pass: 2 x the cell count (top-pool lists above it are intact)
   // test knobs (tests/test_gpu_parity.py forces every escalation level on small grids):
   // DMTZ_TEST_CQ / DMTZ_TEST_WQ shrink the thread / warp queues, DMTZ_TEST_BFS_GROW sets
   // the block level's slot growth (default 16), DMTZ_TEST_BFS_WORDS caps the scratch
@@ -1376,26 +1508,36 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
     TCK(cudaMemsetAsync(ovf, 0, (size_t)ovf_words * 4 + 4, s));
     if (blocks_path && !write)  // descending / ascending paths
       TCK(launch_walk<D>(V, g, nbk[0], conn_base, A, off, write, dc, threads, s));
+    mark(write ? "W:start" : "C:paths");
     if (nbk[2]) {  // connectors: one thread per 2-saddle, small queues in shared memory
       const int64_t nbc = (nbk[2] + CONN_THREADS - 1) / CONN_THREADS;
       const unsigned cgrid = (unsigned)(nbc < 148 * 64 ? nbc : 148 * 64);
       if (g.N < (1ll << 31))
         k_conn_small<D, int><<<cgrid, CONN_THREADS, 0, s>>>(
             V.eview, g, conn_base, nb, A.out_origin, A.out_terminal, off, A.out_cells, write,
-            (unsigned int*)ovf, conn_base, pool, &dc->pad[2], pool_cap, pool_limit, cq_lim);
+            (unsigned int*)ovf, conn_base, pool, &dc->pad[2], pool_cap, pool_limit, cq_lim, top_ok);
       else
         k_conn_small<D, int64_t><<<cgrid, CONN_THREADS, 0, s>>>(
             V.eview, g, conn_base, nb, A.out_origin, A.out_terminal, off, A.out_cells, write,
-            (unsigned int*)ovf, conn_base, pool, &dc->pad[2], pool_cap, pool_limit, cq_lim);
+            (unsigned int*)ovf, conn_base, pool, &dc->pad[2], pool_cap, pool_limit, cq_lim, top_ok);
       if (write && pool) {  // the stored event lists (skipped above): a cooperative copy, which
                             // then marks them done -- after the BFS pass, which reads the marks
         const int64_t nw = (nbk[2] + 31) / 32;
+        // long lists go to k_conn_copy_big (their indices in the overflow list area, which the
+        // escalation below refills only afterwards), then their terminals are set
+        uint32_t* big = (uint32_t*)(ovf + ovf_words + 1);
+        TCK(cudaMemsetAsync(&dc->pad[4], 0, 8, s));
         k_conn_copy<D><<<(unsigned)((nw + 7) / 8 < 148 * 16 ? (nw + 7) / 8 : 148 * 16), 256, 0, s>>>(
-            g, conn_base, nb, A.out_origin, A.out_terminal, off, A.out_cells, pool, pool_limit);
+            g, conn_base, nb, A.out_origin, A.out_terminal, off, A.out_cells, pool, pool_limit, top_ok, big,
+            &dc->pad[4], list_cap);
+        k_conn_copy_big<D><<<dim3(64, 256), 256, 0, s>>>(conn_base, A.out_terminal, off, A.out_cells, pool, big,
+                                                       &dc->pad[4], list_cap);
+        k_conn_big_done<<<16, 256, 0, s>>>(conn_base, A.out_terminal, big, &dc->pad[4], list_cap);
       }
       if (!write) A.level_counts[0] = nbk[2];
     }
     TCK(cudaGetLastError());
+    mark("small");
     if (nbk[2]) {  // connectors that outgrew their slot: retry with 16x bigger slots, fewer threads
       // the overflow bitmask is compacted into a list on the device, in word chunks that fit the list area
       int64_t q = cq_lim;  // level 0: k_conn_small's shared-memory queues
@@ -1465,12 +1607,16 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
           // block size of the BFS: DMTZ_BFS_THREADS=64|128|256|512|1024 (default 64: the
           // connectors of a level are many, so saddles in flight beat threads per saddle --
           // C5 origin planes [427, 597) 1475 -> 1105 ms, C3 342 -> 310 ms vs 256 threads)
+          // levels with queues >= 2^17 (few, huge connectors: the longest BFS is the critical
+          // path, wider batches shorten it) take DMTZ_BFS_THREADS_BIG, default 512 (C3 tier 3
+          // 98 -> 79 s; 256: 79 s, 1024: 81 s)
           const char* bt = getenv("DMTZ_BFS_THREADS");
-          const int bfs_t = bt ? atoi(bt) : 64;
+          const char* btb = getenv("DMTZ_BFS_THREADS_BIG");
+          const int bfs_t = qn >= (1 << 17) ? (btb ? atoi(btb) : 512) : bt ? atoi(bt) : 64;
 #define DMTZ_BFS_LAUNCH(T)                                                                             \
   k_walk_block<D, T><<<(unsigned)nblk, T, 0, s>>>(V.eview, g, dlist, cn, conn_base, A.out_origin,      \
                                                   A.out_terminal, off, A.out_cells, write, sc, qn, h, \
-                                                  (unsigned int*)ovf, dc)
+                                                  (unsigned int*)ovf, dc, pool, pool_cap, &dc->pad[2], &dc->pad[3])
           if (bfs_t == 1024) DMTZ_BFS_LAUNCH(1024);
           else if (bfs_t == 512) DMTZ_BFS_LAUNCH(512);
           else if (bfs_t == 128) DMTZ_BFS_LAUNCH(128);
@@ -1479,6 +1625,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
 #undef DMTZ_BFS_LAUNCH
           TCK(cudaGetLastError());
         }
+        mark(warp_level ? "warp" : "block");
         if (!any) break;
         q = qn;
       }
@@ -1486,6 +1633,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
     if (blocks_path && write)  // after the connectors: the paths overwrite the event pool
       TCK(launch_walk<D>(V, g, nbk[0], conn_base, A, off, write, dc, threads, s));
     TCK(cudaGetLastError());
+    mark(write ? "W:paths" : "C:end");
     if (!write) {
       TCK(cudaMemsetAsync(off + nb, 0, 8, s));
       TCK(scan_i64(off, nb + 1, A.bsum, total, &hc->pad[0], s));
@@ -1496,6 +1644,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
         TCK(cudaMemcpyAsync(&oc, off + conn_base, 8, cudaMemcpyDeviceToHost, s));
         TCK(cudaStreamSynchronize(s));
         pool_limit = 2 * (int64_t)oc;
+        top_ok = 2 * A.n_cells;
       }
     }
   }
