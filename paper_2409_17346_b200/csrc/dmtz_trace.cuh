@@ -670,7 +670,7 @@ constexpr uint64_t CONN_NOT_STORED = ~0ull - 1;        // terminal slot: events 
 // a pool list of full 64-bit cell ids (two u32 per event; the warp-level connectors,
 // whose extent can exceed the 7-bit relative keys of the thread level)
 constexpr uint64_t CONN_WIDE = 1ull << 62;
-constexpr long long CONN_BIG = 8192;   // stored lists longer than this: k_conn_copy_big
+constexpr long long CONN_BIG = 256;   // stored lists longer than this: k_conn_copy_big (a warp each)
 // the terminal slot of connector b says its events are in the pool, below pool_limit
 // (u32 entries: the paths' region, written last) or at or above top_ok (2 x the CSR's
 // cell count: never written) -- the write pass copies them (k_conn_copy) instead of
@@ -896,20 +896,33 @@ k_conn_copy(Grid g, int64_t b0, int64_t nb, const uint64_t* __restrict__ origin,
 }
 
 // the long stored lists k_conn_copy left (big[0 .. *n_big), connector indices from b0):
-// blockIdx.y strides over the lists, blockIdx.x over each list's events (always wide)
+// a warp per list (k_conn_copy's 32-lists-per-warp groups serialise long lists)
 template <int D>
 __global__ void __launch_bounds__(256)
-k_conn_copy_big(int64_t b0, uint64_t* __restrict__ jterm, const long long* __restrict__ off,
-                uint64_t* __restrict__ cells, const uint32_t* __restrict__ pool, const uint32_t* __restrict__ big,
-                const unsigned long long* __restrict__ n_big, int64_t big_cap) {
+k_conn_copy_big(Grid g, int64_t b0, const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
+                const long long* __restrict__ off, uint64_t* __restrict__ cells, const uint32_t* __restrict__ pool,
+                const uint32_t* __restrict__ big, const unsigned long long* __restrict__ n_big, int64_t big_cap) {
   const int64_t n = (int64_t)*n_big < big_cap ? (int64_t)*n_big : big_cap;
-  for (int64_t it = blockIdx.y; it < n; it += gridDim.y) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < n;
+       it += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t b = b0 + big[it];
     const uint64_t pp = jterm[b];
     const long long o0 = off[b], len = off[b + 1] - o0;
     const long long q = (long long)(pp & ~CONN_WIDE);
-    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < len; k += (long long)gridDim.x * blockDim.x)
-      cells[o0 + k] = (uint64_t)pool[q + 2 * k] | ((uint64_t)pool[q + 2 * k + 1] << 32);
+    if (pp & CONN_WIDE) {
+      for (long long k = lane; k < len; k += 32)
+        cells[o0 + k] = (uint64_t)pool[q + 2 * k] | ((uint64_t)pool[q + 2 * k + 1] << 32);
+    } else {   // thread-level list: keys relative to the origin anchor
+      int64_t an;
+      int t;
+      id_cell<D>(origin[b], an, t);
+      for (long long k = lane; k < len; k += 32) {
+        const uint32_t e = pool[q + k];
+        const int ex = (int)(e & 127) - 64, ey = (int)((e >> 7) & 127) - 64, ez = (int)((e >> 14) & 127) - 64;
+        cells[o0 + k] = cell_id<D>(an + ex + ey * g.sy + ez * g.sz, (int)((e >> 21) & 31));
+      }
+    }
   }
 }
 
@@ -1520,6 +1533,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
         k_conn_small<D, int64_t><<<cgrid, CONN_THREADS, 0, s>>>(
             V.eview, g, conn_base, nb, A.out_origin, A.out_terminal, off, A.out_cells, write,
             (unsigned int*)ovf, conn_base, pool, &dc->pad[2], pool_cap, pool_limit, cq_lim, top_ok);
+      if (write && pool) mark("small");
       if (write && pool) {  // the stored event lists (skipped above): a cooperative copy, which
                             // then marks them done -- after the BFS pass, which reads the marks
         const int64_t nw = (nbk[2] + 31) / 32;
@@ -1530,9 +1544,10 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
         k_conn_copy<D><<<(unsigned)((nw + 7) / 8 < 148 * 16 ? (nw + 7) / 8 : 148 * 16), 256, 0, s>>>(
             g, conn_base, nb, A.out_origin, A.out_terminal, off, A.out_cells, pool, pool_limit, top_ok, big,
             &dc->pad[4], list_cap);
-        k_conn_copy_big<D><<<dim3(64, 256), 256, 0, s>>>(conn_base, A.out_terminal, off, A.out_cells, pool, big,
-                                                       &dc->pad[4], list_cap);
+        k_conn_copy_big<D><<<148 * 8, 256, 0, s>>>(g, conn_base, A.out_origin, A.out_terminal, off, A.out_cells,
+                                                 pool, big, &dc->pad[4], list_cap);
         k_conn_big_done<<<16, 256, 0, s>>>(conn_base, A.out_terminal, big, &dc->pad[4], list_cap);
+        mark("copy");
       }
       if (!write) A.level_counts[0] = nbk[2];
     }
