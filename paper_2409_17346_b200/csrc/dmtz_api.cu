@@ -716,6 +716,20 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
     // S-round in round r: the last sweep found no false critical cell
     const unsigned long long r = hls->round;
     CK(cudaEventRecord(e0, s));
+    // DMTZ_T3_LOG: the S-round's phases (host clock, synchronising after each)
+    char plog[512];
+    int plen = 0;
+    auto p_prev = std::chrono::steady_clock::now();
+    auto pmark = [&](const char* what) {
+      if (!c->t3_log) return;
+      cudaStreamSynchronize(s);
+      const auto now = std::chrono::steady_clock::now();
+      if (plen < 400)
+        plen += snprintf(plog + plen, sizeof plog - plen, " %s %.2f", what,
+                         std::chrono::duration<double, std::milli>(now - p_prev).count());
+      p_prev = now;
+    };
+    plog[0] = 0;
     const uint8_t* flag = nullptr;
     CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));
     CK(cudaMemsetAsync(&W.dc->pad[3], 0, 5 * 8, s));
@@ -730,6 +744,7 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
                                                    full, mbits, W.dc);
       st->launches += 1;
     }
+    pmark("tm_cells");
     if (o->tier == 3) {
       // the candidates (branches with a troublemaker) are traced in g; the others end as in f
       long long* cidx = (long long*)(sw + S.cidx);
@@ -745,6 +760,7 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
         }
         CK(cudaMemsetAsync(t3hits, 0, 8, s));
       }
+      pmark("valid");
       CK(cudaMemsetAsync(sw + S.flag, 0, (size_t)nb, s));
       k_t3_cand<D><<<clamp_blocks(nb + 1, 256, 148 * 64), 256, 0, s>>>(cells, off, kind, origin, nb, W.cand_f,
                                                                        W.cand_g, W.crit_f, g, mbits, cidx, W.dc,
@@ -766,6 +782,7 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
         CK(cudaMemcpyAsync(sw + S.save, W.lb, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(sw + S.save + (size_t)g.N * 4, W.state, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
         // trace the candidates in chunks whose g-paths fit the CSR (halving a chunk that does not)
+        pmark("cand+save");
         const auto t3_t0 = std::chrono::steady_clock::now();
         int n_chunks = 0;
         int64_t c0 = 0, chunk = ncand;
@@ -816,6 +833,7 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
                   (long long)g_trace_levels[2], (long long)g_trace_levels[3], (long long)g_trace_levels[4],
                   (long long)g_trace_levels[5]);
         }
+        pmark("trace");
         CK(cudaMemcpyAsync(W.lb, sw + S.save, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(W.state, sw + S.save + (size_t)g.N * 4, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(W.cand_g, sw + S.codes, (size_t)g.N * cs, cudaMemcpyDeviceToDevice, s));
@@ -830,6 +848,7 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
         if (!frontier_mode) CK(units_range(rg, 0, g.nz, W.units, &W.dc->n_units, s));
         CK(cudaGetLastError());
         st->launches += 6;
+        pmark("restore");
       }
       CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));
       CK(cudaMemsetAsync(&W.dc->pad[3], 0, 5 * 8, s));
@@ -853,7 +872,8 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, e0, e1));
       ss->s_ms += ms;
-      if (c->t3_log) fprintf(stderr, "S-round %lld: %.3f ms\n", (long long)ss->s_rounds, ms);
+      pmark("targets");
+      if (c->t3_log) fprintf(stderr, "S-round %lld: %.3f ms:%s\n", (long long)ss->s_rounds, ms, plog);
     }
     if (hc->n_internal) { set_err("troublemaker without an original partner"); status = DMTZ_E_INTERNAL; break; }
     const int64_t ntm = (int64_t)hc->pad[3];

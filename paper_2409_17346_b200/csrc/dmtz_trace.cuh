@@ -1133,7 +1133,11 @@ __global__ void k_bits_compact(uint32_t* __restrict__ bits, int64_t w0, int64_t 
   }
 }
 
-template <int D, int BFS_THREADS>
+// SH: the visited hash in shared memory (SB_HCAP u64 keys + u32 owner words; queues of
+// at most SB_QMAX entries), the slot in global memory holding the queue only
+constexpr int SB_HCAP = 16384, SB_QMAX = 8192;
+constexpr size_t SB_SMEM = (size_t)SB_HCAP * 12;
+template <int D, int BFS_THREADS, bool SH = false>
 __global__ void __launch_bounds__(BFS_THREADS)
 k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restrict__ list,
              int64_t nlist, int64_t conn_base, const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
@@ -1154,9 +1158,16 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
   __shared__ ConnTab CT;
   conn_tables_init<D>(CT);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  unsigned long long* queue = scratch + (int64_t)blockIdx.x * (qcap + 2 * hcap);
-  unsigned long long* keys = queue + qcap;
-  unsigned long long* owner = keys + hcap;
+  extern __shared__ unsigned long long s_hash[];
+  if (SH) hcap = SB_HCAP;
+  unsigned long long* queue = scratch + (int64_t)blockIdx.x * (SH ? qcap : qcap + 2 * hcap);
+  unsigned long long* keys = SH ? s_hash : queue + qcap;
+  unsigned long long* owner = SH ? nullptr : keys + hcap;
+  uint32_t* owner_s = SH ? (uint32_t*)(s_hash + SB_HCAP) : nullptr;
+  if (SH) {
+    for (int i = tid; i < SB_HCAP; i += BFS_THREADS) { keys[i] = 0ull; owner_s[i] = 0u; }
+    __syncthreads();
+  }
   auto key = [](int64_t an, int ty) { return (unsigned long long)(an * 32 + ty) + 1ull; };
   for (int64_t li = blockIdx.x; li < nlist; li += gridDim.x) {
     const int64_t cb = list[li], b = conn_base + cb;
@@ -1167,7 +1178,8 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
     if (tid == 0) {
       queue[0] = key(a0, t0);
       const int64_t sl = bfs_find_or_insert(keys, hcap, key(a0, t0));
-      owner[sl] = ~0ull;  // seen before every batch
+      if (SH) owner_s[sl] = ~0u;  // seen before every batch
+      else owner[sl] = ~0ull;
       s_flag = 0;
     }
     __syncthreads();
@@ -1191,7 +1203,8 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
           const int64_t slot = bfs_find_or_insert(keys, hcap, ckey[j]);
           if (slot < 0) { s_flag = 1; continue; }
           cslot[j] = slot;
-          atomicMax(owner + slot, ~((batch << 32) | (unsigned long long)(tid * 3 + j)));
+          if (SH) atomicMax(owner_s + slot, ~(((uint32_t)batch << 12) | (uint32_t)(tid * 3 + j)));
+          else atomicMax(owner + slot, ~((batch << 32) | (unsigned long long)(tid * 3 + j)));
         }
       }
       __syncthreads();
@@ -1200,7 +1213,9 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
       bool isnew[3] = {false, false, false};
       for (int j = 0; j < 3; j++) {
         if (ckind[j] == 1) nmine++;
-        if (ckind[j] == 2 && owner[cslot[j]] == ~((batch << 32) | (unsigned long long)(tid * 3 + j))) {
+        if (ckind[j] == 2 &&
+            (SH ? owner_s[cslot[j]] == ~(((uint32_t)batch << 12) | (uint32_t)(tid * 3 + j))
+                : owner[cslot[j]] == ~((batch << 32) | (unsigned long long)(tid * 3 + j)))) {
           isnew[j] = true;
           nmine++;
           qmine++;
@@ -1312,12 +1327,20 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
     __syncthreads();
     for (int64_t i = tid; i < tail; i += BFS_THREADS) {
       const long long sl = (long long)queue[i];
-      if (sl >= 0) { keys[sl] = 0ull; owner[sl] = 0ull; }
+      if (sl >= 0) {
+        keys[sl] = 0ull;
+        if (SH) owner_s[sl] = 0u;
+        else owner[sl] = 0ull;
+      }
     }
     __syncthreads();
     if (ovf) {
       // keys inserted beyond the queue (the failing batch) are not tracked: wipe the whole slot
-      for (int64_t i = tid; i < hcap; i += BFS_THREADS) { keys[i] = 0ull; owner[i] = 0ull; }
+      for (int64_t i = tid; i < hcap; i += BFS_THREADS) {
+        keys[i] = 0ull;
+        if (SH) owner_s[i] = 0u;
+        else owner[i] = 0ull;
+      }
       if (tid == 0) atomicOr(overflow + (cb >> 5), 1u << (cb & 31));
     } else if (tid == 0) {
       if (!write) {
@@ -1608,6 +1631,24 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
             k_conn_warp<D><<<wgrid, CONNW_WARPS * 32, CONNW_SMEM, s>>>(
                 V.eview, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write,
                 (unsigned int*)ovf, wq_lim, stage, pool, &dc->pad[2], pool_cap);
+            TCK(cudaGetLastError());
+            continue;
+          }
+          // few connectors (<= 1024) with queues of <= SB_QMAX entries: the visited hash in
+          // shared memory, one 256-thread block per SM -- the longest BFS is the critical path
+          // (C3 tier 3, late S-rounds: 2.4 -> 1.4 ms); many: more 64-thread blocks in flight
+          // with the global hash win (125 K connectors: 32 vs 99 ms).  DMTZ_BFS_SMEM=0: never,
+          // 2: always
+          const char* e_smem = getenv("DMTZ_BFS_SMEM");
+          const int smem_mode = e_smem ? atoi(e_smem) : 1;
+          if (smem_mode && qn <= SB_QMAX && (cn <= 1024 || smem_mode == 2)) {
+            const int64_t ns_s = words / qn < 148 * 4 ? words / qn : 148 * 4;
+            const int64_t nb_s = cn < ns_s ? cn : ns_s;
+            TCK(cudaFuncSetAttribute(k_walk_block<D, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)SB_SMEM));
+            k_walk_block<D, 256, true><<<(unsigned)nb_s, 256, SB_SMEM, s>>>(
+                V.eview, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write, sc, qn,
+                SB_HCAP, (unsigned int*)ovf, dc, pool, pool_cap, &dc->pad[2], &dc->pad[3]);
             TCK(cudaGetLastError());
             continue;
           }

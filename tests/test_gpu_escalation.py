@@ -42,12 +42,16 @@ def c3crop():
     return f, fh
 
 
-@pytest.mark.parametrize("bfs_threads", ["64", "128", "256", "512", "1024"])
-def test_connector_escalation_every_level(dmtz, monkeypatch, c3crop, bfs_threads):
+@pytest.mark.parametrize("bfs_threads,smem", [("64", "2"), ("64", "0"), ("128", "0"), ("256", "0"), ("512", "0"),
+                                               ("1024", "0")])
+def test_connector_escalation_every_level(dmtz, monkeypatch, c3crop, bfs_threads, smem):
+    """smem = 2: levels with queues <= 8192 use the shared-memory hash (all levels here);
+    0: the global-hash kernel at every block size."""
     monkeypatch.setenv("DMTZ_TEST_CQ", "2")
     monkeypatch.setenv("DMTZ_TEST_WQ", "8")
     monkeypatch.setenv("DMTZ_TEST_BFS_GROW", "2")
     monkeypatch.setenv("DMTZ_BFS_THREADS", bfs_threads)
+    monkeypatch.setenv("DMTZ_BFS_SMEM", smem)
     for fld in c3crop:
         ref = _compare_trace(dmtz, fld)
         lv = dmtz.last_trace_levels()
