@@ -542,7 +542,7 @@ dmtz_status correct_impl(dmtz_ctx* c, const float* f, const float* fhat, const d
 // separatrices + per-branch end flags.
 struct SepLayout {
   size_t codes, save, off, cells, origin, term, kind, first, cb, canc, mbits, sdirty, sdil, goff, gcells, gorigin, gterm, gkind,
-      flag, cidx, cmap, cbsum, t3box, t3st, t3psum, t3hits, total;
+      flag, cidx, cmap, cbsum, t3box, t3st, t3psum, t3hits, fsave, fsave_bytes, total;
 };
 
 // tier 3's end cache (k_t3_valid): 16-bit box coordinates, 32-bit prefix sums
@@ -554,7 +554,14 @@ SepLayout sep_layout(const dmtz_ctx* c, int tier, int64_t cap_b, int64_t cap_c) 
   const size_t cs = c->D == 3 ? 8 : 2;
   size_t o = 0;
   S.codes = o; o += align_up(N * cs);
-  if (tier == 3) { S.save = o; o += align_up(N * 8); }
+  if (tier == 3) {
+    S.save = o; o += align_up(N * 8);
+    // f's codes, critical masks and lowest-vertex positions (contiguous in the workspace),
+    // which the candidate traces' scratch overwrites
+    const Layout L = layout_for(c);
+    S.fsave_bytes = L.lb - L.cand_f;
+    S.fsave = o; o += align_up(S.fsave_bytes);
+  }
   S.off = o; o += align_up(((size_t)cap_b + 1) * 8);
   S.cells = o; o += align_up((size_t)cap_c * 8 + 8);
   S.origin = o; o += align_up((size_t)cap_b * 8 + 8);
@@ -781,6 +788,7 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
         CK(cudaMemcpyAsync(sw + S.codes, W.cand_g, (size_t)g.N * cs, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(sw + S.save, W.lb, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(sw + S.save + (size_t)g.N * 4, W.state, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(sw + S.fsave, ws + L.cand_f, S.fsave_bytes, cudaMemcpyDeviceToDevice, s));
         // trace the candidates in chunks whose g-paths fit the CSR (halving a chunk that does not)
         pmark("cand+save");
         const auto t3_t0 = std::chrono::steady_clock::now();
@@ -837,9 +845,7 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
         CK(cudaMemcpyAsync(W.lb, sw + S.save, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(W.state, sw + S.save + (size_t)g.N * 4, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(W.cand_g, sw + S.codes, (size_t)g.N * cs, cudaMemcpyDeviceToDevice, s));
-        launch_codes<D>(g, f, W.cand_f, 0, g.nz, s);
-        k_critmask<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(W.cand_f, W.crit_f, g);
-        k_lowpos<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(f, W.lowpos, g);
+        CK(cudaMemcpyAsync(ws + L.cand_f, sw + S.fsave, S.fsave_bytes, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemsetAsync(W.tbits, 0, nwords * 4, s));
         CK(cudaMemsetAsync(W.fmark, 0, W.rowbit_bytes, s));
         CK(cudaMemsetAsync(W.vchg, 0, 2 * W.rowbit_bytes, s));
@@ -847,7 +853,7 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
         // the trace cleared the counters, the full-sweep unit count among them
         if (!frontier_mode) CK(units_range(rg, 0, g.nz, W.units, &W.dc->n_units, s));
         CK(cudaGetLastError());
-        st->launches += 6;
+        st->launches += frontier_mode ? 0 : 1;
         pmark("restore");
       }
       CK(cudaMemsetAsync(W.dc, 0, offsetof(Counters, first_nonfinite), s));
