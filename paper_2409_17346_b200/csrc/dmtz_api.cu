@@ -70,7 +70,8 @@ struct dmtz_ctx {
   int has_tr = 0;
   void* nccl_comm = nullptr;
   int dist_sync = 8;
-  int t3_log = 0;     // DMTZ_T3_LOG=1: per S-round candidate counts and trace time of tier 3 on stderr  // rounds per host check of the device stop flag (1: host-synchronous rounds)
+  int t3_log = 0;
+  int t3_unordered = 1;  // tier-3 candidate traces fill connectors in any order (DMTZ_T3_ORDERED=1: FIFO)     // DMTZ_T3_LOG=1: per S-round candidate counts and trace time of tier 3 on stderr  // rounds per host check of the device stop flag (1: host-synchronous rounds)
 };
 
 #include "dmtz_dist.cuh"  // needs the context above
@@ -598,8 +599,9 @@ SepLayout sep_layout(const dmtz_ctx* c, int tier, int64_t cap_b, int64_t cap_c) 
 template <int D>
 dmtz_status trace_into(dmtz_ctx* c, char* ws, const Layout& L, const void* codes, char* sw, size_t off, size_t cells,
                        size_t origin, size_t term, size_t kind, int64_t cap_b, int64_t cap_c, int64_t* nb,
-                       int64_t* nc, cudaStream_t s, const int64_t* given_nbk = nullptr) {
+                       int64_t* nc, cudaStream_t s, const int64_t* given_nbk = nullptr, bool unordered = false) {
   TraceArgs a;
+  a.unordered = unordered;
   if (given_nbk)
     for (int k = 0; k < 3; k++) a.given_nbk[k] = given_nbk[k];
   a.g = c->g;
@@ -805,7 +807,7 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
           }
           int64_t gnb = 0, gnc = 0;
           status = trace_into<D>(c, ws, L, sw + S.codes, sw, S.goff, S.gcells, S.gorigin + 8 * c0, S.gterm + 8 * c0,
-                                 S.gkind + c0, c1 - c0, cap_c, &gnb, &gnc, s, knb);
+                                 S.gkind + c0, c1 - c0, cap_c, &gnb, &gnc, s, knb, c->t3_unordered);
           if (status == DMTZ_E_CAPACITY && c1 - c0 > 1 && gnb == c1 - c0) {
             // k_t3_fill's j inputs of this chunk were consumed: refill them, retry half
             k_t3_fill<D><<<clamp_blocks(nb, 256, 148 * 64), 256, 0, s>>>(
@@ -1157,6 +1159,8 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
   c->verbose = vb && vb[0] == '1';
   const char* t3l = getenv("DMTZ_T3_LOG");
   c->t3_log = t3l && t3l[0] == '1';
+  const char* t3o = getenv("DMTZ_T3_ORDERED");
+  c->t3_unordered = !(t3o && t3o[0] == '1');
   const char* ng = getenv("DMTZ_NO_GRAPH");
   c->no_graph = ng && ng[0] == '1';
   const char* nk = getenv("DMTZ_NO_KEYS");

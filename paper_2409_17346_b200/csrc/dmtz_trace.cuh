@@ -48,6 +48,7 @@ struct TraceArgs {
   // out_terminal (= the branch index j) for given_nbk[k] branches of each kind, grouped
   // DESC, ASC, CONN; only those are traced
   int64_t given_nbk[3] = {-1, -1, -1};
+  bool unordered = false;    // connectors' events in any order (k_walk_block UN; tier-3 candidates)
   int verbose = 0;
   int64_t n_branches = 0, n_cells = 0, n_internal = 0;
   int64_t n_overflow = 0;  // connectors whose BFS outgrew all scratch (-> DMTZ_E_CAPACITY)
@@ -1137,7 +1138,10 @@ __global__ void k_bits_compact(uint32_t* __restrict__ bits, int64_t w0, int64_t 
 // at most SB_QMAX entries), the slot in global memory holding the queue only
 constexpr int SB_HCAP = 16384, SB_QMAX = 8192;
 constexpr size_t SB_SMEM = (size_t)SB_HCAP * 12;
-template <int D, int BFS_THREADS, bool SH = false>
+// UN: unordered fill (tier-3 candidate traces, whose consumers -- the end multiset and
+// the box -- do not depend on the order): a discovered triangle is new iff this thread's
+// insert put it in the hash, positions come from shared atomics, one barrier per batch
+template <int D, int BFS_THREADS, bool SH = false, bool UN = false>
 __global__ void __launch_bounds__(BFS_THREADS)
 k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restrict__ list,
              int64_t nlist, int64_t conn_base, const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
@@ -1155,6 +1159,9 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
   __shared__ int s_warp[32];
   __shared__ int s_flag;
   __shared__ long long s_base;
+  // UN: (events, enqueues) of batch b in s_cnt[b % 3]; thread 0 zeroes the next one during
+  // batch b -- last read before batch b - 1's barrier ended (two would race)
+  __shared__ int s_cnt[3][2];
   __shared__ ConnTab CT;
   conn_tables_init<D>(CT);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -1185,6 +1192,65 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
     __syncthreads();
     int64_t head = 0, tail = 1, nev = 0;
     unsigned long long batch = 1;
+    if constexpr (UN) {
+      if (tid < 6) s_cnt[tid >> 1][tid & 1] = 0;
+      __syncthreads();
+      while (head < tail) {
+        const int64_t K = tail - head < BFS_THREADS ? tail - head : BFS_THREADS;
+        int ckind[3] = {0, 0, 0};
+        uint64_t cid[3] = {0, 0, 0};
+        unsigned long long ckey[3] = {0, 0, 0};
+        bool isnew[3] = {false, false, false};
+        int nmine = 0, qmine = 0;
+        if (tid < K) {
+          const unsigned long long cur = queue[head + tid] - 1ull;
+          conn_expand<D>(CT, eview, g, (int64_t)(cur / 32), (int)(cur % 32), ckind, cid, ckey);
+#pragma unroll
+          for (int j = 0; j < 3; j++) {
+            if (ckind[j] == 1) { nmine++; continue; }
+            if (ckind[j] != 2) continue;
+            // new iff this insert claimed the empty slot
+            const unsigned long long hh = (ckey[j] * 0x9E3779B97F4A7C15ull) >> 20;
+            bool done = false;
+            for (int64_t p = 0; p < hcap / 2 && !done; p++) {
+              const int64_t i = (int64_t)((hh + p) & (unsigned long long)(hcap - 1));
+              const unsigned long long v = atomicCAS(keys + i, 0ull, ckey[j]);
+              if (v == 0ull) { isnew[j] = true; done = true; }
+              else if (v == ckey[j]) done = true;
+            }
+            if (!done) s_flag = 1;
+            if (isnew[j]) { nmine++; qmine++; }
+          }
+          if (!write && pool) {
+            unsigned long long oc = 0;
+#pragma unroll
+            for (int j = 0; j < 3; j++) oc |= (unsigned long long)(ckind[j] == 1 ? 1 : isnew[j] ? 2 : 0) << (2 * j);
+            queue[head + tid] = (queue[head + tid] & QMASK) | (oc << QSH);
+          }
+        }
+        int* C = s_cnt[batch % 3];
+        int pe = nmine ? atomicAdd(&C[0], nmine) : 0;
+        int pq = qmine ? atomicAdd(&C[1], qmine) : 0;
+        if (tail + pq + qmine > qcap) s_flag = 1;
+        else {
+#pragma unroll
+          for (int j = 0; j < 3; j++) {
+            if (ckind[j] == 1 || isnew[j]) {
+              if (write) out[nev + pe] = cid[j];
+              pe++;
+            }
+            if (isnew[j]) { queue[tail + pq] = ckey[j]; pq++; }
+          }
+        }
+        if (tid == 0) { s_cnt[(batch + 1) % 3][0] = 0; s_cnt[(batch + 1) % 3][1] = 0; }
+        __syncthreads();
+        if (s_flag) break;
+        nev += C[0];
+        tail += C[1];
+        head += K;
+        batch++;
+      }
+    } else
     while (head < tail) {
       const int64_t K = tail - head < BFS_THREADS ? tail - head : BFS_THREADS;
       // candidates of entry head + tid: per facet j, kind 1 = reached edge, 2 = triangle
@@ -1644,11 +1710,19 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
           if (smem_mode && qn <= SB_QMAX && (cn <= 1024 || smem_mode == 2)) {
             const int64_t ns_s = words / qn < 148 * 4 ? words / qn : 148 * 4;
             const int64_t nb_s = cn < ns_s ? cn : ns_s;
-            TCK(cudaFuncSetAttribute(k_walk_block<D, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)SB_SMEM));
-            k_walk_block<D, 256, true><<<(unsigned)nb_s, 256, SB_SMEM, s>>>(
-                V.eview, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write, sc, qn,
-                SB_HCAP, (unsigned int*)ovf, dc, pool, pool_cap, &dc->pad[2], &dc->pad[3]);
+            if (A.unordered) {
+              TCK(cudaFuncSetAttribute(k_walk_block<D, 256, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)SB_SMEM));
+              k_walk_block<D, 256, true, true><<<(unsigned)nb_s, 256, SB_SMEM, s>>>(
+                  V.eview, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write, sc, qn,
+                  SB_HCAP, (unsigned int*)ovf, dc, pool, pool_cap, &dc->pad[2], &dc->pad[3]);
+            } else {
+              TCK(cudaFuncSetAttribute(k_walk_block<D, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)SB_SMEM));
+              k_walk_block<D, 256, true><<<(unsigned)nb_s, 256, SB_SMEM, s>>>(
+                  V.eview, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write, sc, qn,
+                  SB_HCAP, (unsigned int*)ovf, dc, pool, pool_cap, &dc->pad[2], &dc->pad[3]);
+            }
             TCK(cudaGetLastError());
             continue;
           }
@@ -1669,10 +1743,17 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
           const char* bt = getenv("DMTZ_BFS_THREADS");
           const char* btb = getenv("DMTZ_BFS_THREADS_BIG");
           const int bfs_t = qn >= (1 << 17) ? (btb ? atoi(btb) : 512) : bt ? atoi(bt) : 64;
-#define DMTZ_BFS_LAUNCH(T)                                                                             \
-  k_walk_block<D, T><<<(unsigned)nblk, T, 0, s>>>(V.eview, g, dlist, cn, conn_base, A.out_origin,      \
-                                                  A.out_terminal, off, A.out_cells, write, sc, qn, h, \
-                                                  (unsigned int*)ovf, dc, pool, pool_cap, &dc->pad[2], &dc->pad[3])
+#define DMTZ_BFS_LAUNCH(T)                                                                                  \
+  do {                                                                                                      \
+    if (A.unordered)                                                                                        \
+      k_walk_block<D, T, false, true><<<(unsigned)nblk, T, 0, s>>>(                                         \
+          V.eview, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write, sc, qn, h, \
+          (unsigned int*)ovf, dc, pool, pool_cap, &dc->pad[2], &dc->pad[3]);                                \
+    else                                                                                                    \
+      k_walk_block<D, T><<<(unsigned)nblk, T, 0, s>>>(                                                      \
+          V.eview, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write, sc, qn, h, \
+          (unsigned int*)ovf, dc, pool, pool_cap, &dc->pad[2], &dc->pad[3]);                                \
+  } while (0)
           if (bfs_t == 1024) DMTZ_BFS_LAUNCH(1024);
           else if (bfs_t == 512) DMTZ_BFS_LAUNCH(512);
           else if (bfs_t == 128) DMTZ_BFS_LAUNCH(128);
