@@ -22,9 +22,9 @@ def _cuda(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-def _compare(dmtz, f, fh, xi, tier, q_cap=6, full_sweeps=False):
+def _compare(dmtz, f, fh, xi, tier, q_cap=6, full_sweeps=False, ctx=None):
     ref = oracle.preserve(f, fh, xi, tier=tier, q_cap=q_cap)
-    r = dmtz.preserve(_cuda(f), _cuda(fh), xi, tier=tier, q_cap=q_cap, full_sweeps=full_sweeps)
+    r = (ctx or dmtz).preserve(_cuda(f), _cuda(fh), xi, tier=tier, q_cap=q_cap, full_sweeps=full_sweeps)
     assert r.status == ref["status"], r.message
     assert np.array_equal(r.g.cpu().numpy().view(np.uint32), ref["g"].view(np.uint32))
     e = r.edits_numpy()
@@ -61,6 +61,25 @@ def test_preserve_bit_exact(dmtz, family, shape, seed, eps, perturb, tier, q_cap
     f, fh, xi = di.random_case(shape, seed, eps=eps, family=family, perturb=perturb)
     r, ref = _compare(dmtz, f, fh, xi, tier, q_cap)
     assert ref["stats"]["s_rounds"] > 0
+
+
+@pytest.mark.parametrize("ordered,smem", [("0", "2"), ("0", "0"), ("1", "2"), ("1", "0")])
+def test_tier3_connectors_at_every_level(dmtz, monkeypatch, ordered, smem):
+    """Tier 3's candidate traces with the connector BFS forced through every escalation
+    level (test knobs as in test_gpu_escalation.py), in the unordered fill (default) and
+    the FIFO one, with the shared-memory and the global visited hash: bit-exact vs the
+    oracle."""
+    monkeypatch.setenv("DMTZ_TEST_CQ", "2")
+    monkeypatch.setenv("DMTZ_TEST_WQ", "8")
+    monkeypatch.setenv("DMTZ_TEST_BFS_GROW", "2")
+    monkeypatch.setenv("DMTZ_BFS_SMEM", smem)
+    monkeypatch.setenv("DMTZ_T3_ORDERED", ordered)   # read when the context is created
+    f, fh, xi = di.random_case((20, 31, 45), 3, eps=0.05, family="lognormal", perturb="lorenzo")
+    ctx = dmtz.Context(f.shape, torch.device("cuda", 0))
+    r, ref = _compare(dmtz, f, fh, xi, 3, ctx=ctx)
+    assert ref["stats"]["s_rounds"] > 0
+    lv = dmtz.last_trace_levels()
+    assert lv[2] > 0, lv   # the last candidate trace reached the block levels
 
 
 @pytest.mark.parametrize("tier", [3, 4])
