@@ -137,7 +137,8 @@ Layout layout_for(const dmtz_ctx* c) {
   L.ncache = o; o += align_up(N);      // per anchor: number of those false cells
   L.tbits = o; o += align_up((size_t)(c->g.nz * c->g.ny * ((c->g.nx + 31) / 32)) * 4 + 64);  // row-padded
   L.counters = o; o += align_up(sizeof(Counters) * 2);
-  L.edit_bc = o; o += align_up(((N + EDIT_CHUNK - 1) / EDIT_CHUNK + 2) * 8);
+  // edit-list block counts, and the trace's scan state over <= 64 N branch offsets
+  L.edit_bc = o; o += align_up((64 * (N + EDIT_CHUNK - 1) / EDIT_CHUNK + 2) * 8);
   const RowGeom rg = row_geom(c->g);
   L.fwords = (rg.units + 31) / 32;
   L.ebits = o; o += align_up((size_t)(c->g.nz * c->g.ny * rg.wpr) * 4 + 64);

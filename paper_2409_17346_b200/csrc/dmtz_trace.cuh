@@ -194,6 +194,97 @@ __global__ void k_scan_top(unsigned long long* __restrict__ bsum, int64_t nb, un
   if (threadIdx.x == 1023) *total = part[1023];
 }
 
+// Single-pass exclusive scan (decoupled look-back): block b (in the order blocks start,
+// ticket state[0]) scans its SCAN_CHUNK elements, publishes its aggregate in state[1 + b]
+// (flag 1 << 62), sums its predecessors' words back to the first inclusive prefix (flag
+// 2 << 62), publishes its own inclusive prefix and writes its elements once.  state:
+// 1 + ceil(n / SCAN_CHUNK) words, zeroed.  Values < 2^62.
+constexpr int SCL_THREADS = 512, SCL_PER = SCAN_CHUNK / SCL_THREADS;
+__global__ void __launch_bounds__(SCL_THREADS)
+k_scan_lb(long long* __restrict__ a, int64_t n, unsigned long long* __restrict__ state,
+          unsigned long long* __restrict__ total) {
+  __shared__ long long s_w[SCL_THREADS / 32];
+  __shared__ long long s_excl;
+  __shared__ int64_t s_bid;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) s_bid = (int64_t)atomicAdd(state, 1ull);
+  __syncthreads();
+  const int64_t bid = s_bid;
+  const int64_t base = bid * SCAN_CHUNK + (int64_t)tid * SCL_PER;
+  long long v[SCL_PER];
+  long long sum = 0;
+  const bool vec = base + SCL_PER <= n && ((uintptr_t)a & 15u) == 0;
+  if (vec) {
+    const longlong2* p2 = reinterpret_cast<const longlong2*>(a + base);   // base is even: 16-byte aligned
+#pragma unroll
+    for (int k = 0; k < SCL_PER / 2; k++) {
+      const longlong2 w = p2[k];
+      v[2 * k] = w.x;
+      v[2 * k + 1] = w.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < SCL_PER; k++) v[k] = base + k < n ? a[base + k] : 0;
+  }
+#pragma unroll
+  for (int k = 0; k < SCL_PER; k++) sum += v[k];
+  long long inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) s_w[wid] = inc;
+  __syncthreads();
+  long long wbase = 0, agg = 0;
+#pragma unroll
+  for (int w2 = 0; w2 < SCL_THREADS / 32; w2++) {
+    const long long x = s_w[w2];
+    if (w2 < wid) wbase += x;
+    agg += x;
+  }
+  if (tid == 0) {
+    volatile unsigned long long* st = state + 1;
+    long long excl = 0;
+    if (bid == 0) {
+      st[0] = (2ull << 62) | (unsigned long long)agg;
+    } else {
+      st[bid] = (1ull << 62) | (unsigned long long)agg;
+      __threadfence();
+      for (int64_t j = bid - 1;; ) {
+        const unsigned long long w = st[j];
+        const unsigned f = (unsigned)(w >> 62);
+        if (!f) continue;   // not published yet
+        excl += (long long)(w & ((1ull << 62) - 1));
+        if (f == 2) break;
+        j--;
+      }
+      __threadfence();
+      st[bid] = (2ull << 62) | (unsigned long long)(excl + agg);
+    }
+    s_excl = excl;
+    if ((bid + 1) * SCAN_CHUNK >= n) *total = (unsigned long long)(excl + agg);
+  }
+  __syncthreads();
+  long long run = s_excl + wbase + inc - sum;
+  if (vec) {
+    longlong2* p2 = reinterpret_cast<longlong2*>(a + base);
+#pragma unroll
+    for (int k = 0; k < SCL_PER / 2; k++) {
+      longlong2 w;
+      w.x = run;
+      run += v[2 * k];
+      w.y = run;
+      run += v[2 * k + 1];
+      p2[k] = w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < SCL_PER; k++)
+      if (base + k < n) { a[base + k] = run; run += v[k]; }
+  }
+}
+
 __global__ void k_scan_add(long long* __restrict__ a, int64_t n, const unsigned long long* __restrict__ bsum) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] += (long long)bsum[i / SCAN_CHUNK];
@@ -281,6 +372,12 @@ k_branch_tiles_emit(const uint32_t* __restrict__ crit, Grid g, int kind, int64_t
   const long long wbase = block_exclusive_scan(lane == 0 ? wtot : 0, &tot);
   int64_t b = base + (int64_t)bscan[blockIdx.x] + __shfl_sync(0xffffffffu, wbase, 0);
   const int top = Tr<D>::TOP;
+  // a step's branches are staged in shared memory (lane order = anchor order), then
+  // written out by consecutive lanes (coalesced; the kind byte too); a step with more
+  // than BT_STAGE branches writes directly
+  constexpr int BT_STAGE = 512;
+  __shared__ unsigned long long s_org[BT_THREADS / 32][BT_STAGE];
+  __shared__ uint8_t s_j[BT_THREADS / 32][BT_STAGE];
 #pragma unroll 1
   for (int k = 0; k < BT_PER; k++) {
     int pre = c[k];
@@ -290,30 +387,48 @@ k_branch_tiles_emit(const uint32_t* __restrict__ crit, Grid g, int kind, int64_t
       if (lane >= o) pre += v;
     }
     const int stot = __shfl_sync(0xffffffffu, pre, 31);
-    int64_t p = b + pre - c[k];
+    const int64_t p0 = b;
     b += stot;
-    if (!c[k]) continue;
-    const int64_t a = w0 + k * 32 + lane;
-    if (kind == 1) {
-      for (int tt = 1; tt < t_first_of_dim<D>(2); tt++) {
-        if (!((cm[k] >> tt) & 1u)) continue;
-        for (int j = 0; j < 2; j++) { origin[p] = cell_id<D>(a, tt); kout[p] = 1; jout[p] = (uint64_t)j; p++; }
-      }
-    } else if (kind == 2) {
-      int64_t x, y, z;
-      coords_of(g, a, x, y, z);
-      for (int tt = t_first_of_dim<D>(top - 1); tt < t_first_of_dim<D>(top); tt++) {
-        if (!((cm[k] >> tt) & 1u)) continue;
-        for (int s = 0; s < t_nlink<D>(tt); s++) {
-          if (!link_in_grid_xyz<D>(g, x, y, z, tt, s)) continue;
-          origin[p] = cell_id<D>(a, tt); kout[p] = 2; jout[p] = (uint64_t)s; p++;
+    if (!stot) continue;   // warp-uniform
+    const bool staged = stot <= BT_STAGE;
+    int q = pre - c[k];    // my first entry within the step
+    auto put = [&](uint64_t org, int j) {
+      if (staged) { s_org[wid][q] = org; s_j[wid][q] = (uint8_t)j; }
+      else { origin[p0 + q] = org; kout[p0 + q] = (uint8_t)kind; jout[p0 + q] = (uint64_t)j; }
+      q++;
+    };
+    if (c[k]) {
+      const int64_t a = w0 + k * 32 + lane;
+      if (kind == 1) {
+        for (int tt = 1; tt < t_first_of_dim<D>(2); tt++) {
+          if (!((cm[k] >> tt) & 1u)) continue;
+          for (int j = 0; j < 2; j++) put(cell_id<D>(a, tt), j);
+        }
+      } else if (kind == 2) {
+        int64_t x, y, z;
+        coords_of(g, a, x, y, z);
+        for (int tt = t_first_of_dim<D>(top - 1); tt < t_first_of_dim<D>(top); tt++) {
+          if (!((cm[k] >> tt) & 1u)) continue;
+          for (int sl = 0; sl < t_nlink<D>(tt); sl++) {
+            if (!link_in_grid_xyz<D>(g, x, y, z, tt, sl)) continue;
+            put(cell_id<D>(a, tt), sl);
+          }
+        }
+      } else if (D == 3) {
+        for (int tt = t_first_of_dim<D>(2); tt < t_first_of_dim<D>(3); tt++) {
+          if (!((cm[k] >> tt) & 1u)) continue;
+          put(cell_id<D>(a, tt), 0);
         }
       }
-    } else if (D == 3) {
-      for (int tt = t_first_of_dim<D>(2); tt < t_first_of_dim<D>(3); tt++) {
-        if (!((cm[k] >> tt) & 1u)) continue;
-        origin[p] = cell_id<D>(a, tt); kout[p] = 4; jout[p] = 0; p++;
+    }
+    if (staged) {
+      __syncwarp();
+      for (int i = lane; i < stot; i += 32) {
+        origin[p0 + i] = s_org[wid][i];
+        kout[p0 + i] = (uint8_t)kind;
+        jout[p0 + i] = (uint64_t)s_j[wid][i];
       }
+      __syncwarp();
     }
   }
 }
@@ -1457,9 +1572,8 @@ inline cudaError_t scan_i64(long long* a, int64_t n, unsigned long long* bsum, u
                             unsigned long long* host_total, cudaStream_t s) {
   const int64_t nb = (n + SCAN_CHUNK - 1) / SCAN_CHUNK;
   if (n > 0) {
-    k_scan_local<<<(unsigned)nb, 1024, 0, s>>>(a, n, bsum);
-    k_scan_top<<<1, 1024, 0, s>>>(bsum, nb, total);
-    k_scan_add<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, n, bsum);
+    TCK(cudaMemsetAsync(bsum, 0, (size_t)(nb + 1) * 8, s));
+    k_scan_lb<<<(unsigned)nb, SCL_THREADS, 0, s>>>(a, n, bsum, total);
   } else {
     TCK(cudaMemsetAsync(total, 0, 8, s));
   }
@@ -1549,6 +1663,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   }
   const int64_t nb = nbk[0] + nbk[1] + nbk[2];
   A.n_branches = nb;
+  mark("count-origins");
   if (nb > A.cap_b) return cudaSuccess;  // caller reports DMTZ_E_CAPACITY with the needed size
   if (nb == 0) {
     if (A.out_offsets) TCK(cudaMemsetAsync(A.out_offsets, 0, 8, s));
@@ -1564,6 +1679,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
     TCK(cudaGetLastError());
     base += nbk[ki];
   }
+  mark("emit");
   // walks: lengths -> offsets -> cells.  Connector slots: one per thread of the launch.
   int* ovf = (int*)pre;
   unsigned long long* sc = A.bfs;
@@ -1774,6 +1890,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
     if (!write) {
       TCK(cudaMemsetAsync(off + nb, 0, 8, s));
       TCK(scan_i64(off, nb + 1, A.bsum, total, &hc->pad[0], s));
+      mark("scan");
       A.n_cells = (int64_t)hc->pad[0];
       if (A.n_cells > A.cap_c) break;
       if (pool) {
