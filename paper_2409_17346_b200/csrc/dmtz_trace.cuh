@@ -127,9 +127,24 @@ __device__ __forceinline__ int paired_facet(const void* codes, const Grid& g, in
 }
 
 // ----------------------------------------------------------------------------- counting / emission
+// every link vertex (offsets in [-1, 1]^D) of a cell anchored at (x, y, z) is in the grid
+template <int D>
+__device__ __forceinline__ bool links_interior(const Grid& g, int64_t x, int64_t y, int64_t z) {
+  return x >= 1 && y >= 1 && x + 1 < g.nx && y + 1 < g.ny && (D == 2 || (z >= 1 && z + 1 < g.nz));
+}
+// the types of dimension d as a bit mask, and cell_id for a type of known dimension d
+template <int D, int d> __device__ __forceinline__ constexpr uint32_t dim_mask() {
+  return ((1u << t_first_of_dim_c<D>(d + 1)) - 1u) & ~((1u << t_first_of_dim_c<D>(d)) - 1u);
+}
+template <int D, int d> __device__ __forceinline__ uint64_t cell_id_dim(int64_t a, int t) {
+  return ((uint64_t)d << 56) | (uint64_t)(a * types_of_dim<D>(d) + (t - t_first_of_dim_c<D>(d)));
+}
+
 template <int D>
 __device__ __forceinline__ int branch_count(const Grid& g, int kind, uint32_t cm, int64_t x, int64_t y, int64_t z) {
   const int top = Tr<D>::TOP;
+  // (top-1)-cells have 2 link vertices in both dimensions: interior anchors need no check
+  if (kind == 2 && links_interior<D>(g, x, y, z)) return 2 * __popc(cm & dim_mask<D, Tr<D>::TOP - 1>());
   if (kind == 1) {  // DESC: two branches per critical edge
     const uint32_t em = ((1u << t_first_of_dim<D>(2)) - 1u) & ~1u;
     return 2 * __popc(cm & em);
@@ -400,13 +415,21 @@ k_branch_tiles_emit(const uint32_t* __restrict__ crit, Grid g, int kind, int64_t
     if (c[k]) {
       const int64_t a = w0 + k * 32 + lane;
       if (kind == 1) {
-        for (int tt = 1; tt < t_first_of_dim<D>(2); tt++) {
-          if (!((cm[k] >> tt) & 1u)) continue;
-          for (int j = 0; j < 2; j++) put(cell_id<D>(a, tt), j);
+        for (uint32_t m = cm[k] & dim_mask<D, 1>(); m; m &= m - 1u) {
+          const uint64_t id = cell_id_dim<D, 1>(a, __ffs(m) - 1);
+          put(id, 0);
+          put(id, 1);
         }
       } else if (kind == 2) {
         int64_t x, y, z;
         coords_of(g, a, x, y, z);
+        if (links_interior<D>(g, x, y, z)) {
+          for (uint32_t m = cm[k] & dim_mask<D, Tr<D>::TOP - 1>(); m; m &= m - 1u) {
+            const uint64_t id = cell_id_dim<D, Tr<D>::TOP - 1>(a, __ffs(m) - 1);
+            put(id, 0);
+            put(id, 1);
+          }
+        } else
         for (int tt = t_first_of_dim<D>(top - 1); tt < t_first_of_dim<D>(top); tt++) {
           if (!((cm[k] >> tt) & 1u)) continue;
           for (int sl = 0; sl < t_nlink<D>(tt); sl++) {
@@ -415,10 +438,7 @@ k_branch_tiles_emit(const uint32_t* __restrict__ crit, Grid g, int kind, int64_t
           }
         }
       } else if (D == 3) {
-        for (int tt = t_first_of_dim<D>(2); tt < t_first_of_dim<D>(3); tt++) {
-          if (!((cm[k] >> tt) & 1u)) continue;
-          put(cell_id<D>(a, tt), 0);
-        }
+        for (uint32_t m = cm[k] & dim_mask<D, 2>(); m; m &= m - 1u) put(cell_id_dim<D, 2>(a, __ffs(m) - 1), 0);
       }
     }
     if (staged) {
