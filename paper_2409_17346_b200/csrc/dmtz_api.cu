@@ -547,8 +547,14 @@ struct SepLayout {
       flag, cidx, cmap, cbsum, t3box, t3st, t3psum, t3hits, fsave, fsave_bytes, total;
 };
 
-// tier 3's end cache (k_t3_valid): 16-bit box coordinates, 32-bit prefix sums
-inline bool t3_cache_ok(const Grid& g) { return g.nx <= 65535 && g.ny <= 65535 && g.nz <= 65535 && g.N < (1ll << 31); }
+// tier 3's end cache (k_t3_valid): 16-bit box coordinates, 32-bit prefix sums; 13 B per
+// branch, so it is left out above 2^28 branches (C4's 754 M: 34 S-rounds, no need), and
+// the saved f-side arrays (20 B per voxel) above 2^26 voxels (recomputed instead) -- C4
+// tier 3 stays within a B200's memory
+inline bool t3_cache_ok(const Grid& g, int64_t cap_b) {
+  return g.nx <= 65535 && g.ny <= 65535 && g.nz <= 65535 && g.N < (1ll << 31) && cap_b <= (1ll << 28);
+}
+inline bool t3_fsave_ok(const Grid& g) { return g.N <= (1ll << 26); }
 
 SepLayout sep_layout(const dmtz_ctx* c, int tier, int64_t cap_b, int64_t cap_c) {
   SepLayout S = {};
@@ -560,9 +566,11 @@ SepLayout sep_layout(const dmtz_ctx* c, int tier, int64_t cap_b, int64_t cap_c) 
     S.save = o; o += align_up(N * 8);
     // f's codes, critical masks and lowest-vertex positions (contiguous in the workspace),
     // which the candidate traces' scratch overwrites
-    const Layout L = layout_for(c);
-    S.fsave_bytes = L.lb - L.cand_f;
-    S.fsave = o; o += align_up(S.fsave_bytes);
+    if (t3_fsave_ok(c->g)) {
+      const Layout L = layout_for(c);
+      S.fsave_bytes = L.lb - L.cand_f;
+      S.fsave = o; o += align_up(S.fsave_bytes);
+    }
   }
   S.off = o; o += align_up(((size_t)cap_b + 1) * 8);
   S.cells = o; o += align_up((size_t)cap_c * 8 + 8);
@@ -585,7 +593,7 @@ SepLayout sep_layout(const dmtz_ctx* c, int tier, int64_t cap_b, int64_t cap_c) 
     S.cidx = o; o += align_up(((size_t)cap_b + 1) * 8);        // candidate flags -> indices (scan)
     S.cmap = o; o += align_up((size_t)cap_b * 4 + 8);          // candidate -> branch of f
     S.cbsum = o; o += align_up(((size_t)cap_b / 8192 + 4) * 8);
-    if (t3_cache_ok(c->g)) {
+    if (t3_cache_ok(c->g, cap_b)) {
       S.t3box = o; o += align_up((size_t)cap_b * sizeof(T3Box) + 8);
       S.t3st = o; o += align_up((size_t)cap_b + 8);
       S.t3psum = o; o += align_up(N * 4);
@@ -791,7 +799,7 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
         CK(cudaMemcpyAsync(sw + S.codes, W.cand_g, (size_t)g.N * cs, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(sw + S.save, W.lb, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(sw + S.save + (size_t)g.N * 4, W.state, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
-        CK(cudaMemcpyAsync(sw + S.fsave, ws + L.cand_f, S.fsave_bytes, cudaMemcpyDeviceToDevice, s));
+        if (S.fsave) CK(cudaMemcpyAsync(sw + S.fsave, ws + L.cand_f, S.fsave_bytes, cudaMemcpyDeviceToDevice, s));
         // trace the candidates in chunks whose g-paths fit the CSR (halving a chunk that does not)
         pmark("cand+save");
         const auto t3_t0 = std::chrono::steady_clock::now();
@@ -848,7 +856,14 @@ dmtz_status preserve_impl(dmtz_ctx* c, const float* f, const float* fhat, const 
         CK(cudaMemcpyAsync(W.lb, sw + S.save, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(W.state, sw + S.save + (size_t)g.N * 4, (size_t)g.N * 4, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(W.cand_g, sw + S.codes, (size_t)g.N * cs, cudaMemcpyDeviceToDevice, s));
-        CK(cudaMemcpyAsync(ws + L.cand_f, sw + S.fsave, S.fsave_bytes, cudaMemcpyDeviceToDevice, s));
+        if (S.fsave) {
+          CK(cudaMemcpyAsync(ws + L.cand_f, sw + S.fsave, S.fsave_bytes, cudaMemcpyDeviceToDevice, s));
+        } else {
+          launch_codes<D>(g, f, W.cand_f, 0, g.nz, s);
+          k_critmask<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(W.cand_f, W.crit_f, g);
+          k_lowpos<D><<<anchor_grid(g, 0, g.nz, 128), 128, 0, s>>>(f, W.lowpos, g);
+          st->launches += 3;
+        }
         CK(cudaMemsetAsync(W.tbits, 0, nwords * 4, s));
         CK(cudaMemsetAsync(W.fmark, 0, W.rowbit_bytes, s));
         CK(cudaMemsetAsync(W.vchg, 0, 2 * W.rowbit_bytes, s));
