@@ -806,15 +806,20 @@ constexpr uint64_t CONN_NOT_STORED = ~0ull - 1;        // terminal slot: events 
 // a pool list of full 64-bit cell ids (two u32 per event; the warp-level connectors,
 // whose extent can exceed the 7-bit relative keys of the thread level)
 constexpr uint64_t CONN_WIDE = 1ull << 62;
-constexpr long long CONN_BIG = 256;   // stored lists longer than this: k_conn_copy_big (a warp each)
+constexpr long long CONN_BIG = 256;
+// a list in the scratch pool (the upper part of the BFS scratch, which the write pass
+// does not touch): always intact
+constexpr uint64_t CONN_SCR = 1ull << 61;
+constexpr uint64_t CONN_POS = ~(CONN_WIDE | CONN_SCR);   // stored lists longer than this: k_conn_copy_big (a warp each)
 // the terminal slot of connector b says its events are in the pool, below pool_limit
 // (u32 entries: the paths' region, written last) or at or above top_ok (2 x the CSR's
 // cell count: never written) -- the write pass copies them (k_conn_copy) instead of
 // redoing the BFS
 __device__ __forceinline__ bool conn_stored(uint64_t p, long long len, int64_t pool_limit, int64_t top_ok) {
   if (p >= CONN_NOT_STORED) return false;
+  if (p & CONN_SCR) return true;
   const int64_t w = (p & CONN_WIDE) ? 2 : 1;
-  const int64_t q = (int64_t)(p & ~CONN_WIDE);
+  const int64_t q = (int64_t)(p & CONN_POS);
   return q + w * len <= pool_limit || q >= top_ok;
 }
 // IDX: int when the grid has < 2^31 vertices (32-bit index arithmetic), else int64_t
@@ -969,9 +974,11 @@ __global__ void __launch_bounds__(256)
 k_conn_copy(Grid g, int64_t b0, int64_t nb, const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
             const long long* __restrict__ off, uint64_t* __restrict__ cells, const uint32_t* __restrict__ pool,
             int64_t pool_limit, int64_t top_ok, uint32_t* __restrict__ big, unsigned long long* __restrict__ n_big,
-            int64_t big_cap) {
+            int64_t big_cap, const uint32_t* __restrict__ spool) {
   __shared__ long long s_pre[8][33];
-  __shared__ long long s_pool[8][32], s_out[8][32], s_anc[8][32];
+  __shared__ const uint32_t* s_src[8][32];
+  __shared__ long long s_out[8][32], s_anc[8][32];
+  __shared__ bool s_wide[8][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -994,8 +1001,8 @@ k_conn_copy(Grid g, int64_t b0, int64_t nb, const uint64_t* __restrict__ origin,
         int64_t an;
         int t;
         id_cell<D>(origin[b], an, t);
-        // wide lists: the position with bit 62 set (the flag survives as a sign-free marker)
-        s_pool[w][lane] = (pp & CONN_WIDE) ? -(long long)(pp & ~CONN_WIDE) - 1 : (long long)pp;
+        s_src[w][lane] = ((pp & CONN_SCR) ? spool : pool) + (pp & CONN_POS);
+        s_wide[w][lane] = (pp & CONN_WIDE) != 0;
         s_out[w][lane] = o0;
         s_anc[w][lane] = an;
         jterm[b] = CELL_BOUNDARY;
@@ -1017,12 +1024,11 @@ k_conn_copy(Grid g, int64_t b0, int64_t nb, const uint64_t* __restrict__ origin,
       for (int st = 16; st > 0; st >>= 1)
         if (s_pre[w][j + st] <= i) j += st;
       const long long k = i - s_pre[w][j];
-      const long long pj = s_pool[w][j];
-      if (pj < 0) {   // wide list: the 64-bit cell ids
-        const long long q = -pj - 1 + 2 * k;
-        cells[s_out[w][j] + k] = (uint64_t)pool[q] | ((uint64_t)pool[q + 1] << 32);
+      const uint32_t* src = s_src[w][j];
+      if (s_wide[w][j]) {   // wide list: the 64-bit cell ids
+        cells[s_out[w][j] + k] = (uint64_t)src[2 * k] | ((uint64_t)src[2 * k + 1] << 32);
       } else {
-        const uint32_t e = pool[pj + k];
+        const uint32_t e = src[k];
         const int ex = (int)(e & 127) - 64, ey = (int)((e >> 7) & 127) - 64, ez = (int)((e >> 14) & 127) - 64;
         cells[s_out[w][j] + k] = cell_id<D>(s_anc[w][j] + ex + ey * g.sy + ez * g.sz, (int)((e >> 21) & 31));
       }
@@ -1037,7 +1043,8 @@ template <int D>
 __global__ void __launch_bounds__(256)
 k_conn_copy_big(Grid g, int64_t b0, const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
                 const long long* __restrict__ off, uint64_t* __restrict__ cells, const uint32_t* __restrict__ pool,
-                const uint32_t* __restrict__ big, const unsigned long long* __restrict__ n_big, int64_t big_cap) {
+                const uint32_t* __restrict__ big, const unsigned long long* __restrict__ n_big, int64_t big_cap,
+                const uint32_t* __restrict__ spool) {
   const int64_t n = (int64_t)*n_big < big_cap ? (int64_t)*n_big : big_cap;
   const int lane = threadIdx.x & 31;
   for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < n;
@@ -1045,16 +1052,16 @@ k_conn_copy_big(Grid g, int64_t b0, const uint64_t* __restrict__ origin, uint64_
     const int64_t b = b0 + big[it];
     const uint64_t pp = jterm[b];
     const long long o0 = off[b], len = off[b + 1] - o0;
-    const long long q = (long long)(pp & ~CONN_WIDE);
+    const uint32_t* src = ((pp & CONN_SCR) ? spool : pool) + (pp & CONN_POS);
     if (pp & CONN_WIDE) {
       for (long long k = lane; k < len; k += 32)
-        cells[o0 + k] = (uint64_t)pool[q + 2 * k] | ((uint64_t)pool[q + 2 * k + 1] << 32);
+        cells[o0 + k] = (uint64_t)src[2 * k] | ((uint64_t)src[2 * k + 1] << 32);
     } else {   // thread-level list: keys relative to the origin anchor
       int64_t an;
       int t;
       id_cell<D>(origin[b], an, t);
       for (long long k = lane; k < len; k += 32) {
-        const uint32_t e = pool[q + k];
+        const uint32_t e = src[k];
         const int ex = (int)(e & 127) - 64, ey = (int)((e >> 7) & 127) - 64, ez = (int)((e >> 14) & 127) - 64;
         cells[o0 + k] = cell_id<D>(an + ex + ey * g.sy + ez * g.sz, (int)((e >> 21) & 31));
       }
@@ -1086,7 +1093,8 @@ k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restri
             int64_t nlist, int64_t conn_base, const uint64_t* __restrict__ origin, uint64_t* __restrict__ jterm,
             long long* __restrict__ off, uint64_t* __restrict__ cells, bool write,
             unsigned int* __restrict__ overflow, int wq_lim, uint64_t* __restrict__ stage,
-            uint32_t* __restrict__ pool, unsigned long long* __restrict__ pool_top, int64_t pool_cap) {
+            uint32_t* __restrict__ pool, unsigned long long* __restrict__ pool_top, int64_t pool_cap,
+            uint64_t pool_flag) {
   // count pass with a pool (stage != nullptr): the connector's events (cell ids) go to the
   // warp's staging slot (3 WQ entries) and, once complete, to an exact-size pool list
   extern __shared__ unsigned long long smw[];
@@ -1205,7 +1213,7 @@ k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restri
             pool[p + 2 * i] = (uint32_t)c;
             pool[p + 2 * i + 1] = (uint32_t)(c >> 32);
           }
-        if (lane == 0) jterm[b] = fits ? (p | CONN_WIDE) : CONN_NOT_STORED;
+        if (lane == 0) jterm[b] = fits ? (p | CONN_WIDE | pool_flag) : CONN_NOT_STORED;
       }
     }
     __syncwarp();
@@ -1284,7 +1292,7 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
              unsigned long long* __restrict__ scratch, int64_t qcap, int64_t hcap,
              unsigned int* __restrict__ overflow, Counters* __restrict__ cnt, uint32_t* __restrict__ pool,
              int64_t pool_cap, const unsigned long long* __restrict__ bottom_top,
-             unsigned long long* __restrict__ top_used) {
+             unsigned long long* __restrict__ top_used, uint64_t pool_flag) {
   // Count pass with a pool: each processed queue entry keeps its 3 facet outcomes in
   // the key's top bits (2 bits per facet: 1 reached edge, 2 new triangle), and a
   // completed BFS replays them into a wide event list taken from the top of the pool
@@ -1546,7 +1554,7 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
     } else if (tid == 0) {
       if (!write) {
         off[b] = nev;
-        jterm[b] = stored ? ((uint64_t)s_base | CONN_WIDE) : CONN_NOT_STORED;
+        jterm[b] = stored ? ((uint64_t)s_base | CONN_WIDE | pool_flag) : CONN_NOT_STORED;
       } else {
         jterm[b] = CELL_BOUNDARY;
       }
@@ -1738,7 +1746,29 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   const int cq_lim = (int)env_int("DMTZ_TEST_CQ", CQ, 1, CQ);
   const int wq_lim = (int)env_int("DMTZ_TEST_WQ", WQ, 4, WQ);
   const int64_t grow = env_int("DMTZ_TEST_BFS_GROW", 16, 2, 16);
-  const int64_t words = env_int("DMTZ_TEST_BFS_WORDS", words_all, 1024, words_all);
+  int64_t words = env_int("DMTZ_TEST_BFS_WORDS", words_all, 1024, words_all);
+  // Scratch pool (full and range traces with a large scratch): the upper 3/4 of the BFS
+  // scratch, which the write pass never touches, holds the wide event lists of the warp
+  // and block levels -- intact whatever the CSR's size, so the write pass copies them
+  // instead of redoing those BFS.  The block levels' slots keep the lower quarter.
+  // DMTZ_SCRATCH_POOL=0: off (the lists then go to the output buffer's pools).
+  uint32_t* spool = nullptr;
+  int64_t spool_cap = 0;
+  {
+    const char* sp = getenv("DMTZ_SCRATCH_POOL");   // 0: off, 2: also on small scratch (tests)
+    const int spm = sp ? atoi(sp) : 1;
+    if (pool && !given && words == words_all && spm && (words_all >= (1ll << 24) || spm == 2)) {
+      const int64_t keep = words_all / 4;
+      spool = (uint32_t*)(sc + keep);
+      spool_cap = 2 * (words_all - keep);
+      words = keep;
+    }
+  }
+  // the pool the warp / block levels use: (base, capacity, bottom counter, flag)
+  uint32_t* wpool = spool ? spool : pool;
+  const int64_t wpool_cap = spool ? spool_cap : pool_cap;
+  unsigned long long* wpool_bottom = spool ? &dc->pad[5] : &dc->pad[2];
+  const uint64_t wpool_flag = spool ? CONN_SCR : 0ull;
   for (int i = 0; i < 10; i++) A.level_counts[i] = 0;
   TCK(cudaMemsetAsync(&dc->pad[2], 0, 8, s));
   for (int pass = 0; pass < 2; pass++) {
@@ -1768,9 +1798,9 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
         TCK(cudaMemsetAsync(&dc->pad[4], 0, 8, s));
         k_conn_copy<D><<<(unsigned)((nw + 7) / 8 < 148 * 16 ? (nw + 7) / 8 : 148 * 16), 256, 0, s>>>(
             g, conn_base, nb, A.out_origin, A.out_terminal, off, A.out_cells, pool, pool_limit, top_ok, big,
-            &dc->pad[4], list_cap);
+            &dc->pad[4], list_cap, spool);
         k_conn_copy_big<D><<<148 * 8, 256, 0, s>>>(g, conn_base, A.out_origin, A.out_terminal, off, A.out_cells,
-                                                 pool, big, &dc->pad[4], list_cap);
+                                                 pool, big, &dc->pad[4], list_cap, spool);
         k_conn_big_done<<<16, 256, 0, s>>>(conn_base, A.out_terminal, big, &dc->pad[4], list_cap);
         mark("copy");
       }
@@ -1829,10 +1859,10 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
             const unsigned wgrid = (unsigned)(nbw < 148 * 12 ? nbw : 148 * 12);
             // count pass with a pool: stage the events in the (still unused) BFS scratch
             const size_t stage_bytes = (size_t)wgrid * CONNW_WARPS * 3 * WQ * 8;
-            uint64_t* stage = (!write && pool && stage_bytes <= A.bfs_bytes) ? (uint64_t*)sc : nullptr;
+            uint64_t* stage = (!write && pool && stage_bytes <= (size_t)words * 8) ? (uint64_t*)sc : nullptr;
             k_conn_warp<D><<<wgrid, CONNW_WARPS * 32, CONNW_SMEM, s>>>(
                 V.eview, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write,
-                (unsigned int*)ovf, wq_lim, stage, pool, &dc->pad[2], pool_cap);
+                (unsigned int*)ovf, wq_lim, stage, wpool, wpool_bottom, wpool_cap, wpool_flag);
             TCK(cudaGetLastError());
             continue;
           }
@@ -1851,19 +1881,19 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
                                        (int)SB_SMEM));
               k_walk_block<D, 256, true, true><<<(unsigned)nb_s, 256, SB_SMEM, s>>>(
                   V.eview, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write, sc, qn,
-                  SB_HCAP, (unsigned int*)ovf, dc, pool, pool_cap, &dc->pad[2], &dc->pad[3]);
+                  SB_HCAP, (unsigned int*)ovf, dc, wpool, wpool_cap, wpool_bottom, &dc->pad[3], wpool_flag);
             } else {
               TCK(cudaFuncSetAttribute(k_walk_block<D, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)SB_SMEM));
               k_walk_block<D, 256, true><<<(unsigned)nb_s, 256, SB_SMEM, s>>>(
                   V.eview, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write, sc, qn,
-                  SB_HCAP, (unsigned int*)ovf, dc, pool, pool_cap, &dc->pad[2], &dc->pad[3]);
+                  SB_HCAP, (unsigned int*)ovf, dc, wpool, wpool_cap, wpool_bottom, &dc->pad[3], wpool_flag);
             }
             TCK(cudaGetLastError());
             continue;
           }
           if (!cleared) {  // block-BFS slots: zero once per level (the kernel leaves them zero)
-            TCK(cudaMemsetAsync(sc, 0, A.bfs_bytes, s));
+            TCK(cudaMemsetAsync(sc, 0, (size_t)words * 8, s));
             cleared = true;
           }
           const int64_t nblk = cn < ns ? cn : ns;
@@ -1884,11 +1914,11 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
     if (A.unordered)                                                                                        \
       k_walk_block<D, T, false, true><<<(unsigned)nblk, T, 0, s>>>(                                         \
           V.eview, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write, sc, qn, h, \
-          (unsigned int*)ovf, dc, pool, pool_cap, &dc->pad[2], &dc->pad[3]);                                \
+          (unsigned int*)ovf, dc, wpool, wpool_cap, wpool_bottom, &dc->pad[3], wpool_flag);                 \
     else                                                                                                    \
       k_walk_block<D, T><<<(unsigned)nblk, T, 0, s>>>(                                                      \
           V.eview, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write, sc, qn, h, \
-          (unsigned int*)ovf, dc, pool, pool_cap, &dc->pad[2], &dc->pad[3]);                                \
+          (unsigned int*)ovf, dc, wpool, wpool_cap, wpool_bottom, &dc->pad[3], wpool_flag);                 \
   } while (0)
           if (bfs_t == 1024) DMTZ_BFS_LAUNCH(1024);
           else if (bfs_t == 512) DMTZ_BFS_LAUNCH(512);

@@ -74,6 +74,21 @@ def test_connector_escalation_no_pool(dmtz, monkeypatch, c3crop):
     assert lv[1] > 0 and lv[2] > 0 and lv[3] > 0, lv
 
 
+@pytest.mark.parametrize("smem", ["2", "0"])
+def test_connector_escalation_scratch_pool(dmtz, monkeypatch, c3crop, smem):
+    """Every level with the warp / block levels' event lists in the scratch pool (the
+    upper part of the BFS scratch; forced on this small grid), copied by the write pass."""
+    monkeypatch.setenv("DMTZ_TEST_CQ", "2")
+    monkeypatch.setenv("DMTZ_TEST_WQ", "8")
+    monkeypatch.setenv("DMTZ_TEST_BFS_GROW", "2")
+    monkeypatch.setenv("DMTZ_BFS_SMEM", smem)
+    monkeypatch.setenv("DMTZ_SCRATCH_POOL", "2")
+    for fld in c3crop:
+        _compare_trace(dmtz, fld)
+        lv = dmtz.last_trace_levels()
+        assert lv[1] > 0 and lv[2] > 0 and lv[3] > 0, lv
+
+
 def test_connector_default_levels(dmtz, c3crop):
     """Without knobs the C3 crop's large connectors still reach the warp level."""
     _compare_trace(dmtz, c3crop[0])
