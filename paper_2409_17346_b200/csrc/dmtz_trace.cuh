@@ -1083,9 +1083,11 @@ __global__ void k_conn_big_done(int64_t b0, uint64_t* __restrict__ jterm, const 
 // (entry, facet) order, decided by an atomicMin of batch << 7 | candidate on its
 // slot's owner word), so the events come out in the sequential FIFO order.
 constexpr int WQ = 512, WH = 1024, CONNW_WARPS = 4;
-// per warp: hash keys (u64), owner words (u32), and the queue as hash slots (u16) --
-// 13 KB, so 4 blocks (16 warps) fit an SM (16 KB with a queue of keys: 3 blocks)
-constexpr size_t CONNW_WARP_BYTES = (size_t)WH * 8 + WH * 4 + WQ * 2;
+// per warp: hash keys (u32: the triangle relative to the origin anchor, 8 bits per axis
+// + type, bit 31 set), owner words (u32), and the queue as hash slots (u16) -- 9 KB, so
+// 6 blocks (24 warps) fit an SM (u64 keys: 13 KB, 4 blocks).  A triangle more than 127
+// anchors from the origin on an axis sends the saddle to the block level.
+constexpr size_t CONNW_WARP_BYTES = (size_t)WH * 4 + WH * 4 + WQ * 2;
 constexpr size_t CONNW_SMEM = (size_t)CONNW_WARPS * CONNW_WARP_BYTES;
 template <int D>
 __global__ void __launch_bounds__(CONNW_WARPS * 32)
@@ -1097,26 +1099,34 @@ k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restri
             uint64_t pool_flag) {
   // count pass with a pool (stage != nullptr): the connector's events (cell ids) go to the
   // warp's staging slot (3 WQ entries) and, once complete, to an exact-size pool list
-  extern __shared__ unsigned long long smw[];
+  extern __shared__ uint32_t smw[];
   __shared__ ConnTab CT;
+  __shared__ int64_t s_dmw[8];
   conn_tables_init<D>(CT);
+  if (threadIdx.x < 8) s_dmw[threadIdx.x] = mask_delta(g, (int)threadIdx.x);
+  __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  unsigned long long* keys = smw + (size_t)wid * (CONNW_WARP_BYTES / 8);
-  uint32_t* owner = (uint32_t*)(keys + WH);
+  uint32_t* keys = smw + (size_t)wid * (CONNW_WARP_BYTES / 4);
+  uint32_t* owner = keys + WH;
   uint16_t* queue = (uint16_t*)(owner + WH);  // queue entry = the hash slot of its key
-  for (int i = lane; i < WH; i += 32) { keys[i] = 0ull; owner[i] = 0xFFFFFFFFu; }
+  for (int i = lane; i < WH; i += 32) { keys[i] = 0u; owner[i] = 0xFFFFFFFFu; }
   __syncwarp();
-  auto key = [](int64_t an, int ty) { return (unsigned long long)(an * 32 + ty) + 1ull; };
-  auto hslot = [](unsigned long long k) { return (int)((k * 0x9E3779B97F4A7C15ull) >> 54); };  // 10 bits
-  auto find_or_insert = [&](unsigned long long k) -> int {
+  constexpr int T0 = t_first_of_dim_c<D>(2), E0 = t_first_of_dim_c<D>(1);
+  auto rkey = [](int dx, int dy, int dz, int ty) {
+    return (uint32_t)(dx + 128) | ((uint32_t)(dy + 128) << 8) | ((uint32_t)(dz + 128) << 16) | ((uint32_t)ty << 24) |
+           0x80000000u;
+  };
+  auto hslot = [](uint32_t k) { return (int)((k * 0x9E3779B1u) >> 22); };  // 10 bits
+  auto find_or_insert = [&](uint32_t k) -> int {
     const int h = hslot(k);
     for (int p = 0; p < WH / 2; p++) {
       const int i = (h + p) & (WH - 1);
-      const unsigned long long v = atomicCAS(keys + i, 0ull, k);
-      if (v == 0ull || v == k) return i;
+      const uint32_t v = atomicCAS(keys + i, 0u, k);
+      if (v == 0u || v == k) return i;
     }
     return -1;
   };
+  const int64_t sy = g.sy, sz = g.sz;
   for (int64_t li = (int64_t)blockIdx.x * CONNW_WARPS + wid; li < nlist; li += (int64_t)gridDim.x * CONNW_WARPS) {
     const int64_t cb = list[li], b = conn_base + cb;
     int64_t a0;
@@ -1125,7 +1135,7 @@ k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restri
     uint64_t* stg = stage ? stage + (((int64_t)blockIdx.x * CONNW_WARPS + wid) * (3 * WQ)) : nullptr;
     uint64_t* out = write ? cells + off[b] : stg;
     if (lane == 0) {
-      const int s0 = find_or_insert(key(a0, t0));
+      const int s0 = find_or_insert(rkey(0, 0, 0, t0));
       owner[s0] = 0u;  // seen before every batch
       queue[0] = (uint16_t)s0;
     }
@@ -1138,16 +1148,38 @@ k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restri
       const int K = tail - head < 32 ? tail - head : 32;
       int ckind[3] = {0, 0, 0}, cslot[3] = {-1, -1, -1};
       uint64_t cid[3] = {0, 0, 0};
-      unsigned long long ckey[3] = {0, 0, 0};
+      uint32_t ckey[3] = {0, 0, 0};
       bool bad = false;
       if (lane < K) {
-        const unsigned long long cur = keys[queue[head + lane]] - 1ull;
-        const int64_t B = (int64_t)(cur / 32);
-        const int bt = (int)(cur % 32);
-        conn_expand<D>(CT, eview, g, B, bt, ckind, cid, ckey);
+        // the entry, relative to the origin anchor; its 3 facet edges read at once
+        const uint32_t cur = keys[queue[head + lane]];
+        const int bx = (int)(cur & 255) - 128, by = (int)((cur >> 8) & 255) - 128, bz = (int)((cur >> 16) & 255) - 128;
+        const int bt = (int)((cur >> 24) & 31);
+        const int64_t B = a0 + bx + by * sy + bz * sz;
+        uint32_t tf[3], ev[3];
+        int64_t E[3];
 #pragma unroll
         for (int j = 0; j < 3; j++) {
-          if (ckind[j] != 2) continue;
+          tf[j] = CT.tf[(bt - T0) * 3 + j];
+          E[j] = B + s_dmw[tf[j] & 7];
+          ev[j] = (__ldg(eview + E[j]) >> (4 * (int)(tf[j] >> 3))) & 15u;
+        }
+#pragma unroll
+        for (int j = 0; j < 3; j++) {
+          const int dm = (int)(tf[j] & 7), e = (int)(tf[j] >> 3);
+          if (ev[j] & 8u) { ckind[j] = 1; cid[j] = cell_id<D>(E[j], E0 + e); continue; }
+          const uint32_t sl = ev[j] & 7u;
+          if (sl == 7u) continue;
+          const uint32_t ec = CT.ec[e * 8 + sl];
+          const int nt = (int)(ec & 31);
+          const int ox = (dm & 1) + (int)((ec >> 5) & 3) - 1, oy = ((dm >> 1) & 1) + (int)((ec >> 7) & 3) - 1,
+                    oz = ((dm >> 2) & 1) + (int)((ec >> 9) & 3) - 1;
+          if (ox == 0 && oy == 0 && oz == 0 && nt == bt) continue;
+          const int nx_ = bx + ox, ny_ = by + oy, nz_ = bz + oz;
+          if (nx_ < -127 || nx_ > 127 || ny_ < -127 || ny_ > 127 || nz_ < -127 || nz_ > 127) { bad = true; continue; }
+          ckind[j] = 2;
+          cid[j] = cell_id<D>(B + ox + oy * sy + oz * sz, nt);
+          ckey[j] = rkey(nx_, ny_, nz_, nt);
           const int slot = find_or_insert(ckey[j]);
           if (slot < 0) { bad = true; continue; }
           cslot[j] = slot;
@@ -1189,13 +1221,13 @@ k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restri
     }
     __syncwarp();
     if (ovf) {  // keys of the failing batch are not all queued: wipe the table
-      for (int i = lane; i < WH; i += 32) { keys[i] = 0ull; owner[i] = 0xFFFFFFFFu; }
+      for (int i = lane; i < WH; i += 32) { keys[i] = 0u; owner[i] = 0xFFFFFFFFu; }
       if (lane == 0) atomicOr(overflow + (cb >> 5), 1u << (cb & 31));
     } else {
       // clean the visited set: the queue holds exactly the occupied slots
       for (int i = lane; i < tail; i += 32) {
         const int sl = queue[i];
-        keys[sl] = 0ull;
+        keys[sl] = 0u;
         owner[sl] = 0xFFFFFFFFu;
       }
       if (lane == 0) {
