@@ -807,6 +807,10 @@ __global__ void k_halo(float* __restrict__ gf, const float* __restrict__ planes,
 // only cells anchored there, and every false cell is anchored there relative
 // to its own target), aggregated in shared memory when it fits.
 // ---------------------------------------------------------------------------
+#ifndef DMTZ_EDIT_NW
+#define DMTZ_EDIT_NW 2
+#endif
+constexpr int EDIT_NW = DMTZ_EDIT_NW;
 template <int D>
 __global__ void k_edit_rows(uint32_t* __restrict__ tbits, int64_t nwords, const float* __restrict__ fhat,
                             const float* __restrict__ lb, float* __restrict__ gf, uint32_t* __restrict__ state,
@@ -836,19 +840,22 @@ __global__ void k_edit_rows(uint32_t* __restrict__ tbits, int64_t nwords, const 
     uint32_t word = wi < w_end ? tbits[wi] : 0u;
     if (word) tbits[wi] = 0;
     unsigned nz = __ballot_sync(0xffffffffu, word != 0);
-    // two target words per pass: their loads are independent, one memory round trip for both
+    // EDIT_NW target words per pass: their loads are independent, one memory round trip
     while (nz) {
-      int src[2];
-      src[0] = __ffs(nz) - 1;
-      nz &= nz - 1;
-      src[1] = nz ? __ffs(nz) - 1 : -1;
-      if (nz) nz &= nz - 1;
-      uint32_t st[2] = {0u, 0u};
-      float fh[2] = {0.f, 0.f}, lbv[2] = {0.f, 0.f};
-      int64_t v[2] = {0, 0};
-      bool mine[2];
+      int src[EDIT_NW];
 #pragma unroll
-      for (int h = 0; h < 2; h++) {
+      for (int h = 0; h < EDIT_NW; h++) {
+        src[h] = nz ? __ffs(nz) - 1 : -1;
+        if (nz) nz &= nz - 1;
+      }
+      uint32_t st[EDIT_NW];
+      float fh[EDIT_NW], lbv[EDIT_NW];
+      int64_t v[EDIT_NW];
+      bool mine[EDIT_NW];
+#pragma unroll
+      for (int h = 0; h < EDIT_NW; h++) { st[h] = 0u; fh[h] = 0.f; lbv[h] = 0.f; v[h] = 0; }
+#pragma unroll
+      for (int h = 0; h < EDIT_NW; h++) {
         const int sw = src[h] < 0 ? src[0] : src[h];
         const uint32_t wv = __shfl_sync(0xffffffffu, word, sw);
         mine[h] = src[h] >= 0 && ((wv >> lane) & 1u);
@@ -875,7 +882,7 @@ __global__ void k_edit_rows(uint32_t* __restrict__ tbits, int64_t nwords, const 
         }
       }
 #pragma unroll
-      for (int h = 0; h < 2; h++) {
+      for (int h = 0; h < EDIT_NW; h++) {
         bool ch = false;
         if (mine[h]) {
           targets++;
