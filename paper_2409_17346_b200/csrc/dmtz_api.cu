@@ -151,7 +151,7 @@ Layout layout_for(const dmtz_ctx* c) {
   L.dist = 0;
   if (c->dist) {  // local f, fhat, g, halo staging (f32 each) + the reduced counters
     L.dist = o;
-    o += align_up(4 * N * sizeof(float) + (size_t)(64 + DCTL_N) * 8);
+    o += align_up(4 * N * sizeof(float) + (size_t)(64 + DCTL_N + 1) * 8);   // + the 2 face flags
   }
   L.trace = o; o += align_up(trace_scratch_bytes(c->g, c->D));
   L.total = o;
@@ -988,6 +988,8 @@ static dmtz_status correct_dist(dmtz_ctx* c, const float* f, const float* fhat, 
   std::vector<long long> tot(nout, 0);
   int status = -1;
   int64_t r = 0;
+  unsigned* fflags = (unsigned*)(dcnt + 64 + DCTL_N);   // this round's two face flags (k_face_flags)
+  CK(cudaMemsetAsync(fflags, 0, 8, s));
   if (c->dist_sync > 1) {
     // batched: rounds_per_sync rounds per host check; the stop rule and the halo gates
     // live on the device (k_dist_stop), every face is exchanged, and a face whose planes
@@ -1012,16 +1014,20 @@ static dmtz_status correct_dist(dmtz_ctx* c, const float* f, const float* fhat, 
             }
         }
         uint32_t* vround = W.vchg + (int64_t)(r & 1) * W.vwords;
-        CK(cudaMemsetAsync(vround + oz0 * per_plane, 0, (size_t)(nface * per_plane) * 4, s));
-        CK(cudaMemsetAsync(vround + (oz1 - nface) * per_plane, 0, (size_t)(nface * per_plane) * 4, s));
+        if (c->world > 1) {   // face flags (a one-rank world has no faces)
+          CK(cudaMemsetAsync(vround + oz0 * per_plane, 0, (size_t)(nface * per_plane) * 4, s));
+          CK(cudaMemsetAsync(vround + (oz1 - nface) * per_plane, 0, (size_t)(nface * per_plane) * 4, s));
+        }
         const dmtz_status rs = slab_round_enqueue(c, floc, fhloc, o, &sl, ws, L, gloc, r, o->full_sweeps != 0, s, ctl);
         if (rs) return rs;
-        k_dist_counters<<<1, 256, 0, s>>>(W.dc, r, dcnt, nout, vround, g, rg, oz0, oz0 + nface, oz1 - nface, oz1,
-                                          c->rank, ctl);
+        if (c->world > 1)
+          k_face_flags<<<clamp_blocks(2 * nface * per_plane, 256, 148 * 2), 256, 0, s>>>(
+              vround, per_plane, oz0, oz0 + nface, oz1 - nface, oz1, fflags, ctl);
+        k_dist_counters<<<1, 256, 0, s>>>(W.dc, r, dcnt, nout, fflags, c->rank, ctl);
         CK(cudaGetLastError());
         if (c->tr.allreduce_sum_i64(c->tr.user, (int64_t*)dcnt, nout, (dmtz_stream_t)s)) return comm_fail("allreduce");
         k_dist_stop<<<1, 32, 0, s>>>(dcnt, ctl, max_rounds, c->rank, c->world);
-        st->launches += 7 + (r > 1 ? 1 : 0);  // begin, [units], screen, decode, edit_rows, loop_check, counters, stop
+        st->launches += 8 + (r > 1 ? 1 : 0);  // begin, [units], screen, decode, edit_rows, loop_check, flags, counters, stop
       }
       CK(cudaMemcpyAsync(hctl, ctl, DCTL_N * 8, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
@@ -1060,9 +1066,10 @@ static dmtz_status correct_dist(dmtz_ctx* c, const float* f, const float* fhat, 
     CK(cudaMemsetAsync(vround + (oz1 - nface) * per_plane, 0, (size_t)(nface * per_plane) * 4, s));
     const dmtz_status rs = slab_round_enqueue(c, floc, fhloc, o, &sl, ws, L, gloc, r, o->full_sweeps != 0, s);
     if (rs) return rs;
-    k_dist_counters<<<1, 256, 0, s>>>(W.dc, r, dcnt, nout, vround, g, rg, oz0, oz0 + nface, oz1 - nface, oz1,
-                                      c->rank, nullptr);
-    st->launches += 6 + (r > 1 ? 1 : 0);  // set_round, [units], screen, decode, edit_rows, loop_check, counters
+    k_face_flags<<<clamp_blocks(2 * nface * per_plane, 256, 148 * 2), 256, 0, s>>>(
+        vround, per_plane, oz0, oz0 + nface, oz1 - nface, oz1, fflags, nullptr);
+    k_dist_counters<<<1, 256, 0, s>>>(W.dc, r, dcnt, nout, fflags, c->rank, nullptr);
+    st->launches += 7 + (r > 1 ? 1 : 0);  // set_round, [units], screen, decode, edit_rows, loop_check, flags, counters
     CK(cudaGetLastError());
     if (c->tr.allreduce_sum_i64(c->tr.user, (int64_t*)dcnt, nout, (dmtz_stream_t)s)) return comm_fail("allreduce");
     CK(cudaMemcpyAsync(hcnt, dcnt, (size_t)nout * 8, cudaMemcpyDeviceToHost, s));

@@ -149,25 +149,34 @@ __global__ void k_dist_stop(const long long* __restrict__ tot, long long* __rest
 // face flags per rank at 12 + 2 rank (+1): "an owned vertex of the 3 planes next to the
 // lower (upper) face changed this round" -- from the round's change bitmap, whose rows
 // of those planes are cleared before the round (k_face_clear)
+// the face flags of the round: any changed vertex in the rows of planes [lo0, lo1) /
+// [hi0, hi1) of the change bitmap, OR-ed into flags[0] / flags[1] (zeroed by the
+// counters kernel after it reads them); a grid of blocks, one atomic per warp that saw one
+__global__ void k_face_flags(const uint32_t* __restrict__ vround, int64_t per_plane, int64_t lo0, int64_t lo1,
+                             int64_t hi0, int64_t hi1, unsigned* __restrict__ flags, const long long* ctl) {
+  if (ctl && ctl[DCTL_HALT]) return;
+  const int lane = threadIdx.x & 31;
+  for (int f = 0; f < 2; f++) {
+    const int64_t a = (f ? hi0 : lo0) * per_plane, b = (f ? hi1 : lo1) * per_plane;
+    for (int64_t base = a + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) - lane; base < b;
+         base += (int64_t)gridDim.x * blockDim.x) {
+      const unsigned w = base + lane < b ? vround[base + lane] : 0u;
+      if (__any_sync(0xffffffffu, w != 0u) && lane == 0) atomicOr(flags + f, 1u);
+    }
+  }
+}
+
 // (ctl: the device stop flag of the batched mode -- once set, this writes zeros)
 __global__ void k_dist_counters(const Counters* __restrict__ cnt, long long round, long long* __restrict__ out,
-                                int nout, const uint32_t* __restrict__ vround, Grid g, RowGeom rg, int64_t lo0,
-                                int64_t lo1, int64_t hi0, int64_t hi1, int rank, const long long* ctl) {
+                                int nout, unsigned* __restrict__ flags, int rank, const long long* ctl) {
   if (ctl && ctl[DCTL_HALT]) {
     for (int i = threadIdx.x; i < nout; i += blockDim.x) out[i] = 0;
     return;
   }
   __shared__ unsigned s_flag[2];
-  if (threadIdx.x < 2) s_flag[threadIdx.x] = 0u;
+  if (threadIdx.x < 2) s_flag[threadIdx.x] = flags[threadIdx.x];
   __syncthreads();
-  const int64_t per_plane = g.ny * rg.wpr;
-  for (int f = 0; f < 2; f++) {
-    const int64_t a = (f ? hi0 : lo0) * per_plane, b = (f ? hi1 : lo1) * per_plane;
-    unsigned any = 0u;
-    for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) any |= vround[i];
-    if (__syncthreads_or(any != 0u) && threadIdx.x == 0) s_flag[f] = 1u;
-  }
-  __syncthreads();
+  if (threadIdx.x < 2) flags[threadIdx.x] = 0u;
   for (int i = threadIdx.x; i < nout; i += blockDim.x) {
     long long v = 0;
     if (i == 0) v = (long long)cnt->n_false;
