@@ -16,7 +16,10 @@ time_to_fixed_point  the step time, the second half of BASELINE's metric
 trace   rows a9-a11 (descending / ascending / connector V-paths) of the
         converged field, timed once after the steps
 e2e     the same metric through the public API from pinned HOST arrays: H2D of
-        f and fhat, the C-loop, D2H of g and the edit list, every step
+        f and fhat, the C-loop, the edit list encoded on the device and D2H of the
+        encoded stream (the storable artifact), every step
+        (dmtz_correct_host_stream); e2e_raw: D2H of g and the raw 16-byte edit
+        records instead (dmtz_correct_host)
 roofline the dominant kernel, k_screen (gradient codes of g), on the rounds it
         sweeps every anchor, timed with CUDA events on the launching stream
         inside the library during one extra (host-driven) step; algorithmic work per anchor: 105 SoS compare-selects
@@ -568,10 +571,34 @@ def main():
                                                 edits_host=eh), 2)
         ems = float(np.median(et))
         r3, et3 = timed(lambda: ctx.correct_host(fp, fhp, xi, bufs=hb, g_host=gh, edits_host=eh), 2)
-        e2e = {"value": N * r2.stats["sweeps"] / (ems * 1e-3) / 1e6, "unit": "Mvoxels/s",
-               "h2d_bytes_per_step": 2 * 4 * N, "d2h_bytes_per_step": 4 * N + 16 * r2.n_edits, "ms_per_step": ems,
-               "api": "dmtz_correct_host (full sweeps): pinned host f, fhat in; g + edit list to pinned host",
-               "time_to_fixed_point_ms": float(np.median(et3))}
+        e2e_raw = {"value": N * r2.stats["sweeps"] / (ems * 1e-3) / 1e6, "unit": "Mvoxels/s",
+                   "h2d_bytes_per_step": 2 * 4 * N, "d2h_bytes_per_step": 4 * N + 16 * r2.n_edits,
+                   "ms_per_step": ems,
+                   "api": "dmtz_correct_host (full sweeps): pinned host f, fhat in; g + edit list to pinned host",
+                   "time_to_fixed_point_ms": float(np.median(et3))}
+        # the artifact end to end: host f / fhat in, the encoded edit stream out
+        hbs = dict(hb, stream=torch.empty(max(int(dmtz._lib.dmtz_edit_stream_bound(N)), 1), dtype=torch.uint8,
+                                          device=dev))
+        sh = torch.empty(hbs["stream"].numel(), dtype=torch.uint8).pin_memory()
+        (r4, sb), et4 = timed(lambda: ctx.correct_host_stream(fp, fhp, xi, full_sweeps=True, bufs=hbs,
+                                                              stream_host=sh), 2)
+        (r5, sb5), et5 = timed(lambda: ctx.correct_host_stream(fp, fhp, xi, bufs=hbs, stream_host=sh), 2)
+        # the artifact decodes back to the same g
+        try:   # the host bytes, back on the device, decode and apply to the converged g
+            sd = sb.to(dev)
+            de, dxi, dqm = ctx.decode_edits(sd, fhat=fht)
+            ga = ctx.apply_edits(fht, dxi, de, dqm)
+            dec_ok = bool(torch.equal(ga.view(torch.int32), hbs["g"].view(torch.int32)))
+            del sd, de, ga
+        except Exception as ex:   # noqa: BLE001
+            dec_ok = f"not checked: {str(ex)[:80]}"
+        e4 = float(np.median(et4))
+        e2e = {"value": N * r4.stats["sweeps"] / (e4 * 1e-3) / 1e6, "unit": "Mvoxels/s",
+               "h2d_bytes_per_step": 2 * 4 * N, "d2h_bytes_per_step": int(sb.numel()), "ms_per_step": e4,
+               "api": "dmtz_correct_host_stream (full sweeps): pinned host f, fhat in; the edit list encoded on "
+                      "the device (version 2), the stream to pinned host",
+               "stream_decodes_to_g": dec_ok,
+               "time_to_fixed_point_ms": float(np.median(et5))}
 
     cpu = None
     if not args.no_cpu_baseline:
@@ -638,6 +665,7 @@ def main():
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "e2e_raw": e2e_raw if not args.no_e2e else None,
         "gpu_launches": rfull.stats["launches"],
         "clocks": clk.summary(),
         "parity_vs_oracle": parity,

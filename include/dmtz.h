@@ -353,6 +353,20 @@ dmtz_status dmtz_preserve(dmtz_ctx* ctx, const float* f, const float* fhat, cons
  *   exact and, since fhat - 2 xi <= value <= fhat, d is a few thousand ulps at most];
  *   delta = v for a block's first edit, else v - v_prev - 1; varint = unsigned LEB128.
  * ------------------------------------------------------------------------ */
+/* dmtz_correct_host that returns the storable artifact instead of the raw edit list:
+ * pinned host f and fhat in (as dmtz_correct_host), the C-loop, the edit list encoded
+ * on the device (version 2 below) into stream_dev (capacity stream_cap, e.g.
+ * dmtz_edit_stream_bound(N)), and only the stream's *stream_bytes bytes copied to
+ * stream_host (capacity stream_host_cap) -- plus g to g_host when it is not NULL (g
+ * is also f_hat with the stream applied: dmtz_apply_edits).  edits_dev (capacity
+ * edits_capacity) holds the raw list on return.  Synchronises the stream.  Status as
+ * dmtz_correct; DMTZ_E_CAPACITY if a buffer is too small. */
+dmtz_status dmtz_correct_host_stream(dmtz_ctx* ctx, const float* f_host, const float* fhat_host,
+                                     const dmtz_correct_opts* opts, void* workspace, size_t workspace_bytes,
+                                     float* f_dev, float* fhat_dev, float* g_dev, dmtz_edit* edits_dev,
+                                     int64_t edits_capacity, uint8_t* stream_dev, size_t stream_cap, float* g_host,
+                                     uint8_t* stream_host, size_t stream_host_cap, size_t* stream_bytes /* host */,
+                                     int64_t* n_edits /* host */, dmtz_stats* stats /* host */, dmtz_stream_t stream);
 /* Upper bound of the stream size for n_edits edits. */
 size_t dmtz_edit_stream_bound(int64_t n_edits);
 /* Encode a sorted edit list (device, as dmtz_correct writes it) into `out` (device,

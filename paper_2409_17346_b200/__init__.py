@@ -95,6 +95,10 @@ def _load():
                                ctypes.POINTER(i64), ctypes.POINTER(_Stats), P]
     L.dmtz_correct_host.argtypes = [P, P, P, ctypes.POINTER(_Opts), P, ctypes.c_size_t, P, P, P, P, i64, P, P,
                                     ctypes.POINTER(i64), ctypes.POINTER(_Stats), P]
+    L.dmtz_correct_host_stream.argtypes = [P, P, P, ctypes.POINTER(_Opts), P, ctypes.c_size_t, P, P, P, P, i64, P,
+                                           ctypes.c_size_t, P, P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t),
+                                           ctypes.POINTER(i64), ctypes.POINTER(_Stats), P]
+    L.dmtz_correct_host_stream.restype = ctypes.c_int
     L.dmtz_trace_separatrices.argtypes = [P, P, ctypes.c_uint32, P, ctypes.c_size_t, ctypes.POINTER(_Seps),
                                           i64, i64, ctypes.POINTER(i64), ctypes.POINTER(i64), P]
     SZ = ctypes.c_size_t
@@ -161,7 +165,7 @@ EXPORTED = ("dmtz_ctx_create", "dmtz_ctx_destroy", "dmtz_workspace_bytes", "dmtz
             "dmtz_preserve",
             "dmtz_edit_stream_bound", "dmtz_encode_edits", "dmtz_decode_edits", "dmtz_apply_edits",
             "dmtz_critical_prf", "dmtz_separatrix_prf", "dmtz_last_trace_levels", "dmtz_local_slab",
-            "dmtz_ctx_set_transport", "dmtz_ctx_set_dist_sync", "dmtz_nccl_unique_id")
+            "dmtz_ctx_set_transport", "dmtz_ctx_set_dist_sync", "dmtz_nccl_unique_id", "dmtz_correct_host_stream")
 
 
 def pack_edit_stream(stream: torch.Tensor, level: int = 1) -> bytes:
@@ -353,8 +357,51 @@ class Context:
         return Result(status=status, g=g_host, edits=edits_host[:min(ne.value, cap)], n_edits=ne.value,
                       stats=stats, message=msg)
 
-    def host_buffers(self, device) -> dict:
-        """Device buffers of correct_host: f, fhat, g (float[N]) and the edit list."""
+    def correct_host_stream(self, f_host: torch.Tensor, fhat_host: torch.Tensor, xi: float, q_max: int = 6,
+                            q_cap: int | None = None, tier: int = 2, max_rounds: int = 0, full_sweeps: bool = False,
+                            bufs: dict | None = None, stream_host: torch.Tensor | None = None,
+                            g_host: torch.Tensor | None = None, stream=None, raise_on_error: bool = True):
+        """The end-to-end call that returns the storable artifact
+        (dmtz_correct_host_stream): f and fhat from HOST tensors, the C-loop, the edit
+        list encoded on the device (version 2), and only the stream's bytes back to the
+        host (plus g into g_host when given).  ``bufs`` from host_buffers(device,
+        stream=True).  Returns (Result with g = g_host or None and edits = the device
+        edit list, the host stream bytes as a uint8 tensor view)."""
+        for t in (f_host, fhat_host):
+            assert t.device.type == "cpu" and t.dtype == torch.float32 and tuple(t.shape) == self.shape
+            assert t.is_contiguous()
+        dev = self.workspace.device
+        if bufs is None or "stream" not in bufs:
+            bufs = self.host_buffers(dev, stream=True)
+        if stream_host is None:
+            stream_host = torch.empty(bufs["stream"].numel(), dtype=torch.uint8).pin_memory()
+        cap = bufs["edits"].shape[0]
+        opts = _Opts(float(xi), int(q_max), int(q_max if q_cap is None else q_cap), int(tier), int(max_rounds),
+                     1 if full_sweeps else 0, 0)
+        ne, nbytes, st = ctypes.c_int64(), ctypes.c_size_t(), _Stats()
+        status = _lib.dmtz_correct_host_stream(
+            self._h, ctypes.c_void_p(f_host.data_ptr()), ctypes.c_void_p(fhat_host.data_ptr()), ctypes.byref(opts),
+            ctypes.c_void_p(self.workspace.data_ptr()), self.ws_bytes, ctypes.c_void_p(bufs["f"].data_ptr()),
+            ctypes.c_void_p(bufs["fhat"].data_ptr()), ctypes.c_void_p(bufs["g"].data_ptr()),
+            ctypes.c_void_p(bufs["edits"].data_ptr()), cap, ctypes.c_void_p(bufs["stream"].data_ptr()),
+            bufs["stream"].numel(), ctypes.c_void_p(g_host.data_ptr()) if g_host is not None else None,
+            ctypes.c_void_p(stream_host.data_ptr()), stream_host.numel(), ctypes.byref(nbytes), ctypes.byref(ne),
+            ctypes.byref(st), _stream_ptr(stream))
+        stats = _stats_dict(st, status)
+        msg = _lib.dmtz_last_error().decode() if status != OK else ""
+        if raise_on_error and status not in (OK, E_STUCK, E_ITER_CAP):
+            raise DmtzError(status, msg)
+        return (Result(status=status, g=g_host, edits=bufs["edits"][:min(ne.value, cap)], n_edits=ne.value,
+                       stats=stats, message=msg), stream_host[:nbytes.value])
+
+    def host_buffers(self, device, stream: bool = False) -> dict:
+        """Device buffers of correct_host: f, fhat, g (float[N]) and the edit list (and,
+        with stream=True, the edit-stream buffer of correct_host_stream)."""
+        if stream:
+            d = self.host_buffers(device)
+            d["stream"] = torch.empty(max(int(_lib.dmtz_edit_stream_bound(self.N)), 1), dtype=torch.uint8,
+                                      device=device)
+            return d
         return dict(f=torch.empty(self.shape, dtype=torch.float32, device=device),
                     fhat=torch.empty(self.shape, dtype=torch.float32, device=device),
                     g=torch.empty(self.shape, dtype=torch.float32, device=device),

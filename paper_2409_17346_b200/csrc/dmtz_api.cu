@@ -1353,6 +1353,36 @@ dmtz_status dmtz_correct_host(dmtz_ctx* c, const float* f_host, const float* fha
   return r;
 }
 
+dmtz_status dmtz_correct_host_stream(dmtz_ctx* c, const float* f_host, const float* fhat_host,
+                                     const dmtz_correct_opts* o, void* workspace, size_t workspace_bytes,
+                                     float* f_dev, float* fhat_dev, float* g_dev, dmtz_edit* edits_dev,
+                                     int64_t edits_capacity, uint8_t* stream_dev, size_t stream_cap, float* g_host,
+                                     uint8_t* stream_host, size_t stream_host_cap, size_t* stream_bytes,
+                                     int64_t* n_edits, dmtz_stats* st, dmtz_stream_t stream) {
+  DeviceGuard dg_(c);
+  if (!c || !o || !stream_dev || !stream_host || !stream_bytes || !n_edits || !edits_dev || edits_capacity < 1) {
+    set_err("NULL argument");
+    return DMTZ_E_ARG;
+  }
+  *stream_bytes = 0;
+  const dmtz_status r = dmtz_correct_host(c, f_host, fhat_host, o, workspace, workspace_bytes, f_dev, fhat_dev, g_dev,
+                                          edits_dev, edits_capacity, g_host, nullptr, n_edits, st, stream);
+  if (r != DMTZ_OK && r != DMTZ_E_STUCK && r != DMTZ_E_ITER_CAP) return r;   // (capacity: the list is incomplete)
+  // the artifact: the edit list encoded on the device (version 2, lossless values
+  // relative to fhat), and only its bytes cross to the host
+  const dmtz_status e = dmtz_encode_edits(c, edits_dev, *n_edits, o->xi, o->q_max, fhat_dev, workspace,
+                                          workspace_bytes, stream_dev, stream_cap, stream_bytes, stream);
+  if (e != DMTZ_OK) return e;
+  if (*stream_bytes > stream_host_cap) {
+    set_err("edit stream needs %zu host bytes", *stream_bytes);
+    return DMTZ_E_CAPACITY;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(stream_host, stream_dev, *stream_bytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return r;
+}
+
 static dmtz_status slab_check(dmtz_ctx* c, const dmtz_slab* sl, void* ws, size_t wsb, Layout* L) {
   if (!c || !sl || !ws) { set_err("NULL argument"); return DMTZ_E_ARG; }
   if (c->D != 3) { set_err("slab mode needs a 3D grid"); return DMTZ_E_DIMS; }

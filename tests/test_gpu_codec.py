@@ -141,3 +141,22 @@ def test_v2_warp_decoder_multi_block_and_fuzz(dmtz):
             assert np.array_equal(a["value"][ll].view(np.uint32), b["value"][ll].view(np.uint32)), trial
         verdicts.add(res[0] is None)
     assert True in verdicts
+
+
+@pytest.mark.parametrize("name,shape,full", [("C4", (40, 44, 48), False), ("C3", (20, 50, 50), True),
+                                             ("C2", (180, 360), False)])
+def test_correct_host_stream_is_the_oracle_stream(dmtz, name, shape, full):
+    """dmtz_correct_host_stream (host f / fhat in, the encoded edit stream out): its bytes
+    equal the oracle codec's version-2 stream of the oracle-equal edit list, and they
+    decode and apply back to correct()'s g."""
+    f, fh, xi, _ = di.config_inputs(name, shape=shape)
+    ft, fht = _cuda(f), _cuda(fh)
+    ctx = dmtz.Context(ft.shape, ft.device)
+    r = ctx.correct(ft, fht, xi, full_sweeps=full)
+    rh, sb = ctx.correct_host_stream(torch.from_numpy(f).pin_memory(), torch.from_numpy(fh).pin_memory(), xi,
+                                     full_sweeps=full)
+    assert rh.status == r.status == 0 and rh.n_edits == r.n_edits
+    assert sb.numpy().tobytes() == ec.encode(r.edits_numpy(), xi, 6, fhat=fh)
+    d, x2, qm = ctx.decode_edits(sb.cuda(), fhat=fht)
+    g = ctx.apply_edits(fht, x2, d, q_max=qm)
+    assert torch.equal(g.view(torch.int32), r.g.view(torch.int32))
