@@ -304,9 +304,23 @@ def test_full_size_cloop_C5_one_gpu(dmtz):
     rec[v[~ll]] = fht.reshape(-1)[v[~ll]] - (q[~ll].to(torch.float32) * step)
     rec[v[ll]] = val[ll]
     assert torch.equal(rec.view(torch.int32), g.reshape(-1).view(torch.int32))
-    cf = dmtz.critical_mask(dmtz.compute_gradient(ft))
-    cg = dmtz.critical_mask(dmtz.compute_gradient(g))
+    codes_f, codes_g = dmtz.compute_gradient(ft), dmtz.compute_gradient(g)
+    cf, cg = dmtz.critical_mask(codes_f), dmtz.critical_mask(codes_g)
     assert torch.equal(cf, cg)
+    # sampled outputs the oracle computes one by one: on random 20^3 crops, the GPU's
+    # full-grid codes (anchors whose stencil lies in the crop) and critical masks (anchors
+    # whose 8 codes do) equal the oracle's literal gradient of the crop, for f and g
+    rng = np.random.default_rng(5)
+    for _ in range(6):
+        lo = [int(rng.integers(0, s - 20 + 1)) for s in cfg.shape]
+        sl = tuple(slice(l, l + 20) for l in lo)
+        for fld, codes, crit in ((ft, codes_f, cf), (g, codes_g, cg)):
+            oc, om = oracle.gradient(np.ascontiguousarray(fld[sl].cpu().numpy()))
+            ic, im = tuple(slice(1, 19) for _ in range(3)), tuple(slice(1, 18) for _ in range(3))
+            shp = tuple(cfg.shape)
+            assert np.array_equal(_codes_np(codes.reshape(shp)[sl].contiguous())[ic], oc.reshape(20, 20, 20)[ic])
+            assert np.array_equal(crit.reshape(shp)[sl].cpu().numpy().view(np.uint32)[im],
+                                  om.reshape(20, 20, 20)[im])
 
 
 @pytest.mark.parametrize("cap", ["0", "2048", "5000"])
