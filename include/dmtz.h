@@ -183,6 +183,14 @@ dmtz_status dmtz_ctx_set_transport(dmtz_ctx* ctx, const dmtz_transport* transpor
  *     did not change is not applied (halo_faces_skipped stays 0).
  * Results are identical in both modes.  DMTZ_E_ARG outside [1, 1024]. */
 dmtz_status dmtz_ctx_set_dist_sync(dmtz_ctx* ctx, int rounds_per_sync);
+/* Batched mode over the context's own NCCL communicator with an even rounds_per_sync:
+ * on != 0 captures one batch (rounds 2 .. k + 1: exchanges, rounds, counter all-reduce,
+ * device stop rule) into a CUDA graph once per dmtz_correct and replays it, one graph
+ * launch per k rounds (round 1 runs eagerly; the batch's round-dependent parts repeat
+ * with period 2).  If the capture is refused the batches run eagerly.  on < 0 leaves the
+ * setting; *used_last (may be NULL) = whether the last dmtz_correct replayed the graph.
+ * Default off. */
+dmtz_status dmtz_ctx_set_dist_graph(dmtz_ctx* ctx, int on, int* used_last);
 /* An NCCL unique id (128 bytes into `out`) for dmtz_ctx_create; DMTZ_E_NCCL if
  * libnccl.so.2 cannot be loaded. */
 dmtz_status dmtz_nccl_unique_id(void* out);

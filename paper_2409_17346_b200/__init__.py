@@ -134,6 +134,8 @@ def _load():
     L.dmtz_ctx_set_transport.restype = ctypes.c_int
     L.dmtz_ctx_set_dist_sync.argtypes = [P, ctypes.c_int]
     L.dmtz_ctx_set_dist_sync.restype = ctypes.c_int
+    L.dmtz_ctx_set_dist_graph.argtypes = [P, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+    L.dmtz_ctx_set_dist_graph.restype = ctypes.c_int
     L.dmtz_nccl_unique_id.argtypes = [P]
     L.dmtz_nccl_unique_id.restype = ctypes.c_int
     for fn in ("dmtz_ctx_create", "dmtz_compute_gradient", "dmtz_critical_mask", "dmtz_correct", "dmtz_correct_host",
@@ -165,7 +167,8 @@ EXPORTED = ("dmtz_ctx_create", "dmtz_ctx_destroy", "dmtz_workspace_bytes", "dmtz
             "dmtz_preserve",
             "dmtz_edit_stream_bound", "dmtz_encode_edits", "dmtz_decode_edits", "dmtz_apply_edits",
             "dmtz_critical_prf", "dmtz_separatrix_prf", "dmtz_last_trace_levels", "dmtz_local_slab",
-            "dmtz_ctx_set_transport", "dmtz_ctx_set_dist_sync", "dmtz_nccl_unique_id", "dmtz_correct_host_stream")
+            "dmtz_ctx_set_transport", "dmtz_ctx_set_dist_sync", "dmtz_nccl_unique_id", "dmtz_correct_host_stream",
+            "dmtz_ctx_set_dist_graph")
 
 
 def pack_edit_stream(stream: torch.Tensor, level: int = 1) -> bytes:

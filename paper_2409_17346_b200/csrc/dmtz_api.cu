@@ -69,9 +69,11 @@ struct dmtz_ctx {
   dmtz_transport tr = {nullptr, nullptr, nullptr};
   int has_tr = 0;
   void* nccl_comm = nullptr;
-  int dist_sync = 8;
-  int t3_log = 0;
-  int t3_unordered = 1;  // tier-3 candidate traces fill connectors in any order (DMTZ_T3_ORDERED=1: FIFO)     // DMTZ_T3_LOG=1: per S-round candidate counts and trace time of tier 3 on stderr  // rounds per host check of the device stop flag (1: host-synchronous rounds)
+  int dist_sync = 8;         // rounds per host check of the device stop flag (1: host-synchronous rounds)
+  int dist_graph = 0;        // dmtz_ctx_set_dist_graph: batches as a captured CUDA graph (NCCL transport)
+  int dist_graph_used = 0;   // the last dmtz_correct ran its batches from the graph
+  int t3_log = 0;            // DMTZ_T3_LOG=1: per S-round candidate counts and phase times of tier 3 on stderr
+  int t3_unordered = 1;      // tier-3 candidate traces fill connectors in any order (DMTZ_T3_ORDERED=1: FIFO)
 };
 
 #include "dmtz_dist.cuh"  // needs the context above
@@ -998,41 +1000,98 @@ static dmtz_status correct_dist(dmtz_ctx* c, const float* f, const float* fhat, 
     long long* hctl = hcnt + 64 - DCTL_N;  // the pinned block's tail (nout <= 48 here)
     if (nout > 64 - DCTL_N) { set_err("world %d too large for the batched mode", c->world); return DMTZ_E_ARG; }
     CK(cudaMemsetAsync(ctl, 0, DCTL_N * 8, s));
+    c->dist_graph_used = 0;
+    // one round rr on stream ss: exchange, halo update, round, face flags, counters,
+    // all-reduce, stop rule -- device work and transport calls only (capturable)
+    int64_t launches_per_round = 0;
+    auto one_round = [&](int64_t rr, cudaStream_t ss) -> dmtz_status {
+      int64_t la = 0;
+      if (rr > 1) {
+        HaloPlan h = halo_plan(c, g, gloc, stage, 1, 1, 1, 1);
+        if (run_exchange(c, h, ss)) return comm_fail("exchange");
+        for (int i = 0; i < h.n; i++)
+          if (h.rz1[i] > h.rz0[i]) {
+            const int64_t items = (h.rz1[i] - h.rz0[i]) * g.ny * rg.wpr;
+            k_halo<<<clamp_blocks(items * 32, 256), 256, 0, ss>>>(
+                gloc, stage + h.rz0[i] * sz, h.rz0[i], h.rz1[i], g, rg, W.vchg + (int64_t)((rr - 1) & 1) * W.vwords,
+                W.fbits, ctl, h.rz0[i] == 0 ? DCTL_GATE_LO : DCTL_GATE_HI);
+            la++;
+          }
+      }
+      uint32_t* vround = W.vchg + (int64_t)(rr & 1) * W.vwords;
+      if (c->world > 1) {   // face flags (a one-rank world has no faces)
+        CK(cudaMemsetAsync(vround + oz0 * per_plane, 0, (size_t)(nface * per_plane) * 4, ss));
+        CK(cudaMemsetAsync(vround + (oz1 - nface) * per_plane, 0, (size_t)(nface * per_plane) * 4, ss));
+      }
+      const dmtz_status rs = slab_round_enqueue(c, floc, fhloc, o, &sl, ws, L, gloc, rr, o->full_sweeps != 0, ss, ctl);
+      if (rs) return rs;
+      if (c->world > 1)
+        k_face_flags<<<clamp_blocks(2 * nface * per_plane, 256, 148 * 2), 256, 0, ss>>>(
+            vround, per_plane, oz0, oz0 + nface, oz1 - nface, oz1, fflags, ctl);
+      k_dist_counters<<<1, 256, 0, ss>>>(W.dc, rr, dcnt, nout, fflags, c->rank, ctl);
+      CK(cudaGetLastError());
+      if (c->tr.allreduce_sum_i64(c->tr.user, (int64_t*)dcnt, nout, (dmtz_stream_t)ss)) return comm_fail("allreduce");
+      k_dist_stop<<<1, 32, 0, ss>>>(dcnt, ctl, max_rounds, c->rank, c->world);
+      la += 8 + (rr > 1 ? 1 : 0);  // begin, [units], screen, decode, edit_rows, loop_check, flags, counters, stop
+      launches_per_round = la;
+      st->launches += la;
+      return DMTZ_OK;
+    };
+    // CUDA graph of a batch (dmtz_ctx_set_dist_graph; NCCL transport; even batch): round 1
+    // runs eagerly, then one captured batch of rounds 2 .. k + 1 is replayed -- its
+    // round-dependent parts (change-bitmap parity, round > 1) repeat with period 2, and
+    // the device counts the rounds
+    cudaGraph_t dgraph = nullptr;
+    cudaGraphExec_t dexec = nullptr;
+    const bool try_graph = c->dist_graph && c->nccl_comm && c->cap_stream && c->ev_aux[0] && c->dist_sync % 2 == 0;
+    bool graphed = false;
     for (;;) {
-      for (int b = 0; b < c->dist_sync; b++) {
-        r++;
-        if (r > 1) {
-          HaloPlan h = halo_plan(c, g, gloc, stage, 1, 1, 1, 1);
-          if (run_exchange(c, h, s)) return comm_fail("exchange");
-          for (int i = 0; i < h.n; i++)
-            if (h.rz1[i] > h.rz0[i]) {
-              const int64_t items = (h.rz1[i] - h.rz0[i]) * g.ny * rg.wpr;
-              k_halo<<<clamp_blocks(items * 32, 256), 256, 0, s>>>(
-                  gloc, stage + h.rz0[i] * sz, h.rz0[i], h.rz1[i], g, rg, W.vchg + (int64_t)((r - 1) & 1) * W.vwords,
-                  W.fbits, ctl, h.rz0[i] == 0 ? DCTL_GATE_LO : DCTL_GATE_HI);
-              st->launches++;
-            }
+      if (graphed) {
+        CK(cudaGraphLaunch(dexec, s));
+        r += c->dist_sync;
+        st->launches += launches_per_round * c->dist_sync;
+      } else if (try_graph && r == 1) {
+        // capture rounds 2 .. k + 1 on the private stream, after the work already on s
+        CK(cudaEventRecord(c->ev_aux[0], s));
+        CK(cudaStreamWaitEvent(c->cap_stream, c->ev_aux[0], 0));
+        bool ok = cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        const int64_t l0 = st->launches;
+        for (int b = 0; ok && b < c->dist_sync; b++) ok = one_round(r + 1 + b, c->cap_stream) == DMTZ_OK;
+        const cudaError_t ec = cudaStreamEndCapture(c->cap_stream, &dgraph);
+        st->launches = l0;
+        ok = ok && ec == cudaSuccess && dgraph && cudaGraphInstantiate(&dexec, dgraph, 0) == cudaSuccess;
+        cudaGetLastError();
+        if (!ok) {   // capture refused (transport or driver): eager batches from here on
+          if (dexec) cudaGraphExecDestroy(dexec);
+          if (dgraph) cudaGraphDestroy(dgraph);
+          dexec = nullptr;
+          dgraph = nullptr;
+          set_err("");
+          for (int b = 0; b < c->dist_sync; b++) {
+            r++;
+            const dmtz_status rs = one_round(r, s);
+            if (rs) return rs;
+          }
+        } else {
+          graphed = true;
+          c->dist_graph_used = 1;
+          continue;
         }
-        uint32_t* vround = W.vchg + (int64_t)(r & 1) * W.vwords;
-        if (c->world > 1) {   // face flags (a one-rank world has no faces)
-          CK(cudaMemsetAsync(vround + oz0 * per_plane, 0, (size_t)(nface * per_plane) * 4, s));
-          CK(cudaMemsetAsync(vround + (oz1 - nface) * per_plane, 0, (size_t)(nface * per_plane) * 4, s));
+      } else {
+        for (int b = 0; b < c->dist_sync; b++) {
+          r++;
+          const dmtz_status rs = one_round(r, s);
+          if (rs) return rs;
+          if (try_graph && r == 1) break;   // round 1 alone, then the captured batches
         }
-        const dmtz_status rs = slab_round_enqueue(c, floc, fhloc, o, &sl, ws, L, gloc, r, o->full_sweeps != 0, s, ctl);
-        if (rs) return rs;
-        if (c->world > 1)
-          k_face_flags<<<clamp_blocks(2 * nface * per_plane, 256, 148 * 2), 256, 0, s>>>(
-              vround, per_plane, oz0, oz0 + nface, oz1 - nface, oz1, fflags, ctl);
-        k_dist_counters<<<1, 256, 0, s>>>(W.dc, r, dcnt, nout, fflags, c->rank, ctl);
-        CK(cudaGetLastError());
-        if (c->tr.allreduce_sum_i64(c->tr.user, (int64_t*)dcnt, nout, (dmtz_stream_t)s)) return comm_fail("allreduce");
-        k_dist_stop<<<1, 32, 0, s>>>(dcnt, ctl, max_rounds, c->rank, c->world);
-        st->launches += 8 + (r > 1 ? 1 : 0);  // begin, [units], screen, decode, edit_rows, loop_check, flags, counters, stop
       }
       CK(cudaMemcpyAsync(hctl, ctl, DCTL_N * 8, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       if (hctl[DCTL_HALT]) break;
     }
+    if (dexec) cudaGraphExecDestroy(dexec);
+    if (dgraph) cudaGraphDestroy(dgraph);
+
     status = (int)hctl[DCTL_STATUS];
     st->rounds = hctl[DCTL_ROUNDS];
     st->sweeps = hctl[DCTL_SWEEPS];
@@ -1819,6 +1878,13 @@ dmtz_status dmtz_ctx_set_transport(dmtz_ctx* c, const dmtz_transport* t) {
   if (!t->exchange || !t->allreduce_sum_i64) { set_err("transport without callbacks"); return DMTZ_E_ARG; }
   c->tr = *t;
   c->has_tr = 1;
+  return DMTZ_OK;
+}
+
+dmtz_status dmtz_ctx_set_dist_graph(dmtz_ctx* c, int on, int* used_last) {
+  if (!c) { set_err("NULL argument"); return DMTZ_E_ARG; }
+  if (used_last) *used_last = c->dist_graph_used;
+  if (on >= 0) c->dist_graph = on ? 1 : 0;
   return DMTZ_OK;
 }
 

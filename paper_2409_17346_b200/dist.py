@@ -88,7 +88,7 @@ class DistContext:
     grid (numpy shape (nz, ny, nx)); correct() takes and returns the OWNED planes."""
 
     def __init__(self, global_shape, rank: int, world: int, device=None, nccl_id: bytes | None = None,
-                 rounds_per_sync: int = 8):
+                 rounds_per_sync: int = 8, graph: bool = False):
         self.global_shape = tuple(int(x) for x in global_shape)
         nz, ny, nx = self.global_shape
         self.rank, self.world = int(rank), int(world)
@@ -102,6 +102,7 @@ class DistContext:
                                     self.device.index or 0))
         self._h = h
         _check(_lib.dmtz_ctx_set_dist_sync(h, int(rounds_per_sync)))
+        _check(_lib.dmtz_ctx_set_dist_graph(h, 1 if graph else 0, None))
         self.ws_bytes = int(_lib.dmtz_workspace_bytes(h, None))
         self.workspace = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
         self._cb = None
@@ -149,6 +150,12 @@ class DistContext:
             raise DmtzError(status, msg)
         return Result(status=status, g=g, edits=edits[:min(ne.value, cap)], n_edits=ne.value, stats=stats,
                       message=msg)
+
+    def graph_used(self) -> bool:
+        """Whether the last correct() replayed its batches from a CUDA graph."""
+        u = ctypes.c_int()
+        _check(_lib.dmtz_ctx_set_dist_graph(self._h, -1, ctypes.byref(u)))
+        return bool(u.value)
 
     def close(self):
         if getattr(self, "_h", None):

@@ -102,14 +102,16 @@ def test_dist_one_rank_nccl():
     case = {"kind": "config", "name": "C4", "shape": [32, 32, 32]}
     ref = _single(case)
     f, fh, xi = make_case(case)
-    nid = nccl_unique_id()
-    for sync in (1, 8):
-        ctx = DistContext(f.shape, 0, 1, device="cuda:0", nccl_id=nid if sync == 1 else nccl_unique_id(),
-                          rounds_per_sync=sync)
-        r = ctx.correct(torch.from_numpy(f).cuda(), torch.from_numpy(fh).cuda(), xi)
-        assert r.status == ref.status == 0
-        assert torch.equal(r.g.view(torch.int32), ref.g.view(torch.int32))
-        assert torch.equal(r.edits, ref.edits)
-        for k in STAT_KEYS:
-            assert r.stats[k] == ref.stats[k], k
+    for sync, graph in ((1, False), (8, False), (8, True), (4, True)):
+        ctx = DistContext(f.shape, 0, 1, device="cuda:0", nccl_id=nccl_unique_id(), rounds_per_sync=sync,
+                          graph=graph)
+        for full in (False, True):
+            r = ctx.correct(torch.from_numpy(f).cuda(), torch.from_numpy(fh).cuda(), xi, full_sweeps=full)
+            assert r.status == ref.status == 0
+            assert torch.equal(r.g.view(torch.int32), ref.g.view(torch.int32))
+            assert torch.equal(r.edits, ref.edits)
+            for k in STAT_KEYS:
+                assert r.stats[k] == ref.stats[k], k
+            # graph: round 1 eagerly, then the captured batch replayed (NCCL all-reduce inside)
+            assert ctx.graph_used() == graph
         ctx.close()

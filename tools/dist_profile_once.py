@@ -14,10 +14,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("config", nargs="?", default="C4")
 ap.add_argument("--full", action="store_true")
 ap.add_argument("--sync", type=int, default=8)
+ap.add_argument("--graph", action="store_true")
 a = ap.parse_args()
 f, fh, xi, cfg = di.config_inputs(a.config)
 dev = torch.device("cuda", 0)
-ctx = DistContext(f.shape, 0, 1, device=dev, nccl_id=nccl_unique_id(), rounds_per_sync=a.sync)
+ctx = DistContext(f.shape, 0, 1, device=dev, nccl_id=nccl_unique_id(), rounds_per_sync=a.sync,
+                  graph=a.graph)
 ft, fht = torch.from_numpy(f).to(dev), torch.from_numpy(fh).to(dev)
 for _ in range(int(os.environ.get("REPS", "2"))):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -25,5 +27,5 @@ for _ in range(int(os.environ.get("REPS", "2"))):
     r = ctx.correct(ft, fht, xi, q_max=cfg.q_max, full_sweeps=a.full)
     e1.record()
     torch.cuda.synchronize()
-    print(f"{a.config} dist full={a.full} sync={a.sync}: {e0.elapsed_time(e1):.1f} ms, rounds {r.stats['rounds']}",
-          flush=True)
+    print(f"{a.config} dist full={a.full} sync={a.sync} graph={a.graph} (used {ctx.graph_used()}): "
+          f"{e0.elapsed_time(e1):.1f} ms, rounds {r.stats['rounds']}", flush=True)
