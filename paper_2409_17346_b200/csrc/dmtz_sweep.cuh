@@ -840,6 +840,31 @@ __global__ void k_edit_rows(uint32_t* __restrict__ tbits, int64_t nwords, const 
     uint32_t word = wi < w_end ? tbits[wi] : 0u;
     if (word) tbits[wi] = 0;
     unsigned nz = __ballot_sync(0xffffffffu, word != 0);
+    if (next_frontier && nz) {
+      // the units meeting (y, z) + [-2, 1] depend on the row only: marked once per row of
+      // this pass that has a target word (its first such lane), 8 lanes per row
+      const uint32_t wr = div_wpr.div((uint32_t)wi);             // word indices < 2^32 (host check)
+      const int l0 = lane - (int)((uint32_t)wi - wr * (uint32_t)rg.wpr);   // the row's first lane
+      const unsigned below = (1u << lane) - 1u, rowlanes = l0 > 0 ? below & ~((1u << l0) - 1u) : below;
+      unsigned firsts = __ballot_sync(0xffffffffu, word != 0 && !(nz & rowlanes));
+      while (firsts) {
+        const int fl = __ffs(firsts) - 1;
+        firsts &= firsts - 1;
+        const uint32_t wrow32 = __shfl_sync(0xffffffffu, wr, fl);
+        if (lane < 8) {  // <= 4 planes x 2 row blocks
+          const uint32_t vz32 = div_ny.div(wrow32);
+          const int64_t vz = vz32, vy = (int64_t)(wrow32 - vz32 * (uint32_t)g.ny);
+          const int64_t y0 = vy >= 2 ? vy - 2 : 0, y1 = vy + 1 < g.ny ? vy + 1 : g.ny - 1;
+          const int64_t zz = (vz >= 2 ? vz - 2 : 0) + (lane >> 1), z1 = vz + 1 < g.nz ? vz + 1 : g.nz - 1;
+          const int64_t b = y0 / UY + (lane & 1);
+          if (zz <= z1 && b <= y1 / UY) {
+            const int64_t unit = zz * rg.ub + b;
+            if (use_smem) atomicOr(sfr + ((unit >> 5) - fw0), 1u << (unit & 31));
+            else atomicOr(next_frontier + (unit >> 5), 1u << (unit & 31));
+          }
+        }
+      }
+    }
     // EDIT_NW target words per pass: their loads are independent, one memory round trip
     while (nz) {
       int src[EDIT_NW];
@@ -864,16 +889,6 @@ __global__ void k_edit_rows(uint32_t* __restrict__ tbits, int64_t nwords, const 
         const uint32_t wrow32 = div_wpr.div((uint32_t)(base + sw));   // word indices < 2^32 (host check)
         const uint32_t vz32 = div_ny.div(wrow32);
         const int64_t wrow = wrow32, vz = vz32, vy = (int64_t)(wrow32 - vz32 * (uint32_t)g.ny);
-        if (next_frontier && lane < 8) {  // the units meeting (y, z) + [-2, 1]: <= 4 planes x 2 row blocks
-          const int64_t y0 = vy >= 2 ? vy - 2 : 0, y1 = vy + 1 < g.ny ? vy + 1 : g.ny - 1;
-          const int64_t zz = (vz >= 2 ? vz - 2 : 0) + (lane >> 1), z1 = vz + 1 < g.nz ? vz + 1 : g.nz - 1;
-          const int64_t b = y0 / UY + (lane & 1);
-          if (zz <= z1 && b <= y1 / UY) {
-            const int64_t unit = zz * rg.ub + b;
-            if (use_smem) atomicOr(sfr + ((unit >> 5) - fw0), 1u << (unit & 31));
-            else atomicOr(next_frontier + (unit >> 5), 1u << (unit & 31));
-          }
-        }
         if (mine[h]) {
           v[h] = ((base + sw) - wrow * rg.wpr) * 32 + lane + vy * g.sy + vz * g.sz;
           st[h] = state[v[h]];
