@@ -1342,9 +1342,10 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   extern __shared__ unsigned long long s_hash[];
   if (SH) hcap = SB_HCAP;
-  unsigned long long* queue = scratch + (int64_t)blockIdx.x * (SH ? qcap : qcap + 2 * hcap);
+  // a global slot: the queue, the keys and (FIFO only: UN needs no arbitration) the owners
+  unsigned long long* queue = scratch + (int64_t)blockIdx.x * (SH ? qcap : UN ? qcap + hcap : qcap + 2 * hcap);
   unsigned long long* keys = SH ? s_hash : queue + qcap;
-  unsigned long long* owner = SH ? nullptr : keys + hcap;
+  unsigned long long* owner = (SH || UN) ? nullptr : keys + hcap;
   uint32_t* owner_s = SH ? (uint32_t*)(s_hash + SB_HCAP) : nullptr;
   if (SH) {
     for (int i = tid; i < SB_HCAP; i += BFS_THREADS) { keys[i] = 0ull; owner_s[i] = 0u; }
@@ -1361,7 +1362,7 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
       queue[0] = key(a0, t0);
       const int64_t sl = bfs_find_or_insert(keys, hcap, key(a0, t0));
       if (SH) owner_s[sl] = ~0u;  // seen before every batch
-      else owner[sl] = ~0ull;
+      else if (!UN) owner[sl] = ~0ull;
       s_flag = 0;
     }
     __syncthreads();
@@ -1571,7 +1572,7 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
       if (sl >= 0) {
         keys[sl] = 0ull;
         if (SH) owner_s[sl] = 0u;
-        else owner[sl] = 0ull;
+        else if (!UN) owner[sl] = 0ull;
       }
     }
     __syncthreads();
@@ -1580,7 +1581,7 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
       for (int64_t i = tid; i < hcap; i += BFS_THREADS) {
         keys[i] = 0ull;
         if (SH) owner_s[i] = 0u;
-        else owner[i] = 0ull;
+        else if (!UN) owner[i] = 0ull;
       }
       if (tid == 0) atomicOr(overflow + (cb >> 5), 1u << (cb & 31));
     } else if (tid == 0) {
@@ -1865,8 +1866,9 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
         const int64_t qn = warp_level ? wq_lim : (q * grow < words / 5 ? q * grow : words / 5);
         int64_t h = 1;
         while (h < 2 * qn) h *= 2;
-        while (qn + 2 * h > words) h /= 2;
-        int64_t ns = words / (qn + 2 * h);
+        const int64_t hw = A.unordered ? 1 : 2;   // hash words per slot: keys (+ owners for FIFO)
+        while (qn + hw * h > words) h /= 2;
+        int64_t ns = words / (qn + hw * h);
         if (ns < 1) ns = 1;
         if (ns > 148 * 32) ns = 148 * 32;  // one resident 64-thread block-BFS per slot
         bool any = false, cleared = false;
