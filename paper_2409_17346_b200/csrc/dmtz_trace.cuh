@@ -1324,7 +1324,8 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
              unsigned long long* __restrict__ scratch, int64_t qcap, int64_t hcap,
              unsigned int* __restrict__ overflow, Counters* __restrict__ cnt, uint32_t* __restrict__ pool,
              int64_t pool_cap, const unsigned long long* __restrict__ bottom_top,
-             unsigned long long* __restrict__ top_used, uint64_t pool_flag) {
+             unsigned long long* __restrict__ top_used, uint64_t pool_flag,
+             unsigned long long* __restrict__ next_item) {
   // Count pass with a pool: each processed queue entry keeps its 3 facet outcomes in
   // the key's top bits (2 bits per facet: 1 reached edge, 2 new triangle), and a
   // completed BFS replays them into a wide event list taken from the top of the pool
@@ -1352,7 +1353,15 @@ k_walk_block(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restr
     __syncthreads();
   }
   auto key = [](int64_t an, int ty) { return (unsigned long long)(an * 32 + ty) + 1ull; };
-  for (int64_t li = blockIdx.x; li < nlist; li += gridDim.x) {
+  // connectors are taken dynamically (next_item, zeroed before the launch): a block that
+  // finishes a small BFS takes the next saddle at once (static strides left the level
+  // waiting for the blocks that drew several large ones)
+  __shared__ int64_t s_li;
+  for (;;) {
+    if (tid == 0) s_li = (int64_t)atomicAdd(next_item, 1ull);
+    __syncthreads();
+    const int64_t li = s_li;
+    if (li >= nlist) break;
     const int64_t cb = list[li], b = conn_base + cb;
     int64_t a0;
     int t0;
@@ -1907,6 +1916,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
           // 2: always
           const char* e_smem = getenv("DMTZ_BFS_SMEM");
           const int smem_mode = e_smem ? atoi(e_smem) : 1;
+          TCK(cudaMemsetAsync(&dc->pad[7], 0, 8, s));   // the block kernels' next-saddle counter
           if (smem_mode && qn <= SB_QMAX && (cn <= 1024 || smem_mode == 2)) {
             const int64_t ns_s = words / qn < 148 * 4 ? words / qn : 148 * 4;
             const int64_t nb_s = cn < ns_s ? cn : ns_s;
@@ -1915,13 +1925,15 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
                                        (int)SB_SMEM));
               k_walk_block<D, 256, true, true><<<(unsigned)nb_s, 256, SB_SMEM, s>>>(
                   V.eview, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write, sc, qn,
-                  SB_HCAP, (unsigned int*)ovf, dc, wpool, wpool_cap, wpool_bottom, &dc->pad[3], wpool_flag);
+                  SB_HCAP, (unsigned int*)ovf, dc, wpool, wpool_cap, wpool_bottom, &dc->pad[3], wpool_flag,
+                  &dc->pad[7]);
             } else {
               TCK(cudaFuncSetAttribute(k_walk_block<D, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)SB_SMEM));
               k_walk_block<D, 256, true><<<(unsigned)nb_s, 256, SB_SMEM, s>>>(
                   V.eview, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write, sc, qn,
-                  SB_HCAP, (unsigned int*)ovf, dc, wpool, wpool_cap, wpool_bottom, &dc->pad[3], wpool_flag);
+                  SB_HCAP, (unsigned int*)ovf, dc, wpool, wpool_cap, wpool_bottom, &dc->pad[3], wpool_flag,
+                  &dc->pad[7]);
             }
             TCK(cudaGetLastError());
             continue;
@@ -1948,11 +1960,11 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
     if (A.unordered)                                                                                        \
       k_walk_block<D, T, false, true><<<(unsigned)nblk, T, 0, s>>>(                                         \
           V.eview, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write, sc, qn, h, \
-          (unsigned int*)ovf, dc, wpool, wpool_cap, wpool_bottom, &dc->pad[3], wpool_flag);                 \
+          (unsigned int*)ovf, dc, wpool, wpool_cap, wpool_bottom, &dc->pad[3], wpool_flag, &dc->pad[7]);    \
     else                                                                                                    \
       k_walk_block<D, T><<<(unsigned)nblk, T, 0, s>>>(                                                      \
           V.eview, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write, sc, qn, h, \
-          (unsigned int*)ovf, dc, wpool, wpool_cap, wpool_bottom, &dc->pad[3], wpool_flag);                 \
+          (unsigned int*)ovf, dc, wpool, wpool_cap, wpool_bottom, &dc->pad[3], wpool_flag, &dc->pad[7]);    \
   } while (0)
           if (bfs_t == 1024) DMTZ_BFS_LAUNCH(1024);
           else if (bfs_t == 512) DMTZ_BFS_LAUNCH(512);
