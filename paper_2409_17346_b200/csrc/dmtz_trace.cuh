@@ -1096,7 +1096,7 @@ k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restri
             long long* __restrict__ off, uint64_t* __restrict__ cells, bool write,
             unsigned int* __restrict__ overflow, int wq_lim, uint64_t* __restrict__ stage,
             uint32_t* __restrict__ pool, unsigned long long* __restrict__ pool_top, int64_t pool_cap,
-            uint64_t pool_flag) {
+            uint64_t pool_flag, unsigned long long* __restrict__ next_item) {
   // count pass with a pool (stage != nullptr): the connector's events (cell ids) go to the
   // warp's staging slot (3 WQ entries) and, once complete, to an exact-size pool list
   extern __shared__ uint32_t smw[];
@@ -1127,7 +1127,11 @@ k_conn_warp(const uint32_t* __restrict__ eview, Grid g, const uint32_t* __restri
     return -1;
   };
   const int64_t sy = g.sy, sz = g.sz;
-  for (int64_t li = (int64_t)blockIdx.x * CONNW_WARPS + wid; li < nlist; li += (int64_t)gridDim.x * CONNW_WARPS) {
+  for (;;) {   // saddles taken dynamically, a warp at a time (next_item zeroed before the launch)
+    unsigned long long lv = 0;
+    if (lane == 0) lv = atomicAdd(next_item, 1ull);
+    const int64_t li = (int64_t)__shfl_sync(0xffffffffu, lv, 0);
+    if (li >= nlist) break;
     const int64_t cb = list[li], b = conn_base + cb;
     int64_t a0;
     int t0;
@@ -1903,9 +1907,10 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
             // count pass with a pool: stage the events in the (still unused) BFS scratch
             const size_t stage_bytes = (size_t)wgrid * CONNW_WARPS * 3 * WQ * 8;
             uint64_t* stage = (!write && pool && stage_bytes <= (size_t)words * 8) ? (uint64_t*)sc : nullptr;
+            TCK(cudaMemsetAsync(&dc->pad[7], 0, 8, s));
             k_conn_warp<D><<<wgrid, CONNW_WARPS * 32, CONNW_SMEM, s>>>(
                 V.eview, g, dlist, cn, conn_base, A.out_origin, A.out_terminal, off, A.out_cells, write,
-                (unsigned int*)ovf, wq_lim, stage, wpool, wpool_bottom, wpool_cap, wpool_flag);
+                (unsigned int*)ovf, wq_lim, stage, wpool, wpool_bottom, wpool_cap, wpool_flag, &dc->pad[7]);
             TCK(cudaGetLastError());
             continue;
           }
