@@ -352,9 +352,10 @@ __device__ __forceinline__ long long block_exclusive_scan(long long v, long long
 template <int D>
 __global__ void __launch_bounds__(BT_THREADS)
 k_branch_tiles(const uint32_t* __restrict__ crit, Grid g, int kind, int64_t a_lo, int64_t a_hi,
-               unsigned long long* __restrict__ bsum) {
+               unsigned long long* __restrict__ bsum, int64_t tile0) {
   int c[BT_PER];
-  const int t = tile_counts<D>(crit, g, kind, (int64_t)blockIdx.x * BT_TILE + threadIdx.x * BT_PER, a_lo, a_hi, c);
+  const int t = tile_counts<D>(crit, g, kind, (tile0 + (int64_t)blockIdx.x) * BT_TILE + threadIdx.x * BT_PER, a_lo,
+                               a_hi, c);
   long long tot;
   block_exclusive_scan(t, &tot);
   if (threadIdx.x == 0) bsum[blockIdx.x] = (unsigned long long)tot;
@@ -367,9 +368,9 @@ template <int D>
 __global__ void __launch_bounds__(BT_THREADS)
 k_branch_tiles_emit(const uint32_t* __restrict__ crit, Grid g, int kind, int64_t a_lo, int64_t a_hi,
                     const unsigned long long* __restrict__ bscan, int64_t base, uint64_t* __restrict__ origin,
-                    uint8_t* __restrict__ kout, uint64_t* __restrict__ jout) {
+                    uint8_t* __restrict__ kout, uint64_t* __restrict__ jout, int64_t tile0) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t w0 = (int64_t)blockIdx.x * BT_TILE + (int64_t)wid * 32 * BT_PER;  // the warp's first anchor
+  const int64_t w0 = (tile0 + (int64_t)blockIdx.x) * BT_TILE + (int64_t)wid * 32 * BT_PER;  // the warp's first anchor
   int c[BT_PER];
   uint32_t cm[BT_PER];
   int wtot = 0;
@@ -1713,7 +1714,11 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   const int kinds_list[3] = {1, 2, 4};
   int64_t nbk[3] = {0, 0, 0};
   // origins: per kind, block totals of BT_TILE-anchor tiles (kept, scanned) -> emission
-  const int64_t ntiles = (g.N + BT_TILE - 1) / BT_TILE;
+  // only the tiles holding origin anchors [a_lo, a_hi) (range traces: one slab of the grid)
+  const int64_t a_end = A.a_hi < g.N ? A.a_hi : g.N;
+  const int64_t tile0 = A.a_lo > 0 ? A.a_lo / BT_TILE : 0;
+  const int64_t tile1 = a_end > A.a_lo ? (a_end + BT_TILE - 1) / BT_TILE : tile0 + 1;
+  const int64_t ntiles = tile1 - tile0;
   if ((3 * ntiles + 8) * 8 > (int64_t)A.pre_bytes) return cudaErrorMemoryAllocation;
   unsigned long long* tsum[3] = {(unsigned long long*)pre, (unsigned long long*)pre + ntiles,
                                  (unsigned long long*)pre + 2 * ntiles};
@@ -1724,7 +1729,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
     for (int ki = 0; ki < 3; ki++) {
       const int kind = kinds_list[ki];
       if (!(A.kinds & (uint32_t)kind) || (kind == 4 && D != 3)) continue;
-      k_branch_tiles<D><<<(unsigned)ntiles, BT_THREADS, 0, s>>>(A.crit, g, kind, A.a_lo, A.a_hi, tsum[ki]);
+      k_branch_tiles<D><<<(unsigned)ntiles, BT_THREADS, 0, s>>>(A.crit, g, kind, A.a_lo, A.a_hi, tsum[ki], tile0);
       k_scan_top<<<1, 1024, 0, s>>>(tsum[ki], ntiles, total + ki);
       TCK(cudaGetLastError());
     }
@@ -1749,7 +1754,7 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
     const int kind = kinds_list[ki];
     if (!nbk[ki]) continue;
     k_branch_tiles_emit<D><<<(unsigned)ntiles, BT_THREADS, 0, s>>>(A.crit, g, kind, A.a_lo, A.a_hi, tsum[ki], base,
-                                                                   A.out_origin, A.out_kind, A.out_terminal);
+                                                                   A.out_origin, A.out_kind, A.out_terminal, tile0);
     TCK(cudaGetLastError());
     base += nbk[ki];
   }
