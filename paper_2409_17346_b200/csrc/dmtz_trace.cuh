@@ -521,6 +521,49 @@ __global__ void k_trace_views(const void* codes, const uint32_t* __restrict__ cr
   }
 }
 
+// The critical masks and the views in one pass: per anchor its 8 codes are read once,
+// decode_crit_dp gives the critical mask and, for every paired-down cell, the facet it
+// is paired with (tpair of the top cells)
+template <int D>
+__global__ void k_trace_views_crit(const void* codes, uint32_t* __restrict__ crit, Grid g, TraceViews V) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 2 * p < g.N; p += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t nib = 0;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int64_t u = 2 * p + h;
+      if (u >= g.N) break;
+      int64_t x, y, z;
+      coords_of(g, u, x, y, z);
+      const int ok = axes_ok(g, x, y, z);
+      uint64_t c[Tr<D>::NDELTA];
+      load_codes8<D>((const typename Tr<D>::code_t*)codes, g, u, ok, c);
+      uint64_t dp;
+      const uint32_t cm = decode_crit_dp<D>(c, ok, &dp);
+      crit[u] = cm;
+      nib |= (field_of<D>(c[0], 0) & 15u) << (4 * h);
+      const int tt0 = t_first_of_dim<D>(Tr<D>::TOP);
+      const uint32_t ex = t_exist<D>(ok);
+      uint32_t tp = 0;
+#pragma unroll
+      for (int t = tt0; t < Tr<D>::NT; t++) {
+        const uint32_t j = (((ex >> t) & 1u) && !((cm >> t) & 1u)) ? (uint32_t)(dp >> (2 * t)) & 3u : 7u;
+        tp |= j << (3 * (t - tt0));
+      }
+      V.tpair[u] = tp;
+      if (D == 3) {
+        uint32_t ev = 0;
+#pragma unroll
+        for (int e = 0; e < 7; e++) {
+          const int et = t_first_of_dim<D>(1) + e;
+          ev |= ((field_of<D>(c[0], et) & 7u) | (((cm >> et) & 1u) << 3)) << (4 * e);
+        }
+        V.eview[u] = ev;
+      }
+    }
+    V.vnib[p] = (uint8_t)nib;
+  }
+}
+
 // ----------------------------------------------------------------------------- walks
 // write == false: count cells only.  Returns the cell count or -1 on a cycle.
 template <int D>
@@ -1688,9 +1731,8 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
   } flush_{timing, tlog};
   tlog[0] = 0;
   TCK(cudaMemsetAsync(dc, 0, sizeof(Counters), s));
-  k_critmask<D><<<trace_anchor_grid(g), 128, 0, s>>>((const typename Tr<D>::code_t*)A.codes, A.crit, g);
-  TCK(cudaGetLastError());
-  // compact views at the front of the BFS scratch (the block BFS gets the rest)
+  // compact views at the front of the BFS scratch (the block BFS gets the rest), with the
+  // critical masks in the same pass
   TraceViews V;
   {
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
@@ -1704,8 +1746,8 @@ cudaError_t run_trace(TraceArgs& A, cudaStream_t s) {
     A.bfs = (unsigned long long*)(p + need);
     A.bfs_bytes -= need;
     const int64_t pairs = (g.N + 1) / 2;
-    k_trace_views<D><<<(unsigned)((pairs + 255) / 256 < 148 * 32 ? (pairs + 255) / 256 : 148 * 32), 256, 0, s>>>(
-        A.codes, A.crit, g, V);
+    k_trace_views_crit<D><<<(unsigned)((pairs + 255) / 256 < 148 * 32 ? (pairs + 255) / 256 : 148 * 32), 256, 0,
+                            s>>>(A.codes, A.crit, g, V);
     TCK(cudaGetLastError());
   }
   mark("views");
