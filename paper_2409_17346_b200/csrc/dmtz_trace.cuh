@@ -163,32 +163,7 @@ __device__ __forceinline__ int branch_count(const Grid& g, int kind, uint32_t cm
   return __popc(cm & tm);
 }
 
-// exclusive scan helpers (int64, in place); block sums -> one-block scan -> apply
-__global__ void k_scan_local(long long* __restrict__ a, int64_t n, unsigned long long* __restrict__ bsum) {
-  __shared__ long long part[1024];
-  const int64_t base = (int64_t)blockIdx.x * SCAN_CHUNK;
-  const int per = SCAN_CHUNK / 1024;
-  long long s = 0;
-  for (int k = 0; k < per; k++) {
-    const int64_t i = base + threadIdx.x * per + k;
-    if (i < n) s += a[i];
-  }
-  part[threadIdx.x] = s;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    long long v = threadIdx.x >= (unsigned)o ? part[threadIdx.x - o] : 0;
-    __syncthreads();
-    part[threadIdx.x] += v;
-    __syncthreads();
-  }
-  long long run = part[threadIdx.x] - s;  // exclusive within block
-  for (int k = 0; k < per; k++) {
-    const int64_t i = base + threadIdx.x * per + k;
-    if (i < n) { const long long v = a[i]; a[i] = run; run += v; }
-  }
-  if (threadIdx.x == 1023) bsum[blockIdx.x] = (unsigned long long)part[1023];
-}
-
+// exclusive scan helper: one-block scan of block totals (the branch-origin tiles)
 __global__ void k_scan_top(unsigned long long* __restrict__ bsum, int64_t nb, unsigned long long* __restrict__ total) {
   // exclusive scan of nb block sums by one block of 1024 threads (contiguous ranges)
   __shared__ unsigned long long part[1024];
@@ -298,11 +273,6 @@ k_scan_lb(long long* __restrict__ a, int64_t n, unsigned long long* __restrict__
     for (int k = 0; k < SCL_PER; k++)
       if (base + k < n) { a[base + k] = run; run += v[k]; }
   }
-}
-
-__global__ void k_scan_add(long long* __restrict__ a, int64_t n, const unsigned long long* __restrict__ bsum) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) a[i] += (long long)bsum[i / SCAN_CHUNK];
 }
 
 // Branch origins without an N-sized count array: a block owns BT_TILE consecutive
@@ -475,51 +445,6 @@ struct TraceViews {
   uint32_t* tpair;
   uint32_t* eview;
 };
-
-template <int D>
-__global__ void k_trace_views(const void* codes, const uint32_t* __restrict__ crit, Grid g, TraceViews V) {
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 2 * p < g.N; p += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t nib = 0;
-#pragma unroll
-    for (int h = 0; h < 2; h++) {
-      const int64_t u = 2 * p + h;
-      if (u >= g.N) break;
-      const uint64_t c = code_at<D>(codes, u);
-      nib |= (field_of<D>(c, 0) & 15u) << (4 * h);
-      int64_t x, y, z;
-      coords_of(g, u, x, y, z);
-      const int ok = axes_ok(g, x, y, z);
-      const int tt0 = t_first_of_dim<D>(Tr<D>::TOP);
-      uint32_t tp = 0;
-#pragma unroll
-      for (int t = tt0; t < Tr<D>::NT; t++) {
-        uint32_t j = 7;
-        if (((t_exist<D>(ok) >> t) & 1u) && !((crit[u] >> t) & 1u)) {
-#pragma unroll
-          for (int jj = 0; jj < 4; jj++) {
-            if (jj < t_nfacet<D>(t)) {
-              const int dm = t_facet<D>(t, jj, 0), ft = t_facet<D>(t, jj, 1), sl = t_facet<D>(t, jj, 2);
-              if (field_of<D>(code_at<D>(codes, u + mask_delta(g, dm)), ft) == (uint32_t)sl) j = (uint32_t)jj;
-            }
-          }
-        }
-        tp |= j << (3 * (t - tt0));
-      }
-      V.tpair[u] = tp;
-      if (D == 3) {
-        const uint32_t cm = crit[u];
-        uint32_t ev = 0;
-#pragma unroll
-        for (int e = 0; e < 7; e++) {
-          const int et = t_first_of_dim<D>(1) + e;
-          ev |= ((field_of<D>(c, et) & 7u) | (((cm >> et) & 1u) << 3)) << (4 * e);
-        }
-        V.eview[u] = ev;
-      }
-    }
-    V.vnib[p] = (uint8_t)nib;
-  }
-}
 
 // The critical masks and the views in one pass: per anchor its 8 codes are read once,
 // decode_crit_dp gives the critical mask and, for every paired-down cell, the facet it
