@@ -124,6 +124,7 @@ typedef struct {
   int64_t anchors_replayed;   /* sum over sweeps of anchors whose unchanged targets were replayed */
   int64_t halo_faces_sent;    /* world > 1: halo faces this rank sent over the rounds */
   int64_t halo_faces_skipped; /* world > 1: faces skipped (no edit touched their 3 planes) */
+  double edit_ms;             /* opts.profile: summed k_edit_rows time (Eq. 2 edits + frontier marks) */
 } dmtz_stats;
 
 typedef struct dmtz_ctx dmtz_ctx;

@@ -53,7 +53,8 @@ class _Stats(ctypes.Structure):
                 ("decode_ms", ctypes.c_double), ("screen_ms_full", ctypes.c_double), ("n_screen_full", ctypes.c_int64),
                 ("anchors_recomputed", ctypes.c_int64), ("anchors_decoded", ctypes.c_int64),
                 ("cells_evaluated", ctypes.c_int64), ("anchors_replayed", ctypes.c_int64),
-                ("halo_faces_sent", ctypes.c_int64), ("halo_faces_skipped", ctypes.c_int64)]
+                ("halo_faces_sent", ctypes.c_int64), ("halo_faces_skipped", ctypes.c_int64),
+                ("edit_ms", ctypes.c_double)]
 
 
 class _SStats(ctypes.Structure):
@@ -232,7 +233,7 @@ def _stats_dict(st, status):
                 screen_ms_full=st.screen_ms_full, n_screen_full=st.n_screen_full,
                 anchors_recomputed=st.anchors_recomputed, anchors_decoded=st.anchors_decoded,
                 cells_evaluated=st.cells_evaluated, anchors_replayed=st.anchors_replayed,
-                halo_faces_sent=st.halo_faces_sent, halo_faces_skipped=st.halo_faces_skipped)
+                halo_faces_sent=st.halo_faces_sent, halo_faces_skipped=st.halo_faces_skipped, edit_ms=st.edit_ms)
 
 
 class Context:

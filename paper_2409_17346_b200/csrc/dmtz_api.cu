@@ -51,7 +51,7 @@ struct dmtz_ctx {
   int device;
   int rank, world;
   Counters* host_cnt = nullptr;  // pinned
-  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};  // sweep timing (opts.profile): screen | decode
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // sweep timing (opts.profile): screen | decode | edit
   int verbose;         // DMTZ_VERBOSE=1: per-round counters on stderr (host-driven rounds)
   int no_graph;        // DMTZ_NO_GRAPH=1: host-driven rounds instead of the CUDA-graph loop
   cudaStream_t aux_stream = nullptr;   // dmtz_correct_host: f's gradient while fhat is uploaded
@@ -336,6 +336,7 @@ dmtz_status enqueue_round(dmtz_ctx* c, const float* f, const float* fhat, const 
   k_edit_rows<D><<<clamp_blocks(nwords, 256), 256, fwords_smem * 4, s>>>(
       W.tbits, nwords, fhat, W.lb, g_out, W.state, W.dc, step, o->q_cap, fbits, g, rg, fwords_smem,
       (use_skip || fbits) ? W.vchg : nullptr, W.vwords, W.ls, FastDiv((uint32_t)rg.wpr), FastDiv((uint32_t)g.ny));
+  if (profile) CK(cudaEventRecord(c->ev[3], s));
   k_loop_check<<<1, 32, 0, s>>>(W.dc, W.ls, max_rounds, h, use_cond, fbits && X.list_after ? n_units : nullptr);
   *launches += 4;
   if (fbits && X.list_after) {
@@ -468,9 +469,12 @@ dmtz_status run_cloop(dmtz_ctx* c, const float* f, const float* fhat, const dmtz
       if (status != DMTZ_OK) break;
       float ms0 = 0.f, ms1 = 0.f;
       if (o->profile) {
+        float ms2 = 0.f;
         CK(cudaEventElapsedTime(&ms0, c->ev[0], c->ev[1]));
         CK(cudaEventElapsedTime(&ms1, c->ev[1], c->ev[2]));
+        CK(cudaEventElapsedTime(&ms2, c->ev[2], c->ev[3]));
         st->sweep_ms += ms0 + ms1;
+        st->edit_ms += ms2;
         st->screen_ms += ms0;
         st->decode_ms += ms1;
         if (ms0 > 0 && (int64_t)hc->n_recomputed == g.N) { st->screen_ms_full += ms0; st->n_screen_full++; }
@@ -1262,7 +1266,7 @@ dmtz_status dmtz_ctx_create(dmtz_ctx** out, const dmtz_dims* d, int rank, int wo
     dmtz_ctx_destroy(c);
     return DMTZ_E_CUDA;
   }
-  for (int i = 0; i < 3; i++) {
+  for (int i = 0; i < 4; i++) {
     e = cudaEventCreate(&c->ev[i]);
     if (e != cudaSuccess) {
       set_err("cudaEventCreate: %s", cudaGetErrorString(e));
@@ -1305,7 +1309,7 @@ void dmtz_ctx_destroy(dmtz_ctx* c) {
     if (c->ev_aux[i]) cudaEventDestroy(c->ev_aux[i]);
   if (c->host_cnt) cudaFreeHost(c->host_cnt);
   if (c->host_ls) cudaFreeHost(c->host_ls);
-  for (int i = 0; i < 3; i++)
+  for (int i = 0; i < 4; i++)
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
   delete c;
 }
